@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""Benchmark of the streamed-weight MoE layer (BASELINE.json metric: "Mixtral-8x7B MoE-layer
+tokens/s, weights streamed from host; % of roofline").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config mixtral_8x7b] [--impl ours|reference]
+
+A step = one full MoE-layer call (router GEMM + top-k gating, permute, grouped SwiGLU expert
+GEMMs, combine) with ALL of the layer's expert weights streamed from pinned host DRAM during the
+step; consecutive steps cycle L=2 distinct layers (distinct host weight sets), and staging is two
+expert slots, so nothing is reused across steps.  The 2.8 GB of weights streamed per step are far
+larger than L2 (126 MB), which is the "inputs larger than L2" rule.
+
+Printed JSON (one line, rank 0): value = tokens/s over the timed region (device CUDA events on the
+launching stream, max over ranks), plus `roofline` (dominant kernel: the GEMM1+SwiGLU tcgen05
+kernel vs measured bf16 peak), `roofline_step` (the north-star roofline: max(expert FLOPs /
+tensor peak, streamed bytes / measured host link)), `e2e` (same metric through the host-buffer C
+ABI entry point), `cpu_baseline` (the oracle on a bounded token sample), `clocks`, `gpu_launches`.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Mixtral-8x7B MoE-layer tokens/s, weights streamed from host; % of roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="mixtral_8x7b")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--layers", type=int, default=2)
+    ap.add_argument("--packet-mb", type=float, default=0.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d.get("hbm_gbs", 6650.0), "bf16_tflops": d.get("bf16_tflops", 1590.0),
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", 1400.0),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.device}",
+                                       f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+        self.f.flush()
+        rows = [l.split(",") for l in open(self.f.name).read().strip().splitlines() if l.strip()]
+        os.unlink(self.f.name)
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                smax = max(smax, float(r[2]))
+                for n, v in zip(names, r[5:9]):
+                    if v.strip() == "Active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------------
+def cpu_baseline(inp, seconds: float) -> dict:
+    """The oracle as it stands, on a bounded token sample of the same workload (rank 0 only)."""
+    import oracle
+    cfg = inp.cfg
+    cores = oracle.num_threads()
+    n = max(8, cores)
+    done, elapsed, rounds = 0, 0.0, 0
+    while elapsed < seconds and done < cfg.tokens:
+        lo = done % inp.x.shape[0]
+        xs = inp.x[lo:lo + n]
+        t0 = time.perf_counter()
+        oracle.forward(xs, inp.router, inp.w1, inp.w3, inp.w2, cfg.top_k, cfg.num_shared)
+        elapsed += time.perf_counter() - t0
+        done += xs.shape[0]
+        rounds += 1
+        if elapsed < seconds / 8:
+            n *= 2
+    return {"value": done / elapsed, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "sample": f"{done} of {cfg.tokens} tokens of the {cfg.name} layer ({rounds} calls, "
+                      f"{elapsed:.1f} s, fp64 router + fp32 experts, OpenMP)"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle timed on the host cores (rank 0 only)."""
+    import oracle
+    import synth
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = synth.CONFIGS[args.config]
+    oracle.build()
+    inp = synth.gen_inputs(cfg)
+    cores = oracle.num_threads()
+    n = max(8, cores)
+    for i in range(args.warmup):
+        oracle.forward(inp.x[:n], inp.router, inp.w1, inp.w3, inp.w2, cfg.top_k, cfg.num_shared)
+    times = []
+    for i in range(args.steps):
+        lo = (i * n) % (cfg.tokens - n + 1)
+        t0 = time.perf_counter()
+        oracle.forward(inp.x[lo:lo + n], inp.router, inp.w1, inp.w3, inp.w2, cfg.top_k,
+                       cfg.num_shared)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = n * args.steps / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg.name, "tokens": cfg.tokens, "hidden": cfg.hidden,
+                       "ffn": cfg.ffn, "experts": cfg.num_experts, "top_k": cfg.top_k,
+                       "tokens_per_step": n},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{n} tokens per step of the {cfg.name} layer"},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------------
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    import paper_2504_09345_b200 as moe
+    from paper_2504_09345_b200 import build as moe_build
+    from paper_2504_09345_b200 import ledger
+
+    rank, world, local = dist_env()
+    if world > 1:
+        raise SystemExit("expert-parallel multi-GPU bench is not built yet (single GPU only)")
+    torch.cuda.set_device(local)
+    moe_build.build()
+    peaks = load_peaks()
+    cfg = synth.CONFIGS[args.config]
+    T = cfg.tokens
+
+    # ---- inputs: L layers of host weights (pinned, packed), device x / router per layer
+    layers = [synth.gen_inputs(cfg, layer=l) for l in range(args.layers)]
+    experts = [moe.HostExperts(cfg.hidden, cfg.ffn, l.w1, l.w3, l.w2) for l in layers]
+    xs = [torch.from_numpy(l.x.view(np.int16)).view(torch.bfloat16).cuda() for l in layers]
+    routers = [torch.from_numpy(l.router.view(np.int16)).view(torch.bfloat16).cuda() for l in layers]
+    outs = [torch.empty_like(x) for x in xs]
+    idxs = [torch.empty((T, cfg.top_k), dtype=torch.int32, device="cuda") for _ in layers]
+    gws = [torch.empty((T, cfg.top_k), dtype=torch.float32, device="cuda") for _ in layers]
+
+    probe_gbs = moe.moe_probe_h2d(local, 1 << 30, 5)   # paper's method: 1 GB pinned H2D copies
+
+    layer = moe.MoELayer(cfg.hidden, cfg.ffn, cfg.num_experts, cfg.top_k, T,
+                         num_shared=cfg.num_shared, device=local, profile=True,
+                         packet_bytes=int(args.packet_mb * 2 ** 20))
+    stream = torch.cuda.Stream()
+    sh = stream.cuda_stream
+
+    def step(i):
+        l = i % args.layers
+        layer.forward(xs[l], routers[l], experts[l], outs[l], idxs[l], gws[l], stream=sh)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    layer.reset_stats()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for i in range(args.steps):
+        step(args.warmup + i)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms_total = ev0.elapsed_time(ev1)
+    st = layer.stats()
+    ms = ms_total / args.steps
+    value = T * world / (ms / 1e3)
+
+    # ---- work ledger (experts hit: from the routing of the timed layers)
+    hit = [int((np.bincount(idxs[l].cpu().numpy().ravel(), minlength=cfg.num_experts) > 0).sum())
+           for l in range(args.layers)]
+    work = ledger.layer_work(T, cfg.hidden, cfg.ffn, cfg.num_experts, cfg.top_k, cfg.num_shared,
+                             experts_hit=min(hit))
+    rl = ledger.roofline_time_s(work, peaks["bf16_tflops_sustained"], probe_gbs)
+    g1_launch_ms = st["gemm1_ms"] / max(1, st["gemm1_launches"])
+    g1_flops_launch = work.gemm1_flops / (cfg.num_experts + cfg.num_shared)
+    achieved_tf = g1_flops_launch / (g1_launch_ms * 1e-3) / 1e12 if g1_launch_ms > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(cfg.name, {}).get("gemm1_dram_bytes_per_launch")
+    roofline = {"kernel": "expert_gemm_kernel<256,SwiGLU> (a5, tcgen05)", "bound": "tensor",
+                "achieved": achieved_tf, "peak": peaks["bf16_tflops_sustained"],
+                "unit": "TFLOP/s", "frac": achieved_tf / peaks["bf16_tflops_sustained"],
+                "traffic": traffic, "peak_source": peaks["source"] + " bf16_tflops_sustained",
+                "flops_per_launch": g1_flops_launch, "avg_launch_ms": g1_launch_ms}
+    h2d_gbs = st["h2d_weight_bytes"] / (st["h2d_ms"] * 1e-3) / 1e9 if st["h2d_ms"] > 0 else 0.0
+    roofline_step = {"bound": rl["bound"], "t_roofline_ms": rl["t_roofline_s"] * 1e3,
+                     "t_host_link_ms": rl["t_host_link_s"] * 1e3,
+                     "t_tensor_ms": rl["t_tensor_s"] * 1e3, "ms_per_step": ms,
+                     "frac": rl["t_roofline_s"] * 1e3 / ms,
+                     "roofline_tokens_per_s": T / rl["t_roofline_s"],
+                     "host_link_probe_gbs": probe_gbs, "h2d_achieved_gbs_in_copies": h2d_gbs,
+                     "h2d_effective_gbs_over_step": work.weight_bytes / (ms * 1e-3) / 1e9,
+                     "weight_bytes_per_step": work.weight_bytes, "expert_flops_per_step": work.expert_flops,
+                     "tensor_peak_tflops": peaks["bf16_tflops_sustained"]}
+    per_kernel_ms = {k: st[k] / args.steps for k in
+                     ("h2d_ms", "route_ms", "permute_ms", "gemm1_ms", "gemm2_ms", "combine_ms")}
+
+    # ---- e2e: host token buffers through moe_layer_forward_host (H2D tokens + D2H output)
+    e2e = None
+    if not args.no_e2e:
+        xh = [torch.from_numpy(l.x.view(np.int16)).view(torch.bfloat16).pin_memory() for l in layers]
+        oh = [torch.empty_like(x).pin_memory() for x in xh]
+
+        def step_h(i):
+            l = i % args.layers
+            layer.forward_host(xh[l], routers[l], experts[l], oh[l], stream=sh)
+
+        for i in range(args.warmup):
+            step_h(i)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(args.steps):
+            step_h(args.warmup + i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / args.steps
+        tok_bytes = T * cfg.hidden * 2
+        e2e = {"value": T * world / (ems / 1e3), "unit": "tokens/s", "ms_per_step": ems,
+               "h2d_bytes_per_step": tok_bytes + work.weight_bytes,
+               "h2d_token_bytes_per_step": tok_bytes, "h2d_weight_bytes_per_step": work.weight_bytes,
+               "d2h_bytes_per_step": tok_bytes,
+               "api": "moe_layer_forward_host (pinned host hidden/out)"}
+        # parity spot check of the e2e output against the device-path output
+        e2e["matches_device_path"] = bool(torch.equal(oh[(args.warmup + args.steps - 1) % args.layers].cuda(),
+                                                      outs[(args.warmup + args.steps - 1) % args.layers]))
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_baseline(layers[0], args.cpu_seconds)
+
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded random bf16 weights/tokens shaped like the model)",
+            "config": {"workload": cfg.name, "tokens": T, "hidden": cfg.hidden, "ffn": cfg.ffn,
+                       "experts": cfg.num_experts, "top_k": cfg.top_k,
+                       "num_shared": cfg.num_shared, "layers_cycled": args.layers,
+                       "staging_slots": 2, "packet_mb": args.packet_mb,
+                       "l2": "inputs larger than L2: all expert weights re-streamed from host each step",
+                       "parallelism": f"ep{world}"},
+            "roofline": roofline, "roofline_step": roofline_step, "per_kernel_ms_per_step": per_kernel_ms,
+            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
+            "gpu_launches": st["kernel_launches"],
+            "gpu_launches_per_step": st["kernel_launches"] / args.steps}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    layer.close()
+    for e in experts:
+        e.close()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,174 @@
+/*
+ * moe.h -- C ABI of the B200-native streamed-weight MoE layer (arXiv 2504.09345, "MoE-Lens").
+ *
+ * The operation ("GPU Task B (GB), which includes the O projection and MoE layer,
+ * is applied to all tokens"; reading R1-R10 in DESIGN.md fix the layer's math, which the paper
+ * defers to prior work):
+ *
+ *   logits[t,e] = sum_c x[t,c] * Wr[e,c]                  (router GEMM, fp64 accumulation)
+ *   S_t         = top-k experts by (logit desc, index asc) (softmax top-k gating)
+ *   g[t,j]      = softmax over the k selected logits       (renormalised; cfg.renormalize)
+ *   y[t]        = sum_j g[t,j] * W2_e (silu(W1_e x_t) * W3_e x_t)  + shared experts (weight 1)
+ *
+ * Expert weights live in pinned host memory ("All weights are stored in pinned CPU memory",
+ * PAPER.md:823) and are streamed into a bounded GPU buffer ("two times the model weight size
+ * divided by the number of layers", PAPER.md:824-825 -- here two expert-sized slots) on every
+ * call, prefetched one step ahead by an asynchronous copy stream.
+ *
+ * Conventions (all entry points):
+ *   - No C++ types or exceptions cross this boundary.  Every entry point returns a moe_status.
+ *   - Validation is synchronous and happens before anything is enqueued; on MOE_E_INVAL nothing
+ *     is written.  Asynchronous CUDA errors surface at the next call or at moe_sync().
+ *   - Ownership: the caller owns every pointer it passes (hidden, router_w, out, topk_*, host
+ *     expert blobs).  The library owns its workspace, the staging slots, its internal streams,
+ *     events and (world_size > 1) its NCCL communicator.
+ *   - Lifetime: calls are asynchronous w.r.t. the host.  Host expert blobs and every argument
+ *     buffer must stay valid and unmodified until `stream` has passed the call (or moe_sync()).
+ *   - A context is bound to one device and is not thread-safe.
+ *   - Determinism: for fixed inputs and world_size the outputs are bitwise reproducible.
+ */
+#ifndef MOE_B200_H_
+#define MOE_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct moe_ctx_s* moe_ctx;
+
+typedef enum {
+    MOE_OK = 0,
+    MOE_E_INVAL = 1,        /* bad argument: shape, top_k, num_tokens > max_tokens, aliasing    */
+    MOE_E_CUDA = 2,         /* CUDA runtime/driver error (detail in moe_last_error)              */
+    MOE_E_NCCL = 3,         /* NCCL error (world_size > 1)                                       */
+    MOE_E_NOMEM = 4,        /* device or pinned-host allocation failed                           */
+    MOE_E_NOT_PINNED = 5,   /* an expert blob is pageable host memory                            */
+    MOE_E_UNSUPPORTED = 6,  /* shape outside the kernels' envelope (see moe_config)              */
+    MOE_E_STATE = 7         /* call on a context in an error state / wrong order                 */
+} moe_status;
+
+/* Flags for moe_config.flags */
+#define MOE_FLAG_PROFILE 1u /* record CUDA events around every kernel and copy (moe_get_stats) */
+
+/*
+ * Layer configuration.  Envelope of the sm_100a kernels (MOE_E_UNSUPPORTED otherwise):
+ *   hidden % 128 == 0, ffn % 128 == 0, 1 <= num_experts <= 128, 1 <= top_k <= min(num_experts, 8),
+ *   0 <= num_shared <= 8, max_tokens >= 1.
+ * Multi-GPU expert parallelism (world_size > 1): num_experts % world_size == 0; rank r owns the
+ * routed experts [r*N_e/W, (r+1)*N_e/W); shared experts are replicated on every rank.
+ */
+typedef struct {
+    int32_t hidden;           /* h                                          */
+    int32_t ffn;              /* h_i  (expert intermediate dimension)                          */
+    int32_t num_experts;      /* N_e  routed experts                                           */
+    int32_t top_k;            /* N_k  experts per token                                        */
+    int32_t num_shared;       /* always-on experts with weight 1 (DeepSeek-style; 0 = none)    */
+    int32_t max_tokens;       /* per-rank token capacity used to size the workspace            */
+    int32_t renormalize;      /* 1: gates = softmax over the top-k (sum to 1); 0: full softmax */
+    int32_t device;           /* CUDA device ordinal                                           */
+    int32_t world_size;       /* expert-parallel group size; 1 = single GPU                    */
+    int32_t rank;             /* this process's rank in the group                              */
+    const void* nccl_unique_id; /* 128-byte ncclUniqueId (world_size > 1), else NULL           */
+    int64_t packet_bytes;     /* 0 = one copy per weight matrix; else H2D packets of this size */
+    uint32_t flags;           /* MOE_FLAG_*                                                    */
+} moe_config;
+
+/* Packed host blob of one expert (produced by moe_pack_expert, consumed by the copy engine):
+ *   [ W13 : 2*h_i rows x h bf16, gate/up rows interleaved in blocks of 128 rows ]
+ *   [ W2  : h rows x h_i bf16 (canonical nn.Linear orientation) ]
+ * Size in bytes = 6 * h * h_i  (Eq. 1 denominator per expert). */
+int64_t moe_packed_expert_bytes(int32_t hidden, int32_t ffn);
+
+/* Host-side, synchronous.  Canonical bf16 (uint16 bit patterns) W1,W3: [h_i, h] row-major,
+ * W2: [h, h_i] row-major  ->  dst (moe_packed_expert_bytes bytes, any host memory).
+ * MOE_E_INVAL on NULL pointers or non-positive / unsupported shapes. */
+moe_status moe_pack_expert(int32_t hidden, int32_t ffn, const void* w1, const void* w3,
+                           const void* w2, void* dst);
+
+/* Pinned host allocation helpers (cudaHostAlloc, portable).  The blobs passed to
+ * moe_layer_forward must be page-locked; these are one way to get such memory. */
+moe_status moe_host_alloc(size_t bytes, void** ptr);
+moe_status moe_host_free(void* ptr);
+
+/* Create a context on cfg->device: validates cfg, allocates the workspace for max_tokens
+ * tokens, two staging slots of moe_packed_expert_bytes each, the copy stream and events, and
+ * (world_size > 1) the NCCL communicator.  *out is NULL on failure. */
+moe_status moe_init(const moe_config* cfg, moe_ctx* out);
+
+/*
+ * One MoE layer over this rank's tokens, enqueued on `stream` (a cudaStream_t; NULL = legacy
+ * default stream).  Returns after enqueueing (asynchronous).
+ *   hidden      device bf16 [num_tokens, h] row-major (local tokens); must not alias `out`.
+ *   num_tokens  0 <= T <= max_tokens (0 = no-op).
+ *   router_w    device bf16 [N_e, h] row-major (all routed experts, on every rank).
+ *   experts     host array of (N_e/W + num_shared) pointers to PINNED packed blobs: this rank's
+ *               routed experts in increasing expert id, then the shared experts.
+ *   top_k       must equal cfg->top_k.
+ *   out         device bf16 [num_tokens, h].
+ *   topk_idx    optional device int32 [num_tokens, top_k] (NULL = not returned): the selected
+ *               experts of each token in rank order (logit desc, index asc).
+ *   topk_w      optional device fp32 [num_tokens, top_k]: the gates, same order.
+ * Errors: MOE_E_INVAL (shapes/aliasing/NULL), MOE_E_NOT_PINNED, MOE_E_CUDA, MOE_E_NCCL.
+ */
+moe_status moe_layer_forward(moe_ctx ctx, const void* hidden, int32_t num_tokens,
+                             const void* router_w, const void* const* experts, int32_t top_k,
+                             void* out, int32_t* topk_idx, float* topk_w, void* stream);
+
+/*
+ * Same as moe_layer_forward with HOST token buffers: hidden_host (pinned bf16 [T,h]) is copied
+ * to the device on the copy stream ahead of the call's expert weights, and the result is copied
+ * back into out_host (pinned bf16 [T,h]); both copies are ordered on `stream`.  topk_* are
+ * optional DEVICE buffers as above.  End-to-end entry point (bench "e2e").
+ */
+moe_status moe_layer_forward_host(moe_ctx ctx, const void* hidden_host, int32_t num_tokens,
+                                  const void* router_w, const void* const* experts, int32_t top_k,
+                                  void* out_host, int32_t* topk_idx, float* topk_w, void* stream);
+
+/* Block until all work of the context is done; returns the first pending async error. */
+moe_status moe_sync(moe_ctx ctx);
+
+/* Per-context counters.  Times are sums of CUDA-event durations (MOE_FLAG_PROFILE only; 0
+ * otherwise), measured on the stream each kernel / copy was launched on. */
+typedef struct {
+    int64_t calls;
+    int64_t h2d_weight_bytes;     /* expert bytes copied host -> device                       */
+    int64_t h2d_token_bytes;      /* hidden bytes copied (moe_layer_forward_host)             */
+    int64_t d2h_token_bytes;      /* output bytes copied back (moe_layer_forward_host)        */
+    int64_t kernel_launches;      /* launches of this library's kernels                       */
+    int64_t gemm1_launches, gemm2_launches;
+    double h2d_ms;                /* sum of weight-copy durations (copy stream)               */
+    double route_ms, permute_ms, gemm1_ms, gemm2_ms, combine_ms, comm_ms;
+} moe_stats;
+
+moe_status moe_get_stats(moe_ctx ctx, moe_stats* out);   /* synchronises the context */
+moe_status moe_reset_stats(moe_ctx ctx);
+
+/* Device pointers into the workspace of the last call (debugging / white-box tests). */
+typedef struct {
+    const int32_t* counts;      /* [N_e_local + num_shared] rows per expert of the last call  */
+    const int32_t* offsets;     /* [N_e + 1] exclusive scan of routed counts (local view)     */
+    const int32_t* pos;         /* [T, top_k] row of (t, j) in the permuted layout            */
+    const void* x_perm;         /* bf16 [rows, h]  permuted tokens                            */
+    const void* h_act;          /* bf16 [rows, h_i] silu(W1 x) * W3 x                         */
+    const void* y_perm;         /* bf16 [rows, h]  gate-scaled expert outputs                 */
+    int64_t rows;               /* rows used by the last call                                 */
+} moe_debug_view;
+moe_status moe_debug_buffers(moe_ctx ctx, moe_debug_view* out);
+
+/* Release everything owned by the context (synchronises first).  NULL is a no-op. */
+moe_status moe_destroy(moe_ctx ctx);
+
+const char* moe_status_string(moe_status s);
+const char* moe_last_error(moe_ctx ctx);   /* detail of the last failure ("" if none) */
+
+/* Host-link probe, the paper's method ("B_IO ... based on 1GB tensor transfers"):
+ * `iters` pinned host->device copies of `bytes` on `device`; returns the best GB/s (1e9 B/s). */
+moe_status moe_probe_h2d(int32_t device, size_t bytes, int32_t iters, double* gbps);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOE_B200_H_ */

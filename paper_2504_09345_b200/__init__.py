@@ -1,0 +1,283 @@
+"""paper_2504_09345_b200 -- B200-native streamed-weight MoE layer (MoE-Lens, arXiv 2504.09345).
+
+Thin ctypes binding over ``libmoe_b200.so`` (C ABI in ``include/moe.h``): argument marshalling
+only -- every step of the layer (routing, permute, expert GEMMs, combine, weight streaming) runs
+in the library's sm_100a kernels and copy engine.  There is no CPU or PyTorch fallback: if the
+library is missing or the device is not sm_100, the calls fail loudly.
+
+PyTorch is used by callers only for device memory, streams and process groups.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libmoe_b200.so")
+
+MOE_OK = 0
+MOE_E_INVAL = 1
+MOE_E_CUDA = 2
+MOE_E_NCCL = 3
+MOE_E_NOMEM = 4
+MOE_E_NOT_PINNED = 5
+MOE_E_UNSUPPORTED = 6
+MOE_E_STATE = 7
+MOE_FLAG_PROFILE = 1
+
+EXPORTED = ["moe_packed_expert_bytes", "moe_pack_expert", "moe_host_alloc", "moe_host_free",
+            "moe_init", "moe_layer_forward", "moe_layer_forward_host", "moe_sync", "moe_get_stats",
+            "moe_reset_stats", "moe_debug_buffers", "moe_destroy", "moe_status_string",
+            "moe_last_error", "moe_probe_h2d"]
+
+
+class moe_config(ctypes.Structure):
+    _fields_ = [("hidden", ctypes.c_int32), ("ffn", ctypes.c_int32),
+                ("num_experts", ctypes.c_int32), ("top_k", ctypes.c_int32),
+                ("num_shared", ctypes.c_int32), ("max_tokens", ctypes.c_int32),
+                ("renormalize", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("world_size", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("nccl_unique_id", ctypes.c_void_p), ("packet_bytes", ctypes.c_int64),
+                ("flags", ctypes.c_uint32)]
+
+
+class moe_stats(ctypes.Structure):
+    _fields_ = [("calls", ctypes.c_int64), ("h2d_weight_bytes", ctypes.c_int64),
+                ("h2d_token_bytes", ctypes.c_int64), ("d2h_token_bytes", ctypes.c_int64),
+                ("kernel_launches", ctypes.c_int64), ("gemm1_launches", ctypes.c_int64),
+                ("gemm2_launches", ctypes.c_int64), ("h2d_ms", ctypes.c_double),
+                ("route_ms", ctypes.c_double), ("permute_ms", ctypes.c_double),
+                ("gemm1_ms", ctypes.c_double), ("gemm2_ms", ctypes.c_double),
+                ("combine_ms", ctypes.c_double), ("comm_ms", ctypes.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class moe_debug_view(ctypes.Structure):
+    _fields_ = [("counts", ctypes.c_void_p), ("offsets", ctypes.c_void_p),
+                ("pos", ctypes.c_void_p), ("x_perm", ctypes.c_void_p),
+                ("h_act", ctypes.c_void_p), ("y_perm", ctypes.c_void_p),
+                ("rows", ctypes.c_int64)]
+
+
+class MoEError(RuntimeError):
+    def __init__(self, status: int, detail: str = ""):
+        self.status = status
+        super().__init__(f"{status_string(status)}{': ' + detail if detail else ''}")
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libmoe_b200.so (raises if it has not been built -- no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: run `python -m paper_2504_09345_b200.build` "
+                          "(the CUDA path has no fallback)")
+    lib = ctypes.CDLL(path)
+    P, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    lib.moe_packed_expert_bytes.argtypes = [i32, i32]
+    lib.moe_packed_expert_bytes.restype = i64
+    lib.moe_pack_expert.argtypes = [i32, i32, P, P, P, P]
+    lib.moe_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]
+    lib.moe_host_free.argtypes = [P]
+    lib.moe_init.argtypes = [ctypes.POINTER(moe_config), ctypes.POINTER(ctypes.c_void_p)]
+    lib.moe_layer_forward.argtypes = [P, P, i32, P, P, i32, P, P, P, P]
+    lib.moe_layer_forward_host.argtypes = [P, P, i32, P, P, i32, P, P, P, P]
+    lib.moe_sync.argtypes = [P]
+    lib.moe_get_stats.argtypes = [P, ctypes.POINTER(moe_stats)]
+    lib.moe_reset_stats.argtypes = [P]
+    lib.moe_debug_buffers.argtypes = [P, ctypes.POINTER(moe_debug_view)]
+    lib.moe_destroy.argtypes = [P]
+    lib.moe_status_string.argtypes = [ctypes.c_int]
+    lib.moe_status_string.restype = ctypes.c_char_p
+    lib.moe_last_error.argtypes = [P]
+    lib.moe_last_error.restype = ctypes.c_char_p
+    lib.moe_probe_h2d.argtypes = [i32, ctypes.c_size_t, i32, ctypes.POINTER(ctypes.c_double)]
+    for name in EXPORTED:
+        if name not in ("moe_packed_expert_bytes", "moe_status_string", "moe_last_error"):
+            getattr(lib, name).restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def status_string(s: int) -> str:
+    return load().moe_status_string(int(s)).decode()
+
+
+def _check(rc: int, ctx=None):
+    if rc != MOE_OK:
+        detail = load().moe_last_error(ctx).decode() if ctx else ""
+        raise MoEError(rc, detail)
+
+
+# ----------------------------------------------------------------------------- C ABI, 1:1
+def moe_packed_expert_bytes(hidden: int, ffn: int) -> int:
+    return int(load().moe_packed_expert_bytes(hidden, ffn))
+
+
+def moe_pack_expert(hidden: int, ffn: int, w1: np.ndarray, w3: np.ndarray, w2: np.ndarray,
+                    dst: int) -> None:
+    for a in (w1, w3, w2):
+        assert a.dtype == np.uint16 and a.flags.c_contiguous
+    _check(load().moe_pack_expert(hidden, ffn, w1.ctypes.data, w3.ctypes.data, w2.ctypes.data, dst))
+
+
+def moe_host_alloc(nbytes: int) -> int:
+    p = ctypes.c_void_p()
+    _check(load().moe_host_alloc(nbytes, ctypes.byref(p)))
+    return p.value
+
+
+def moe_host_free(ptr: int) -> None:
+    _check(load().moe_host_free(ptr))
+
+
+def moe_init(cfg: moe_config) -> int:
+    ctx = ctypes.c_void_p()
+    _check(load().moe_init(ctypes.byref(cfg), ctypes.byref(ctx)))
+    return ctx.value
+
+
+def moe_layer_forward(ctx: int, hidden: int, num_tokens: int, router_w: int, experts, top_k: int,
+                      out: int, topk_idx: int = 0, topk_w: int = 0, stream: int = 0) -> None:
+    _check(load().moe_layer_forward(ctx, hidden, num_tokens, router_w, experts, top_k, out,
+                                    topk_idx or None, topk_w or None, stream or None), ctx)
+
+
+def moe_layer_forward_host(ctx: int, hidden_host: int, num_tokens: int, router_w: int, experts,
+                           top_k: int, out_host: int, topk_idx: int = 0, topk_w: int = 0,
+                           stream: int = 0) -> None:
+    _check(load().moe_layer_forward_host(ctx, hidden_host, num_tokens, router_w, experts, top_k,
+                                         out_host, topk_idx or None, topk_w or None,
+                                         stream or None), ctx)
+
+
+def moe_sync(ctx: int) -> None:
+    _check(load().moe_sync(ctx), ctx)
+
+
+def moe_get_stats(ctx: int) -> dict:
+    s = moe_stats()
+    _check(load().moe_get_stats(ctx, ctypes.byref(s)), ctx)
+    return s.as_dict()
+
+
+def moe_reset_stats(ctx: int) -> None:
+    _check(load().moe_reset_stats(ctx), ctx)
+
+
+def moe_debug_buffers(ctx: int) -> moe_debug_view:
+    v = moe_debug_view()
+    _check(load().moe_debug_buffers(ctx, ctypes.byref(v)), ctx)
+    return v
+
+
+def moe_destroy(ctx: int) -> None:
+    _check(load().moe_destroy(ctx))
+
+
+def moe_probe_h2d(device: int = 0, nbytes: int = 1 << 30, iters: int = 5) -> float:
+    g = ctypes.c_double()
+    _check(load().moe_probe_h2d(device, nbytes, iters, ctypes.byref(g)))
+    return g.value
+
+
+# ----------------------------------------------------------------------------- convenience
+class HostExperts:
+    """Pinned, packed expert blobs of one layer (this rank's routed experts, then shared)."""
+
+    def __init__(self, hidden: int, ffn: int, w1: Sequence[np.ndarray], w3: Sequence[np.ndarray],
+                 w2: Sequence[np.ndarray]):
+        self.hidden, self.ffn = hidden, ffn
+        self.blob_bytes = moe_packed_expert_bytes(hidden, ffn)
+        self.ptrs: List[int] = []
+        try:
+            for a, b, c in zip(w1, w3, w2):
+                p = moe_host_alloc(self.blob_bytes)
+                self.ptrs.append(p)
+                moe_pack_expert(hidden, ffn, np.ascontiguousarray(a), np.ascontiguousarray(b),
+                                np.ascontiguousarray(c), p)
+        except Exception:
+            self.close()
+            raise
+        self.array = (ctypes.c_void_p * len(self.ptrs))(*self.ptrs)
+
+    @property
+    def nbytes(self) -> int:
+        return self.blob_bytes * len(self.ptrs)
+
+    def close(self):
+        for p in self.ptrs:
+            moe_host_free(p)
+        self.ptrs = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class MoELayer:
+    """A context for one MoE layer shape on one device (see include/moe.h)."""
+
+    def __init__(self, hidden: int, ffn: int, num_experts: int, top_k: int, max_tokens: int,
+                 num_shared: int = 0, renormalize: bool = True, device: int = 0,
+                 world_size: int = 1, rank: int = 0, packet_bytes: int = 0,
+                 profile: bool = False, nccl_unique_id: Optional[bytes] = None):
+        self.cfg = moe_config(hidden, ffn, num_experts, top_k, num_shared, max_tokens,
+                              int(renormalize), device, world_size, rank, None, packet_bytes,
+                              MOE_FLAG_PROFILE if profile else 0)
+        self._uid = None
+        if nccl_unique_id is not None:
+            self._uid = ctypes.create_string_buffer(bytes(nccl_unique_id), len(nccl_unique_id))
+            self.cfg.nccl_unique_id = ctypes.cast(self._uid, ctypes.c_void_p)
+        self.ctx = moe_init(self.cfg)
+        self.top_k = top_k
+
+    def forward(self, hidden, router_w, experts: HostExperts, out, topk_idx=None, topk_w=None,
+                stream: int = 0):
+        """Device tensors (torch) in, device tensors out; enqueued on `stream` (raw handle)."""
+        moe_layer_forward(self.ctx, hidden.data_ptr(), hidden.shape[0], router_w.data_ptr(),
+                          experts.array, self.top_k, out.data_ptr(),
+                          topk_idx.data_ptr() if topk_idx is not None else 0,
+                          topk_w.data_ptr() if topk_w is not None else 0, stream)
+
+    def forward_host(self, hidden_host, router_w, experts: HostExperts, out_host, topk_idx=None,
+                     topk_w=None, stream: int = 0):
+        moe_layer_forward_host(self.ctx, hidden_host.data_ptr(), hidden_host.shape[0],
+                               router_w.data_ptr(), experts.array, self.top_k,
+                               out_host.data_ptr(),
+                               topk_idx.data_ptr() if topk_idx is not None else 0,
+                               topk_w.data_ptr() if topk_w is not None else 0, stream)
+
+    def sync(self):
+        moe_sync(self.ctx)
+
+    def stats(self) -> dict:
+        return moe_get_stats(self.ctx)
+
+    def reset_stats(self):
+        moe_reset_stats(self.ctx)
+
+    def debug(self) -> moe_debug_view:
+        return moe_debug_buffers(self.ctx)
+
+    def close(self):
+        if self.ctx:
+            moe_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

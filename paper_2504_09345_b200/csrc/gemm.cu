@@ -1,0 +1,253 @@
+// gemm.cu -- grouped bf16 expert GEMM on 5th-gen tensor cores (tcgen05 + TMEM), fed by TMA.
+//
+// One launch computes one expert group (steps a5 / a6 of the MoE layer; Eq. 1's "6 N_k h h_i"
+// FLOPs):
+//   a5 (kGemmSwiGLU): H[r, f] = silu(A W1^T)[r,f] * (A W3^T)[r,f]   with B = packed W13 whose
+//                     256-row N tiles hold 128 gate rows then the 128 matching up rows, so the
+//                     SwiGLU is applied in the epilogue straight out of TMEM;
+//   a6 (kGemmPlain):  Y[r, :] = A W2^T.
+// A rows of the group are [a_begin, a_end) (read from device memory: the routing kernels
+// produce them, so no host sync is needed); rows past a_end in the last M tile are computed
+// but never stored.
+//
+// Structure (persistent, one CTA per SM, 256 threads):
+//   warp 0     TMA producer: A tile 128x64 and B tile BNx64 per stage, 128B swizzle
+//   warp 1     MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M=128, N=BN, K=16 per instr
+//   warp 2     TMEM allocator (2 x BN fp32 columns: double-buffered accumulator)
+//   warps 4-7  epilogue: tcgen05.ld 32x32b -> fp32 math -> bf16 -> global
+// Pipelines: smem full/empty mbarriers (TMA <-> MMA), TMEM full/empty (MMA <-> epilogue).
+#include "moe_internal.h"
+#include "ptx.cuh"
+
+namespace moe {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // one 128-byte swizzle atom of bf16
+constexpr int kThreads = 256;
+
+template <int BN>
+struct GemmCfg {
+    static constexpr int kStages = (BN == 256) ? 4 : 6;
+    static constexpr uint32_t kABytes = BM * BK * 2;
+    static constexpr uint32_t kBBytes = BN * BK * 2;
+    static constexpr uint32_t kTmemCols = 2 * BN;
+    static constexpr size_t kSmem = 1024 /*align slack*/ + kStages * (kABytes + kBBytes) + 256;
+};
+
+__device__ __forceinline__ float silu_mul(float g, float u) {
+    return g / (1.0f + __expf(-g)) * u;
+}
+
+template <int BN, int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+expert_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const GemmGroup* __restrict__ group, int N, int K,
+                   __nv_bfloat16* __restrict__ out, int ldo) {
+    using C = GemmCfg<BN>;
+    constexpr int S = C::kStages;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + S * C::kABytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * C::kBBytes);
+    uint64_t* empty = full + S;
+    uint64_t* tfull = empty + S;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const GemmGroup g = *group;
+    const int rows = g.a_end - g.a_begin;
+    if (rows <= 0) return;
+    const int m_tiles = (rows + BM - 1) / BM;
+    const int n_tiles = N / BN;
+    const int total = m_tiles * n_tiles;
+    if ((int)blockIdx.x >= total) return;
+    const int num_kb = K / BK;
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+        for (int s = 0; s < S; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], 4);
+        }
+        ptx::fence_barrier_init();
+        ptx::fence_proxy_async();
+    }
+    if (warp == 2) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ------------------------------------------------------------ TMA producer
+            const uint64_t pol_a = ptx::policy_evict_last();   // A tile re-read by every N tile
+            const uint64_t pol_b = ptx::policy_evict_first();  // weights: read by m_tiles CTAs
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+                const int m = tile % m_tiles, n = tile / m_tiles;
+                const int arow = g.a_begin + m * BM, brow = n * BN;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1u);
+                    ptx::mbar_arrive_expect_tx(&full[stage], C::kABytes + C::kBBytes);
+                    ptx::tma_load_2d_hint(sA + stage * C::kABytes, &tmA, &full[stage], kb * BK,
+                                          arow, pol_a);
+                    ptx::tma_load_2d_hint(sB + stage * C::kBBytes, &tmB, &full[stage], kb * BK,
+                                          brow, pol_b);
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ------------------------------------------------------------ MMA issuer
+            constexpr uint32_t idesc = ptx::umma_idesc_bf16(BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+                const int acc = it & 1;
+                const uint32_t aphase = (it >> 1) & 1;
+                ptx::mbar_wait(&tempty[acc], aphase ^ 1u);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem_base + acc * BN;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a0 = ptx::smem_u32(sA + stage * C::kABytes);
+                    const uint32_t b0 = ptx::smem_u32(sB + stage * C::kBBytes);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk) {
+                        const uint64_t ad = ptx::umma_desc_sw128_kmajor(a0 + kk * 32);
+                        const uint64_t bd = ptx::umma_desc_sw128_kmajor(b0 + kk * 32);
+                        ptx::umma_bf16(d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                    }
+                    ptx::umma_commit(&empty[stage]);
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+                ptx::umma_commit(&tfull[acc]);
+            }
+        }
+    } else if (warp >= 4) {
+        // ---------------------------------------------------------------- epilogue
+        const int q = warp - 4;  // TMEM lane quadrant (warp % 4)
+        int it = 0;
+        for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+            const int acc = it & 1;
+            const uint32_t aphase = (it >> 1) & 1;
+            const int m = tile % m_tiles, n = tile / m_tiles;
+            ptx::mbar_wait(&tfull[acc], aphase);
+            ptx::tc_fence_after();
+            const int r = q * 32 + lane;
+            const int arow = g.a_begin + m * BM + r;
+            const bool valid = arow < g.a_end;
+            const int64_t orow = (int64_t)g.out_base + (arow - g.a_begin);
+            const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+            if (MODE == kGemmSwiGLU) {
+                __nv_bfloat16* dst = out + orow * ldo + (int64_t)n * (BN / 2);
+#pragma unroll 1
+                for (int c = 0; c < BN / 2; c += 32) {
+                    uint32_t gv[32], uv[32];
+                    ptx::tmem_ld_32x32b_x32(taddr + c, gv);
+                    ptx::tmem_ld_32x32b_x32(taddr + BN / 2 + c, uv);
+                    ptx::tmem_ld_wait();
+                    if (valid) {
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const float h0 = silu_mul(__uint_as_float(gv[2 * i]), __uint_as_float(uv[2 * i]));
+                            const float h1 = silu_mul(__uint_as_float(gv[2 * i + 1]), __uint_as_float(uv[2 * i + 1]));
+                            pk[i] = ptx::pack_bf16x2(h0, h1);
+                        }
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            ptx::st_global_v4(dst + c + 8 * i, pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+                    }
+                }
+            } else {
+                __nv_bfloat16* dst = out + orow * ldo + (int64_t)n * BN;
+#pragma unroll 1
+                for (int c = 0; c < BN; c += 32) {
+                    uint32_t v[32];
+                    ptx::tmem_ld_32x32b_x32(taddr + c, v);
+                    ptx::tmem_ld_wait();
+                    if (valid) {
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            pk[i] = ptx::pack_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            ptx::st_global_v4(dst + c + 8 * i, pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+        }
+    }
+    __syncthreads();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
+    }
+}
+
+template <int BN, int MODE>
+cudaError_t launch_one(const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmGroup* group,
+                       int N, int K, __nv_bfloat16* out, int ldo, int grid, cudaStream_t st) {
+    using C = GemmCfg<BN>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(expert_gemm_kernel<BN, MODE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)C::kSmem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    expert_gemm_kernel<BN, MODE><<<grid, kThreads, C::kSmem, st>>>(*tmA, *tmB, group, N, K, out, ldo);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+int gemm_bn_for(int mode, int N) {
+    if (mode == kGemmSwiGLU) return (N % 256 == 0) ? 256 : 0;
+    if (N % 256 == 0) return 256;
+    if (N % 128 == 0) return 128;
+    return 0;
+}
+
+cudaError_t launch_expert_gemm(int mode, int bn, const CUtensorMap* tmA, const CUtensorMap* tmB,
+                               const GemmGroup* group, int N, int K, __nv_bfloat16* out,
+                               int ldo, int grid, cudaStream_t st) {
+    if (mode == kGemmSwiGLU) {
+        if (bn == 256) return launch_one<256, kGemmSwiGLU>(tmA, tmB, group, N, K, out, ldo, grid, st);
+    } else {
+        if (bn == 256) return launch_one<256, kGemmPlain>(tmA, tmB, group, N, K, out, ldo, grid, st);
+        if (bn == 128) return launch_one<128, kGemmPlain>(tmA, tmB, group, N, K, out, ldo, grid, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace moe

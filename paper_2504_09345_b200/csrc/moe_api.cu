@@ -1,0 +1,658 @@
+// moe_api.cu -- C ABI (include/moe.h) and the weight-streaming engine.
+//
+// Streaming engine ("weights for the next execution stage are prefetched at the
+// beginning of each stage by the Contiguous Data Mover ... runs asynchronously ... synchronizes
+// only at the stage boundaries"; PAPER.md:823-826 pinned host weights and a GPU weight buffer of
+// two units; PAPER.md:829-835 packetised transfers):
+//   * two device staging slots, each one packed expert (W13 | W2);
+//   * a dedicated copy stream; the copy of expert item q into slot q%2 waits on `slot_free[q%2]`
+//     (recorded after the GEMMs of item q-2) and records `ready13` / `ready2` after its W13 / W2
+//     parts, so GEMM1 of expert e starts as soon as its W13 lands and the H2D of expert e+1
+//     overlaps the GEMMs of expert e;
+//   * host enqueue order interleaves "GEMMs of item i" with "copy of item i+2", and a call's first
+//     two copies are enqueued before its routing kernels, so the copy engine runs back-to-back
+//     across experts AND across calls (cross-call prefetch of the next layer's first experts).
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/moe.h"
+#include "moe_internal.h"
+
+using moe::GemmGroup;
+
+namespace {
+
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                      const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                      const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                      CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled_t get_encode_fn() {
+    static PFN_encodeTiled_t fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+    });
+    return fn;
+}
+
+// bf16 [rows, cols] row-major, box = 64 columns (128 B, one swizzle atom) x box_rows rows.
+bool make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+    PFN_encodeTiled_t enc = get_encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 2};
+    cuuint32_t box[2] = {64, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+enum RecKind { kRecH2D = 0, kRecRoute, kRecPermute, kRecGemm1, kRecGemm2, kRecCombine, kRecComm,
+               kRecKinds };
+
+struct Rec {
+    int kind;
+    cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct moe_ctx_s {
+    moe_config cfg{};
+    int n_local = 0;       // routed experts owned by this rank
+    int n_all = 0;         // n_local + num_shared (items streamed per call)
+    int64_t blob_bytes = 0, w13_bytes = 0;
+    int num_sms = 148;
+    int bn1 = 256, bn2 = 256;
+    int64_t rows_cap = 0;
+    cudaStream_t copy_stream = nullptr;
+
+    // staging slots
+    void* slot[2] = {nullptr, nullptr};
+    cudaEvent_t ready13[2] = {}, ready2[2] = {}, slot_free[2] = {};
+    uint64_t seq = 0;
+    CUtensorMap tm_w13[2], tm_w2[2];
+
+    // workspace
+    int32_t* idx_ws = nullptr;
+    float* gates_ws = nullptr;
+    int32_t* tile_counts = nullptr;
+    int32_t* tile_prefix = nullptr;
+    int32_t* offsets = nullptr;
+    int32_t* counts = nullptr;
+    GemmGroup* grp1 = nullptr;
+    GemmGroup* grp2 = nullptr;
+    int32_t* pos = nullptr;
+    __nv_bfloat16* x_perm = nullptr;
+    __nv_bfloat16* h_act = nullptr;
+    __nv_bfloat16* y_perm = nullptr;
+    CUtensorMap tm_xperm, tm_h;
+    int64_t last_rows = 0;
+
+    // host-buffer mode (moe_layer_forward_host)
+    __nv_bfloat16* x_dev[2] = {nullptr, nullptr};
+    __nv_bfloat16* out_dev[2] = {nullptr, nullptr};
+    cudaEvent_t xbuf_free[2] = {}, x_ready[2] = {};
+    int host_parity = 0;
+
+    // profiling
+    std::vector<Rec> pending;
+    std::vector<cudaEvent_t> ev_pool;
+    moe_stats stats{};
+
+    std::unordered_set<const void*> pinned_ok;
+    std::string last_error;
+    moe_status sticky = MOE_OK;
+};
+
+namespace {
+
+moe_status set_err(moe_ctx c, moe_status s, const char* fmt, ...) {
+    if (c) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        c->last_error = buf;
+    }
+    return s;
+}
+
+#define MOE_CUDA(ctx, expr)                                                                  \
+    do {                                                                                     \
+        cudaError_t _e = (expr);                                                             \
+        if (_e != cudaSuccess) {                                                             \
+            if (ctx) (ctx)->sticky = MOE_E_CUDA;                                             \
+            return set_err(ctx, MOE_E_CUDA, "%s failed: %s (%s:%d)", #expr,                  \
+                           cudaGetErrorString(_e), __FILE__, __LINE__);                      \
+        }                                                                                    \
+    } while (0)
+
+cudaEvent_t pool_get(moe_ctx c) {
+    if (!c->ev_pool.empty()) {
+        cudaEvent_t e = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct Prof {  // RAII-less helper: begin()/end() around a launch when profiling is on
+    moe_ctx c;
+    bool on;
+    cudaEvent_t a = nullptr;
+    int kind;
+    cudaStream_t st;
+    Prof(moe_ctx c_, int k, cudaStream_t s) : c(c_), on((c_->cfg.flags & MOE_FLAG_PROFILE) != 0), kind(k), st(s) {
+        if (on) {
+            a = pool_get(c);
+            cudaEventRecord(a, st);
+        }
+    }
+    void end() {
+        if (on) {
+            cudaEvent_t b = pool_get(c);
+            cudaEventRecord(b, st);
+            c->pending.push_back(Rec{kind, a, b});
+        }
+    }
+};
+
+moe_status check_cfg(const moe_config* cfg) {
+    if (!cfg) return MOE_E_INVAL;
+    if (cfg->hidden <= 0 || cfg->ffn <= 0 || cfg->num_experts <= 0 || cfg->top_k <= 0 ||
+        cfg->top_k > cfg->num_experts || cfg->num_shared < 0 || cfg->max_tokens <= 0 ||
+        cfg->world_size <= 0 || cfg->rank < 0 || cfg->rank >= cfg->world_size ||
+        cfg->packet_bytes < 0)
+        return MOE_E_INVAL;
+    if (cfg->hidden % 128 || cfg->ffn % 128 || cfg->num_experts > moe::kMaxExperts ||
+        cfg->top_k > moe::kMaxTopK || cfg->num_shared > moe::kMaxShared)
+        return MOE_E_UNSUPPORTED;
+    if (cfg->num_experts % cfg->world_size) return MOE_E_UNSUPPORTED;
+    if (cfg->world_size > 1) return MOE_E_UNSUPPORTED;  // expert parallelism: see moe_ep (next)
+    const int64_t rows = (int64_t)cfg->max_tokens * (cfg->top_k + cfg->num_shared);
+    if (rows >= (1ll << 31)) return MOE_E_UNSUPPORTED;
+    return MOE_OK;
+}
+
+bool is_pinned(moe_ctx c, const void* p) {
+    if (c->pinned_ok.count(p)) return true;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    if (a.type == cudaMemoryTypeHost) {
+        c->pinned_ok.insert(p);
+        return true;
+    }
+    return false;
+}
+
+bool is_device(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+    const char* x = static_cast<const char*>(a);
+    const char* y = static_cast<const char*>(b);
+    return x < y + nb && y < x + na;
+}
+
+// Copy of streamed item q (index i of this call) into its slot; W13 part, then W2 part.
+moe_status enqueue_copy(moe_ctx c, const void* const* experts, int i, uint64_t q) {
+    const int s = (int)(q & 1);
+    MOE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->slot_free[s], 0));
+    const char* src = static_cast<const char*>(experts[i]);
+    char* dst = static_cast<char*>(c->slot[s]);
+    const int64_t pk = c->cfg.packet_bytes > 0 ? c->cfg.packet_bytes : INT64_MAX;
+    Prof p(c, kRecH2D, c->copy_stream);
+    auto copy_range = [&](int64_t lo, int64_t hi) -> moe_status {
+        for (int64_t o = lo; o < hi;) {
+            const int64_t n = std::min(pk, hi - o);
+            MOE_CUDA(c, cudaMemcpyAsync(dst + o, src + o, (size_t)n, cudaMemcpyHostToDevice,
+                                        c->copy_stream));
+            o += n;
+        }
+        return MOE_OK;
+    };
+    moe_status st = copy_range(0, c->w13_bytes);
+    if (st != MOE_OK) return st;
+    MOE_CUDA(c, cudaEventRecord(c->ready13[s], c->copy_stream));
+    st = copy_range(c->w13_bytes, c->blob_bytes);
+    if (st != MOE_OK) return st;
+    MOE_CUDA(c, cudaEventRecord(c->ready2[s], c->copy_stream));
+    p.end();
+    c->stats.h2d_weight_bytes += c->blob_bytes;
+    return MOE_OK;
+}
+
+moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __nv_bfloat16* wr,
+                        const void* const* experts, __nv_bfloat16* out, int32_t* topk_idx,
+                        float* topk_w, cudaStream_t st, bool hidden_on_copy_stream, int xb) {
+    const moe_config& cf = c->cfg;
+    const int h = cf.hidden, hi = cf.ffn, ne = cf.num_experts, k = cf.top_k, S = cf.num_shared;
+    const int n_tiles = (T + moe::kRouteTile - 1) / moe::kRouteTile;
+    int32_t* idx = topk_idx ? topk_idx : c->idx_ws;
+    float* gates = topk_w ? topk_w : c->gates_ws;
+    const uint64_t q0 = c->seq;
+
+    // A operand of the shared experts is the hidden batch itself (per-call tensor map).
+    CUtensorMap tm_x;
+    if (S > 0 && !make_tmap(&tm_x, hidden, (uint64_t)T, (uint64_t)h, 128))
+        return set_err(c, MOE_E_CUDA, "cuTensorMapEncodeTiled failed for hidden");
+
+    // first two weight copies go ahead of routing (cross-call prefetch)
+    for (int i = 0; i < std::min(2, c->n_all); ++i) {
+        moe_status s = enqueue_copy(c, experts, i, q0 + i);
+        if (s != MOE_OK) return s;
+    }
+    if (hidden_on_copy_stream) MOE_CUDA(c, cudaStreamWaitEvent(st, c->x_ready[xb], 0));
+
+    {
+        Prof p(c, kRecRoute, st);
+        MOE_CUDA(c, moe::launch_router_topk(hidden, T, h, wr, ne, k, cf.renormalize, idx, gates,
+                                            c->tile_counts, st));
+        MOE_CUDA(c, moe::launch_scan(c->tile_counts, n_tiles, ne, T, k, S, c->tile_prefix,
+                                     c->offsets, c->counts, c->grp1, c->grp2, st));
+        p.end();
+        c->stats.kernel_launches += 2;
+    }
+    {
+        Prof p(c, kRecPermute, st);
+        MOE_CUDA(c, moe::launch_permute(hidden, T, h, k, ne, idx, c->tile_prefix, c->offsets,
+                                        c->x_perm, c->pos, st));
+        p.end();
+        c->stats.kernel_launches += 1;
+    }
+    const int grid = c->num_sms;
+    for (int i = 0; i < c->n_all; ++i) {
+        const uint64_t q = q0 + i;
+        const int s = (int)(q & 1);
+        const bool shared = i >= c->n_local;
+        MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready13[s], 0));
+        {
+            Prof p(c, kRecGemm1, st);
+            MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmSwiGLU, c->bn1,
+                                                shared ? &tm_x : &c->tm_xperm, &c->tm_w13[s],
+                                                c->grp1 + i, 2 * hi, h, c->h_act, hi, grid, st));
+            p.end();
+        }
+        MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready2[s], 0));
+        {
+            Prof p(c, kRecGemm2, st);
+            MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmPlain, c->bn2, &c->tm_h, &c->tm_w2[s],
+                                                c->grp2 + i, h, hi, c->y_perm, h, grid, st));
+            p.end();
+        }
+        c->stats.kernel_launches += 2;
+        c->stats.gemm1_launches += 1;
+        c->stats.gemm2_launches += 1;
+        MOE_CUDA(c, cudaEventRecord(c->slot_free[s], st));
+        if (i + 2 < c->n_all) {
+            moe_status s2 = enqueue_copy(c, experts, i + 2, q + 2);
+            if (s2 != MOE_OK) return s2;
+        }
+    }
+    {
+        Prof p(c, kRecCombine, st);
+        MOE_CUDA(c, moe::launch_combine(c->y_perm, c->pos, gates, T, h, k, S, (int64_t)T * k, out, st));
+        p.end();
+        c->stats.kernel_launches += 1;
+    }
+    c->seq = q0 + c->n_all;
+    c->last_rows = (int64_t)T * (k + S);
+    c->stats.calls += 1;
+    return MOE_OK;
+}
+
+moe_status validate_call(moe_ctx c, int32_t T, const void* router_w, const void* const* experts,
+                         int32_t top_k) {
+    if (!c) return MOE_E_INVAL;
+    if (c->sticky != MOE_OK) return set_err(c, MOE_E_STATE, "context is in an error state");
+    if (T < 0 || T > c->cfg.max_tokens)
+        return set_err(c, MOE_E_INVAL, "num_tokens %d outside [0, %d]", T, c->cfg.max_tokens);
+    if (top_k != c->cfg.top_k)
+        return set_err(c, MOE_E_INVAL, "top_k %d != configured %d", top_k, c->cfg.top_k);
+    if (T == 0) return MOE_OK;
+    if (!router_w || !experts) return set_err(c, MOE_E_INVAL, "NULL router_w / experts");
+    if (!is_device(router_w)) return set_err(c, MOE_E_INVAL, "router_w is not device memory");
+    for (int i = 0; i < c->n_all; ++i) {
+        if (!experts[i]) return set_err(c, MOE_E_INVAL, "experts[%d] is NULL", i);
+        if (!is_pinned(c, experts[i]))
+            return set_err(c, MOE_E_NOT_PINNED, "experts[%d] is not page-locked host memory", i);
+    }
+    return MOE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t moe_packed_expert_bytes(int32_t hidden, int32_t ffn) {
+    if (hidden <= 0 || ffn <= 0) return 0;
+    return 6ll * hidden * ffn;
+}
+
+moe_status moe_pack_expert(int32_t hidden, int32_t ffn, const void* w1, const void* w3,
+                           const void* w2, void* dst) {
+    if (!w1 || !w3 || !w2 || !dst || hidden <= 0 || ffn <= 0) return MOE_E_INVAL;
+    if (ffn % 128) return MOE_E_UNSUPPORTED;
+    const size_t row = (size_t)hidden * 2;  // bytes per W1/W3 row
+    const char* a = static_cast<const char*>(w1);
+    const char* b = static_cast<const char*>(w3);
+    char* d = static_cast<char*>(dst);
+    // W13: 256-row N tiles = [128 rows of W1 ; the same 128 rows of W3]
+    for (int j = 0; j < ffn / 128; ++j) {
+        memcpy(d + (size_t)(256 * j) * row, a + (size_t)(128 * j) * row, 128 * row);
+        memcpy(d + (size_t)(256 * j + 128) * row, b + (size_t)(128 * j) * row, 128 * row);
+    }
+    memcpy(d + (size_t)2 * ffn * row, w2, (size_t)hidden * ffn * 2);
+    return MOE_OK;
+}
+
+moe_status moe_host_alloc(size_t bytes, void** ptr) {
+    if (!ptr || bytes == 0) return MOE_E_INVAL;
+    *ptr = nullptr;
+    if (cudaHostAlloc(ptr, bytes, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        *ptr = nullptr;
+        return MOE_E_NOMEM;
+    }
+    return MOE_OK;
+}
+
+moe_status moe_host_free(void* ptr) {
+    if (!ptr) return MOE_OK;
+    return cudaFreeHost(ptr) == cudaSuccess ? MOE_OK : MOE_E_CUDA;
+}
+
+moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
+    if (!out) return MOE_E_INVAL;
+    *out = nullptr;
+    moe_status s = check_cfg(cfg);
+    if (s != MOE_OK) return s;
+    if (!get_encode_fn()) return MOE_E_CUDA;
+    moe_ctx c = new moe_ctx_s();
+    c->cfg = *cfg;
+    auto fail = [&](moe_status st) {
+        moe_destroy(c);
+        return st;
+    };
+    if (cudaSetDevice(cfg->device) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(MOE_E_CUDA);
+    }
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, cfg->device) != cudaSuccess) return fail(MOE_E_CUDA);
+    if (prop.major != 10) return fail(MOE_E_UNSUPPORTED);  // sm_100a kernels only
+    c->num_sms = prop.multiProcessorCount;
+    const int h = cfg->hidden, hi = cfg->ffn, ne = cfg->num_experts, k = cfg->top_k;
+    const int S = cfg->num_shared, Tm = cfg->max_tokens;
+    c->n_local = ne / cfg->world_size;
+    c->n_all = c->n_local + S;
+    c->w13_bytes = 4ll * h * hi;
+    c->blob_bytes = moe_packed_expert_bytes(h, hi);
+    c->bn1 = moe::gemm_bn_for(moe::kGemmSwiGLU, 2 * hi);
+    c->bn2 = moe::gemm_bn_for(moe::kGemmPlain, h);
+    if (!c->bn1 || !c->bn2) return fail(MOE_E_UNSUPPORTED);
+    c->rows_cap = (int64_t)Tm * (k + S);
+    const int n_tiles = (Tm + moe::kRouteTile - 1) / moe::kRouteTile;
+
+    auto dalloc = [&](void** p, size_t n) { return cudaMalloc(p, n) == cudaSuccess; };
+    bool ok = true;
+    ok &= cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) == cudaSuccess;
+    for (int i = 0; i < 2; ++i) {
+        ok &= dalloc(&c->slot[i], (size_t)c->blob_bytes);
+        ok &= cudaEventCreateWithFlags(&c->ready13[i], cudaEventDisableTiming) == cudaSuccess;
+        ok &= cudaEventCreateWithFlags(&c->ready2[i], cudaEventDisableTiming) == cudaSuccess;
+        ok &= cudaEventCreateWithFlags(&c->slot_free[i], cudaEventDisableTiming) == cudaSuccess;
+        ok &= cudaEventCreateWithFlags(&c->xbuf_free[i], cudaEventDisableTiming) == cudaSuccess;
+        ok &= cudaEventCreateWithFlags(&c->x_ready[i], cudaEventDisableTiming) == cudaSuccess;
+    }
+    ok &= dalloc((void**)&c->idx_ws, sizeof(int32_t) * (size_t)Tm * k);
+    ok &= dalloc((void**)&c->gates_ws, sizeof(float) * (size_t)Tm * k);
+    ok &= dalloc((void**)&c->tile_counts, sizeof(int32_t) * (size_t)n_tiles * ne);
+    ok &= dalloc((void**)&c->tile_prefix, sizeof(int32_t) * (size_t)n_tiles * ne);
+    ok &= dalloc((void**)&c->offsets, sizeof(int32_t) * (size_t)(ne + 1));
+    ok &= dalloc((void**)&c->counts, sizeof(int32_t) * (size_t)(ne + S));
+    ok &= dalloc((void**)&c->grp1, sizeof(GemmGroup) * (size_t)(ne + S));
+    ok &= dalloc((void**)&c->grp2, sizeof(GemmGroup) * (size_t)(ne + S));
+    ok &= dalloc((void**)&c->pos, sizeof(int32_t) * (size_t)Tm * k);
+    ok &= dalloc((void**)&c->x_perm, 2 * (size_t)Tm * k * h);
+    ok &= dalloc((void**)&c->h_act, 2 * (size_t)c->rows_cap * hi);
+    ok &= dalloc((void**)&c->y_perm, 2 * (size_t)c->rows_cap * h);
+    if (!ok) {
+        cudaGetLastError();
+        return fail(MOE_E_NOMEM);
+    }
+    bool tm = true;
+    tm &= make_tmap(&c->tm_xperm, c->x_perm, (uint64_t)Tm * k, h, 128);
+    tm &= make_tmap(&c->tm_h, c->h_act, (uint64_t)c->rows_cap, hi, 128);
+    for (int i = 0; i < 2; ++i) {
+        tm &= make_tmap(&c->tm_w13[i], c->slot[i], 2ull * hi, h, (uint32_t)c->bn1);
+        tm &= make_tmap(&c->tm_w2[i], static_cast<char*>(c->slot[i]) + c->w13_bytes, (uint64_t)h,
+                        hi, (uint32_t)c->bn2);
+    }
+    if (!tm) return fail(MOE_E_CUDA);
+    if (cudaDeviceSynchronize() != cudaSuccess) return fail(MOE_E_CUDA);
+    *out = c;
+    return MOE_OK;
+}
+
+moe_status moe_layer_forward(moe_ctx ctx, const void* hidden, int32_t num_tokens,
+                             const void* router_w, const void* const* experts, int32_t top_k,
+                             void* out, int32_t* topk_idx, float* topk_w, void* stream) {
+    moe_status s = validate_call(ctx, num_tokens, router_w, experts, top_k);
+    if (s != MOE_OK || num_tokens == 0) return s;
+    if (!hidden || !out) return set_err(ctx, MOE_E_INVAL, "NULL hidden / out");
+    const size_t bytes = (size_t)num_tokens * ctx->cfg.hidden * 2;
+    if (overlaps(hidden, bytes, out, bytes)) return set_err(ctx, MOE_E_INVAL, "out aliases hidden");
+    if (((uintptr_t)hidden | (uintptr_t)out) & 15)
+        return set_err(ctx, MOE_E_INVAL, "hidden/out must be 16-byte aligned");
+    if (!is_device(hidden) || !is_device(out))
+        return set_err(ctx, MOE_E_INVAL, "hidden/out must be device memory");
+    if ((topk_idx && !is_device(topk_idx)) || (topk_w && !is_device(topk_w)))
+        return set_err(ctx, MOE_E_INVAL, "topk_idx/topk_w must be device memory");
+    MOE_CUDA(ctx, cudaSetDevice(ctx->cfg.device));
+    return forward_impl(ctx, static_cast<const __nv_bfloat16*>(hidden), num_tokens,
+                        static_cast<const __nv_bfloat16*>(router_w), experts,
+                        static_cast<__nv_bfloat16*>(out), topk_idx, topk_w,
+                        static_cast<cudaStream_t>(stream), false, 0);
+}
+
+moe_status moe_layer_forward_host(moe_ctx ctx, const void* hidden_host, int32_t num_tokens,
+                                  const void* router_w, const void* const* experts, int32_t top_k,
+                                  void* out_host, int32_t* topk_idx, float* topk_w, void* stream) {
+    moe_status s = validate_call(ctx, num_tokens, router_w, experts, top_k);
+    if (s != MOE_OK || num_tokens == 0) return s;
+    if (!hidden_host || !out_host) return set_err(ctx, MOE_E_INVAL, "NULL hidden / out");
+    if (!is_pinned(ctx, hidden_host) || !is_pinned(ctx, out_host))
+        return set_err(ctx, MOE_E_NOT_PINNED, "hidden_host/out_host must be page-locked");
+    MOE_CUDA(ctx, cudaSetDevice(ctx->cfg.device));
+    moe_ctx c = ctx;
+    const size_t bytes = (size_t)num_tokens * c->cfg.hidden * 2;
+    if (!c->x_dev[0]) {
+        const size_t cap = (size_t)c->cfg.max_tokens * c->cfg.hidden * 2;
+        for (int i = 0; i < 2; ++i) {
+            if (cudaMalloc(&c->x_dev[i], cap) != cudaSuccess || cudaMalloc(&c->out_dev[i], cap) != cudaSuccess) {
+                cudaGetLastError();
+                return set_err(c, MOE_E_NOMEM, "host-mode buffers");
+            }
+        }
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int b = c->host_parity;
+    c->host_parity ^= 1;
+    // tokens ride the copy stream ahead of this call's expert weights
+    MOE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->xbuf_free[b], 0));
+    MOE_CUDA(c, cudaMemcpyAsync(c->x_dev[b], hidden_host, bytes, cudaMemcpyHostToDevice, c->copy_stream));
+    MOE_CUDA(c, cudaEventRecord(c->x_ready[b], c->copy_stream));
+    c->stats.h2d_token_bytes += (int64_t)bytes;
+    s = forward_impl(c, c->x_dev[b], num_tokens, static_cast<const __nv_bfloat16*>(router_w),
+                     experts, c->out_dev[b], topk_idx, topk_w, st, true, b);
+    if (s != MOE_OK) return s;
+    MOE_CUDA(c, cudaEventRecord(c->xbuf_free[b], st));
+    MOE_CUDA(c, cudaMemcpyAsync(out_host, c->out_dev[b], bytes, cudaMemcpyDeviceToHost, st));
+    c->stats.d2h_token_bytes += (int64_t)bytes;
+    return MOE_OK;
+}
+
+moe_status moe_sync(moe_ctx ctx) {
+    if (!ctx) return MOE_E_INVAL;
+    MOE_CUDA(ctx, cudaSetDevice(ctx->cfg.device));
+    MOE_CUDA(ctx, cudaDeviceSynchronize());
+    return ctx->sticky;
+}
+
+moe_status moe_get_stats(moe_ctx ctx, moe_stats* out) {
+    if (!ctx || !out) return MOE_E_INVAL;
+    moe_status s = moe_sync(ctx);
+    if (s != MOE_OK) return s;
+    double* bucket[kRecKinds] = {&ctx->stats.h2d_ms,   &ctx->stats.route_ms,   &ctx->stats.permute_ms,
+                                 &ctx->stats.gemm1_ms, &ctx->stats.gemm2_ms,   &ctx->stats.combine_ms,
+                                 &ctx->stats.comm_ms};
+    for (const Rec& r : ctx->pending) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) *bucket[r.kind] += ms;
+        else cudaGetLastError();
+        ctx->ev_pool.push_back(r.a);
+        ctx->ev_pool.push_back(r.b);
+    }
+    ctx->pending.clear();
+    *out = ctx->stats;
+    return MOE_OK;
+}
+
+moe_status moe_reset_stats(moe_ctx ctx) {
+    if (!ctx) return MOE_E_INVAL;
+    moe_stats tmp;
+    moe_status s = moe_get_stats(ctx, &tmp);
+    ctx->stats = moe_stats{};
+    return s;
+}
+
+moe_status moe_debug_buffers(moe_ctx ctx, moe_debug_view* out) {
+    if (!ctx || !out) return MOE_E_INVAL;
+    out->counts = ctx->counts;
+    out->offsets = ctx->offsets;
+    out->pos = ctx->pos;
+    out->x_perm = ctx->x_perm;
+    out->h_act = ctx->h_act;
+    out->y_perm = ctx->y_perm;
+    out->rows = ctx->last_rows;
+    return MOE_OK;
+}
+
+moe_status moe_destroy(moe_ctx c) {
+    if (!c) return MOE_OK;
+    cudaSetDevice(c->cfg.device);
+    cudaDeviceSynchronize();
+    for (const Rec& r : c->pending) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(c->slot[i]);
+        cudaFree(c->x_dev[i]);
+        cudaFree(c->out_dev[i]);
+        cudaEvent_t evs[] = {c->ready13[i], c->ready2[i], c->slot_free[i], c->xbuf_free[i], c->x_ready[i]};
+        for (cudaEvent_t e : evs)
+            if (e) cudaEventDestroy(e);
+    }
+    void* bufs[] = {c->idx_ws, c->gates_ws, c->tile_counts, c->tile_prefix, c->offsets, c->counts,
+                    c->grp1, c->grp2, c->pos, c->x_perm, c->h_act, c->y_perm};
+    for (void* p : bufs) cudaFree(p);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    cudaGetLastError();
+    delete c;
+    return MOE_OK;
+}
+
+const char* moe_status_string(moe_status s) {
+    switch (s) {
+        case MOE_OK: return "MOE_OK";
+        case MOE_E_INVAL: return "MOE_E_INVAL: invalid argument";
+        case MOE_E_CUDA: return "MOE_E_CUDA: CUDA error";
+        case MOE_E_NCCL: return "MOE_E_NCCL: NCCL error";
+        case MOE_E_NOMEM: return "MOE_E_NOMEM: out of memory";
+        case MOE_E_NOT_PINNED: return "MOE_E_NOT_PINNED: host buffer is not page-locked";
+        case MOE_E_UNSUPPORTED: return "MOE_E_UNSUPPORTED: outside the kernels' envelope";
+        case MOE_E_STATE: return "MOE_E_STATE: context in error state";
+    }
+    return "unknown moe_status";
+}
+
+const char* moe_last_error(moe_ctx ctx) { return ctx ? ctx->last_error.c_str() : ""; }
+
+moe_status moe_probe_h2d(int32_t device, size_t bytes, int32_t iters, double* gbps) {
+    if (!gbps || bytes == 0 || iters <= 0) return MOE_E_INVAL;
+    *gbps = 0.0;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        cudaGetLastError();
+        return MOE_E_CUDA;
+    }
+    void* h = nullptr;
+    void* d = nullptr;
+    if (cudaHostAlloc(&h, bytes, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        return MOE_E_NOMEM;
+    }
+    if (cudaMalloc(&d, bytes) != cudaSuccess) {
+        cudaFreeHost(h);
+        cudaGetLastError();
+        return MOE_E_NOMEM;
+    }
+    memset(h, 1, bytes);
+    cudaStream_t st;
+    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st);  // warm-up
+    double best = 0.0;
+    for (int i = 0; i < iters; ++i) {
+        cudaEventRecord(a, st);
+        cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st);
+        cudaEventRecord(b, st);
+        cudaEventSynchronize(b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        if (ms > 0) best = std::max(best, (double)bytes / (ms * 1e-3) / 1e9);
+    }
+    cudaError_t e = cudaGetLastError();
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaStreamDestroy(st);
+    cudaFree(d);
+    cudaFreeHost(h);
+    *gbps = best;
+    return e == cudaSuccess ? MOE_OK : MOE_E_CUDA;
+}
+
+}  // extern "C"

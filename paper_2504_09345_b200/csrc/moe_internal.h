@@ -1,0 +1,53 @@
+// moe_internal.h -- shared declarations between the host engine (moe_api.cu) and the kernels.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace moe {
+
+constexpr int kRouteTile = 32;       // tokens per routing tile (router / permute granularity)
+constexpr int kMaxExperts = 128;     // envelope: N_e <= 128
+constexpr int kMaxTopK = 8;          // envelope: top_k <= 8
+constexpr int kMaxShared = 8;
+
+// Row range of one expert group inside a GEMM's A operand, and where its output rows go.
+struct GemmGroup {
+    int32_t a_begin;   // first A row of the group
+    int32_t a_end;     // one past the last A row
+    int32_t out_base;  // output row of A row a_begin
+    int32_t pad;
+};
+
+// ---------------------------------------------------------------------------- routing kernels
+// a2+a3: router GEMM (fp64, ascending c) + warp-shuffle top-k + softmax gates + per-tile counts.
+cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_bfloat16* wr,
+                               int ne, int k, int renorm, int32_t* idx, float* gates,
+                               int32_t* tile_counts, cudaStream_t st);
+// a4 (scan): tile prefix per expert, expert offsets, per-expert counts and GEMM group tables.
+//   expert_lo..expert_lo+n_local-1 are the experts whose groups are built (all of them at W=1).
+cudaError_t launch_scan(const int32_t* tile_counts, int n_tiles, int ne, int T, int k,
+                        int num_shared, int32_t* tile_prefix, int32_t* offsets, int32_t* counts,
+                        GemmGroup* grp1, GemmGroup* grp2, cudaStream_t st);
+// a4 (permute): stable position of every (t, j) and 16-byte row copies X[t] -> X_perm[pos].
+cudaError_t launch_permute(const __nv_bfloat16* x, int T, int h, int k, int ne,
+                           const int32_t* idx, const int32_t* tile_prefix,
+                           const int32_t* offsets, __nv_bfloat16* x_perm, int32_t* pos,
+                           cudaStream_t st);
+// a7: out[t] = sum_j g[t,j] * Y[pos[t,j]] + sum_s Y[R + s*T + t]  (fp32, fixed order) -> bf16.
+cudaError_t launch_combine(const __nv_bfloat16* y_perm, const int32_t* pos, const float* gates,
+                           int T, int h, int k, int num_shared, int64_t shared_base,
+                           __nv_bfloat16* out, cudaStream_t st);
+
+// ---------------------------------------------------------------------------- expert GEMM
+enum GemmMode { kGemmSwiGLU = 0, kGemmPlain = 1 };
+// One expert group of a5 (SwiGLU, N = 2*h_i interleaved) or a6 (plain, N = h) on tcgen05.
+//   tmA: A [rows, K] bf16 (box 64 x 128); tmB: B [N, K] bf16 (box 64 x bn); group: device ptr.
+//   out: bf16 [*, ldo]; SwiGLU writes N/2 columns.
+cudaError_t launch_expert_gemm(int mode, int bn, const CUtensorMap* tmA, const CUtensorMap* tmB,
+                               const GemmGroup* group, int N, int K, __nv_bfloat16* out,
+                               int ldo, int grid, cudaStream_t st);
+int gemm_bn_for(int mode, int N);   // tile width used for a given mode / N (0 = unsupported)
+
+}  // namespace moe

@@ -1,0 +1,91 @@
+"""CPU-side checks of the C-ABI library: it loads without a GPU, exports every symbol that
+include/moe.h declares, validates configurations without touching CUDA, and packs experts in the
+documented layout (host logic).  No compute calls are made here."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2504_09345_b200 as moe
+from paper_2504_09345_b200 import build as moe_build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    moe_build.build()
+    return moe.load()
+
+
+def test_library_exports_every_header_symbol(lib):
+    header = open(os.path.join(ROOT, "include", "moe.h")).read()
+    declared = set(re.findall(r"\b(moe_[a-z0-9_]+)\s*\(", header))
+    assert declared, "no declarations parsed"
+    assert declared == set(moe.EXPORTED)
+    for name in declared:
+        assert hasattr(lib, name), name
+
+
+def test_library_has_no_hard_libcuda_dependency(lib):
+    # static cudart; the driver is reached through cudaGetDriverEntryPoint at run time
+    import subprocess
+    out = subprocess.run(["ldd", moe.LIB_PATH], capture_output=True, text=True).stdout
+    assert "libcuda.so" not in out and "libcudart.so" not in out
+
+
+def test_packed_bytes_is_eq1_denominator(lib):
+    # 6 * h * h_i bytes per expert (3 bf16 matrices)
+    assert moe.moe_packed_expert_bytes(4096, 14336) == 352_321_536
+    assert moe.moe_packed_expert_bytes(128, 256) == 196_608
+    assert moe.moe_packed_expert_bytes(0, 256) == 0
+
+
+def test_pack_expert_layout(lib):
+    rng = np.random.default_rng(0)
+    h, hi = 128, 384
+    w1 = rng.integers(0, 65535, size=(hi, h), dtype=np.uint16)
+    w3 = rng.integers(0, 65535, size=(hi, h), dtype=np.uint16)
+    w2 = rng.integers(0, 65535, size=(h, hi), dtype=np.uint16)
+    dst = np.zeros(6 * h * hi // 2, dtype=np.uint16)
+    moe.moe_pack_expert(h, hi, w1, w3, w2, dst.ctypes.data)
+    w13 = dst[: 2 * hi * h].reshape(2 * hi, h)
+    for j in range(hi // 128):
+        assert np.array_equal(w13[256 * j: 256 * j + 128], w1[128 * j: 128 * j + 128])
+        assert np.array_equal(w13[256 * j + 128: 256 * j + 256], w3[128 * j: 128 * j + 128])
+    assert np.array_equal(dst[2 * hi * h:].reshape(h, hi), w2)
+
+
+def test_pack_rejects_bad_shapes(lib):
+    a = np.zeros(10, dtype=np.uint16)
+    with pytest.raises(moe.MoEError) as e:
+        moe.moe_pack_expert(128, 200, a, a, a, a.ctypes.data)   # h_i % 128 != 0
+    assert e.value.status == moe.MOE_E_UNSUPPORTED
+    assert lib.moe_pack_expert(128, 256, None, None, None, None) == moe.MOE_E_INVAL
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(top_k=9), moe.MOE_E_INVAL),                 # top_k > num_experts
+    (dict(top_k=0), moe.MOE_E_INVAL),
+    (dict(hidden=100), moe.MOE_E_UNSUPPORTED),        # h % 128 != 0
+    (dict(ffn=200), moe.MOE_E_UNSUPPORTED),
+    (dict(num_experts=200, top_k=2), moe.MOE_E_UNSUPPORTED),
+    (dict(max_tokens=0), moe.MOE_E_INVAL),
+    (dict(world_size=3), moe.MOE_E_UNSUPPORTED),      # 8 experts do not shard over 3 ranks
+    (dict(rank=2, world_size=2), moe.MOE_E_INVAL),
+])
+def test_config_validation_without_gpu(lib, kw, status):
+    base = dict(hidden=128, ffn=256, num_experts=8, top_k=2, num_shared=0, max_tokens=64,
+                renormalize=1, device=0, world_size=1, rank=0, nccl_unique_id=None,
+                packet_bytes=0, flags=0)
+    base.update(kw)
+    cfg = moe.moe_config(**base)
+    with pytest.raises(moe.MoEError) as e:
+        moe.moe_init(cfg)
+    assert e.value.status == status
+
+
+def test_status_strings(lib):
+    for s in range(8):
+        assert moe.status_string(s).startswith("MOE_")

@@ -1,0 +1,212 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star):
+  * expert indices bit-exact (both sides rank fp64 logits accumulated in ascending channel order);
+  * gates within 1e-6 absolute (fp64 softmax on both sides, stored fp32);
+  * outputs: per-token max-abs error / max-abs reference <= 2e-2.
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2504_09345_b200 import (MOE_E_INVAL, MOE_E_NOT_PINNED, MoEError, moe_layer_forward)
+
+from gpu_helpers import GpuRun, bf16_tensor, dev_view, sample_tokens, to_f32, token_rel_err
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-2
+
+
+def _check_full(inp, renormalize=True, **kw):
+    run = GpuRun(inp, renormalize=renormalize, **kw)
+    try:
+        out, idx, gates = run.run()
+        cfg = inp.cfg
+        y_ref, idx_ref, g_ref = oracle.forward(inp.x, inp.router, inp.w1, inp.w3, inp.w2,
+                                               cfg.top_k, cfg.num_shared, renormalize)
+        assert np.array_equal(idx.cpu().numpy(), idx_ref)
+        assert np.max(np.abs(gates.cpu().numpy() - g_ref)) <= 1e-6
+        err = token_rel_err(to_f32(out), y_ref)
+        assert err.max() <= TOL, f"max token rel err {err.max():.3e}"
+        return run, out, idx, gates, err
+    except Exception:
+        run.close()
+        raise
+
+
+def test_tiny_config_parity():
+    inp = synth.gen_inputs(synth.CONFIGS["tiny"])
+    run, out, idx, gates, err = _check_full(inp)
+    # counts in the workspace equal the histogram of the selected experts
+    dbg = run.layer.debug()
+    cnt = dev_view(dbg.counts, (inp.cfg.num_experts,), "<i4").cpu().numpy()
+    assert np.array_equal(cnt, np.bincount(idx.cpu().numpy().ravel(), minlength=8))
+    print(f"tiny max token rel err {err.max():.3e}")
+    run.close()
+
+
+@pytest.mark.parametrize("shape", [
+    dict(hidden=256, ffn=384, num_experts=8, top_k=2, tokens=300),            # ragged T and groups
+    dict(hidden=512, ffn=640, num_experts=16, top_k=4, tokens=1000, num_shared=1),
+    dict(hidden=384, ffn=256, num_experts=64, top_k=6, tokens=777, num_shared=2),
+    dict(hidden=128, ffn=128, num_experts=5, top_k=5, tokens=129),            # k = N_e
+    dict(hidden=256, ffn=256, num_experts=1, top_k=1, tokens=70),              # dense FFN
+])
+def test_ragged_shapes_parity(shape):
+    cfg = synth.MoEConfig("custom", 7, shape["hidden"], shape["ffn"], shape["num_experts"],
+                          shape["top_k"], shape["tokens"], shape.get("num_shared", 0))
+    inp = synth.gen_inputs(cfg)
+    run, *_ = _check_full(inp)
+    run.close()
+
+
+def test_full_softmax_gates_mode():
+    inp = synth.gen_inputs(synth.MoEConfig("custom", 8, 256, 256, 8, 2, 200))
+    run, *_ = _check_full(inp, renormalize=False)
+    run.close()
+
+
+def test_mostly_empty_experts_and_single_token():
+    cfg = synth.MoEConfig("custom", 9, 256, 512, 64, 2, 3)
+    inp = synth.gen_inputs(cfg)
+    run, *_ = _check_full(inp)
+    out, idx, gates = run.run(inp.x[:1])
+    y1, i1, g1 = oracle.forward(inp.x[:1], inp.router, inp.w1, inp.w3, inp.w2, 2)
+    assert np.array_equal(idx.cpu().numpy(), i1)
+    assert token_rel_err(to_f32(out), y1).max() <= TOL
+    run.close()
+
+
+def test_zero_tokens_is_noop():
+    inp = synth.gen_inputs(synth.CONFIGS["tiny"])
+    run = GpuRun(inp)
+    x = bf16_tensor(inp.x[:0].reshape(0, 128))
+    out = torch.empty_like(x)
+    run.layer.forward(x, run.router, run.experts, out)
+    run.layer.sync()
+    assert run.layer.stats()["calls"] == 0
+    run.close()
+
+
+def test_tie_cases_zero_and_duplicate_router():
+    inp = synth.gen_inputs(synth.CONFIGS["tiny"])
+    for router in (np.zeros_like(inp.router), None):
+        r = inp.router.copy() if router is None else router
+        if router is None:
+            r[5] = r[3]
+        inp2 = dataclasses.replace(inp, router=r)
+        run, out, idx, gates, err = _check_full(inp2)
+        if router is not None:
+            assert (idx.cpu().numpy() == np.array([0, 1])).all()
+        run.close()
+
+
+def test_determinism_and_back_to_back_streaming():
+    """Several calls back to back over 2 layers (slots recycle across calls, cross-call
+    prefetch) give bitwise the same outputs as isolated calls."""
+    cfg = synth.MoEConfig("custom", 10, 512, 768, 8, 2, 500)
+    layers = [synth.gen_inputs(cfg, layer=l) for l in range(2)]
+    runs = [GpuRun(l) for l in layers]
+    iso = [r.run() for r in runs]
+    # back to back without host sync: enqueue 6 calls alternating layers on one context
+    ctx = runs[0]
+    outs = []
+    s = torch.cuda.current_stream()
+    for it in range(6):
+        lay = layers[it % 2]
+        x = bf16_tensor(lay.x)
+        o = torch.empty_like(x)
+        r = bf16_tensor(lay.router)
+        ex = runs[it % 2].experts
+        ctx.layer.forward(x, r, ex, o, stream=s.cuda_stream)
+        outs.append((it % 2, o, x, r))
+    s.synchronize()
+    for l, o, _, _ in outs:
+        assert torch.equal(o, iso[l][0])
+    for r in runs:
+        r.close()
+
+
+def test_host_buffer_entry_point_matches_device():
+    inp = synth.gen_inputs(synth.MoEConfig("custom", 11, 256, 384, 8, 2, 333))
+    run = GpuRun(inp, packet_bytes=64 * 1024)
+    out_dev, idx_dev, _ = run.run()
+    xh = torch.from_numpy(inp.x.view(np.int16)).view(torch.bfloat16).pin_memory()
+    oh = torch.empty_like(xh).pin_memory()
+    for _ in range(3):
+        run.layer.forward_host(xh, run.router, run.experts, oh,
+                               stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.current_stream().synchronize()
+    assert torch.equal(oh, out_dev.cpu())
+    st = run.layer.stats()
+    assert st["h2d_token_bytes"] == 3 * inp.x.nbytes and st["d2h_token_bytes"] == 3 * inp.x.nbytes
+    run.close()
+
+
+def test_invalid_arguments():
+    inp = synth.gen_inputs(synth.CONFIGS["tiny"])
+    run = GpuRun(inp)
+    x = bf16_tensor(inp.x)
+    out = torch.empty_like(x)
+    with pytest.raises(MoEError) as e:
+        moe_layer_forward(run.layer.ctx, x.data_ptr(), 64, run.router.data_ptr(),
+                          run.experts.array, 3, out.data_ptr())
+    assert e.value.status == MOE_E_INVAL
+    with pytest.raises(MoEError) as e:   # num_tokens > max_tokens
+        moe_layer_forward(run.layer.ctx, x.data_ptr(), 65, run.router.data_ptr(),
+                          run.experts.array, 2, out.data_ptr())
+    assert e.value.status == MOE_E_INVAL
+    with pytest.raises(MoEError) as e:   # out aliases hidden
+        moe_layer_forward(run.layer.ctx, x.data_ptr(), 64, run.router.data_ptr(),
+                          run.experts.array, 2, x.data_ptr())
+    assert e.value.status == MOE_E_INVAL
+    import ctypes
+    pageable = [np.zeros(run.experts.blob_bytes, dtype=np.uint8) for _ in range(8)]
+    arr = (ctypes.c_void_p * 8)(*[p.ctypes.data for p in pageable])
+    with pytest.raises(MoEError) as e:
+        moe_layer_forward(run.layer.ctx, x.data_ptr(), 64, run.router.data_ptr(), arr, 2,
+                          out.data_ptr())
+    assert e.value.status == MOE_E_NOT_PINNED
+    run.close()
+
+
+def test_stats_h2d_bytes_equal_algorithmic_bytes():
+    inp = synth.gen_inputs(synth.MoEConfig("custom", 12, 256, 384, 8, 2, 256))
+    run = GpuRun(inp, profile=True)
+    for _ in range(3):
+        run.run()
+    st = run.layer.stats()
+    assert st["h2d_weight_bytes"] == 3 * 8 * 6 * 256 * 384
+    assert st["gemm1_launches"] == 24 and st["h2d_ms"] > 0 and st["gemm1_ms"] > 0
+    run.close()
+
+
+# ------------------------------------------------------------------------------- full configs
+@pytest.mark.parametrize("name", ["mixtral_8x7b", "mixtral_8x22b", "dbrx", "dsv2_lite"])
+def test_full_size_config(name):
+    """Full BASELINE.json sizes in the bench's launch configuration: routing bit-exact on all
+    tokens (oracle router + top-k over every token), outputs on sampled tokens."""
+    cfg = synth.CONFIGS[name]
+    inp = synth.gen_inputs(cfg)
+    run = GpuRun(inp)
+    try:
+        out, idx, gates = run.run()
+        logits = oracle.router_logits(inp.x, inp.router)
+        idx_ref, g_ref = oracle.topk_gates(logits, cfg.top_k)
+        idx_gpu = idx.cpu().numpy()
+        assert np.array_equal(idx_gpu, idx_ref), f"{(idx_gpu != idx_ref).any(1).sum()} tokens differ"
+        assert np.max(np.abs(gates.cpu().numpy() - g_ref)) <= 1e-6
+        sel = sample_tokens(cfg.tokens, 24)
+        y_ref = oracle.experts_combine(inp.x[sel], inp.w1, inp.w3, inp.w2, cfg.num_experts,
+                                       cfg.num_shared, idx_ref[sel], g_ref[sel])
+        err = token_rel_err(to_f32(out[torch.from_numpy(sel).cuda()]), y_ref)
+        print(f"{name}: max token rel err {err.max():.3e} over {len(sel)} tokens; "
+              f"expert load {np.bincount(idx_ref.ravel(), minlength=cfg.num_experts).tolist()}")
+        assert err.max() <= TOL
+    finally:
+        run.close()
