@@ -160,7 +160,7 @@ def run_reference(args):
     value = n * args.steps / tot
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg.name, "tokens": cfg.tokens, "hidden": cfg.hidden,
                        "ffn": cfg.ffn, "experts": cfg.num_experts, "top_k": cfg.top_k,
@@ -184,28 +184,58 @@ def run_ours(args):
     from paper_2504_09345_b200 import ledger
 
     rank, world, local = dist_env()
-    if world > 1:
-        raise SystemExit("expert-parallel multi-GPU bench is not built yet (single GPU only)")
     torch.cuda.set_device(local)
-    moe_build.build()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if rank == 0:
+        moe_build.build()
+    if world > 1:
+        dist.barrier()
     peaks = load_peaks()
     cfg = synth.CONFIGS[args.config]
-    T = cfg.tokens
+    T = cfg.tokens                      # global tokens per step (strong scaling over ranks)
+    if T % world or cfg.num_experts % world:
+        raise SystemExit(f"{cfg.name}: tokens/experts do not split over {world} ranks")
+    Tr = T // world
+    nl = cfg.num_experts // world
+    ids = list(range(rank * nl, (rank + 1) * nl)) + [cfg.num_experts + s for s in range(cfg.num_shared)]
 
-    # ---- inputs: L layers of host weights (pinned, packed), device x / router per layer
-    layers = [synth.gen_inputs(cfg, layer=l) for l in range(args.layers)]
+    def allmax(v):
+        if world == 1:
+            return v
+        t = torch.tensor([float(v)], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(v):
+        if world == 1:
+            return v
+        t = torch.tensor([float(v)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # ---- inputs: L layers; this rank's token slice and only its own experts (pinned, packed)
+    layers = [synth.gen_inputs(cfg, layer=l, expert_ids=ids) for l in range(args.layers)]
     experts = [moe.HostExperts(cfg.hidden, cfg.ffn, l.w1, l.w3, l.w2) for l in layers]
-    xs = [torch.from_numpy(l.x.view(np.int16)).view(torch.bfloat16).cuda() for l in layers]
+    xslice = [np.ascontiguousarray(l.x[rank * Tr:(rank + 1) * Tr]) for l in layers]
+    xs = [torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).cuda() for x in xslice]
     routers = [torch.from_numpy(l.router.view(np.int16)).view(torch.bfloat16).cuda() for l in layers]
     outs = [torch.empty_like(x) for x in xs]
-    idxs = [torch.empty((T, cfg.top_k), dtype=torch.int32, device="cuda") for _ in layers]
-    gws = [torch.empty((T, cfg.top_k), dtype=torch.float32, device="cuda") for _ in layers]
+    idxs = [torch.empty((Tr, cfg.top_k), dtype=torch.int32, device="cuda") for _ in layers]
+    gws = [torch.empty((Tr, cfg.top_k), dtype=torch.float32, device="cuda") for _ in layers]
 
+    if world > 1:
+        dist.barrier()   # all ranks probe their host links at the same time (shared host DRAM)
     probe_gbs = moe.moe_probe_h2d(local, 1 << 30, 5)   # paper's method: 1 GB pinned H2D copies
-
-    layer = moe.MoELayer(cfg.hidden, cfg.ffn, cfg.num_experts, cfg.top_k, T,
+    uid = None
+    if world > 1:
+        obj = [moe.moe_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    layer = moe.MoELayer(cfg.hidden, cfg.ffn, cfg.num_experts, cfg.top_k, Tr,
                          num_shared=cfg.num_shared, device=local, profile=True,
-                         packet_bytes=int(args.packet_mb * 2 ** 20))
+                         packet_bytes=int(args.packet_mb * 2 ** 20), world_size=world, rank=rank,
+                         nccl_unique_id=uid)
     stream = torch.cuda.Stream()
     sh = stream.cuda_stream
 
@@ -213,33 +243,52 @@ def run_ours(args):
         l = i % args.layers
         layer.forward(xs[l], routers[l], experts[l], outs[l], idxs[l], gws[l], stream=sh)
 
-    for i in range(args.warmup):
-        step(i)
-    torch.cuda.synchronize()
-    layer.reset_stats()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clocks = ClockSampler(local)
-    clocks.start()
-    torch.cuda.synchronize()
-    ev0.record(stream)
-    for i in range(args.steps):
-        step(args.warmup + i)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    clk = clocks.stop()
-    ms_total = ev0.elapsed_time(ev1)
-    st = layer.stats()
-    ms = ms_total / args.steps
-    value = T * world / (ms / 1e3)
+    def timed(fn, sampler=None):
+        for i in range(args.warmup):
+            fn(i)
+        torch.cuda.synchronize()
+        layer.reset_stats()          # per-kernel stats cover the timed steps only
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if sampler is not None:
+            sampler.start()
+        e0.record(stream)
+        for i in range(args.steps):
+            fn(args.warmup + i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if sampler is not None:
+            sampler.result = sampler.stop()
+        if world > 1:
+            dist.barrier()
+        return allmax(e0.elapsed_time(e1)) / args.steps
 
-    # ---- work ledger (experts hit: from the routing of the timed layers)
-    hit = [int((np.bincount(idxs[l].cpu().numpy().ravel(), minlength=cfg.num_experts) > 0).sum())
-           for l in range(args.layers)]
+    clocks = ClockSampler(local)
+    ms = timed(step, clocks)
+    clk = clocks.result
+    st = layer.stats()
+    value = T / (ms / 1e3)
+
+    # ---- work ledger (experts hit: from the routing of the timed layers, all ranks)
+    cnt = torch.zeros(cfg.num_experts, dtype=torch.int64, device="cuda")
+    for l in range(args.layers):
+        cnt += torch.bincount(idxs[l].flatten().long(), minlength=cfg.num_experts)
+    if world > 1:
+        dist.all_reduce(cnt)
+    hit = int((cnt > 0).sum().item())
     work = ledger.layer_work(T, cfg.hidden, cfg.ffn, cfg.num_experts, cfg.top_k, cfg.num_shared,
-                             experts_hit=min(hit))
-    rl = ledger.roofline_time_s(work, peaks["bf16_tflops_sustained"], probe_gbs)
-    g1_launch_ms = st["gemm1_ms"] / max(1, st["gemm1_launches"])
-    g1_flops_launch = work.gemm1_flops / (cfg.num_experts + cfg.num_shared)
+                             experts_hit=hit)
+    rank_bytes = (nl + cfg.num_shared) * ledger.expert_bytes(cfg.hidden, cfg.ffn)
+    t_io = allmax(rank_bytes / (probe_gbs * 1e9))                  # slowest rank's host link
+    t_tc = work.expert_flops / world / (peaks["bf16_tflops_sustained"] * 1e12)
+    t_roof = max(t_io, t_tc)
+    # dominant kernel: GEMM1 (+SwiGLU).  FLOPs per launch over all ranks / avg launch time.
+    g1_ms, g1_n = allsum(st["gemm1_ms"]), allsum(st["gemm1_launches"])
+    g1_flops_total = work.gemm1_flops * args.steps
+    g1_flops_launch = g1_flops_total / max(1.0, g1_n)
+    g1_launch_ms = g1_ms / max(1.0, g1_n)
     achieved_tf = g1_flops_launch / (g1_launch_ms * 1e-3) / 1e12 if g1_launch_ms > 0 else 0.0
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -248,74 +297,74 @@ def run_ours(args):
     roofline = {"kernel": "expert_gemm_kernel<256,SwiGLU> (a5, tcgen05)", "bound": "tensor",
                 "achieved": achieved_tf, "peak": peaks["bf16_tflops_sustained"],
                 "unit": "TFLOP/s", "frac": achieved_tf / peaks["bf16_tflops_sustained"],
-                "traffic": traffic, "peak_source": peaks["source"] + " bf16_tflops_sustained",
+                "traffic": traffic if world == 1 else None,
+                "peak_source": peaks["source"] + " bf16_tflops_sustained",
                 "flops_per_launch": g1_flops_launch, "avg_launch_ms": g1_launch_ms}
     h2d_gbs = st["h2d_weight_bytes"] / (st["h2d_ms"] * 1e-3) / 1e9 if st["h2d_ms"] > 0 else 0.0
-    roofline_step = {"bound": rl["bound"], "t_roofline_ms": rl["t_roofline_s"] * 1e3,
-                     "t_host_link_ms": rl["t_host_link_s"] * 1e3,
-                     "t_tensor_ms": rl["t_tensor_s"] * 1e3, "ms_per_step": ms,
-                     "frac": rl["t_roofline_s"] * 1e3 / ms,
-                     "roofline_tokens_per_s": T / rl["t_roofline_s"],
-                     "host_link_probe_gbs": probe_gbs, "h2d_achieved_gbs_in_copies": h2d_gbs,
-                     "h2d_effective_gbs_over_step": work.weight_bytes / (ms * 1e-3) / 1e9,
-                     "weight_bytes_per_step": work.weight_bytes, "expert_flops_per_step": work.expert_flops,
+    roofline_step = {"bound": "host_link" if t_io >= t_tc else "tensor",
+                     "t_roofline_ms": t_roof * 1e3, "t_host_link_ms": t_io * 1e3,
+                     "t_tensor_ms": t_tc * 1e3, "ms_per_step": ms, "frac": t_roof * 1e3 / ms,
+                     "roofline_tokens_per_s": T / t_roof,
+                     "host_link_probe_gbs_rank0": probe_gbs,
+                     "host_link_probe_gbs_min": -allmax(-probe_gbs),
+                     "h2d_achieved_gbs_in_copies_rank0": h2d_gbs,
+                     "h2d_aggregate_gbs_over_step": work.weight_bytes / (ms * 1e-3) / 1e9,
+                     "weight_bytes_per_step": work.weight_bytes,
+                     "weight_bytes_per_rank": rank_bytes,
+                     "expert_flops_per_step": work.expert_flops,
                      "tensor_peak_tflops": peaks["bf16_tflops_sustained"]}
     per_kernel_ms = {k: st[k] / args.steps for k in
-                     ("h2d_ms", "route_ms", "permute_ms", "gemm1_ms", "gemm2_ms", "combine_ms")}
+                     ("h2d_ms", "route_ms", "permute_ms", "gemm1_ms", "gemm2_ms", "combine_ms",
+                      "comm_ms")}
+    launches = allsum(st["kernel_launches"])
 
     # ---- e2e: host token buffers through moe_layer_forward_host (H2D tokens + D2H output)
     e2e = None
     if not args.no_e2e:
-        xh = [torch.from_numpy(l.x.view(np.int16)).view(torch.bfloat16).pin_memory() for l in layers]
+        xh = [torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).pin_memory() for x in xslice]
         oh = [torch.empty_like(x).pin_memory() for x in xh]
 
         def step_h(i):
             l = i % args.layers
             layer.forward_host(xh[l], routers[l], experts[l], oh[l], stream=sh)
 
-        for i in range(args.warmup):
-            step_h(i)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for i in range(args.steps):
-            step_h(args.warmup + i)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1) / args.steps
+        ems = timed(step_h)
         tok_bytes = T * cfg.hidden * 2
-        e2e = {"value": T * world / (ems / 1e3), "unit": "tokens/s", "ms_per_step": ems,
+        e2e = {"value": T / (ems / 1e3), "unit": "tokens/s", "ms_per_step": ems,
                "h2d_bytes_per_step": tok_bytes + work.weight_bytes,
                "h2d_token_bytes_per_step": tok_bytes, "h2d_weight_bytes_per_step": work.weight_bytes,
                "d2h_bytes_per_step": tok_bytes,
                "api": "moe_layer_forward_host (pinned host hidden/out)"}
-        # parity spot check of the e2e output against the device-path output
-        e2e["matches_device_path"] = bool(torch.equal(oh[(args.warmup + args.steps - 1) % args.layers].cuda(),
-                                                      outs[(args.warmup + args.steps - 1) % args.layers]))
+        last = (args.warmup + args.steps - 1) % args.layers
+        e2e["matches_device_path"] = bool(allmax(0.0 if torch.equal(oh[last].cuda(), outs[last]) else 1.0) == 0.0)
 
     cpu = None
     if rank == 0 and not args.no_cpu:
-        cpu = cpu_baseline(layers[0], args.cpu_seconds)
+        full = synth.gen_inputs(cfg, layer=0) if world > 1 else layers[0]
+        cpu = cpu_baseline(full, args.cpu_seconds)
 
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded random bf16 weights/tokens shaped like the model)",
-            "config": {"workload": cfg.name, "tokens": T, "hidden": cfg.hidden, "ffn": cfg.ffn,
-                       "experts": cfg.num_experts, "top_k": cfg.top_k,
-                       "num_shared": cfg.num_shared, "layers_cycled": args.layers,
-                       "staging_slots": 2, "packet_mb": args.packet_mb,
+            "config": {"workload": cfg.name, "tokens": T, "tokens_per_rank": Tr,
+                       "hidden": cfg.hidden, "ffn": cfg.ffn, "experts": cfg.num_experts,
+                       "experts_per_rank": nl, "top_k": cfg.top_k, "num_shared": cfg.num_shared,
+                       "layers_cycled": args.layers, "staging_slots": 2, "packet_mb": args.packet_mb,
                        "l2": "inputs larger than L2: all expert weights re-streamed from host each step",
                        "parallelism": f"ep{world}"},
-            "roofline": roofline, "roofline_step": roofline_step, "per_kernel_ms_per_step": per_kernel_ms,
+            "roofline": roofline, "roofline_step": roofline_step,
+            "per_kernel_ms_per_step_rank0": per_kernel_ms,
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
-            "gpu_launches": st["kernel_launches"],
-            "gpu_launches_per_step": st["kernel_launches"] / args.steps}
+            "gpu_launches": int(launches),
+            "gpu_launches_per_step": launches / args.steps}
     if rank == 0:
         print(json.dumps(line), flush=True)
     layer.close()
     for e in experts:
         e.close()
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def main():

@@ -51,7 +51,9 @@ typedef enum {
 } moe_status;
 
 /* Flags for moe_config.flags */
-#define MOE_FLAG_PROFILE 1u /* record CUDA events around every kernel and copy (moe_get_stats) */
+#define MOE_FLAG_PROFILE 1u  /* record CUDA events around every kernel and copy (moe_get_stats) */
+#define MOE_FLAG_FORCE_EP 2u /* world_size == 1: still run the expert-parallel exchange through a
+                                one-rank NCCL communicator (tests the EP path on one GPU)        */
 
 /*
  * Layer configuration.  Envelope of the sm_100a kernels (MOE_E_UNSUPPORTED otherwise):
@@ -163,6 +165,27 @@ moe_status moe_destroy(moe_ctx ctx);
 
 const char* moe_status_string(moe_status s);
 const char* moe_last_error(moe_ctx ctx);   /* detail of the last failure ("" if none) */
+
+/*
+ * Expert-parallel exchange plan (host-only, deterministic).  Rank r owns routed
+ * experts [r*n_local, (r+1)*n_local), n_local = num_experts / world.  Given counts[W][N_e] (rows
+ * each rank routes to each expert, all-gathered), fills for `rank`:
+ *   send_off[d*n_local + le], send_cnt[...]  rows of this rank's expert-sorted x_perm that go to
+ *                                            (destination rank d, its local expert le);
+ *   recv_off[s*n_local + le], recv_cnt[...]  where rows from (source rank s, local expert le)
+ *                                            land in x_recv, laid out expert-major
+ *                                            (local expert, then source rank, then token);
+ *   grp_off[n_local + 1]                     expert group boundaries in x_recv.
+ * The combine exchange is the exact reverse (recv_* -> send_*).  Returns the number of rows this
+ * rank receives, or -1 on invalid arguments.
+ */
+int64_t moe_ep_plan(int32_t world, int32_t rank, int32_t num_experts, const int32_t* counts,
+                    int32_t* send_off, int32_t* send_cnt, int32_t* recv_off, int32_t* recv_cnt,
+                    int32_t* grp_off);
+
+/* 128-byte ncclUniqueId for moe_config.nccl_unique_id (call on one rank, broadcast to all).
+ * MOE_E_NCCL if libnccl.so.2 cannot be loaded. */
+moe_status moe_nccl_unique_id(void* out128);
 
 /* Host-link probe, the paper's method ("B_IO ... based on 1GB tensor transfers"):
  * `iters` pinned host->device copies of `bytes` on `device`; returns the best GB/s (1e9 B/s). */

@@ -27,11 +27,12 @@ MOE_E_NOT_PINNED = 5
 MOE_E_UNSUPPORTED = 6
 MOE_E_STATE = 7
 MOE_FLAG_PROFILE = 1
+MOE_FLAG_FORCE_EP = 2
 
 EXPORTED = ["moe_packed_expert_bytes", "moe_pack_expert", "moe_host_alloc", "moe_host_free",
             "moe_init", "moe_layer_forward", "moe_layer_forward_host", "moe_sync", "moe_get_stats",
             "moe_reset_stats", "moe_debug_buffers", "moe_destroy", "moe_status_string",
-            "moe_last_error", "moe_probe_h2d"]
+            "moe_last_error", "moe_probe_h2d", "moe_ep_plan", "moe_nccl_unique_id"]
 
 
 class moe_config(ctypes.Structure):
@@ -101,8 +102,12 @@ def load(path: str = LIB_PATH):
     lib.moe_last_error.argtypes = [P]
     lib.moe_last_error.restype = ctypes.c_char_p
     lib.moe_probe_h2d.argtypes = [i32, ctypes.c_size_t, i32, ctypes.POINTER(ctypes.c_double)]
+    lib.moe_ep_plan.argtypes = [i32, i32, i32, P, P, P, P, P, P]
+    lib.moe_ep_plan.restype = i64
+    lib.moe_nccl_unique_id.argtypes = [P]
     for name in EXPORTED:
-        if name not in ("moe_packed_expert_bytes", "moe_status_string", "moe_last_error"):
+        if name not in ("moe_packed_expert_bytes", "moe_status_string", "moe_last_error",
+                        "moe_ep_plan"):
             getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -190,6 +195,29 @@ def moe_probe_h2d(device: int = 0, nbytes: int = 1 << 30, iters: int = 5) -> flo
     return g.value
 
 
+def moe_ep_plan(world: int, rank: int, num_experts: int, counts: np.ndarray) -> dict:
+    """Expert-parallel exchange plan (host logic in the library; see include/moe.h)."""
+    counts = np.ascontiguousarray(counts, dtype=np.int32).reshape(world, num_experts)
+    nl = num_experts // world if world > 0 else 0
+    n = max(1, world * nl)
+    out = {k: np.zeros(n, dtype=np.int32) for k in ("send_off", "send_cnt", "recv_off", "recv_cnt")}
+    out["grp_off"] = np.zeros(nl + 1, dtype=np.int32)
+    rows = load().moe_ep_plan(world, rank, num_experts, counts.ctypes.data,
+                              out["send_off"].ctypes.data, out["send_cnt"].ctypes.data,
+                              out["recv_off"].ctypes.data, out["recv_cnt"].ctypes.data,
+                              out["grp_off"].ctypes.data)
+    if rows < 0:
+        raise MoEError(MOE_E_INVAL, "moe_ep_plan")
+    out["recv_rows"] = int(rows)
+    return out
+
+
+def moe_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load().moe_nccl_unique_id(buf))
+    return buf.raw
+
+
 # ----------------------------------------------------------------------------- convenience
 class HostExperts:
     """Pinned, packed expert blobs of one layer (this rank's routed experts, then shared)."""
@@ -232,10 +260,12 @@ class MoELayer:
     def __init__(self, hidden: int, ffn: int, num_experts: int, top_k: int, max_tokens: int,
                  num_shared: int = 0, renormalize: bool = True, device: int = 0,
                  world_size: int = 1, rank: int = 0, packet_bytes: int = 0,
-                 profile: bool = False, nccl_unique_id: Optional[bytes] = None):
+                 profile: bool = False, nccl_unique_id: Optional[bytes] = None,
+                 force_ep: bool = False):
+        flags = (MOE_FLAG_PROFILE if profile else 0) | (MOE_FLAG_FORCE_EP if force_ep else 0)
         self.cfg = moe_config(hidden, ffn, num_experts, top_k, num_shared, max_tokens,
                               int(renormalize), device, world_size, rank, None, packet_bytes,
-                              MOE_FLAG_PROFILE if profile else 0)
+                              flags)
         self._uid = None
         if nccl_unique_id is not None:
             self._uid = ctypes.create_string_buffer(bytes(nccl_unique_id), len(nccl_unique_id))
@@ -246,8 +276,9 @@ class MoELayer:
     def forward(self, hidden, router_w, experts: HostExperts, out, topk_idx=None, topk_w=None,
                 stream: int = 0):
         """Device tensors (torch) in, device tensors out; enqueued on `stream` (raw handle)."""
-        moe_layer_forward(self.ctx, hidden.data_ptr(), hidden.shape[0], router_w.data_ptr(),
-                          experts.array, self.top_k, out.data_ptr(),
+        moe_layer_forward(self.ctx, hidden.data_ptr() if hidden.numel() else 0, hidden.shape[0],
+                          router_w.data_ptr(),
+                          experts.array, self.top_k, out.data_ptr() if out.numel() else 0,
                           topk_idx.data_ptr() if topk_idx is not None else 0,
                           topk_w.data_ptr() if topk_w is not None else 0, stream)
 

@@ -1,0 +1,169 @@
+// engine.h -- the context object behind the C ABI and helpers shared by moe_api.cu / ep.cu.
+#pragma once
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/moe.h"
+#include "moe_internal.h"
+
+namespace moe {
+
+enum RecKind { kRecH2D = 0, kRecRoute, kRecPermute, kRecGemm1, kRecGemm2, kRecCombine, kRecComm,
+               kRecKinds };
+
+struct Rec {
+    int kind;
+    cudaEvent_t a, b;
+};
+
+// ------------------------------------------------------------------ NCCL (dlopen'ed, EP only)
+// Minimal ABI-stable declarations (NCCL >= 2.10): we never link NCCL at build time, so the
+// library loads on machines without it; expert parallelism dlopens the process's libnccl.so.2
+// (the one torch.distributed already loaded, or MOE_NCCL_LIBRARY).
+typedef struct ncclComm* ncclComm_t;
+typedef int ncclResult_t;
+struct ncclUniqueId { char internal[128]; };
+enum { kNcclInt32 = 2, kNcclBfloat16 = 9 };
+
+struct NcclApi {
+    void* handle = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+const NcclApi* nccl_api();  // nullptr if libnccl cannot be found
+
+}  // namespace moe
+
+struct moe_ctx_s {
+    moe_config cfg{};
+    int n_local = 0;       // routed experts owned by this rank
+    int n_all = 0;         // n_local + num_shared (items streamed per call)
+    int64_t blob_bytes = 0, w13_bytes = 0;
+    int num_sms = 148;
+    int bn1 = 256, bn2 = 256;
+    int64_t rows_cap = 0;  // rows of h_act / y_perm (single GPU)
+    cudaStream_t copy_stream = nullptr;
+
+    // staging slots (a GPU weight buffer of two units)
+    void* slot[2] = {nullptr, nullptr};
+    cudaEvent_t ready13[2] = {}, ready2[2] = {}, slot_free[2] = {};
+    uint64_t seq = 0;  // streamed-item counter across calls: item q uses slot q % 2
+    CUtensorMap tm_w13[2], tm_w2[2];
+
+    // workspace
+    int32_t* idx_ws = nullptr;
+    float* gates_ws = nullptr;
+    int32_t* tile_counts = nullptr;
+    int32_t* tile_prefix = nullptr;
+    int32_t* offsets = nullptr;
+    int32_t* counts = nullptr;
+    moe::GemmGroup* grp1 = nullptr;
+    moe::GemmGroup* grp2 = nullptr;
+    int32_t* pos = nullptr;
+    __nv_bfloat16* x_perm = nullptr;
+    __nv_bfloat16* h_act = nullptr;
+    __nv_bfloat16* y_perm = nullptr;
+    CUtensorMap tm_xperm, tm_h;
+    int64_t last_rows = 0;
+
+    // expert parallelism (world_size > 1, or MOE_FLAG_FORCE_EP)
+    bool ep = false;
+    moe::ncclComm_t comm = nullptr;
+    int64_t cap_recv = 0;              // rows a rank can receive: W * max_tokens * top_k
+    int32_t* counts_all = nullptr;     // device [W][N_e]
+    int32_t* counts_all_h = nullptr;   // pinned host copy
+    moe::GemmGroup* ep_grp_h = nullptr;  // pinned [2][n_all]
+    moe::GemmGroup* ep_grp = nullptr;    // device [2][n_all]
+    __nv_bfloat16* x_recv = nullptr;
+    __nv_bfloat16* y_recv = nullptr;
+    CUtensorMap tm_xrecv;
+    std::vector<int32_t> send_off, send_cnt, recv_off, recv_cnt, grp_off;
+    int64_t last_recv_rows = 0, comm_bytes = 0;
+
+    // host-buffer mode (moe_layer_forward_host)
+    __nv_bfloat16* x_dev[2] = {nullptr, nullptr};
+    __nv_bfloat16* out_dev[2] = {nullptr, nullptr};
+    cudaEvent_t xbuf_free[2] = {}, x_ready[2] = {};
+    int host_parity = 0;
+
+    // profiling
+    std::vector<moe::Rec> pending;
+    std::vector<cudaEvent_t> ev_pool;
+    moe_stats stats{};
+
+    std::unordered_set<const void*> pinned_ok;
+    std::string last_error;
+    moe_status sticky = MOE_OK;
+};
+
+namespace moe {
+
+moe_status set_err(moe_ctx c, moe_status s, const char* fmt, ...);
+bool make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
+cudaEvent_t pool_get(moe_ctx c);
+
+#define MOE_CUDA(ctx, expr)                                                                  \
+    do {                                                                                     \
+        cudaError_t _e = (expr);                                                             \
+        if (_e != cudaSuccess) {                                                             \
+            if (ctx) (ctx)->sticky = MOE_E_CUDA;                                             \
+            return ::moe::set_err(ctx, MOE_E_CUDA, "%s failed: %s (%s:%d)", #expr,           \
+                                  cudaGetErrorString(_e), __FILE__, __LINE__);               \
+        }                                                                                    \
+    } while (0)
+
+#define MOE_NCCL(ctx, expr)                                                                  \
+    do {                                                                                     \
+        ::moe::ncclResult_t _r = (expr);                                                     \
+        if (_r != 0) {                                                                       \
+            if (ctx) (ctx)->sticky = MOE_E_NCCL;                                             \
+            return ::moe::set_err(ctx, MOE_E_NCCL, "%s failed: %s (%s:%d)", #expr,           \
+                                  ::moe::nccl_api()->GetErrorString(_r), __FILE__, __LINE__); \
+        }                                                                                    \
+    } while (0)
+
+// CUDA-event bracket around a launch when MOE_FLAG_PROFILE is set.
+struct Prof {
+    moe_ctx c;
+    bool on;
+    cudaEvent_t a = nullptr;
+    int kind;
+    cudaStream_t st;
+    Prof(moe_ctx c_, int k, cudaStream_t s)
+        : c(c_), on((c_->cfg.flags & MOE_FLAG_PROFILE) != 0), kind(k), st(s) {
+        if (on) {
+            a = pool_get(c);
+            cudaEventRecord(a, st);
+        }
+    }
+    void end() {
+        if (on) {
+            cudaEvent_t b = pool_get(c);
+            cudaEventRecord(b, st);
+            c->pending.push_back(Rec{kind, a, b});
+        }
+    }
+};
+
+// expert parallelism (ep.cu)
+moe_status ep_init(moe_ctx c);
+void ep_destroy(moe_ctx c);
+// After routing/permute on `st`: exchange counts (host sync), build the plan, dispatch x_perm
+// rows to their experts' ranks (NCCL grouped send/recv).
+moe_status ep_dispatch(moe_ctx c, int T, cudaStream_t st);
+// After the local expert GEMMs: return y_recv rows to their source ranks' y_perm.
+moe_status ep_combine(moe_ctx c, cudaStream_t st);
+
+}  // namespace moe

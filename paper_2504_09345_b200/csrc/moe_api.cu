@@ -5,31 +5,26 @@
 // only at the stage boundaries"; PAPER.md:823-826 pinned host weights and a GPU weight buffer of
 // two units; PAPER.md:829-835 packetised transfers):
 //   * two device staging slots, each one packed expert (W13 | W2);
-//   * a dedicated copy stream; the copy of expert item q into slot q%2 waits on `slot_free[q%2]`
+//   * a dedicated copy stream; the copy of streamed item q into slot q%2 waits on `slot_free[q%2]`
 //     (recorded after the GEMMs of item q-2) and records `ready13` / `ready2` after its W13 / W2
 //     parts, so GEMM1 of expert e starts as soon as its W13 lands and the H2D of expert e+1
 //     overlaps the GEMMs of expert e;
 //   * host enqueue order interleaves "GEMMs of item i" with "copy of item i+2", and a call's first
 //     two copies are enqueued before its routing kernels, so the copy engine runs back-to-back
 //     across experts AND across calls (cross-call prefetch of the next layer's first experts).
-#include <dlfcn.h>
-
 #include <algorithm>
-#include <cstdarg>
-#include <cstdio>
+#include <climits>
 #include <cstring>
 #include <mutex>
-#include <string>
-#include <unordered_set>
-#include <vector>
 
-#include "../../include/moe.h"
-#include "moe_internal.h"
+#include "engine.h"
 
 using moe::GemmGroup;
+using moe::Prof;
+
+namespace moe {
 
 namespace {
-
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                       const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                       const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -45,14 +40,16 @@ PFN_encodeTiled_t get_encode_fn() {
                 cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
             fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+        cudaGetLastError();
     });
     return fn;
 }
+}  // namespace
 
 // bf16 [rows, cols] row-major, box = 64 columns (128 B, one swizzle atom) x box_rows rows.
 bool make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
     PFN_encodeTiled_t enc = get_encode_fn();
-    if (!enc) return false;
+    if (!enc || rows == 0) return false;
     cuuint64_t dims[2] = {cols, rows};
     cuuint64_t strides[1] = {cols * 2};
     cuuint32_t box[2] = {64, box_rows};
@@ -62,66 +59,6 @@ bool make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, u
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
-
-enum RecKind { kRecH2D = 0, kRecRoute, kRecPermute, kRecGemm1, kRecGemm2, kRecCombine, kRecComm,
-               kRecKinds };
-
-struct Rec {
-    int kind;
-    cudaEvent_t a, b;
-};
-
-}  // namespace
-
-struct moe_ctx_s {
-    moe_config cfg{};
-    int n_local = 0;       // routed experts owned by this rank
-    int n_all = 0;         // n_local + num_shared (items streamed per call)
-    int64_t blob_bytes = 0, w13_bytes = 0;
-    int num_sms = 148;
-    int bn1 = 256, bn2 = 256;
-    int64_t rows_cap = 0;
-    cudaStream_t copy_stream = nullptr;
-
-    // staging slots
-    void* slot[2] = {nullptr, nullptr};
-    cudaEvent_t ready13[2] = {}, ready2[2] = {}, slot_free[2] = {};
-    uint64_t seq = 0;
-    CUtensorMap tm_w13[2], tm_w2[2];
-
-    // workspace
-    int32_t* idx_ws = nullptr;
-    float* gates_ws = nullptr;
-    int32_t* tile_counts = nullptr;
-    int32_t* tile_prefix = nullptr;
-    int32_t* offsets = nullptr;
-    int32_t* counts = nullptr;
-    GemmGroup* grp1 = nullptr;
-    GemmGroup* grp2 = nullptr;
-    int32_t* pos = nullptr;
-    __nv_bfloat16* x_perm = nullptr;
-    __nv_bfloat16* h_act = nullptr;
-    __nv_bfloat16* y_perm = nullptr;
-    CUtensorMap tm_xperm, tm_h;
-    int64_t last_rows = 0;
-
-    // host-buffer mode (moe_layer_forward_host)
-    __nv_bfloat16* x_dev[2] = {nullptr, nullptr};
-    __nv_bfloat16* out_dev[2] = {nullptr, nullptr};
-    cudaEvent_t xbuf_free[2] = {}, x_ready[2] = {};
-    int host_parity = 0;
-
-    // profiling
-    std::vector<Rec> pending;
-    std::vector<cudaEvent_t> ev_pool;
-    moe_stats stats{};
-
-    std::unordered_set<const void*> pinned_ok;
-    std::string last_error;
-    moe_status sticky = MOE_OK;
-};
-
-namespace {
 
 moe_status set_err(moe_ctx c, moe_status s, const char* fmt, ...) {
     if (c) {
@@ -135,16 +72,6 @@ moe_status set_err(moe_ctx c, moe_status s, const char* fmt, ...) {
     return s;
 }
 
-#define MOE_CUDA(ctx, expr)                                                                  \
-    do {                                                                                     \
-        cudaError_t _e = (expr);                                                             \
-        if (_e != cudaSuccess) {                                                             \
-            if (ctx) (ctx)->sticky = MOE_E_CUDA;                                             \
-            return set_err(ctx, MOE_E_CUDA, "%s failed: %s (%s:%d)", #expr,                  \
-                           cudaGetErrorString(_e), __FILE__, __LINE__);                      \
-        }                                                                                    \
-    } while (0)
-
 cudaEvent_t pool_get(moe_ctx c) {
     if (!c->ev_pool.empty()) {
         cudaEvent_t e = c->ev_pool.back();
@@ -156,26 +83,11 @@ cudaEvent_t pool_get(moe_ctx c) {
     return e;
 }
 
-struct Prof {  // RAII-less helper: begin()/end() around a launch when profiling is on
-    moe_ctx c;
-    bool on;
-    cudaEvent_t a = nullptr;
-    int kind;
-    cudaStream_t st;
-    Prof(moe_ctx c_, int k, cudaStream_t s) : c(c_), on((c_->cfg.flags & MOE_FLAG_PROFILE) != 0), kind(k), st(s) {
-        if (on) {
-            a = pool_get(c);
-            cudaEventRecord(a, st);
-        }
-    }
-    void end() {
-        if (on) {
-            cudaEvent_t b = pool_get(c);
-            cudaEventRecord(b, st);
-            c->pending.push_back(Rec{kind, a, b});
-        }
-    }
-};
+}  // namespace moe
+
+namespace {
+
+using moe::set_err;
 
 moe_status check_cfg(const moe_config* cfg) {
     if (!cfg) return MOE_E_INVAL;
@@ -188,8 +100,9 @@ moe_status check_cfg(const moe_config* cfg) {
         cfg->top_k > moe::kMaxTopK || cfg->num_shared > moe::kMaxShared)
         return MOE_E_UNSUPPORTED;
     if (cfg->num_experts % cfg->world_size) return MOE_E_UNSUPPORTED;
-    if (cfg->world_size > 1) return MOE_E_UNSUPPORTED;  // expert parallelism: see moe_ep (next)
-    const int64_t rows = (int64_t)cfg->max_tokens * (cfg->top_k + cfg->num_shared);
+    if (cfg->world_size > 1 && !cfg->nccl_unique_id) return MOE_E_INVAL;
+    const int64_t rows = (int64_t)cfg->max_tokens * cfg->world_size * cfg->top_k +
+                         (int64_t)cfg->max_tokens * cfg->num_shared;
     if (rows >= (1ll << 31)) return MOE_E_UNSUPPORTED;
     return MOE_OK;
 }
@@ -230,7 +143,7 @@ moe_status enqueue_copy(moe_ctx c, const void* const* experts, int i, uint64_t q
     const char* src = static_cast<const char*>(experts[i]);
     char* dst = static_cast<char*>(c->slot[s]);
     const int64_t pk = c->cfg.packet_bytes > 0 ? c->cfg.packet_bytes : INT64_MAX;
-    Prof p(c, kRecH2D, c->copy_stream);
+    Prof p(c, moe::kRecH2D, c->copy_stream);
     auto copy_range = [&](int64_t lo, int64_t hi) -> moe_status {
         for (int64_t o = lo; o < hi;) {
             const int64_t n = std::min(pk, hi - o);
@@ -262,8 +175,10 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     const uint64_t q0 = c->seq;
 
     // A operand of the shared experts is the hidden batch itself (per-call tensor map).
-    CUtensorMap tm_x;
-    if (S > 0 && !make_tmap(&tm_x, hidden, (uint64_t)T, (uint64_t)h, 128))
+    // (T == 0 only happens under EP: the rank serves other ranks' tokens; its shared-expert
+    // groups are then empty and never touch the map.)
+    CUtensorMap tm_x = c->tm_xperm;
+    if (S > 0 && T > 0 && !moe::make_tmap(&tm_x, hidden, (uint64_t)T, (uint64_t)h, 128))
         return set_err(c, MOE_E_CUDA, "cuTensorMapEncodeTiled failed for hidden");
 
     // first two weight copies go ahead of routing (cross-call prefetch)
@@ -274,7 +189,7 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     if (hidden_on_copy_stream) MOE_CUDA(c, cudaStreamWaitEvent(st, c->x_ready[xb], 0));
 
     {
-        Prof p(c, kRecRoute, st);
+        Prof p(c, moe::kRecRoute, st);
         MOE_CUDA(c, moe::launch_router_topk(hidden, T, h, wr, ne, k, cf.renormalize, idx, gates,
                                             c->tile_counts, st));
         MOE_CUDA(c, moe::launch_scan(c->tile_counts, n_tiles, ne, T, k, S, c->tile_prefix,
@@ -283,12 +198,29 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         c->stats.kernel_launches += 2;
     }
     {
-        Prof p(c, kRecPermute, st);
+        Prof p(c, moe::kRecPermute, st);
         MOE_CUDA(c, moe::launch_permute(hidden, T, h, k, ne, idx, c->tile_prefix, c->offsets,
                                         c->x_perm, c->pos, st));
         p.end();
         c->stats.kernel_launches += 1;
     }
+
+    // Expert parallelism: ship each token row to the rank owning its expert.
+    const CUtensorMap* tmA_routed = &c->tm_xperm;
+    const GemmGroup* g1 = c->grp1;
+    const GemmGroup* g2 = c->grp2;
+    __nv_bfloat16* y_routed = c->y_perm;
+    if (c->ep) {
+        Prof p(c, moe::kRecComm, st);
+        moe_status s = moe::ep_dispatch(c, T, st);
+        if (s != MOE_OK) return s;
+        p.end();
+        tmA_routed = &c->tm_xrecv;
+        g1 = c->ep_grp;
+        g2 = c->ep_grp + c->n_all;
+        y_routed = c->y_recv;
+    }
+
     const int grid = c->num_sms;
     for (int i = 0; i < c->n_all; ++i) {
         const uint64_t q = q0 + i;
@@ -296,17 +228,18 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         const bool shared = i >= c->n_local;
         MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready13[s], 0));
         {
-            Prof p(c, kRecGemm1, st);
+            Prof p(c, moe::kRecGemm1, st);
             MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmSwiGLU, c->bn1,
-                                                shared ? &tm_x : &c->tm_xperm, &c->tm_w13[s],
-                                                c->grp1 + i, 2 * hi, h, c->h_act, hi, grid, st));
+                                                shared ? &tm_x : tmA_routed, &c->tm_w13[s],
+                                                g1 + i, 2 * hi, h, c->h_act, hi, grid, st));
             p.end();
         }
         MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready2[s], 0));
         {
-            Prof p(c, kRecGemm2, st);
+            Prof p(c, moe::kRecGemm2, st);
             MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmPlain, c->bn2, &c->tm_h, &c->tm_w2[s],
-                                                c->grp2 + i, h, hi, c->y_perm, h, grid, st));
+                                                g2 + i, h, hi, shared ? c->y_perm : y_routed, h,
+                                                grid, st));
             p.end();
         }
         c->stats.kernel_launches += 2;
@@ -318,8 +251,14 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
             if (s2 != MOE_OK) return s2;
         }
     }
+    if (c->ep) {
+        Prof p(c, moe::kRecComm, st);
+        moe_status s = moe::ep_combine(c, st);
+        if (s != MOE_OK) return s;
+        p.end();
+    }
     {
-        Prof p(c, kRecCombine, st);
+        Prof p(c, moe::kRecCombine, st);
         MOE_CUDA(c, moe::launch_combine(c->y_perm, c->pos, gates, T, h, k, S, (int64_t)T * k, out, st));
         p.end();
         c->stats.kernel_launches += 1;
@@ -338,7 +277,7 @@ moe_status validate_call(moe_ctx c, int32_t T, const void* router_w, const void*
         return set_err(c, MOE_E_INVAL, "num_tokens %d outside [0, %d]", T, c->cfg.max_tokens);
     if (top_k != c->cfg.top_k)
         return set_err(c, MOE_E_INVAL, "top_k %d != configured %d", top_k, c->cfg.top_k);
-    if (T == 0) return MOE_OK;
+    if (T == 0 && !c->ep) return MOE_OK;
     if (!router_w || !experts) return set_err(c, MOE_E_INVAL, "NULL router_w / experts");
     if (!is_device(router_w)) return set_err(c, MOE_E_INVAL, "router_w is not device memory");
     for (int i = 0; i < c->n_all; ++i) {
@@ -396,7 +335,6 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     *out = nullptr;
     moe_status s = check_cfg(cfg);
     if (s != MOE_OK) return s;
-    if (!get_encode_fn()) return MOE_E_CUDA;
     moe_ctx c = new moe_ctx_s();
     c->cfg = *cfg;
     auto fail = [&](moe_status st) {
@@ -412,15 +350,19 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     if (prop.major != 10) return fail(MOE_E_UNSUPPORTED);  // sm_100a kernels only
     c->num_sms = prop.multiProcessorCount;
     const int h = cfg->hidden, hi = cfg->ffn, ne = cfg->num_experts, k = cfg->top_k;
-    const int S = cfg->num_shared, Tm = cfg->max_tokens;
-    c->n_local = ne / cfg->world_size;
+    const int S = cfg->num_shared, Tm = cfg->max_tokens, W = cfg->world_size;
+    c->ep = W > 1 || (cfg->flags & MOE_FLAG_FORCE_EP);
+    c->n_local = ne / W;
     c->n_all = c->n_local + S;
     c->w13_bytes = 4ll * h * hi;
     c->blob_bytes = moe_packed_expert_bytes(h, hi);
     c->bn1 = moe::gemm_bn_for(moe::kGemmSwiGLU, 2 * hi);
     c->bn2 = moe::gemm_bn_for(moe::kGemmPlain, h);
     if (!c->bn1 || !c->bn2) return fail(MOE_E_UNSUPPORTED);
-    c->rows_cap = (int64_t)Tm * (k + S);
+    c->cap_recv = c->ep ? (int64_t)W * Tm * k : (int64_t)Tm * k;
+    // h_act rows: routed rows (received rows under EP) then S * Tm shared rows
+    const int64_t h_rows = c->cap_recv + (int64_t)S * Tm;
+    c->rows_cap = (int64_t)Tm * (k + S);  // y_perm rows
     const int n_tiles = (Tm + moe::kRouteTile - 1) / moe::kRouteTile;
 
     auto dalloc = [&](void** p, size_t n) { return cudaMalloc(p, n) == cudaSuccess; };
@@ -444,21 +386,25 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     ok &= dalloc((void**)&c->grp2, sizeof(GemmGroup) * (size_t)(ne + S));
     ok &= dalloc((void**)&c->pos, sizeof(int32_t) * (size_t)Tm * k);
     ok &= dalloc((void**)&c->x_perm, 2 * (size_t)Tm * k * h);
-    ok &= dalloc((void**)&c->h_act, 2 * (size_t)c->rows_cap * hi);
+    ok &= dalloc((void**)&c->h_act, 2 * (size_t)h_rows * hi);
     ok &= dalloc((void**)&c->y_perm, 2 * (size_t)c->rows_cap * h);
     if (!ok) {
         cudaGetLastError();
         return fail(MOE_E_NOMEM);
     }
     bool tm = true;
-    tm &= make_tmap(&c->tm_xperm, c->x_perm, (uint64_t)Tm * k, h, 128);
-    tm &= make_tmap(&c->tm_h, c->h_act, (uint64_t)c->rows_cap, hi, 128);
+    tm &= moe::make_tmap(&c->tm_xperm, c->x_perm, (uint64_t)Tm * k, h, 128);
+    tm &= moe::make_tmap(&c->tm_h, c->h_act, (uint64_t)h_rows, hi, 128);
     for (int i = 0; i < 2; ++i) {
-        tm &= make_tmap(&c->tm_w13[i], c->slot[i], 2ull * hi, h, (uint32_t)c->bn1);
-        tm &= make_tmap(&c->tm_w2[i], static_cast<char*>(c->slot[i]) + c->w13_bytes, (uint64_t)h,
-                        hi, (uint32_t)c->bn2);
+        tm &= moe::make_tmap(&c->tm_w13[i], c->slot[i], 2ull * hi, h, (uint32_t)c->bn1);
+        tm &= moe::make_tmap(&c->tm_w2[i], static_cast<char*>(c->slot[i]) + c->w13_bytes,
+                             (uint64_t)h, hi, (uint32_t)c->bn2);
     }
     if (!tm) return fail(MOE_E_CUDA);
+    if (c->ep) {
+        moe_status es = moe::ep_init(c);
+        if (es != MOE_OK) return fail(es);
+    }
     if (cudaDeviceSynchronize() != cudaSuccess) return fail(MOE_E_CUDA);
     *out = c;
     return MOE_OK;
@@ -468,16 +414,18 @@ moe_status moe_layer_forward(moe_ctx ctx, const void* hidden, int32_t num_tokens
                              const void* router_w, const void* const* experts, int32_t top_k,
                              void* out, int32_t* topk_idx, float* topk_w, void* stream) {
     moe_status s = validate_call(ctx, num_tokens, router_w, experts, top_k);
-    if (s != MOE_OK || num_tokens == 0) return s;
-    if (!hidden || !out) return set_err(ctx, MOE_E_INVAL, "NULL hidden / out");
-    const size_t bytes = (size_t)num_tokens * ctx->cfg.hidden * 2;
-    if (overlaps(hidden, bytes, out, bytes)) return set_err(ctx, MOE_E_INVAL, "out aliases hidden");
-    if (((uintptr_t)hidden | (uintptr_t)out) & 15)
-        return set_err(ctx, MOE_E_INVAL, "hidden/out must be 16-byte aligned");
-    if (!is_device(hidden) || !is_device(out))
-        return set_err(ctx, MOE_E_INVAL, "hidden/out must be device memory");
-    if ((topk_idx && !is_device(topk_idx)) || (topk_w && !is_device(topk_w)))
-        return set_err(ctx, MOE_E_INVAL, "topk_idx/topk_w must be device memory");
+    if (s != MOE_OK || (num_tokens == 0 && !ctx->ep)) return s;
+    if (num_tokens > 0) {
+        if (!hidden || !out) return set_err(ctx, MOE_E_INVAL, "NULL hidden / out");
+        const size_t bytes = (size_t)num_tokens * ctx->cfg.hidden * 2;
+        if (overlaps(hidden, bytes, out, bytes)) return set_err(ctx, MOE_E_INVAL, "out aliases hidden");
+        if (((uintptr_t)hidden | (uintptr_t)out) & 15)
+            return set_err(ctx, MOE_E_INVAL, "hidden/out must be 16-byte aligned");
+        if (!is_device(hidden) || !is_device(out))
+            return set_err(ctx, MOE_E_INVAL, "hidden/out must be device memory");
+        if ((topk_idx && !is_device(topk_idx)) || (topk_w && !is_device(topk_w)))
+            return set_err(ctx, MOE_E_INVAL, "topk_idx/topk_w must be device memory");
+    }
     MOE_CUDA(ctx, cudaSetDevice(ctx->cfg.device));
     return forward_impl(ctx, static_cast<const __nv_bfloat16*>(hidden), num_tokens,
                         static_cast<const __nv_bfloat16*>(router_w), experts,
@@ -489,12 +437,16 @@ moe_status moe_layer_forward_host(moe_ctx ctx, const void* hidden_host, int32_t 
                                   const void* router_w, const void* const* experts, int32_t top_k,
                                   void* out_host, int32_t* topk_idx, float* topk_w, void* stream) {
     moe_status s = validate_call(ctx, num_tokens, router_w, experts, top_k);
-    if (s != MOE_OK || num_tokens == 0) return s;
+    if (s != MOE_OK || (num_tokens == 0 && !ctx->ep)) return s;
+    moe_ctx c = ctx;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (num_tokens == 0)  // EP: this rank still serves the other ranks' tokens
+        return forward_impl(c, nullptr, 0, static_cast<const __nv_bfloat16*>(router_w), experts,
+                            nullptr, topk_idx, topk_w, st, false, 0);
     if (!hidden_host || !out_host) return set_err(ctx, MOE_E_INVAL, "NULL hidden / out");
     if (!is_pinned(ctx, hidden_host) || !is_pinned(ctx, out_host))
         return set_err(ctx, MOE_E_NOT_PINNED, "hidden_host/out_host must be page-locked");
     MOE_CUDA(ctx, cudaSetDevice(ctx->cfg.device));
-    moe_ctx c = ctx;
     const size_t bytes = (size_t)num_tokens * c->cfg.hidden * 2;
     if (!c->x_dev[0]) {
         const size_t cap = (size_t)c->cfg.max_tokens * c->cfg.hidden * 2;
@@ -505,7 +457,6 @@ moe_status moe_layer_forward_host(moe_ctx ctx, const void* hidden_host, int32_t 
             }
         }
     }
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int b = c->host_parity;
     c->host_parity ^= 1;
     // tokens ride the copy stream ahead of this call's expert weights
@@ -526,6 +477,14 @@ moe_status moe_sync(moe_ctx ctx) {
     if (!ctx) return MOE_E_INVAL;
     MOE_CUDA(ctx, cudaSetDevice(ctx->cfg.device));
     MOE_CUDA(ctx, cudaDeviceSynchronize());
+    if (ctx->comm && moe::nccl_api()) {
+        moe::ncclResult_t r = 0;
+        moe::nccl_api()->CommGetAsyncError(ctx->comm, &r);
+        if (r != 0) {
+            ctx->sticky = MOE_E_NCCL;
+            return set_err(ctx, MOE_E_NCCL, "NCCL async error: %s", moe::nccl_api()->GetErrorString(r));
+        }
+    }
     return ctx->sticky;
 }
 
@@ -533,10 +492,10 @@ moe_status moe_get_stats(moe_ctx ctx, moe_stats* out) {
     if (!ctx || !out) return MOE_E_INVAL;
     moe_status s = moe_sync(ctx);
     if (s != MOE_OK) return s;
-    double* bucket[kRecKinds] = {&ctx->stats.h2d_ms,   &ctx->stats.route_ms,   &ctx->stats.permute_ms,
-                                 &ctx->stats.gemm1_ms, &ctx->stats.gemm2_ms,   &ctx->stats.combine_ms,
-                                 &ctx->stats.comm_ms};
-    for (const Rec& r : ctx->pending) {
+    double* bucket[moe::kRecKinds] = {&ctx->stats.h2d_ms,   &ctx->stats.route_ms,   &ctx->stats.permute_ms,
+                                      &ctx->stats.gemm1_ms, &ctx->stats.gemm2_ms,   &ctx->stats.combine_ms,
+                                      &ctx->stats.comm_ms};
+    for (const moe::Rec& r : ctx->pending) {
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) *bucket[r.kind] += ms;
         else cudaGetLastError();
@@ -561,10 +520,10 @@ moe_status moe_debug_buffers(moe_ctx ctx, moe_debug_view* out) {
     out->counts = ctx->counts;
     out->offsets = ctx->offsets;
     out->pos = ctx->pos;
-    out->x_perm = ctx->x_perm;
+    out->x_perm = ctx->ep ? ctx->x_recv : ctx->x_perm;
     out->h_act = ctx->h_act;
     out->y_perm = ctx->y_perm;
-    out->rows = ctx->last_rows;
+    out->rows = ctx->ep ? ctx->last_recv_rows : ctx->last_rows;
     return MOE_OK;
 }
 
@@ -572,7 +531,8 @@ moe_status moe_destroy(moe_ctx c) {
     if (!c) return MOE_OK;
     cudaSetDevice(c->cfg.device);
     cudaDeviceSynchronize();
-    for (const Rec& r : c->pending) {
+    moe::ep_destroy(c);
+    for (const moe::Rec& r : c->pending) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
     }

@@ -316,6 +316,7 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
                                int ne, int k, int renorm, int32_t* idx, float* gates,
                                int32_t* tile_counts, cudaStream_t st) {
     const int n_tiles = (T + kRouteTile - 1) / kRouteTile;
+    if (n_tiles == 0) return cudaSuccess;
     const size_t dyn = sizeof(double) * (size_t)ne * kChunk;  // == 32 * ne doubles (logits too)
     const int ept = (ne + 7) / 8;
 #define MOE_ROUTER(E)                                                                        \
@@ -343,6 +344,7 @@ cudaError_t launch_permute(const __nv_bfloat16* x, int T, int h, int k, int ne,
                            const int32_t* offsets, __nv_bfloat16* x_perm, int32_t* pos,
                            cudaStream_t st) {
     const int n_tiles = (T + kRouteTile - 1) / kRouteTile;
+    if (n_tiles == 0) return cudaSuccess;
     permute_kernel<<<n_tiles * (kRouteTile / kPermuteTokens), 256, 0, st>>>(
         x, T, h, k, ne, idx, tile_prefix, offsets, x_perm, pos);
     return cudaGetLastError();
@@ -351,6 +353,7 @@ cudaError_t launch_permute(const __nv_bfloat16* x, int T, int h, int k, int ne,
 cudaError_t launch_combine(const __nv_bfloat16* y_perm, const int32_t* pos, const float* gates,
                            int T, int h, int k, int num_shared, int64_t shared_base,
                            __nv_bfloat16* out, cudaStream_t st) {
+    if (T == 0) return cudaSuccess;
     combine_kernel<<<(T + 7) / 8, 256, 0, st>>>(y_perm, pos, gates, T, h, k, num_shared,
                                                 shared_base, out);
     return cudaGetLastError();

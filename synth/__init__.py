@@ -171,8 +171,10 @@ def gen_hidden(cfg: MoEConfig, router_bits: np.ndarray, layer: int = 0, tokens: 
 
 
 def gen_inputs(cfg: MoEConfig, layer: int = 0, threads: int = 8, tokens: Optional[int] = None,
-               experts: bool = True) -> MoEInputs:
-    """All inputs of one layer call: x, router and (optionally) every expert's canonical weights."""
+               experts: bool = True, expert_ids: Optional[List[int]] = None) -> MoEInputs:
+    """All inputs of one layer call: x, router and (optionally) the experts' canonical weights.
+    expert_ids selects a subset (indices over routed experts then shared ones, e.g. one rank's
+    experts under expert parallelism); the weights of expert i never depend on the subset."""
     ch = _seed_children(cfg, layer)
     router = gen_router(cfg, layer)
     x, topic = gen_hidden(cfg, router, layer, tokens)
@@ -181,7 +183,8 @@ def gen_inputs(cfg: MoEConfig, layer: int = 0, threads: int = 8, tokens: Optiona
     w2: List[np.ndarray] = []
     if experts:
         n_all = cfg.num_experts + cfg.num_shared
-        kids = ch[2:2 + n_all]
+        ids = list(range(n_all)) if expert_ids is None else list(expert_ids)
+        kids = [ch[2 + i] for i in ids]
         with ThreadPoolExecutor(max(1, threads)) as ex:
             mats = list(ex.map(lambda c: gen_expert(cfg, c), kids))
         for a, b, c in mats:
