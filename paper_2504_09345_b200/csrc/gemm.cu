@@ -36,6 +36,19 @@ struct GemmCfg {
     static constexpr size_t kSmem = 1024 /*align slack*/ + kStages * (kABytes + kBBytes) + 256;
 };
 
+// Persistent tile order: groups of `gm` M tiles, M fastest inside a group, then N.  The ~148
+// concurrently running tiles then share gm A tiles and ~148/gm B tiles, which stay in L2 (an
+// M-fastest order over all M tiles thrashes L2 once m_tiles x A-tile bytes > 126 MB).
+__device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, int gm, int& m,
+                                            int& n) {
+    const int group = tile / (gm * n_tiles);
+    const int first = group * gm;
+    const int width = min(gm, m_tiles - first);
+    const int r = tile - group * gm * n_tiles;
+    m = first + r % width;
+    n = r / width;
+}
+
 __device__ __forceinline__ float silu_mul(float g, float u) {
     return g / (1.0f + __expf(-g)) * u;
 }
@@ -66,6 +79,7 @@ expert_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     const int total = m_tiles * n_tiles;
     if ((int)blockIdx.x >= total) return;
     const int num_kb = K / BK;
+    const int group_m = (K <= 8192) ? 16 : 8;  // A tile = 128 x K bf16 (1 MB at K=4096)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -98,7 +112,8 @@ expert_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-                const int m = tile % m_tiles, n = tile / m_tiles;
+                int m, n;
+                tile_coords(tile, m_tiles, n_tiles, group_m, m, n);
                 const int arow = g.a_begin + m * BM, brow = n * BN;
                 for (int kb = 0; kb < num_kb; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1u);
@@ -154,7 +169,8 @@ expert_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
             const int acc = it & 1;
             const uint32_t aphase = (it >> 1) & 1;
-            const int m = tile % m_tiles, n = tile / m_tiles;
+            int m, n;
+            tile_coords(tile, m_tiles, n_tiles, group_m, m, n);
             ptx::mbar_wait(&tfull[acc], aphase);
             ptx::tc_fence_after();
             const int r = q * 32 + lane;

@@ -19,7 +19,8 @@ namespace moe {
 namespace {
 
 constexpr int kRouterThreads = 256;
-constexpr int kChunk = 32;  // channels staged per iteration
+constexpr int kChunk = 64;  // channels staged per iteration (one 16-byte vector per thread of x)
+constexpr int kXsPitch = kRouteTile + 1;  // padded row (doubles): conflict-free transposed stores
 
 __device__ __forceinline__ bool ranks_above(double la, int a, double lb, int b) {
     const bool na = isnan(la), nb = isnan(lb);
@@ -29,15 +30,28 @@ __device__ __forceinline__ bool ranks_above(double la, int a, double lb, int b) 
     return a < b;
 }
 
+__device__ __forceinline__ void bf16x8_to_f64(const int4& v, double (&o)[8]) {
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(b[i]);  // exact
+        o[2 * i] = (double)f.x;
+        o[2 * i + 1] = (double)f.y;
+    }
+}
+
 // One block = kRouteTile (32) tokens.  Warp w computes experts {w, w+8, w+16, ...} for all 32
-// tokens (lane = token), EPT accumulators per thread.
+// tokens (lane = token), EPT accumulators per thread; each accumulator is ONE fp64 FMA chain in
+// ascending channel order (the definition's order, reading R6).  Staging: 64-channel chunks, one
+// 16-byte x vector per thread and up to 4 router vectors, prefetched into registers one chunk
+// ahead so global latency overlaps the FMA chains.
 template <int EPT>
 __global__ void __launch_bounds__(kRouterThreads)
 router_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
                    const __nv_bfloat16* __restrict__ wr, int ne, int k, int renorm,
                    int32_t* __restrict__ idx_out, float* __restrict__ gate_out,
                    int32_t* __restrict__ tile_counts) {
-    __shared__ double xs[kChunk][kRouteTile];  // x tile, transposed, fp64
+    __shared__ double xs[kChunk * kXsPitch];   // x tile, transposed [c][t], fp64
     __shared__ int cnt[kMaxExperts];
     extern __shared__ double dyn[];            // ws [ne][kChunk]  then logits [32][ne]
     double* ws = dyn;
@@ -50,20 +64,44 @@ router_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
 #pragma unroll
     for (int i = 0; i < EPT; ++i) acc[i] = 0.0;
 
+    // staging assignment: x vector (token xt, channels xc..xc+7); router vectors v = tid + 256 i
+    const int xt = tid >> 3, xc = (tid & 7) * 8;
+    const bool xvalid = t0 + xt < T;
+    const int nwv = ne * (kChunk / 8);
+    int4 xr = make_int4(0, 0, 0, 0);
+    int4 wv[kMaxExperts * (kChunk / 8) / kRouterThreads];
+    auto load = [&](int c0) {
+        if (xvalid) xr = ptx::ld_nc_v4(x + (size_t)(t0 + xt) * h + c0 + xc);
+#pragma unroll
+        for (int i = 0; i < kMaxExperts * (kChunk / 8) / kRouterThreads; ++i) {
+            const int v = tid + kRouterThreads * i;
+            if (v < nwv) wv[i] = ptx::ld_nc_v4(wr + (size_t)(v >> 3) * h + c0 + (v & 7) * 8);
+        }
+    };
+    auto store = [&]() {
+        double d[8];
+        bf16x8_to_f64(xr, d);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) xs[(xc + j) * kXsPitch + xt] = d[j];
+#pragma unroll
+        for (int i = 0; i < kMaxExperts * (kChunk / 8) / kRouterThreads; ++i) {
+            const int v = tid + kRouterThreads * i;
+            if (v < nwv) {
+                bf16x8_to_f64(wv[i], d);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) ws[(v >> 3) * kChunk + (v & 7) * 8 + j] = d[j];
+            }
+        }
+    };
+
+    load(0);
     for (int c0 = 0; c0 < h; c0 += kChunk) {
-        for (int i = tid; i < kRouteTile * kChunk; i += kRouterThreads) {
-            const int t = i / kChunk, c = i % kChunk;
-            const float v = (t0 + t < T) ? __bfloat162float(x[(size_t)(t0 + t) * h + c0 + c]) : 0.f;
-            xs[c][t] = (double)v;
-        }
-        for (int i = tid; i < ne * kChunk; i += kRouterThreads) {
-            const int e = i / kChunk, c = i % kChunk;
-            ws[e * kChunk + c] = (double)__bfloat162float(wr[(size_t)e * h + c0 + c]);
-        }
+        store();
         __syncthreads();
-#pragma unroll 4
+        if (c0 + kChunk < h) load(c0 + kChunk);   // next chunk in flight during the FMAs
+#pragma unroll 8
         for (int c = 0; c < kChunk; ++c) {
-            const double xv = xs[c][lane];
+            const double xv = xs[c * kXsPitch + lane];
 #pragma unroll
             for (int i = 0; i < EPT; ++i) {
                 const int e = warp + 8 * i;
@@ -317,11 +355,22 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
                                int32_t* tile_counts, cudaStream_t st) {
     const int n_tiles = (T + kRouteTile - 1) / kRouteTile;
     if (n_tiles == 0) return cudaSuccess;
-    const size_t dyn = sizeof(double) * (size_t)ne * kChunk;  // == 32 * ne doubles (logits too)
+    const size_t dyn = sizeof(double) * (size_t)ne * kChunk;  // >= 32 * ne doubles (logits too)
     const int ept = (ne + 7) / 8;
 #define MOE_ROUTER(E)                                                                        \
-    router_topk_kernel<E><<<n_tiles, kRouterThreads, dyn, st>>>(x, T, h, wr, ne, k, renorm, \
-                                                                 idx, gates, tile_counts)
+    do {                                                                                     \
+        static bool attr = false;                                                            \
+        if (!attr) {                                                                         \
+            cudaError_t e_ = cudaFuncSetAttribute(router_topk_kernel<E>,                     \
+                cudaFuncAttributeMaxDynamicSharedMemorySize,                                 \
+                (int)(sizeof(double) * kMaxExperts * kChunk));                               \
+            if (e_ != cudaSuccess) return e_;                                                \
+            attr = true;                                                                     \
+        }                                                                                    \
+        router_topk_kernel<E><<<n_tiles, kRouterThreads, dyn, st>>>(x, T, h, wr, ne, k,      \
+                                                                     renorm, idx, gates,     \
+                                                                     tile_counts);           \
+    } while (0)
     if (ept <= 1) MOE_ROUTER(1);
     else if (ept <= 2) MOE_ROUTER(2);
     else if (ept <= 4) MOE_ROUTER(4);
