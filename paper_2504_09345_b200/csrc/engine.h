@@ -61,6 +61,9 @@ struct moe_ctx_s {
     cudaEvent_t ready13[2] = {}, ready2[2] = {}, slot_free[2] = {};
     uint64_t seq = 0;  // streamed-item counter across calls: item q uses slot q % 2
     CUtensorMap tm_w13[2], tm_w2[2];
+    CUtensorMap tm_w13_pair[2], tm_w2_pair[2];  // 128-row boxes for the CTA-pair GEMM
+    int pair_mode = 0;        // MOE_GEMM_PAIR: 0 never (default), 1 always, -1 auto (rows per group)
+    int pair_min_rows = 2048; // auto: CTA-pair GEMM when the expected group has >= this many rows
 
     // workspace
     int32_t* idx_ws = nullptr;

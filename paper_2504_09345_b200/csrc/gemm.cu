@@ -49,8 +49,67 @@ __device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, 
     n = r / width;
 }
 
+// L2 policies of the operand loads (MOE_GEMM_L2HINT: 0 = evict_normal for both, 1 = A evict_last
+// + B evict_first).  Set once per process by set_gemm_l2_hints().
+__device__ int g_l2_hints = 0;
+
+__device__ __forceinline__ uint64_t l2_policy_a() {
+    return g_l2_hints ? ptx::policy_evict_last() : ptx::policy_evict_normal();
+}
+__device__ __forceinline__ uint64_t l2_policy_b() {
+    return g_l2_hints ? ptx::policy_evict_first() : ptx::policy_evict_normal();
+}
+
 __device__ __forceinline__ float silu_mul(float g, float u) {
     return g / (1.0f + __expf(-g)) * u;
+}
+
+// Epilogue of one accumulator row (this thread's TMEM lane): TMEM -> registers -> fp32 math ->
+// bf16 -> global.  SwiGLU tiles hold gate columns [0, BN/2) and the matching up columns
+// [BN/2, BN); they produce BN/2 outputs.  tcgen05.ld is warp-collective: every lane loads, only
+// rows inside the group store.
+template <int BN, int MODE>
+__device__ __forceinline__ void epilogue_row(uint32_t taddr, bool valid, __nv_bfloat16* row_out,
+                                             int n) {
+    if (MODE == kGemmSwiGLU) {
+        __nv_bfloat16* dst = row_out + (int64_t)n * (BN / 2);
+#pragma unroll 1
+        for (int c = 0; c < BN / 2; c += 32) {
+            uint32_t gv[32], uv[32];
+            ptx::tmem_ld_32x32b_x32(taddr + c, gv);
+            ptx::tmem_ld_32x32b_x32(taddr + BN / 2 + c, uv);
+            ptx::tmem_ld_wait();
+            if (valid) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const float h0 = silu_mul(__uint_as_float(gv[2 * i]), __uint_as_float(uv[2 * i]));
+                    const float h1 = silu_mul(__uint_as_float(gv[2 * i + 1]), __uint_as_float(uv[2 * i + 1]));
+                    pk[i] = ptx::pack_bf16x2(h0, h1);
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    ptx::st_global_v4(dst + c + 8 * i, pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+            }
+        }
+    } else {
+        __nv_bfloat16* dst = row_out + (int64_t)n * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+            uint32_t v[32];
+            ptx::tmem_ld_32x32b_x32(taddr + c, v);
+            ptx::tmem_ld_wait();
+            if (valid) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    pk[i] = ptx::pack_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    ptx::st_global_v4(dst + c + 8 * i, pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+            }
+        }
+    }
 }
 
 template <int BN, int MODE>
@@ -107,8 +166,8 @@ expert_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     if (warp == 0) {
         if (lane == 0) {
             // ------------------------------------------------------------ TMA producer
-            const uint64_t pol_a = ptx::policy_evict_last();   // A tile re-read by every N tile
-            const uint64_t pol_b = ptx::policy_evict_first();  // weights: read by m_tiles CTAs
+            const uint64_t pol_a = l2_policy_a();  // A tile re-read by every N tile of the group
+            const uint64_t pol_b = l2_policy_b();  // weight tile: read by the group's M tiles
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
@@ -178,45 +237,7 @@ expert_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
             const bool valid = arow < g.a_end;
             const int64_t orow = (int64_t)g.out_base + (arow - g.a_begin);
             const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-            if (MODE == kGemmSwiGLU) {
-                __nv_bfloat16* dst = out + orow * ldo + (int64_t)n * (BN / 2);
-#pragma unroll 1
-                for (int c = 0; c < BN / 2; c += 32) {
-                    uint32_t gv[32], uv[32];
-                    ptx::tmem_ld_32x32b_x32(taddr + c, gv);
-                    ptx::tmem_ld_32x32b_x32(taddr + BN / 2 + c, uv);
-                    ptx::tmem_ld_wait();
-                    if (valid) {
-                        uint32_t pk[16];
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            const float h0 = silu_mul(__uint_as_float(gv[2 * i]), __uint_as_float(uv[2 * i]));
-                            const float h1 = silu_mul(__uint_as_float(gv[2 * i + 1]), __uint_as_float(uv[2 * i + 1]));
-                            pk[i] = ptx::pack_bf16x2(h0, h1);
-                        }
-#pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            ptx::st_global_v4(dst + c + 8 * i, pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-                    }
-                }
-            } else {
-                __nv_bfloat16* dst = out + orow * ldo + (int64_t)n * BN;
-#pragma unroll 1
-                for (int c = 0; c < BN; c += 32) {
-                    uint32_t v[32];
-                    ptx::tmem_ld_32x32b_x32(taddr + c, v);
-                    ptx::tmem_ld_wait();
-                    if (valid) {
-                        uint32_t pk[16];
-#pragma unroll
-                        for (int i = 0; i < 16; ++i)
-                            pk[i] = ptx::pack_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
-#pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            ptx::st_global_v4(dst + c + 8 * i, pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-                    }
-                }
-            }
+            epilogue_row<BN, MODE>(taddr, valid, out + orow * ldo, n);
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
@@ -227,6 +248,177 @@ expert_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         ptx::tc_fence_after();
         ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
     }
+}
+
+// ------------------------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of 2 CTAs on one TPC computes 256 x 256 tiles.
+// Each CTA stages its own 128 rows of A and half (128 rows) of the B tile per K step (32 KB, 6
+// stages), the leader issues tcgen05.mma.cta_group::2 (M=256) reading both CTAs' smem, and each
+// CTA's TMEM holds its 128 rows of the fp32 accumulator.  Per SM this halves the B bytes moved
+// per MMA and doubles the bytes in flight (6 x 32 KB vs 4 x 48 KB), for large expert groups.
+// Barrier protocol: full[s] (leader; arrivals: leader expect_tx + peer remote arrive; TMA bytes
+// of both CTAs), empty[s] (both; MMA commit multicast), tfull[a] (both; multicast), tempty[a]
+// (leader; 4 epilogue warps x 2 CTAs).
+constexpr int kPairStages = 6;
+constexpr uint32_t kPairABytes = 128 * BK * 2;   // per CTA
+constexpr uint32_t kPairBBytes = 128 * BK * 2;   // per CTA (half of a 256-row B tile)
+constexpr size_t kPairSmem = 1024 + kPairStages * (kPairABytes + kPairBBytes) + 256;
+
+template <int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+expert_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
+                        const __grid_constant__ CUtensorMap tmB,
+                        const GemmGroup* __restrict__ group, int N, int K,
+                        __nv_bfloat16* __restrict__ out, int ldo) {
+    constexpr int BN = 256, PM = 256, S = kPairStages;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + S * kPairABytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * kPairBBytes);
+    uint64_t* empty = full + S;
+    uint64_t* tfull = empty + S;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const uint32_t rank = ptx::cluster_ctarank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const GemmGroup g = *group;
+    const int rows = g.a_end - g.a_begin;
+    if (rows <= 0) return;                       // uniform over the cluster
+    const int m_tiles = (rows + PM - 1) / PM;
+    const int n_tiles = N / BN;
+    const int total = m_tiles * n_tiles;
+    if (pair >= total) return;                   // both CTAs of a pair leave together
+    const int num_kb = K / BK;
+    const int group_m = (K <= 8192) ? 8 : 4;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+        for (int s = 0; s < S; ++s) {
+            ptx::mbar_init(&full[s], 2);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], 8);
+        }
+        ptx::fence_barrier_init();
+        ptx::fence_proxy_async();
+    }
+    if (warp == 2) ptx::tmem_alloc_cta2<2 * BN>(tmem_slot);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------------------------------------------- TMA producer (both CTAs)
+            const uint64_t pol_a = l2_policy_a();
+            const uint64_t pol_b = l2_policy_b();
+            const uint32_t full0 = ptx::mapa_shared(&full[0], 0);  // leader's full[0]
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = pair; tile < total; tile += npairs) {
+                int m, n;
+                tile_coords(tile, m_tiles, n_tiles, group_m, m, n);
+                const int arow = g.a_begin + m * PM + (int)rank * 128;
+                const int brow = n * BN + (int)rank * 128;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1u);
+                    const uint32_t fbar = full0 + stage * 8;
+                    if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (kPairABytes + kPairBBytes));
+                    else ptx::mbar_arrive_cluster(fbar);
+                    ptx::tma_load_2d_cta2(sA + stage * kPairABytes, &tmA, fbar, kb * BK, arow, pol_a);
+                    ptx::tma_load_2d_cta2(sB + stage * kPairBBytes, &tmB, fbar, kb * BK, brow, pol_b);
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {
+            // ---------------------------------------------------- MMA issuer (leader only)
+            constexpr uint32_t idesc = ptx::umma_idesc_bf16(PM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int tile = pair; tile < total; tile += npairs, ++it) {
+                const int acc = it & 1;
+                const uint32_t aphase = (it >> 1) & 1;
+                ptx::mbar_wait(&tempty[acc], aphase ^ 1u);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem_base + acc * BN;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a0 = ptx::smem_u32(sA + stage * kPairABytes);
+                    const uint32_t b0 = ptx::smem_u32(sB + stage * kPairBBytes);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk)
+                        ptx::umma_bf16_cta2(d, ptx::umma_desc_sw128_kmajor(a0 + kk * 32),
+                                            ptx::umma_desc_sw128_kmajor(b0 + kk * 32), idesc,
+                                            (kb | kk) != 0 ? 1u : 0u);
+                    ptx::umma_commit_cta2_mc(&empty[stage], 0x3);
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+                ptx::umma_commit_cta2_mc(&tfull[acc], 0x3);
+            }
+        }
+    } else if (warp >= 4) {
+        // -------------------------------------------------------- epilogue (both CTAs)
+        const int q = warp - 4;
+        const uint32_t tempty0 = ptx::mapa_shared(&tempty[0], 0);
+        int it = 0;
+        for (int tile = pair; tile < total; tile += npairs, ++it) {
+            const int acc = it & 1;
+            const uint32_t aphase = (it >> 1) & 1;
+            int m, n;
+            tile_coords(tile, m_tiles, n_tiles, group_m, m, n);
+            ptx::mbar_wait(&tfull[acc], aphase);
+            ptx::tc_fence_after();
+            const int arow = g.a_begin + m * PM + (int)rank * 128 + q * 32 + lane;
+            const bool valid = arow < g.a_end;
+            const int64_t orow = (int64_t)g.out_base + (arow - g.a_begin);
+            const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+            epilogue_row<BN, MODE>(taddr, valid, out + orow * ldo, n);
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster(tempty0 + acc * 8);
+        }
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc_cta2<2 * BN>(tmem_base);
+    }
+}
+
+template <int MODE>
+cudaError_t launch_pair(const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmGroup* group,
+                        int N, int K, __nv_bfloat16* out, int ldo, int grid, cudaStream_t st) {
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(expert_gemm_pair_kernel<MODE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kPairSmem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    expert_gemm_pair_kernel<MODE><<<grid & ~1, kThreads, kPairSmem, st>>>(*tmA, *tmB, group, N, K,
+                                                                          out, ldo);
+    return cudaGetLastError();
 }
 
 template <int BN, int MODE>
@@ -254,9 +446,14 @@ int gemm_bn_for(int mode, int N) {
     return 0;
 }
 
-cudaError_t launch_expert_gemm(int mode, int bn, const CUtensorMap* tmA, const CUtensorMap* tmB,
-                               const GemmGroup* group, int N, int K, __nv_bfloat16* out,
-                               int ldo, int grid, cudaStream_t st) {
+cudaError_t launch_expert_gemm(int mode, int bn, bool pair, const CUtensorMap* tmA,
+                               const CUtensorMap* tmB, const GemmGroup* group, int N, int K,
+                               __nv_bfloat16* out, int ldo, int grid, cudaStream_t st) {
+    if (pair) {
+        if (bn != 256) return cudaErrorInvalidValue;
+        if (mode == kGemmSwiGLU) return launch_pair<kGemmSwiGLU>(tmA, tmB, group, N, K, out, ldo, grid, st);
+        return launch_pair<kGemmPlain>(tmA, tmB, group, N, K, out, ldo, grid, st);
+    }
     if (mode == kGemmSwiGLU) {
         if (bn == 256) return launch_one<256, kGemmSwiGLU>(tmA, tmB, group, N, K, out, ldo, grid, st);
     } else {
@@ -266,4 +463,10 @@ cudaError_t launch_expert_gemm(int mode, int bn, const CUtensorMap* tmA, const C
     return cudaErrorInvalidValue;
 }
 
+}  // namespace moe
+
+namespace moe {
+cudaError_t set_gemm_l2_hints(int mode) {
+    return cudaMemcpyToSymbol(g_l2_hints, &mode, sizeof(int));
+}
 }  // namespace moe

@@ -222,6 +222,15 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     }
 
     const int grid = c->num_sms;
+    // Tile shape: the CTA-pair kernel (256-row tiles) for large groups, else 128-row tiles.
+    // The host does not know the group sizes (they live on the device), so it decides on the
+    // expected size: T*k*W/N_e rows per routed expert, T rows per shared expert.
+    const int64_t exp_routed = (int64_t)T * k * cf.world_size / ne;
+    auto use_pair = [&](bool shared, int bn) {
+        if (bn != 256 || c->pair_mode == 0) return false;
+        if (c->pair_mode == 1) return true;
+        return (shared ? (int64_t)T : exp_routed) >= c->pair_min_rows;
+    };
     for (int i = 0; i < c->n_all; ++i) {
         const uint64_t q = q0 + i;
         const int s = (int)(q & 1);
@@ -229,17 +238,20 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready13[s], 0));
         {
             Prof p(c, moe::kRecGemm1, st);
-            MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmSwiGLU, c->bn1,
-                                                shared ? &tm_x : tmA_routed, &c->tm_w13[s],
-                                                g1 + i, 2 * hi, h, c->h_act, hi, grid, st));
+            const bool pr = use_pair(shared, c->bn1);
+            MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmSwiGLU, c->bn1, pr,
+                                                shared ? &tm_x : tmA_routed,
+                                                pr ? &c->tm_w13_pair[s] : &c->tm_w13[s], g1 + i,
+                                                2 * hi, h, c->h_act, hi, grid, st));
             p.end();
         }
         MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready2[s], 0));
         {
             Prof p(c, moe::kRecGemm2, st);
-            MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmPlain, c->bn2, &c->tm_h, &c->tm_w2[s],
-                                                g2 + i, h, hi, shared ? c->y_perm : y_routed, h,
-                                                grid, st));
+            const bool pr = use_pair(shared, c->bn2);
+            MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmPlain, c->bn2, pr, &c->tm_h,
+                                                pr ? &c->tm_w2_pair[s] : &c->tm_w2[s], g2 + i, h,
+                                                hi, shared ? c->y_perm : y_routed, h, grid, st));
             p.end();
         }
         c->stats.kernel_launches += 2;
@@ -399,8 +411,22 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
         tm &= moe::make_tmap(&c->tm_w13[i], c->slot[i], 2ull * hi, h, (uint32_t)c->bn1);
         tm &= moe::make_tmap(&c->tm_w2[i], static_cast<char*>(c->slot[i]) + c->w13_bytes,
                              (uint64_t)h, hi, (uint32_t)c->bn2);
+        tm &= moe::make_tmap(&c->tm_w13_pair[i], c->slot[i], 2ull * hi, h, 128);
+        tm &= moe::make_tmap(&c->tm_w2_pair[i], static_cast<char*>(c->slot[i]) + c->w13_bytes,
+                             (uint64_t)h, hi, 128);
     }
     if (!tm) return fail(MOE_E_CUDA);
+    if (const char* e = getenv("MOE_GEMM_PAIR")) {
+        if (!strcmp(e, "0")) c->pair_mode = 0;
+        else if (!strcmp(e, "1")) c->pair_mode = 1;
+        else if (!strcmp(e, "auto")) c->pair_mode = -1;
+    }
+    if (const char* e = getenv("MOE_GEMM_PAIR_MIN_ROWS")) c->pair_min_rows = atoi(e);
+    {
+        int hints = 0;   // measured: evict_normal beats evict_last/evict_first (profiles/r01)
+        if (const char* e = getenv("MOE_GEMM_L2HINT")) hints = atoi(e);
+        if (moe::set_gemm_l2_hints(hints) != cudaSuccess) return fail(MOE_E_CUDA);
+    }
     if (c->ep) {
         moe_status es = moe::ep_init(c);
         if (es != MOE_OK) return fail(es);

@@ -43,11 +43,15 @@ cudaError_t launch_combine(const __nv_bfloat16* y_perm, const int32_t* pos, cons
 // ---------------------------------------------------------------------------- expert GEMM
 enum GemmMode { kGemmSwiGLU = 0, kGemmPlain = 1 };
 // One expert group of a5 (SwiGLU, N = 2*h_i interleaved) or a6 (plain, N = h) on tcgen05.
-//   tmA: A [rows, K] bf16 (box 64 x 128); tmB: B [N, K] bf16 (box 64 x bn); group: device ptr.
+//   tmA: A [rows, K] bf16 (box 64 x 128); tmB: B [N, K] bf16 (box 64 x bn, or 64 x 128 when
+//   `pair`: the CTA-pair kernel, 256 x 256 tiles, bn must be 256); group: device ptr.
 //   out: bf16 [*, ldo]; SwiGLU writes N/2 columns.
-cudaError_t launch_expert_gemm(int mode, int bn, const CUtensorMap* tmA, const CUtensorMap* tmB,
-                               const GemmGroup* group, int N, int K, __nv_bfloat16* out,
-                               int ldo, int grid, cudaStream_t st);
+cudaError_t launch_expert_gemm(int mode, int bn, bool pair, const CUtensorMap* tmA,
+                               const CUtensorMap* tmB, const GemmGroup* group, int N, int K,
+                               __nv_bfloat16* out, int ldo, int grid, cudaStream_t st);
 int gemm_bn_for(int mode, int N);   // tile width used for a given mode / N (0 = unsupported)
+// L2 policy of the GEMM operand loads for the current device: 0 evict_normal, 1 A evict_last +
+// B evict_first.
+cudaError_t set_gemm_l2_hints(int mode);
 
 }  // namespace moe
