@@ -294,11 +294,16 @@ def run_ours(args):
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(cfg.name, {}).get("gemm1_dram_bytes_per_launch")
+    # Peak: the BURST cuBLAS figure.  The kernel runs inside a long step, but the step is
+    # host-link bound and the GPU idles between expert GEMMs, so it runs at full boost clock
+    # (see `clocks`), not at the power-capped clock of the sustained figure; the burst peak is
+    # the conservative denominator here.  The sustained-peak fraction is reported beside it.
     roofline = {"kernel": "expert_gemm_kernel<256,SwiGLU> (a5, tcgen05)", "bound": "tensor",
-                "achieved": achieved_tf, "peak": peaks["bf16_tflops_sustained"],
-                "unit": "TFLOP/s", "frac": achieved_tf / peaks["bf16_tflops_sustained"],
+                "achieved": achieved_tf, "peak": peaks["bf16_tflops"],
+                "unit": "TFLOP/s", "frac": achieved_tf / peaks["bf16_tflops"],
+                "frac_of_sustained_peak": achieved_tf / peaks["bf16_tflops_sustained"],
                 "traffic": traffic if world == 1 else None,
-                "peak_source": peaks["source"] + " bf16_tflops_sustained",
+                "peak_source": peaks["source"] + " bf16_tflops (burst)",
                 "flops_per_launch": g1_flops_launch, "avg_launch_ms": g1_launch_ms}
     h2d_gbs = st["h2d_weight_bytes"] / (st["h2d_ms"] * 1e-3) / 1e9 if st["h2d_ms"] > 0 else 0.0
     roofline_step = {"bound": "host_link" if t_io >= t_tc else "tensor",
