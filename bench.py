@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--layers", type=int, default=2)
     ap.add_argument("--packet-mb", type=float, default=0.0)
+    ap.add_argument("--slots", type=int, default=0, help="expert staging slots (0 = auto)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -235,7 +236,7 @@ def run_ours(args):
     layer = moe.MoELayer(cfg.hidden, cfg.ffn, cfg.num_experts, cfg.top_k, Tr,
                          num_shared=cfg.num_shared, device=local, profile=True,
                          packet_bytes=int(args.packet_mb * 2 ** 20), world_size=world, rank=rank,
-                         nccl_unique_id=uid)
+                         nccl_unique_id=uid, num_slots=args.slots)
     stream = torch.cuda.Stream()
     sh = stream.cuda_stream
 
@@ -355,7 +356,8 @@ def run_ours(args):
             "config": {"workload": cfg.name, "tokens": T, "tokens_per_rank": Tr,
                        "hidden": cfg.hidden, "ffn": cfg.ffn, "experts": cfg.num_experts,
                        "experts_per_rank": nl, "top_k": cfg.top_k, "num_shared": cfg.num_shared,
-                       "layers_cycled": args.layers, "staging_slots": 2, "packet_mb": args.packet_mb,
+                       "layers_cycled": args.layers, "staging_slots": st["num_slots"],
+                       "packet_mb": args.packet_mb,
                        "l2": "inputs larger than L2: all expert weights re-streamed from host each step",
                        "parallelism": f"ep{world}"},
             "roofline": roofline, "roofline_step": roofline_step,

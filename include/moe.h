@@ -74,8 +74,13 @@ typedef struct {
     int32_t world_size;       /* expert-parallel group size; 1 = single GPU                    */
     int32_t rank;             /* this process's rank in the group                              */
     const void* nccl_unique_id; /* 128-byte ncclUniqueId (world_size > 1), else NULL           */
-    int64_t packet_bytes;     /* 0 = one copy per weight matrix; else H2D packets of this size */
+    int64_t packet_bytes;     /* 0 = one DMA per expert; else H2D packets of this size          */
     uint32_t flags;           /* MOE_FLAG_*                                                    */
+    int32_t num_slots;        /* expert staging slots, 2..16 (must be < streamed experts per
+                                 call when > 2); 0 = auto: enough slots to hold ~256 MiB of
+                                 weights (2 for Mixtral-size experts, up to 8 for fine-grained
+                                 ones).  The paper's buffer is two LAYERS;
+                                 slots are recycled every call, so weights are always re-streamed. */
 } moe_config;
 
 /* Packed host blob of one expert (produced by moe_pack_expert, consumed by the copy engine):
@@ -143,6 +148,8 @@ typedef struct {
     int64_t gemm1_launches, gemm2_launches;
     double h2d_ms;                /* sum of weight-copy durations (copy stream)               */
     double route_ms, permute_ms, gemm1_ms, gemm2_ms, combine_ms, comm_ms;
+    int64_t num_slots;            /* expert staging slots in use                              */
+    int64_t comm_bytes;           /* bytes this rank sent in EP dispatch + combine            */
 } moe_stats;
 
 moe_status moe_get_stats(moe_ctx ctx, moe_stats* out);   /* synchronises the context */

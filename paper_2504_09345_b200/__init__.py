@@ -42,7 +42,7 @@ class moe_config(ctypes.Structure):
                 ("renormalize", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("world_size", ctypes.c_int32), ("rank", ctypes.c_int32),
                 ("nccl_unique_id", ctypes.c_void_p), ("packet_bytes", ctypes.c_int64),
-                ("flags", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("num_slots", ctypes.c_int32)]
 
 
 class moe_stats(ctypes.Structure):
@@ -52,7 +52,8 @@ class moe_stats(ctypes.Structure):
                 ("gemm2_launches", ctypes.c_int64), ("h2d_ms", ctypes.c_double),
                 ("route_ms", ctypes.c_double), ("permute_ms", ctypes.c_double),
                 ("gemm1_ms", ctypes.c_double), ("gemm2_ms", ctypes.c_double),
-                ("combine_ms", ctypes.c_double), ("comm_ms", ctypes.c_double)]
+                ("combine_ms", ctypes.c_double), ("comm_ms", ctypes.c_double),
+                ("num_slots", ctypes.c_int64), ("comm_bytes", ctypes.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -261,11 +262,11 @@ class MoELayer:
                  num_shared: int = 0, renormalize: bool = True, device: int = 0,
                  world_size: int = 1, rank: int = 0, packet_bytes: int = 0,
                  profile: bool = False, nccl_unique_id: Optional[bytes] = None,
-                 force_ep: bool = False):
+                 force_ep: bool = False, num_slots: int = 0):
         flags = (MOE_FLAG_PROFILE if profile else 0) | (MOE_FLAG_FORCE_EP if force_ep else 0)
         self.cfg = moe_config(hidden, ffn, num_experts, top_k, num_shared, max_tokens,
                               int(renormalize), device, world_size, rank, None, packet_bytes,
-                              flags)
+                              flags, num_slots)
         self._uid = None
         if nccl_unique_id is not None:
             self._uid = ctypes.create_string_buffer(bytes(nccl_unique_id), len(nccl_unique_id))

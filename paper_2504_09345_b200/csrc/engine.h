@@ -56,12 +56,14 @@ struct moe_ctx_s {
     int64_t rows_cap = 0;  // rows of h_act / y_perm (single GPU)
     cudaStream_t copy_stream = nullptr;
 
-    // staging slots (a GPU weight buffer of two units)
-    void* slot[2] = {nullptr, nullptr};
-    cudaEvent_t ready13[2] = {}, ready2[2] = {}, slot_free[2] = {};
-    uint64_t seq = 0;  // streamed-item counter across calls: item q uses slot q % 2
-    CUtensorMap tm_w13[2], tm_w2[2];
-    CUtensorMap tm_w13_pair[2], tm_w2_pair[2];  // 128-row boxes for the CTA-pair GEMM
+    // staging slots (a bounded GPU weight buffer, recycled every call)
+    int nslots = 2;
+    void* slot[moe::kMaxSlots] = {};
+    cudaEvent_t ready13[moe::kMaxSlots] = {}, ready2[moe::kMaxSlots] = {};
+    cudaEvent_t slot_free[moe::kMaxSlots] = {};
+    uint64_t seq = 0;  // streamed-item counter across calls: item q uses slot q % nslots
+    CUtensorMap tm_w13[moe::kMaxSlots], tm_w2[moe::kMaxSlots];
+    CUtensorMap tm_w13_pair[moe::kMaxSlots], tm_w2_pair[moe::kMaxSlots];  // 128-row boxes (pair GEMM)
     int pair_mode = 0;        // MOE_GEMM_PAIR: 0 never (default), 1 always, -1 auto (rows per group)
     int pair_min_rows = 2048; // auto: CTA-pair GEMM when the expected group has >= this many rows
 

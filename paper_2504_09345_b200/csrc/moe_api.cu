@@ -101,6 +101,10 @@ moe_status check_cfg(const moe_config* cfg) {
         return MOE_E_UNSUPPORTED;
     if (cfg->num_experts % cfg->world_size) return MOE_E_UNSUPPORTED;
     if (cfg->world_size > 1 && !cfg->nccl_unique_id) return MOE_E_INVAL;
+    if (cfg->num_slots < 0 || cfg->num_slots == 1 || cfg->num_slots > moe::kMaxSlots)
+        return MOE_E_INVAL;
+    if (cfg->num_slots > 2 && cfg->num_slots >= cfg->num_experts / cfg->world_size + cfg->num_shared)
+        return MOE_E_INVAL;  // more slots than streamed experts would let weights stay resident
     const int64_t rows = (int64_t)cfg->max_tokens * cfg->world_size * cfg->top_k +
                          (int64_t)cfg->max_tokens * cfg->num_shared;
     if (rows >= (1ll << 31)) return MOE_E_UNSUPPORTED;
@@ -136,9 +140,9 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
     return x < y + nb && y < x + na;
 }
 
-// Copy of streamed item q (index i of this call) into its slot; W13 part, then W2 part.
+// Copy of streamed item q (index i of this call) into slot q % nslots.
 moe_status enqueue_copy(moe_ctx c, const void* const* experts, int i, uint64_t q) {
-    const int s = (int)(q & 1);
+    const int s = (int)(q % (uint64_t)c->nslots);
     MOE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->slot_free[s], 0));
     const char* src = static_cast<const char*>(experts[i]);
     char* dst = static_cast<char*>(c->slot[s]);
@@ -153,12 +157,23 @@ moe_status enqueue_copy(moe_ctx c, const void* const* experts, int i, uint64_t q
         }
         return MOE_OK;
     };
-    moe_status st = copy_range(0, c->w13_bytes);
-    if (st != MOE_OK) return st;
-    MOE_CUDA(c, cudaEventRecord(c->ready13[s], c->copy_stream));
-    st = copy_range(c->w13_bytes, c->blob_bytes);
-    if (st != MOE_OK) return st;
-    MOE_CUDA(c, cudaEventRecord(c->ready2[s], c->copy_stream));
+    if (c->cfg.packet_bytes == 0) {
+        // One DMA per expert: every extra copy/event boundary on the copy stream costs a few
+        // microseconds of idle link (measured ~0.4% of the step with separate W13/W2 copies).
+        // GEMM1 then starts after the whole blob landed -- still long before the next expert's
+        // copy ends, so nothing is exposed.
+        moe_status st = copy_range(0, c->blob_bytes);
+        if (st != MOE_OK) return st;
+        MOE_CUDA(c, cudaEventRecord(c->ready13[s], c->copy_stream));
+        MOE_CUDA(c, cudaEventRecord(c->ready2[s], c->copy_stream));
+    } else {
+        moe_status st = copy_range(0, c->w13_bytes);
+        if (st != MOE_OK) return st;
+        MOE_CUDA(c, cudaEventRecord(c->ready13[s], c->copy_stream));
+        st = copy_range(c->w13_bytes, c->blob_bytes);
+        if (st != MOE_OK) return st;
+        MOE_CUDA(c, cudaEventRecord(c->ready2[s], c->copy_stream));
+    }
     p.end();
     c->stats.h2d_weight_bytes += c->blob_bytes;
     return MOE_OK;
@@ -181,8 +196,9 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     if (S > 0 && T > 0 && !moe::make_tmap(&tm_x, hidden, (uint64_t)T, (uint64_t)h, 128))
         return set_err(c, MOE_E_CUDA, "cuTensorMapEncodeTiled failed for hidden");
 
-    // first two weight copies go ahead of routing (cross-call prefetch)
-    for (int i = 0; i < std::min(2, c->n_all); ++i) {
+    // the first nslots weight copies go ahead of routing (cross-call prefetch)
+    const int ns = c->nslots;
+    for (int i = 0; i < std::min(ns, c->n_all); ++i) {
         moe_status s = enqueue_copy(c, experts, i, q0 + i);
         if (s != MOE_OK) return s;
     }
@@ -233,7 +249,7 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     };
     for (int i = 0; i < c->n_all; ++i) {
         const uint64_t q = q0 + i;
-        const int s = (int)(q & 1);
+        const int s = (int)(q % (uint64_t)ns);
         const bool shared = i >= c->n_local;
         MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready13[s], 0));
         {
@@ -258,8 +274,8 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         c->stats.gemm1_launches += 1;
         c->stats.gemm2_launches += 1;
         MOE_CUDA(c, cudaEventRecord(c->slot_free[s], st));
-        if (i + 2 < c->n_all) {
-            moe_status s2 = enqueue_copy(c, experts, i + 2, q + 2);
+        if (i + ns < c->n_all) {
+            moe_status s2 = enqueue_copy(c, experts, i + ns, q + ns);
             if (s2 != MOE_OK) return s2;
         }
     }
@@ -371,6 +387,12 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     c->bn1 = moe::gemm_bn_for(moe::kGemmSwiGLU, 2 * hi);
     c->bn2 = moe::gemm_bn_for(moe::kGemmPlain, h);
     if (!c->bn1 || !c->bn2) return fail(MOE_E_UNSUPPORTED);
+    if (cfg->num_slots > 0) {
+        c->nslots = cfg->num_slots;
+    } else {  // auto: ~256 MiB of staging, 2..8 slots, fewer than the experts streamed per call
+        const int64_t want = (moe::kAutoSlotBytes + c->blob_bytes - 1) / c->blob_bytes;
+        c->nslots = (int)std::max<int64_t>(2, std::min<int64_t>({want, 8, (int64_t)c->n_all - 1}));
+    }
     c->cap_recv = c->ep ? (int64_t)W * Tm * k : (int64_t)Tm * k;
     // h_act rows: routed rows (received rows under EP) then S * Tm shared rows
     const int64_t h_rows = c->cap_recv + (int64_t)S * Tm;
@@ -380,11 +402,13 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     auto dalloc = [&](void** p, size_t n) { return cudaMalloc(p, n) == cudaSuccess; };
     bool ok = true;
     ok &= cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) == cudaSuccess;
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < c->nslots; ++i) {
         ok &= dalloc(&c->slot[i], (size_t)c->blob_bytes);
         ok &= cudaEventCreateWithFlags(&c->ready13[i], cudaEventDisableTiming) == cudaSuccess;
         ok &= cudaEventCreateWithFlags(&c->ready2[i], cudaEventDisableTiming) == cudaSuccess;
         ok &= cudaEventCreateWithFlags(&c->slot_free[i], cudaEventDisableTiming) == cudaSuccess;
+    }
+    for (int i = 0; i < 2; ++i) {
         ok &= cudaEventCreateWithFlags(&c->xbuf_free[i], cudaEventDisableTiming) == cudaSuccess;
         ok &= cudaEventCreateWithFlags(&c->x_ready[i], cudaEventDisableTiming) == cudaSuccess;
     }
@@ -407,7 +431,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     bool tm = true;
     tm &= moe::make_tmap(&c->tm_xperm, c->x_perm, (uint64_t)Tm * k, h, 128);
     tm &= moe::make_tmap(&c->tm_h, c->h_act, (uint64_t)h_rows, hi, 128);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < c->nslots; ++i) {
         tm &= moe::make_tmap(&c->tm_w13[i], c->slot[i], 2ull * hi, h, (uint32_t)c->bn1);
         tm &= moe::make_tmap(&c->tm_w2[i], static_cast<char*>(c->slot[i]) + c->w13_bytes,
                              (uint64_t)h, hi, (uint32_t)c->bn2);
@@ -529,6 +553,8 @@ moe_status moe_get_stats(moe_ctx ctx, moe_stats* out) {
         ctx->ev_pool.push_back(r.b);
     }
     ctx->pending.clear();
+    ctx->stats.num_slots = ctx->nslots;
+    ctx->stats.comm_bytes = ctx->comm_bytes;
     *out = ctx->stats;
     return MOE_OK;
 }
@@ -563,11 +589,16 @@ moe_status moe_destroy(moe_ctx c) {
         cudaEventDestroy(r.b);
     }
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < moe::kMaxSlots; ++i) {
         cudaFree(c->slot[i]);
+        cudaEvent_t evs[] = {c->ready13[i], c->ready2[i], c->slot_free[i]};
+        for (cudaEvent_t e : evs)
+            if (e) cudaEventDestroy(e);
+    }
+    for (int i = 0; i < 2; ++i) {
         cudaFree(c->x_dev[i]);
         cudaFree(c->out_dev[i]);
-        cudaEvent_t evs[] = {c->ready13[i], c->ready2[i], c->slot_free[i], c->xbuf_free[i], c->x_ready[i]};
+        cudaEvent_t evs[] = {c->xbuf_free[i], c->x_ready[i]};
         for (cudaEvent_t e : evs)
             if (e) cudaEventDestroy(e);
     }

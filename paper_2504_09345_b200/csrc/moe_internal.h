@@ -11,6 +11,8 @@ constexpr int kRouteTile = 32;       // tokens per routing tile (router / permut
 constexpr int kMaxExperts = 128;     // envelope: N_e <= 128
 constexpr int kMaxTopK = 8;          // envelope: top_k <= 8
 constexpr int kMaxShared = 8;
+constexpr int kMaxSlots = 16;        // expert staging slots
+constexpr int64_t kAutoSlotBytes = 256ll << 20;  // auto slot count: ~256 MiB of staging
 
 // Row range of one expert group inside a GEMM's A operand, and where its output rows go.
 struct GemmGroup {

@@ -74,11 +74,15 @@ def test_pack_rejects_bad_shapes(lib):
     (dict(max_tokens=0), moe.MOE_E_INVAL),
     (dict(world_size=3), moe.MOE_E_UNSUPPORTED),      # 8 experts do not shard over 3 ranks
     (dict(rank=2, world_size=2), moe.MOE_E_INVAL),
+    (dict(num_slots=1), moe.MOE_E_INVAL),             # double buffering needs >= 2 slots
+    (dict(num_slots=17), moe.MOE_E_INVAL),            # > kMaxSlots
+    (dict(num_slots=8), moe.MOE_E_INVAL),             # >= experts streamed per call (8)
+    (dict(world_size=2, rank=0), moe.MOE_E_INVAL),    # EP needs an ncclUniqueId
 ])
 def test_config_validation_without_gpu(lib, kw, status):
     base = dict(hidden=128, ffn=256, num_experts=8, top_k=2, num_shared=0, max_tokens=64,
                 renormalize=1, device=0, world_size=1, rank=0, nccl_unique_id=None,
-                packet_bytes=0, flags=0)
+                packet_bytes=0, flags=0, num_slots=0)
     base.update(kw)
     cfg = moe.moe_config(**base)
     with pytest.raises(moe.MoEError) as e:

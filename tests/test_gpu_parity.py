@@ -251,3 +251,36 @@ def test_gemm_tile_variants(shape, mode, monkeypatch):
     inp = synth.gen_inputs(cfg)
     run, out, *_ = _check_full(inp)
     run.close()
+
+
+# ------------------------------------------------------------------------- staging slots
+@pytest.mark.parametrize("slots", [2, 3, 5])
+def test_staging_slot_counts_back_to_back(slots):
+    """N-slot streaming (item q -> slot q % N, copy of item i+N after item i's GEMMs): several
+    calls over 2 layers back to back, odd slot counts included, equal isolated calls bitwise."""
+    cfg = synth.MoEConfig("custom", 15, 256, 384, 16, 4, 700, num_shared=1)
+    layers = [synth.gen_inputs(cfg, layer=l) for l in range(2)]
+    ref = [GpuRun(l) for l in layers]
+    iso = [r.run() for r in ref]
+    y_ref, idx_ref, _ = oracle.forward(layers[0].x, layers[0].router, layers[0].w1, layers[0].w3,
+                                       layers[0].w2, cfg.top_k, cfg.num_shared)
+    assert np.array_equal(iso[0][1].cpu().numpy(), idx_ref)
+    assert token_rel_err(to_f32(iso[0][0]), y_ref).max() <= TOL
+    from paper_2504_09345_b200 import MoELayer
+    layer = MoELayer(cfg.hidden, cfg.ffn, cfg.num_experts, cfg.top_k, cfg.tokens,
+                     num_shared=cfg.num_shared, num_slots=slots)
+    s = torch.cuda.current_stream()
+    outs = []
+    for it in range(5):
+        l = it % 2
+        x = bf16_tensor(layers[l].x)
+        o = torch.empty_like(x)
+        layer.forward(x, ref[l].router, ref[l].experts, o, stream=s.cuda_stream)
+        outs.append((l, o, x))
+    s.synchronize()
+    for l, o, _ in outs:
+        assert torch.equal(o, iso[l][0])
+    assert layer.stats()["num_slots"] == slots
+    layer.close()
+    for r in ref:
+        r.close()
