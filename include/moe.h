@@ -54,6 +54,11 @@ typedef enum {
 #define MOE_FLAG_PROFILE 1u  /* record CUDA events around every kernel and copy (moe_get_stats) */
 #define MOE_FLAG_FORCE_EP 2u /* world_size == 1: still run the expert-parallel exchange through a
                                 one-rank NCCL communicator (tests the EP path on one GPU)        */
+#define MOE_FLAG_LOCAL_EP 4u /* expert parallelism among `world_size` contexts of ONE process
+                                (typically on one GPU, one host thread per rank): the exchange
+                                uses device-to-device copies and host barriers instead of NCCL;
+                                nccl_unique_id points to a 128-byte group key shared by the ranks.
+                                Same plan, layouts and kernels as the NCCL path (testing).        */
 
 /*
  * Layer configuration.  Envelope of the sm_100a kernels (MOE_E_UNSUPPORTED otherwise):

@@ -28,6 +28,7 @@ MOE_E_UNSUPPORTED = 6
 MOE_E_STATE = 7
 MOE_FLAG_PROFILE = 1
 MOE_FLAG_FORCE_EP = 2
+MOE_FLAG_LOCAL_EP = 4
 
 EXPORTED = ["moe_packed_expert_bytes", "moe_pack_expert", "moe_host_alloc", "moe_host_free",
             "moe_init", "moe_layer_forward", "moe_layer_forward_host", "moe_sync", "moe_get_stats",
@@ -262,8 +263,11 @@ class MoELayer:
                  num_shared: int = 0, renormalize: bool = True, device: int = 0,
                  world_size: int = 1, rank: int = 0, packet_bytes: int = 0,
                  profile: bool = False, nccl_unique_id: Optional[bytes] = None,
-                 force_ep: bool = False, num_slots: int = 0):
-        flags = (MOE_FLAG_PROFILE if profile else 0) | (MOE_FLAG_FORCE_EP if force_ep else 0)
+                 force_ep: bool = False, num_slots: int = 0, local_ep: bool = False):
+        """local_ep: in-process expert parallelism (MOE_FLAG_LOCAL_EP); nccl_unique_id is then
+        the 128-byte group key shared by the `world_size` contexts (one host thread each)."""
+        flags = ((MOE_FLAG_PROFILE if profile else 0) | (MOE_FLAG_FORCE_EP if force_ep else 0) |
+                 (MOE_FLAG_LOCAL_EP if local_ep else 0))
         self.cfg = moe_config(hidden, ffn, num_experts, top_k, num_shared, max_tokens,
                               int(renormalize), device, world_size, rank, None, packet_bytes,
                               flags, num_slots)

@@ -85,6 +85,8 @@ struct moe_ctx_s {
 
     // expert parallelism (world_size > 1, or MOE_FLAG_FORCE_EP)
     bool ep = false;
+    bool local_ep = false;             // MOE_FLAG_LOCAL_EP: in-process transport
+    void* local_group = nullptr;       // ep.cu LocalGroup*
     moe::ncclComm_t comm = nullptr;
     int64_t cap_recv = 0;              // rows a rank can receive: W * max_tokens * top_k
     int32_t* counts_all = nullptr;     // device [W][N_e]

@@ -379,7 +379,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     c->num_sms = prop.multiProcessorCount;
     const int h = cfg->hidden, hi = cfg->ffn, ne = cfg->num_experts, k = cfg->top_k;
     const int S = cfg->num_shared, Tm = cfg->max_tokens, W = cfg->world_size;
-    c->ep = W > 1 || (cfg->flags & MOE_FLAG_FORCE_EP);
+    c->ep = W > 1 || (cfg->flags & (MOE_FLAG_FORCE_EP | MOE_FLAG_LOCAL_EP));
+    c->local_ep = (cfg->flags & MOE_FLAG_LOCAL_EP) != 0;
     c->n_local = ne / W;
     c->n_all = c->n_local + S;
     c->w13_bytes = 4ll * h * hi;

@@ -284,3 +284,76 @@ def test_staging_slot_counts_back_to_back(slots):
     layer.close()
     for r in ref:
         r.close()
+
+
+# ----------------------------------------------- expert parallelism, W ranks on one GPU
+@pytest.mark.parametrize("world,shape", [
+    (2, dict(hidden=256, ffn=384, num_experts=8, top_k=2, tokens=600, num_shared=0)),
+    (4, dict(hidden=256, ffn=256, num_experts=16, top_k=4, tokens=1000, num_shared=1)),
+    (8, dict(hidden=384, ffn=256, num_experts=64, top_k=6, tokens=804, num_shared=2)),
+    (8, dict(hidden=256, ffn=384, num_experts=8, top_k=2, tokens=5, num_shared=1)),  # empty ranks
+])
+def test_ep_local_transport_world_ranks(world, shape):
+    """MOE_FLAG_LOCAL_EP: W contexts on this GPU, one host thread per rank, each streaming ONLY
+    its N_e/W experts (+ replicated shared ones) and owning T/W tokens; the exchange plan,
+    expert-major receive layout, dispatch/combine offsets and group tables are the NCCL path's.
+    Every rank's output must equal the oracle on its token slice and, bitwise, the one-GPU
+    (non-EP) result for the same tokens."""
+    import os
+    import threading
+    from paper_2504_09345_b200 import HostExperts, MoELayer
+    cfg = synth.MoEConfig("custom", 16, shape["hidden"], shape["ffn"], shape["num_experts"],
+                          shape["top_k"], shape["tokens"], shape["num_shared"])
+    inp = synth.gen_inputs(cfg)
+    full = GpuRun(inp)
+    out_full, idx_full, _ = full.run()
+    y_ref, idx_ref, _ = oracle.forward(inp.x, inp.router, inp.w1, inp.w3, inp.w2, cfg.top_k,
+                                       cfg.num_shared)
+    ne, nl, S = cfg.num_experts, cfg.num_experts // world, cfg.num_shared
+    T = cfg.tokens
+    bounds = [T * r // world for r in range(world + 1)]
+    key = os.urandom(128)
+    layers, experts, outs, idxs, errors = [], [], [None] * world, [None] * world, []
+    for r in range(world):
+        ids = list(range(r * nl, (r + 1) * nl)) + [ne + s for s in range(S)]
+        experts.append(HostExperts(cfg.hidden, cfg.ffn, [inp.w1[i] for i in ids],
+                                   [inp.w3[i] for i in ids], [inp.w2[i] for i in ids]))
+    # contexts must all exist before any forward (they register in the group at init)
+    for r in range(world):
+        layers.append(MoELayer(cfg.hidden, cfg.ffn, ne, cfg.top_k,
+                               max(1, bounds[r + 1] - bounds[r]), num_shared=S, world_size=world,
+                               rank=r, nccl_unique_id=key, local_ep=True))
+
+    def work(r):
+        try:
+            s = torch.cuda.Stream()
+            x = bf16_tensor(inp.x[bounds[r]:bounds[r + 1]].reshape(-1, cfg.hidden))
+            o = torch.empty_like(x)
+            idx = torch.empty((x.shape[0], cfg.top_k), dtype=torch.int32, device="cuda")
+            for _ in range(2):   # twice: buffers and plans are reused across calls
+                layers[r].forward(x, full.router, experts[r], o, idx, stream=s.cuda_stream)
+            s.synchronize()
+            outs[r], idxs[r] = o, idx
+        except Exception as e:  # surfaced below
+            errors.append((r, e))
+
+    threads = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=300)
+    assert not errors, errors
+    for r in range(world):
+        lo, hi = bounds[r], bounds[r + 1]
+        if hi == lo:
+            continue
+        assert np.array_equal(idxs[r].cpu().numpy(), idx_ref[lo:hi])
+        assert token_rel_err(to_f32(outs[r]), y_ref[lo:hi]).max() <= TOL
+        assert torch.equal(outs[r], out_full[lo:hi]), f"rank {r} differs from the 1-GPU result"
+    st = [l.stats() for l in layers]
+    assert sum(s["h2d_weight_bytes"] for s in st) == 2 * (ne + world * S) * 6 * cfg.hidden * cfg.ffn
+    for l in layers:
+        l.close()
+    for e in experts:
+        e.close()
+    full.close()
