@@ -225,14 +225,24 @@ class HostExperts:
     """Pinned, packed expert blobs of one layer (this rank's routed experts, then shared)."""
 
     def __init__(self, hidden: int, ffn: int, w1: Sequence[np.ndarray], w3: Sequence[np.ndarray],
-                 w2: Sequence[np.ndarray]):
+                 w2: Sequence[np.ndarray], contiguous: bool = True):
+        """contiguous: one pinned region holding every blob back to back (the library then
+        moves consecutive small experts with one DMA); else one allocation per expert."""
         self.hidden, self.ffn = hidden, ffn
         self.blob_bytes = moe_packed_expert_bytes(hidden, ffn)
         self.ptrs: List[int] = []
+        self._allocs: List[int] = []
+        n = len(w1)
         try:
-            for a, b, c in zip(w1, w3, w2):
-                p = moe_host_alloc(self.blob_bytes)
-                self.ptrs.append(p)
+            if contiguous and n > 0:
+                base = moe_host_alloc(self.blob_bytes * n)
+                self._allocs.append(base)
+                self.ptrs = [base + i * self.blob_bytes for i in range(n)]
+            else:
+                for _ in range(n):
+                    self._allocs.append(moe_host_alloc(self.blob_bytes))
+                self.ptrs = list(self._allocs)
+            for p, a, b, c in zip(self.ptrs, w1, w3, w2):
                 moe_pack_expert(hidden, ffn, np.ascontiguousarray(a), np.ascontiguousarray(b),
                                 np.ascontiguousarray(c), p)
         except Exception:
@@ -245,8 +255,9 @@ class HostExperts:
         return self.blob_bytes * len(self.ptrs)
 
     def close(self):
-        for p in self.ptrs:
+        for p in self._allocs:
             moe_host_free(p)
+        self._allocs = []
         self.ptrs = []
 
     def __del__(self):

@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <unordered_map>
 #include <unordered_set>
 #include <vector>
 
@@ -58,7 +59,14 @@ struct moe_ctx_s {
 
     // staging slots (a bounded GPU weight buffer, recycled every call)
     int nslots = 2;
+    char* slot_base = nullptr;          // one allocation: slot s = slot_base + s * blob_bytes
     void* slot[moe::kMaxSlots] = {};
+    // DMA coalescing: consecutive streamed items whose host blobs are contiguous and whose slots
+    // are adjacent are moved by one cudaMemcpyAsync of up to copy_group experts.
+    int copy_group = 1;
+    int pend_n = 0;                     // items in the pending batch
+    uint64_t pend_q0 = 0;               // streamed-item index of the batch's first item
+    const char* pend_src = nullptr;     // host address of the batch's first blob
     cudaEvent_t ready13[moe::kMaxSlots] = {}, ready2[moe::kMaxSlots] = {};
     cudaEvent_t slot_free[moe::kMaxSlots] = {};
     uint64_t seq = 0;  // streamed-item counter across calls: item q uses slot q % nslots
@@ -111,6 +119,7 @@ struct moe_ctx_s {
     moe_stats stats{};
 
     std::unordered_set<const void*> pinned_ok;
+    std::unordered_map<const void*, uintptr_t> alloc_base;  // host blob -> start of its allocation
     std::string last_error;
     moe_status sticky = MOE_OK;
 };

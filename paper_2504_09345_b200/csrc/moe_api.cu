@@ -111,6 +111,29 @@ moe_status check_cfg(const moe_config* cfg) {
     return MOE_OK;
 }
 
+typedef CUresult (*PFN_pointerGetAttribute_t)(void*, CUpointer_attribute, CUdeviceptr);
+
+// Start address of the CUDA allocation containing p (0 if unknown).  A DMA may only be merged
+// across blobs of the SAME pinned allocation: separately allocated blobs can be adjacent in the
+// address space, and one cudaMemcpyAsync must not span two allocations.
+uintptr_t alloc_start(const void* p) {
+    static PFN_pointerGetAttribute_t fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuPointerGetAttribute", &f, cudaEnableDefault, &q) ==
+                cudaSuccess && q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_pointerGetAttribute_t>(f);
+        cudaGetLastError();
+    });
+    CUdeviceptr start = 0;
+    if (!fn || fn(&start, CU_POINTER_ATTRIBUTE_RANGE_START_ADDR, (CUdeviceptr)(uintptr_t)p) !=
+                   CUDA_SUCCESS)
+        return 0;
+    return (uintptr_t)start;
+}
+
 bool is_pinned(moe_ctx c, const void* p) {
     if (c->pinned_ok.count(p)) return true;
     cudaPointerAttributes a;
@@ -120,6 +143,7 @@ bool is_pinned(moe_ctx c, const void* p) {
     }
     if (a.type == cudaMemoryTypeHost) {
         c->pinned_ok.insert(p);
+        c->alloc_base[p] = alloc_start(p);
         return true;
     }
     return false;
@@ -140,42 +164,79 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
     return x < y + nb && y < x + na;
 }
 
-// Copy of streamed item q (index i of this call) into slot q % nslots.
-moe_status enqueue_copy(moe_ctx c, const void* const* experts, int i, uint64_t q) {
-    const int s = (int)(q % (uint64_t)c->nslots);
-    MOE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->slot_free[s], 0));
-    const char* src = static_cast<const char*>(experts[i]);
-    char* dst = static_cast<char*>(c->slot[s]);
+// Issue the pending batch of streamed items [pend_q0, pend_q0 + pend_n): their slots are
+// adjacent (no wrap) and their host blobs contiguous, so one DMA moves them all.
+moe_status flush_copies(moe_ctx c) {
+    if (c->pend_n == 0) return MOE_OK;
+    const int n = c->pend_n;
+    const int s0 = (int)(c->pend_q0 % (uint64_t)c->nslots);
+    for (int j = 0; j < n; ++j)  // each slot must have been released by its previous item's GEMMs
+        MOE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->slot_free[s0 + j], 0));
+    const char* src = c->pend_src;
+    char* dst = static_cast<char*>(c->slot[s0]);
     const int64_t pk = c->cfg.packet_bytes > 0 ? c->cfg.packet_bytes : INT64_MAX;
     Prof p(c, moe::kRecH2D, c->copy_stream);
     auto copy_range = [&](int64_t lo, int64_t hi) -> moe_status {
         for (int64_t o = lo; o < hi;) {
-            const int64_t n = std::min(pk, hi - o);
-            MOE_CUDA(c, cudaMemcpyAsync(dst + o, src + o, (size_t)n, cudaMemcpyHostToDevice,
+            const int64_t m = std::min(pk, hi - o);
+            MOE_CUDA(c, cudaMemcpyAsync(dst + o, src + o, (size_t)m, cudaMemcpyHostToDevice,
                                         c->copy_stream));
-            o += n;
+            o += m;
         }
         return MOE_OK;
     };
     if (c->cfg.packet_bytes == 0) {
-        // One DMA per expert: every extra copy/event boundary on the copy stream costs a few
-        // microseconds of idle link (measured ~0.4% of the step with separate W13/W2 copies).
-        // GEMM1 then starts after the whole blob landed -- still long before the next expert's
-        // copy ends, so nothing is exposed.
-        moe_status st = copy_range(0, c->blob_bytes);
+        // One DMA for the whole batch: every copy/event boundary on the copy stream costs a few
+        // microseconds of idle link (measured: separate W13/W2 copies lost ~0.4% of the C1 step,
+        // 17 MB per-expert copies ran at 54.0 of 55.6 GB/s).  GEMM1 then starts after the
+        // batch landed -- still long before the next batch's copy ends.
+        moe_status st = copy_range(0, (int64_t)n * c->blob_bytes);
         if (st != MOE_OK) return st;
-        MOE_CUDA(c, cudaEventRecord(c->ready13[s], c->copy_stream));
-        MOE_CUDA(c, cudaEventRecord(c->ready2[s], c->copy_stream));
-    } else {
-        moe_status st = copy_range(0, c->w13_bytes);
-        if (st != MOE_OK) return st;
-        MOE_CUDA(c, cudaEventRecord(c->ready13[s], c->copy_stream));
-        st = copy_range(c->w13_bytes, c->blob_bytes);
-        if (st != MOE_OK) return st;
-        MOE_CUDA(c, cudaEventRecord(c->ready2[s], c->copy_stream));
+        for (int j = 0; j < n; ++j) {
+            MOE_CUDA(c, cudaEventRecord(c->ready13[s0 + j], c->copy_stream));
+            MOE_CUDA(c, cudaEventRecord(c->ready2[s0 + j], c->copy_stream));
+        }
+    } else {  // packetised: W13 first so GEMM1 can start early
+        for (int j = 0; j < n; ++j) {
+            const int64_t b = (int64_t)j * c->blob_bytes;
+            moe_status st = copy_range(b, b + c->w13_bytes);
+            if (st != MOE_OK) return st;
+            MOE_CUDA(c, cudaEventRecord(c->ready13[s0 + j], c->copy_stream));
+            st = copy_range(b + c->w13_bytes, b + c->blob_bytes);
+            if (st != MOE_OK) return st;
+            MOE_CUDA(c, cudaEventRecord(c->ready2[s0 + j], c->copy_stream));
+        }
     }
     p.end();
-    c->stats.h2d_weight_bytes += c->blob_bytes;
+    c->stats.h2d_weight_bytes += (int64_t)n * c->blob_bytes;
+    c->pend_n = 0;
+    return MOE_OK;
+}
+
+// Request the copy of streamed item q (blob experts[i]) into slot q % nslots.  Requests
+// are batched (see flush_copies); a batch is flushed when full, when the next item is not
+// contiguous (host blob or slot), and at the end of each call.  Items are requested nslots ahead
+// of their GEMMs and copy_group <= nslots, so an item's batch is always flushed before the
+// compute stream waits on it.
+moe_status request_copy(moe_ctx c, const void* const* experts, int i, uint64_t q) {
+    const char* src = static_cast<const char*>(experts[i]);
+    const int s = (int)(q % (uint64_t)c->nslots);
+    if (c->pend_n > 0) {
+        const uintptr_t a0 = c->alloc_base[c->pend_src], a1 = c->alloc_base[src];
+        const bool contiguous = src == c->pend_src + (int64_t)c->pend_n * c->blob_bytes &&
+                                q == c->pend_q0 + (uint64_t)c->pend_n && s != 0 && a0 != 0 &&
+                                a0 == a1;
+        if (!contiguous || c->pend_n >= c->copy_group) {
+            moe_status st = flush_copies(c);
+            if (st != MOE_OK) return st;
+        }
+    }
+    if (c->pend_n == 0) {
+        c->pend_q0 = q;
+        c->pend_src = src;
+    }
+    ++c->pend_n;
+    if (c->pend_n >= c->copy_group) return flush_copies(c);
     return MOE_OK;
 }
 
@@ -196,10 +257,15 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     if (S > 0 && T > 0 && !moe::make_tmap(&tm_x, hidden, (uint64_t)T, (uint64_t)h, 128))
         return set_err(c, MOE_E_CUDA, "cuTensorMapEncodeTiled failed for hidden");
 
+    // Streaming order: shared experts first (their GEMMs need only the hidden batch, and they are
+    // the longest GEMMs -- T rows each -- so they must not sit at the end of a call where they
+    // would hold slots the next call's first copies wait on), then the routed experts.
+    // expert_of(i) is the index into `experts` / the group tables of streamed item i.
+    auto expert_of = [&](int i) { return i < S ? c->n_local + i : i - S; };
     // the first nslots weight copies go ahead of routing (cross-call prefetch)
     const int ns = c->nslots;
     for (int i = 0; i < std::min(ns, c->n_all); ++i) {
-        moe_status s = enqueue_copy(c, experts, i, q0 + i);
+        moe_status s = request_copy(c, experts, expert_of(i), q0 + i);
         if (s != MOE_OK) return s;
     }
     if (hidden_on_copy_stream) MOE_CUDA(c, cudaStreamWaitEvent(st, c->x_ready[xb], 0));
@@ -250,14 +316,19 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     for (int i = 0; i < c->n_all; ++i) {
         const uint64_t q = q0 + i;
         const int s = (int)(q % (uint64_t)ns);
-        const bool shared = i >= c->n_local;
+        const int e = expert_of(i);
+        const bool shared = e >= c->n_local;
+        if (c->pend_n > 0 && c->pend_q0 <= q) {  // this item's batch is still pending: issue it
+            moe_status fs = flush_copies(c);
+            if (fs != MOE_OK) return fs;
+        }
         MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready13[s], 0));
         {
             Prof p(c, moe::kRecGemm1, st);
             const bool pr = use_pair(shared, c->bn1);
             MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmSwiGLU, c->bn1, pr,
                                                 shared ? &tm_x : tmA_routed,
-                                                pr ? &c->tm_w13_pair[s] : &c->tm_w13[s], g1 + i,
+                                                pr ? &c->tm_w13_pair[s] : &c->tm_w13[s], g1 + e,
                                                 2 * hi, h, c->h_act, hi, grid, st));
             p.end();
         }
@@ -266,7 +337,7 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
             Prof p(c, moe::kRecGemm2, st);
             const bool pr = use_pair(shared, c->bn2);
             MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmPlain, c->bn2, pr, &c->tm_h,
-                                                pr ? &c->tm_w2_pair[s] : &c->tm_w2[s], g2 + i, h,
+                                                pr ? &c->tm_w2_pair[s] : &c->tm_w2[s], g2 + e, h,
                                                 hi, shared ? c->y_perm : y_routed, h, grid, st));
             p.end();
         }
@@ -275,9 +346,13 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         c->stats.gemm2_launches += 1;
         MOE_CUDA(c, cudaEventRecord(c->slot_free[s], st));
         if (i + ns < c->n_all) {
-            moe_status s2 = enqueue_copy(c, experts, i + ns, q + ns);
+            moe_status s2 = request_copy(c, experts, expert_of(i + ns), q + ns);
             if (s2 != MOE_OK) return s2;
         }
+    }
+    {
+        moe_status fs = flush_copies(c);  // nothing may stay pending across calls
+        if (fs != MOE_OK) return fs;
     }
     if (c->ep) {
         Prof p(c, moe::kRecComm, st);
@@ -394,6 +469,10 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
         const int64_t want = (moe::kAutoSlotBytes + c->blob_bytes - 1) / c->blob_bytes;
         c->nslots = (int)std::max<int64_t>(2, std::min<int64_t>({want, 8, (int64_t)c->n_all - 1}));
     }
+    // DMA batches of ~64 MiB, at most half the slots (two batches in flight)
+    c->copy_group = (int)std::max<int64_t>(
+        1, std::min<int64_t>((moe::kCopyBatchBytes + c->blob_bytes - 1) / c->blob_bytes, c->nslots / 2));
+    if (const char* e = getenv("MOE_COPY_GROUP")) c->copy_group = std::max(1, std::min(atoi(e), c->nslots));
     c->cap_recv = c->ep ? (int64_t)W * Tm * k : (int64_t)Tm * k;
     // h_act rows: routed rows (received rows under EP) then S * Tm shared rows
     const int64_t h_rows = c->cap_recv + (int64_t)S * Tm;
@@ -403,8 +482,9 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     auto dalloc = [&](void** p, size_t n) { return cudaMalloc(p, n) == cudaSuccess; };
     bool ok = true;
     ok &= cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) == cudaSuccess;
+    ok &= dalloc((void**)&c->slot_base, (size_t)c->blob_bytes * c->nslots);
     for (int i = 0; i < c->nslots; ++i) {
-        ok &= dalloc(&c->slot[i], (size_t)c->blob_bytes);
+        c->slot[i] = c->slot_base ? c->slot_base + (size_t)i * c->blob_bytes : nullptr;
         ok &= cudaEventCreateWithFlags(&c->ready13[i], cudaEventDisableTiming) == cudaSuccess;
         ok &= cudaEventCreateWithFlags(&c->ready2[i], cudaEventDisableTiming) == cudaSuccess;
         ok &= cudaEventCreateWithFlags(&c->slot_free[i], cudaEventDisableTiming) == cudaSuccess;
@@ -590,8 +670,8 @@ moe_status moe_destroy(moe_ctx c) {
         cudaEventDestroy(r.b);
     }
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    cudaFree(c->slot_base);
     for (int i = 0; i < moe::kMaxSlots; ++i) {
-        cudaFree(c->slot[i]);
         cudaEvent_t evs[] = {c->ready13[i], c->ready2[i], c->slot_free[i]};
         for (cudaEvent_t e : evs)
             if (e) cudaEventDestroy(e);

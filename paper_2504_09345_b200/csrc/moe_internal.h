@@ -13,6 +13,7 @@ constexpr int kMaxTopK = 8;          // envelope: top_k <= 8
 constexpr int kMaxShared = 8;
 constexpr int kMaxSlots = 16;        // expert staging slots
 constexpr int64_t kAutoSlotBytes = 256ll << 20;  // auto slot count: ~256 MiB of staging
+constexpr int64_t kCopyBatchBytes = 64ll << 20;  // coalesced H2D DMA size target
 
 // Row range of one expert group inside a GEMM's A operand, and where its output rows go.
 struct GemmGroup {
