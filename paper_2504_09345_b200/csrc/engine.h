@@ -72,8 +72,7 @@ struct moe_ctx_s {
     uint64_t seq = 0;  // streamed-item counter across calls: item q uses slot q % nslots
     CUtensorMap tm_w13[moe::kMaxSlots], tm_w2[moe::kMaxSlots];
     CUtensorMap tm_w13_pair[moe::kMaxSlots], tm_w2_pair[moe::kMaxSlots];  // 128-row boxes (pair GEMM)
-    int pair_mode = 0;        // MOE_GEMM_PAIR: 0 never (default), 1 always, -1 auto (rows per group)
-    int pair_min_rows = 2048; // auto: CTA-pair GEMM when the expected group has >= this many rows
+    int pair_mode = -1;       // MOE_GEMM_PAIR: 0 never, 1 always, -1 auto (default: wave model)
 
     // workspace
     int32_t* idx_ws = nullptr;

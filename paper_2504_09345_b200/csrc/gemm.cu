@@ -52,6 +52,7 @@ __device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, 
 // L2 policies of the operand loads (MOE_GEMM_L2HINT: 0 = evict_normal for both, 1 = A evict_last
 // + B evict_first).  Set once per process by set_gemm_l2_hints().
 __device__ int g_l2_hints = 0;
+__device__ int g_group_m = 0;  // raster group override (0 = kernel default); experiments only
 
 __device__ __forceinline__ uint64_t l2_policy_a() {
     return g_l2_hints ? ptx::policy_evict_last() : ptx::policy_evict_normal();
@@ -138,7 +139,9 @@ expert_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     const int total = m_tiles * n_tiles;
     if ((int)blockIdx.x >= total) return;
     const int num_kb = K / BK;
-    const int group_m = (K <= 8192) ? 16 : 8;  // A tile = 128 x K bf16 (1 MB at K=4096)
+    // rows per raster group: A footprint ~32 MB (measured at 65k tokens, K=4096: group 16 ->
+    // 2.0 GB DRAM per launch, group 32 -> 1.08 GB; the weight tiles are re-read once per group)
+    const int group_m = g_group_m > 0 ? g_group_m : ((K <= 8192) ? 32 : 8);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -293,7 +296,7 @@ expert_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
     const int total = m_tiles * n_tiles;
     if (pair >= total) return;                   // both CTAs of a pair leave together
     const int num_kb = K / BK;
-    const int group_m = (K <= 8192) ? 8 : 4;
+    const int group_m = g_group_m > 0 ? g_group_m : ((K <= 8192) ? 16 : 4);  // 256-row tiles
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -468,5 +471,8 @@ cudaError_t launch_expert_gemm(int mode, int bn, bool pair, const CUtensorMap* t
 namespace moe {
 cudaError_t set_gemm_l2_hints(int mode) {
     return cudaMemcpyToSymbol(g_l2_hints, &mode, sizeof(int));
+}
+cudaError_t set_gemm_group_m(int gm) {
+    return cudaMemcpyToSymbol(g_group_m, &gm, sizeof(int));
 }
 }  // namespace moe

@@ -4,13 +4,12 @@
 // beginning of each stage by the Contiguous Data Mover ... runs asynchronously ... synchronizes
 // only at the stage boundaries"; PAPER.md:823-826 pinned host weights and a GPU weight buffer of
 // two units; PAPER.md:829-835 packetised transfers):
-//   * two device staging slots, each one packed expert (W13 | W2);
-//   * a dedicated copy stream; the copy of streamed item q into slot q%2 waits on `slot_free[q%2]`
-//     (recorded after the GEMMs of item q-2) and records `ready13` / `ready2` after its W13 / W2
-//     parts, so GEMM1 of expert e starts as soon as its W13 lands and the H2D of expert e+1
-//     overlaps the GEMMs of expert e;
-//   * host enqueue order interleaves "GEMMs of item i" with "copy of item i+2", and a call's first
-//     two copies are enqueued before its routing kernels, so the copy engine runs back-to-back
+//   * N device staging slots (N = num_slots, auto ~256 MiB), each one packed expert (W13 | W2);
+//   * a dedicated copy stream; the copy of streamed item q into slot q%N waits on `slot_free[q%N]`
+//     (recorded after the GEMMs of item q-N) and records `ready13` / `ready2`, so the H2D of the
+//     next experts overlaps the GEMMs of expert e; consecutive small experts move in one DMA;
+//   * host enqueue order interleaves "GEMMs of item i" with "copy of item i+N", and a call's first
+//     N copies are enqueued before its routing kernels, so the copy engine runs back-to-back
 //     across experts AND across calls (cross-call prefetch of the next layer's first experts).
 #include <algorithm>
 #include <climits>
@@ -304,14 +303,24 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     }
 
     const int grid = c->num_sms;
-    // Tile shape: the CTA-pair kernel (256-row tiles) for large groups, else 128-row tiles.
-    // The host does not know the group sizes (they live on the device), so it decides on the
-    // expected size: T*k*W/N_e rows per routed expert, T rows per shared expert.
+    // Tile shape per launch: the CTA-pair kernel (256x256 tiles on SM pairs, ~97% tensor-pipe
+    // activity) or the single-CTA kernel (128x256, ~76%: shared-memory bandwidth bound, but half
+    // the M granularity and twice the concurrent tiles).  The host does not know the group sizes
+    // (they live on the device), so it decides on the expected size -- T*k*W/N_e rows per routed
+    // expert (+10% for routing variance), T per shared expert -- with a wave model:
+    //   time ~ ceil(tiles / concurrent tiles) / tensor efficiency.
     const int64_t exp_routed = (int64_t)T * k * cf.world_size / ne;
-    auto use_pair = [&](bool shared, int bn) {
+    const int sms = c->num_sms;
+    auto use_pair = [&](bool shared, int bn, int N) {
         if (bn != 256 || c->pair_mode == 0) return false;
         if (c->pair_mode == 1) return true;
-        return (shared ? (int64_t)T : exp_routed) >= c->pair_min_rows;
+        const int64_t rows = shared ? (int64_t)T : exp_routed + exp_routed / 10;
+        if (rows <= 0) return false;
+        const int64_t nt = N / 256;
+        const int64_t t1 = ((rows + 127) / 128) * nt, t2 = ((rows + 255) / 256) * nt;
+        const double w1 = (double)((t1 + sms - 1) / sms) / 0.76;
+        const double w2 = (double)((t2 + sms / 2 - 1) / (sms / 2)) / 0.97;
+        return w2 < w1;
     };
     for (int i = 0; i < c->n_all; ++i) {
         const uint64_t q = q0 + i;
@@ -325,7 +334,7 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready13[s], 0));
         {
             Prof p(c, moe::kRecGemm1, st);
-            const bool pr = use_pair(shared, c->bn1);
+            const bool pr = use_pair(shared, c->bn1, 2 * hi);
             MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmSwiGLU, c->bn1, pr,
                                                 shared ? &tm_x : tmA_routed,
                                                 pr ? &c->tm_w13_pair[s] : &c->tm_w13[s], g1 + e,
@@ -335,7 +344,7 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready2[s], 0));
         {
             Prof p(c, moe::kRecGemm2, st);
-            const bool pr = use_pair(shared, c->bn2);
+            const bool pr = use_pair(shared, c->bn2, h);
             MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmPlain, c->bn2, pr, &c->tm_h,
                                                 pr ? &c->tm_w2_pair[s] : &c->tm_w2[s], g2 + e, h,
                                                 hi, shared ? c->y_perm : y_routed, h, grid, st));
@@ -528,11 +537,12 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
         else if (!strcmp(e, "1")) c->pair_mode = 1;
         else if (!strcmp(e, "auto")) c->pair_mode = -1;
     }
-    if (const char* e = getenv("MOE_GEMM_PAIR_MIN_ROWS")) c->pair_min_rows = atoi(e);
     {
         int hints = 0;   // measured: evict_normal beats evict_last/evict_first (profiles/r01)
         if (const char* e = getenv("MOE_GEMM_L2HINT")) hints = atoi(e);
         if (moe::set_gemm_l2_hints(hints) != cudaSuccess) return fail(MOE_E_CUDA);
+        const char* gm = getenv("MOE_GEMM_GROUPM");
+        if (moe::set_gemm_group_m(gm ? atoi(gm) : 0) != cudaSuccess) return fail(MOE_E_CUDA);
     }
     if (c->ep) {
         moe_status es = moe::ep_init(c);

@@ -56,5 +56,6 @@ int gemm_bn_for(int mode, int N);   // tile width used for a given mode / N (0 =
 // L2 policy of the GEMM operand loads for the current device: 0 evict_normal, 1 A evict_last +
 // B evict_first.
 cudaError_t set_gemm_l2_hints(int mode);
+cudaError_t set_gemm_group_m(int gm);   // 0 = per-kernel default (MOE_GEMM_GROUPM, experiments)
 
 }  // namespace moe
