@@ -1,0 +1,165 @@
+"""NEXT-4: the paper's Stage 1 / Stage 2 performance model (§5, Eqs. 3-14), pinned to the
+numbers the paper prints, SPEC.md's worked examples (each recomputed independently here, e.g. q by
+brute-force summation) and the model's limits; plus the B200 calibration of the streamed layer
+against the profiler measurements committed under profiles/."""
+import glob
+import json
+import math
+import os
+
+import pytest
+
+from paper_2504_09345_b200 import ledger
+from paper_2504_09345_b200 import perfmodel as pm
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+# ------------------------------------------------------------------------------ Stage 1
+def test_pme_closed_form_examples():
+    # p=100, g=128 -> 456/41984
+    assert pm.pme(100, 128) == pytest.approx(456 / 41984)
+    # g = 1 -> 2(p+1)/(2p+1); p = 1 -> 4/3
+    assert pm.pme(1, 1) == pytest.approx(4 / 3)
+    assert pm.pme(7, 1) == pytest.approx(16 / 15)
+    # monotone decreasing in g
+    assert all(pm.pme(50, g) > pm.pme(50, g + 1) for g in range(1, 300))
+
+
+def test_pme_closed_form_vs_lifetime_sum():
+    """Eq. 3's closed form uses the midpoint g/2 of the lifetime sum sum_{j<g}(p+j); the two
+    agree within 1/(2p+g)."""
+    for p in (1, 10, 100, 1000):
+        for g in (1, 7, 64, 512):
+            exact = (p + g) / sum(p + j for j in range(g))
+            assert abs(pm.pme(p, g) - exact) / exact <= 1.0 / (2 * p + g) + 1e-12
+
+
+def test_weight_transfer_delta():
+    # delta = 94 GB / 19.5 GB/s ~ 4.82 s ("approximately 5 seconds")
+    assert pm.weight_transfer_time(94e9, 19.5e9) == pytest.approx(4.82, abs=0.01)
+    assert pm.weight_transfer_time(282e9, 19.5e9) == pytest.approx(14.46, abs=0.01)
+
+
+def test_t_max_regimes():
+    p, g, delta, t_gpu = 100, 128, 4.82, 1e5
+    big = pm.t_max(p, g, 1e12, delta, t_gpu)
+    assert big["utilization"] == 1.0 and big["regime"] == "GpuBound"
+    m_half = t_gpu / 2 * delta / pm.pme(p, g)          # PME*M/delta = T_GPU/2
+    half = pm.t_max(p, g, m_half, delta, t_gpu)
+    assert half["utilization"] == pytest.approx(0.5) and half["regime"] == "MemoryBound"
+    with pytest.raises(ValueError):
+        pm.t_max(p, g, p + g - 1, delta, t_gpu)
+    # linear in M then flat (Fig. 3b shape)
+    us = [pm.t_max(p, g, m, delta, t_gpu)["utilization"] for m in (m_half / 2, m_half, 2 * m_half, 4 * m_half)]
+    assert us == pytest.approx([0.25, 0.5, 1.0, 1.0])
+
+
+def test_required_bandwidths_paper_example():
+    # "KV cache is twice the size of the model weights ... B_Mem = 60 GB/s" at ~20 GB/s PCIe
+    r = pm.required_bandwidths(kv_bytes=200e9, weight_bytes=100e9, b_io=20e9)
+    assert r["b_mem"] == pytest.approx(60e9) and r["b_kv"] + 20e9 == pytest.approx(r["b_mem"])
+    assert pm.required_bandwidths(0, 94e9, 19.5e9)["b_mem"] == pytest.approx(19.5e9)
+    assert pm.required_bandwidths(94e9, 94e9, 19.5e9)["b_mem"] == pytest.approx(39e9)
+
+
+def test_cpu_attention_throughput_magnitude():
+    # s=4, I=2 FLOP/B, B_KV=40 GB/s -> 640 GFLOP/s: "hundreds of GFLOPs"
+    assert pm.required_cpu_attn_throughput(4, 2, 40e9) == pytest.approx(640e9)
+    assert pm.required_cpu_attn_throughput(8, 2, 40e9) == pytest.approx(1280e9)
+
+
+def test_effective_kv_capacity():
+    assert pm.effective_kv_capacity(100, 128, 1.0) == pytest.approx(228 / 164)
+    assert pm.effective_kv_capacity(100, 1e-9, 1.0) == pytest.approx(1.0)
+    assert all(pm.effective_kv_capacity(p, 1000, 1.0) < 2 for p in (1, 10, 100))
+
+
+def test_utilization_surface_properties():
+    grid = pm.utilization_surface([50, 100, 500], [32, 64, 128, 256], 5e6, 4.82, 1e6)
+    assert all(0 <= u <= 1 for row in grid for u in row)
+    assert all(row[i] >= row[i + 1] for row in grid for i in range(3))   # decreasing in g
+
+
+# ------------------------------------------------------------------------------ Stage 2
+def test_prefill_rate_brute_force_and_b1_closed_form():
+    # N=1000, b=16, p=100, g=128: sum_i ceil((100+i)/16) = 1383
+    demand = 0
+    for i in range(129):
+        demand += -(-(100 + i) // 16)
+    assert demand == 1383
+    assert pm.prefill_rate(1000, 16, 100, 128) == pytest.approx(1000 / 1383)
+    # b = 1: q = N / ((g+1)(p + g/2))
+    assert pm.prefill_rate(5000, 1, 100, 128) == pytest.approx(5000 / (129 * (100 + 64)))
+    # Eq. 9: more sequences decode in parallel than with separated stages (b = 1)
+    q = pm.prefill_rate(5000, 1, 100, 128)
+    assert 128 * q > 5000 / (100 + 128)
+
+
+def test_t1_forms_and_limits():
+    K, g, q, d = 20000, 128, 1000 / 1383, 4.82
+    t1 = pm.t1_memory_bound(K, g, q, d)
+    assert t1 == pytest.approx(K / (K + g * q) * (g * q / d), rel=1e-12)   # Eq. 10 identity
+    assert pm.t1_memory_bound(1e15, g, q, d) == pytest.approx(g * q / d, rel=1e-6)
+    assert pm.t1_memory_bound(g * q, g, q, d) == pytest.approx(g * q / (2 * d))
+
+
+def test_t2_worked_example():
+    # K=20000, p=100, g=128, T_GPU=18750 tok/iter, delta=4.82 -> It ~ 289.3, T2 ~ 1835
+    r = pm.t2_gpu_bound(20000, 100, 128, 18750, 4.82)
+    assert r["t_prefill"] == pytest.approx(18750 * 100 / 228)
+    assert r["iterations"] == pytest.approx(289.3, abs=0.05)
+    assert r["t2"] == pytest.approx(1835, rel=1e-3)
+    with pytest.raises(ValueError):
+        pm.t2_gpu_bound(10, 100, 128, 18750, 4.82)       # batch ends in the prologue
+
+
+def test_stage2_converges_to_stage1():
+    """K -> inf, b = 1: Stage 2 -> Stage 1.  Exactly: in the memory-bound regime the
+    ratio is g/(g+1) -- Eq. 8 sums g+1 ceilings while Eq. 3's closed form counts g terms
+    (reading R17) -- and both saturate at utilisation 1 in the GPU-bound regime."""
+    delta, t_gpu = 4.82, 2000.0
+    for p, g in ((100, 128), (500, 64), (50, 32), (1000, 256)):
+        for n_blocks in (20000, 200000, 2000000, 20000000):
+            s2 = pm.predict(10 ** 9, p, g, n_blocks, 1, t_gpu, delta)
+            s1 = pm.t_max(p, g, n_blocks, delta, t_gpu)
+            if s1["regime"] == "MemoryBound" and s2["regime"] == "MemoryBound":
+                assert s2["predicted_utilization"] / s1["utilization"] == pytest.approx(
+                    g / (g + 1), rel=1e-4), (p, g, n_blocks)   # finite-K epilogue K/(K+gq)
+            else:
+                assert s2["predicted_utilization"] == pytest.approx(s1["utilization"], rel=1.0 / g)
+
+
+def test_stage2_monotonicity():
+    delta, t_gpu, p, g = 4.82, 2000.0, 100, 128
+    caps = [pm.predict(20000, p, g, n, 16, t_gpu, delta)["predicted_throughput"]
+            for n in (2000, 5000, 20000, 100000)]
+    assert caps == sorted(caps)                                           # nondecreasing in M
+    ks = [pm.predict(k, p, g, 20000, 16, t_gpu, delta)["predicted_throughput"]
+          for k in (1000, 10000, 100000)]
+    assert ks == sorted(ks)                                               # nondecreasing in K
+    m_tokens = 320000                                   # fixed capacity in tokens, N = M / b
+    bs = [pm.predict(20000, p, g, m_tokens // b, b, t_gpu, delta)["predicted_throughput"]
+          for b in (1, 4, 16, 64)]
+    assert bs == sorted(bs, reverse=True)                                 # nonincreasing in b
+
+
+# --------------------------------------------------------------- B200 calibration (measured)
+def _profiler_files():
+    return sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "**", "profiler_*.json"),
+                            recursive=True))
+
+
+@pytest.mark.skipif(not _profiler_files(), reason="no committed profiler measurement")
+def test_b200_layer_model_predicts_measured_step_times():
+    """Stage 1 for one streamed layer -- time = max(delta, GPU line) -- against the measured
+    step times of the profiler sweep on a B200: mean accuracy >= 94% (the paper's own figure,
+    P:975), and n_real within the Eq. 2 estimate's neighbourhood."""
+    for f in _profiler_files():
+        prof = json.load(open(f))
+        v = pm.validate_against_profiler(prof)
+        assert v["mean_accuracy"] >= 0.94, (f, v)
+        n_eq2 = ledger.eq2_tokens_to_saturate(prof["eq2_inputs"]["tensor_tflops"],
+                                              prof["eq2_inputs"]["host_link_gbs"], 8, 2,
+                                              binary_prefixes=False)
+        assert 0.5 * n_eq2 < v["n_real"] < 1.2 * n_eq2
