@@ -299,7 +299,9 @@ def run_ours(args):
     # host-link bound and the GPU idles between expert GEMMs, so it runs at full boost clock
     # (see `clocks`), not at the power-capped clock of the sustained figure; the burst peak is
     # the conservative denominator here.  The sustained-peak fraction is reported beside it.
-    roofline = {"kernel": "expert_gemm_kernel<256,SwiGLU> (a5, tcgen05)", "bound": "tensor",
+    roofline = {"kernel": "expert GEMM1 + fused SwiGLU (a5): tcgen05 expert_gemm_pair_kernel / "
+                          "expert_gemm_kernel<256,0>, chosen per launch by the wave model",
+                "bound": "tensor",
                 "achieved": achieved_tf, "peak": peaks["bf16_tflops"],
                 "unit": "TFLOP/s", "frac": achieved_tf / peaks["bf16_tflops"],
                 "frac_of_sustained_peak": achieved_tf / peaks["bf16_tflops_sustained"],
