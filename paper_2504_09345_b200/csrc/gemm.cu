@@ -411,14 +411,12 @@ expert_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
 template <int MODE>
 cudaError_t launch_pair(const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmGroup* group,
                         int N, int K, __nv_bfloat16* out, int ldo, int grid, cudaStream_t st) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(expert_gemm_pair_kernel<MODE>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)kPairSmem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    // Set on every launch: the attribute is per device context, contexts may be driven from
+    // several host threads (MOE_FLAG_LOCAL_EP), and the call is a cheap host-side update.
+    cudaError_t e = cudaFuncSetAttribute(expert_gemm_pair_kernel<MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kPairSmem);
+    if (e != cudaSuccess) return e;
     expert_gemm_pair_kernel<MODE><<<grid & ~1, kThreads, kPairSmem, st>>>(*tmA, *tmB, group, N, K,
                                                                           out, ldo);
     return cudaGetLastError();
@@ -428,14 +426,10 @@ template <int BN, int MODE>
 cudaError_t launch_one(const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmGroup* group,
                        int N, int K, __nv_bfloat16* out, int ldo, int grid, cudaStream_t st) {
     using C = GemmCfg<BN>;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(expert_gemm_kernel<BN, MODE>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)C::kSmem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    cudaError_t e = cudaFuncSetAttribute(expert_gemm_kernel<BN, MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)C::kSmem);   // every launch, see launch_pair
+    if (e != cudaSuccess) return e;
     expert_gemm_kernel<BN, MODE><<<grid, kThreads, C::kSmem, st>>>(*tmA, *tmB, group, N, K, out, ldo);
     return cudaGetLastError();
 }

@@ -359,14 +359,10 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
     const int ept = (ne + 7) / 8;
 #define MOE_ROUTER(E)                                                                        \
     do {                                                                                     \
-        static bool attr = false;                                                            \
-        if (!attr) {                                                                         \
-            cudaError_t e_ = cudaFuncSetAttribute(router_topk_kernel<E>,                     \
-                cudaFuncAttributeMaxDynamicSharedMemorySize,                                 \
-                (int)(sizeof(double) * kMaxExperts * kChunk));                               \
-            if (e_ != cudaSuccess) return e_;                                                \
-            attr = true;                                                                     \
-        }                                                                                    \
+        cudaError_t e_ = cudaFuncSetAttribute(router_topk_kernel<E>,                         \
+            cudaFuncAttributeMaxDynamicSharedMemorySize,                                     \
+            (int)(sizeof(double) * kMaxExperts * kChunk));                                   \
+        if (e_ != cudaSuccess) return e_;                                                    \
         router_topk_kernel<E><<<n_tiles, kRouterThreads, dyn, st>>>(x, T, h, wr, ne, k,      \
                                                                      renorm, idx, gates,     \
                                                                      tile_counts);           \
