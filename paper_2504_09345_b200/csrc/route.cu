@@ -18,7 +18,6 @@ namespace moe {
 
 namespace {
 
-constexpr int kRouterThreads = 256;
 constexpr int kChunk = 64;  // channels staged per iteration (one 16-byte vector per thread of x)
 constexpr int kXsPitch = kRouteTile + 1;  // padded row (doubles): conflict-free transposed stores
 
@@ -40,61 +39,87 @@ __device__ __forceinline__ void bf16x8_to_f64(const int4& v, double (&o)[8]) {
     }
 }
 
-// One block = kRouteTile (32) tokens.  Warp w computes experts {w, w+8, w+16, ...} for all 32
-// tokens (lane = token), EPT accumulators per thread; each accumulator is ONE fp64 FMA chain in
-// ascending channel order (the definition's order, reading R6).  Staging: 64-channel chunks, one
-// 16-byte x vector per thread and up to 4 router vectors, prefetched into registers one chunk
-// ahead so global latency overlaps the FMA chains.
+// Router: one block = kRouteTile (32) tokens; warp w owns experts [w*EPT, (w+1)*EPT) for all 32
+// tokens (lane = token).  Every (token, expert) logit is ONE fp64 FMA chain over the channels in
+// ascending order -- the definition's order (reading R6) -- so selection is bit-exact.  Per
+// channel a lane reads its x value (fp64, transposed tile) and its EPT router weights as EPT/2
+// double2 broadcasts from a [channel][expert] tile zero-padded to a multiple of EPT experts:
+// 1 + EPT/2 shared-memory wavefront groups per EPT DFMAs and no branches in the inner loop.
+// 64-channel chunks are staged with 16-byte loads prefetched into registers one chunk ahead.
 template <int EPT>
-__global__ void __launch_bounds__(kRouterThreads)
+__global__ void __launch_bounds__(EPT >= 8 ? 512 : 256)
 router_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
                    const __nv_bfloat16* __restrict__ wr, int ne, int k, int renorm,
                    int32_t* __restrict__ idx_out, float* __restrict__ gate_out,
                    int32_t* __restrict__ tile_counts) {
-    __shared__ double xs[kChunk * kXsPitch];   // x tile, transposed [c][t], fp64
+    extern __shared__ __align__(16) double dyn[];
     __shared__ int cnt[kMaxExperts];
-    extern __shared__ double dyn[];            // ws [ne][kChunk]  then logits [32][ne]
-    double* ws = dyn;
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nw = blockDim.x >> 5;            // warps = ne_pad / EPT
+    const int ne_pad = nw * EPT;
+    double* xs = dyn;                           // [kChunk][kXsPitch]
+    double* ws = dyn + kChunk * kXsPitch;       // [kChunk][ne_pad], later logits [32][ne_pad]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
     const int t0 = blockIdx.x * kRouteTile;
-    for (int e = tid; e < kMaxExperts; e += kRouterThreads) cnt[e] = 0;
+    for (int e = tid; e < kMaxExperts; e += nthr) cnt[e] = 0;
 
     double acc[EPT];
 #pragma unroll
     for (int i = 0; i < EPT; ++i) acc[i] = 0.0;
 
-    // staging assignment: x vector (token xt, channels xc..xc+7); router vectors v = tid + 256 i
-    const int xt = tid >> 3, xc = (tid & 7) * 8;
-    const bool xvalid = t0 + xt < T;
-    const int nwv = ne * (kChunk / 8);
-    int4 xr = make_int4(0, 0, 0, 0);
-    int4 wv[kMaxExperts * (kChunk / 8) / kRouterThreads];
+    constexpr int kXV = kRouteTile * (kChunk / 8) / 32;  // x vectors per thread (1 warp) = 8
+    constexpr int kWV = (EPT * (kChunk / 8) + 31) / 32;  // router vectors per thread
+    const int n_xv = kRouteTile * (kChunk / 8);
+    const int n_wv = ne_pad * (kChunk / 8);
+    int4 xr[kXV], wv[kWV];
+    // Staging maps consecutive lanes to consecutive TOKENS (x) / EXPERTS (router) at a fixed
+    // 8-channel group, so the transposed fp64 stores hit consecutive shared-memory words (the
+    // row-major mapping caused ~72M bank conflicts per C4 call); each lane still reads 16 B.
     auto load = [&](int c0) {
-        if (xvalid) xr = ptx::ld_nc_v4(x + (size_t)(t0 + xt) * h + c0 + xc);
 #pragma unroll
-        for (int i = 0; i < kMaxExperts * (kChunk / 8) / kRouterThreads; ++i) {
-            const int v = tid + kRouterThreads * i;
-            if (v < nwv) wv[i] = ptx::ld_nc_v4(wr + (size_t)(v >> 3) * h + c0 + (v & 7) * 8);
+        for (int j = 0; j < kXV; ++j) {
+            const int v = tid + j * nthr;
+            if (v < n_xv) {
+                const int t = v & 31, cc = (v >> 5) * 8;
+                xr[j] = (t0 + t < T) ? ptx::ld_nc_v4(x + (size_t)(t0 + t) * h + c0 + cc)
+                                     : make_int4(0, 0, 0, 0);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kWV; ++j) {
+            const int v = tid + j * nthr;
+            if (v < n_wv) {
+                const int e = v % ne_pad, cc = (v / ne_pad) * 8;
+                wv[j] = (e < ne) ? ptx::ld_nc_v4(wr + (size_t)e * h + c0 + cc)
+                                 : make_int4(0, 0, 0, 0);
+            }
         }
     };
     auto store = [&]() {
         double d[8];
-        bf16x8_to_f64(xr, d);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) xs[(xc + j) * kXsPitch + xt] = d[j];
+        for (int j = 0; j < kXV; ++j) {
+            const int v = tid + j * nthr;
+            if (v < n_xv) {
+                const int t = v & 31, cc = (v >> 5) * 8;
+                bf16x8_to_f64(xr[j], d);
 #pragma unroll
-        for (int i = 0; i < kMaxExperts * (kChunk / 8) / kRouterThreads; ++i) {
-            const int v = tid + kRouterThreads * i;
-            if (v < nwv) {
-                bf16x8_to_f64(wv[i], d);
+                for (int q = 0; q < 8; ++q) xs[(cc + q) * kXsPitch + t] = d[q];
+            }
+        }
 #pragma unroll
-                for (int j = 0; j < 8; ++j) ws[(v >> 3) * kChunk + (v & 7) * 8 + j] = d[j];
+        for (int j = 0; j < kWV; ++j) {
+            const int v = tid + j * nthr;
+            if (v < n_wv) {
+                const int e = v % ne_pad, cc = (v / ne_pad) * 8;
+                bf16x8_to_f64(wv[j], d);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) ws[(cc + q) * ne_pad + e] = d[q];
             }
         }
     };
 
     load(0);
+    const double* wbase = ws + warp * EPT;
     for (int c0 = 0; c0 < h; c0 += kChunk) {
         store();
         __syncthreads();
@@ -102,32 +127,35 @@ router_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
 #pragma unroll 8
         for (int c = 0; c < kChunk; ++c) {
             const double xv = xs[c * kXsPitch + lane];
+            if constexpr (EPT == 1) {
+                acc[0] = fma(xv, wbase[c * ne_pad], acc[0]);
+            } else {
+                const double2* w2 = reinterpret_cast<const double2*>(wbase + c * ne_pad);
 #pragma unroll
-            for (int i = 0; i < EPT; ++i) {
-                const int e = warp + 8 * i;
-                if (e < ne) acc[i] = fma(xv, ws[e * kChunk + c], acc[i]);
+                for (int i = 0; i < EPT / 2; ++i) {
+                    const double2 w = w2[i];
+                    acc[2 * i] = fma(xv, w.x, acc[2 * i]);
+                    acc[2 * i + 1] = fma(xv, w.y, acc[2 * i + 1]);
+                }
             }
         }
         __syncthreads();
     }
-    // logits -> shared [32][ne]
-    double* lg = dyn;
+    // logits -> shared [32][ne_pad]
+    double* lg = ws;
 #pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-        const int e = warp + 8 * i;
-        if (e < ne) lg[lane * ne + e] = acc[i];
-    }
+    for (int i = 0; i < EPT; ++i) lg[lane * ne_pad + warp * EPT + i] = acc[i];
     __syncthreads();
 
-    // warp-shuffle top-k: warp w handles tokens w, w+8, w+16, w+24 of the tile
-    for (int tt = warp; tt < kRouteTile; tt += 8) {
+    // warp-shuffle top-k: warp w handles tokens w, w+nw, ... of the tile
+    for (int tt = warp; tt < kRouteTile; tt += nw) {
         const int t = t0 + tt;
         if (t >= T) break;
         double v[kMaxExperts / 32];
 #pragma unroll
         for (int i = 0; i < kMaxExperts / 32; ++i) {
             const int e = lane + 32 * i;
-            v[i] = (e < ne) ? lg[tt * ne + e] : 0.0;
+            v[i] = (e < ne) ? lg[tt * ne_pad + e] : 0.0;
         }
         uint32_t taken = 0;
         double sel_l[kMaxTopK];
@@ -192,7 +220,7 @@ router_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
         }
     }
     __syncthreads();
-    for (int e = tid; e < ne; e += kRouterThreads) tile_counts[(size_t)blockIdx.x * ne + e] = cnt[e];
+    for (int e = tid; e < ne; e += nthr) tile_counts[(size_t)blockIdx.x * ne + e] = cnt[e];
 }
 
 // Single block of 1024 threads.  Warp w scans experts w, w+32, ... over the tiles.
@@ -355,23 +383,25 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
                                int32_t* tile_counts, cudaStream_t st) {
     const int n_tiles = (T + kRouteTile - 1) / kRouteTile;
     if (n_tiles == 0) return cudaSuccess;
-    const size_t dyn = sizeof(double) * (size_t)ne * kChunk;  // >= 32 * ne doubles (logits too)
-    const int ept = (ne + 7) / 8;
+    // EPT experts per warp: few experts -> fewer per warp, so a 32-token tile still spreads over
+    // several warps (C1's 4096 tokens are only 128 tiles); many experts -> 8 per warp (16 regs
+    // of accumulators, 1 x load per 8 DFMAs).
+    const int ept = ne <= 8 ? 1 : (ne <= 16 ? 2 : 8);
+    const int nw = (ne + ept - 1) / ept;
+    const int ne_pad = nw * ept;
+    const size_t dyn = sizeof(double) * (size_t)(kChunk * kXsPitch + kChunk * ne_pad);
+    const int smem_max = (int)(sizeof(double) * (kChunk * kXsPitch + kChunk * kMaxExperts));
 #define MOE_ROUTER(E)                                                                        \
     do {                                                                                     \
         cudaError_t e_ = cudaFuncSetAttribute(router_topk_kernel<E>,                         \
-            cudaFuncAttributeMaxDynamicSharedMemorySize,                                     \
-            (int)(sizeof(double) * kMaxExperts * kChunk));                                   \
+            cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);                          \
         if (e_ != cudaSuccess) return e_;                                                    \
-        router_topk_kernel<E><<<n_tiles, kRouterThreads, dyn, st>>>(x, T, h, wr, ne, k,      \
-                                                                     renorm, idx, gates,     \
-                                                                     tile_counts);           \
+        router_topk_kernel<E><<<n_tiles, nw * 32, dyn, st>>>(x, T, h, wr, ne, k, renorm, idx, \
+                                                              gates, tile_counts);           \
     } while (0)
-    if (ept <= 1) MOE_ROUTER(1);
-    else if (ept <= 2) MOE_ROUTER(2);
-    else if (ept <= 4) MOE_ROUTER(4);
-    else if (ept <= 8) MOE_ROUTER(8);
-    else MOE_ROUTER(16);
+    if (ept == 1) MOE_ROUTER(1);
+    else if (ept == 2) MOE_ROUTER(2);
+    else MOE_ROUTER(8);
 #undef MOE_ROUTER
     return cudaGetLastError();
 }

@@ -4,7 +4,7 @@ sys.path.insert(0, ".")
 import synth
 import paper_2504_09345_b200 as moe
 cfg = synth.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "mixtral_8x7b"]
-T = int(sys.argv[2]) if len(sys.argv) > 2 else cfg.tokens
+T = int(sys.argv[2]) if len(sys.argv) > 2 and int(sys.argv[2]) > 0 else cfg.tokens
 calls = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 inp = synth.gen_inputs(cfg, tokens=T)
 ex = moe.HostExperts(cfg.hidden, cfg.ffn, inp.w1, inp.w3, inp.w2)
