@@ -155,6 +155,8 @@ typedef struct {
     double route_ms, permute_ms, gemm1_ms, gemm2_ms, combine_ms, comm_ms;
     int64_t num_slots;            /* expert staging slots in use                              */
     int64_t comm_bytes;           /* bytes this rank sent in EP dispatch + combine            */
+    int64_t host_calls;           /* moe_layer_forward_host calls                             */
+    double token_latency_ms;      /* sum over host calls: enqueue -> tokens resident on the GPU */
 } moe_stats;
 
 moe_status moe_get_stats(moe_ctx ctx, moe_stats* out);   /* synchronises the context */

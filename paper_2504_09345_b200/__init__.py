@@ -54,7 +54,8 @@ class moe_stats(ctypes.Structure):
                 ("route_ms", ctypes.c_double), ("permute_ms", ctypes.c_double),
                 ("gemm1_ms", ctypes.c_double), ("gemm2_ms", ctypes.c_double),
                 ("combine_ms", ctypes.c_double), ("comm_ms", ctypes.c_double),
-                ("num_slots", ctypes.c_int64), ("comm_bytes", ctypes.c_int64)]
+                ("num_slots", ctypes.c_int64), ("comm_bytes", ctypes.c_int64),
+                ("host_calls", ctypes.c_int64), ("token_latency_ms", ctypes.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -14,7 +14,7 @@
 namespace moe {
 
 enum RecKind { kRecH2D = 0, kRecRoute, kRecPermute, kRecGemm1, kRecGemm2, kRecCombine, kRecComm,
-               kRecKinds };
+               kRecTokenLatency, kRecKinds };
 
 struct Rec {
     int kind;
@@ -56,6 +56,14 @@ struct moe_ctx_s {
     int bn1 = 256, bn2 = 256;
     int64_t rows_cap = 0;  // rows of h_act / y_perm (single GPU)
     cudaStream_t copy_stream = nullptr;
+    // Token copies of moe_layer_forward_host ride the weight stream, just ahead of their call's
+    // weights (right for throughput).  MOE_TOKEN_LANE=1 puts them on a highest-priority stream
+    // instead -- measured NOT to help: DMAs are served in submission order across streams, so a
+    // priority lane needs host-paced packets (the paper's one-packet-in-flight mover,
+    // PAPER.md:829-835); see DESIGN.md §7.
+    cudaStream_t token_stream = nullptr;
+    cudaStream_t clock_stream = nullptr;  // idle stream: events on it timestamp enqueue time
+    bool token_lane = false;
 
     // staging slots (a bounded GPU weight buffer, recycled every call)
     int nslots = 2;

@@ -493,6 +493,14 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     auto dalloc = [&](void** p, size_t n) { return cudaMalloc(p, n) == cudaSuccess; };
     bool ok = true;
     ok &= cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) == cudaSuccess;
+    {
+        int least = 0, greatest = 0;
+        ok &= cudaDeviceGetStreamPriorityRange(&least, &greatest) == cudaSuccess;
+        ok &= cudaStreamCreateWithPriority(&c->token_stream, cudaStreamNonBlocking, greatest) ==
+              cudaSuccess;
+        ok &= cudaStreamCreateWithFlags(&c->clock_stream, cudaStreamNonBlocking) == cudaSuccess;
+        if (const char* e = getenv("MOE_TOKEN_LANE")) c->token_lane = atoi(e) != 0;
+    }
     ok &= dalloc((void**)&c->slot_base, (size_t)c->blob_bytes * c->nslots);
     for (int i = 0; i < c->nslots; ++i) {
         c->slot[i] = c->slot_base ? c->slot_base + (size_t)i * c->blob_bytes : nullptr;
@@ -602,11 +610,24 @@ moe_status moe_layer_forward_host(moe_ctx ctx, const void* hidden_host, int32_t 
     }
     const int b = c->host_parity;
     c->host_parity ^= 1;
-    // tokens ride the copy stream ahead of this call's expert weights
-    MOE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->xbuf_free[b], 0));
-    MOE_CUDA(c, cudaMemcpyAsync(c->x_dev[b], hidden_host, bytes, cudaMemcpyHostToDevice, c->copy_stream));
-    MOE_CUDA(c, cudaEventRecord(c->x_ready[b], c->copy_stream));
+    // Tokens go on the weight stream ahead of this call's weights (see engine.h token_lane).
+    cudaStream_t ts = c->token_lane ? c->token_stream : c->copy_stream;
+    cudaEvent_t t0 = nullptr;
+    const bool prof = (c->cfg.flags & MOE_FLAG_PROFILE) != 0;
+    if (prof) {  // enqueue-time stamp: the clock stream is always idle
+        t0 = moe::pool_get(c);
+        MOE_CUDA(c, cudaEventRecord(t0, c->clock_stream));
+    }
+    MOE_CUDA(c, cudaStreamWaitEvent(ts, c->xbuf_free[b], 0));
+    MOE_CUDA(c, cudaMemcpyAsync(c->x_dev[b], hidden_host, bytes, cudaMemcpyHostToDevice, ts));
+    MOE_CUDA(c, cudaEventRecord(c->x_ready[b], ts));
+    if (prof) {
+        cudaEvent_t t1 = moe::pool_get(c);
+        MOE_CUDA(c, cudaEventRecord(t1, ts));
+        c->pending.push_back(moe::Rec{moe::kRecTokenLatency, t0, t1});
+    }
     c->stats.h2d_token_bytes += (int64_t)bytes;
+    c->stats.host_calls += 1;
     s = forward_impl(c, c->x_dev[b], num_tokens, static_cast<const __nv_bfloat16*>(router_w),
                      experts, c->out_dev[b], topk_idx, topk_w, st, true, b);
     if (s != MOE_OK) return s;
@@ -637,7 +658,7 @@ moe_status moe_get_stats(moe_ctx ctx, moe_stats* out) {
     if (s != MOE_OK) return s;
     double* bucket[moe::kRecKinds] = {&ctx->stats.h2d_ms,   &ctx->stats.route_ms,   &ctx->stats.permute_ms,
                                       &ctx->stats.gemm1_ms, &ctx->stats.gemm2_ms,   &ctx->stats.combine_ms,
-                                      &ctx->stats.comm_ms};
+                                      &ctx->stats.comm_ms,  &ctx->stats.token_latency_ms};
     for (const moe::Rec& r : ctx->pending) {
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) *bucket[r.kind] += ms;
@@ -699,6 +720,8 @@ moe_status moe_destroy(moe_ctx c) {
                     c->grp1, c->grp2, c->pos, c->x_perm, c->h_act, c->y_perm};
     for (void* p : bufs) cudaFree(p);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->token_stream) cudaStreamDestroy(c->token_stream);
+    if (c->clock_stream) cudaStreamDestroy(c->clock_stream);
     cudaGetLastError();
     delete c;
     return MOE_OK;

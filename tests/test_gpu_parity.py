@@ -148,6 +148,36 @@ def test_host_buffer_entry_point_matches_device():
     run.close()
 
 
+@pytest.mark.parametrize("lane,packet_mb", [("0", 0), ("0", 8), ("1", 8)])
+def test_token_copy_latency_stat(lane, packet_mb, monkeypatch):
+    """The enqueue -> resident latency of host tokens is measured (MOE_FLAG_PROFILE) for the
+    default placement (weight stream) and the experimental priority stream; outputs are
+    identical either way.  Measured: stream priority does not reorder DMAs, so
+    the second call's tokens wait for the first call's weight copies in both placements."""
+    monkeypatch.setenv("MOE_TOKEN_LANE", lane)
+    cfg = synth.MoEConfig("custom", 18, 1024, 4096, 8, 2, 512)   # 25 MB experts: ~3.6 ms/call
+    inp = synth.gen_inputs(cfg)
+    run = GpuRun(inp, profile=True, packet_bytes=packet_mb << 20)
+    out_dev, _, _ = run.run()
+    xh = torch.from_numpy(inp.x.view(np.int16)).view(torch.bfloat16).pin_memory()
+    # two calls back to back (the library double-buffers host-mode tokens, so a third call would
+    # also wait for a free token buffer): call 2's tokens are enqueued behind call 1's weights
+    oh = [torch.empty_like(xh).pin_memory() for _ in range(2)]
+    s = torch.cuda.current_stream()
+    run.layer.reset_stats()
+    for o in oh:
+        run.layer.forward_host(xh, run.router, run.experts, o, stream=s.cuda_stream)
+    s.synchronize()
+    st = run.layer.stats()
+    for o in oh:
+        assert torch.equal(o, out_dev.cpu())
+    lat = st["token_latency_ms"] / st["host_calls"]
+    print(f"lane={lane} packet={packet_mb}MB: mean enqueue->resident token latency {lat:.3f} ms "
+          f"over {st['host_calls']} calls")
+    assert st["host_calls"] == 2 and 0.0 < lat < 50.0
+    run.close()
+
+
 def test_invalid_arguments():
     inp = synth.gen_inputs(synth.CONFIGS["tiny"])
     run = GpuRun(inp)
