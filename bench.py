@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--taskb", action="store_true",
+                    help="time GPU Task B (O-projection + RMSNorm + MoE layer, streamed Wo) "
+                         "instead of the MoE layer alone (no e2e / cpu legs)")
     return ap.parse_args()
 
 
@@ -239,9 +242,24 @@ def run_ours(args):
                          nccl_unique_id=uid, num_slots=args.slots)
     stream = torch.cuda.Stream()
     sh = stream.cuda_stream
+    layer_bytes = 0
+    if args.taskb:   # GPU Task B: per layer a streamed Wo + gamma blob, attention output, residual
+        args.no_e2e = args.no_cpu = True
+        tbs = [synth.gen_taskb(cfg, l.x, layer=i) for i, l in enumerate(layers)]
+        hls = [moe.HostLayer(cfg.hidden, tb.wo, tb.gamma) for tb in tbs]
+        layer_bytes = hls[0].nbytes
+
+        def _dev(bits):
+            return torch.from_numpy(np.ascontiguousarray(bits[rank * Tr:(rank + 1) * Tr]).view(np.int16)).view(torch.bfloat16).cuda()
+        attns = [_dev(tb.attn) for tb in tbs]
+        resids = [_dev(tb.resid) for tb in tbs]
 
     def step(i):
         l = i % args.layers
+        if args.taskb:
+            layer.taskb_forward(attns[l], resids[l], hls[l], tbs[l].eps, routers[l], experts[l],
+                                outs[l], idxs[l], gws[l], stream=sh)
+            return
         layer.forward(xs[l], routers[l], experts[l], outs[l], idxs[l], gws[l], stream=sh)
 
     def timed(fn, sampler=None):
@@ -281,9 +299,11 @@ def run_ours(args):
     hit = int((cnt > 0).sum().item())
     work = ledger.layer_work(T, cfg.hidden, cfg.ffn, cfg.num_experts, cfg.top_k, cfg.num_shared,
                              experts_hit=hit)
-    rank_bytes = (nl + cfg.num_shared) * ledger.expert_bytes(cfg.hidden, cfg.ffn)
+    rank_bytes = (nl + cfg.num_shared) * ledger.expert_bytes(cfg.hidden, cfg.ffn) + layer_bytes
+    step_weight_bytes = work.weight_bytes + world * layer_bytes
+    oproj_flops = 2.0 * T * cfg.hidden * cfg.hidden if args.taskb else 0.0
     t_io = allmax(rank_bytes / (probe_gbs * 1e9))                  # slowest rank's host link
-    t_tc = work.expert_flops / world / (peaks["bf16_tflops_sustained"] * 1e12)
+    t_tc = (work.expert_flops + oproj_flops) / world / (peaks["bf16_tflops_sustained"] * 1e12)
     t_roof = max(t_io, t_tc)
     # dominant kernel: GEMM1 (+SwiGLU).  FLOPs per launch over all ranks / avg launch time.
     g1_ms, g1_n = allsum(st["gemm1_ms"]), allsum(st["gemm1_launches"])
@@ -316,14 +336,15 @@ def run_ours(args):
                      "host_link_probe_gbs_rank0": probe_gbs,
                      "host_link_probe_gbs_min": -allmax(-probe_gbs),
                      "h2d_achieved_gbs_in_copies_rank0": h2d_gbs,
-                     "h2d_aggregate_gbs_over_step": work.weight_bytes / (ms * 1e-3) / 1e9,
-                     "weight_bytes_per_step": work.weight_bytes,
+                     "h2d_aggregate_gbs_over_step": step_weight_bytes / (ms * 1e-3) / 1e9,
+                     "weight_bytes_per_step": step_weight_bytes,
                      "weight_bytes_per_rank": rank_bytes,
                      "expert_flops_per_step": work.expert_flops,
+                     "oproj_flops_per_step": oproj_flops,
                      "tensor_peak_tflops": peaks["bf16_tflops_sustained"]}
     per_kernel_ms = {k: st[k] / args.steps for k in
                      ("h2d_ms", "route_ms", "permute_ms", "gemm1_ms", "gemm2_ms", "combine_ms",
-                      "comm_ms")}
+                      "comm_ms", "oproj_ms", "norm_ms")}
     launches = allsum(st["kernel_launches"])
 
     # ---- e2e: host token buffers through moe_layer_forward_host (H2D tokens + D2H output)
@@ -355,7 +376,8 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded random bf16 weights/tokens shaped like the model)",
-            "config": {"workload": cfg.name, "tokens": T, "tokens_per_rank": Tr,
+            "config": {"workload": cfg.name + (" GPU Task B (O-proj + RMSNorm + MoE)" if args.taskb else ""),
+                       "tokens": T, "tokens_per_rank": Tr,
                        "hidden": cfg.hidden, "ffn": cfg.ffn, "experts": cfg.num_experts,
                        "experts_per_rank": nl, "top_k": cfg.top_k, "num_shared": cfg.num_shared,
                        "layers_cycled": args.layers, "staging_slots": st["num_slots"],
@@ -372,6 +394,9 @@ def run_ours(args):
     layer.close()
     for e in experts:
         e.close()
+    if args.taskb:
+        for hl in hls:
+            hl.close()
     if world > 1:
         dist.destroy_process_group()
 

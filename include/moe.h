@@ -139,6 +139,41 @@ moe_status moe_layer_forward_host(moe_ctx ctx, const void* hidden_host, int32_t 
                                   const void* router_w, const void* const* experts, int32_t top_k,
                                   void* out_host, int32_t* topk_idx, float* topk_w, void* stream);
 
+/*
+ * GPU Task B: "GPU Task B (GB), which includes the O projection and MoE
+ * layer, is applied to all tokens"; the layer-wise weights are streamed from host
+ * memory like the experts ("weights ... are placed in CPU memory ... transferred to the GPU
+ * layer by layer").  Around the two operations sits the standard pre-norm decoder
+ * block of the paper's models (Mixtral/DBRX; readings R19-R21):
+ *   h1 = bf16(resid + attn Wo^T)                     O-projection + residual (one rounding)
+ *   u  = RMSNorm(h1) * gamma                         post-attention norm (R21 arithmetic)
+ *   out = bf16(h1 + MoE(u))                          the MoE layer of moe_layer_forward + residual
+ *
+ * Packed layer blob (pinned host): Wo bf16 [h, h] row-major (nn.Linear out x in), then gamma
+ * bf16 [h]; moe_packed_layer_bytes(h) = 2h^2 + 2h bytes.
+ */
+int64_t moe_packed_layer_bytes(int32_t hidden);
+moe_status moe_pack_layer(int32_t hidden, const void* wo, const void* gamma, void* dst);
+
+/*
+ * One Task B over this rank's tokens, enqueued on `stream` (asynchronous, like
+ * moe_layer_forward; the two share the context's staging and must be issued in program order).
+ *   attn        device bf16 [T, h]: attention output (heads concatenated), the O-proj input.
+ *   resid       device bf16 [T, h]: residual stream entering the block's attention half.
+ *   layer       pinned host packed layer blob (above), streamed each call into one of two
+ *               device slots ahead of this call's expert weights.
+ *   eps         RMSNorm epsilon (>= 0, finite).
+ *   router_w, experts, top_k, topk_idx, topk_w: as moe_layer_forward (routing is on u).
+ *   out         device bf16 [T, h]; may alias attn and/or resid (both are consumed first).
+ * The intermediate h1 and u of the last call are exposed by moe_debug_buffers.
+ * Errors: MOE_E_INVAL, MOE_E_NOT_PINNED, MOE_E_NOMEM (first call allocates 2 layer slots and
+ * 2 x max_tokens x h bf16 of workspace), MOE_E_CUDA, MOE_E_NCCL.
+ */
+moe_status moe_taskb_forward(moe_ctx ctx, const void* attn, const void* resid, int32_t num_tokens,
+                             const void* layer, float eps, const void* router_w,
+                             const void* const* experts, int32_t top_k, void* out,
+                             int32_t* topk_idx, float* topk_w, void* stream);
+
 /* Block until all work of the context is done; returns the first pending async error. */
 moe_status moe_sync(moe_ctx ctx);
 
@@ -157,6 +192,8 @@ typedef struct {
     int64_t comm_bytes;           /* bytes this rank sent in EP dispatch + combine            */
     int64_t host_calls;           /* moe_layer_forward_host calls                             */
     double token_latency_ms;      /* sum over host calls: enqueue -> tokens resident on the GPU */
+    int64_t taskb_calls;          /* moe_taskb_forward calls (each also counts in `calls`)    */
+    double oproj_ms, norm_ms;     /* Task B: O-projection GEMM, RMSNorm                       */
 } moe_stats;
 
 moe_status moe_get_stats(moe_ctx ctx, moe_stats* out);   /* synchronises the context */
@@ -171,6 +208,9 @@ typedef struct {
     const void* h_act;          /* bf16 [rows, h_i] silu(W1 x) * W3 x                         */
     const void* y_perm;         /* bf16 [rows, h]  gate-scaled expert outputs                 */
     int64_t rows;               /* rows used by the last call                                 */
+    const void* h1;             /* bf16 [T, h] Task B: residual stream after the O-projection */
+    const void* moe_in;         /* bf16 [T, h] Task B: RMSNorm output u (the MoE input)       */
+    int64_t taskb_tokens;       /* T of the last moe_taskb_forward (-1: none yet)             */
 } moe_debug_view;
 moe_status moe_debug_buffers(moe_ctx ctx, moe_debug_view* out);
 

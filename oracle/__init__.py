@@ -11,6 +11,9 @@ Parity status of each function:
   topk_gates     -- pinned (subset enumeration, rank-count definition, ties, 2-expert sigmoid)
   expert_ffn     -- pinned (torch fp64 textbook SwiGLU, W2=0, linearity)
   forward        -- pinned (dense equivalence, k=N_e mixture, permutation equivariance, shared experts)
+  oproj_residual -- pinned (Wo = 0 / I, one-hot columns, fp64 brute force; tests/test_oracle_taskb.py)
+  rmsnorm        -- pinned (constant rows, power-of-2 scale invariance, gamma scaling, fp64 formula)
+  taskb_forward  -- pinned (W2 = 0 -> y = h1, composition of the pinned steps)
 """
 from __future__ import annotations
 
@@ -139,3 +142,58 @@ def forward(x, router, w1, w3, w2, top_k: int, n_shared: int = 0, renormalize: b
     if want_logits:
         return y, idx, gates, logits
     return y, idx, gates
+
+
+# ----------------------------------------------------------------------------- GPU Task B
+def _load_taskb():
+    lib = _load()
+    if not getattr(lib, "_taskb_ready", False):
+        P, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+        lib.moe_ref_oproj_residual.argtypes = [P, P, i64, i32, P, P]
+        lib.moe_ref_rmsnorm.argtypes = [P, i64, i32, P, ctypes.c_float, P]
+        lib.moe_ref_taskb_forward.argtypes = [P, P, i64, i32, P, P, ctypes.c_float, P, i32, i32,
+                                              i32, P, P, P, i32, i32, P, P, P, P, P]
+        lib.moe_ref_taskb_forward.restype = ctypes.c_int
+        lib._taskb_ready = True
+    return lib
+
+
+def oproj_residual(attn, resid, wo) -> np.ndarray:
+    """b1 (readings R19/R20): h1 = bf16(resid + attn Wo^T), bf16 bits [T, h]."""
+    attn, resid, wo = _u16(attn), _u16(resid), _u16(wo)
+    T, h = attn.shape
+    h1 = np.empty((T, h), dtype=np.uint16)
+    _load_taskb().moe_ref_oproj_residual(_ptr(attn), _ptr(resid), T, h, _ptr(wo), _ptr(h1))
+    return h1
+
+
+def rmsnorm(h1, gamma, eps: float) -> np.ndarray:
+    """b2 (reading R21): u = bf16(gamma * bf16(h1 / sqrt(mean(h1^2) + eps))), bf16 bits."""
+    h1, gamma = _u16(h1), _u16(gamma)
+    T, h = h1.shape
+    u = np.empty((T, h), dtype=np.uint16)
+    _load_taskb().moe_ref_rmsnorm(_ptr(h1), T, h, _ptr(gamma), eps, _ptr(u))
+    return u
+
+
+def taskb_forward(attn, resid, wo, gamma, eps: float, router, w1, w3, w2, top_k: int,
+                  n_shared: int = 0, renormalize: bool = True):
+    """GPU Task B.  Returns (y fp32 [T,h], h1 bf16 bits, u bf16 bits, idx, gates)."""
+    attn, resid, wo, gamma, router = _u16(attn), _u16(resid), _u16(wo), _u16(gamma), _u16(router)
+    T, h = attn.shape
+    ne = router.shape[0]
+    ffn = w1[0].shape[0]
+    w1, w3, w2 = [_u16(m) for m in w1], [_u16(m) for m in w3], [_u16(m) for m in w2]
+    h1 = np.empty((T, h), dtype=np.uint16)
+    u = np.empty((T, h), dtype=np.uint16)
+    y = np.empty((T, h), dtype=np.float32)
+    idx = np.empty((T, top_k), dtype=np.int32)
+    gates = np.empty((T, top_k), dtype=np.float32)
+    p1, p3, p2 = _ptr_array(w1), _ptr_array(w3), _ptr_array(w2)
+    rc = _load_taskb().moe_ref_taskb_forward(
+        _ptr(attn), _ptr(resid), T, h, _ptr(wo), _ptr(gamma), eps, _ptr(router), ne, top_k,
+        int(renormalize), ctypes.addressof(p1), ctypes.addressof(p3), ctypes.addressof(p2), ffn,
+        n_shared, _ptr(h1), _ptr(u), _ptr(y), _ptr(idx), _ptr(gates))
+    if rc != 0:
+        raise ValueError(f"moe_ref_taskb_forward: invalid arguments (rc={rc})")
+    return y, h1, u, idx, gates

@@ -171,3 +171,78 @@ int moe_ref_forward(const uint16_t* x, int64_t T, int32_t h, const uint16_t* rou
     if (!logits) free(l);
     return 0;
 }
+
+/* ------------------------------------------------------------------------------------------
+ * GPU Task B ("GPU Task B (GB), which includes the O projection and MoE layer, is
+ * applied to all tokens").  Between the two the standard pre-norm decoder block of the paper's
+ * models (Mixtral, DBRX) has a residual add and the post-attention RMSNorm; DESIGN.md readings:
+ *   R19  h1 = resid + attn Wo^T (Wo [h, h], nn.Linear out x in); y = h1 + MoE(u).
+ *   R20  h1 is stored as bf16 (the model's residual stream dtype), rounded once:
+ *        h1 = bf16(float(sum_i attn[t,i] Wo[c,i] + resid[t,c])), the sum in fp64, ascending i.
+ *   R21  u = RMSNorm(h1) * gamma:  r = 1 / sqrt(sum_c h1^2 / h + eps) (fp64, ascending c),
+ *        n = bf16(float(h1 * r)),  u = bf16(float(gamma) * float(n))  (fp32 multiply).
+ * bf16 rounding is round-to-nearest-even (NaN kept quiet).
+ * ------------------------------------------------------------------------------------------ */
+static uint16_t f32_to_bf16(float f) {
+    uint32_t u;
+    memcpy(&u, &f, sizeof u);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)((u >> 16) | 0x40u); /* NaN */
+    const uint32_t lsb = (u >> 16) & 1u;
+    u += 0x7fffu + lsb;
+    return (uint16_t)(u >> 16);
+}
+
+/* b1 (R19, R20).  attn, resid, h1: [T, h] bf16 bits; wo: [h, h] bf16 bits. */
+void moe_ref_oproj_residual(const uint16_t* attn, const uint16_t* resid, int64_t T, int32_t h,
+                            const uint16_t* wo, uint16_t* h1) {
+    int64_t t;
+#pragma omp parallel for schedule(static)
+    for (t = 0; t < T; ++t) {
+        for (int32_t c = 0; c < h; ++c) {
+            double acc = 0.0;
+            for (int32_t i = 0; i < h; ++i)
+                acc += (double)bf16_to_f32(attn[t * h + i]) * (double)bf16_to_f32(wo[(int64_t)c * h + i]);
+            acc += (double)bf16_to_f32(resid[t * h + c]);
+            h1[t * h + c] = f32_to_bf16((float)acc);
+        }
+    }
+}
+
+/* b2 (R21).  h1, u: [T, h] bf16 bits; gamma: [h] bf16 bits. */
+void moe_ref_rmsnorm(const uint16_t* h1, int64_t T, int32_t h, const uint16_t* gamma, float eps,
+                     uint16_t* u) {
+    int64_t t;
+#pragma omp parallel for schedule(static)
+    for (t = 0; t < T; ++t) {
+        double ss = 0.0;
+        for (int32_t c = 0; c < h; ++c) {
+            const double x = (double)bf16_to_f32(h1[t * h + c]);
+            ss += x * x;
+        }
+        const double r = 1.0 / sqrt(ss / (double)h + (double)eps);
+        for (int32_t c = 0; c < h; ++c) {
+            const double x = (double)bf16_to_f32(h1[t * h + c]);
+            const float n = bf16_to_f32(f32_to_bf16((float)(x * r)));
+            u[t * h + c] = f32_to_bf16(bf16_to_f32(gamma[c]) * n);
+        }
+    }
+}
+
+/* The whole Task B: h1 (b1), u (b2), the MoE layer on u, y = float(h1) + MoE(u) (fp32).
+ * h1, u: [T, h] bf16 bits out; y: [T, h] fp32 out; idx/gates as moe_ref_forward. */
+int moe_ref_taskb_forward(const uint16_t* attn, const uint16_t* resid, int64_t T, int32_t h,
+                          const uint16_t* wo, const uint16_t* gamma, float eps,
+                          const uint16_t* router, int32_t n_experts, int32_t top_k,
+                          int32_t renormalize, const uint16_t* const* w1, const uint16_t* const* w3,
+                          const uint16_t* const* w2, int32_t ffn, int32_t n_shared, uint16_t* h1,
+                          uint16_t* u, float* y, int32_t* idx, float* gates) {
+    if (T < 0 || h <= 0 || !(eps >= 0.0f)) return 1;
+    if (T == 0) return 0;
+    moe_ref_oproj_residual(attn, resid, T, h, wo, h1);
+    moe_ref_rmsnorm(h1, T, h, gamma, eps, u);
+    int rc = moe_ref_forward(u, T, h, router, n_experts, top_k, renormalize, w1, w3, w2, ffn,
+                             n_shared, y, idx, gates, NULL);
+    if (rc != 0) return rc;
+    for (int64_t i = 0; i < T * (int64_t)h; ++i) y[i] = bf16_to_f32(h1[i]) + y[i];
+    return 0;
+}

@@ -33,7 +33,8 @@ MOE_FLAG_LOCAL_EP = 4
 EXPORTED = ["moe_packed_expert_bytes", "moe_pack_expert", "moe_host_alloc", "moe_host_free",
             "moe_init", "moe_layer_forward", "moe_layer_forward_host", "moe_sync", "moe_get_stats",
             "moe_reset_stats", "moe_debug_buffers", "moe_destroy", "moe_status_string",
-            "moe_last_error", "moe_probe_h2d", "moe_ep_plan", "moe_nccl_unique_id"]
+            "moe_last_error", "moe_probe_h2d", "moe_ep_plan", "moe_nccl_unique_id",
+            "moe_packed_layer_bytes", "moe_pack_layer", "moe_taskb_forward"]
 
 
 class moe_config(ctypes.Structure):
@@ -55,7 +56,9 @@ class moe_stats(ctypes.Structure):
                 ("gemm1_ms", ctypes.c_double), ("gemm2_ms", ctypes.c_double),
                 ("combine_ms", ctypes.c_double), ("comm_ms", ctypes.c_double),
                 ("num_slots", ctypes.c_int64), ("comm_bytes", ctypes.c_int64),
-                ("host_calls", ctypes.c_int64), ("token_latency_ms", ctypes.c_double)]
+                ("host_calls", ctypes.c_int64), ("token_latency_ms", ctypes.c_double),
+                ("taskb_calls", ctypes.c_int64), ("oproj_ms", ctypes.c_double),
+                ("norm_ms", ctypes.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -65,7 +68,8 @@ class moe_debug_view(ctypes.Structure):
     _fields_ = [("counts", ctypes.c_void_p), ("offsets", ctypes.c_void_p),
                 ("pos", ctypes.c_void_p), ("x_perm", ctypes.c_void_p),
                 ("h_act", ctypes.c_void_p), ("y_perm", ctypes.c_void_p),
-                ("rows", ctypes.c_int64)]
+                ("rows", ctypes.c_int64), ("h1", ctypes.c_void_p), ("moe_in", ctypes.c_void_p),
+                ("taskb_tokens", ctypes.c_int64)]
 
 
 class MoEError(RuntimeError):
@@ -108,9 +112,13 @@ def load(path: str = LIB_PATH):
     lib.moe_ep_plan.argtypes = [i32, i32, i32, P, P, P, P, P, P]
     lib.moe_ep_plan.restype = i64
     lib.moe_nccl_unique_id.argtypes = [P]
+    lib.moe_packed_layer_bytes.argtypes = [i32]
+    lib.moe_packed_layer_bytes.restype = i64
+    lib.moe_pack_layer.argtypes = [i32, P, P, P]
+    lib.moe_taskb_forward.argtypes = [P, P, P, i32, P, ctypes.c_float, P, P, i32, P, P, P, P]
     for name in EXPORTED:
         if name not in ("moe_packed_expert_bytes", "moe_status_string", "moe_last_error",
-                        "moe_ep_plan"):
+                        "moe_ep_plan", "moe_packed_layer_bytes"):
             getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -166,6 +174,24 @@ def moe_layer_forward_host(ctx: int, hidden_host: int, num_tokens: int, router_w
     _check(load().moe_layer_forward_host(ctx, hidden_host, num_tokens, router_w, experts, top_k,
                                          out_host, topk_idx or None, topk_w or None,
                                          stream or None), ctx)
+
+
+def moe_packed_layer_bytes(hidden: int) -> int:
+    return int(load().moe_packed_layer_bytes(hidden))
+
+
+def moe_pack_layer(hidden: int, wo: np.ndarray, gamma: np.ndarray, dst: int) -> None:
+    for a in (wo, gamma):
+        assert a.dtype == np.uint16 and a.flags.c_contiguous
+    _check(load().moe_pack_layer(hidden, wo.ctypes.data, gamma.ctypes.data, dst))
+
+
+def moe_taskb_forward(ctx: int, attn: int, resid: int, num_tokens: int, layer: int, eps: float,
+                      router_w: int, experts, top_k: int, out: int, topk_idx: int = 0,
+                      topk_w: int = 0, stream: int = 0) -> None:
+    _check(load().moe_taskb_forward(ctx, attn or None, resid or None, num_tokens, layer or None,
+                                    eps, router_w, experts, top_k, out or None, topk_idx or None,
+                                    topk_w or None, stream or None), ctx)
 
 
 def moe_sync(ctx: int) -> None:
@@ -268,6 +294,31 @@ class HostExperts:
             pass
 
 
+class HostLayer:
+    """Pinned, packed layer-wise weights of GPU Task B: Wo [h, h] then the RMSNorm gamma [h]."""
+
+    def __init__(self, hidden: int, wo: np.ndarray, gamma: np.ndarray):
+        self.hidden = hidden
+        self.nbytes = moe_packed_layer_bytes(hidden)
+        self.ptr = moe_host_alloc(self.nbytes)
+        try:
+            moe_pack_layer(hidden, np.ascontiguousarray(wo), np.ascontiguousarray(gamma), self.ptr)
+        except Exception:
+            self.close()
+            raise
+
+    def close(self):
+        if self.ptr:
+            moe_host_free(self.ptr)
+            self.ptr = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class MoELayer:
     """A context for one MoE layer shape on one device (see include/moe.h)."""
 
@@ -306,6 +357,16 @@ class MoELayer:
                                out_host.data_ptr(),
                                topk_idx.data_ptr() if topk_idx is not None else 0,
                                topk_w.data_ptr() if topk_w is not None else 0, stream)
+
+    def taskb_forward(self, attn, resid, layer: HostLayer, eps: float, router_w,
+                      experts: HostExperts, out, topk_idx=None, topk_w=None, stream: int = 0):
+        """GPU Task B: out = h1 + MoE(RMSNorm(h1)), h1 = resid + attn Wo^T (device tensors)."""
+        T = attn.shape[0]
+        moe_taskb_forward(self.ctx, attn.data_ptr() if T else 0, resid.data_ptr() if T else 0, T,
+                          layer.ptr, eps, router_w.data_ptr(), experts.array, self.top_k,
+                          out.data_ptr() if T else 0,
+                          topk_idx.data_ptr() if topk_idx is not None else 0,
+                          topk_w.data_ptr() if topk_w is not None else 0, stream)
 
     def sync(self):
         moe_sync(self.ctx)

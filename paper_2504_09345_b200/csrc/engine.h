@@ -14,7 +14,7 @@
 namespace moe {
 
 enum RecKind { kRecH2D = 0, kRecRoute, kRecPermute, kRecGemm1, kRecGemm2, kRecCombine, kRecComm,
-               kRecTokenLatency, kRecKinds };
+               kRecTokenLatency, kRecOproj, kRecNorm, kRecKinds };
 
 struct Rec {
     int kind;
@@ -113,6 +113,19 @@ struct moe_ctx_s {
     CUtensorMap tm_xrecv;
     std::vector<int32_t> send_off, send_cnt, recv_off, recv_cnt, grp_off;
     int64_t last_recv_rows = 0, comm_bytes = 0;
+
+    // GPU Task B (moe_taskb_forward; allocated on first use).  The layer weights (Wo + gamma,
+    // moe_packed_layer_bytes) are streamed like the experts, into two slots of their own, on the
+    // same copy stream just ahead of the call's expert weights.
+    int64_t layer_bytes = 0;
+    char* lw_slot[2] = {nullptr, nullptr};
+    cudaEvent_t lw_ready[2] = {}, lw_free[2] = {};
+    CUtensorMap tm_wo[2], tm_wo_pair[2];
+    uint64_t lw_seq = 0;
+    __nv_bfloat16* h1_ws = nullptr;   // [max_tokens, h] residual stream after the O-projection
+    __nv_bfloat16* u_ws = nullptr;    // [max_tokens, h] normalised MoE input
+    moe::GemmGroup* oproj_grp = nullptr;
+    int64_t last_taskb_T = -1;
 
     // host-buffer mode (moe_layer_forward_host)
     __nv_bfloat16* x_dev[2] = {nullptr, nullptr};

@@ -71,7 +71,7 @@ __device__ __forceinline__ float silu_mul(float g, float u) {
 // rows inside the group store.
 template <int BN, int MODE>
 __device__ __forceinline__ void epilogue_row(uint32_t taddr, bool valid, __nv_bfloat16* row_out,
-                                             int n) {
+                                             const __nv_bfloat16* row_res, int n) {
     if (MODE == kGemmSwiGLU) {
         __nv_bfloat16* dst = row_out + (int64_t)n * (BN / 2);
 #pragma unroll 1
@@ -101,6 +101,21 @@ __device__ __forceinline__ void epilogue_row(uint32_t taddr, bool valid, __nv_bf
             ptx::tmem_ld_32x32b_x32(taddr + c, v);
             ptx::tmem_ld_wait();
             if (valid) {
+                if (MODE == kGemmResidual) {  // + residual row, one rounding (reading R20)
+                    const __nv_bfloat16* src = row_res + (int64_t)n * BN + c;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int4 r = ptx::ld_nc_v4(src + 8 * i);
+                        const uint32_t rw[4] = {(uint32_t)r.x, (uint32_t)r.y, (uint32_t)r.z, (uint32_t)r.w};
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            v[8 * i + 2 * j] = __float_as_uint(__uint_as_float(v[8 * i + 2 * j]) +
+                                                               __uint_as_float(rw[j] << 16));
+                            v[8 * i + 2 * j + 1] = __float_as_uint(
+                                __uint_as_float(v[8 * i + 2 * j + 1]) + __uint_as_float(rw[j] & 0xffff0000u));
+                        }
+                    }
+                }
                 uint32_t pk[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i)
@@ -117,7 +132,8 @@ template <int BN, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 expert_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GemmGroup* __restrict__ group, int N, int K,
-                   __nv_bfloat16* __restrict__ out, int ldo) {
+                   __nv_bfloat16* __restrict__ out, int ldo,
+                   const __nv_bfloat16* __restrict__ resid) {
     using C = GemmCfg<BN>;
     constexpr int S = C::kStages;
     extern __shared__ uint8_t smem_raw[];
@@ -240,7 +256,8 @@ expert_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
             const bool valid = arow < g.a_end;
             const int64_t orow = (int64_t)g.out_base + (arow - g.a_begin);
             const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-            epilogue_row<BN, MODE>(taddr, valid, out + orow * ldo, n);
+            epilogue_row<BN, MODE>(taddr, valid, out + orow * ldo,
+                                   resid ? resid + orow * ldo : nullptr, n);
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
@@ -272,7 +289,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 expert_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
                         const GemmGroup* __restrict__ group, int N, int K,
-                        __nv_bfloat16* __restrict__ out, int ldo) {
+                        __nv_bfloat16* __restrict__ out, int ldo,
+                   const __nv_bfloat16* __restrict__ resid) {
     constexpr int BN = 256, PM = 256, S = kPairStages;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -394,7 +412,8 @@ expert_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
             const bool valid = arow < g.a_end;
             const int64_t orow = (int64_t)g.out_base + (arow - g.a_begin);
             const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-            epilogue_row<BN, MODE>(taddr, valid, out + orow * ldo, n);
+            epilogue_row<BN, MODE>(taddr, valid, out + orow * ldo,
+                                   resid ? resid + orow * ldo : nullptr, n);
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_cluster(tempty0 + acc * 8);
@@ -410,7 +429,8 @@ expert_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
 
 template <int MODE>
 cudaError_t launch_pair(const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmGroup* group,
-                        int N, int K, __nv_bfloat16* out, int ldo, int grid, cudaStream_t st) {
+                        int N, int K, __nv_bfloat16* out, int ldo, const __nv_bfloat16* resid,
+                        int grid, cudaStream_t st) {
     // Set on every launch: the attribute is per device context, contexts may be driven from
     // several host threads (MOE_FLAG_LOCAL_EP), and the call is a cheap host-side update.
     cudaError_t e = cudaFuncSetAttribute(expert_gemm_pair_kernel<MODE>,
@@ -418,19 +438,20 @@ cudaError_t launch_pair(const CUtensorMap* tmA, const CUtensorMap* tmB, const Ge
                                          (int)kPairSmem);
     if (e != cudaSuccess) return e;
     expert_gemm_pair_kernel<MODE><<<grid & ~1, kThreads, kPairSmem, st>>>(*tmA, *tmB, group, N, K,
-                                                                          out, ldo);
+                                                                          out, ldo, resid);
     return cudaGetLastError();
 }
 
 template <int BN, int MODE>
 cudaError_t launch_one(const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmGroup* group,
-                       int N, int K, __nv_bfloat16* out, int ldo, int grid, cudaStream_t st) {
+                       int N, int K, __nv_bfloat16* out, int ldo, const __nv_bfloat16* resid,
+                        int grid, cudaStream_t st) {
     using C = GemmCfg<BN>;
     cudaError_t e = cudaFuncSetAttribute(expert_gemm_kernel<BN, MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)C::kSmem);   // every launch, see launch_pair
     if (e != cudaSuccess) return e;
-    expert_gemm_kernel<BN, MODE><<<grid, kThreads, C::kSmem, st>>>(*tmA, *tmB, group, N, K, out, ldo);
+    expert_gemm_kernel<BN, MODE><<<grid, kThreads, C::kSmem, st>>>(*tmA, *tmB, group, N, K, out, ldo, resid);
     return cudaGetLastError();
 }
 
@@ -445,17 +466,23 @@ int gemm_bn_for(int mode, int N) {
 
 cudaError_t launch_expert_gemm(int mode, int bn, bool pair, const CUtensorMap* tmA,
                                const CUtensorMap* tmB, const GemmGroup* group, int N, int K,
-                               __nv_bfloat16* out, int ldo, int grid, cudaStream_t st) {
+                               __nv_bfloat16* out, int ldo, const __nv_bfloat16* resid, int grid,
+                               cudaStream_t st) {
+    if ((mode == kGemmResidual) != (resid != nullptr)) return cudaErrorInvalidValue;
     if (pair) {
         if (bn != 256) return cudaErrorInvalidValue;
-        if (mode == kGemmSwiGLU) return launch_pair<kGemmSwiGLU>(tmA, tmB, group, N, K, out, ldo, grid, st);
-        return launch_pair<kGemmPlain>(tmA, tmB, group, N, K, out, ldo, grid, st);
+        if (mode == kGemmSwiGLU) return launch_pair<kGemmSwiGLU>(tmA, tmB, group, N, K, out, ldo, resid, grid, st);
+        if (mode == kGemmResidual) return launch_pair<kGemmResidual>(tmA, tmB, group, N, K, out, ldo, resid, grid, st);
+        return launch_pair<kGemmPlain>(tmA, tmB, group, N, K, out, ldo, resid, grid, st);
     }
     if (mode == kGemmSwiGLU) {
-        if (bn == 256) return launch_one<256, kGemmSwiGLU>(tmA, tmB, group, N, K, out, ldo, grid, st);
+        if (bn == 256) return launch_one<256, kGemmSwiGLU>(tmA, tmB, group, N, K, out, ldo, resid, grid, st);
+    } else if (mode == kGemmResidual) {
+        if (bn == 256) return launch_one<256, kGemmResidual>(tmA, tmB, group, N, K, out, ldo, resid, grid, st);
+        if (bn == 128) return launch_one<128, kGemmResidual>(tmA, tmB, group, N, K, out, ldo, resid, grid, st);
     } else {
-        if (bn == 256) return launch_one<256, kGemmPlain>(tmA, tmB, group, N, K, out, ldo, grid, st);
-        if (bn == 128) return launch_one<128, kGemmPlain>(tmA, tmB, group, N, K, out, ldo, grid, st);
+        if (bn == 256) return launch_one<256, kGemmPlain>(tmA, tmB, group, N, K, out, ldo, resid, grid, st);
+        if (bn == 128) return launch_one<128, kGemmPlain>(tmA, tmB, group, N, K, out, ldo, resid, grid, st);
     }
     return cudaErrorInvalidValue;
 }

@@ -13,6 +13,7 @@
 //     across experts AND across calls (cross-call prefetch of the next layer's first experts).
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstring>
 #include <mutex>
 
@@ -239,9 +240,27 @@ moe_status request_copy(moe_ctx c, const void* const* experts, int i, uint64_t q
     return MOE_OK;
 }
 
+// Tile shape of one GEMM launch of `rows` expected rows and N output columns: the CTA-pair kernel
+// (256x256 tiles on SM pairs, ~97% tensor-pipe activity) or the single-CTA kernel (128x256, ~76%:
+// shared-memory bandwidth bound, but half the M granularity and twice the concurrent tiles),
+// by a wave model: time ~ ceil(tiles / concurrent tiles) / tensor efficiency.
+bool pick_pair(moe_ctx c, int64_t rows, int bn, int N) {
+    if (bn != 256 || c->pair_mode == 0) return false;
+    if (c->pair_mode == 1) return true;
+    if (rows <= 0) return false;
+    const int sms = c->num_sms;
+    const int64_t nt = N / 256;
+    const int64_t t1 = ((rows + 127) / 128) * nt, t2 = ((rows + 255) / 256) * nt;
+    const double w1 = (double)((t1 + sms - 1) / sms) / 0.76;
+    const double w2 = (double)((t2 + sms / 2 - 1) / (sms / 2)) / 0.97;
+    return w2 < w1;
+}
+
+// resid (Task B): added to every output row in the combine (nullptr for the plain MoE layer).
 moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __nv_bfloat16* wr,
                         const void* const* experts, __nv_bfloat16* out, int32_t* topk_idx,
-                        float* topk_w, cudaStream_t st, bool hidden_on_copy_stream, int xb) {
+                        float* topk_w, cudaStream_t st, bool hidden_on_copy_stream, int xb,
+                        const __nv_bfloat16* resid = nullptr) {
     const moe_config& cf = c->cfg;
     const int h = cf.hidden, hi = cf.ffn, ne = cf.num_experts, k = cf.top_k, S = cf.num_shared;
     const int n_tiles = (T + moe::kRouteTile - 1) / moe::kRouteTile;
@@ -303,24 +322,12 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     }
 
     const int grid = c->num_sms;
-    // Tile shape per launch: the CTA-pair kernel (256x256 tiles on SM pairs, ~97% tensor-pipe
-    // activity) or the single-CTA kernel (128x256, ~76%: shared-memory bandwidth bound, but half
-    // the M granularity and twice the concurrent tiles).  The host does not know the group sizes
-    // (they live on the device), so it decides on the expected size -- T*k*W/N_e rows per routed
-    // expert (+10% for routing variance), T per shared expert -- with a wave model:
-    //   time ~ ceil(tiles / concurrent tiles) / tensor efficiency.
+    // The host does not know the group sizes (they live on the device), so the tile shape is
+    // chosen on the expected size: T*k*W/N_e rows per routed expert (+10% for routing
+    // variance), T per shared expert.
     const int64_t exp_routed = (int64_t)T * k * cf.world_size / ne;
-    const int sms = c->num_sms;
     auto use_pair = [&](bool shared, int bn, int N) {
-        if (bn != 256 || c->pair_mode == 0) return false;
-        if (c->pair_mode == 1) return true;
-        const int64_t rows = shared ? (int64_t)T : exp_routed + exp_routed / 10;
-        if (rows <= 0) return false;
-        const int64_t nt = N / 256;
-        const int64_t t1 = ((rows + 127) / 128) * nt, t2 = ((rows + 255) / 256) * nt;
-        const double w1 = (double)((t1 + sms - 1) / sms) / 0.76;
-        const double w2 = (double)((t2 + sms / 2 - 1) / (sms / 2)) / 0.97;
-        return w2 < w1;
+        return pick_pair(c, shared ? (int64_t)T : exp_routed + exp_routed / 10, bn, N);
     };
     for (int i = 0; i < c->n_all; ++i) {
         const uint64_t q = q0 + i;
@@ -338,7 +345,7 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
             MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmSwiGLU, c->bn1, pr,
                                                 shared ? &tm_x : tmA_routed,
                                                 pr ? &c->tm_w13_pair[s] : &c->tm_w13[s], g1 + e,
-                                                2 * hi, h, c->h_act, hi, grid, st));
+                                                2 * hi, h, c->h_act, hi, nullptr, grid, st));
             p.end();
         }
         MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready2[s], 0));
@@ -347,7 +354,8 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
             const bool pr = use_pair(shared, c->bn2, h);
             MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmPlain, c->bn2, pr, &c->tm_h,
                                                 pr ? &c->tm_w2_pair[s] : &c->tm_w2[s], g2 + e, h,
-                                                hi, shared ? c->y_perm : y_routed, h, grid, st));
+                                                hi, shared ? c->y_perm : y_routed, h, nullptr,
+                                                grid, st));
             p.end();
         }
         c->stats.kernel_launches += 2;
@@ -371,7 +379,8 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     }
     {
         Prof p(c, moe::kRecCombine, st);
-        MOE_CUDA(c, moe::launch_combine(c->y_perm, c->pos, gates, T, h, k, S, (int64_t)T * k, out, st));
+        MOE_CUDA(c, moe::launch_combine(c->y_perm, c->pos, gates, T, h, k, S, (int64_t)T * k,
+                                        resid, out, st));
         p.end();
         c->stats.kernel_launches += 1;
     }
@@ -398,6 +407,91 @@ moe_status validate_call(moe_ctx c, int32_t T, const void* router_w, const void*
             return set_err(c, MOE_E_NOT_PINNED, "experts[%d] is not page-locked host memory", i);
     }
     return MOE_OK;
+}
+
+// Task B resources, allocated on the first moe_taskb_forward.
+moe_status taskb_resources(moe_ctx c) {
+    if (c->lw_slot[0]) return MOE_OK;
+    const int h = c->cfg.hidden;
+    const size_t act = (size_t)c->cfg.max_tokens * h * 2;
+    c->layer_bytes = moe_packed_layer_bytes(h);
+    bool ok = true;
+    for (int i = 0; i < 2; ++i) {
+        ok &= cudaMalloc((void**)&c->lw_slot[i], (size_t)c->layer_bytes) == cudaSuccess;
+        ok &= cudaEventCreateWithFlags(&c->lw_ready[i], cudaEventDisableTiming) == cudaSuccess;
+        ok &= cudaEventCreateWithFlags(&c->lw_free[i], cudaEventDisableTiming) == cudaSuccess;
+    }
+    ok &= cudaMalloc((void**)&c->h1_ws, act) == cudaSuccess;
+    ok &= cudaMalloc((void**)&c->u_ws, act) == cudaSuccess;
+    ok &= cudaMalloc((void**)&c->oproj_grp, sizeof(GemmGroup)) == cudaSuccess;
+    if (!ok) {
+        cudaGetLastError();
+        for (int i = 0; i < 2; ++i) {  // leave the context as it was (the next call retries)
+            cudaFree(c->lw_slot[i]);
+            c->lw_slot[i] = nullptr;
+        }
+        return set_err(c, MOE_E_NOMEM, "Task B buffers (2 x %lld B layer slots + 2 x %zu B)",
+                       (long long)c->layer_bytes, act);
+    }
+    bool tm = true;
+    for (int i = 0; i < 2; ++i) {  // Wo [h, h]: N = h output rows, K = h
+        tm &= moe::make_tmap(&c->tm_wo[i], c->lw_slot[i], (uint64_t)h, (uint64_t)h, (uint32_t)c->bn2);
+        tm &= moe::make_tmap(&c->tm_wo_pair[i], c->lw_slot[i], (uint64_t)h, (uint64_t)h, 128);
+    }
+    if (!tm) return set_err(c, MOE_E_CUDA, "cuTensorMapEncodeTiled failed for Wo");
+    return MOE_OK;
+}
+
+// b1 O-projection + residual, b2 RMSNorm, then the MoE layer on u with h1 as the combine's
+// residual (R19-R21).
+moe_status taskb_impl(moe_ctx c, const __nv_bfloat16* attn, const __nv_bfloat16* resid, int T,
+                      const void* layer, float eps, const __nv_bfloat16* wr,
+                      const void* const* experts, __nv_bfloat16* out, int32_t* topk_idx,
+                      float* topk_w, cudaStream_t st) {
+    const int h = c->cfg.hidden;
+    c->stats.taskb_calls += 1;
+    if (T == 0) {  // EP only: no local tokens, this rank still serves its experts
+        c->last_taskb_T = 0;
+        return forward_impl(c, nullptr, 0, wr, experts, nullptr, topk_idx, topk_w, st, false, 0);
+    }
+    CUtensorMap tm_attn;
+    if (!moe::make_tmap(&tm_attn, attn, (uint64_t)T, (uint64_t)h, 128))
+        return set_err(c, MOE_E_CUDA, "cuTensorMapEncodeTiled failed for attn");
+    // The layer weights ride the copy stream just ahead of this call's expert weights (nothing
+    // is pending between calls: forward_impl flushes at its end).
+    const int b = (int)(c->lw_seq & 1);
+    c->lw_seq += 1;
+    MOE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->lw_free[b], 0));
+    {
+        Prof p(c, moe::kRecH2D, c->copy_stream);
+        MOE_CUDA(c, cudaMemcpyAsync(c->lw_slot[b], layer, (size_t)c->layer_bytes,
+                                    cudaMemcpyHostToDevice, c->copy_stream));
+        p.end();
+    }
+    MOE_CUDA(c, cudaEventRecord(c->lw_ready[b], c->copy_stream));
+    c->stats.h2d_weight_bytes += c->layer_bytes;
+
+    MOE_CUDA(c, moe::launch_fill_group(c->oproj_grp, 0, T, 0, st));
+    MOE_CUDA(c, cudaStreamWaitEvent(st, c->lw_ready[b], 0));
+    {
+        Prof p(c, moe::kRecOproj, st);
+        const bool pr = pick_pair(c, T, c->bn2, h);
+        MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmResidual, c->bn2, pr, &tm_attn,
+                                            pr ? &c->tm_wo_pair[b] : &c->tm_wo[b], c->oproj_grp,
+                                            h, h, c->h1_ws, h, resid, c->num_sms, st));
+        p.end();
+    }
+    {
+        Prof p(c, moe::kRecNorm, st);
+        const __nv_bfloat16* gamma =
+            reinterpret_cast<const __nv_bfloat16*>(c->lw_slot[b] + 2ll * h * h);
+        MOE_CUDA(c, moe::launch_rmsnorm(c->h1_ws, gamma, T, h, eps, c->u_ws, st));
+        p.end();
+    }
+    MOE_CUDA(c, cudaEventRecord(c->lw_free[b], st));
+    c->stats.kernel_launches += 3;
+    c->last_taskb_T = T;
+    return forward_impl(c, c->u_ws, T, wr, experts, out, topk_idx, topk_w, st, false, 0, c->h1_ws);
 }
 
 }  // namespace
@@ -637,6 +731,49 @@ moe_status moe_layer_forward_host(moe_ctx ctx, const void* hidden_host, int32_t 
     return MOE_OK;
 }
 
+int64_t moe_packed_layer_bytes(int32_t hidden) {
+    if (hidden <= 0) return 0;
+    return 2ll * hidden * hidden + 2ll * hidden;
+}
+
+moe_status moe_pack_layer(int32_t hidden, const void* wo, const void* gamma, void* dst) {
+    if (!wo || !gamma || !dst || hidden <= 0) return MOE_E_INVAL;
+    const size_t wo_bytes = (size_t)hidden * hidden * 2;
+    memcpy(dst, wo, wo_bytes);
+    memcpy(static_cast<char*>(dst) + wo_bytes, gamma, (size_t)hidden * 2);
+    return MOE_OK;
+}
+
+moe_status moe_taskb_forward(moe_ctx ctx, const void* attn, const void* resid, int32_t num_tokens,
+                             const void* layer, float eps, const void* router_w,
+                             const void* const* experts, int32_t top_k, void* out,
+                             int32_t* topk_idx, float* topk_w, void* stream) {
+    moe_status s = validate_call(ctx, num_tokens, router_w, experts, top_k);
+    if (s != MOE_OK || (num_tokens == 0 && !ctx->ep)) return s;
+    if (!(eps >= 0.0f) || !std::isfinite(eps))
+        return set_err(ctx, MOE_E_INVAL, "eps must be finite and >= 0");
+    if (num_tokens > 0) {
+        if (!attn || !resid || !out || !layer)
+            return set_err(ctx, MOE_E_INVAL, "NULL attn / resid / out / layer");
+        if (((uintptr_t)attn | (uintptr_t)resid | (uintptr_t)out) & 15)
+            return set_err(ctx, MOE_E_INVAL, "attn/resid/out must be 16-byte aligned");
+        if (!is_device(attn) || !is_device(resid) || !is_device(out))
+            return set_err(ctx, MOE_E_INVAL, "attn/resid/out must be device memory");
+        if ((topk_idx && !is_device(topk_idx)) || (topk_w && !is_device(topk_w)))
+            return set_err(ctx, MOE_E_INVAL, "topk_idx/topk_w must be device memory");
+        if (!is_pinned(ctx, layer))
+            return set_err(ctx, MOE_E_NOT_PINNED, "layer blob is not page-locked host memory");
+    }
+    MOE_CUDA(ctx, cudaSetDevice(ctx->cfg.device));
+    s = taskb_resources(ctx);
+    if (s != MOE_OK) return s;
+    return taskb_impl(ctx, static_cast<const __nv_bfloat16*>(attn),
+                      static_cast<const __nv_bfloat16*>(resid), num_tokens, layer, eps,
+                      static_cast<const __nv_bfloat16*>(router_w), experts,
+                      static_cast<__nv_bfloat16*>(out), topk_idx, topk_w,
+                      static_cast<cudaStream_t>(stream));
+}
+
 moe_status moe_sync(moe_ctx ctx) {
     if (!ctx) return MOE_E_INVAL;
     MOE_CUDA(ctx, cudaSetDevice(ctx->cfg.device));
@@ -658,7 +795,8 @@ moe_status moe_get_stats(moe_ctx ctx, moe_stats* out) {
     if (s != MOE_OK) return s;
     double* bucket[moe::kRecKinds] = {&ctx->stats.h2d_ms,   &ctx->stats.route_ms,   &ctx->stats.permute_ms,
                                       &ctx->stats.gemm1_ms, &ctx->stats.gemm2_ms,   &ctx->stats.combine_ms,
-                                      &ctx->stats.comm_ms,  &ctx->stats.token_latency_ms};
+                                      &ctx->stats.comm_ms,  &ctx->stats.token_latency_ms,
+                                      &ctx->stats.oproj_ms, &ctx->stats.norm_ms};
     for (const moe::Rec& r : ctx->pending) {
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) *bucket[r.kind] += ms;
@@ -690,6 +828,9 @@ moe_status moe_debug_buffers(moe_ctx ctx, moe_debug_view* out) {
     out->h_act = ctx->h_act;
     out->y_perm = ctx->y_perm;
     out->rows = ctx->ep ? ctx->last_recv_rows : ctx->last_rows;
+    out->h1 = ctx->h1_ws;
+    out->moe_in = ctx->u_ws;
+    out->taskb_tokens = ctx->last_taskb_T;
     return MOE_OK;
 }
 
@@ -712,12 +853,14 @@ moe_status moe_destroy(moe_ctx c) {
     for (int i = 0; i < 2; ++i) {
         cudaFree(c->x_dev[i]);
         cudaFree(c->out_dev[i]);
-        cudaEvent_t evs[] = {c->xbuf_free[i], c->x_ready[i]};
+        cudaEvent_t evs[] = {c->xbuf_free[i], c->x_ready[i], c->lw_ready[i], c->lw_free[i]};
         for (cudaEvent_t e : evs)
             if (e) cudaEventDestroy(e);
+        cudaFree(c->lw_slot[i]);
     }
     void* bufs[] = {c->idx_ws, c->gates_ws, c->tile_counts, c->tile_prefix, c->offsets, c->counts,
-                    c->grp1, c->grp2, c->pos, c->x_perm, c->h_act, c->y_perm};
+                    c->grp1, c->grp2, c->pos, c->x_perm, c->h_act, c->y_perm,
+                    c->h1_ws, c->u_ws, c->oproj_grp};
     for (void* p : bufs) cudaFree(p);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->token_stream) cudaStreamDestroy(c->token_stream);

@@ -38,20 +38,32 @@ cudaError_t launch_permute(const __nv_bfloat16* x, int T, int h, int k, int ne,
                            const int32_t* idx, const int32_t* tile_prefix,
                            const int32_t* offsets, __nv_bfloat16* x_perm, int32_t* pos,
                            cudaStream_t st);
-// a7: out[t] = sum_j g[t,j] * Y[pos[t,j]] + sum_s Y[R + s*T + t]  (fp32, fixed order) -> bf16.
+// a7: out[t] = sum_j g[t,j] * Y[pos[t,j]] + sum_s Y[R + s*T + t] (+ resid[t] if resid != NULL)
+//     (fp32, fixed order) -> bf16.
 cudaError_t launch_combine(const __nv_bfloat16* y_perm, const int32_t* pos, const float* gates,
                            int T, int h, int k, int num_shared, int64_t shared_base,
-                           __nv_bfloat16* out, cudaStream_t st);
+                           const __nv_bfloat16* resid, __nv_bfloat16* out, cudaStream_t st);
+// Task B (b2): u[t] = RMSNorm(h1[t]) * gamma, reading R21:
+//   r = 1 / sqrt(sum_c h1[t,c]^2 / h + eps)  (fp64),  n = bf16(float(h1 * r)),
+//   u = bf16(float(gamma) * float(n))  (fp32 multiply).
+cudaError_t launch_rmsnorm(const __nv_bfloat16* h1, const __nv_bfloat16* gamma, int T, int h,
+                           float eps, __nv_bfloat16* u, cudaStream_t st);
+// One GEMM group {a_begin, a_end, out_base} written on the stream (device-side group tables are
+// how the GEMM learns its rows without a host sync).
+cudaError_t launch_fill_group(GemmGroup* g, int a_begin, int a_end, int out_base, cudaStream_t st);
 
 // ---------------------------------------------------------------------------- expert GEMM
-enum GemmMode { kGemmSwiGLU = 0, kGemmPlain = 1 };
-// One expert group of a5 (SwiGLU, N = 2*h_i interleaved) or a6 (plain, N = h) on tcgen05.
+enum GemmMode { kGemmSwiGLU = 0, kGemmPlain = 1, kGemmResidual = 2 };
+// One expert group of a5 (SwiGLU, N = 2*h_i interleaved) or a6 (plain, N = h) on tcgen05, or
+// the O-projection of Task B (residual: out = bf16(A B^T + resid), N = h).
 //   tmA: A [rows, K] bf16 (box 64 x 128); tmB: B [N, K] bf16 (box 64 x bn, or 64 x 128 when
 //   `pair`: the CTA-pair kernel, 256 x 256 tiles, bn must be 256); group: device ptr.
-//   out: bf16 [*, ldo]; SwiGLU writes N/2 columns.
+//   out: bf16 [*, ldo]; SwiGLU writes N/2 columns.  resid: bf16 [*, ldo] (residual mode only,
+//   else nullptr), read at the output's rows.
 cudaError_t launch_expert_gemm(int mode, int bn, bool pair, const CUtensorMap* tmA,
                                const CUtensorMap* tmB, const GemmGroup* group, int N, int K,
-                               __nv_bfloat16* out, int ldo, int grid, cudaStream_t st);
+                               __nv_bfloat16* out, int ldo, const __nv_bfloat16* resid, int grid,
+                               cudaStream_t st);
 int gemm_bn_for(int mode, int N);   // tile width used for a given mode / N (0 = unsupported)
 // L2 policy of the GEMM operand loads for the current device: 0 evict_normal, 1 A evict_last +
 // B evict_first.

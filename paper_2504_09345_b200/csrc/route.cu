@@ -330,7 +330,8 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int h, int k, int ne,
 __global__ void __launch_bounds__(256)
 combine_kernel(const __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ pos,
                const float* __restrict__ gates, int T, int h, int k, int num_shared,
-               int64_t shared_base, __nv_bfloat16* __restrict__ out) {
+               int64_t shared_base, const __nv_bfloat16* __restrict__ resid,
+               __nv_bfloat16* __restrict__ out) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int t = blockIdx.x * 8 + warp;
     if (t >= T) return;
@@ -359,6 +360,16 @@ combine_kernel(const __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ 
         for (int s = 0; s < num_shared; ++s) {
             const int64_t row = shared_base + (int64_t)s * T + t;
             const int4 raw = ptx::ld_nc_v4(reinterpret_cast<const int4*>(y + (size_t)row * h) + v);
+            const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float2 f = __bfloat1622float2(b[i]);
+                acc[2 * i] += f.x;
+                acc[2 * i + 1] += f.y;
+            }
+        }
+        if (resid) {  // Task B: the block's residual connection around the MoE layer
+            const int4 raw = ptx::ld_nc_v4(reinterpret_cast<const int4*>(resid + (size_t)t * h) + v);
             const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -427,10 +438,10 @@ cudaError_t launch_permute(const __nv_bfloat16* x, int T, int h, int k, int ne,
 
 cudaError_t launch_combine(const __nv_bfloat16* y_perm, const int32_t* pos, const float* gates,
                            int T, int h, int k, int num_shared, int64_t shared_base,
-                           __nv_bfloat16* out, cudaStream_t st) {
+                           const __nv_bfloat16* resid, __nv_bfloat16* out, cudaStream_t st) {
     if (T == 0) return cudaSuccess;
     combine_kernel<<<(T + 7) / 8, 256, 0, st>>>(y_perm, pos, gates, T, h, k, num_shared,
-                                                shared_base, out);
+                                                shared_base, resid, out);
     return cudaGetLastError();
 }
 

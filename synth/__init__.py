@@ -194,3 +194,28 @@ def gen_inputs(cfg: MoEConfig, layer: int = 0, threads: int = 8, tokens: Optiona
     if tokens is not None:
         cfg = cfg.with_tokens(tokens)
     return MoEInputs(cfg, x, router, w1, w3, w2, topic)
+
+
+@dataclasses.dataclass
+class TaskBInputs:
+    """GPU Task B inputs: attention output, residual stream, Wo, RMSNorm gamma."""
+    attn: np.ndarray         # [T, h] uint16 (bf16)
+    resid: np.ndarray        # [T, h]
+    wo: np.ndarray           # [h, h]  nn.Linear (out x in)
+    gamma: np.ndarray        # [h]
+    eps: float
+
+
+def gen_taskb(cfg: MoEConfig, x_bits: np.ndarray, layer: int = 0) -> TaskBInputs:
+    """Task B inputs around a layer's MoE hidden batch x (DESIGN.md input recipe): the residual
+    stream carries the config's token structure (resid = 4 x, so the post-norm MoE input keeps
+    the routing skew of the MoE-only workload), the attention output is an iid N(0, 1) per
+    channel, Wo ~ U(+-1/sqrt(h)) (nn.Linear init scale), gamma ~ U(0.5, 1.5); eps 1e-5 (Mixtral)."""
+    ss = np.random.SeedSequence(entropy=ENTROPY, spawn_key=(cfg.config_id, layer, 0xB))
+    ra, rw, rg = [np.random.default_rng(c) for c in ss.spawn(3)]
+    T, h = x_bits.shape
+    attn = f32_to_bf16_bits(ra.standard_normal((T, h), dtype=np.float32))
+    resid = f32_to_bf16_bits(bf16_bits_to_f32(x_bits) * np.float32(4.0))
+    wo = _uniform_bf16(rw, (h, h), 1.0 / math.sqrt(h))
+    g = rg.random(h, dtype=np.float32) + np.float32(0.5)
+    return TaskBInputs(attn, resid, wo, f32_to_bf16_bits(g), 1e-5)

@@ -1,0 +1,222 @@
+"""GPU parity of GPU Task B (O projection + MoE layer over all tokens; SURVEY.md §8
+NEXT-2) through the C ABI against the oracle (oracle.taskb_forward and its pinned steps).
+
+Staged bar (readings R19-R21):
+  * h1 = bf16(resid + attn Wo^T): per-token max-abs error / max-abs reference <= 1e-2 (tensor-core
+    fp32 vs oracle fp64 accumulation, one bf16 rounding each), and >= 97% of elements bit-equal;
+  * u = RMSNorm(h1) * gamma: BIT-EXACT given the GPU's h1 (both sides use the same correctly
+    rounded IEEE operations, R21);
+  * routing on u: expert indices bit-exact, gates within 1e-6;
+  * out = h1 + MoE(u): per-token relative error <= 2e-2 (the MoE layer's bar).
+  * end to end from (attn, resid) alone: the same output bar on every token whose routing agrees
+    with the pure-oracle run; tokens whose routing flips (h1 rounding moved u across a near-tie)
+    must be rare (< 0.5%).
+"""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2504_09345_b200 import (MOE_E_INVAL, MOE_E_NOT_PINNED, HostLayer, MoEError,
+                                   moe_taskb_forward)
+
+from gpu_helpers import GpuRun, bf16_tensor, dev_view, sample_tokens, to_f32, token_rel_err
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-2
+H1_TOL = 1e-2
+
+
+def _bits(t: torch.Tensor) -> np.ndarray:
+    return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+class TaskBRun:
+    def __init__(self, inp, tb, force_ep=False, profile=False, max_tokens=None):
+        self.inp, self.tb = inp, tb
+        self.run = GpuRun(inp, force_ep=force_ep, profile=profile, max_tokens=max_tokens)
+        self.layer = HostLayer(inp.cfg.hidden, tb.wo, tb.gamma)
+
+    def forward(self, attn_bits=None, resid_bits=None, out_alias=None, layer=None):
+        attn_bits = self.tb.attn if attn_bits is None else attn_bits
+        resid_bits = self.tb.resid if resid_bits is None else resid_bits
+        T, k = attn_bits.shape[0], self.inp.cfg.top_k
+        attn, resid = bf16_tensor(attn_bits), bf16_tensor(resid_bits)
+        out = {"resid": resid, "attn": attn}.get(out_alias) if out_alias else torch.empty_like(attn)
+        idx = torch.empty((T, k), dtype=torch.int32, device="cuda")
+        gates = torch.empty((T, k), dtype=torch.float32, device="cuda")
+        s = torch.cuda.current_stream()
+        self.run.layer.taskb_forward(attn, resid, layer or self.layer, self.tb.eps,
+                                     self.run.router, self.run.experts, out, idx, gates,
+                                     stream=s.cuda_stream)
+        s.synchronize()
+        self.run.layer.sync()
+        dbg = self.run.layer.debug()
+        assert dbg.taskb_tokens == T
+        h = self.inp.cfg.hidden
+        h1 = _bits(dev_view(dbg.h1, (T, h), "<i2").clone().view(torch.int16))
+        u = _bits(dev_view(dbg.moe_in, (T, h), "<i2").clone().view(torch.int16))
+        return out, idx, gates, h1, u
+
+    def close(self):
+        self.layer.close()
+        self.run.close()
+
+
+def _check_staged(inp, tb, out, idx, gates, h1, u, rows=None):
+    """Stage-by-stage parity on the token rows `rows` (all when None)."""
+    cfg = inp.cfg
+    sel = np.arange(tb.attn.shape[0]) if rows is None else rows
+    # b1: O-projection + residual
+    h1_ref = oracle.oproj_residual(tb.attn[sel], tb.resid[sel], tb.wo)
+    e1 = token_rel_err(synth.bf16_bits_to_f32(h1[sel]), synth.bf16_bits_to_f32(h1_ref))
+    same = np.mean(h1[sel] == h1_ref)
+    assert e1.max() <= H1_TOL and same >= 0.97, f"h1: max rel {e1.max():.3e}, bit-equal {same:.4f}"
+    # b2: RMSNorm -- bit-exact on the GPU's h1
+    u_ref = oracle.rmsnorm(h1[sel], tb.gamma, tb.eps)
+    assert np.array_equal(u[sel], u_ref), f"u: {(u[sel] != u_ref).sum()} elements differ"
+    # routing on u (all tokens: cheap)
+    logits = oracle.router_logits(u, inp.router)
+    idx_ref, g_ref = oracle.topk_gates(logits, cfg.top_k)
+    assert np.array_equal(idx.cpu().numpy(), idx_ref)
+    assert np.max(np.abs(gates.cpu().numpy() - g_ref)) <= 1e-6
+    # out = h1 + MoE(u)
+    y = oracle.experts_combine(u[sel], inp.w1, inp.w3, inp.w2, cfg.num_experts, cfg.num_shared,
+                               idx_ref[sel], g_ref[sel])
+    y += synth.bf16_bits_to_f32(h1[sel])
+    err = token_rel_err(to_f32(out[torch.from_numpy(sel).cuda()]), y)
+    assert err.max() <= TOL, f"out: max token rel err {err.max():.3e}"
+    return e1.max(), err.max()
+
+
+def _inputs(hidden, ffn, ne, k, T, S=0, seed_id=9):
+    cfg = synth.MoEConfig("custom", seed_id, hidden, ffn, ne, k, T, S)
+    inp = synth.gen_inputs(cfg)
+    return inp, synth.gen_taskb(cfg, inp.x)
+
+
+@pytest.mark.parametrize("shape", [
+    dict(hidden=256, ffn=384, ne=8, k=2, T=300),
+    dict(hidden=512, ffn=640, ne=16, k=4, T=1000, S=1),
+    dict(hidden=384, ffn=256, ne=64, k=6, T=777, S=2),
+    dict(hidden=128, ffn=128, ne=4, k=2, T=1),
+])
+@pytest.mark.parametrize("force_ep", [False, True])
+def test_taskb_staged_parity(shape, force_ep):
+    inp, tb = _inputs(shape["hidden"], shape["ffn"], shape["ne"], shape["k"], shape["T"],
+                      shape.get("S", 0))
+    r = TaskBRun(inp, tb, force_ep=force_ep)
+    try:
+        out, idx, gates, h1, u = r.forward()
+        e1, e = _check_staged(inp, tb, out, idx, gates, h1, u)
+        print(f"{shape} ep={force_ep}: h1 rel {e1:.2e}, out rel {e:.2e}")
+    finally:
+        r.close()
+
+
+def test_taskb_end_to_end_vs_pure_oracle():
+    """From (attn, resid) alone: the whole oracle Task B vs the CUDA path."""
+    inp, tb = _inputs(512, 640, 16, 4, 700, S=1)
+    cfg = inp.cfg
+    r = TaskBRun(inp, tb)
+    try:
+        out, idx, gates, h1, u = r.forward()
+    finally:
+        r.close()
+    y, h1_ref, u_ref, idx_ref, g_ref = oracle.taskb_forward(
+        tb.attn, tb.resid, tb.wo, tb.gamma, tb.eps, inp.router, inp.w1, inp.w3, inp.w2,
+        cfg.top_k, cfg.num_shared)
+    agree = (idx.cpu().numpy() == idx_ref).all(axis=1)
+    assert agree.mean() >= 0.995, f"{(~agree).sum()} tokens routed differently"
+    err = token_rel_err(to_f32(out)[agree], y[agree])
+    assert err.max() <= TOL, f"max token rel err {err.max():.3e}"
+
+
+@pytest.mark.parametrize("name", ["mixtral_8x7b", "dsv2_lite"])
+def test_taskb_full_size(name):
+    """BASELINE.json sizes: routing bit-exact on every token, other stages on sampled tokens."""
+    cfg = synth.CONFIGS[name]
+    inp = synth.gen_inputs(cfg)
+    tb = synth.gen_taskb(cfg, inp.x)
+    r = TaskBRun(inp, tb)
+    try:
+        out, idx, gates, h1, u = r.forward()
+        sel = sample_tokens(cfg.tokens, 16)
+        e1, e = _check_staged(inp, tb, out, idx, gates, h1, u, rows=sel)
+        print(f"{name}: h1 rel {e1:.2e}, out rel {e:.2e} over {len(sel)} tokens")
+    finally:
+        r.close()
+
+
+def test_taskb_back_to_back_layers_and_in_place():
+    """Alternating layer blobs (both layer slots cycle) interleaved with plain MoE calls; the
+    output may alias resid (in-place residual update)."""
+    inp, tb = _inputs(256, 256, 8, 2, 200, S=1)
+    tb2 = synth.TaskBInputs(tb.attn, tb.resid, synth.f32_to_bf16_bits(
+        -synth.bf16_bits_to_f32(tb.wo)), tb.gamma[::-1].copy(), 1e-6)
+    r = TaskBRun(inp, tb)
+    layer2 = HostLayer(inp.cfg.hidden, tb2.wo, tb2.gamma)
+    try:
+        ref1 = [t.clone() for t in r.forward()[:3]]
+        r.tb = tb2
+        ref2 = [t.clone() for t in r.forward(layer=layer2)[:3]]
+        for it in range(3):
+            r.tb = tb
+            a = r.forward()
+            r.run.run()                      # a plain MoE layer call in between
+            r.tb = tb2
+            b = r.forward(layer=layer2)
+            for x, y in zip(a[:3], ref1):
+                assert torch.equal(x, y), f"iteration {it}: layer 1 changed"
+            for x, y in zip(b[:3], ref2):
+                assert torch.equal(x, y), f"iteration {it}: layer 2 changed"
+        r.tb = tb
+        out, idx, gates, h1, u = r.forward(out_alias="resid")
+        assert torch.equal(out, ref1[0]) and torch.equal(idx, ref1[1])
+    finally:
+        layer2.close()
+        r.close()
+
+
+def test_taskb_stats_and_errors():
+    inp, tb = _inputs(256, 256, 8, 2, 64)
+    r = TaskBRun(inp, tb, profile=True)
+    try:
+        r.run.layer.reset_stats()
+        r.forward()
+        st = r.run.layer.stats()
+        blob = 6 * 256 * 256
+        assert st["taskb_calls"] == 1 and st["calls"] == 1
+        assert st["h2d_weight_bytes"] == 8 * blob + (2 * 256 * 256 + 2 * 256)
+        assert st["oproj_ms"] > 0 and st["norm_ms"] > 0
+        lay = r.run.layer
+        attn = bf16_tensor(tb.attn)
+        out = torch.empty_like(attn)
+
+        def call(eps=1e-5, layer_ptr=r.layer.ptr, T=64, a=attn):
+            moe_taskb_forward(lay.ctx, a.data_ptr(), a.data_ptr(), T, layer_ptr, eps,
+                              r.run.router.data_ptr(), r.run.experts.array, 2, out.data_ptr())
+
+        with pytest.raises(MoEError) as e:
+            call(eps=-1.0)
+        assert e.value.status == MOE_E_INVAL
+        with pytest.raises(MoEError) as e:
+            call(eps=float("nan"))
+        assert e.value.status == MOE_E_INVAL
+        pageable = np.zeros(2 * 256 * 256 + 2 * 256, np.uint16)
+        with pytest.raises(MoEError) as e:
+            call(layer_ptr=pageable.ctypes.data)
+        assert e.value.status == MOE_E_NOT_PINNED
+        with pytest.raises(MoEError) as e:
+            call(T=65)      # > max_tokens
+        assert e.value.status == MOE_E_INVAL
+        call(T=0)           # no-op at W = 1
+        # the context is still healthy
+        a2 = r.forward()
+        assert a2[0].shape == (64, 256)
+    finally:
+        r.close()
