@@ -89,7 +89,11 @@ typedef struct {
 } moe_config;
 
 /* Packed host blob of one expert (produced by moe_pack_expert, consumed by the copy engine):
- *   [ W13 : 2*h_i rows x h bf16, gate/up rows interleaved in blocks of 128 rows ]
+ *   [ W13 : 2*h_i rows x h bf16, gate/up rows interleaved in blocks of 16 rows:
+ *           rows [32j, 32j+16) = W1 rows [16j, 16j+16), rows [32j+16, 32j+32) = W3 rows
+ *           [16j, 16j+16) -- every 32 accumulator columns (tokens-as-M GEMM) or every warp's
+ *           32 TMEM lanes (weights-as-M GEMM) hold matching gate and up rows, so the SwiGLU is
+ *           applied in the GEMM epilogue in either operand role ]
  *   [ W2  : h rows x h_i bf16 (canonical nn.Linear orientation) ]
  * Size in bytes = 6 * h * h_i  (Eq. 1 denominator per expert). */
 int64_t moe_packed_expert_bytes(int32_t hidden, int32_t ffn);

@@ -96,6 +96,8 @@ struct moe_ctx_s {
     __nv_bfloat16* h_act = nullptr;
     __nv_bfloat16* y_perm = nullptr;
     CUtensorMap tm_xperm, tm_h;
+    moe::TokenMaps tm_xperm_t, tm_h_t;  // token operands of the swap-AB GEMM
+    int swap_mode = 0;                  // MOE_GEMM_SWAP: 0 never, 1 always
     int64_t last_rows = 0;
 
     // expert parallelism (world_size > 1, or MOE_FLAG_FORCE_EP)
@@ -111,6 +113,7 @@ struct moe_ctx_s {
     __nv_bfloat16* x_recv = nullptr;
     __nv_bfloat16* y_recv = nullptr;
     CUtensorMap tm_xrecv;
+    moe::TokenMaps tm_xrecv_t;
     std::vector<int32_t> send_off, send_cnt, recv_off, recv_cnt, grp_off;
     int64_t last_recv_rows = 0, comm_bytes = 0;
 

@@ -129,7 +129,8 @@ moe_status ep_init(moe_ctx c) {
         cudaGetLastError();
         return set_err(c, MOE_E_NOMEM, "EP buffers");
     }
-    if (!make_tmap(&c->tm_xrecv, c->x_recv, (uint64_t)c->cap_recv, cf.hidden, 128))
+    if (!make_tmap(&c->tm_xrecv, c->x_recv, (uint64_t)c->cap_recv, cf.hidden, 128) ||
+        !make_token_maps(&c->tm_xrecv_t, c->x_recv, (uint64_t)c->cap_recv, cf.hidden))
         return set_err(c, MOE_E_CUDA, "tensor map x_recv");
     const int np = W * c->n_local;
     c->send_off.assign(np, 0);

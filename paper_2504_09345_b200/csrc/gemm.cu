@@ -3,7 +3,7 @@
 // One launch computes one expert group (steps a5 / a6 of the MoE layer; Eq. 1's "6 N_k h h_i"
 // FLOPs):
 //   a5 (kGemmSwiGLU): H[r, f] = silu(A W1^T)[r,f] * (A W3^T)[r,f]   with B = packed W13 whose
-//                     256-row N tiles hold 128 gate rows then the 128 matching up rows, so the
+//                     32-row blocks hold 16 gate rows then the 16 matching up rows, so the
 //                     SwiGLU is applied in the epilogue straight out of TMEM;
 //   a6 (kGemmPlain):  Y[r, :] = A W2^T.
 // A rows of the group are [a_begin, a_end) (read from device memory: the routing kernels
@@ -73,24 +73,24 @@ template <int BN, int MODE>
 __device__ __forceinline__ void epilogue_row(uint32_t taddr, bool valid, __nv_bfloat16* row_out,
                                              const __nv_bfloat16* row_res, int n) {
     if (MODE == kGemmSwiGLU) {
+        // packed W13 (moe_pack_expert): 32-column blocks = 16 gate columns, then the 16 matching
+        // up columns -> 16 output features per 32 accumulator columns
         __nv_bfloat16* dst = row_out + (int64_t)n * (BN / 2);
 #pragma unroll 1
-        for (int c = 0; c < BN / 2; c += 32) {
-            uint32_t gv[32], uv[32];
-            ptx::tmem_ld_32x32b_x32(taddr + c, gv);
-            ptx::tmem_ld_32x32b_x32(taddr + BN / 2 + c, uv);
+        for (int c = 0; c < BN; c += 32) {
+            uint32_t v[32];
+            ptx::tmem_ld_32x32b_x32(taddr + c, v);
             ptx::tmem_ld_wait();
             if (valid) {
-                uint32_t pk[16];
+                uint32_t pk[8];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const float h0 = silu_mul(__uint_as_float(gv[2 * i]), __uint_as_float(uv[2 * i]));
-                    const float h1 = silu_mul(__uint_as_float(gv[2 * i + 1]), __uint_as_float(uv[2 * i + 1]));
+                for (int i = 0; i < 8; ++i) {
+                    const float h0 = silu_mul(__uint_as_float(v[2 * i]), __uint_as_float(v[16 + 2 * i]));
+                    const float h1 = silu_mul(__uint_as_float(v[2 * i + 1]), __uint_as_float(v[17 + 2 * i]));
                     pk[i] = ptx::pack_bf16x2(h0, h1);
                 }
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    ptx::st_global_v4(dst + c + 8 * i, pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+                ptx::st_global_v4(dst + c / 2, pk[0], pk[1], pk[2], pk[3]);
+                ptx::st_global_v4(dst + c / 2 + 8, pk[4], pk[5], pk[6], pk[7]);
             }
         }
     } else {
@@ -427,6 +427,304 @@ expert_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// Swap-AB CTA-pair variant: D^T = W X^T.  The weights are the M side (a 256-row pair tile: 128
+// rows per CTA, the same operand maps as the pair kernel's B), the group's tokens the N side:
+// tcgen05 takes N = 16..256 in steps of 16 at run time, so a group of R rows costs
+// ceil(R/32)*32 columns instead of ceil(R/256)*256 rows (C1: 1053 rows -> 1056 instead of 1280).
+// Tiles are handed out round-robin over a grouped raster (SwapRR).
+// Token rows are loaded in 16-row TMA boxes (a CTA holds N/2 of them).  The epilogue transposes
+// through shared memory: TMEM lane = weight row (feature), column = token.
+constexpr int kSwapStages = 6;
+constexpr uint32_t kSwapABytes = 128 * BK * 2;      // per CTA: 128 weight rows
+constexpr uint32_t kSwapBBytes = 128 * BK * 2;      // per CTA: up to 128 token rows
+constexpr uint32_t kSwapEpiBytes = 4 * 32 * 33 * 4;  // per-warp transpose tiles (4 warps)
+constexpr size_t kSwapSmem = 1024 + kSwapStages * (kSwapABytes + kSwapBBytes) + kSwapEpiBytes + 256;
+
+// Round-robin tile order (tile t -> pair t % npairs) over a grouped raster: the token columns of
+// a group are cut into nck near-equal chunks (<= 256 columns, multiples of 32); chunk groups of
+// kSwapGroup chunks (<= 4096 tokens, ~33 MB at K = 4096) are the outer loop, weight tiles next,
+// chunks innermost -- so the ~74 tiles in flight share a few weight tiles and one token group
+// in L2.  (A contiguous-range-per-pair split balances work better but re-reads each weight tile
+// once per chunk from DRAM: 4.5x the traffic at C1, measured.)
+constexpr int kSwapGroup = 16;
+struct SwapRR {
+    int nck, ucols, extra, m_tiles, total, t, step, grp;
+    __device__ __forceinline__ void init(int rows, int m_tiles_, int pair, int npairs) {
+        grp = g_group_m > 0 ? g_group_m : kSwapGroup;
+        const int upm = (rows + 31) >> 5;
+        nck = (upm + 7) / 8;
+        ucols = upm / nck;               // units per chunk (the first `extra` get one more)
+        extra = upm % nck;
+        m_tiles = m_tiles_;
+        total = m_tiles * nck;
+        t = pair;
+        step = npairs;
+    }
+    __device__ __forceinline__ bool next(int& m, int& col, int& ncols) {
+        if (t >= total) return false;
+        const int per_group = grp * m_tiles;
+        const int gidx = t / per_group, r = t % per_group;
+        const int gsize = min(grp, nck - gidx * grp);
+        m = r / gsize;
+        const int ck = gidx * grp + r % gsize;
+        col = 32 * (ck * ucols + min(ck, extra));
+        ncols = 32 * (ucols + (ck < extra ? 1 : 0));
+        t += step;
+        return true;
+    }
+    __device__ __forceinline__ bool empty() const { return t >= total; }
+};
+
+// Epilogue of one swap tile, one warp (TMEM lane quadrant): 32 token columns at a time, TMEM ->
+// registers -> the warp's own smem tile `wt` (32 x 33 fp32; __syncwarp only) -> 16-byte global
+// stores.  fcol: first output feature of the warp's 32 lanes
+//   SwiGLU: the quadrant's 32 weight rows are 16 gate rows then the 16 matching up rows
+//           (moe_pack_expert's 16-row blocks) -> 16 output features;
+//   Plain / Residual: 32 output features.
+template <int MODE>
+__device__ __forceinline__ void swap_epilogue(uint32_t taddr, int lane, int ncols, int tok0,
+                                              int rows, int64_t orow0, __nv_bfloat16* out,
+                                              int ldo, int fcol, const __nv_bfloat16* resid,
+                                              float* wt) {
+#pragma unroll 1
+    for (int c = 0; c < ncols; c += 32) {
+        uint32_t v[32];
+        ptx::tmem_ld_32x32b_x32(taddr + c, v);
+        ptx::tmem_ld_wait();
+        if (MODE == kGemmSwiGLU) {
+            // lane l < 16: gate row of feature f = fcol + l; lane l + 16: the matching up row.
+            // One xor-16 shuffle per pair: the gate lane finishes tokens c..c+15, the up lane
+            // tokens c+16..c+31 of the same feature.
+            // The results are transposed through the warp's smem tile (token-major, padded) so
+            // each lane then writes one token's 16 features as two 16-byte stores.
+            const bool up = lane >= 16;
+            const int fl = lane & 15;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const float mine = __uint_as_float(up ? v[j] : v[16 + j]);
+                const float x = __shfl_xor_sync(0xffffffffu, mine, 16);
+                const float hv = up ? silu_mul(x, __uint_as_float(v[16 + j]))
+                                    : silu_mul(__uint_as_float(v[j]), x);
+                wt[(j + (up ? 16 : 0)) * 17 + fl] = hv;
+            }
+            __syncwarp();
+            if (tok0 + c + lane < rows) {
+                const float* src = wt + lane * 17;
+                uint32_t pk[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) pk[i] = ptx::pack_bf16x2(src[2 * i], src[2 * i + 1]);
+                __nv_bfloat16* dst = out + (orow0 + c + lane) * ldo + fcol;
+                ptx::st_global_v4(dst, pk[0], pk[1], pk[2], pk[3]);
+                ptx::st_global_v4(dst + 8, pk[4], pk[5], pk[6], pk[7]);
+            }
+            __syncwarp();
+        } else {
+            // lane = output feature fcol + lane; transpose through the warp's smem tile so each
+            // lane owns one token's 32 features: (+ residual,) four 16-byte stores.
+#pragma unroll
+            for (int j = 0; j < 32; ++j) wt[j * 33 + lane] = __uint_as_float(v[j]);
+            __syncwarp();
+            if (tok0 + c + lane < rows) {
+                const float* src = wt + lane * 33;
+                const int64_t off = (orow0 + c + lane) * ldo + fcol;
+                float f[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) f[i] = src[i];
+                if (MODE == kGemmResidual) {   // + residual, one rounding (reading R20)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int4 r = ptx::ld_nc_v4(resid + off + 8 * i);
+                        const uint32_t rw[4] = {(uint32_t)r.x, (uint32_t)r.y, (uint32_t)r.z, (uint32_t)r.w};
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            f[8 * i + 2 * q] += __uint_as_float(rw[q] << 16);
+                            f[8 * i + 2 * q + 1] += __uint_as_float(rw[q] & 0xffff0000u);
+                        }
+                    }
+                }
+                uint32_t pk[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) pk[i] = ptx::pack_bf16x2(f[2 * i], f[2 * i + 1]);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    ptx::st_global_v4(out + off + 8 * i, pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// tmW: weights [M, K] (box 64 x 128); tmX: group tokens [*, K] (TokenMaps); M = 2 h_i (SwiGLU)
+// or h (plain / residual).  out: [*, ldo], SwiGLU writes M/2 columns.
+template <int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+expert_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmW,
+                        const __grid_constant__ TokenMaps tmX,
+                        const GemmGroup* __restrict__ group, int M, int K,
+                        __nv_bfloat16* __restrict__ out, int ldo,
+                        const __nv_bfloat16* __restrict__ resid) {
+    constexpr int S = kSwapStages;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + S * kSwapABytes;
+    float* sE = reinterpret_cast<float*>(sB + S * kSwapBBytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * kSwapBBytes + kSwapEpiBytes);
+    uint64_t* empty = full + S;
+    uint64_t* tfull = empty + S;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const uint32_t rank = ptx::cluster_ctarank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const GemmGroup g = *group;
+    const int rows = g.a_end - g.a_begin;
+    if (rows <= 0) return;                       // uniform over the cluster
+    const int m_tiles = M / 256;
+    SwapRR probe;
+    probe.init(rows, m_tiles, pair, npairs);
+    if (probe.empty()) return;                   // no tile for this pair: both CTAs leave
+    const int num_kb = K / BK;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        ptx::prefetch_tmap(&tmW);
+        for (int i = 0; i < 4; ++i) ptx::prefetch_tmap(&tmX.box[i]);
+        for (int s = 0; s < S; ++s) {
+            ptx::mbar_init(&full[s], 2);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], 8);
+        }
+        ptx::fence_barrier_init();
+        ptx::fence_proxy_async();
+    }
+    if (warp == 2) ptx::tmem_alloc_cta2<512>(tmem_slot);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------------------------------------------- TMA producer (both CTAs)
+            const uint64_t pol = ptx::policy_evict_normal();
+            const uint32_t full0 = ptx::mapa_shared(&full[0], 0);
+            SwapRR sc = probe;
+            int stage = 0;
+            uint32_t phase = 0;
+            int m, col, nc;
+            while (sc.next(m, col, nc)) {
+                const int wrow = m * 256 + (int)rank * 128;
+                const int half = nc >> 1;                      // token rows of this CTA
+                const int trow = g.a_begin + col + (int)rank * half;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1u);
+                    const uint32_t fbar = full0 + stage * 8;
+                    if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * kSwapABytes + (uint32_t)nc * BK * 2);
+                    else ptx::mbar_arrive_cluster(fbar);
+                    ptx::tma_load_2d_cta2(sA + stage * kSwapABytes, &tmW, fbar, kb * BK, wrow, pol);
+                    uint8_t* b = sB + stage * kSwapBBytes;
+                    for (int i = 0, r = 0; i < 4; ++i) {   // boxes of 128, 64, 32, 16 rows
+                        const int box = 128 >> i;
+                        if (half - r >= box) {
+                            ptx::tma_load_2d_cta2(b + r * (BK * 2), &tmX.box[i], fbar, kb * BK,
+                                                  trow + r, pol);
+                            r += box;
+                        }
+                    }
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {
+            // ---------------------------------------------------- MMA issuer (leader only)
+            SwapRR sc = probe;
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            int m, col, nc;
+            while (sc.next(m, col, nc)) {
+                const uint32_t idesc = ptx::umma_idesc_bf16(256, (uint32_t)nc);
+                const int acc = it & 1;
+                const uint32_t aphase = (it >> 1) & 1;
+                ptx::mbar_wait(&tempty[acc], aphase ^ 1u);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem_base + acc * 256;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a0 = ptx::smem_u32(sA + stage * kSwapABytes);
+                    const uint32_t b0 = ptx::smem_u32(sB + stage * kSwapBBytes);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk)
+                        ptx::umma_bf16_cta2(d, ptx::umma_desc_sw128_kmajor(a0 + kk * 32),
+                                            ptx::umma_desc_sw128_kmajor(b0 + kk * 32), idesc,
+                                            (kb | kk) != 0 ? 1u : 0u);
+                    ptx::umma_commit_cta2_mc(&empty[stage], 0x3);
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+                ptx::umma_commit_cta2_mc(&tfull[acc], 0x3);
+                ++it;
+            }
+        }
+    } else if (warp >= 4) {
+        // -------------------------------------------------------- epilogue (both CTAs)
+        const int q = warp - 4;
+        const uint32_t tempty0 = ptx::mapa_shared(&tempty[0], 0);
+        SwapRR sc = probe;
+        int it = 0;
+        int m, col, nc;
+        while (sc.next(m, col, nc)) {
+            const int acc = it & 1;
+            const uint32_t aphase = (it >> 1) & 1;
+            ptx::mbar_wait(&tfull[acc], aphase);
+            ptx::tc_fence_after();
+            const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256;
+            // weight rows of this warp: m*256 + rank*128 + q*32 + [0, 32)
+            const int fcol = (MODE == kGemmSwiGLU) ? m * 128 + (int)rank * 64 + q * 16
+                                                   : m * 256 + (int)rank * 128 + q * 32;
+            swap_epilogue<MODE>(taddr, lane, nc, col, rows, (int64_t)g.out_base + col, out, ldo,
+                                fcol, resid, sE + q * (32 * 33));
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster(tempty0 + acc * 8);
+            ++it;
+        }
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc_cta2<512>(tmem_base);
+    }
+}
+
+template <int MODE>
+cudaError_t launch_swap(const CUtensorMap* tmW, const TokenMaps* tmX, const GemmGroup* group,
+                        int M, int K, __nv_bfloat16* out, int ldo, const __nv_bfloat16* resid,
+                        int grid, cudaStream_t st) {
+    cudaError_t e = cudaFuncSetAttribute(expert_gemm_swap_kernel<MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kSwapSmem);   // every launch, see launch_pair
+    if (e != cudaSuccess) return e;
+    expert_gemm_swap_kernel<MODE><<<grid & ~1, kThreads, kSwapSmem, st>>>(*tmW, *tmX, group, M, K,
+                                                                          out, ldo, resid);
+    return cudaGetLastError();
+}
+
 template <int MODE>
 cudaError_t launch_pair(const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmGroup* group,
                         int N, int K, __nv_bfloat16* out, int ldo, const __nv_bfloat16* resid,
@@ -456,6 +754,15 @@ cudaError_t launch_one(const CUtensorMap* tmA, const CUtensorMap* tmB, const Gem
 }
 
 }  // namespace
+
+cudaError_t launch_expert_gemm_swap(int mode, const CUtensorMap* tmW, const TokenMaps* tmX,
+                                    const GemmGroup* group, int M, int K, __nv_bfloat16* out,
+                                    int ldo, const __nv_bfloat16* resid, int grid, cudaStream_t st) {
+    if ((mode == kGemmResidual) != (resid != nullptr) || M % 256 || K % BK) return cudaErrorInvalidValue;
+    if (mode == kGemmSwiGLU) return launch_swap<kGemmSwiGLU>(tmW, tmX, group, M, K, out, ldo, resid, grid, st);
+    if (mode == kGemmResidual) return launch_swap<kGemmResidual>(tmW, tmX, group, M, K, out, ldo, resid, grid, st);
+    return launch_swap<kGemmPlain>(tmW, tmX, group, M, K, out, ldo, resid, grid, st);
+}
 
 int gemm_bn_for(int mode, int N) {
     if (mode == kGemmSwiGLU) return (N % 256 == 0) ? 256 : 0;

@@ -60,6 +60,12 @@ bool make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, u
     return r == CUDA_SUCCESS;
 }
 
+bool make_token_maps(TokenMaps* t, const void* base, uint64_t rows, uint64_t cols) {
+    for (int i = 0; i < 4; ++i)
+        if (!make_tmap(&t->box[i], base, rows, cols, 128u >> i)) return false;
+    return true;
+}
+
 moe_status set_err(moe_ctx c, moe_status s, const char* fmt, ...) {
     if (c) {
         char buf[512];
@@ -272,7 +278,10 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     // (T == 0 only happens under EP: the rank serves other ranks' tokens; its shared-expert
     // groups are then empty and never touch the map.)
     CUtensorMap tm_x = c->tm_xperm;
-    if (S > 0 && T > 0 && !moe::make_tmap(&tm_x, hidden, (uint64_t)T, (uint64_t)h, 128))
+    moe::TokenMaps tm_x_t = c->tm_xperm_t;
+    if (S > 0 && T > 0 &&
+        (!moe::make_tmap(&tm_x, hidden, (uint64_t)T, (uint64_t)h, 128) ||
+         !moe::make_token_maps(&tm_x_t, hidden, (uint64_t)T, (uint64_t)h)))
         return set_err(c, MOE_E_CUDA, "cuTensorMapEncodeTiled failed for hidden");
 
     // Streaming order: shared experts first (their GEMMs need only the hidden batch, and they are
@@ -307,6 +316,7 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
 
     // Expert parallelism: ship each token row to the rank owning its expert.
     const CUtensorMap* tmA_routed = &c->tm_xperm;
+    const moe::TokenMaps* tmT_routed = &c->tm_xperm_t;
     const GemmGroup* g1 = c->grp1;
     const GemmGroup* g2 = c->grp2;
     __nv_bfloat16* y_routed = c->y_perm;
@@ -316,6 +326,7 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         if (s != MOE_OK) return s;
         p.end();
         tmA_routed = &c->tm_xrecv;
+        tmT_routed = &c->tm_xrecv_t;
         g1 = c->ep_grp;
         g2 = c->ep_grp + c->n_all;
         y_routed = c->y_recv;
@@ -329,6 +340,8 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     auto use_pair = [&](bool shared, int bn, int N) {
         return pick_pair(c, shared ? (int64_t)T : exp_routed + exp_routed / 10, bn, N);
     };
+    // swap-AB kernel: weight rows must fill 256-row pair tiles
+    auto use_swap = [&](int M) { return c->swap_mode == 1 && M % 256 == 0; };
     for (int i = 0; i < c->n_all; ++i) {
         const uint64_t q = q0 + i;
         const int s = (int)(q % (uint64_t)ns);
@@ -341,21 +354,35 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready13[s], 0));
         {
             Prof p(c, moe::kRecGemm1, st);
-            const bool pr = use_pair(shared, c->bn1, 2 * hi);
-            MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmSwiGLU, c->bn1, pr,
-                                                shared ? &tm_x : tmA_routed,
-                                                pr ? &c->tm_w13_pair[s] : &c->tm_w13[s], g1 + e,
-                                                2 * hi, h, c->h_act, hi, nullptr, grid, st));
+            if (use_swap(2 * hi)) {
+                MOE_CUDA(c, moe::launch_expert_gemm_swap(moe::kGemmSwiGLU, &c->tm_w13_pair[s],
+                                                         shared ? &tm_x_t : tmT_routed, g1 + e,
+                                                         2 * hi, h, c->h_act, hi, nullptr, grid, st));
+            } else {
+                const bool pr = use_pair(shared, c->bn1, 2 * hi);
+                MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmSwiGLU, c->bn1, pr,
+                                                    shared ? &tm_x : tmA_routed,
+                                                    pr ? &c->tm_w13_pair[s] : &c->tm_w13[s],
+                                                    g1 + e, 2 * hi, h, c->h_act, hi, nullptr,
+                                                    grid, st));
+            }
             p.end();
         }
         MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready2[s], 0));
         {
             Prof p(c, moe::kRecGemm2, st);
-            const bool pr = use_pair(shared, c->bn2, h);
-            MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmPlain, c->bn2, pr, &c->tm_h,
-                                                pr ? &c->tm_w2_pair[s] : &c->tm_w2[s], g2 + e, h,
-                                                hi, shared ? c->y_perm : y_routed, h, nullptr,
-                                                grid, st));
+            if (use_swap(h)) {
+                MOE_CUDA(c, moe::launch_expert_gemm_swap(moe::kGemmPlain, &c->tm_w2_pair[s],
+                                                         &c->tm_h_t, g2 + e, h, hi,
+                                                         shared ? c->y_perm : y_routed, h,
+                                                         nullptr, grid, st));
+            } else {
+                const bool pr = use_pair(shared, c->bn2, h);
+                MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmPlain, c->bn2, pr, &c->tm_h,
+                                                    pr ? &c->tm_w2_pair[s] : &c->tm_w2[s], g2 + e,
+                                                    h, hi, shared ? c->y_perm : y_routed, h,
+                                                    nullptr, grid, st));
+            }
             p.end();
         }
         c->stats.kernel_launches += 2;
@@ -475,10 +502,20 @@ moe_status taskb_impl(moe_ctx c, const __nv_bfloat16* attn, const __nv_bfloat16*
     MOE_CUDA(c, cudaStreamWaitEvent(st, c->lw_ready[b], 0));
     {
         Prof p(c, moe::kRecOproj, st);
-        const bool pr = pick_pair(c, T, c->bn2, h);
-        MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmResidual, c->bn2, pr, &tm_attn,
-                                            pr ? &c->tm_wo_pair[b] : &c->tm_wo[b], c->oproj_grp,
-                                            h, h, c->h1_ws, h, resid, c->num_sms, st));
+        if (c->swap_mode == 1 && h % 256 == 0) {
+            moe::TokenMaps tm_attn_t;
+            if (!moe::make_token_maps(&tm_attn_t, attn, (uint64_t)T, (uint64_t)h))
+                return set_err(c, MOE_E_CUDA, "cuTensorMapEncodeTiled failed for attn");
+            MOE_CUDA(c, moe::launch_expert_gemm_swap(moe::kGemmResidual, &c->tm_wo_pair[b],
+                                                     &tm_attn_t, c->oproj_grp, h, h, c->h1_ws, h,
+                                                     resid, c->num_sms, st));
+        } else {
+            const bool pr = pick_pair(c, T, c->bn2, h);
+            MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmResidual, c->bn2, pr, &tm_attn,
+                                                pr ? &c->tm_wo_pair[b] : &c->tm_wo[b],
+                                                c->oproj_grp, h, h, c->h1_ws, h, resid,
+                                                c->num_sms, st));
+        }
         p.end();
     }
     {
@@ -511,10 +548,10 @@ moe_status moe_pack_expert(int32_t hidden, int32_t ffn, const void* w1, const vo
     const char* a = static_cast<const char*>(w1);
     const char* b = static_cast<const char*>(w3);
     char* d = static_cast<char*>(dst);
-    // W13: 256-row N tiles = [128 rows of W1 ; the same 128 rows of W3]
-    for (int j = 0; j < ffn / 128; ++j) {
-        memcpy(d + (size_t)(256 * j) * row, a + (size_t)(128 * j) * row, 128 * row);
-        memcpy(d + (size_t)(256 * j + 128) * row, b + (size_t)(128 * j) * row, 128 * row);
+    // W13: 32-row blocks = [16 rows of W1 ; the same 16 rows of W3]
+    for (int j = 0; j < ffn / 16; ++j) {
+        memcpy(d + (size_t)(32 * j) * row, a + (size_t)(16 * j) * row, 16 * row);
+        memcpy(d + (size_t)(32 * j + 16) * row, b + (size_t)(16 * j) * row, 16 * row);
     }
     memcpy(d + (size_t)2 * ffn * row, w2, (size_t)hidden * ffn * 2);
     return MOE_OK;
@@ -625,6 +662,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     bool tm = true;
     tm &= moe::make_tmap(&c->tm_xperm, c->x_perm, (uint64_t)Tm * k, h, 128);
     tm &= moe::make_tmap(&c->tm_h, c->h_act, (uint64_t)h_rows, hi, 128);
+    tm &= moe::make_token_maps(&c->tm_xperm_t, c->x_perm, (uint64_t)Tm * k, h);
+    tm &= moe::make_token_maps(&c->tm_h_t, c->h_act, (uint64_t)h_rows, hi);
     for (int i = 0; i < c->nslots; ++i) {
         tm &= moe::make_tmap(&c->tm_w13[i], c->slot[i], 2ull * hi, h, (uint32_t)c->bn1);
         tm &= moe::make_tmap(&c->tm_w2[i], static_cast<char*>(c->slot[i]) + c->w13_bytes,
@@ -634,6 +673,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
                              (uint64_t)h, hi, 128);
     }
     if (!tm) return fail(MOE_E_CUDA);
+    if (const char* e = getenv("MOE_GEMM_SWAP")) c->swap_mode = atoi(e) != 0;
     if (const char* e = getenv("MOE_GEMM_PAIR")) {
         if (!strcmp(e, "0")) c->pair_mode = 0;
         else if (!strcmp(e, "1")) c->pair_mode = 1;

@@ -64,6 +64,18 @@ cudaError_t launch_expert_gemm(int mode, int bn, bool pair, const CUtensorMap* t
                                const CUtensorMap* tmB, const GemmGroup* group, int N, int K,
                                __nv_bfloat16* out, int ldo, const __nv_bfloat16* resid, int grid,
                                cudaStream_t st);
+// Token operand of the swap-AB kernel: the same [rows, K] bf16 tensor with 64-column boxes of
+// 128, 64, 32 and 16 rows, so a CTA's N/2 token rows (a multiple of 16) load in <= 4 TMA ops.
+struct TokenMaps {
+    CUtensorMap box[4];
+};
+bool make_token_maps(TokenMaps* t, const void* base, uint64_t rows, uint64_t cols);  // moe_api.cu
+// Swap-AB CTA-pair kernel (gemm.cu): weights are the 256-row M side (tmW: box 64 x 128, M rows
+// = 2 h_i for SwiGLU, h otherwise, M % 256 == 0), the group's tokens the N side, N = 32..256
+// per tile (a multiple of 32).
+cudaError_t launch_expert_gemm_swap(int mode, const CUtensorMap* tmW, const TokenMaps* tmX,
+                                    const GemmGroup* group, int M, int K, __nv_bfloat16* out,
+                                    int ldo, const __nv_bfloat16* resid, int grid, cudaStream_t st);
 int gemm_bn_for(int mode, int N);   // tile width used for a given mode / N (0 = unsupported)
 // L2 policy of the GEMM operand loads for the current device: 0 evict_normal, 1 A evict_last +
 // B evict_first.

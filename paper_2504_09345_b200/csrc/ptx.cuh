@@ -230,6 +230,10 @@ __device__ __forceinline__ void umma_commit_cta2_mc(uint64_t* bar, uint16_t mask
 }
 
 // ---------------------------------------------------------------------------------- misc
+// Named barrier `id` (1..15) over `nthreads` threads (whole warps).
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&v);

@@ -51,9 +51,9 @@ def test_pack_expert_layout(lib):
     dst = np.zeros(6 * h * hi // 2, dtype=np.uint16)
     moe.moe_pack_expert(h, hi, w1, w3, w2, dst.ctypes.data)
     w13 = dst[: 2 * hi * h].reshape(2 * hi, h)
-    for j in range(hi // 128):
-        assert np.array_equal(w13[256 * j: 256 * j + 128], w1[128 * j: 128 * j + 128])
-        assert np.array_equal(w13[256 * j + 128: 256 * j + 256], w3[128 * j: 128 * j + 128])
+    for j in range(hi // 16):
+        assert np.array_equal(w13[32 * j: 32 * j + 16], w1[16 * j: 16 * j + 16])
+        assert np.array_equal(w13[32 * j + 16: 32 * j + 32], w3[16 * j: 16 * j + 16])
     assert np.array_equal(dst[2 * hi * h:].reshape(h, hi), w2)
 
 

@@ -283,6 +283,27 @@ def test_gemm_tile_variants(shape, mode, monkeypatch):
     run.close()
 
 
+# ------------------------------------------------------------ swap-AB (weights as M) GEMM
+@pytest.mark.parametrize("shape", [
+    dict(hidden=256, ffn=384, num_experts=8, top_k=2, tokens=1500),
+    dict(hidden=512, ffn=640, num_experts=4, top_k=2, tokens=2100, num_shared=1),
+    dict(hidden=256, ffn=256, num_experts=64, top_k=6, tokens=333),     # many tiny groups
+    dict(hidden=384, ffn=256, num_experts=16, top_k=4, tokens=777, num_shared=2),  # h % 256 != 0
+    dict(hidden=1024, ffn=512, num_experts=2, top_k=1, tokens=70),      # one tile per group
+    dict(hidden=768, ffn=1280, num_experts=8, top_k=2, tokens=9000),    # many tiles per pair
+])
+def test_gemm_swap_ab(shape, monkeypatch):
+    """MOE_GEMM_SWAP=1: expert GEMMs with the weights as the 256-row M side and the tokens as a
+    run-time N (32..256 per tile), work split evenly over SM pairs, transposed epilogue (GEMMs
+    whose weight rows are not a multiple of 256 fall back to the regular kernels)."""
+    monkeypatch.setenv("MOE_GEMM_SWAP", "1")
+    cfg = synth.MoEConfig("custom", 15, shape["hidden"], shape["ffn"], shape["num_experts"],
+                          shape["top_k"], shape["tokens"], shape.get("num_shared", 0))
+    inp = synth.gen_inputs(cfg)
+    run, out, *_ = _check_full(inp)
+    run.close()
+
+
 # ------------------------------------------------------------------------- staging slots
 @pytest.mark.parametrize("slots", [2, 3, 5])
 def test_staging_slot_counts_back_to_back(slots):

@@ -105,15 +105,16 @@ def _inputs(hidden, ffn, ne, k, T, S=0, seed_id=9):
     dict(hidden=384, ffn=256, ne=64, k=6, T=777, S=2),
     dict(hidden=128, ffn=128, ne=4, k=2, T=1),
 ])
-@pytest.mark.parametrize("force_ep", [False, True])
-def test_taskb_staged_parity(shape, force_ep):
+@pytest.mark.parametrize("force_ep,swap", [(False, "0"), (True, "0"), (False, "1")])
+def test_taskb_staged_parity(shape, force_ep, swap, monkeypatch):
+    monkeypatch.setenv("MOE_GEMM_SWAP", swap)
     inp, tb = _inputs(shape["hidden"], shape["ffn"], shape["ne"], shape["k"], shape["T"],
                       shape.get("S", 0))
     r = TaskBRun(inp, tb, force_ep=force_ep)
     try:
         out, idx, gates, h1, u = r.forward()
         e1, e = _check_staged(inp, tb, out, idx, gates, h1, u)
-        print(f"{shape} ep={force_ep}: h1 rel {e1:.2e}, out rel {e:.2e}")
+        print(f"{shape} ep={force_ep} swap={swap}: h1 rel {e1:.2e}, out rel {e:.2e}")
     finally:
         r.close()
 
