@@ -110,8 +110,10 @@ moe_status moe_host_alloc(size_t bytes, void** ptr);
 moe_status moe_host_free(void* ptr);
 
 /* Create a context on cfg->device: validates cfg, allocates the workspace for max_tokens
- * tokens, two staging slots of moe_packed_expert_bytes each, the copy stream and events, and
- * (world_size > 1) the NCCL communicator.  *out is NULL on failure. */
+ * tokens, cfg->num_slots (0 = auto, ~256 MiB) staging slots of moe_packed_expert_bytes each, the
+ * copy stream and events, and (world_size > 1) the NCCL communicator.  *out is NULL on failure:
+ * MOE_E_INVAL (bad cfg), MOE_E_UNSUPPORTED (outside the envelope or not an sm_100 device),
+ * MOE_E_NOMEM, MOE_E_CUDA, MOE_E_NCCL. */
 moe_status moe_init(const moe_config* cfg, moe_ctx* out);
 
 /*
