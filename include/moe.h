@@ -180,6 +180,19 @@ moe_status moe_taskb_forward(moe_ctx ctx, const void* attn, const void* resid, i
                              const void* const* experts, int32_t top_k, void* out,
                              int32_t* topk_idx, float* topk_w, void* stream);
 
+/*
+ * Same as moe_taskb_forward with the attention output and the result in HOST memory -- the
+ * paper's pipeline, where attention runs on the CPU and its output is moved
+ * to the GPU for Task B.  attn_host (pinned bf16 [T, h]) is copied on the copy stream ahead of
+ * the call's layer and expert weights; out_host (pinned bf16 [T, h]) receives the result (D2H
+ * ordered on `stream`).  resid stays on the device (the residual stream lives on the GPU).
+ * End-to-end entry point of `bench.py --taskb` ("e2e").
+ */
+moe_status moe_taskb_forward_host(moe_ctx ctx, const void* attn_host, const void* resid,
+                                  int32_t num_tokens, const void* layer, float eps,
+                                  const void* router_w, const void* const* experts, int32_t top_k,
+                                  void* out_host, int32_t* topk_idx, float* topk_w, void* stream);
+
 /* Block until all work of the context is done; returns the first pending async error. */
 moe_status moe_sync(moe_ctx ctx);
 

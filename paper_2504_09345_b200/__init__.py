@@ -34,7 +34,8 @@ EXPORTED = ["moe_packed_expert_bytes", "moe_pack_expert", "moe_host_alloc", "moe
             "moe_init", "moe_layer_forward", "moe_layer_forward_host", "moe_sync", "moe_get_stats",
             "moe_reset_stats", "moe_debug_buffers", "moe_destroy", "moe_status_string",
             "moe_last_error", "moe_probe_h2d", "moe_ep_plan", "moe_nccl_unique_id",
-            "moe_packed_layer_bytes", "moe_pack_layer", "moe_taskb_forward"]
+            "moe_packed_layer_bytes", "moe_pack_layer", "moe_taskb_forward",
+            "moe_taskb_forward_host"]
 
 
 class moe_config(ctypes.Structure):
@@ -116,6 +117,7 @@ def load(path: str = LIB_PATH):
     lib.moe_packed_layer_bytes.restype = i64
     lib.moe_pack_layer.argtypes = [i32, P, P, P]
     lib.moe_taskb_forward.argtypes = [P, P, P, i32, P, ctypes.c_float, P, P, i32, P, P, P, P]
+    lib.moe_taskb_forward_host.argtypes = [P, P, P, i32, P, ctypes.c_float, P, P, i32, P, P, P, P]
     for name in EXPORTED:
         if name not in ("moe_packed_expert_bytes", "moe_status_string", "moe_last_error",
                         "moe_ep_plan", "moe_packed_layer_bytes"):
@@ -192,6 +194,15 @@ def moe_taskb_forward(ctx: int, attn: int, resid: int, num_tokens: int, layer: i
     _check(load().moe_taskb_forward(ctx, attn or None, resid or None, num_tokens, layer or None,
                                     eps, router_w, experts, top_k, out or None, topk_idx or None,
                                     topk_w or None, stream or None), ctx)
+
+
+def moe_taskb_forward_host(ctx: int, attn_host: int, resid: int, num_tokens: int, layer: int,
+                           eps: float, router_w: int, experts, top_k: int, out_host: int,
+                           topk_idx: int = 0, topk_w: int = 0, stream: int = 0) -> None:
+    _check(load().moe_taskb_forward_host(ctx, attn_host or None, resid or None, num_tokens,
+                                         layer or None, eps, router_w, experts, top_k,
+                                         out_host or None, topk_idx or None, topk_w or None,
+                                         stream or None), ctx)
 
 
 def moe_sync(ctx: int) -> None:
@@ -367,6 +378,18 @@ class MoELayer:
                           out.data_ptr() if T else 0,
                           topk_idx.data_ptr() if topk_idx is not None else 0,
                           topk_w.data_ptr() if topk_w is not None else 0, stream)
+
+    def taskb_forward_host(self, attn_host, resid, layer: HostLayer, eps: float, router_w,
+                           experts: HostExperts, out_host, topk_idx=None, topk_w=None,
+                           stream: int = 0):
+        """GPU Task B with the attention output and the result in pinned host tensors."""
+        T = attn_host.shape[0]
+        moe_taskb_forward_host(self.ctx, attn_host.data_ptr() if T else 0,
+                               resid.data_ptr() if T else 0, T, layer.ptr, eps,
+                               router_w.data_ptr(), experts.array, self.top_k,
+                               out_host.data_ptr() if T else 0,
+                               topk_idx.data_ptr() if topk_idx is not None else 0,
+                               topk_w.data_ptr() if topk_w is not None else 0, stream)
 
     def sync(self):
         moe_sync(self.ctx)

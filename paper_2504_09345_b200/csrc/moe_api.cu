@@ -436,6 +436,42 @@ moe_status validate_call(moe_ctx c, int32_t T, const void* router_w, const void*
     return MOE_OK;
 }
 
+// Host-buffer entry points: copy `bytes` of pinned host tokens into device buffer x_dev[*b] (two
+// buffers alternate between calls) on the weight stream, just ahead of the call's weights (see
+// engine.h token_lane); x_ready[*b] marks them resident.  Allocates the buffers on first use.
+moe_status stage_host_tokens(moe_ctx c, const void* host, size_t bytes, int* b_out) {
+    if (!c->x_dev[0]) {
+        const size_t cap = (size_t)c->cfg.max_tokens * c->cfg.hidden * 2;
+        for (int i = 0; i < 2; ++i) {
+            if (cudaMalloc(&c->x_dev[i], cap) != cudaSuccess || cudaMalloc(&c->out_dev[i], cap) != cudaSuccess) {
+                cudaGetLastError();
+                return set_err(c, MOE_E_NOMEM, "host-mode buffers");
+            }
+        }
+    }
+    const int b = c->host_parity;
+    c->host_parity ^= 1;
+    cudaStream_t ts = c->token_lane ? c->token_stream : c->copy_stream;
+    cudaEvent_t t0 = nullptr;
+    const bool prof = (c->cfg.flags & MOE_FLAG_PROFILE) != 0;
+    if (prof) {  // enqueue-time stamp: the clock stream is always idle
+        t0 = moe::pool_get(c);
+        MOE_CUDA(c, cudaEventRecord(t0, c->clock_stream));
+    }
+    MOE_CUDA(c, cudaStreamWaitEvent(ts, c->xbuf_free[b], 0));
+    MOE_CUDA(c, cudaMemcpyAsync(c->x_dev[b], host, bytes, cudaMemcpyHostToDevice, ts));
+    MOE_CUDA(c, cudaEventRecord(c->x_ready[b], ts));
+    if (prof) {
+        cudaEvent_t t1 = moe::pool_get(c);
+        MOE_CUDA(c, cudaEventRecord(t1, ts));
+        c->pending.push_back(moe::Rec{moe::kRecTokenLatency, t0, t1});
+    }
+    c->stats.h2d_token_bytes += (int64_t)bytes;
+    c->stats.host_calls += 1;
+    *b_out = b;
+    return MOE_OK;
+}
+
 // Task B resources, allocated on the first moe_taskb_forward.
 moe_status taskb_resources(moe_ctx c) {
     if (c->lw_slot[0]) return MOE_OK;
@@ -474,7 +510,8 @@ moe_status taskb_resources(moe_ctx c) {
 moe_status taskb_impl(moe_ctx c, const __nv_bfloat16* attn, const __nv_bfloat16* resid, int T,
                       const void* layer, float eps, const __nv_bfloat16* wr,
                       const void* const* experts, __nv_bfloat16* out, int32_t* topk_idx,
-                      float* topk_w, cudaStream_t st) {
+                      float* topk_w, cudaStream_t st, bool attn_on_copy_stream = false,
+                      int xb = 0) {
     const int h = c->cfg.hidden;
     c->stats.taskb_calls += 1;
     if (T == 0) {  // EP only: no local tokens, this rank still serves its experts
@@ -499,6 +536,7 @@ moe_status taskb_impl(moe_ctx c, const __nv_bfloat16* attn, const __nv_bfloat16*
     c->stats.h2d_weight_bytes += c->layer_bytes;
 
     MOE_CUDA(c, moe::launch_fill_group(c->oproj_grp, 0, T, 0, st));
+    if (attn_on_copy_stream) MOE_CUDA(c, cudaStreamWaitEvent(st, c->x_ready[xb], 0));
     MOE_CUDA(c, cudaStreamWaitEvent(st, c->lw_ready[b], 0));
     {
         Prof p(c, moe::kRecOproj, st);
@@ -733,35 +771,9 @@ moe_status moe_layer_forward_host(moe_ctx ctx, const void* hidden_host, int32_t 
         return set_err(ctx, MOE_E_NOT_PINNED, "hidden_host/out_host must be page-locked");
     MOE_CUDA(ctx, cudaSetDevice(ctx->cfg.device));
     const size_t bytes = (size_t)num_tokens * c->cfg.hidden * 2;
-    if (!c->x_dev[0]) {
-        const size_t cap = (size_t)c->cfg.max_tokens * c->cfg.hidden * 2;
-        for (int i = 0; i < 2; ++i) {
-            if (cudaMalloc(&c->x_dev[i], cap) != cudaSuccess || cudaMalloc(&c->out_dev[i], cap) != cudaSuccess) {
-                cudaGetLastError();
-                return set_err(c, MOE_E_NOMEM, "host-mode buffers");
-            }
-        }
-    }
-    const int b = c->host_parity;
-    c->host_parity ^= 1;
-    // Tokens go on the weight stream ahead of this call's weights (see engine.h token_lane).
-    cudaStream_t ts = c->token_lane ? c->token_stream : c->copy_stream;
-    cudaEvent_t t0 = nullptr;
-    const bool prof = (c->cfg.flags & MOE_FLAG_PROFILE) != 0;
-    if (prof) {  // enqueue-time stamp: the clock stream is always idle
-        t0 = moe::pool_get(c);
-        MOE_CUDA(c, cudaEventRecord(t0, c->clock_stream));
-    }
-    MOE_CUDA(c, cudaStreamWaitEvent(ts, c->xbuf_free[b], 0));
-    MOE_CUDA(c, cudaMemcpyAsync(c->x_dev[b], hidden_host, bytes, cudaMemcpyHostToDevice, ts));
-    MOE_CUDA(c, cudaEventRecord(c->x_ready[b], ts));
-    if (prof) {
-        cudaEvent_t t1 = moe::pool_get(c);
-        MOE_CUDA(c, cudaEventRecord(t1, ts));
-        c->pending.push_back(moe::Rec{moe::kRecTokenLatency, t0, t1});
-    }
-    c->stats.h2d_token_bytes += (int64_t)bytes;
-    c->stats.host_calls += 1;
+    int b = 0;
+    s = stage_host_tokens(c, hidden_host, bytes, &b);
+    if (s != MOE_OK) return s;
     s = forward_impl(c, c->x_dev[b], num_tokens, static_cast<const __nv_bfloat16*>(router_w),
                      experts, c->out_dev[b], topk_idx, topk_w, st, true, b);
     if (s != MOE_OK) return s;
@@ -812,6 +824,48 @@ moe_status moe_taskb_forward(moe_ctx ctx, const void* attn, const void* resid, i
                       static_cast<const __nv_bfloat16*>(router_w), experts,
                       static_cast<__nv_bfloat16*>(out), topk_idx, topk_w,
                       static_cast<cudaStream_t>(stream));
+}
+
+moe_status moe_taskb_forward_host(moe_ctx ctx, const void* attn_host, const void* resid,
+                                  int32_t num_tokens, const void* layer, float eps,
+                                  const void* router_w, const void* const* experts, int32_t top_k,
+                                  void* out_host, int32_t* topk_idx, float* topk_w, void* stream) {
+    moe_status s = validate_call(ctx, num_tokens, router_w, experts, top_k);
+    if (s != MOE_OK || (num_tokens == 0 && !ctx->ep)) return s;
+    if (!(eps >= 0.0f) || !std::isfinite(eps))
+        return set_err(ctx, MOE_E_INVAL, "eps must be finite and >= 0");
+    moe_ctx c = ctx;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    MOE_CUDA(c, cudaSetDevice(c->cfg.device));
+    if (num_tokens == 0) {  // EP: this rank still serves the other ranks' tokens
+        s = taskb_resources(c);
+        if (s != MOE_OK) return s;
+        return taskb_impl(c, nullptr, nullptr, 0, layer, eps,
+                          static_cast<const __nv_bfloat16*>(router_w), experts, nullptr, topk_idx,
+                          topk_w, st);
+    }
+    if (!attn_host || !resid || !out_host || !layer)
+        return set_err(c, MOE_E_INVAL, "NULL attn_host / resid / out_host / layer");
+    if (((uintptr_t)resid & 15) || !is_device(resid))
+        return set_err(c, MOE_E_INVAL, "resid must be 16-byte aligned device memory");
+    if ((topk_idx && !is_device(topk_idx)) || (topk_w && !is_device(topk_w)))
+        return set_err(c, MOE_E_INVAL, "topk_idx/topk_w must be device memory");
+    if (!is_pinned(c, attn_host) || !is_pinned(c, out_host) || !is_pinned(c, layer))
+        return set_err(c, MOE_E_NOT_PINNED, "attn_host/out_host/layer must be page-locked");
+    s = taskb_resources(c);
+    if (s != MOE_OK) return s;
+    const size_t bytes = (size_t)num_tokens * c->cfg.hidden * 2;
+    int b = 0;
+    s = stage_host_tokens(c, attn_host, bytes, &b);   // attention output: ahead of Wo + experts
+    if (s != MOE_OK) return s;
+    s = taskb_impl(c, c->x_dev[b], static_cast<const __nv_bfloat16*>(resid), num_tokens, layer,
+                   eps, static_cast<const __nv_bfloat16*>(router_w), experts, c->out_dev[b],
+                   topk_idx, topk_w, st, true, b);
+    if (s != MOE_OK) return s;
+    MOE_CUDA(c, cudaEventRecord(c->xbuf_free[b], st));
+    MOE_CUDA(c, cudaMemcpyAsync(out_host, c->out_dev[b], bytes, cudaMemcpyDeviceToHost, st));
+    c->stats.d2h_token_bytes += (int64_t)bytes;
+    return MOE_OK;
 }
 
 moe_status moe_sync(moe_ctx ctx) {

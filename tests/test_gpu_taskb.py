@@ -221,3 +221,27 @@ def test_taskb_stats_and_errors():
         assert a2[0].shape == (64, 256)
     finally:
         r.close()
+
+
+def test_taskb_host_entry_point_matches_device():
+    """moe_taskb_forward_host (attention output and result in pinned host memory, residual on the
+    device): bitwise equal to moe_taskb_forward, over back-to-back calls (both host buffers)."""
+    inp, tb = _inputs(512, 640, 16, 4, 900, S=1)
+    r = TaskBRun(inp, tb)
+    try:
+        ref = r.forward()[0].clone()
+        attn_h = bf16_tensor(tb.attn, device="cpu").pin_memory()
+        resid = bf16_tensor(tb.resid)
+        outs = [torch.empty_like(attn_h).pin_memory() for _ in range(3)]
+        s = torch.cuda.current_stream()
+        for o in outs:
+            r.run.layer.taskb_forward_host(attn_h, resid, r.layer, tb.eps, r.run.router,
+                                           r.run.experts, o, stream=s.cuda_stream)
+        s.synchronize()
+        r.run.layer.sync()
+        for o in outs:
+            assert torch.equal(o.cuda(), ref)
+        st = r.run.layer.stats()
+        assert st["host_calls"] == 3 and st["taskb_calls"] == 4
+    finally:
+        r.close()
