@@ -55,10 +55,16 @@ typedef enum {
 #define MOE_FLAG_FORCE_EP 2u /* world_size == 1: still run the expert-parallel exchange through a
                                 one-rank NCCL communicator (tests the EP path on one GPU)        */
 #define MOE_FLAG_LOCAL_EP 4u /* expert parallelism among `world_size` contexts of ONE process
-                                (typically on one GPU, one host thread per rank): the exchange
-                                uses device-to-device copies and host barriers instead of NCCL;
-                                nccl_unique_id points to a 128-byte group key shared by the ranks.
-                                Same plan, layouts and kernels as the NCCL path (testing).        */
+                                (one host thread per rank; the GPUs of one box, or one GPU):
+                                the P2P transport -- the permute kernel writes each token row
+                                straight into its expert owner's receive buffer, the combine
+                                kernel reads the owners' results, device flags order the calls
+                                (no host sync, no NCCL).  nccl_unique_id points to a 128-byte
+                                group key shared by the ranks.                                    */
+#define MOE_FLAG_IPC_EP 8u   /* the P2P transport across PROCESSES (one per GPU, e.g. torchrun):
+                                buffers are shared with CUDA IPC -- call moe_ep_ipc_handle on
+                                every rank, all-gather the handles, then moe_ep_ipc_connect
+                                before the first forward call.  Takes precedence over NCCL.      */
 
 /*
  * Layer configuration.  Envelope of the sm_100a kernels (MOE_E_UNSUPPORTED otherwise):
@@ -255,6 +261,15 @@ const char* moe_last_error(moe_ctx ctx);   /* detail of the last failure ("" if 
 int64_t moe_ep_plan(int32_t world, int32_t rank, int32_t num_experts, const int32_t* counts,
                     int32_t* send_off, int32_t* send_cnt, int32_t* recv_off, int32_t* recv_cnt,
                     int32_t* grp_off);
+
+/* MOE_FLAG_IPC_EP bootstrap.  moe_ep_ipc_handle writes this rank's MOE_IPC_HANDLE_BYTES-byte
+ * blob (CUDA IPC handles of its receive buffers, counts and flags); the caller all-gathers the
+ * blobs of all ranks (rank order) and passes them to moe_ep_ipc_connect, which maps the peers'
+ * buffers (cudaIpcOpenMemHandle, peer access enabled lazily).  MOE_E_STATE if the context is
+ * not an IPC_EP context or is already connected. */
+#define MOE_IPC_HANDLE_BYTES 256
+moe_status moe_ep_ipc_handle(moe_ctx ctx, void* out);
+moe_status moe_ep_ipc_connect(moe_ctx ctx, const void* all_handles);
 
 /* 128-byte ncclUniqueId for moe_config.nccl_unique_id (call on one rank, broadcast to all).
  * MOE_E_NCCL if libnccl.so.2 cannot be loaded. */

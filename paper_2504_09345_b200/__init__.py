@@ -35,7 +35,9 @@ EXPORTED = ["moe_packed_expert_bytes", "moe_pack_expert", "moe_host_alloc", "moe
             "moe_reset_stats", "moe_debug_buffers", "moe_destroy", "moe_status_string",
             "moe_last_error", "moe_probe_h2d", "moe_ep_plan", "moe_nccl_unique_id",
             "moe_packed_layer_bytes", "moe_pack_layer", "moe_taskb_forward",
-            "moe_taskb_forward_host"]
+            "moe_taskb_forward_host", "moe_ep_ipc_handle", "moe_ep_ipc_connect"]
+MOE_FLAG_IPC_EP = 8
+MOE_IPC_HANDLE_BYTES = 256
 
 
 class moe_config(ctypes.Structure):
@@ -118,6 +120,8 @@ def load(path: str = LIB_PATH):
     lib.moe_pack_layer.argtypes = [i32, P, P, P]
     lib.moe_taskb_forward.argtypes = [P, P, P, i32, P, ctypes.c_float, P, P, i32, P, P, P, P]
     lib.moe_taskb_forward_host.argtypes = [P, P, P, i32, P, ctypes.c_float, P, P, i32, P, P, P, P]
+    lib.moe_ep_ipc_handle.argtypes = [P, P]
+    lib.moe_ep_ipc_connect.argtypes = [P, P]
     for name in EXPORTED:
         if name not in ("moe_packed_expert_bytes", "moe_status_string", "moe_last_error",
                         "moe_ep_plan", "moe_packed_layer_bytes"):
@@ -203,6 +207,18 @@ def moe_taskb_forward_host(ctx: int, attn_host: int, resid: int, num_tokens: int
                                          layer or None, eps, router_w, experts, top_k,
                                          out_host or None, topk_idx or None, topk_w or None,
                                          stream or None), ctx)
+
+
+def moe_ep_ipc_handle(ctx: int) -> bytes:
+    buf = ctypes.create_string_buffer(MOE_IPC_HANDLE_BYTES)
+    _check(load().moe_ep_ipc_handle(ctx, buf), ctx)
+    return buf.raw
+
+
+def moe_ep_ipc_connect(ctx: int, handles: Sequence[bytes]) -> None:
+    blob = b"".join(handles)
+    buf = ctypes.create_string_buffer(blob, len(blob))
+    _check(load().moe_ep_ipc_connect(ctx, buf), ctx)
 
 
 def moe_sync(ctx: int) -> None:
@@ -337,11 +353,14 @@ class MoELayer:
                  num_shared: int = 0, renormalize: bool = True, device: int = 0,
                  world_size: int = 1, rank: int = 0, packet_bytes: int = 0,
                  profile: bool = False, nccl_unique_id: Optional[bytes] = None,
-                 force_ep: bool = False, num_slots: int = 0, local_ep: bool = False):
-        """local_ep: in-process expert parallelism (MOE_FLAG_LOCAL_EP); nccl_unique_id is then
-        the 128-byte group key shared by the `world_size` contexts (one host thread each)."""
+                 force_ep: bool = False, num_slots: int = 0, local_ep: bool = False,
+                 ipc_ep: bool = False):
+        """local_ep: in-process expert parallelism over peer memory (MOE_FLAG_LOCAL_EP);
+        nccl_unique_id is then the 128-byte group key shared by the `world_size` contexts (one
+        host thread each).  ipc_ep: the same transport across processes (MOE_FLAG_IPC_EP): call
+        ipc_connect(all ranks' ipc_handle()) before the first forward."""
         flags = ((MOE_FLAG_PROFILE if profile else 0) | (MOE_FLAG_FORCE_EP if force_ep else 0) |
-                 (MOE_FLAG_LOCAL_EP if local_ep else 0))
+                 (MOE_FLAG_LOCAL_EP if local_ep else 0) | (MOE_FLAG_IPC_EP if ipc_ep else 0))
         self.cfg = moe_config(hidden, ffn, num_experts, top_k, num_shared, max_tokens,
                               int(renormalize), device, world_size, rank, None, packet_bytes,
                               flags, num_slots)
@@ -390,6 +409,12 @@ class MoELayer:
                                out_host.data_ptr() if T else 0,
                                topk_idx.data_ptr() if topk_idx is not None else 0,
                                topk_w.data_ptr() if topk_w is not None else 0, stream)
+
+    def ipc_handle(self) -> bytes:
+        return moe_ep_ipc_handle(self.ctx)
+
+    def ipc_connect(self, handles: Sequence[bytes]) -> None:
+        moe_ep_ipc_connect(self.ctx, handles)
 
     def sync(self):
         moe_sync(self.ctx)

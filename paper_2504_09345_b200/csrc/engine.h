@@ -63,6 +63,10 @@ struct moe_ctx_s {
     // PAPER.md:829-835); see DESIGN.md §7.
     cudaStream_t token_stream = nullptr;
     cudaStream_t clock_stream = nullptr;  // idle stream: events on it timestamp enqueue time
+    // Recorded at the end of every call on the caller's stream: moe_sync waits on it (and the
+    // copy stream) instead of the whole device -- a device-wide sync from one rank's thread
+    // would also wait on the other in-process ranks' flag-wait kernels (LOCAL_EP deadlock).
+    cudaEvent_t done_ev = nullptr;
     bool token_lane = false;
 
     // staging slots (a bounded GPU weight buffer, recycled every call)
@@ -116,6 +120,27 @@ struct moe_ctx_s {
     moe::TokenMaps tm_xrecv_t;
     std::vector<int32_t> send_off, send_cnt, recv_off, recv_cnt, grp_off;
     int64_t last_recv_rows = 0, comm_bytes = 0;
+    // P2P transport (MOE_FLAG_LOCAL_EP: ranks in this process; MOE_FLAG_IPC_EP: ranks in other
+    // processes, buffers mapped with CUDA IPC): fused permute+dispatch and combine kernels over
+    // peer memory, synchronised by device flags (ep_p2p.cu) -- no host sync per call.
+    bool p2p = false;
+    bool p2p_ready = false;                  // peer tables filled (connect done)
+    uint64_t p2p_seq = 0;                    // calls issued (flag values)
+    unsigned long long* p2p_flags = nullptr; // device [kP2PFlags][kMaxRanks], written by peers
+    int32_t* p2p_counts = nullptr;           // device [2][W][N_e], row s written by rank s
+    moe::P2PTable* p2p_tab = nullptr;        // device tables (peers' buffers in this process)
+    moe::PeerRows* pr_x = nullptr;           // peers' x_recv + this rank's send bases
+    moe::PeerRows* pr_y = nullptr;           // peers' y_recv + the same bases
+    int32_t* p2p_rows = nullptr;             // device: rows received by the last call
+    long long* p2p_bytes = nullptr;          // device: bytes moved (stats)
+    void* ipc_opened[moe::kMaxRanks][4] = {};  // IPC mappings to close (MOE_FLAG_IPC_EP)
+    long long* p2p_diag_h = nullptr;         // pinned, mapped: a timed-out flag wait (moe_sync)
+    long long* p2p_diag_d = nullptr;
+    // LOCAL_EP synchronises with events instead of device flag waits: [flag][call parity],
+    // recorded by this rank, waited on by its peers after a host barrier (enqueue order) -- a
+    // spinning wait kernel could share a hardware queue with the peer work it waits for when
+    // several ranks run on one GPU.
+    cudaEvent_t p2p_ev[moe::kP2PFlags][2] = {};
 
     // GPU Task B (moe_taskb_forward; allocated on first use).  The layer weights (Wo + gamma,
     // moe_packed_layer_bytes) are streamed like the experts, into two slots of their own, on the
@@ -204,5 +229,14 @@ void ep_destroy(moe_ctx c);
 moe_status ep_dispatch(moe_ctx c, int T, cudaStream_t st);
 // After the local expert GEMMs: return y_recv rows to their source ranks' y_perm.
 moe_status ep_combine(moe_ctx c, cudaStream_t st);
+// P2P transport steps (see ep_p2p.cu for the protocol), all on `st`:
+//   before the permute: counts exchange + plan + wait until the owners' x_recv are free;
+moe_status p2p_before_dispatch(moe_ctx c, int T, cudaStream_t st);
+//   after the permute (which wrote into the owners' x_recv): signal + wait for all dispatches;
+moe_status p2p_after_dispatch(moe_ctx c, cudaStream_t st);
+//   after the expert GEMMs: signal x_recv free / y_recv ready, wait for every owner's y_recv;
+moe_status p2p_after_gemms(moe_ctx c, cudaStream_t st);
+//   after the combine: signal y_recv read.
+moe_status p2p_after_combine(moe_ctx c, cudaStream_t st);
 
 }  // namespace moe

@@ -15,11 +15,13 @@
 // copies are enqueued, so the copy engine keeps streaming while the host waits.
 //
 // Two transports share the plan and the layouts:
-//   NCCL  (default): ncclAllGather + grouped ncclSend/ncclRecv on the caller's stream.
-//   local (MOE_FLAG_LOCAL_EP): W contexts of one process, one host thread per rank; counts are
-//         exchanged through host memory and rows are PULLED with device-to-device copies from
-//         the peers' buffers between host barriers.  It exists to run the multi-rank EP path on
-//         a single GPU (tests); it is synchronous and not a performance path.
+//   NCCL  (default): ncclAllGather + grouped ncclSend/ncclRecv on the caller's stream, one host
+//         sync per call (the counts, for the plan).
+//   P2P   (MOE_FLAG_LOCAL_EP: ranks are contexts of this process; MOE_FLAG_IPC_EP: ranks are
+//         processes, buffers mapped with CUDA IPC): every rank holds device pointers to every
+//         rank's x_recv / y_recv / counts / flags; the permute kernel writes rows straight into
+//         the owners' x_recv, the combine kernel reads the owners' y_recv, and device flags
+//         order the calls (ep_p2p.cu) -- no host sync, no staging copies.
 #include <dlfcn.h>
 
 #include <condition_variable>
@@ -76,7 +78,6 @@ struct LocalGroup {
     int arrived = 0;
     uint64_t generation = 0;
     std::vector<moe_ctx> ranks;
-    std::vector<int32_t> counts;  // [W][N_e]
 
     void barrier() {
         std::unique_lock<std::mutex> lk(m);
@@ -95,22 +96,6 @@ std::mutex g_groups_mu;
 std::map<std::string, std::shared_ptr<LocalGroup>> g_groups;
 
 LocalGroup* local_group(moe_ctx c) { return static_cast<LocalGroup*>(c->local_group); }
-
-// Rows of x_perm (sorted by global expert) that rank s holds for expert e: exclusive scan.
-int64_t send_offset(const int32_t* counts, int ne, int s, int e) {
-    int64_t o = 0;
-    for (int i = 0; i < e; ++i) o += counts[(size_t)s * ne + i];
-    return o;
-}
-// Row of x_recv on rank d where (source s, local expert le) lands (expert-major layout).
-int64_t recv_offset(const int32_t* counts, int ne, int W, int d, int s, int le) {
-    const int nl = ne / W;
-    int64_t o = 0;
-    for (int l = 0; l < le; ++l)
-        for (int q = 0; q < W; ++q) o += counts[(size_t)q * ne + d * nl + l];
-    for (int q = 0; q < s; ++q) o += counts[(size_t)q * ne + d * nl + le];
-    return o;
-}
 
 }  // namespace
 
@@ -139,6 +124,36 @@ moe_status ep_init(moe_ctx c) {
     c->recv_cnt.assign(np, 0);
     c->grp_off.assign(c->n_local + 1, 0);
 
+    if (c->p2p) {
+        bool pk = true;
+        pk &= cudaMalloc((void**)&c->p2p_flags, sizeof(unsigned long long) * kP2PFlags * kMaxRanks) == cudaSuccess;
+        pk &= cudaMalloc((void**)&c->p2p_counts, sizeof(int32_t) * 2 * (size_t)W * ne) == cudaSuccess;
+        pk &= cudaMalloc((void**)&c->p2p_tab, sizeof(P2PTable)) == cudaSuccess;
+        pk &= cudaMalloc((void**)&c->pr_x, sizeof(PeerRows)) == cudaSuccess;
+        pk &= cudaMalloc((void**)&c->pr_y, sizeof(PeerRows)) == cudaSuccess;
+        pk &= cudaMalloc((void**)&c->p2p_rows, sizeof(int32_t)) == cudaSuccess;
+        pk &= cudaMalloc((void**)&c->p2p_bytes, sizeof(long long)) == cudaSuccess;
+        pk &= cudaHostAlloc((void**)&c->p2p_diag_h, 8 * sizeof(long long), cudaHostAllocMapped) == cudaSuccess;
+        if (pk) {
+            memset(c->p2p_diag_h, 0, 8 * sizeof(long long));
+            pk &= cudaHostGetDevicePointer((void**)&c->p2p_diag_d, c->p2p_diag_h, 0) == cudaSuccess;
+        }
+        if (!pk) {
+            cudaGetLastError();
+            return set_err(c, MOE_E_NOMEM, "P2P EP buffers");
+        }
+        pk &= cudaMemset(c->p2p_flags, 0, sizeof(unsigned long long) * kP2PFlags * kMaxRanks) == cudaSuccess;
+        pk &= cudaMemset(c->p2p_counts, 0, sizeof(int32_t) * 2 * (size_t)W * ne) == cudaSuccess;
+        pk &= cudaMemset(c->p2p_rows, 0, sizeof(int32_t)) == cudaSuccess;
+        pk &= cudaMemset(c->p2p_bytes, 0, sizeof(long long)) == cudaSuccess;
+        pk &= cudaDeviceSynchronize() == cudaSuccess;
+        if (!pk) return set_err(c, MOE_E_CUDA, "P2P EP init");
+        if (!c->local_ep) return MOE_OK;   // IPC: moe_ep_ipc_connect maps the peers
+        for (int f = 0; f < kP2PFlags; ++f)
+            for (int p = 0; p < 2; ++p)
+                if (cudaEventCreateWithFlags(&c->p2p_ev[f][p], cudaEventDisableTiming) != cudaSuccess)
+                    return set_err(c, MOE_E_CUDA, "P2P EP events");
+    }
     if (c->local_ep) {
         if (!cf.nccl_unique_id) return set_err(c, MOE_E_INVAL, "LOCAL_EP needs a group key");
         const std::string key(static_cast<const char*>(cf.nccl_unique_id), 128);
@@ -148,7 +163,6 @@ moe_status ep_init(moe_ctx c) {
             g = std::make_shared<LocalGroup>();
             g->world = W;
             g->ranks.assign(W, nullptr);
-            g->counts.assign((size_t)W * ne, 0);
         }
         if (g->world != W || g->ranks[cf.rank]) return set_err(c, MOE_E_INVAL, "LOCAL_EP group mismatch");
         g->ranks[cf.rank] = c;
@@ -183,6 +197,30 @@ void ep_destroy(moe_ctx c) {
         }
         c->local_group = nullptr;
     }
+    for (int d = 0; d < kMaxRanks; ++d)
+        for (int i = 0; i < 4; ++i)
+            if (c->ipc_opened[d][i]) {
+                cudaIpcCloseMemHandle(c->ipc_opened[d][i]);
+                c->ipc_opened[d][i] = nullptr;
+            }
+    void* pbufs[] = {c->p2p_flags, c->p2p_counts, c->p2p_tab, c->pr_x, c->pr_y, c->p2p_rows,
+                     c->p2p_bytes};
+    for (void* p : pbufs) cudaFree(p);
+    for (int f = 0; f < kP2PFlags; ++f)
+        for (int p = 0; p < 2; ++p)
+            if (c->p2p_ev[f][p]) {
+                cudaEventDestroy(c->p2p_ev[f][p]);
+                c->p2p_ev[f][p] = nullptr;
+            }
+    if (c->p2p_diag_h) cudaFreeHost(c->p2p_diag_h);
+    c->p2p_diag_h = nullptr;
+    c->p2p_diag_d = nullptr;
+    c->p2p_flags = nullptr;
+    c->p2p_counts = nullptr;
+    c->p2p_tab = nullptr;
+    c->pr_x = c->pr_y = nullptr;
+    c->p2p_rows = nullptr;
+    c->p2p_bytes = nullptr;
     cudaFree(c->counts_all);
     cudaFreeHost(c->counts_all_h);
     cudaFree(c->ep_grp);
@@ -204,23 +242,7 @@ moe_status ep_dispatch(moe_ctx c, int T, cudaStream_t st) {
     const size_t row = (size_t)h;
 
     // 1. counts exchange -> host
-    if (c->local_ep) {
-        LocalGroup* g = local_group(c);
-        MOE_CUDA(c, cudaMemcpyAsync(c->counts_all_h + (size_t)rank * ne, c->counts,
-                                    sizeof(int32_t) * ne, cudaMemcpyDeviceToHost, st));
-        MOE_CUDA(c, cudaStreamSynchronize(st));  // also: this rank's x_perm is complete
-        {
-            std::lock_guard<std::mutex> lk(g->m);
-            memcpy(g->counts.data() + (size_t)rank * ne, c->counts_all_h + (size_t)rank * ne,
-                   sizeof(int32_t) * ne);
-        }
-        g->barrier();
-        {
-            std::lock_guard<std::mutex> lk(g->m);
-            memcpy(c->counts_all_h, g->counts.data(), sizeof(int32_t) * (size_t)W * ne);
-        }
-        g->barrier();  // everyone has read the counts before any rank's next call overwrites them
-    } else {
+    {
         const NcclApi* n = nccl_api();
         MOE_NCCL(c, n->AllGather(c->counts, c->counts_all, (size_t)ne, kNcclInt32, c->comm, st));
         MOE_CUDA(c, cudaMemcpyAsync(c->counts_all_h, c->counts_all, sizeof(int32_t) * (size_t)W * ne,
@@ -249,24 +271,7 @@ moe_status ep_dispatch(moe_ctx c, int T, cudaStream_t st) {
                                 cudaMemcpyHostToDevice, st));
     // 3. rows: x_perm blocks -> the owners' x_recv (expert-major)
     int64_t bytes = 0;
-    if (c->local_ep) {
-        LocalGroup* g = local_group(c);
-        for (int s = 0; s < W; ++s) {
-            const moe_ctx peer = g->ranks[s];
-            for (int le = 0; le < nl; ++le) {
-                const int i = s * nl + le;
-                const int32_t cnt = c->recv_cnt[i];
-                if (cnt <= 0) continue;
-                const int64_t src = send_offset(c->counts_all_h, ne, s, rank * nl + le);
-                MOE_CUDA(c, cudaMemcpyAsync(c->x_recv + (size_t)c->recv_off[i] * row,
-                                            peer->x_perm + (size_t)src * row,
-                                            (size_t)cnt * row * 2, cudaMemcpyDeviceToDevice, st));
-            }
-        }
-        for (int i = 0; i < W * nl; ++i) bytes += (int64_t)c->send_cnt[i] * h * 2;
-        MOE_CUDA(c, cudaStreamSynchronize(st));
-        g->barrier();  // all pulls done: peers may reuse x_perm
-    } else {
+    {
         const NcclApi* n = nccl_api();
         MOE_NCCL(c, n->GroupStart());
         for (int p = 0; p < W; ++p) {
@@ -295,26 +300,7 @@ moe_status ep_combine(moe_ctx c, cudaStream_t st) {
     const int rank = cf.rank;
     const size_t row = (size_t)h;
     int64_t bytes = 0;
-    if (c->local_ep) {
-        LocalGroup* g = local_group(c);
-        MOE_CUDA(c, cudaStreamSynchronize(st));  // this rank's y_recv is complete
-        g->barrier();                            // ... and every peer's
-        for (int d = 0; d < W; ++d) {            // pull my rows back from each expert owner
-            const moe_ctx peer = g->ranks[d];
-            for (int le = 0; le < nl; ++le) {
-                const int i = d * nl + le;
-                const int32_t cnt = c->send_cnt[i];
-                if (cnt <= 0) continue;
-                const int64_t src = recv_offset(c->counts_all_h, ne, W, d, rank, le);
-                MOE_CUDA(c, cudaMemcpyAsync(c->y_perm + (size_t)c->send_off[i] * row,
-                                            peer->y_recv + (size_t)src * row,
-                                            (size_t)cnt * row * 2, cudaMemcpyDeviceToDevice, st));
-            }
-        }
-        for (int i = 0; i < W * nl; ++i) bytes += (int64_t)c->recv_cnt[i] * h * 2;
-        MOE_CUDA(c, cudaStreamSynchronize(st));
-        g->barrier();  // all pulls done: peers may reuse y_recv
-    } else {
+    {
         const NcclApi* n = nccl_api();
         MOE_NCCL(c, n->GroupStart());
         for (int p = 0; p < W; ++p) {
@@ -334,6 +320,136 @@ moe_status ep_combine(moe_ctx c, cudaStream_t st) {
     }
     c->comm_bytes += bytes;
     return MOE_OK;
+}
+
+// ---------------------------------------------------------------------------- P2P transport
+namespace {
+
+// This rank's device tables, filled from the peers' buffers as mapped in this process.
+// Uploaded on `st` (stream-ordered before the kernels that read them): a legacy-stream copy
+// could wait on peers' flag-wait kernels and deadlock the group.
+moe_status p2p_upload(moe_ctx c, unsigned long long* const* flags, int32_t* const* counts,
+                      __nv_bfloat16* const* xr, __nv_bfloat16* const* yr, cudaStream_t st) {
+    const int W = c->cfg.world_size;
+    P2PTable tab{};
+    PeerRows px{}, py{};
+    for (int d = 0; d < W; ++d) {
+        tab.flags[d] = flags[d];
+        tab.counts[d] = counts[d];
+        px.rows[d] = xr[d];
+        py.rows[d] = yr[d];
+    }
+    px.nl = py.nl = c->n_local;
+    MOE_CUDA(c, cudaMemcpyAsync(c->p2p_tab, &tab, sizeof tab, cudaMemcpyHostToDevice, st));
+    MOE_CUDA(c, cudaMemcpyAsync(c->pr_x, &px, sizeof px, cudaMemcpyHostToDevice, st));
+    MOE_CUDA(c, cudaMemcpyAsync(c->pr_y, &py, sizeof py, cudaMemcpyHostToDevice, st));
+    MOE_CUDA(c, cudaStreamSynchronize(st));   // the host structs go out of scope
+    c->p2p_ready = true;
+    return MOE_OK;
+}
+
+// LOCAL_EP: wait until every rank of the group exists (first call only), then map them.
+moe_status p2p_connect_local(moe_ctx c, cudaStream_t st) {
+    LocalGroup* g = local_group(c);
+    g->barrier();
+    const int W = c->cfg.world_size;
+    unsigned long long* flags[kMaxRanks];
+    int32_t* counts[kMaxRanks];
+    __nv_bfloat16 *xr[kMaxRanks], *yr[kMaxRanks];
+    {
+        std::lock_guard<std::mutex> lk(g->m);
+        for (int d = 0; d < W; ++d) {
+            const moe_ctx p = g->ranks[d];
+            if (!p) return set_err(c, MOE_E_STATE, "LOCAL_EP rank %d missing", d);
+            flags[d] = p->p2p_flags;
+            counts[d] = p->p2p_counts;
+            xr[d] = p->x_recv;
+            yr[d] = p->y_recv;
+        }
+    }
+    return p2p_upload(c, flags, counts, xr, yr, st);
+}
+
+// Sync point `which` of call `val`.  IPC: device flags (release / acquire, system scope).
+// LOCAL: an event recorded on this rank's stream; the waiters pass a host barrier (so every
+// rank has enqueued its record, in program order before this wait) and enqueue stream waits.
+moe_status p2p_signal(moe_ctx c, int which, unsigned long long val, cudaStream_t st) {
+    if (c->local_ep) {
+        MOE_CUDA(c, cudaEventRecord(c->p2p_ev[which][val & 1], st));
+        return MOE_OK;
+    }
+    MOE_CUDA(c, launch_p2p_signal(c->p2p_tab, c->cfg.world_size, c->cfg.rank, which, val, st));
+    c->stats.kernel_launches += 1;
+    return MOE_OK;
+}
+
+moe_status p2p_wait(moe_ctx c, int which, unsigned long long val, cudaStream_t st) {
+    if (val == 0) return MOE_OK;   // call 0 never happened
+    const int W = c->cfg.world_size;
+    if (c->local_ep) {
+        LocalGroup* g = local_group(c);
+        g->barrier();
+        for (int d = 0; d < W; ++d)
+            if (d != c->cfg.rank)
+                MOE_CUDA(c, cudaStreamWaitEvent(st, g->ranks[d]->p2p_ev[which][val & 1], 0));
+        return MOE_OK;
+    }
+    MOE_CUDA(c, launch_p2p_wait(c->p2p_flags, W, which, val, c->p2p_diag_d, st));
+    c->stats.kernel_launches += 1;
+    return MOE_OK;
+}
+
+#define P2P_TRY(expr)                           \
+    do {                                        \
+        moe_status _s = (expr);                 \
+        if (_s != MOE_OK) return _s;            \
+    } while (0)
+
+}  // namespace
+
+moe_status p2p_before_dispatch(moe_ctx c, int T, cudaStream_t st) {
+    if (!c->p2p_ready) {
+        if (!c->local_ep)
+            return set_err(c, MOE_E_STATE, "IPC_EP context not connected (moe_ep_ipc_connect)");
+        moe_status s = p2p_connect_local(c, st);
+        if (s != MOE_OK) return s;
+    }
+    const moe_config& cf = c->cfg;
+    const int W = cf.world_size, ne = cf.num_experts, me = cf.rank;
+    const unsigned long long seq = ++c->p2p_seq;
+    const int par = (int)(seq & 1);
+    static const bool trace = getenv("MOE_P2P_TRACE") != nullptr;
+    if (trace) fprintf(stderr, "[p2p] rank %d call %llu T=%d stream=%p\n", me, seq, T, (void*)st);
+    // the push kernel also releases kFlagCounts on every peer (used by IPC; harmless in LOCAL)
+    MOE_CUDA(c, launch_p2p_push_counts(c->p2p_tab, c->counts, ne, W, me, par, seq, st));
+    c->stats.kernel_launches += 2;
+    if (c->local_ep) MOE_CUDA(c, cudaEventRecord(c->p2p_ev[kFlagCounts][par], st));
+    P2P_TRY(p2p_wait(c, kFlagCounts, seq, st));
+    MOE_CUDA(c, launch_p2p_plan(c->p2p_counts + (size_t)par * W * ne, W, ne, me, T, cf.top_k,
+                                cf.num_shared, c->cap_recv, c->n_all, cf.hidden, c->ep_grp,
+                                c->pr_x, c->pr_y, c->p2p_rows, c->p2p_bytes, st));
+    P2P_TRY(p2p_wait(c, kFlagXFree, seq - 1, st));
+    return MOE_OK;
+}
+
+moe_status p2p_after_dispatch(moe_ctx c, cudaStream_t st) {
+    const unsigned long long seq = c->p2p_seq;
+    P2P_TRY(p2p_signal(c, kFlagDispatched, seq, st));
+    P2P_TRY(p2p_wait(c, kFlagDispatched, seq, st));
+    P2P_TRY(p2p_wait(c, kFlagYDone, seq - 1, st));
+    return MOE_OK;
+}
+
+moe_status p2p_after_gemms(moe_ctx c, cudaStream_t st) {
+    const unsigned long long seq = c->p2p_seq;
+    P2P_TRY(p2p_signal(c, kFlagXFree, seq, st));
+    P2P_TRY(p2p_signal(c, kFlagYReady, seq, st));
+    P2P_TRY(p2p_wait(c, kFlagYReady, seq, st));
+    return MOE_OK;
+}
+
+moe_status p2p_after_combine(moe_ctx c, cudaStream_t st) {
+    return p2p_signal(c, kFlagYDone, c->p2p_seq, st);
 }
 
 }  // namespace moe
@@ -380,6 +496,55 @@ moe_status moe_nccl_unique_id(void* out128) {
     if (n->GetUniqueId(&id) != 0) return MOE_E_NCCL;
     memcpy(out128, &id, sizeof id);
     return MOE_OK;
+}
+
+moe_status moe_ep_ipc_handle(moe_ctx c, void* out) {
+    if (!c || !out) return MOE_E_INVAL;
+    if (!c->p2p || c->local_ep) return moe::set_err(c, MOE_E_STATE, "not an IPC_EP context");
+    MOE_CUDA(c, cudaSetDevice(c->cfg.device));
+    void* bufs[4] = {c->x_recv, c->y_recv, c->p2p_counts, c->p2p_flags};
+    static_assert(4 * sizeof(cudaIpcMemHandle_t) <= MOE_IPC_HANDLE_BYTES, "IPC blob size");
+    char* o = static_cast<char*>(out);
+    memset(o, 0, MOE_IPC_HANDLE_BYTES);
+    for (int i = 0; i < 4; ++i) {
+        cudaIpcMemHandle_t hnd;
+        MOE_CUDA(c, cudaIpcGetMemHandle(&hnd, bufs[i]));
+        memcpy(o + i * sizeof hnd, &hnd, sizeof hnd);
+    }
+    return MOE_OK;
+}
+
+moe_status moe_ep_ipc_connect(moe_ctx c, const void* all) {
+    if (!c || !all) return MOE_E_INVAL;
+    if (!c->p2p || c->local_ep || c->p2p_ready)
+        return moe::set_err(c, MOE_E_STATE, "not an unconnected IPC_EP context");
+    MOE_CUDA(c, cudaSetDevice(c->cfg.device));
+    const int W = c->cfg.world_size, me = c->cfg.rank;
+    unsigned long long* flags[moe::kMaxRanks];
+    int32_t* counts[moe::kMaxRanks];
+    __nv_bfloat16 *xr[moe::kMaxRanks], *yr[moe::kMaxRanks];
+    for (int d = 0; d < W; ++d) {
+        if (d == me) {
+            xr[d] = c->x_recv;
+            yr[d] = c->y_recv;
+            counts[d] = c->p2p_counts;
+            flags[d] = c->p2p_flags;
+            continue;
+        }
+        void* p[4];
+        for (int i = 0; i < 4; ++i) {
+            cudaIpcMemHandle_t hnd;
+            memcpy(&hnd, static_cast<const char*>(all) + (size_t)d * MOE_IPC_HANDLE_BYTES + i * sizeof hnd,
+                   sizeof hnd);
+            MOE_CUDA(c, cudaIpcOpenMemHandle(&p[i], hnd, cudaIpcMemLazyEnablePeerAccess));
+            c->ipc_opened[d][i] = p[i];
+        }
+        xr[d] = static_cast<__nv_bfloat16*>(p[0]);
+        yr[d] = static_cast<__nv_bfloat16*>(p[1]);
+        counts[d] = static_cast<int32_t*>(p[2]);
+        flags[d] = static_cast<unsigned long long*>(p[3]);
+    }
+    return moe::p2p_upload(c, flags, counts, xr, yr, c->copy_stream);
 }
 
 }  // extern "C"

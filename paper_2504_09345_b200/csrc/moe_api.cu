@@ -106,7 +106,8 @@ moe_status check_cfg(const moe_config* cfg) {
         cfg->top_k > moe::kMaxTopK || cfg->num_shared > moe::kMaxShared)
         return MOE_E_UNSUPPORTED;
     if (cfg->num_experts % cfg->world_size) return MOE_E_UNSUPPORTED;
-    if (cfg->world_size > 1 && !cfg->nccl_unique_id) return MOE_E_INVAL;
+    if (cfg->world_size > 1 && !cfg->nccl_unique_id && !(cfg->flags & MOE_FLAG_IPC_EP))
+        return MOE_E_INVAL;
     if (cfg->num_slots < 0 || cfg->num_slots == 1 || cfg->num_slots > moe::kMaxSlots)
         return MOE_E_INVAL;
     if (cfg->num_slots > 2 && cfg->num_slots >= cfg->num_experts / cfg->world_size + cfg->num_shared)
@@ -306,10 +307,16 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         p.end();
         c->stats.kernel_launches += 2;
     }
+    if (c->p2p) {   // P2P EP: counts exchange + plan before the permute writes into the owners
+        Prof p(c, moe::kRecComm, st);
+        moe_status s = moe::p2p_before_dispatch(c, T, st);
+        if (s != MOE_OK) return s;
+        p.end();
+    }
     {
         Prof p(c, moe::kRecPermute, st);
         MOE_CUDA(c, moe::launch_permute(hidden, T, h, k, ne, idx, c->tile_prefix, c->offsets,
-                                        c->x_perm, c->pos, st));
+                                        c->x_perm, c->pos, c->p2p ? c->pr_x : nullptr, st));
         p.end();
         c->stats.kernel_launches += 1;
     }
@@ -322,7 +329,7 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     __nv_bfloat16* y_routed = c->y_perm;
     if (c->ep) {
         Prof p(c, moe::kRecComm, st);
-        moe_status s = moe::ep_dispatch(c, T, st);
+        moe_status s = c->p2p ? moe::p2p_after_dispatch(c, st) : moe::ep_dispatch(c, T, st);
         if (s != MOE_OK) return s;
         p.end();
         tmA_routed = &c->tm_xrecv;
@@ -400,20 +407,26 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     }
     if (c->ep) {
         Prof p(c, moe::kRecComm, st);
-        moe_status s = moe::ep_combine(c, st);
+        moe_status s = c->p2p ? moe::p2p_after_gemms(c, st) : moe::ep_combine(c, st);
         if (s != MOE_OK) return s;
         p.end();
     }
     {
         Prof p(c, moe::kRecCombine, st);
         MOE_CUDA(c, moe::launch_combine(c->y_perm, c->pos, gates, T, h, k, S, (int64_t)T * k,
-                                        resid, out, st));
+                                        resid, out, idx, c->offsets,
+                                        c->p2p ? c->pr_y : nullptr, st));
         p.end();
         c->stats.kernel_launches += 1;
+    }
+    if (c->p2p) {
+        moe_status s = moe::p2p_after_combine(c, st);
+        if (s != MOE_OK) return s;
     }
     c->seq = q0 + c->n_all;
     c->last_rows = (int64_t)T * (k + S);
     c->stats.calls += 1;
+    MOE_CUDA(c, cudaEventRecord(c->done_ev, st));
     return MOE_OK;
 }
 
@@ -632,8 +645,10 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     c->num_sms = prop.multiProcessorCount;
     const int h = cfg->hidden, hi = cfg->ffn, ne = cfg->num_experts, k = cfg->top_k;
     const int S = cfg->num_shared, Tm = cfg->max_tokens, W = cfg->world_size;
-    c->ep = W > 1 || (cfg->flags & (MOE_FLAG_FORCE_EP | MOE_FLAG_LOCAL_EP));
+    c->ep = W > 1 || (cfg->flags & (MOE_FLAG_FORCE_EP | MOE_FLAG_LOCAL_EP | MOE_FLAG_IPC_EP));
     c->local_ep = (cfg->flags & MOE_FLAG_LOCAL_EP) != 0;
+    c->p2p = c->local_ep || (cfg->flags & MOE_FLAG_IPC_EP) != 0;
+    if (W > moe::kMaxRanks && c->p2p) return fail(MOE_E_UNSUPPORTED);
     c->n_local = ne / W;
     c->n_all = c->n_local + S;
     c->w13_bytes = 4ll * h * hi;
@@ -663,12 +678,18 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     bool ok = true;
     ok &= cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) == cudaSuccess;
     {
-        int least = 0, greatest = 0;
-        ok &= cudaDeviceGetStreamPriorityRange(&least, &greatest) == cudaSuccess;
-        ok &= cudaStreamCreateWithPriority(&c->token_stream, cudaStreamNonBlocking, greatest) ==
-              cudaSuccess;
-        ok &= cudaStreamCreateWithFlags(&c->clock_stream, cudaStreamNonBlocking) == cudaSuccess;
+        // Streams only where used: every extra stream shares the device's hardware work queues
+        // (CUDA_DEVICE_MAX_CONNECTIONS) with the other contexts of the process.
         if (const char* e = getenv("MOE_TOKEN_LANE")) c->token_lane = atoi(e) != 0;
+        if (c->token_lane) {
+            int least = 0, greatest = 0;
+            ok &= cudaDeviceGetStreamPriorityRange(&least, &greatest) == cudaSuccess;
+            ok &= cudaStreamCreateWithPriority(&c->token_stream, cudaStreamNonBlocking, greatest) ==
+                  cudaSuccess;
+        }
+        if (cfg->flags & MOE_FLAG_PROFILE)
+            ok &= cudaStreamCreateWithFlags(&c->clock_stream, cudaStreamNonBlocking) == cudaSuccess;
+        ok &= cudaEventCreateWithFlags(&c->done_ev, cudaEventDisableTiming) == cudaSuccess;
     }
     ok &= dalloc((void**)&c->slot_base, (size_t)c->blob_bytes * c->nslots);
     for (int i = 0; i < c->nslots; ++i) {
@@ -780,6 +801,7 @@ moe_status moe_layer_forward_host(moe_ctx ctx, const void* hidden_host, int32_t 
     MOE_CUDA(c, cudaEventRecord(c->xbuf_free[b], st));
     MOE_CUDA(c, cudaMemcpyAsync(out_host, c->out_dev[b], bytes, cudaMemcpyDeviceToHost, st));
     c->stats.d2h_token_bytes += (int64_t)bytes;
+    MOE_CUDA(c, cudaEventRecord(c->done_ev, st));   // moe_sync covers the result copy
     return MOE_OK;
 }
 
@@ -865,13 +887,23 @@ moe_status moe_taskb_forward_host(moe_ctx ctx, const void* attn_host, const void
     MOE_CUDA(c, cudaEventRecord(c->xbuf_free[b], st));
     MOE_CUDA(c, cudaMemcpyAsync(out_host, c->out_dev[b], bytes, cudaMemcpyDeviceToHost, st));
     c->stats.d2h_token_bytes += (int64_t)bytes;
+    MOE_CUDA(c, cudaEventRecord(c->done_ev, st));   // moe_sync covers the result copy
     return MOE_OK;
 }
 
 moe_status moe_sync(moe_ctx ctx) {
     if (!ctx) return MOE_E_INVAL;
+    if (ctx->p2p_diag_h && ctx->p2p_diag_h[0]) {   // a P2P flag wait timed out (ep_p2p.cu)
+        ctx->sticky = MOE_E_CUDA;
+        return set_err(ctx, MOE_E_CUDA,
+                       "P2P EP: rank %d timed out waiting for flag %lld of rank %lld to reach "
+                       "call %lld (saw %lld)", ctx->cfg.rank, ctx->p2p_diag_h[1],
+                       ctx->p2p_diag_h[2], ctx->p2p_diag_h[3], ctx->p2p_diag_h[4]);
+    }
     MOE_CUDA(ctx, cudaSetDevice(ctx->cfg.device));
-    MOE_CUDA(ctx, cudaDeviceSynchronize());
+    MOE_CUDA(ctx, cudaEventSynchronize(ctx->done_ev));     // the last call (see engine.h)
+    MOE_CUDA(ctx, cudaStreamSynchronize(ctx->copy_stream));
+    if (ctx->token_stream) MOE_CUDA(ctx, cudaStreamSynchronize(ctx->token_stream));
     if (ctx->comm && moe::nccl_api()) {
         moe::ncclResult_t r = 0;
         moe::nccl_api()->CommGetAsyncError(ctx->comm, &r);
@@ -901,6 +933,13 @@ moe_status moe_get_stats(moe_ctx ctx, moe_stats* out) {
     ctx->pending.clear();
     ctx->stats.num_slots = ctx->nslots;
     ctx->stats.comm_bytes = ctx->comm_bytes;
+    if (ctx->p2p && ctx->p2p_bytes) {   // P2P transport: counted on the device by the plan kernel
+        long long b = 0;
+        MOE_CUDA(ctx, cudaMemcpyAsync(&b, ctx->p2p_bytes, sizeof b, cudaMemcpyDeviceToHost,
+                                      ctx->copy_stream));
+        MOE_CUDA(ctx, cudaStreamSynchronize(ctx->copy_stream));
+        ctx->stats.comm_bytes = b;
+    }
     *out = ctx->stats;
     return MOE_OK;
 }
@@ -922,6 +961,16 @@ moe_status moe_debug_buffers(moe_ctx ctx, moe_debug_view* out) {
     out->h_act = ctx->h_act;
     out->y_perm = ctx->y_perm;
     out->rows = ctx->ep ? ctx->last_recv_rows : ctx->last_rows;
+    if (ctx->p2p && ctx->p2p_rows) {   // P2P transport: the plan kernel counted the rows
+        int32_t r = 0;
+        MOE_CUDA(ctx, cudaSetDevice(ctx->cfg.device));
+        moe_status s = moe_sync(ctx);
+        if (s != MOE_OK) return s;
+        MOE_CUDA(ctx, cudaMemcpyAsync(&r, ctx->p2p_rows, sizeof r, cudaMemcpyDeviceToHost,
+                                      ctx->copy_stream));
+        MOE_CUDA(ctx, cudaStreamSynchronize(ctx->copy_stream));
+        out->rows = r;
+    }
     out->h1 = ctx->h1_ws;
     out->moe_in = ctx->u_ws;
     out->taskb_tokens = ctx->last_taskb_T;
@@ -959,6 +1008,7 @@ moe_status moe_destroy(moe_ctx c) {
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->token_stream) cudaStreamDestroy(c->token_stream);
     if (c->clock_stream) cudaStreamDestroy(c->clock_stream);
+    if (c->done_ev) cudaEventDestroy(c->done_ev);
     cudaGetLastError();
     delete c;
     return MOE_OK;

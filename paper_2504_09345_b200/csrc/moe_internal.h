@@ -23,6 +23,46 @@ struct GemmGroup {
     int32_t pad;
 };
 
+// ------------------------------------------------------------ expert parallelism, P2P transport
+constexpr int kMaxRanks = 8;         // EP group size (one B200 box)
+// Row buffers of the EP group as seen by one rank (device-resident, rewritten by the plan kernel
+// every call): routed row (t, j) of expert e lives in rank e / nl's buffer at row
+// base[e] + (pos[t, j] - offsets[e]) -- base[e] is where this rank's block for expert e starts
+// in the owner's expert-major layout (moe_ep_plan's recv_off).
+struct PeerRows {
+    __nv_bfloat16* rows[kMaxRanks];
+    int32_t base[kMaxExperts];
+    int32_t nl;
+};
+
+// Per-call synchronisation of the P2P transport: each rank owns flags[kP2PFlags][kMaxRanks]
+// (uint64 call numbers) that its PEERS write (release, system scope) and it waits on (acquire).
+enum P2PFlag { kFlagCounts = 0, kFlagDispatched, kFlagXFree, kFlagYReady, kFlagYDone, kP2PFlags };
+struct P2PTable {   // device-resident: every rank's buffers, as mapped in this process
+    unsigned long long* flags[kMaxRanks];
+    int32_t* counts[kMaxRanks];      // [2][W][N_e] (call parity, source rank, expert)
+};
+// Push this rank's per-expert counts into every peer's counts[par][me][:], then release
+// kFlagCounts = seq on every peer.
+cudaError_t launch_p2p_push_counts(const P2PTable* tab, const int32_t* counts, int ne, int W,
+                                   int me, int par, unsigned long long seq, cudaStream_t st);
+// flags[which][me] = val on every peer (after a system-scope fence).
+cudaError_t launch_p2p_signal(const P2PTable* tab, int W, int me, int which,
+                              unsigned long long val, cudaStream_t st);
+// Spin (acquire, system scope) until my flags[which][s] >= val for every rank s; traps after
+// ~20 s (a lost peer must not hang the GPU), first writing {1, which, s, val, seen} to the
+// host-mapped diag[5] (nullable).
+cudaError_t launch_p2p_wait(const unsigned long long* flags, int W, int which,
+                            unsigned long long val, long long* diag, cudaStream_t st);
+// From counts[par] (all ranks' per-expert counts): this rank's GEMM groups over x_recv
+// (expert-major, moe_ep_plan's layout) + shared-expert groups, the send bases of pr_x / pr_y
+// (where this rank's rows for expert e start in the owner's buffers), rows received (rows_out)
+// and bytes sent (+= bytes_acc).
+cudaError_t launch_p2p_plan(const int32_t* counts_par, int W, int ne, int me, int T, int k,
+                            int S, long long cap_recv, int n_all, int h, GemmGroup* grp,
+                            PeerRows* pr_x, PeerRows* pr_y, int32_t* rows_out,
+                            long long* bytes_acc, cudaStream_t st);
+
 // ---------------------------------------------------------------------------- routing kernels
 // a2+a3: router GEMM (fp64, ascending c) + warp-shuffle top-k + softmax gates + per-tile counts.
 cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_bfloat16* wr,
@@ -34,15 +74,21 @@ cudaError_t launch_scan(const int32_t* tile_counts, int n_tiles, int ne, int T, 
                         int num_shared, int32_t* tile_prefix, int32_t* offsets, int32_t* counts,
                         GemmGroup* grp1, GemmGroup* grp2, cudaStream_t st);
 // a4 (permute): stable position of every (t, j) and 16-byte row copies X[t] -> X_perm[pos].
+//   pr != NULL (P2P expert parallelism): the row goes straight to its expert owner's x_recv
+//   (PeerRows, possibly another GPU's memory) -- permute and dispatch in one kernel; each
+//   thread ends with a system-scope fence so a following flag release covers its stores.
 cudaError_t launch_permute(const __nv_bfloat16* x, int T, int h, int k, int ne,
                            const int32_t* idx, const int32_t* tile_prefix,
                            const int32_t* offsets, __nv_bfloat16* x_perm, int32_t* pos,
-                           cudaStream_t st);
+                           const PeerRows* pr, cudaStream_t st);
 // a7: out[t] = sum_j g[t,j] * Y[pos[t,j]] + sum_s Y[R + s*T + t] (+ resid[t] if resid != NULL)
-//     (fp32, fixed order) -> bf16.
+//     (fp32, fixed order) -> bf16.  pr != NULL (P2P expert parallelism): routed rows are read
+//     from their owners' y_recv (PeerRows; needs idx and offsets), shared rows from y_perm.
 cudaError_t launch_combine(const __nv_bfloat16* y_perm, const int32_t* pos, const float* gates,
                            int T, int h, int k, int num_shared, int64_t shared_base,
-                           const __nv_bfloat16* resid, __nv_bfloat16* out, cudaStream_t st);
+                           const __nv_bfloat16* resid, __nv_bfloat16* out,
+                           const int32_t* idx, const int32_t* offsets, const PeerRows* pr,
+                           cudaStream_t st);
 // Task B (b2): u[t] = RMSNorm(h1[t]) * gamma, reading R21:
 //   r = 1 / sqrt(sum_c h1[t,c]^2 / h + eps)  (fp64),  n = bf16(float(h1 * r)),
 //   u = bf16(float(gamma) * float(n))  (fp32 multiply).

@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(256)
 permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int h, int k, int ne,
                const int32_t* __restrict__ idx, const int32_t* __restrict__ tile_prefix,
                const int32_t* __restrict__ offsets, __nv_bfloat16* __restrict__ x_perm,
-               int32_t* __restrict__ pos_out) {
+               int32_t* __restrict__ pos_out, const PeerRows* __restrict__ pr) {
     __shared__ int sidx[kRouteTile * kMaxTopK];
     __shared__ int spos[kPermuteTokens * kMaxTopK];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -303,9 +303,20 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int h, int k, int ne,
         const int t = tbase + tt0 + q;
         if (t >= T) break;
         const int4* src = reinterpret_cast<const int4*>(x + (size_t)t * h);
-        int dst_row[kMaxTopK];
+        __nv_bfloat16* dst_ptr[kMaxTopK];
 #pragma unroll
-        for (int j = 0; j < kMaxTopK; ++j) dst_row[j] = (j < k) ? spos[q * k + j] : 0;
+        for (int j = 0; j < kMaxTopK; ++j) {
+            dst_ptr[j] = x_perm;
+            if (j < k) {
+                const int p = spos[q * k + j];
+                if (pr) {   // straight into the expert owner's x_recv (P2P dispatch)
+                    const int e = sidx[(tt0 + q) * k + j];
+                    dst_ptr[j] = pr->rows[e / pr->nl] + (size_t)(pr->base[e] + p - offsets[e]) * h;
+                } else {
+                    dst_ptr[j] = x_perm + (size_t)p * h;
+                }
+            }
+        }
         constexpr int U = 4;
         for (int v0 = lane; v0 < nvec; v0 += 32 * U) {
             int4 buf[U];
@@ -315,7 +326,7 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int h, int k, int ne,
                 if (v < nvec) buf[u] = ptx::ld_nc_v4(src + v);
             }
             for (int j = 0; j < k; ++j) {
-                int4* dst = reinterpret_cast<int4*>(x_perm + (size_t)dst_row[j] * h);
+                int4* dst = reinterpret_cast<int4*>(dst_ptr[j]);
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int v = v0 + 32 * u;
@@ -324,6 +335,7 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int h, int k, int ne,
             }
         }
     }
+    if (pr) __threadfence_system();   // peer stores performed before the dispatch flag release
 }
 
 // Warp per token; lane handles 8 consecutive columns per 16-byte vector.
@@ -331,16 +343,27 @@ __global__ void __launch_bounds__(256)
 combine_kernel(const __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ pos,
                const float* __restrict__ gates, int T, int h, int k, int num_shared,
                int64_t shared_base, const __nv_bfloat16* __restrict__ resid,
-               __nv_bfloat16* __restrict__ out) {
+               __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ idx,
+               const int32_t* __restrict__ offsets, const PeerRows* __restrict__ pr) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int t = blockIdx.x * 8 + warp;
     if (t >= T) return;
-    int prow[kMaxTopK];
+    const __nv_bfloat16* prow[kMaxTopK];
     float g[kMaxTopK];
 #pragma unroll
     for (int j = 0; j < kMaxTopK; ++j) {
-        prow[j] = (j < k) ? pos[(size_t)t * k + j] : 0;
-        g[j] = (j < k) ? gates[(size_t)t * k + j] : 0.f;
+        prow[j] = y;
+        g[j] = 0.f;
+        if (j < k) {
+            const int p = pos[(size_t)t * k + j];
+            g[j] = gates[(size_t)t * k + j];
+            if (pr) {   // the expert owner's y_recv (P2P combine)
+                const int e = idx[(size_t)t * k + j];
+                prow[j] = pr->rows[e / pr->nl] + (size_t)(pr->base[e] + p - offsets[e]) * h;
+            } else {
+                prow[j] = y + (size_t)p * h;
+            }
+        }
     }
     const int nvec = h / 8;
     for (int v = lane; v < nvec; v += 32) {
@@ -348,7 +371,7 @@ combine_kernel(const __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ 
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] = 0.f;
         for (int j = 0; j < k; ++j) {
-            const int4 raw = ptx::ld_nc_v4(reinterpret_cast<const int4*>(y + (size_t)prow[j] * h) + v);
+            const int4 raw = ptx::ld_nc_v4(reinterpret_cast<const int4*>(prow[j]) + v);
             const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -428,20 +451,22 @@ cudaError_t launch_scan(const int32_t* tile_counts, int n_tiles, int ne, int T, 
 cudaError_t launch_permute(const __nv_bfloat16* x, int T, int h, int k, int ne,
                            const int32_t* idx, const int32_t* tile_prefix,
                            const int32_t* offsets, __nv_bfloat16* x_perm, int32_t* pos,
-                           cudaStream_t st) {
+                           const PeerRows* pr, cudaStream_t st) {
     const int n_tiles = (T + kRouteTile - 1) / kRouteTile;
     if (n_tiles == 0) return cudaSuccess;
     permute_kernel<<<n_tiles * (kRouteTile / kPermuteTokens), 256, 0, st>>>(
-        x, T, h, k, ne, idx, tile_prefix, offsets, x_perm, pos);
+        x, T, h, k, ne, idx, tile_prefix, offsets, x_perm, pos, pr);
     return cudaGetLastError();
 }
 
 cudaError_t launch_combine(const __nv_bfloat16* y_perm, const int32_t* pos, const float* gates,
                            int T, int h, int k, int num_shared, int64_t shared_base,
-                           const __nv_bfloat16* resid, __nv_bfloat16* out, cudaStream_t st) {
+                           const __nv_bfloat16* resid, __nv_bfloat16* out,
+                           const int32_t* idx, const int32_t* offsets, const PeerRows* pr,
+                           cudaStream_t st) {
     if (T == 0) return cudaSuccess;
     combine_kernel<<<(T + 7) / 8, 256, 0, st>>>(y_perm, pos, gates, T, h, k, num_shared,
-                                                shared_base, resid, out);
+                                                shared_base, resid, out, idx, offsets, pr);
     return cudaGetLastError();
 }
 

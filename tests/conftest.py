@@ -3,6 +3,11 @@ import sys
 
 import pytest
 
+# In-process expert-parallel tests put W ranks (2 streams each) on ONE GPU; their device-side
+# flag waits must not share a hardware work queue with the peer work they wait for, so give the
+# process the maximum number of queues (read once, before CUDA initialises).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

@@ -1,0 +1,57 @@
+"""Worker of tests/test_gpu_ep_ipc.py: one process = one expert-parallel rank (MOE_FLAG_IPC_EP).
+
+The ranks exchange their CUDA IPC handles through a gloo process group (127.0.0.1), connect,
+run `calls` MoE-layer calls on their token slice and return (rank, idx, out bits) through the
+queue.  All ranks may share one GPU (the test box has one): CUDA IPC maps same-device memory
+across processes like peer memory, so the P2P transport runs unchanged."""
+import os
+import sys
+
+
+def run_rank(rank, world, port, cfg_tuple, calls, device, q):
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if root not in sys.path:
+        sys.path.insert(0, root)
+    try:
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+
+        import synth
+        from paper_2504_09345_b200 import HostExperts, MoELayer
+
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(device)
+        cfg = synth.MoEConfig(*cfg_tuple)
+        inp = synth.gen_inputs(cfg)
+        ne, nl, S, T = cfg.num_experts, cfg.num_experts // world, cfg.num_shared, cfg.tokens
+        lo, hi = T * rank // world, T * (rank + 1) // world
+        ids = list(range(rank * nl, (rank + 1) * nl)) + [ne + s for s in range(S)]
+        experts = HostExperts(cfg.hidden, cfg.ffn, [inp.w1[i] for i in ids],
+                              [inp.w3[i] for i in ids], [inp.w2[i] for i in ids])
+        layer = MoELayer(cfg.hidden, cfg.ffn, ne, cfg.top_k, max(1, hi - lo), num_shared=S,
+                         device=device, world_size=world, rank=rank, ipc_ep=True)
+        handles = [None] * world
+        dist.all_gather_object(handles, layer.ipc_handle())
+        layer.ipc_connect(handles)
+        router = torch.from_numpy(inp.router.view(np.int16)).view(torch.bfloat16).cuda()
+        x = torch.from_numpy(np.ascontiguousarray(inp.x[lo:hi]).view(np.int16)).view(torch.bfloat16)
+        x = x.reshape(-1, cfg.hidden).cuda()
+        out = torch.empty_like(x)
+        idx = torch.empty((x.shape[0], cfg.top_k), dtype=torch.int32, device="cuda")
+        s = torch.cuda.Stream()
+        for _ in range(calls):
+            layer.forward(x, router, experts, out, idx, stream=s.cuda_stream)
+        s.synchronize()
+        layer.sync()
+        st = layer.stats()
+        q.put((rank, idx.cpu().numpy(), out.view(torch.int16).cpu().numpy(), st["comm_bytes"],
+               None))
+        dist.barrier()          # peers may still read this rank's y_recv until they are done
+        layer.close()
+        experts.close()
+        dist.destroy_process_group()
+    except Exception as e:  # reported by the parent
+        import traceback
+        q.put((rank, None, None, None, traceback.format_exc()))

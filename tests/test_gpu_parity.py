@@ -346,9 +346,11 @@ def test_staging_slot_counts_back_to_back(slots):
 ])
 def test_ep_local_transport_world_ranks(world, shape):
     """MOE_FLAG_LOCAL_EP: W contexts on this GPU, one host thread per rank, each streaming ONLY
-    its N_e/W experts (+ replicated shared ones) and owning T/W tokens; the exchange plan,
-    expert-major receive layout, dispatch/combine offsets and group tables are the NCCL path's.
-    Every rank's output must equal the oracle on its token slice and, bitwise, the one-GPU
+    its N_e/W experts (+ replicated shared ones) and owning T/W tokens, exchanging rows over
+    peer memory (the P2P transport: permute writes into the owners' x_recv, combine reads their
+    y_recv, device flags order the calls -- no host sync).  The plan and expert-major receive
+    layout are the NCCL path's (moe_ep_plan).  Three calls (both counts buffers, flag reuse);
+    every rank's output must equal the oracle on its token slice and, bitwise, the one-GPU
     (non-EP) result for the same tokens."""
     import os
     import threading
@@ -375,25 +377,36 @@ def test_ep_local_transport_world_ranks(world, shape):
                                max(1, bounds[r + 1] - bounds[r]), num_shared=S, world_size=world,
                                rank=r, nccl_unique_id=key, local_ep=True))
 
+    # Device memory is set up before the rank threads start: an allocation (or any device-wide
+    # sync) in one rank's thread could wait on the other ranks' in-flight flag waits.
+    bufs = []
+    for r in range(world):
+        x = bf16_tensor(inp.x[bounds[r]:bounds[r + 1]].reshape(-1, cfg.hidden))
+        bufs.append((torch.cuda.Stream(), x, torch.empty_like(x),
+                     torch.empty((x.shape[0], cfg.top_k), dtype=torch.int32, device="cuda")))
+    torch.cuda.synchronize()
+
     def work(r):
         try:
-            s = torch.cuda.Stream()
-            x = bf16_tensor(inp.x[bounds[r]:bounds[r + 1]].reshape(-1, cfg.hidden))
-            o = torch.empty_like(x)
-            idx = torch.empty((x.shape[0], cfg.top_k), dtype=torch.int32, device="cuda")
-            for _ in range(2):   # twice: buffers and plans are reused across calls
+            s, x, o, idx = bufs[r]
+            for _ in range(3):   # buffers, flags and both counts parities reused across calls
                 layers[r].forward(x, full.router, experts[r], o, idx, stream=s.cuda_stream)
             s.synchronize()
             outs[r], idxs[r] = o, idx
-        except Exception as e:  # surfaced below
-            errors.append((r, e))
+        except Exception as e:  # surfaced below, with the library's diagnosis if it has one
+            msg = repr(e)[:300]
+            try:
+                layers[r].sync()
+            except Exception as e2:
+                msg += f" | sync: {e2!r}"[:300]
+            errors.append((r, msg))
 
     threads = [threading.Thread(target=work, args=(r,)) for r in range(world)]
     for t in threads:
         t.start()
     for t in threads:
         t.join(timeout=300)
-    assert not errors, errors
+    assert not errors, "\n".join(f"rank {r}: {str(e)[:300]}" for r, e in errors)
     for r in range(world):
         lo, hi = bounds[r], bounds[r + 1]
         if hi == lo:
@@ -402,7 +415,9 @@ def test_ep_local_transport_world_ranks(world, shape):
         assert token_rel_err(to_f32(outs[r]), y_ref[lo:hi]).max() <= TOL
         assert torch.equal(outs[r], out_full[lo:hi]), f"rank {r} differs from the 1-GPU result"
     st = [l.stats() for l in layers]
-    assert sum(s["h2d_weight_bytes"] for s in st) == 2 * (ne + world * S) * 6 * cfg.hidden * cfg.ffn
+    assert sum(s["h2d_weight_bytes"] for s in st) == 3 * (ne + world * S) * 6 * cfg.hidden * cfg.ffn
+    # every routed row crosses once each way: 2 x T*k rows of h bf16 per call, all ranks
+    assert sum(s["comm_bytes"] for s in st) == 3 * 2 * T * cfg.top_k * cfg.hidden * 2
     for l in layers:
         l.close()
     for e in experts:
