@@ -48,7 +48,11 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--taskb", action="store_true",
                     help="time GPU Task B (O-projection + RMSNorm + MoE layer, streamed Wo) "
-                         "instead of the MoE layer alone (no e2e / cpu legs)")
+                         "instead of the MoE layer alone (no cpu leg)")
+    ap.add_argument("--ep-transport", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1: p2p = fused dispatch/combine over peer memory (CUDA IPC), "
+                         "falling back to NCCL if the peers cannot be mapped; nccl = NCCL "
+                         "all-to-all")
     return ap.parse_args()
 
 
@@ -188,9 +192,18 @@ def run_ours(args):
     from paper_2504_09345_b200 import ledger
 
     rank, world, local = dist_env()
+    # MOE_BENCH_SHARE_GPU=1 (path check only, timings meaningless): every rank on GPU 0 and a
+    # gloo group for the bench's own plumbing -- exercises the N > 1 code path on a 1-GPU box
+    # with the P2P transport (NCCL refuses two ranks on one GPU).
+    share = os.environ.get("MOE_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if rank == 0:
         moe_build.build()
     if world > 1:
@@ -232,14 +245,35 @@ def run_ours(args):
         dist.barrier()   # all ranks probe their host links at the same time (shared host DRAM)
     probe_gbs = moe.moe_probe_h2d(local, 1 << 30, 5)   # paper's method: 1 GB pinned H2D copies
     uid = None
-    if world > 1:
+    transport = "single" if world == 1 else args.ep_transport
+    layer = None
+    if transport == "p2p":   # CUDA IPC peer mapping; every rank must succeed, else NCCL
+        try:
+            layer = moe.MoELayer(cfg.hidden, cfg.ffn, cfg.num_experts, cfg.top_k, Tr,
+                                 num_shared=cfg.num_shared, device=local, profile=True,
+                                 packet_bytes=int(args.packet_mb * 2 ** 20), world_size=world,
+                                 rank=rank, num_slots=args.slots, ipc_ep=True)
+            handles = [None] * world
+            dist.all_gather_object(handles, layer.ipc_handle())
+            layer.ipc_connect(handles)
+            ok = 1.0
+        except Exception as e:  # noqa: BLE001 -- reported, then the NCCL transport
+            print(f"[bench] rank {rank}: P2P transport unavailable ({e}); using NCCL",
+                  file=sys.stderr, flush=True)
+            ok = 0.0
+        if allmax(1.0 - ok) > 0:
+            if layer is not None:
+                layer.close()
+            layer, transport = None, "nccl"
+    if world > 1 and transport == "nccl":
         obj = [moe.moe_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
-    layer = moe.MoELayer(cfg.hidden, cfg.ffn, cfg.num_experts, cfg.top_k, Tr,
-                         num_shared=cfg.num_shared, device=local, profile=True,
-                         packet_bytes=int(args.packet_mb * 2 ** 20), world_size=world, rank=rank,
-                         nccl_unique_id=uid, num_slots=args.slots)
+    if layer is None:
+        layer = moe.MoELayer(cfg.hidden, cfg.ffn, cfg.num_experts, cfg.top_k, Tr,
+                             num_shared=cfg.num_shared, device=local, profile=True,
+                             packet_bytes=int(args.packet_mb * 2 ** 20), world_size=world,
+                             rank=rank, nccl_unique_id=uid, num_slots=args.slots)
     stream = torch.cuda.Stream()
     sh = stream.cuda_stream
     layer_bytes = 0
@@ -392,7 +426,7 @@ def run_ours(args):
                        "layers_cycled": args.layers, "staging_slots": st["num_slots"],
                        "packet_mb": args.packet_mb,
                        "l2": "inputs larger than L2: all expert weights re-streamed from host each step",
-                       "parallelism": f"ep{world}"},
+                       "parallelism": f"ep{world}", "ep_transport": transport},
             "roofline": roofline, "roofline_step": roofline_step,
             "per_kernel_ms_per_step_rank0": per_kernel_ms,
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
