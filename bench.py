@@ -434,6 +434,9 @@ def run_ours(args):
             "gpu_launches_per_step": launches / args.steps}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    layer.sync()
+    if world > 1:
+        dist.barrier()   # P2P: peers may read this rank's buffers until their last combine ends
     layer.close()
     for e in experts:
         e.close()
