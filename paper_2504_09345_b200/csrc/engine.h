@@ -82,8 +82,14 @@ struct moe_ctx_s {
     cudaEvent_t ready13[moe::kMaxSlots] = {}, ready2[moe::kMaxSlots] = {};
     cudaEvent_t slot_free[moe::kMaxSlots] = {};
     uint64_t seq = 0;  // streamed-item counter across calls: item q uses slot q % nslots
-    CUtensorMap tm_w13[moe::kMaxSlots], tm_w2[moe::kMaxSlots];
-    CUtensorMap tm_w13_pair[moe::kMaxSlots], tm_w2_pair[moe::kMaxSlots];  // 128-row boxes (pair GEMM)
+    // The staging buffer seen as one W13 matrix [nslots * 3 h_i, h] and one W2 matrix
+    // [nslots * 3 h, h_i]: slot s's W13 starts at row 3 h_i s, its W2 at row 3 h s + 2 h, so one
+    // GEMM launch can cover experts in different slots (GemmBatch::b_row).
+    CUtensorMap tm_w13, tm_w2;
+    CUtensorMap tm_w13_pair, tm_w2_pair;   // 128-row boxes (CTA-pair GEMM)
+    // DMA batches (flush_copies): slot s holds item batch_q0[s] + j of a batch of batch_n[s]
+    uint64_t batch_q0[moe::kMaxSlots] = {};
+    int batch_n[moe::kMaxSlots] = {};
     int pair_mode = -1;       // MOE_GEMM_PAIR: 0 never, 1 always, -1 auto (default: wave model)
 
     // workspace

@@ -27,13 +27,16 @@ constexpr int BM = 128;
 constexpr int BK = 64;  // one 128-byte swizzle atom of bf16
 constexpr int kThreads = 256;
 
+constexpr size_t kBatchReserve = 512;   // shared memory for BatchInfo (below)
+
 template <int BN>
 struct GemmCfg {
     static constexpr int kStages = (BN == 256) ? 4 : 6;
     static constexpr uint32_t kABytes = BM * BK * 2;
     static constexpr uint32_t kBBytes = BN * BK * 2;
     static constexpr uint32_t kTmemCols = 2 * BN;
-    static constexpr size_t kSmem = 1024 /*align slack*/ + kStages * (kABytes + kBBytes) + 256;
+    static constexpr size_t kSmem =
+        1024 /*align slack*/ + kStages * (kABytes + kBBytes) + kBatchReserve + 256;
 };
 
 // Persistent tile order: groups of `gm` M tiles, M fastest inside a group, then N.  The ~148
@@ -128,10 +131,48 @@ __device__ __forceinline__ void epilogue_row(uint32_t taddr, bool valid, __nv_bf
     }
 }
 
+// The groups of one launch (up to kMaxBatch experts whose weights sit in different staging slots
+// of one tensor map), resolved once per CTA into shared memory: global tile t belongs to group
+// g with first[g] <= t < first[g + 1]; inside a group tiles follow tile_coords().
+struct BatchInfo {
+    int n, total;
+    int first[kMaxBatch + 1];
+    int m_tiles[kMaxBatch];
+    int a_begin[kMaxBatch], a_end[kMaxBatch], out_base[kMaxBatch], b_row[kMaxBatch];
+};
+constexpr size_t kBatchSmem = (sizeof(BatchInfo) + 15) & ~size_t(15);
+static_assert(kBatchSmem <= kBatchReserve, "BatchInfo does not fit its reservation");
+
+__device__ __forceinline__ void batch_init(BatchInfo* bi, const GemmBatch& b, int bm,
+                                           int n_tiles) {
+    int t = 0;
+    for (int i = 0; i < b.n; ++i) {
+        const GemmGroup g = b.table[b.idx[i]];
+        const int rows = max(0, g.a_end - g.a_begin);
+        bi->a_begin[i] = g.a_begin;
+        bi->a_end[i] = g.a_end;
+        bi->out_base[i] = g.out_base;
+        bi->b_row[i] = b.b_row[i];
+        bi->m_tiles[i] = (rows + bm - 1) / bm;
+        bi->first[i] = t;
+        t += bi->m_tiles[i] * n_tiles;
+    }
+    bi->first[b.n] = t;
+    bi->n = b.n;
+    bi->total = t;
+}
+
+__device__ __forceinline__ int batch_locate(const BatchInfo* bi, int tile, int& local) {
+    int g = 0;
+    while (tile >= bi->first[g + 1]) ++g;
+    local = tile - bi->first[g];
+    return g;
+}
+
 template <int BN, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 expert_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const GemmGroup* __restrict__ group, int N, int K,
+                   const __grid_constant__ GemmBatch batch, int N, int K,
                    __nv_bfloat16* __restrict__ out, int ldo,
                    const __nv_bfloat16* __restrict__ resid) {
     using C = GemmCfg<BN>;
@@ -141,18 +182,17 @@ expert_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + S * C::kABytes;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * C::kBBytes);
+    BatchInfo* bi = reinterpret_cast<BatchInfo*>(sB + S * C::kBBytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(bi) + kBatchSmem);
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-    const GemmGroup g = *group;
-    const int rows = g.a_end - g.a_begin;
-    if (rows <= 0) return;
-    const int m_tiles = (rows + BM - 1) / BM;
     const int n_tiles = N / BN;
-    const int total = m_tiles * n_tiles;
+    if (threadIdx.x == 0) batch_init(bi, batch, BM, n_tiles);
+    __syncthreads();
+    const int total = bi->total;
     if ((int)blockIdx.x >= total) return;
     const int num_kb = K / BK;
     // rows per raster group: A footprint ~32 MB (measured at 65k tokens, K=4096: group 16 ->
@@ -190,9 +230,10 @@ expert_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-                int m, n;
-                tile_coords(tile, m_tiles, n_tiles, group_m, m, n);
-                const int arow = g.a_begin + m * BM, brow = n * BN;
+                int m, n, local;
+                const int gi = batch_locate(bi, tile, local);
+                tile_coords(local, bi->m_tiles[gi], n_tiles, group_m, m, n);
+                const int arow = bi->a_begin[gi] + m * BM, brow = bi->b_row[gi] + n * BN;
                 for (int kb = 0; kb < num_kb; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1u);
                     ptx::mbar_arrive_expect_tx(&full[stage], C::kABytes + C::kBBytes);
@@ -247,14 +288,15 @@ expert_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
             const int acc = it & 1;
             const uint32_t aphase = (it >> 1) & 1;
-            int m, n;
-            tile_coords(tile, m_tiles, n_tiles, group_m, m, n);
+            int m, n, local;
+            const int gi = batch_locate(bi, tile, local);
+            tile_coords(local, bi->m_tiles[gi], n_tiles, group_m, m, n);
             ptx::mbar_wait(&tfull[acc], aphase);
             ptx::tc_fence_after();
             const int r = q * 32 + lane;
-            const int arow = g.a_begin + m * BM + r;
-            const bool valid = arow < g.a_end;
-            const int64_t orow = (int64_t)g.out_base + (arow - g.a_begin);
+            const int arow = bi->a_begin[gi] + m * BM + r;
+            const bool valid = arow < bi->a_end[gi];
+            const int64_t orow = (int64_t)bi->out_base[gi] + (arow - bi->a_begin[gi]);
             const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
             epilogue_row<BN, MODE>(taddr, valid, out + orow * ldo,
                                    resid ? resid + orow * ldo : nullptr, n);
@@ -282,22 +324,24 @@ expert_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
 constexpr int kPairStages = 6;
 constexpr uint32_t kPairABytes = 128 * BK * 2;   // per CTA
 constexpr uint32_t kPairBBytes = 128 * BK * 2;   // per CTA (half of a 256-row B tile)
-constexpr size_t kPairSmem = 1024 + kPairStages * (kPairABytes + kPairBBytes) + 256;
+constexpr size_t kPairSmem =
+    1024 + kPairStages * (kPairABytes + kPairBBytes) + kBatchReserve + 256;
 
 template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 expert_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
-                        const GemmGroup* __restrict__ group, int N, int K,
+                        const __grid_constant__ GemmBatch batch, int N, int K,
                         __nv_bfloat16* __restrict__ out, int ldo,
-                   const __nv_bfloat16* __restrict__ resid) {
+                        const __nv_bfloat16* __restrict__ resid) {
     constexpr int BN = 256, PM = 256, S = kPairStages;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + S * kPairABytes;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * kPairBBytes);
+    BatchInfo* bi = reinterpret_cast<BatchInfo*>(sB + S * kPairBBytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(bi) + kBatchSmem);
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;
     uint64_t* tempty = tfull + 2;
@@ -306,12 +350,10 @@ expert_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
     const uint32_t rank = ptx::cluster_ctarank();
     const bool leader = rank == 0;
     const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-    const GemmGroup g = *group;
-    const int rows = g.a_end - g.a_begin;
-    if (rows <= 0) return;                       // uniform over the cluster
-    const int m_tiles = (rows + PM - 1) / PM;
     const int n_tiles = N / BN;
-    const int total = m_tiles * n_tiles;
+    if (threadIdx.x == 0) batch_init(bi, batch, PM, n_tiles);
+    __syncthreads();
+    const int total = bi->total;                 // identical in both CTAs of the cluster
     if (pair >= total) return;                   // both CTAs of a pair leave together
     const int num_kb = K / BK;
     const int group_m = g_group_m > 0 ? g_group_m : ((K <= 8192) ? 16 : 4);  // 256-row tiles
@@ -346,10 +388,11 @@ expert_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = pair; tile < total; tile += npairs) {
-                int m, n;
-                tile_coords(tile, m_tiles, n_tiles, group_m, m, n);
-                const int arow = g.a_begin + m * PM + (int)rank * 128;
-                const int brow = n * BN + (int)rank * 128;
+                int m, n, local;
+                const int gi = batch_locate(bi, tile, local);
+                tile_coords(local, bi->m_tiles[gi], n_tiles, group_m, m, n);
+                const int arow = bi->a_begin[gi] + m * PM + (int)rank * 128;
+                const int brow = bi->b_row[gi] + n * BN + (int)rank * 128;
                 for (int kb = 0; kb < num_kb; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1u);
                     const uint32_t fbar = full0 + stage * 8;
@@ -404,13 +447,14 @@ expert_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
         for (int tile = pair; tile < total; tile += npairs, ++it) {
             const int acc = it & 1;
             const uint32_t aphase = (it >> 1) & 1;
-            int m, n;
-            tile_coords(tile, m_tiles, n_tiles, group_m, m, n);
+            int m, n, local;
+            const int gi = batch_locate(bi, tile, local);
+            tile_coords(local, bi->m_tiles[gi], n_tiles, group_m, m, n);
             ptx::mbar_wait(&tfull[acc], aphase);
             ptx::tc_fence_after();
-            const int arow = g.a_begin + m * PM + (int)rank * 128 + q * 32 + lane;
-            const bool valid = arow < g.a_end;
-            const int64_t orow = (int64_t)g.out_base + (arow - g.a_begin);
+            const int arow = bi->a_begin[gi] + m * PM + (int)rank * 128 + q * 32 + lane;
+            const bool valid = arow < bi->a_end[gi];
+            const int64_t orow = (int64_t)bi->out_base[gi] + (arow - bi->a_begin[gi]);
             const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
             epilogue_row<BN, MODE>(taddr, valid, out + orow * ldo,
                                    resid ? resid + orow * ldo : nullptr, n);
@@ -561,7 +605,7 @@ template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 expert_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmW,
                         const __grid_constant__ TokenMaps tmX,
-                        const GemmGroup* __restrict__ group, int M, int K,
+                        const __grid_constant__ GemmBatch batch, int M, int K,
                         __nv_bfloat16* __restrict__ out, int ldo,
                         const __nv_bfloat16* __restrict__ resid) {
     constexpr int S = kSwapStages;
@@ -580,7 +624,8 @@ expert_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmW,
     const uint32_t rank = ptx::cluster_ctarank();
     const bool leader = rank == 0;
     const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-    const GemmGroup g = *group;
+    const GemmGroup g = batch.table[batch.idx[0]];   // one group per launch (host checks)
+    const int wrow0 = batch.b_row[0];
     const int rows = g.a_end - g.a_begin;
     if (rows <= 0) return;                       // uniform over the cluster
     const int m_tiles = M / 256;
@@ -620,7 +665,7 @@ expert_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmW,
             uint32_t phase = 0;
             int m, col, nc;
             while (sc.next(m, col, nc)) {
-                const int wrow = m * 256 + (int)rank * 128;
+                const int wrow = wrow0 + m * 256 + (int)rank * 128;
                 const int half = nc >> 1;                      // token rows of this CTA
                 const int trow = g.a_begin + col + (int)rank * half;
                 for (int kb = 0; kb < num_kb; ++kb) {
@@ -713,20 +758,20 @@ expert_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmW,
 }
 
 template <int MODE>
-cudaError_t launch_swap(const CUtensorMap* tmW, const TokenMaps* tmX, const GemmGroup* group,
+cudaError_t launch_swap(const CUtensorMap* tmW, const TokenMaps* tmX, const GemmBatch& batch,
                         int M, int K, __nv_bfloat16* out, int ldo, const __nv_bfloat16* resid,
                         int grid, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(expert_gemm_swap_kernel<MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kSwapSmem);   // every launch, see launch_pair
     if (e != cudaSuccess) return e;
-    expert_gemm_swap_kernel<MODE><<<grid & ~1, kThreads, kSwapSmem, st>>>(*tmW, *tmX, group, M, K,
+    expert_gemm_swap_kernel<MODE><<<grid & ~1, kThreads, kSwapSmem, st>>>(*tmW, *tmX, batch, M, K,
                                                                           out, ldo, resid);
     return cudaGetLastError();
 }
 
 template <int MODE>
-cudaError_t launch_pair(const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmGroup* group,
+cudaError_t launch_pair(const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmBatch& batch,
                         int N, int K, __nv_bfloat16* out, int ldo, const __nv_bfloat16* resid,
                         int grid, cudaStream_t st) {
     // Set on every launch: the attribute is per device context, contexts may be driven from
@@ -735,13 +780,13 @@ cudaError_t launch_pair(const CUtensorMap* tmA, const CUtensorMap* tmB, const Ge
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kPairSmem);
     if (e != cudaSuccess) return e;
-    expert_gemm_pair_kernel<MODE><<<grid & ~1, kThreads, kPairSmem, st>>>(*tmA, *tmB, group, N, K,
+    expert_gemm_pair_kernel<MODE><<<grid & ~1, kThreads, kPairSmem, st>>>(*tmA, *tmB, batch, N, K,
                                                                           out, ldo, resid);
     return cudaGetLastError();
 }
 
 template <int BN, int MODE>
-cudaError_t launch_one(const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmGroup* group,
+cudaError_t launch_one(const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmBatch& batch,
                        int N, int K, __nv_bfloat16* out, int ldo, const __nv_bfloat16* resid,
                         int grid, cudaStream_t st) {
     using C = GemmCfg<BN>;
@@ -749,19 +794,20 @@ cudaError_t launch_one(const CUtensorMap* tmA, const CUtensorMap* tmB, const Gem
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)C::kSmem);   // every launch, see launch_pair
     if (e != cudaSuccess) return e;
-    expert_gemm_kernel<BN, MODE><<<grid, kThreads, C::kSmem, st>>>(*tmA, *tmB, group, N, K, out, ldo, resid);
+    expert_gemm_kernel<BN, MODE><<<grid, kThreads, C::kSmem, st>>>(*tmA, *tmB, batch, N, K, out, ldo, resid);
     return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_expert_gemm_swap(int mode, const CUtensorMap* tmW, const TokenMaps* tmX,
-                                    const GemmGroup* group, int M, int K, __nv_bfloat16* out,
+                                    const GemmBatch& batch, int M, int K, __nv_bfloat16* out,
                                     int ldo, const __nv_bfloat16* resid, int grid, cudaStream_t st) {
-    if ((mode == kGemmResidual) != (resid != nullptr) || M % 256 || K % BK) return cudaErrorInvalidValue;
-    if (mode == kGemmSwiGLU) return launch_swap<kGemmSwiGLU>(tmW, tmX, group, M, K, out, ldo, resid, grid, st);
-    if (mode == kGemmResidual) return launch_swap<kGemmResidual>(tmW, tmX, group, M, K, out, ldo, resid, grid, st);
-    return launch_swap<kGemmPlain>(tmW, tmX, group, M, K, out, ldo, resid, grid, st);
+    if ((mode == kGemmResidual) != (resid != nullptr) || M % 256 || K % BK || batch.n != 1)
+        return cudaErrorInvalidValue;
+    if (mode == kGemmSwiGLU) return launch_swap<kGemmSwiGLU>(tmW, tmX, batch, M, K, out, ldo, resid, grid, st);
+    if (mode == kGemmResidual) return launch_swap<kGemmResidual>(tmW, tmX, batch, M, K, out, ldo, resid, grid, st);
+    return launch_swap<kGemmPlain>(tmW, tmX, batch, M, K, out, ldo, resid, grid, st);
 }
 
 int gemm_bn_for(int mode, int N) {
@@ -772,24 +818,25 @@ int gemm_bn_for(int mode, int N) {
 }
 
 cudaError_t launch_expert_gemm(int mode, int bn, bool pair, const CUtensorMap* tmA,
-                               const CUtensorMap* tmB, const GemmGroup* group, int N, int K,
+                               const CUtensorMap* tmB, const GemmBatch& batch, int N, int K,
                                __nv_bfloat16* out, int ldo, const __nv_bfloat16* resid, int grid,
                                cudaStream_t st) {
-    if ((mode == kGemmResidual) != (resid != nullptr)) return cudaErrorInvalidValue;
+    if ((mode == kGemmResidual) != (resid != nullptr) || batch.n < 1 || batch.n > kMaxBatch)
+        return cudaErrorInvalidValue;
     if (pair) {
         if (bn != 256) return cudaErrorInvalidValue;
-        if (mode == kGemmSwiGLU) return launch_pair<kGemmSwiGLU>(tmA, tmB, group, N, K, out, ldo, resid, grid, st);
-        if (mode == kGemmResidual) return launch_pair<kGemmResidual>(tmA, tmB, group, N, K, out, ldo, resid, grid, st);
-        return launch_pair<kGemmPlain>(tmA, tmB, group, N, K, out, ldo, resid, grid, st);
+        if (mode == kGemmSwiGLU) return launch_pair<kGemmSwiGLU>(tmA, tmB, batch, N, K, out, ldo, resid, grid, st);
+        if (mode == kGemmResidual) return launch_pair<kGemmResidual>(tmA, tmB, batch, N, K, out, ldo, resid, grid, st);
+        return launch_pair<kGemmPlain>(tmA, tmB, batch, N, K, out, ldo, resid, grid, st);
     }
     if (mode == kGemmSwiGLU) {
-        if (bn == 256) return launch_one<256, kGemmSwiGLU>(tmA, tmB, group, N, K, out, ldo, resid, grid, st);
+        if (bn == 256) return launch_one<256, kGemmSwiGLU>(tmA, tmB, batch, N, K, out, ldo, resid, grid, st);
     } else if (mode == kGemmResidual) {
-        if (bn == 256) return launch_one<256, kGemmResidual>(tmA, tmB, group, N, K, out, ldo, resid, grid, st);
-        if (bn == 128) return launch_one<128, kGemmResidual>(tmA, tmB, group, N, K, out, ldo, resid, grid, st);
+        if (bn == 256) return launch_one<256, kGemmResidual>(tmA, tmB, batch, N, K, out, ldo, resid, grid, st);
+        if (bn == 128) return launch_one<128, kGemmResidual>(tmA, tmB, batch, N, K, out, ldo, resid, grid, st);
     } else {
-        if (bn == 256) return launch_one<256, kGemmPlain>(tmA, tmB, group, N, K, out, ldo, resid, grid, st);
-        if (bn == 128) return launch_one<128, kGemmPlain>(tmA, tmB, group, N, K, out, ldo, resid, grid, st);
+        if (bn == 256) return launch_one<256, kGemmPlain>(tmA, tmB, batch, N, K, out, ldo, resid, grid, st);
+        if (bn == 128) return launch_one<128, kGemmPlain>(tmA, tmB, batch, N, K, out, ldo, resid, grid, st);
     }
     return cudaErrorInvalidValue;
 }

@@ -215,6 +215,10 @@ moe_status flush_copies(moe_ctx c) {
         }
     }
     p.end();
+    for (int j = 0; j < n; ++j) {   // the GEMMs take the batch as one launch (forward_impl)
+        c->batch_q0[s0 + j] = c->pend_q0;
+        c->batch_n[s0 + j] = n;
+    }
     c->stats.h2d_weight_bytes += (int64_t)n * c->blob_bytes;
     c->pend_n = 0;
     return MOE_OK;
@@ -251,13 +255,19 @@ moe_status request_copy(moe_ctx c, const void* const* experts, int i, uint64_t q
 // (256x256 tiles on SM pairs, ~97% tensor-pipe activity) or the single-CTA kernel (128x256, ~76%:
 // shared-memory bandwidth bound, but half the M granularity and twice the concurrent tiles),
 // by a wave model: time ~ ceil(tiles / concurrent tiles) / tensor efficiency.
-bool pick_pair(moe_ctx c, int64_t rows, int bn, int N) {
+// (rows: the expected rows of each of the launch's n groups; their tiles share the waves.)
+bool pick_pair(moe_ctx c, const int64_t* rows, int n, int bn, int N) {
     if (bn != 256 || c->pair_mode == 0) return false;
     if (c->pair_mode == 1) return true;
-    if (rows <= 0) return false;
     const int sms = c->num_sms;
     const int64_t nt = N / 256;
-    const int64_t t1 = ((rows + 127) / 128) * nt, t2 = ((rows + 255) / 256) * nt;
+    int64_t t1 = 0, t2 = 0;
+    for (int i = 0; i < n; ++i) {
+        if (rows[i] <= 0) continue;
+        t1 += ((rows[i] + 127) / 128) * nt;
+        t2 += ((rows[i] + 255) / 256) * nt;
+    }
+    if (t1 == 0) return false;
     const double w1 = (double)((t1 + sms - 1) / sms) / 0.76;
     const double w2 = (double)((t2 + sms / 2 - 1) / (sms / 2)) / 0.97;
     return w2 < w1;
@@ -344,62 +354,81 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     // chosen on the expected size: T*k*W/N_e rows per routed expert (+10% for routing
     // variance), T per shared expert.
     const int64_t exp_routed = (int64_t)T * k * cf.world_size / ne;
-    auto use_pair = [&](bool shared, int bn, int N) {
-        return pick_pair(c, shared ? (int64_t)T : exp_routed + exp_routed / 10, bn, N);
-    };
     // swap-AB kernel: weight rows must fill 256-row pair tiles
     auto use_swap = [&](int M) { return c->swap_mode == 1 && M % 256 == 0; };
-    for (int i = 0; i < c->n_all; ++i) {
+    // One GEMM1 + one GEMM2 launch per DMA batch (flush_copies): the batch's experts sit in
+    // adjacent slots of the staging buffer and their tiles are scheduled together (GemmBatch),
+    // so many small experts no longer pay one partial last wave each.  A batch never mixes
+    // shared and routed experts (different A operands and outputs).
+    for (int i = 0; i < c->n_all;) {
         const uint64_t q = q0 + i;
-        const int s = (int)(q % (uint64_t)ns);
-        const int e = expert_of(i);
-        const bool shared = e >= c->n_local;
         if (c->pend_n > 0 && c->pend_q0 <= q) {  // this item's batch is still pending: issue it
             moe_status fs = flush_copies(c);
             if (fs != MOE_OK) return fs;
         }
-        MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready13[s], 0));
+        const int s = (int)(q % (uint64_t)ns);
+        const bool shared = expert_of(i) >= c->n_local;
+        int nb = (int)(c->batch_q0[s] + (uint64_t)c->batch_n[s] - q);
+        nb = std::max(1, std::min(nb, (shared ? S : c->n_all) - i));
+        if (use_swap(2 * hi) || use_swap(h)) nb = 1;   // the swap kernel takes one group
+        moe::GemmBatch b1{}, b2{};
+        b1.table = g1;
+        b2.table = g2;
+        b1.n = b2.n = nb;
+        int64_t rows[moe::kMaxBatch];
+        for (int j = 0; j < nb; ++j) {
+            const int sj = (int)((q + j) % (uint64_t)ns), e = expert_of(i + j);
+            MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready13[sj], 0));
+            b1.idx[j] = b2.idx[j] = e;
+            b1.b_row[j] = 3 * hi * sj;           // W13 of slot sj in tm_w13*
+            b2.b_row[j] = 3 * h * sj + 2 * h;    // W2 of slot sj in tm_w2*
+            rows[j] = shared ? (int64_t)T : exp_routed + exp_routed / 10;
+        }
         {
             Prof p(c, moe::kRecGemm1, st);
             if (use_swap(2 * hi)) {
-                MOE_CUDA(c, moe::launch_expert_gemm_swap(moe::kGemmSwiGLU, &c->tm_w13_pair[s],
-                                                         shared ? &tm_x_t : tmT_routed, g1 + e,
+                MOE_CUDA(c, moe::launch_expert_gemm_swap(moe::kGemmSwiGLU, &c->tm_w13_pair,
+                                                         shared ? &tm_x_t : tmT_routed, b1,
                                                          2 * hi, h, c->h_act, hi, nullptr, grid, st));
             } else {
-                const bool pr = use_pair(shared, c->bn1, 2 * hi);
+                const bool pr = pick_pair(c, rows, nb, c->bn1, 2 * hi);
                 MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmSwiGLU, c->bn1, pr,
                                                     shared ? &tm_x : tmA_routed,
-                                                    pr ? &c->tm_w13_pair[s] : &c->tm_w13[s],
-                                                    g1 + e, 2 * hi, h, c->h_act, hi, nullptr,
-                                                    grid, st));
+                                                    pr ? &c->tm_w13_pair : &c->tm_w13, b1,
+                                                    2 * hi, h, c->h_act, hi, nullptr, grid, st));
             }
             p.end();
         }
-        MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready2[s], 0));
+        for (int j = 0; j < nb; ++j)
+            MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready2[(q + j) % (uint64_t)ns], 0));
         {
             Prof p(c, moe::kRecGemm2, st);
             if (use_swap(h)) {
-                MOE_CUDA(c, moe::launch_expert_gemm_swap(moe::kGemmPlain, &c->tm_w2_pair[s],
-                                                         &c->tm_h_t, g2 + e, h, hi,
+                MOE_CUDA(c, moe::launch_expert_gemm_swap(moe::kGemmPlain, &c->tm_w2_pair,
+                                                         &c->tm_h_t, b2, h, hi,
                                                          shared ? c->y_perm : y_routed, h,
                                                          nullptr, grid, st));
             } else {
-                const bool pr = use_pair(shared, c->bn2, h);
+                const bool pr = pick_pair(c, rows, nb, c->bn2, h);
                 MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmPlain, c->bn2, pr, &c->tm_h,
-                                                    pr ? &c->tm_w2_pair[s] : &c->tm_w2[s], g2 + e,
-                                                    h, hi, shared ? c->y_perm : y_routed, h,
-                                                    nullptr, grid, st));
+                                                    pr ? &c->tm_w2_pair : &c->tm_w2, b2, h, hi,
+                                                    shared ? c->y_perm : y_routed, h, nullptr,
+                                                    grid, st));
             }
             p.end();
         }
         c->stats.kernel_launches += 2;
         c->stats.gemm1_launches += 1;
         c->stats.gemm2_launches += 1;
-        MOE_CUDA(c, cudaEventRecord(c->slot_free[s], st));
-        if (i + ns < c->n_all) {
-            moe_status s2 = request_copy(c, experts, expert_of(i + ns), q + ns);
-            if (s2 != MOE_OK) return s2;
+        for (int j = 0; j < nb; ++j)
+            MOE_CUDA(c, cudaEventRecord(c->slot_free[(q + j) % (uint64_t)ns], st));
+        for (int j = 0; j < nb; ++j) {   // the freed slots take the items ns ahead
+            if (i + j + ns < c->n_all) {
+                moe_status s2 = request_copy(c, experts, expert_of(i + j + ns), q + j + ns);
+                if (s2 != MOE_OK) return s2;
+            }
         }
+        i += nb;
     }
     {
         moe_status fs = flush_copies(c);  // nothing may stay pending across calls
@@ -553,19 +582,22 @@ moe_status taskb_impl(moe_ctx c, const __nv_bfloat16* attn, const __nv_bfloat16*
     MOE_CUDA(c, cudaStreamWaitEvent(st, c->lw_ready[b], 0));
     {
         Prof p(c, moe::kRecOproj, st);
+        moe::GemmBatch ob{};
+        ob.table = c->oproj_grp;
+        ob.n = 1;   // idx[0] = 0, b_row[0] = 0: Wo is the whole map
         if (c->swap_mode == 1 && h % 256 == 0) {
             moe::TokenMaps tm_attn_t;
             if (!moe::make_token_maps(&tm_attn_t, attn, (uint64_t)T, (uint64_t)h))
                 return set_err(c, MOE_E_CUDA, "cuTensorMapEncodeTiled failed for attn");
             MOE_CUDA(c, moe::launch_expert_gemm_swap(moe::kGemmResidual, &c->tm_wo_pair[b],
-                                                     &tm_attn_t, c->oproj_grp, h, h, c->h1_ws, h,
+                                                     &tm_attn_t, ob, h, h, c->h1_ws, h,
                                                      resid, c->num_sms, st));
         } else {
-            const bool pr = pick_pair(c, T, c->bn2, h);
+            const int64_t rows = T;
+            const bool pr = pick_pair(c, &rows, 1, c->bn2, h);
             MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmResidual, c->bn2, pr, &tm_attn,
-                                                pr ? &c->tm_wo_pair[b] : &c->tm_wo[b],
-                                                c->oproj_grp, h, h, c->h1_ws, h, resid,
-                                                c->num_sms, st));
+                                                pr ? &c->tm_wo_pair[b] : &c->tm_wo[b], ob, h, h,
+                                                c->h1_ws, h, resid, c->num_sms, st));
         }
         p.end();
     }
@@ -723,13 +755,12 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     tm &= moe::make_tmap(&c->tm_h, c->h_act, (uint64_t)h_rows, hi, 128);
     tm &= moe::make_token_maps(&c->tm_xperm_t, c->x_perm, (uint64_t)Tm * k, h);
     tm &= moe::make_token_maps(&c->tm_h_t, c->h_act, (uint64_t)h_rows, hi);
-    for (int i = 0; i < c->nslots; ++i) {
-        tm &= moe::make_tmap(&c->tm_w13[i], c->slot[i], 2ull * hi, h, (uint32_t)c->bn1);
-        tm &= moe::make_tmap(&c->tm_w2[i], static_cast<char*>(c->slot[i]) + c->w13_bytes,
-                             (uint64_t)h, hi, (uint32_t)c->bn2);
-        tm &= moe::make_tmap(&c->tm_w13_pair[i], c->slot[i], 2ull * hi, h, 128);
-        tm &= moe::make_tmap(&c->tm_w2_pair[i], static_cast<char*>(c->slot[i]) + c->w13_bytes,
-                             (uint64_t)h, hi, 128);
+    {   // the whole staging buffer as one W13 view and one W2 view (see engine.h)
+        const uint64_t r13 = 3ull * hi * c->nslots, r2 = 3ull * h * c->nslots;
+        tm &= moe::make_tmap(&c->tm_w13, c->slot_base, r13, h, (uint32_t)c->bn1);
+        tm &= moe::make_tmap(&c->tm_w13_pair, c->slot_base, r13, h, 128);
+        tm &= moe::make_tmap(&c->tm_w2, c->slot_base, r2, hi, (uint32_t)c->bn2);
+        tm &= moe::make_tmap(&c->tm_w2_pair, c->slot_base, r2, hi, 128);
     }
     if (!tm) return fail(MOE_E_CUDA);
     if (const char* e = getenv("MOE_GEMM_SWAP")) c->swap_mode = atoi(e) != 0;

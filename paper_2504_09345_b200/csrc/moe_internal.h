@@ -23,6 +23,17 @@ struct GemmGroup {
     int32_t pad;
 };
 
+// The expert groups of one GEMM launch (kernel parameter, by value): entry i is group
+// table[idx[i]] (a device table written by the routing / EP plan kernels), whose weights start
+// at row b_row[i] of the launch's B tensor map (one map spans all staging slots).
+constexpr int kMaxBatch = 16;
+struct GemmBatch {
+    const GemmGroup* table;
+    int32_t idx[kMaxBatch];
+    int32_t b_row[kMaxBatch];
+    int32_t n;
+};
+
 // ------------------------------------------------------------ expert parallelism, P2P transport
 constexpr int kMaxRanks = 8;         // EP group size (one B200 box)
 // Row buffers of the EP group as seen by one rank (device-resident, rewritten by the plan kernel
@@ -106,8 +117,11 @@ enum GemmMode { kGemmSwiGLU = 0, kGemmPlain = 1, kGemmResidual = 2 };
 //   `pair`: the CTA-pair kernel, 256 x 256 tiles, bn must be 256); group: device ptr.
 //   out: bf16 [*, ldo]; SwiGLU writes N/2 columns.  resid: bf16 [*, ldo] (residual mode only,
 //   else nullptr), read at the output's rows.
+//   batch: the launch's expert groups (GemmBatch below): ONE persistent launch covers up to
+//   kMaxBatch experts -- their tiles are scheduled together, so small experts no longer pay a
+//   partial last wave each.
 cudaError_t launch_expert_gemm(int mode, int bn, bool pair, const CUtensorMap* tmA,
-                               const CUtensorMap* tmB, const GemmGroup* group, int N, int K,
+                               const CUtensorMap* tmB, const GemmBatch& batch, int N, int K,
                                __nv_bfloat16* out, int ldo, const __nv_bfloat16* resid, int grid,
                                cudaStream_t st);
 // Token operand of the swap-AB kernel: the same [rows, K] bf16 tensor with 64-column boxes of
@@ -120,7 +134,7 @@ bool make_token_maps(TokenMaps* t, const void* base, uint64_t rows, uint64_t col
 // = 2 h_i for SwiGLU, h otherwise, M % 256 == 0), the group's tokens the N side, N = 32..256
 // per tile (a multiple of 32).
 cudaError_t launch_expert_gemm_swap(int mode, const CUtensorMap* tmW, const TokenMaps* tmX,
-                                    const GemmGroup* group, int M, int K, __nv_bfloat16* out,
+                                    const GemmBatch& batch, int M, int K, __nv_bfloat16* out,
                                     int ldo, const __nv_bfloat16* resid, int grid, cudaStream_t st);
 int gemm_bn_for(int mode, int N);   // tile width used for a given mode / N (0 = unsupported)
 // L2 policy of the GEMM operand loads for the current device: 0 evict_normal, 1 A evict_last +

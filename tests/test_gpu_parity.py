@@ -205,14 +205,24 @@ def test_invalid_arguments():
     run.close()
 
 
-def test_stats_h2d_bytes_equal_algorithmic_bytes():
+@pytest.mark.parametrize("group", ["1", "auto"])
+def test_stats_h2d_bytes_equal_algorithmic_bytes(group, monkeypatch):
+    """H2D bytes = the algorithmic bytes; one GEMM1/GEMM2 launch per DMA batch (one per expert
+    with MOE_COPY_GROUP=1, fewer when small experts are coalesced into one DMA + one launch)."""
+    if group != "auto":
+        monkeypatch.setenv("MOE_COPY_GROUP", group)
     inp = synth.gen_inputs(synth.MoEConfig("custom", 12, 256, 384, 8, 2, 256))
     run = GpuRun(inp, profile=True)
     for _ in range(3):
         run.run()
     st = run.layer.stats()
     assert st["h2d_weight_bytes"] == 3 * 8 * 6 * 256 * 384
-    assert st["gemm1_launches"] == 24 and st["h2d_ms"] > 0 and st["gemm1_ms"] > 0
+    assert st["gemm1_launches"] == st["gemm2_launches"]
+    if group == "1":
+        assert st["gemm1_launches"] == 24
+    else:
+        assert 3 <= st["gemm1_launches"] < 24
+    assert st["h2d_ms"] > 0 and st["gemm1_ms"] > 0
     run.close()
 
 
