@@ -91,6 +91,14 @@ struct moe_ctx_s {
     uint64_t batch_q0[moe::kMaxSlots] = {};
     int batch_n[moe::kMaxSlots] = {};
     int pair_mode = -1;       // MOE_GEMM_PAIR: 0 never, 1 always, -1 auto (default: wave model)
+    // Tail split (MOE_GEMM_TAILSPLIT=1, experiment, default off): a CTA-pair GEMM covers only
+    // whole 256-row tiles of each group; the < 256-row remainder runs as 128-row tiles in a
+    // concurrent launch on tail_stream (forked / joined with events).  Measured slower at C1
+    // (GEMM1 1.61 -> 1.74 ms/step) and C4, +2% at C3: the tail CTAs do not just fill the pair
+    // kernel's idle last wave.
+    bool tail_split = false;
+    cudaStream_t tail_stream = nullptr;
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
 
     // workspace
     int32_t* idx_ws = nullptr;

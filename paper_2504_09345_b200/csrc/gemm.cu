@@ -147,7 +147,14 @@ __device__ __forceinline__ void batch_init(BatchInfo* bi, const GemmBatch& b, in
                                            int n_tiles) {
     int t = 0;
     for (int i = 0; i < b.n; ++i) {
-        const GemmGroup g = b.table[b.idx[i]];
+        GemmGroup g = b.table[b.idx[i]];
+        const int head = (max(0, g.a_end - g.a_begin) / kPairRows) * kPairRows;
+        if (b.part == 1) {          // whole 256-row tiles only
+            g.a_end = g.a_begin + head;
+        } else if (b.part == 2) {   // the remainder
+            g.a_begin += head;
+            g.out_base += head;
+        }
         const int rows = max(0, g.a_end - g.a_begin);
         bi->a_begin[i] = g.a_begin;
         bi->a_end[i] = g.a_end;

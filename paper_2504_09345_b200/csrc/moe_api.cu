@@ -273,6 +273,34 @@ bool pick_pair(moe_ctx c, const int64_t* rows, int n, int bn, int N) {
     return w2 < w1;
 }
 
+// One expert-GEMM step over a batch of groups on `st`.  With the CTA-pair kernel and tail split
+// on, the pair kernel covers the whole 256-row tiles and the single-CTA kernel the < 256-row
+// remainders, concurrently on tail_stream (fork/join events: the tail needs the same inputs and
+// `st` continues only after both).
+moe_status launch_grouped(moe_ctx c, int mode, int bn, bool pair, const CUtensorMap* tmA,
+                          const CUtensorMap* tmB, const CUtensorMap* tmB_pair,
+                          moe::GemmBatch batch, int N, int K, __nv_bfloat16* out, int ldo,
+                          cudaStream_t st) {
+    const int grid = c->num_sms;
+    if (!pair || !c->tail_split) {
+        MOE_CUDA(c, moe::launch_expert_gemm(mode, bn, pair, tmA, pair ? tmB_pair : tmB, batch, N,
+                                            K, out, ldo, nullptr, grid, st));
+        return MOE_OK;
+    }
+    MOE_CUDA(c, cudaEventRecord(c->fork_ev, st));
+    batch.part = 1;
+    MOE_CUDA(c, moe::launch_expert_gemm(mode, bn, true, tmA, tmB_pair, batch, N, K, out, ldo,
+                                        nullptr, grid, st));
+    batch.part = 2;
+    MOE_CUDA(c, cudaStreamWaitEvent(c->tail_stream, c->fork_ev, 0));
+    MOE_CUDA(c, moe::launch_expert_gemm(mode, bn, false, tmA, tmB, batch, N, K, out, ldo,
+                                        nullptr, grid, c->tail_stream));
+    MOE_CUDA(c, cudaEventRecord(c->join_ev, c->tail_stream));
+    MOE_CUDA(c, cudaStreamWaitEvent(st, c->join_ev, 0));
+    c->stats.kernel_launches += 1;
+    return MOE_OK;
+}
+
 // resid (Task B): added to every output row in the combine (nullptr for the plain MoE layer).
 moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __nv_bfloat16* wr,
                         const void* const* experts, __nv_bfloat16* out, int32_t* topk_idx,
@@ -392,10 +420,10 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
                                                          2 * hi, h, c->h_act, hi, nullptr, grid, st));
             } else {
                 const bool pr = pick_pair(c, rows, nb, c->bn1, 2 * hi);
-                MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmSwiGLU, c->bn1, pr,
-                                                    shared ? &tm_x : tmA_routed,
-                                                    pr ? &c->tm_w13_pair : &c->tm_w13, b1,
-                                                    2 * hi, h, c->h_act, hi, nullptr, grid, st));
+                moe_status gs = launch_grouped(c, moe::kGemmSwiGLU, c->bn1, pr,
+                                               shared ? &tm_x : tmA_routed, &c->tm_w13,
+                                               &c->tm_w13_pair, b1, 2 * hi, h, c->h_act, hi, st);
+                if (gs != MOE_OK) return gs;
             }
             p.end();
         }
@@ -410,10 +438,10 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
                                                          nullptr, grid, st));
             } else {
                 const bool pr = pick_pair(c, rows, nb, c->bn2, h);
-                MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmPlain, c->bn2, pr, &c->tm_h,
-                                                    pr ? &c->tm_w2_pair : &c->tm_w2, b2, h, hi,
-                                                    shared ? c->y_perm : y_routed, h, nullptr,
-                                                    grid, st));
+                moe_status gs = launch_grouped(c, moe::kGemmPlain, c->bn2, pr, &c->tm_h,
+                                               &c->tm_w2, &c->tm_w2_pair, b2, h, hi,
+                                               shared ? c->y_perm : y_routed, h, st);
+                if (gs != MOE_OK) return gs;
             }
             p.end();
         }
@@ -722,6 +750,12 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
         if (cfg->flags & MOE_FLAG_PROFILE)
             ok &= cudaStreamCreateWithFlags(&c->clock_stream, cudaStreamNonBlocking) == cudaSuccess;
         ok &= cudaEventCreateWithFlags(&c->done_ev, cudaEventDisableTiming) == cudaSuccess;
+        if (const char* e = getenv("MOE_GEMM_TAILSPLIT")) c->tail_split = atoi(e) != 0;
+        if (c->tail_split) {
+            ok &= cudaStreamCreateWithFlags(&c->tail_stream, cudaStreamNonBlocking) == cudaSuccess;
+            ok &= cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming) == cudaSuccess;
+            ok &= cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming) == cudaSuccess;
+        }
     }
     ok &= dalloc((void**)&c->slot_base, (size_t)c->blob_bytes * c->nslots);
     for (int i = 0; i < c->nslots; ++i) {
@@ -1040,6 +1074,9 @@ moe_status moe_destroy(moe_ctx c) {
     if (c->token_stream) cudaStreamDestroy(c->token_stream);
     if (c->clock_stream) cudaStreamDestroy(c->clock_stream);
     if (c->done_ev) cudaEventDestroy(c->done_ev);
+    if (c->tail_stream) cudaStreamDestroy(c->tail_stream);
+    if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+    if (c->join_ev) cudaEventDestroy(c->join_ev);
     cudaGetLastError();
     delete c;
     return MOE_OK;

@@ -26,12 +26,17 @@ struct GemmGroup {
 // The expert groups of one GEMM launch (kernel parameter, by value): entry i is group
 // table[idx[i]] (a device table written by the routing / EP plan kernels), whose weights start
 // at row b_row[i] of the launch's B tensor map (one map spans all staging slots).
+// part: 0 = every row of each group; 1 = the head (the largest multiple of 256 rows -- whole
+// CTA-pair tiles); 2 = the tail (the remaining < 256 rows), so a pair-kernel launch on the head
+// and a concurrent 128-row-tile launch on the tail split a group without padding it to 256.
 constexpr int kMaxBatch = 16;
+constexpr int kPairRows = 256;
 struct GemmBatch {
     const GemmGroup* table;
     int32_t idx[kMaxBatch];
     int32_t b_row[kMaxBatch];
     int32_t n;
+    int32_t part;
 };
 
 // ------------------------------------------------------------ expert parallelism, P2P transport
