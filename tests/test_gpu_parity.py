@@ -276,7 +276,7 @@ def test_ep_path_one_rank_nccl_matches_oracle_and_single_gpu(shape):
 
 
 # ------------------------------------------------------------- CTA-pair (cta_group::2) GEMM
-@pytest.mark.parametrize("mode", ["1", "0"])
+@pytest.mark.parametrize("mode", ["1", "0", "split"])
 @pytest.mark.parametrize("shape", [
     dict(hidden=256, ffn=384, num_experts=8, top_k=2, tokens=1500),
     dict(hidden=512, ffn=640, num_experts=4, top_k=2, tokens=2100, num_shared=1),
@@ -284,8 +284,12 @@ def test_ep_path_one_rank_nccl_matches_oracle_and_single_gpu(shape):
 ])
 def test_gemm_tile_variants(shape, mode, monkeypatch):
     """MOE_GEMM_PAIR=1 forces the 256x256 CTA-pair kernel (tcgen05.mma.cta_group::2, 2-CTA TMA)
-    for every bn=256 GEMM; 0 forces the 128-row kernel.  Both must match the oracle."""
-    monkeypatch.setenv("MOE_GEMM_PAIR", mode)
+    for every bn=256 GEMM; 0 forces the 128-row kernel; split = pair kernel on whole 256-row
+    tiles + a concurrent 128-row launch on the remainders (MOE_GEMM_TAILSPLIT).  All must match
+    the oracle."""
+    monkeypatch.setenv("MOE_GEMM_PAIR", "1" if mode == "split" else mode)
+    if mode == "split":
+        monkeypatch.setenv("MOE_GEMM_TAILSPLIT", "1")
     cfg = synth.MoEConfig("custom", 14, shape["hidden"], shape["ffn"], shape["num_experts"],
                           shape["top_k"], shape["tokens"], shape.get("num_shared", 0))
     inp = synth.gen_inputs(cfg)
