@@ -275,3 +275,31 @@ def test_determinism(tiny_inputs):
     b = oracle.forward(inp.x, inp.router, inp.w1, inp.w3, inp.w2, top_k=2)
     for u, v in zip(a, b):
         assert np.array_equal(u, v)
+
+
+def test_whole_layer_c4_slice_vs_torch_fp64():
+    """SURVEY §8(c.3) 'whole layer': an independent torch fp64 implementation on a token slice of
+    the C4 (DeepSeek-V2-Lite-shaped: 64 routed experts, top-6, 2 shared) workload -- routing by
+    torch.topk on fp64 logits, renormalised softmax gates, SwiGLU experts, shared experts added
+    with weight 1 (readings R1-R3, R10) -- against the oracle: idx equal, y within 1e-5."""
+    cfg = synth.CONFIGS["dsv2_lite"]
+    inp = synth.gen_inputs(cfg, tokens=48)
+    y, idx, g = oracle.forward(inp.x, inp.router, inp.w1, inp.w3, inp.w2, cfg.top_k,
+                               n_shared=cfg.num_shared)
+    x = _t64(inp.x)
+    logits = x @ _t64(inp.router).T
+    top = torch.topk(logits, cfg.top_k, dim=1)     # no exact ties in this draw
+    assert np.array_equal(top.indices.numpy(), idx)
+    p = torch.softmax(top.values, dim=1)
+    assert np.max(np.abs(p.numpy() - g)) <= 1e-6
+    ref = torch.zeros(x.shape[0], cfg.hidden, dtype=torch.float64)
+    used = sorted(set(idx.ravel().tolist()))
+    ffn = {e: _dense_swiglu_fp64(inp.x, inp.w1[e], inp.w3[e], inp.w2[e]) for e in used}
+    for t in range(x.shape[0]):
+        for j in range(cfg.top_k):
+            ref[t] += p[t, j] * ffn[int(top.indices[t, j])][t]
+    for s in range(cfg.num_shared):
+        e = cfg.num_experts + s
+        ref += _dense_swiglu_fp64(inp.x, inp.w1[e], inp.w3[e], inp.w2[e])
+    ref = ref.numpy()
+    assert np.max(np.abs(y - ref)) <= 1e-5 * np.max(np.abs(ref))
