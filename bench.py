@@ -231,6 +231,23 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
+    # ---- N > 1: pin this rank's host threads (and so its pinned weight pages, first-touched by
+    # cudaHostAlloc) to the CPUs local to its GPU, so each GPU streams from its own NUMA node
+    # (the paper used numactl).
+    all_cpus = os.sched_getaffinity(0)
+    affinity = {"numa_local": False, "cpus": len(all_cpus)}
+    if world > 1:
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            p = torch.cuda.get_device_properties(local)
+            busid = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            pynvml.nvmlDeviceSetCpuAffinity(pynvml.nvmlDeviceGetHandleByPciBusId(busid))
+            affinity = {"numa_local": True, "cpus": len(os.sched_getaffinity(0)),
+                        "gpu_pci": busid}
+        except Exception as e:  # noqa: BLE001 -- affinity is an optimisation; report and go on
+            affinity["error"] = str(e)[:120]
+
     # ---- inputs: L layers; this rank's token slice and only its own experts (pinned, packed)
     layers = [synth.gen_inputs(cfg, layer=l, expert_ids=ids) for l in range(args.layers)]
     experts = [moe.HostExperts(cfg.hidden, cfg.ffn, l.w1, l.w3, l.w2) for l in layers]
@@ -304,25 +321,39 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         if sampler is not None:
             sampler.start()
-        e0.record(stream)
+        evs[0].record(stream)
         for i in range(args.steps):
             fn(args.warmup + i)
-        e1.record(stream)
+            evs[i + 1].record(stream)
         torch.cuda.synchronize()
         if sampler is not None:
             sampler.result = sampler.stop()
         if world > 1:
             dist.barrier()
-        return allmax(e0.elapsed_time(e1)) / args.steps
+        per_step = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps))
+        q = lambda f: per_step[min(len(per_step) - 1, int(f * len(per_step)))]  # noqa: E731
+        timed.dist = {"p10": q(0.1), "p50": q(0.5), "p90": q(0.9)}
+        return allmax(evs[0].elapsed_time(evs[-1])) / args.steps
 
     clocks = ClockSampler(local)
     ms = timed(step, clocks)
+    step_dist = dict(timed.dist)
     clk = clocks.result
     st = layer.stats()
     value = T / (ms / 1e3)
+    # single-call latency: one isolated call (no cross-call prefetch), all ranks together
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0.record(stream)
+    step(args.warmup + args.steps)
+    l1.record(stream)
+    torch.cuda.synchronize()
+    latency_ms = allmax(l0.elapsed_time(l1))
 
     # ---- work ledger (experts hit: from the routing of the timed layers, all ranks)
     cnt = torch.zeros(cfg.num_experts, dtype=torch.int64, device="cuda")
@@ -413,6 +444,7 @@ def run_ours(args):
     cpu = None
     if rank == 0 and not args.no_cpu:
         full = synth.gen_inputs(cfg, layer=0) if world > 1 else layers[0]
+        os.sched_setaffinity(0, all_cpus)   # the oracle gets every host core
         cpu = cpu_baseline(full, args.cpu_seconds)
 
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
@@ -431,7 +463,10 @@ def run_ours(args):
             "per_kernel_ms_per_step_rank0": per_kernel_ms,
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
             "gpu_launches": int(launches),
-            "gpu_launches_per_step": launches / args.steps}
+            "gpu_launches_per_step": launches / args.steps,
+            "ms_per_step_dist_rank0": step_dist,
+            "single_call_latency_ms": latency_ms,
+            "host_affinity": affinity}
     if rank == 0:
         print(json.dumps(line), flush=True)
     layer.sync()
