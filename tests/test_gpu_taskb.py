@@ -245,3 +245,60 @@ def test_taskb_host_entry_point_matches_device():
         assert st["host_calls"] == 3 and st["taskb_calls"] == 4
     finally:
         r.close()
+
+
+def test_taskb_local_expert_parallel_matches_single_gpu():
+    """GPU Task B under in-process expert parallelism (MOE_FLAG_LOCAL_EP, the P2P transport):
+    each of W = 2 ranks runs the O-projection + RMSNorm on its token slice and the MoE layer
+    over its N_e/W experts; every rank's output equals, bitwise, the one-GPU Task B output on
+    its slice over two back-to-back calls."""
+    import os
+    import threading
+    from paper_2504_09345_b200 import HostExperts, MoELayer
+    world = 2
+    inp, tb = _inputs(256, 256, 8, 2, 300, S=1)
+    cfg = inp.cfg
+    r = TaskBRun(inp, tb)
+    try:
+        ref = r.forward()[0].clone()
+        router = r.run.router
+        ne, nl, S, T = cfg.num_experts, cfg.num_experts // world, cfg.num_shared, cfg.tokens
+        bounds = [T * q // world for q in range(world + 1)]
+        key = os.urandom(128)
+        exps, lays, bufs, errors = [], [], [], []
+        for q in range(world):
+            ids = list(range(q * nl, (q + 1) * nl)) + [ne + s for s in range(S)]
+            exps.append(HostExperts(cfg.hidden, cfg.ffn, [inp.w1[i] for i in ids],
+                                    [inp.w3[i] for i in ids], [inp.w2[i] for i in ids]))
+            lays.append(MoELayer(cfg.hidden, cfg.ffn, ne, cfg.top_k, bounds[q + 1] - bounds[q],
+                                 num_shared=S, world_size=world, rank=q, nccl_unique_id=key,
+                                 local_ep=True))
+            a = bf16_tensor(tb.attn[bounds[q]:bounds[q + 1]])
+            bufs.append((torch.cuda.Stream(), a, bf16_tensor(tb.resid[bounds[q]:bounds[q + 1]]),
+                         torch.empty_like(a)))
+        torch.cuda.synchronize()
+
+        def work(q):
+            try:
+                s, a, res, o = bufs[q]
+                for _ in range(2):
+                    lays[q].taskb_forward(a, res, r.layer, tb.eps, router, exps[q], o,
+                                          stream=s.cuda_stream)
+                s.synchronize()
+            except Exception as e:  # noqa: BLE001
+                errors.append((q, repr(e)[:300]))
+
+        th = [threading.Thread(target=work, args=(q,)) for q in range(world)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=300)
+        assert not errors, errors
+        for q in range(world):
+            assert torch.equal(bufs[q][3], ref[bounds[q]:bounds[q + 1]]), f"rank {q} differs"
+        for l in lays:
+            l.close()
+        for e in exps:
+            e.close()
+    finally:
+        r.close()
