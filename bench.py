@@ -344,6 +344,11 @@ def run_ours(args):
     clk = clocks.result
     st = layer.stats()
     value = T / (ms / 1e3)
+    # every expert is re-streamed every call: fewer staging slots than experts per call (the
+    # library enforces it for explicit slot counts; asserted here for the run's auto choice)
+    assert st["num_slots"] == 2 or st["num_slots"] < nl + cfg.num_shared, st["num_slots"]
+    assert st["h2d_weight_bytes"] >= args.steps * (nl + cfg.num_shared) * \
+        ledger.expert_bytes(cfg.hidden, cfg.ffn), "weights were not re-streamed every step"
     # single-call latency: one isolated call (no cross-call prefetch), all ranks together
     if world > 1:
         dist.barrier()
@@ -456,6 +461,7 @@ def run_ours(args):
                        "hidden": cfg.hidden, "ffn": cfg.ffn, "experts": cfg.num_experts,
                        "experts_per_rank": nl, "top_k": cfg.top_k, "num_shared": cfg.num_shared,
                        "layers_cycled": args.layers, "staging_slots": st["num_slots"],
+                       "experts_streamed_per_call": nl + cfg.num_shared,
                        "packet_mb": args.packet_mb,
                        "l2": "inputs larger than L2: all expert weights re-streamed from host each step",
                        "parallelism": f"ep{world}", "ep_transport": transport},
