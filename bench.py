@@ -273,6 +273,7 @@ def run_ours(args):
             handles = [None] * world
             dist.all_gather_object(handles, layer.ipc_handle())
             layer.ipc_connect(handles)
+            layer.ipc_selftest(5.0)   # flags + rows through the mapping, before trusting it
             ok = 1.0
         except Exception as e:  # noqa: BLE001 -- reported, then the NCCL transport
             print(f"[bench] rank {rank}: P2P transport unavailable ({e}); using NCCL",

@@ -270,6 +270,12 @@ int64_t moe_ep_plan(int32_t world, int32_t rank, int32_t num_experts, const int3
 #define MOE_IPC_HANDLE_BYTES 256
 moe_status moe_ep_ipc_handle(moe_ctx ctx, void* out);
 moe_status moe_ep_ipc_connect(moe_ctx ctx, const void* all_handles);
+/* Collective check of a connected IPC_EP group (call on every rank): each rank writes a tagged
+ * word into every peer's receive buffer and releases a flag; each then waits up to timeout_s for
+ * all peers (no trap) and verifies what it received.  MOE_E_NCCL (with the failing peers in
+ * moe_last_error) if any peer did not signal or its data did not arrive -- the caller can then
+ * fall back to the NCCL transport with a new context. */
+moe_status moe_ep_ipc_selftest(moe_ctx ctx, double timeout_s);
 
 /* 128-byte ncclUniqueId for moe_config.nccl_unique_id (call on one rank, broadcast to all).
  * MOE_E_NCCL if libnccl.so.2 cannot be loaded. */

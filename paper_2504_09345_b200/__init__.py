@@ -35,7 +35,8 @@ EXPORTED = ["moe_packed_expert_bytes", "moe_pack_expert", "moe_host_alloc", "moe
             "moe_reset_stats", "moe_debug_buffers", "moe_destroy", "moe_status_string",
             "moe_last_error", "moe_probe_h2d", "moe_ep_plan", "moe_nccl_unique_id",
             "moe_packed_layer_bytes", "moe_pack_layer", "moe_taskb_forward",
-            "moe_taskb_forward_host", "moe_ep_ipc_handle", "moe_ep_ipc_connect"]
+            "moe_taskb_forward_host", "moe_ep_ipc_handle", "moe_ep_ipc_connect",
+            "moe_ep_ipc_selftest"]
 MOE_FLAG_IPC_EP = 8
 MOE_IPC_HANDLE_BYTES = 256
 
@@ -122,6 +123,7 @@ def load(path: str = LIB_PATH):
     lib.moe_taskb_forward_host.argtypes = [P, P, P, i32, P, ctypes.c_float, P, P, i32, P, P, P, P]
     lib.moe_ep_ipc_handle.argtypes = [P, P]
     lib.moe_ep_ipc_connect.argtypes = [P, P]
+    lib.moe_ep_ipc_selftest.argtypes = [P, ctypes.c_double]
     for name in EXPORTED:
         if name not in ("moe_packed_expert_bytes", "moe_status_string", "moe_last_error",
                         "moe_ep_plan", "moe_packed_layer_bytes"):
@@ -415,6 +417,10 @@ class MoELayer:
 
     def ipc_connect(self, handles: Sequence[bytes]) -> None:
         moe_ep_ipc_connect(self.ctx, handles)
+
+    def ipc_selftest(self, timeout_s: float = 5.0) -> None:
+        """Collective: raises MoEError if the peer mapping does not work (see include/moe.h)."""
+        _check(load().moe_ep_ipc_selftest(self.ctx, timeout_s), self.ctx)
 
     def sync(self):
         moe_sync(self.ctx)

@@ -140,6 +140,7 @@ struct moe_ctx_s {
     bool p2p = false;
     bool p2p_ready = false;                  // peer tables filled (connect done)
     uint64_t p2p_seq = 0;                    // calls issued (flag values)
+    uint64_t p2p_selftest_seq = 0;           // moe_ep_ipc_selftest tokens
     unsigned long long* p2p_flags = nullptr; // device [kP2PFlags][kMaxRanks], written by peers
     int32_t* p2p_counts = nullptr;           // device [2][W][N_e], row s written by rank s
     moe::P2PTable* p2p_tab = nullptr;        // device tables (peers' buffers in this process)

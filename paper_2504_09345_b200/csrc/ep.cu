@@ -547,4 +547,28 @@ moe_status moe_ep_ipc_connect(moe_ctx c, const void* all) {
     return moe::p2p_upload(c, flags, counts, xr, yr, c->copy_stream);
 }
 
+moe_status moe_ep_ipc_selftest(moe_ctx c, double timeout_s) {
+    if (!c) return MOE_E_INVAL;
+    if (!c->p2p || c->local_ep || !c->p2p_ready)
+        return moe::set_err(c, MOE_E_STATE, "not a connected IPC_EP context");
+    MOE_CUDA(c, cudaSetDevice(c->cfg.device));
+    int* d_res = nullptr;
+    int h_res = -1;
+    MOE_CUDA(c, cudaMalloc((void**)&d_res, sizeof(int)));
+    const long long cycles = (long long)(timeout_s * 2.0e9);   // SM clock <= 2 GHz
+    cudaError_t e = moe::launch_p2p_selftest(c->p2p_tab, c->pr_x, c->p2p_flags,
+                                             reinterpret_cast<const uint32_t*>(c->x_recv),
+                                             c->cfg.world_size, c->cfg.rank,
+                                             ++c->p2p_selftest_seq, cycles, d_res, c->copy_stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(&h_res, d_res, sizeof(int), cudaMemcpyDeviceToHost, c->copy_stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->copy_stream);
+    cudaFree(d_res);
+    MOE_CUDA(c, e);
+    if (h_res != 0)
+        return moe::set_err(c, MOE_E_NCCL, "P2P self-test failed on rank %d (mask 0x%x: low byte "
+                            "= peers that never signalled, high byte = peers whose rows did not "
+                            "arrive)", c->cfg.rank, h_res);
+    return MOE_OK;
+}
 }  // extern "C"

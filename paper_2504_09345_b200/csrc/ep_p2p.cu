@@ -113,7 +113,52 @@ __global__ void p2p_plan_kernel(const int32_t* __restrict__ counts, int W, int n
     }
 }
 
+__global__ void p2p_selftest_kernel(const P2PTable* __restrict__ tab,
+                                    const PeerRows* __restrict__ pr_x,
+                                    const unsigned long long* __restrict__ my_flags,
+                                    const uint32_t* __restrict__ my_xrecv, int W, int me,
+                                    unsigned long long token, long long timeout_cycles,
+                                    int* __restrict__ result) {
+    const int d = threadIdx.x;
+    if (d == 0) *result = 0;
+    if (d < W) {   // my word in peer d's x_recv: tag | (me << 8) | d
+        volatile uint32_t* w = reinterpret_cast<uint32_t*>(pr_x->rows[d]) + me;
+        *w = 0x5E1F0000u | ((uint32_t)me << 8) | (uint32_t)d;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (d < W) st_release_sys(tab->flags[d] + kFlagSelftest * kMaxRanks + me, token);
+    if (d < W) {
+        const unsigned long long* f = my_flags + kFlagSelftest * kMaxRanks + d;
+        const long long t0 = clock64();
+        bool ok = true;
+        while (ld_acquire_sys(f) < token) {
+            __nanosleep(256);
+            if (clock64() - t0 > timeout_cycles) {
+                ok = false;
+                break;
+            }
+        }
+        if (!ok) {
+            atomicOr(result, 1 << d);
+        } else {
+            const uint32_t want = 0x5E1F0000u | ((uint32_t)d << 8) | (uint32_t)me;
+            if (reinterpret_cast<const volatile uint32_t*>(my_xrecv)[d] != want)
+                atomicOr(result, 1 << (8 + d));
+        }
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_p2p_selftest(const P2PTable* tab, const PeerRows* pr_x,
+                                const unsigned long long* my_flags, const uint32_t* my_xrecv,
+                                int W, int me, unsigned long long token,
+                                long long timeout_cycles, int* result, cudaStream_t st) {
+    p2p_selftest_kernel<<<1, 32, 0, st>>>(tab, pr_x, my_flags, my_xrecv, W, me, token,
+                                          timeout_cycles, result);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_p2p_push_counts(const P2PTable* tab, const int32_t* counts, int ne, int W,
                                    int me, int par, unsigned long long seq, cudaStream_t st) {

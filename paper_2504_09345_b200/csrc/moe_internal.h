@@ -53,7 +53,8 @@ struct PeerRows {
 
 // Per-call synchronisation of the P2P transport: each rank owns flags[kP2PFlags][kMaxRanks]
 // (uint64 call numbers) that its PEERS write (release, system scope) and it waits on (acquire).
-enum P2PFlag { kFlagCounts = 0, kFlagDispatched, kFlagXFree, kFlagYReady, kFlagYDone, kP2PFlags };
+enum P2PFlag { kFlagCounts = 0, kFlagDispatched, kFlagXFree, kFlagYReady, kFlagYDone,
+               kFlagSelftest, kP2PFlags };
 struct P2PTable {   // device-resident: every rank's buffers, as mapped in this process
     unsigned long long* flags[kMaxRanks];
     int32_t* counts[kMaxRanks];      // [2][W][N_e] (call parity, source rank, expert)
@@ -70,6 +71,14 @@ cudaError_t launch_p2p_signal(const P2PTable* tab, int W, int me, int which,
 // host-mapped diag[5] (nullable).
 cudaError_t launch_p2p_wait(const unsigned long long* flags, int W, int which,
                             unsigned long long val, long long* diag, cudaStream_t st);
+// Transport self-test (collective, once after connect): every rank writes a tagged word into
+// each peer's x_recv and releases kFlagSelftest = token; then waits (acquire, NO trap: gives up
+// after timeout_cycles) for every peer and checks the words it received.  *result = bitmask:
+// bit s = peer s never signalled, bit 8+s = peer s's word wrong or missing.
+cudaError_t launch_p2p_selftest(const P2PTable* tab, const PeerRows* pr_x,
+                                const unsigned long long* my_flags, const uint32_t* my_xrecv,
+                                int W, int me, unsigned long long token,
+                                long long timeout_cycles, int* result, cudaStream_t st);
 // From counts[par] (all ranks' per-expert counts): this rank's GEMM groups over x_recv
 // (expert-major, moe_ep_plan's layout) + shared-expert groups, the send bases of pr_x / pr_y
 // (where this rank's rows for expert e start in the owner's buffers), rows received (rows_out)

@@ -35,6 +35,7 @@ def run_rank(rank, world, port, cfg_tuple, calls, device, q):
         handles = [None] * world
         dist.all_gather_object(handles, layer.ipc_handle())
         layer.ipc_connect(handles)
+        layer.ipc_selftest(30.0)
         router = torch.from_numpy(inp.router.view(np.int16)).view(torch.bfloat16).cuda()
         x = torch.from_numpy(np.ascontiguousarray(inp.x[lo:hi]).view(np.int16)).view(torch.bfloat16)
         x = x.reshape(-1, cfg.hidden).cuda()
