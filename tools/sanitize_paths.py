@@ -1,0 +1,60 @@
+"""Small runs of every engine path for compute-sanitizer (memcheck / racecheck / synccheck):
+tiny MoE layer, GPU Task B, grouped launches over many small experts, CTA-pair + tail split,
+and in-process P2P expert parallelism (W = 2)."""
+import os, sys, threading
+sys.path.insert(0, "."); sys.path.insert(0, "tests")
+import numpy as np, torch
+import synth
+from paper_2504_09345_b200 import HostExperts, HostLayer, MoELayer
+from gpu_helpers import GpuRun, bf16_tensor
+
+torch.cuda.set_device(0)
+# 1. tiny layer + Task B
+inp = synth.gen_inputs(synth.CONFIGS["tiny"])
+r = GpuRun(inp)
+r.run()
+tb = synth.gen_taskb(inp.cfg, inp.x)
+hl = HostLayer(inp.cfg.hidden, tb.wo, tb.gamma)
+a, res = bf16_tensor(tb.attn), bf16_tensor(tb.resid)
+o = torch.empty_like(a)
+r.layer.taskb_forward(a, res, hl, tb.eps, r.router, r.experts, o)
+torch.cuda.synchronize(); r.layer.sync(); hl.close(); r.close()
+# 2. many small experts (coalesced DMAs -> grouped GEMM launches), shared experts
+cfg = synth.MoEConfig("custom", 21, 256, 256, 32, 4, 300, 2)
+inp = synth.gen_inputs(cfg)
+r = GpuRun(inp); r.run(); r.run(); r.close()
+# 3. CTA-pair kernel with the tail split
+os.environ["MOE_GEMM_PAIR"] = "1"; os.environ["MOE_GEMM_TAILSPLIT"] = "1"
+cfg = synth.MoEConfig("custom", 22, 256, 384, 8, 2, 700, 1)
+inp = synth.gen_inputs(cfg)
+r = GpuRun(inp); r.run(); r.close()
+del os.environ["MOE_GEMM_PAIR"], os.environ["MOE_GEMM_TAILSPLIT"]
+# 4. in-process P2P expert parallelism, W = 2
+W = 2
+cfg = synth.MoEConfig("custom", 23, 256, 256, 8, 2, 200, 1)
+inp = synth.gen_inputs(cfg)
+full = GpuRun(inp)
+nl, S, T = cfg.num_experts // W, cfg.num_shared, cfg.tokens
+bounds = [T * q // W for q in range(W + 1)]
+key = os.urandom(128)
+ex, ly, bufs = [], [], []
+for q in range(W):
+    ids = list(range(q * nl, (q + 1) * nl)) + [cfg.num_experts + s for s in range(S)]
+    ex.append(HostExperts(cfg.hidden, cfg.ffn, [inp.w1[i] for i in ids], [inp.w3[i] for i in ids],
+                          [inp.w2[i] for i in ids]))
+    ly.append(MoELayer(cfg.hidden, cfg.ffn, cfg.num_experts, cfg.top_k, bounds[q + 1] - bounds[q],
+                       num_shared=S, world_size=W, rank=q, nccl_unique_id=key, local_ep=True))
+    x = bf16_tensor(inp.x[bounds[q]:bounds[q + 1]])
+    bufs.append((torch.cuda.Stream(), x, torch.empty_like(x)))
+torch.cuda.synchronize()
+def work(q):
+    s, x, o = bufs[q]
+    for _ in range(2):
+        ly[q].forward(x, full.router, ex[q], o, stream=s.cuda_stream)
+    s.synchronize()
+th = [threading.Thread(target=work, args=(q,)) for q in range(W)]
+[t.start() for t in th]; [t.join(300) for t in th]
+for l in ly: l.close()
+for e in ex: e.close()
+full.close()
+print("sanitize paths done")
