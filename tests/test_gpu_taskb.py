@@ -302,3 +302,49 @@ def test_taskb_local_expert_parallel_matches_single_gpu():
             e.close()
     finally:
         r.close()
+
+
+def test_taskb_chained_layers():
+    """NEXT-2 'chain L layers': three Task B layers back to back on one context, each layer's
+    output feeding the next layer's residual stream (with a fresh attention output), all weights
+    streamed (the copy stream prefetches layer l+1's Wo and experts while layer l computes).
+    Each layer is checked against the oracle on the GPU's own input to that layer (staged)."""
+    cfgs = [synth.MoEConfig("custom", 30 + l, 256, 384, 8, 2, 257, 1) for l in range(3)]
+    inps = [synth.gen_inputs(c) for c in cfgs]
+    tbs = [synth.gen_taskb(c, i.x) for c, i in zip(cfgs, inps)]
+    run = GpuRun(inps[0])
+    layers = [HostLayer(256, tb.wo, tb.gamma) for tb in tbs]
+    from paper_2504_09345_b200 import HostExperts
+    experts = [run.experts] + [HostExperts(256, 384, i.w1, i.w3, i.w2) for i in inps[1:]]
+    routers = [run.router] + [bf16_tensor(i.router) for i in inps[1:]]
+    try:
+        resid = bf16_tensor(tbs[0].resid)
+        s = torch.cuda.current_stream()
+        outs, ins = [], []
+        for l in range(3):   # enqueue all three layers, then synchronise once
+            attn = bf16_tensor(tbs[l].attn)
+            out = torch.empty_like(attn)
+            idx = torch.empty((257, 2), dtype=torch.int32, device="cuda")
+            run.layer.taskb_forward(attn, resid, layers[l], tbs[l].eps, routers[l], experts[l],
+                                    out, idx, stream=s.cuda_stream)
+            ins.append(resid)
+            outs.append((out, idx))
+            resid = out
+        s.synchronize()
+        run.layer.sync()
+        for l in range(3):
+            r_bits = _bits(ins[l])
+            y, h1, u, idx_ref, g = oracle.taskb_forward(
+                tbs[l].attn, r_bits, tbs[l].wo, tbs[l].gamma, tbs[l].eps, inps[l].router,
+                inps[l].w1, inps[l].w3, inps[l].w2, 2, 1)
+            out, idx = outs[l]
+            agree = (idx.cpu().numpy() == idx_ref).all(axis=1)
+            assert agree.mean() >= 0.99, f"layer {l}: {(~agree).sum()} tokens routed differently"
+            err = token_rel_err(to_f32(out)[agree], y[agree])
+            assert err.max() <= TOL, f"layer {l}: max token rel err {err.max():.3e}"
+    finally:
+        for hl in layers:
+            hl.close()
+        for e in experts[1:]:
+            e.close()
+        run.close()
