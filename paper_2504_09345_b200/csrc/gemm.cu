@@ -1,16 +1,21 @@
 // gemm.cu -- grouped bf16 expert GEMM on 5th-gen tensor cores (tcgen05 + TMEM), fed by TMA.
 //
-// One launch computes one expert group (steps a5 / a6 of the MoE layer; Eq. 1's "6 N_k h h_i"
-// FLOPs):
+// One launch computes a batch of expert groups (steps a5 / a6 of the MoE layer; Eq. 1's
+// "6 N_k h h_i" FLOPs) -- the experts one coalesced H2D copy brought in, whose
+// tiles share the persistent CTAs' waves (GemmBatch):
 //   a5 (kGemmSwiGLU): H[r, f] = silu(A W1^T)[r,f] * (A W3^T)[r,f]   with B = packed W13 whose
 //                     32-row blocks hold 16 gate rows then the 16 matching up rows, so the
 //                     SwiGLU is applied in the epilogue straight out of TMEM;
-//   a6 (kGemmPlain):  Y[r, :] = A W2^T.
-// A rows of the group are [a_begin, a_end) (read from device memory: the routing kernels
+//   a6 (kGemmPlain):  Y[r, :] = A W2^T;
+//   Task B O-projection (kGemmResidual): out = bf16(A Wo^T + resid).
+// A rows of each group are [a_begin, a_end) (read from device memory: the routing kernels
 // produce them, so no host sync is needed); rows past a_end in the last M tile are computed
-// but never stored.
+// but never stored.  B rows of group i start at GemmBatch::b_row[i] of one tensor map that
+// spans every staging slot.
 //
-// Structure (persistent, one CTA per SM, 256 threads):
+// Kernels: expert_gemm_kernel (1 CTA, M = 128), expert_gemm_pair_kernel (CTA pair,
+// cta_group::2, M = 256), expert_gemm_swap_kernel (weights as M, tokens as N; experimental).
+// Structure of the first (persistent, one CTA per SM, 256 threads):
 //   warp 0     TMA producer: A tile 128x64 and B tile BNx64 per stage, 128B swizzle
 //   warp 1     MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M=128, N=BN, K=16 per instr
 //   warp 2     TMEM allocator (2 x BN fp32 columns: double-buffered accumulator)
