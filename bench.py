@@ -36,7 +36,7 @@ METRIC = "Mixtral-8x7B MoE-layer tokens/s, weights streamed from host; % of roof
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)   # >= 20 timed calls
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="mixtral_8x7b")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
