@@ -554,30 +554,51 @@ __device__ __forceinline__ void swap_epilogue(uint32_t taddr, int lane, int ncol
             // tokens c+16..c+31 of the same feature.
             // The results are transposed through the warp's smem tile (token-major, padded) so
             // each lane then writes one token's 16 features as two 16-byte stores.
+            // Staged as bf16 (the output precision; one rounding either way) in rows of 18
+            // elements: conflict-free 2-byte writes and 4-byte reads, half the smem traffic of
+            // fp32 staging (this kernel is shared-memory-bandwidth sensitive).
             const bool up = lane >= 16;
             const int fl = lane & 15;
+            __nv_bfloat16* wb = reinterpret_cast<__nv_bfloat16*>(wt);
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
                 const float mine = __uint_as_float(up ? v[j] : v[16 + j]);
                 const float x = __shfl_xor_sync(0xffffffffu, mine, 16);
                 const float hv = up ? silu_mul(x, __uint_as_float(v[16 + j]))
                                     : silu_mul(__uint_as_float(v[j]), x);
-                wt[(j + (up ? 16 : 0)) * 17 + fl] = hv;
+                wb[(j + (up ? 16 : 0)) * 18 + fl] = __float2bfloat16_rn(hv);
             }
             __syncwarp();
             if (tok0 + c + lane < rows) {
-                const float* src = wt + lane * 17;
+                const uint32_t* src = reinterpret_cast<const uint32_t*>(wb + lane * 18);
                 uint32_t pk[8];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) pk[i] = ptx::pack_bf16x2(src[2 * i], src[2 * i + 1]);
+                for (int i = 0; i < 8; ++i) pk[i] = src[i];
                 __nv_bfloat16* dst = out + (orow0 + c + lane) * ldo + fcol;
                 ptx::st_global_v4(dst, pk[0], pk[1], pk[2], pk[3]);
                 ptx::st_global_v4(dst + 8, pk[4], pk[5], pk[6], pk[7]);
             }
             __syncwarp();
+        } else if (MODE == kGemmPlain) {
+            // lane = output feature fcol + lane; transpose through the warp's smem tile (bf16,
+            // rows of 34 elements) so each lane owns one token's 32 features: four 16-B stores.
+            __nv_bfloat16* wb = reinterpret_cast<__nv_bfloat16*>(wt);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) wb[j * 34 + lane] = __float2bfloat16_rn(__uint_as_float(v[j]));
+            __syncwarp();
+            if (tok0 + c + lane < rows) {
+                const uint32_t* src = reinterpret_cast<const uint32_t*>(wb + lane * 34);
+                uint32_t pk[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) pk[i] = src[i];
+                __nv_bfloat16* dst = out + (orow0 + c + lane) * ldo + fcol;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    ptx::st_global_v4(dst + 8 * i, pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+            }
+            __syncwarp();
         } else {
-            // lane = output feature fcol + lane; transpose through the warp's smem tile so each
-            // lane owns one token's 32 features: (+ residual,) four 16-byte stores.
+            // residual mode: fp32 staging so the residual is added before the single rounding
 #pragma unroll
             for (int j = 0; j < 32; ++j) wt[j * 33 + lane] = __uint_as_float(v[j]);
             __syncwarp();
