@@ -109,6 +109,7 @@ struct moe_ctx_s {
     int32_t* counts = nullptr;
     moe::GemmGroup* grp1 = nullptr;
     moe::GemmGroup* grp2 = nullptr;
+    moe::GemmGroup* shared_grp = nullptr;   // [2][n_all]: shared experts' groups (before routing)
     int32_t* pos = nullptr;
     __nv_bfloat16* x_perm = nullptr;
     __nv_bfloat16* h_act = nullptr;

@@ -336,47 +336,11 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     }
     if (hidden_on_copy_stream) MOE_CUDA(c, cudaStreamWaitEvent(st, c->x_ready[xb], 0));
 
-    {
-        Prof p(c, moe::kRecRoute, st);
-        MOE_CUDA(c, moe::launch_router_topk(hidden, T, h, wr, ne, k, cf.renormalize, idx, gates,
-                                            c->tile_counts, st));
-        MOE_CUDA(c, moe::launch_scan(c->tile_counts, n_tiles, ne, T, k, S, c->tile_prefix,
-                                     c->offsets, c->counts, c->grp1, c->grp2, st));
-        p.end();
-        c->stats.kernel_launches += 2;
-    }
-    if (c->p2p) {   // P2P EP: counts exchange + plan before the permute writes into the owners
-        Prof p(c, moe::kRecComm, st);
-        moe_status s = moe::p2p_before_dispatch(c, T, st);
-        if (s != MOE_OK) return s;
-        p.end();
-    }
-    {
-        Prof p(c, moe::kRecPermute, st);
-        MOE_CUDA(c, moe::launch_permute(hidden, T, h, k, ne, idx, c->tile_prefix, c->offsets,
-                                        c->x_perm, c->pos, c->p2p ? c->pr_x : nullptr, st));
-        p.end();
-        c->stats.kernel_launches += 1;
-    }
-
-    // Expert parallelism: ship each token row to the rank owning its expert.
-    const CUtensorMap* tmA_routed = &c->tm_xperm;
-    const moe::TokenMaps* tmT_routed = &c->tm_xperm_t;
-    const GemmGroup* g1 = c->grp1;
-    const GemmGroup* g2 = c->grp2;
-    __nv_bfloat16* y_routed = c->y_perm;
-    if (c->ep) {
-        Prof p(c, moe::kRecComm, st);
-        moe_status s = c->p2p ? moe::p2p_after_dispatch(c, st) : moe::ep_dispatch(c, T, st);
-        if (s != MOE_OK) return s;
-        p.end();
-        tmA_routed = &c->tm_xrecv;
-        tmT_routed = &c->tm_xrecv_t;
-        g1 = c->ep_grp;
-        g2 = c->ep_grp + c->n_all;
-        y_routed = c->y_recv;
-    }
-
+    // One GEMM1 + one GEMM2 launch per DMA batch (flush_copies): the batch's experts sit in
+    // adjacent slots of the staging buffer and their tiles are scheduled together (GemmBatch),
+    // so many small experts no longer pay one partial last wave each.  A batch never mixes
+    // shared and routed experts (different A operands and outputs).  Items [i0, i1), group
+    // tables g1 (GEMM1) / g2 (GEMM2) indexed by expert_of(i).
     const int grid = c->num_sms;
     // The host does not know the group sizes (they live on the device), so the tile shape is
     // chosen on the expected size: T*k*W/N_e rows per routed expert (+10% for routing
@@ -384,11 +348,11 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     const int64_t exp_routed = (int64_t)T * k * cf.world_size / ne;
     // swap-AB kernel: weight rows must fill 256-row pair tiles
     auto use_swap = [&](int M) { return c->swap_mode == 1 && M % 256 == 0; };
-    // One GEMM1 + one GEMM2 launch per DMA batch (flush_copies): the batch's experts sit in
-    // adjacent slots of the staging buffer and their tiles are scheduled together (GemmBatch),
-    // so many small experts no longer pay one partial last wave each.  A batch never mixes
-    // shared and routed experts (different A operands and outputs).
-    for (int i = 0; i < c->n_all;) {
+    const CUtensorMap* tmA_routed = &c->tm_xperm;
+    const moe::TokenMaps* tmT_routed = &c->tm_xperm_t;
+    __nv_bfloat16* y_routed = c->y_perm;
+    auto run_items = [&](int i0, int i1, const GemmGroup* g1, const GemmGroup* g2) -> moe_status {
+    for (int i = i0; i < i1;) {
         const uint64_t q = q0 + i;
         if (c->pend_n > 0 && c->pend_q0 <= q) {  // this item's batch is still pending: issue it
             moe_status fs = flush_copies(c);
@@ -458,6 +422,61 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         }
         i += nb;
     }
+    return MOE_OK;
+    };
+
+    // Shared experts first, BEFORE routing: they need only the hidden batch, so their GEMMs run
+    // while the router works and their slots are free for the next copies early (the copy
+    // engine never waits on the router).  Their group tables are written here (not by scan).
+    if (S > 0) {
+        const int hbase = (int)(c->ep ? c->cap_recv : (int64_t)T * k);
+        MOE_CUDA(c, moe::launch_fill_shared_groups(c->shared_grp, c->n_local, c->n_all, S, T,
+                                                   hbase, T * k, st));
+        c->stats.kernel_launches += 1;
+        const moe_status ss = run_items(0, S, c->shared_grp, c->shared_grp + c->n_all);
+        if (ss != MOE_OK) return ss;
+    }
+
+    {
+        Prof p(c, moe::kRecRoute, st);
+        MOE_CUDA(c, moe::launch_router_topk(hidden, T, h, wr, ne, k, cf.renormalize, idx, gates,
+                                            c->tile_counts, st));
+        MOE_CUDA(c, moe::launch_scan(c->tile_counts, n_tiles, ne, T, k, S, c->tile_prefix,
+                                     c->offsets, c->counts, c->grp1, c->grp2, st));
+        p.end();
+        c->stats.kernel_launches += 2;
+    }
+    if (c->p2p) {   // P2P EP: counts exchange + plan before the permute writes into the owners
+        Prof p(c, moe::kRecComm, st);
+        moe_status s = moe::p2p_before_dispatch(c, T, st);
+        if (s != MOE_OK) return s;
+        p.end();
+    }
+    {
+        Prof p(c, moe::kRecPermute, st);
+        MOE_CUDA(c, moe::launch_permute(hidden, T, h, k, ne, idx, c->tile_prefix, c->offsets,
+                                        c->x_perm, c->pos, c->p2p ? c->pr_x : nullptr, st));
+        p.end();
+        c->stats.kernel_launches += 1;
+    }
+
+    // Expert parallelism: ship each token row to the rank owning its expert.
+    const GemmGroup* g1 = c->grp1;
+    const GemmGroup* g2 = c->grp2;
+    if (c->ep) {
+        Prof p(c, moe::kRecComm, st);
+        moe_status s = c->p2p ? moe::p2p_after_dispatch(c, st) : moe::ep_dispatch(c, T, st);
+        if (s != MOE_OK) return s;
+        p.end();
+        tmA_routed = &c->tm_xrecv;
+        tmT_routed = &c->tm_xrecv_t;
+        g1 = c->ep_grp;
+        g2 = c->ep_grp + c->n_all;
+        y_routed = c->y_recv;
+    }
+
+    const moe_status rs = run_items(S, c->n_all, g1, g2);   // the routed experts
+    if (rs != MOE_OK) return rs;
     {
         moe_status fs = flush_copies(c);  // nothing may stay pending across calls
         if (fs != MOE_OK) return fs;
@@ -776,6 +795,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     ok &= dalloc((void**)&c->counts, sizeof(int32_t) * (size_t)(ne + S));
     ok &= dalloc((void**)&c->grp1, sizeof(GemmGroup) * (size_t)(ne + S));
     ok &= dalloc((void**)&c->grp2, sizeof(GemmGroup) * (size_t)(ne + S));
+    ok &= dalloc((void**)&c->shared_grp, sizeof(GemmGroup) * 2 * (size_t)c->n_all);
     ok &= dalloc((void**)&c->pos, sizeof(int32_t) * (size_t)Tm * k);
     ok &= dalloc((void**)&c->x_perm, 2 * (size_t)Tm * k * h);
     ok &= dalloc((void**)&c->h_act, 2 * (size_t)h_rows * hi);
@@ -1067,7 +1087,7 @@ moe_status moe_destroy(moe_ctx c) {
         cudaFree(c->lw_slot[i]);
     }
     void* bufs[] = {c->idx_ws, c->gates_ws, c->tile_counts, c->tile_prefix, c->offsets, c->counts,
-                    c->grp1, c->grp2, c->pos, c->x_perm, c->h_act, c->y_perm,
+                    c->grp1, c->grp2, c->shared_grp, c->pos, c->x_perm, c->h_act, c->y_perm,
                     c->h1_ws, c->u_ws, c->oproj_grp};
     for (void* p : bufs) cudaFree(p);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);

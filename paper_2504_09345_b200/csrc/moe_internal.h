@@ -122,6 +122,11 @@ cudaError_t launch_rmsnorm(const __nv_bfloat16* h1, const __nv_bfloat16* gamma, 
 // One GEMM group {a_begin, a_end, out_base} written on the stream (device-side group tables are
 // how the GEMM learns its rows without a host sync).
 cudaError_t launch_fill_group(GemmGroup* g, int a_begin, int a_end, int out_base, cudaStream_t st);
+// Groups of the S shared experts (A = the T local tokens): GEMM1 g[n_local + s] =
+// {0, T, hbase + s T} (h_act rows), GEMM2 g[n_all + n_local + s] = {hbase + s T, ... + T,
+// ybase + s T} (y_perm rows).
+cudaError_t launch_fill_shared_groups(GemmGroup* g, int n_local, int n_all, int S, int T,
+                                      int hbase, int ybase, cudaStream_t st);
 
 // ---------------------------------------------------------------------------- expert GEMM
 enum GemmMode { kGemmSwiGLU = 0, kGemmPlain = 1, kGemmResidual = 2 };

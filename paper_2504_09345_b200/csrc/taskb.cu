@@ -61,6 +61,16 @@ __global__ void fill_group_kernel(GemmGroup* g, int a_begin, int a_end, int out_
     *g = GemmGroup{a_begin, a_end, out_base, 0};
 }
 
+__global__ void fill_shared_groups_kernel(GemmGroup* g, int n_local, int n_all, int S, int T,
+                                          int hbase, int ybase) {
+    const int s = threadIdx.x;
+    if (s < S) {
+        const int hb = hbase + s * T;
+        g[n_local + s] = GemmGroup{0, T, hb, 0};
+        g[n_all + n_local + s] = GemmGroup{hb, hb + T, ybase + s * T, 0};
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_rmsnorm(const __nv_bfloat16* h1, const __nv_bfloat16* gamma, int T, int h,
@@ -73,6 +83,12 @@ cudaError_t launch_rmsnorm(const __nv_bfloat16* h1, const __nv_bfloat16* gamma, 
 
 cudaError_t launch_fill_group(GemmGroup* g, int a_begin, int a_end, int out_base, cudaStream_t st) {
     fill_group_kernel<<<1, 1, 0, st>>>(g, a_begin, a_end, out_base);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_shared_groups(GemmGroup* g, int n_local, int n_all, int S, int T,
+                                      int hbase, int ybase, cudaStream_t st) {
+    fill_shared_groups_kernel<<<1, 32, 0, st>>>(g, n_local, n_all, S, T, hbase, ybase);
     return cudaGetLastError();
 }
 

@@ -61,3 +61,26 @@ def test_random_shapes(case, mode, monkeypatch):
         assert err.max() <= TOL, f"{shape}: max token rel err {err.max():.3e}"
     finally:
         run.close()
+
+
+@pytest.mark.parametrize("shape", [
+    dict(hidden=8192, ffn=256, num_experts=128, top_k=8, num_shared=8, tokens=64),  # maxima
+    dict(hidden=128, ffn=4096, num_experts=2, top_k=2, num_shared=0, tokens=1),     # k = N_e, T=1
+    dict(hidden=2048, ffn=128, num_experts=128, top_k=1, num_shared=0, tokens=4000),
+])
+def test_envelope_maxima(shape):
+    """Envelope corners of include/moe.h: N_e = 128, top_k = 8, num_shared = 8, h = 8192 (K up
+    to 8192 in GEMM1), a single token, 128 experts with top-1 over 4000 tokens."""
+    cfg = synth.MoEConfig("custom", 140, shape["hidden"], shape["ffn"], shape["num_experts"],
+                          shape["top_k"], shape["tokens"], shape["num_shared"])
+    inp = synth.gen_inputs(cfg)
+    run = GpuRun(inp)
+    try:
+        out, idx, gates = run.run()
+        y_ref, idx_ref, g_ref = oracle.forward(inp.x, inp.router, inp.w1, inp.w3, inp.w2,
+                                               cfg.top_k, cfg.num_shared)
+        assert np.array_equal(idx.cpu().numpy(), idx_ref)
+        assert np.max(np.abs(gates.cpu().numpy() - g_ref)) <= 1e-6
+        assert token_rel_err(to_f32(out), y_ref).max() <= TOL
+    finally:
+        run.close()
