@@ -12,8 +12,9 @@
  *
  * Expert weights live in pinned host memory ("All weights are stored in pinned CPU memory",
  * PAPER.md:823) and are streamed into a bounded GPU buffer ("two times the model weight size
- * divided by the number of layers", PAPER.md:824-825 -- here two expert-sized slots) on every
- * call, prefetched one step ahead by an asynchronous copy stream.
+ * divided by the number of layers", PAPER.md:824-825 -- here N expert-sized slots, at most
+ * ~512 MiB, always fewer than the experts of a call) on every call, prefetched ahead by an
+ * asynchronous copy stream.
  *
  * Conventions (all entry points):
  *   - No C++ types or exceptions cross this boundary.  Every entry point returns a moe_status.
@@ -87,10 +88,10 @@ typedef struct {
     const void* nccl_unique_id; /* 128-byte ncclUniqueId (world_size > 1), else NULL           */
     int64_t packet_bytes;     /* 0 = one DMA per expert; else H2D packets of this size          */
     uint32_t flags;           /* MOE_FLAG_*                                                    */
-    int32_t num_slots;        /* expert staging slots, 2..16 (must be < streamed experts per
-                                 call when > 2); 0 = auto: enough slots to hold ~256 MiB of
-                                 weights (2 for Mixtral-size experts, up to 8 for fine-grained
-                                 ones).  The paper's buffer is two LAYERS;
+    int32_t num_slots;        /* expert staging slots, 2..32 (must be < streamed experts per
+                                 call when > 2); 0 = auto: enough slots to hold ~512 MiB of
+                                 weights (2 for Mixtral-size experts, 32 for DeepSeek-V2-Lite-
+                                 size ones).  The paper's buffer is two LAYERS;
                                  slots are recycled every call, so weights are always re-streamed. */
 } moe_config;
 
@@ -116,7 +117,7 @@ moe_status moe_host_alloc(size_t bytes, void** ptr);
 moe_status moe_host_free(void* ptr);
 
 /* Create a context on cfg->device: validates cfg, allocates the workspace for max_tokens
- * tokens, cfg->num_slots (0 = auto, ~256 MiB) staging slots of moe_packed_expert_bytes each, the
+ * tokens, cfg->num_slots (0 = auto, ~512 MiB) staging slots of moe_packed_expert_bytes each, the
  * copy stream and events, and (world_size > 1) the NCCL communicator.  *out is NULL on failure:
  * MOE_E_INVAL (bad cfg), MOE_E_UNSUPPORTED (outside the envelope or not an sm_100 device),
  * MOE_E_NOMEM, MOE_E_CUDA, MOE_E_NCCL. */

@@ -4,7 +4,7 @@
 // beginning of each stage by the Contiguous Data Mover ... runs asynchronously ... synchronizes
 // only at the stage boundaries"; PAPER.md:823-826 pinned host weights and a GPU weight buffer of
 // two units; PAPER.md:829-835 packetised transfers):
-//   * N device staging slots (N = num_slots, auto ~256 MiB), each one packed expert (W13 | W2);
+//   * N device staging slots (N = num_slots, auto ~512 MiB), each one packed expert (W13 | W2);
 //   * a dedicated copy stream; the copy of streamed item q into slot q%N waits on `slot_free[q%N]`
 //     (recorded after the GEMMs of item q-N) and records `ready13` / `ready2`, so the H2D of the
 //     next experts overlaps the GEMMs of expert e; consecutive small experts move in one DMA;
@@ -361,7 +361,7 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         const int s = (int)(q % (uint64_t)ns);
         const bool shared = expert_of(i) >= c->n_local;
         int nb = (int)(c->batch_q0[s] + (uint64_t)c->batch_n[s] - q);
-        nb = std::max(1, std::min(nb, (shared ? S : c->n_all) - i));
+        nb = std::max(1, std::min({nb, (shared ? S : c->n_all) - i, moe::kMaxBatch}));
         if (use_swap(2 * hi) || use_swap(h)) nb = 1;   // the swap kernel takes one group
         moe::GemmBatch b1{}, b2{};
         b1.table = g1;
@@ -737,13 +737,14 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     if (!c->bn1 || !c->bn2) return fail(MOE_E_UNSUPPORTED);
     if (cfg->num_slots > 0) {
         c->nslots = cfg->num_slots;
-    } else {  // auto: ~256 MiB of staging, 2..16 slots, fewer than the experts streamed per call
-        // (measured on DSV2-Lite-size experts: 8 slots 95.1%, 12-16 slots 98.7% of roofline)
+    } else {  // auto: ~512 MiB of staging, 2..32 slots, fewer than the experts streamed per call
+        // (measured on DSV2-Lite-size experts: 8 slots 95.1%, 16 slots 98.9%, 24-32 slots with
+        // 12-16-expert DMAs 99.4% of roofline)
         const int64_t want = (moe::kAutoSlotBytes + c->blob_bytes - 1) / c->blob_bytes;
         c->nslots = (int)std::max<int64_t>(
             2, std::min<int64_t>({want, (int64_t)moe::kMaxSlots, (int64_t)c->n_all - 1}));
     }
-    // DMA batches of ~64 MiB, at most half the slots (two batches in flight)
+    // DMA batches of ~192 MiB, at most half the slots (two batches in flight)
     c->copy_group = (int)std::max<int64_t>(
         1, std::min<int64_t>((moe::kCopyBatchBytes + c->blob_bytes - 1) / c->blob_bytes, c->nslots / 2));
     if (const char* e = getenv("MOE_COPY_GROUP")) c->copy_group = std::max(1, std::min(atoi(e), c->nslots));

@@ -75,7 +75,7 @@ def test_pack_rejects_bad_shapes(lib):
     (dict(world_size=3), moe.MOE_E_UNSUPPORTED),      # 8 experts do not shard over 3 ranks
     (dict(rank=2, world_size=2), moe.MOE_E_INVAL),
     (dict(num_slots=1), moe.MOE_E_INVAL),             # double buffering needs >= 2 slots
-    (dict(num_slots=17), moe.MOE_E_INVAL),            # > kMaxSlots
+    (dict(num_slots=33), moe.MOE_E_INVAL),            # > kMaxSlots
     (dict(num_slots=8), moe.MOE_E_INVAL),             # >= experts streamed per call (8)
     (dict(world_size=2, rank=0), moe.MOE_E_INVAL),    # EP needs an ncclUniqueId
 ])
