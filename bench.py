@@ -231,12 +231,12 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
-    # ---- N > 1: pin this rank's host threads (and so its pinned weight pages, first-touched by
+    # ---- pin this rank's host threads (and so its pinned weight pages, first-touched by
     # cudaHostAlloc) to the CPUs local to its GPU, so each GPU streams from its own NUMA node
-    # (the paper used numactl).
+    # (the paper used numactl).  MOE_BENCH_NO_AFFINITY=1 disables it.
     all_cpus = os.sched_getaffinity(0)
     affinity = {"numa_local": False, "cpus": len(all_cpus)}
-    if world > 1:
+    if os.environ.get("MOE_BENCH_NO_AFFINITY") != "1":
         try:
             import pynvml
             pynvml.nvmlInit()
