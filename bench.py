@@ -140,7 +140,25 @@ def cpu_baseline(inp, seconds: float) -> dict:
             n *= 2
     return {"value": done / elapsed, "unit": "tokens/s", "cores": cores, "kind": "oracle",
             "sample": f"{done} of {cfg.tokens} tokens of the {cfg.name} layer ({rounds} calls, "
-                      f"{elapsed:.1f} s, fp64 router + fp32 experts, OpenMP)"}
+                      f"{elapsed:.1f} s, fp64 router + fp32 experts, OpenMP)",
+            "host": host_cpu_info()}
+
+
+def host_cpu_info() -> dict:
+    """lscpu model / sockets / cores / SMT of the box the oracle ran on."""
+    info = {}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        keys = {"Model name": "model", "Socket(s)": "sockets", "Core(s) per socket":
+                "cores_per_socket", "Thread(s) per core": "threads_per_core",
+                "NUMA node(s)": "numa_nodes"}
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in keys:
+                info[keys[k.strip()]] = v.strip()
+    except Exception as e:  # noqa: BLE001 -- informational only
+        info["error"] = str(e)[:80]
+    return info
 
 
 def run_reference(args):
@@ -174,7 +192,8 @@ def run_reference(args):
                        "ffn": cfg.ffn, "experts": cfg.num_experts, "top_k": cfg.top_k,
                        "tokens_per_step": n},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
-                             "sample": f"{n} tokens per step of the {cfg.name} layer"},
+                             "sample": f"{n} tokens per step of the {cfg.name} layer",
+                             "host": host_cpu_info()},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
