@@ -6,9 +6,11 @@ tokens/s, weights streamed from host; % of roofline").
 
 A step = one full MoE-layer call (router GEMM + top-k gating, permute, grouped SwiGLU expert
 GEMMs, combine) with ALL of the layer's expert weights streamed from pinned host DRAM during the
-step; consecutive steps cycle L=2 distinct layers (distinct host weight sets), and staging is two
-expert slots, so nothing is reused across steps.  The 2.8 GB of weights streamed per step are far
-larger than L2 (126 MB), which is the "inputs larger than L2" rule.
+step; consecutive steps cycle L=2 distinct layers (distinct host weight sets), and staging holds
+fewer expert slots than the layer has experts (2 at C1; asserted), so nothing is reused across
+steps.  The 2.8 GB of weights streamed per step are far larger than L2 (126 MB), which is the
+"inputs larger than L2" rule.  --taskb times GPU Task B (O-projection + RMSNorm + MoE); N > 1
+runs under torchrun with expert parallelism (P2P transport over CUDA IPC, NCCL fallback).
 
 Printed JSON (one line, rank 0): value = tokens/s over the timed region (device CUDA events on the
 launching stream, max over ranks), plus `roofline` (dominant kernel: the GEMM1+SwiGLU tcgen05
