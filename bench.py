@@ -420,6 +420,18 @@ def run_ours(args):
                 "traffic": traffic if world == 1 else None,
                 "peak_source": peaks["source"] + " bf16_tflops (burst)",
                 "flops_per_launch": g1_flops_launch, "avg_launch_ms": g1_launch_ms}
+    # The SM clock the GEMM1 launches actually ran at (in-kernel clock64 / globaltimer, CTA 0,
+    # averaged over launches; moe_stats.gemm1_sm_mhz) and the tensor-pipe efficiency at that
+    # clock: achieved / (148 SMs x 8192 dense bf16 FLOP/clk/SM x clock).  8192 FLOP/clk/SM is
+    # 2.25 PFLOP/s nominal at 1.856 GHz -- higher than 2.25 PF / 1.965 GHz (7737), so the
+    # conservative per-cycle denominator.  Power management lowers the clock under dense MMA load.
+    g1_mhz = st.get("gemm1_sm_mhz", 0.0)
+    if g1_mhz > 0:
+        per_clk_peak_tf = torch.cuda.get_device_properties(local).multi_processor_count * 8192.0 * g1_mhz * 1e6 / 1e12
+        roofline["sm_mhz_in_kernel"] = g1_mhz
+        roofline["peak_at_kernel_clock"] = per_clk_peak_tf
+        roofline["frac_at_kernel_clock"] = achieved_tf / per_clk_peak_tf
+        roofline["gemm2_sm_mhz_in_kernel"] = st.get("gemm2_sm_mhz", 0.0)
     h2d_gbs = st["h2d_weight_bytes"] / (st["h2d_ms"] * 1e-3) / 1e9 if st["h2d_ms"] > 0 else 0.0
     roofline_step = {"bound": "host_link" if t_io >= t_tc else "tensor",
                      "t_roofline_ms": t_roof * 1e3, "t_host_link_ms": t_io * 1e3,

@@ -220,6 +220,10 @@ typedef struct {
     double token_latency_ms;      /* sum over host calls: enqueue -> tokens resident on the GPU */
     int64_t taskb_calls;          /* moe_taskb_forward calls (each also counts in `calls`)    */
     double oproj_ms, norm_ms;     /* Task B: O-projection GEMM, RMSNorm                       */
+    /* Mean SM clock while the expert GEMMs ran (MOE_FLAG_PROFILE): clock64 cycles / globaltimer
+     * ns of CTA 0 from its first to its last instruction, summed over launches -- the clock the
+     * tensor-core roofline of those kernels must be scaled to (power management).  0 = none. */
+    double gemm1_sm_mhz, gemm2_sm_mhz;
 } moe_stats;
 
 moe_status moe_get_stats(moe_ctx ctx, moe_stats* out);   /* synchronises the context */

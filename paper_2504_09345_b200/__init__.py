@@ -62,7 +62,8 @@ class moe_stats(ctypes.Structure):
                 ("num_slots", ctypes.c_int64), ("comm_bytes", ctypes.c_int64),
                 ("host_calls", ctypes.c_int64), ("token_latency_ms", ctypes.c_double),
                 ("taskb_calls", ctypes.c_int64), ("oproj_ms", ctypes.c_double),
-                ("norm_ms", ctypes.c_double)]
+                ("norm_ms", ctypes.c_double), ("gemm1_sm_mhz", ctypes.c_double),
+                ("gemm2_sm_mhz", ctypes.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -87,16 +87,22 @@ struct moe_ctx_s {
     // GEMM launch can cover experts in different slots (GemmBatch::b_row).
     CUtensorMap tm_w13, tm_w2;
     CUtensorMap tm_w13_pair, tm_w2_pair;   // 128-row boxes (CTA-pair GEMM)
+    moe::PairBMaps tm_w13_alt, tm_w2_alt;  // 112 / 96-row boxes (224 / 192-wide pair tiles)
     // DMA batches (flush_copies): slot s holds item batch_q0[s] + j of a batch of batch_n[s]
     uint64_t batch_q0[moe::kMaxSlots] = {};
     int batch_n[moe::kMaxSlots] = {};
-    int pair_mode = -1;       // MOE_GEMM_PAIR: 0 never, 1 always, -1 auto (default: wave model)
+    // MOE_GEMM_PAIR: 0 never, 1 always, -1 auto (default): the host's wave model on the
+    // EXPECTED group sizes, one launch; 2 ("device"): both kernels are launched and the device
+    // picks by the wave model on the ACTUAL group sizes (GemmBatch::select; measured slower
+    // in-bench: the losing launch costs ~10 us).
+    int pair_mode = -1;
     // Tail split (MOE_GEMM_TAILSPLIT=1, experiment, default off): a CTA-pair GEMM covers only
     // whole 256-row tiles of each group; the < 256-row remainder runs as 128-row tiles in a
     // concurrent launch on tail_stream (forked / joined with events).  Measured slower at C1
     // (GEMM1 1.61 -> 1.74 ms/step) and C4, +2% at C3: the tail CTAs do not just fill the pair
     // kernel's idle last wave.
     bool tail_split = false;
+    bool alt_tiles = false;   // MOE_GEMM_ALT=1: pair kernel may pick 224/192-wide tiles
     cudaStream_t tail_stream = nullptr;
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
 
@@ -117,6 +123,10 @@ struct moe_ctx_s {
     CUtensorMap tm_xperm, tm_h;
     moe::TokenMaps tm_xperm_t, tm_h_t;  // token operands of the swap-AB GEMM
     int swap_mode = 0;                  // MOE_GEMM_SWAP: 0 never, 1 always
+    // MOE_GEMM_TAILSWAP: pair-kernel groups end in a swap-AB tail tile when the last partial
+    // tile has <= 128 rows; MOE_GEMM_TAILCOST: its scheduling cost in full-tile units.
+    bool tail_swap = false;   // measured: no gain
+    float tail_cost = 0.6f;
     int64_t last_rows = 0;
 
     // expert parallelism (world_size > 1, or MOE_FLAG_FORCE_EP)
@@ -149,6 +159,7 @@ struct moe_ctx_s {
     moe::PeerRows* pr_y = nullptr;           // peers' y_recv + the same bases
     int32_t* p2p_rows = nullptr;             // device: rows received by the last call
     long long* p2p_bytes = nullptr;          // device: bytes moved (stats)
+    unsigned long long* clk_acc = nullptr;   // device [4]: GEMM1 / GEMM2 SM cycles, ns (profile)
     void* ipc_opened[moe::kMaxRanks][4] = {};  // IPC mappings to close (MOE_FLAG_IPC_EP)
     long long* p2p_diag_h = nullptr;         // pinned, mapped: a timed-out flag wait (moe_sync)
     long long* p2p_diag_d = nullptr;
@@ -165,6 +176,7 @@ struct moe_ctx_s {
     char* lw_slot[2] = {nullptr, nullptr};
     cudaEvent_t lw_ready[2] = {}, lw_free[2] = {};
     CUtensorMap tm_wo[2], tm_wo_pair[2];
+    moe::PairBMaps tm_wo_alt[2];
     uint64_t lw_seq = 0;
     __nv_bfloat16* h1_ws = nullptr;   // [max_tokens, h] residual stream after the O-projection
     __nv_bfloat16* u_ws = nullptr;    // [max_tokens, h] normalised MoE input

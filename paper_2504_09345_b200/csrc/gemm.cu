@@ -21,6 +21,8 @@
 //   warp 2     TMEM allocator (2 x BN fp32 columns: double-buffered accumulator)
 //   warps 4-7  epilogue: tcgen05.ld 32x32b -> fp32 math -> bf16 -> global
 // Pipelines: smem full/empty mbarriers (TMA <-> MMA), TMEM full/empty (MMA <-> epilogue).
+#include <algorithm>
+
 #include "moe_internal.h"
 #include "ptx.cuh"
 
@@ -32,7 +34,7 @@ constexpr int BM = 128;
 constexpr int BK = 64;  // one 128-byte swizzle atom of bf16
 constexpr int kThreads = 256;
 
-constexpr size_t kBatchReserve = 512;   // shared memory for BatchInfo (below)
+constexpr size_t kBatchReserve = 640;   // shared memory for BatchInfo (below)
 
 template <int BN>
 struct GemmCfg {
@@ -69,6 +71,24 @@ __device__ __forceinline__ uint64_t l2_policy_b() {
     return g_l2_hints ? ptx::policy_evict_first() : ptx::policy_evict_normal();
 }
 
+// SM clock probe (GemmBatch::clk): thread 0 of CTA 0 samples at entry and adds at exit.
+struct ClkProbe {
+    uint64_t c0 = 0, t0 = 0;
+    __device__ __forceinline__ void start(const GemmBatch& b) {
+        if (b.clk && blockIdx.x == 0 && threadIdx.x == 0) {
+            t0 = ptx::globaltimer_ns();
+            c0 = clock64();
+        }
+    }
+    __device__ __forceinline__ void stop(const GemmBatch& b) {
+        if (b.clk && blockIdx.x == 0 && threadIdx.x == 0) {
+            const uint64_t c1 = clock64(), t1 = ptx::globaltimer_ns();
+            atomicAdd(b.clk, (unsigned long long)(c1 - c0));
+            atomicAdd(b.clk + 1, (unsigned long long)(t1 - t0));
+        }
+    }
+};
+
 __device__ __forceinline__ float silu_mul(float g, float u) {
     return g / (1.0f + __expf(-g)) * u;
 }
@@ -77,9 +97,9 @@ __device__ __forceinline__ float silu_mul(float g, float u) {
 // bf16 -> global.  SwiGLU tiles hold gate columns [0, BN/2) and the matching up columns
 // [BN/2, BN); they produce BN/2 outputs.  tcgen05.ld is warp-collective: every lane loads, only
 // rows inside the group store.
-template <int BN, int MODE>
+template <int MODE>
 __device__ __forceinline__ void epilogue_row(uint32_t taddr, bool valid, __nv_bfloat16* row_out,
-                                             const __nv_bfloat16* row_res, int n) {
+                                             const __nv_bfloat16* row_res, int n, int BN) {
     if (MODE == kGemmSwiGLU) {
         // packed W13 (moe_pack_expert): 32-column blocks = 16 gate columns, then the 16 matching
         // up columns -> 16 output features per 32 accumulator columns
@@ -139,18 +159,29 @@ __device__ __forceinline__ void epilogue_row(uint32_t taddr, bool valid, __nv_bf
 // The groups of one launch (up to kMaxBatch experts whose weights sit in different staging slots
 // of one tensor map), resolved once per CTA into shared memory: global tile t belongs to group
 // g with first[g] <= t < first[g + 1]; inside a group tiles follow tile_coords().
+// With tail swap (pair kernel): a group whose last partial tile has r <= 128 rows has m_tiles =
+// rows / 256 full tiles plus n_tiles swap-AB tail tiles of tail_nc = ceil(r/32)*32 token columns;
+// the tail tiles of all such groups are numbered after the full tiles (TailSched below).
 struct BatchInfo {
-    int n, total;
+    int n, total, n_tail_grp, plan;
     int first[kMaxBatch + 1];
     int m_tiles[kMaxBatch];
     int a_begin[kMaxBatch], a_end[kMaxBatch], out_base[kMaxBatch], b_row[kMaxBatch];
+    int tail_nc[kMaxBatch];
+    int tail_grp[kMaxBatch];   // groups with a swap tail, last group first
 };
 constexpr size_t kBatchSmem = (sizeof(BatchInfo) + 15) & ~size_t(15);
 static_assert(kBatchSmem <= kBatchReserve, "BatchInfo does not fit its reservation");
 
-__device__ __forceinline__ void batch_init(BatchInfo* bi, const GemmBatch& b, int bm,
-                                           int n_tiles) {
-    int t = 0;
+// Tail rule shared by the kernel and the host model: rows of a group -> full 256-row tiles and
+// the swap-tail width (0 = no swap tail; the partial tile, if any, is an ordinary padded tile).
+__host__ __device__ __forceinline__ int tail_cols(int rows, bool tail_swap) {
+    const int rem = rows % kPairRows;
+    return (tail_swap && rem > 0 && rem <= 128) ? ((rem + 31) & ~31) : 0;
+}
+
+// Row ranges of the launch's groups (after the tail-split `part` cut), no tiling yet.
+__device__ __forceinline__ void batch_load(BatchInfo* bi, const GemmBatch& b) {
     for (int i = 0; i < b.n; ++i) {
         GemmGroup g = b.table[b.idx[i]];
         const int head = (max(0, g.a_end - g.a_begin) / kPairRows) * kPairRows;
@@ -160,18 +191,72 @@ __device__ __forceinline__ void batch_init(BatchInfo* bi, const GemmBatch& b, in
             g.a_begin += head;
             g.out_base += head;
         }
-        const int rows = max(0, g.a_end - g.a_begin);
         bi->a_begin[i] = g.a_begin;
-        bi->a_end[i] = g.a_end;
+        bi->a_end[i] = max(g.a_begin, g.a_end);
         bi->out_base[i] = g.out_base;
         bi->b_row[i] = b.b_row[i];
-        bi->m_tiles[i] = (rows + bm - 1) / bm;
+    }
+    bi->n = b.n;
+}
+
+// Tiles of bm rows x n_tiles weight tiles per group, numbered group after group.
+__device__ __forceinline__ void batch_tiles(BatchInfo* bi, int bm, int n_tiles, bool tail_swap) {
+    int t = 0;
+    for (int i = 0; i < bi->n; ++i) {
+        const int rows = bi->a_end[i] - bi->a_begin[i];
+        bi->tail_nc[i] = tail_cols(rows, tail_swap);
+        bi->m_tiles[i] = bi->tail_nc[i] ? rows / bm : (rows + bm - 1) / bm;
         bi->first[i] = t;
         t += bi->m_tiles[i] * n_tiles;
     }
-    bi->first[b.n] = t;
-    bi->n = b.n;
+    bi->first[bi->n] = t;
     bi->total = t;
+    int nt = 0;
+    for (int i = bi->n - 1; i >= 0; --i)
+        if (bi->tail_nc[i]) bi->tail_grp[nt++] = i;
+    bi->n_tail_grp = nt;
+}
+
+__device__ __forceinline__ void batch_init(BatchInfo* bi, const GemmBatch& b, int bm,
+                                           int n_tiles, bool tail_swap = false) {
+    batch_load(bi, b);
+    batch_tiles(bi, bm, n_tiles, tail_swap);
+}
+
+// Tile shape of a launch from the ACTUAL group sizes (both kernels evaluate it identically; see
+// GemmBatch::select): wave model time ~ ceil(tiles / concurrent tiles) x tile width / tensor
+// efficiency -- single-CTA 128 x bn_single tiles at 0.76 (shared-memory bound), CTA-pair
+// 256 x BN tiles at 0.97, BN in {256, 224, 192} where N % BN == 0.  Returns 0 (single-CTA
+// kernel) or the pair tile width; -1 if there is no work.
+__device__ __forceinline__ int plan_tiles(const BatchInfo* bi, int N, int sms, int bn_single,
+                                          bool allow_single, bool allow_pair, bool alt_maps) {
+    int rows128 = 0, rows256 = 0;
+    for (int i = 0; i < bi->n; ++i) {
+        const int r = bi->a_end[i] - bi->a_begin[i];
+        rows128 += (r + 127) / 128;
+        rows256 += (r + 255) / 256;
+    }
+    if (rows128 == 0) return -1;
+    int choice = -1;
+    float best = 3.0e38f;
+    if (allow_single && bn_single > 0) {
+        const int t = rows128 * (N / bn_single), conc = sms;
+        best = (float)((t + conc - 1) / conc) * ((float)bn_single / 256.f) / 0.76f;
+        choice = 0;
+    }
+    if (allow_pair) {
+        const int conc = sms / 2;
+        for (int bn = 256; bn >= 192; bn -= 32) {
+            if (N % bn || (bn != 256 && !alt_maps)) continue;
+            const int t = rows256 * (N / bn);
+            const float w = (float)((t + conc - 1) / conc) * ((float)bn / 256.f) / 0.97f;
+            if (w < best * 0.999f) {
+                best = w;
+                choice = bn;
+            }
+        }
+    }
+    return choice;
 }
 
 __device__ __forceinline__ int batch_locate(const BatchInfo* bi, int tile, int& local) {
@@ -180,6 +265,35 @@ __device__ __forceinline__ int batch_locate(const BatchInfo* bi, int tile, int& 
     local = tile - bi->first[g];
     return g;
 }
+
+// Static schedule of the pair kernel (every thread of every CTA computes it identically, so no
+// tile queue is needed): full tile t goes to pair t % P -- pair p has q = F / P full tiles, plus
+// one more if p < r = F % P -- then the R tail tiles (cost c each, in full-tile units) are dealt
+// out in rounds in order of the time a round would finish: a "light" round gives one tail to each
+// pair p >= r (done at q + c*(i+1)), a "heavy" round one to each pair p < r (q + 1 + c*(i+1)).
+// This is greedy least-loaded assignment for two load classes; next() yields pair p's tails.
+struct TailSched {
+    int R, p, q, r, nl, nh, j, li, hi;
+    float c;
+    __host__ __device__ void init(int F, int R_, int P, int p_, float c_) {
+        R = R_; p = p_; q = F / P; r = F % P; nl = P - r; nh = r; j = 0; li = 0; hi = 0; c = c_;
+    }
+    __host__ __device__ bool next(int& tj) {
+        while (j < R) {
+            const float tl = q + c * (li + 1);
+            const float th = nh ? q + 1 + c * (hi + 1) : 3.0e38f;
+            const int base = j;
+            if (tl <= th) {
+                j += nl; ++li;
+                if (p >= r && base + (p - r) < R) { tj = base + (p - r); return true; }
+            } else {
+                j += nh; ++hi;
+                if (p < r && base + p < R) { tj = base + p; return true; }
+            }
+        }
+        return false;
+    }
+};
 
 template <int BN, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -202,8 +316,14 @@ expert_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int n_tiles = N / BN;
-    if (threadIdx.x == 0) batch_init(bi, batch, BM, n_tiles);
+    ClkProbe clk;
+    clk.start(batch);
+    if (threadIdx.x == 0) {
+        batch_init(bi, batch, BM, n_tiles);
+        bi->plan = batch.select ? plan_tiles(bi, N, batch.select, BN, true, true, batch.alt_ok != 0) : 0;
+    }
     __syncthreads();
+    if (bi->plan != 0) return;                   // the CTA-pair kernel of this launch runs it
     const int total = bi->total;
     if ((int)blockIdx.x >= total) return;
     const int num_kb = K / BK;
@@ -310,8 +430,8 @@ expert_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
             const bool valid = arow < bi->a_end[gi];
             const int64_t orow = (int64_t)bi->out_base[gi] + (arow - bi->a_begin[gi]);
             const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-            epilogue_row<BN, MODE>(taddr, valid, out + orow * ldo,
-                                   resid ? resid + orow * ldo : nullptr, n);
+            epilogue_row<MODE>(taddr, valid, out + orow * ldo,
+                               resid ? resid + orow * ldo : nullptr, n, BN);
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
@@ -322,165 +442,7 @@ expert_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         ptx::tc_fence_after();
         ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
     }
-}
-
-// ------------------------------------------------------------------------------------------
-// CTA-pair variant (cta_group::2): a cluster of 2 CTAs on one TPC computes 256 x 256 tiles.
-// Each CTA stages its own 128 rows of A and half (128 rows) of the B tile per K step (32 KB, 6
-// stages), the leader issues tcgen05.mma.cta_group::2 (M=256) reading both CTAs' smem, and each
-// CTA's TMEM holds its 128 rows of the fp32 accumulator.  Per SM this halves the B bytes moved
-// per MMA and doubles the bytes in flight (6 x 32 KB vs 4 x 48 KB), for large expert groups.
-// Barrier protocol: full[s] (leader; arrivals: leader expect_tx + peer remote arrive; TMA bytes
-// of both CTAs), empty[s] (both; MMA commit multicast), tfull[a] (both; multicast), tempty[a]
-// (leader; 4 epilogue warps x 2 CTAs).
-constexpr int kPairStages = 6;
-constexpr uint32_t kPairABytes = 128 * BK * 2;   // per CTA
-constexpr uint32_t kPairBBytes = 128 * BK * 2;   // per CTA (half of a 256-row B tile)
-constexpr size_t kPairSmem =
-    1024 + kPairStages * (kPairABytes + kPairBBytes) + kBatchReserve + 256;
-
-template <int MODE>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-expert_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
-                        const __grid_constant__ CUtensorMap tmB,
-                        const __grid_constant__ GemmBatch batch, int N, int K,
-                        __nv_bfloat16* __restrict__ out, int ldo,
-                        const __nv_bfloat16* __restrict__ resid) {
-    constexpr int BN = 256, PM = 256, S = kPairStages;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    uint8_t* sA = smem;
-    uint8_t* sB = smem + S * kPairABytes;
-    BatchInfo* bi = reinterpret_cast<BatchInfo*>(sB + S * kPairBBytes);
-    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(bi) + kBatchSmem);
-    uint64_t* empty = full + S;
-    uint64_t* tfull = empty + S;
-    uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-
-    const uint32_t rank = ptx::cluster_ctarank();
-    const bool leader = rank == 0;
-    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-    const int n_tiles = N / BN;
-    if (threadIdx.x == 0) batch_init(bi, batch, PM, n_tiles);
-    __syncthreads();
-    const int total = bi->total;                 // identical in both CTAs of the cluster
-    if (pair >= total) return;                   // both CTAs of a pair leave together
-    const int num_kb = K / BK;
-    const int group_m = g_group_m > 0 ? g_group_m : ((K <= 8192) ? 16 : 4);  // 256-row tiles
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-    if (threadIdx.x == 0) {
-        ptx::prefetch_tmap(&tmA);
-        ptx::prefetch_tmap(&tmB);
-        for (int s = 0; s < S; ++s) {
-            ptx::mbar_init(&full[s], 2);
-            ptx::mbar_init(&empty[s], 1);
-        }
-        for (int a = 0; a < 2; ++a) {
-            ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], 8);
-        }
-        ptx::fence_barrier_init();
-        ptx::fence_proxy_async();
-    }
-    if (warp == 2) ptx::tmem_alloc_cta2<2 * BN>(tmem_slot);
-    ptx::tc_fence_before();
-    ptx::cluster_sync();
-    ptx::tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            // ---------------------------------------------------- TMA producer (both CTAs)
-            const uint64_t pol_a = l2_policy_a();
-            const uint64_t pol_b = l2_policy_b();
-            const uint32_t full0 = ptx::mapa_shared(&full[0], 0);  // leader's full[0]
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int tile = pair; tile < total; tile += npairs) {
-                int m, n, local;
-                const int gi = batch_locate(bi, tile, local);
-                tile_coords(local, bi->m_tiles[gi], n_tiles, group_m, m, n);
-                const int arow = bi->a_begin[gi] + m * PM + (int)rank * 128;
-                const int brow = bi->b_row[gi] + n * BN + (int)rank * 128;
-                for (int kb = 0; kb < num_kb; ++kb) {
-                    ptx::mbar_wait(&empty[stage], phase ^ 1u);
-                    const uint32_t fbar = full0 + stage * 8;
-                    if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (kPairABytes + kPairBBytes));
-                    else ptx::mbar_arrive_cluster(fbar);
-                    ptx::tma_load_2d_cta2(sA + stage * kPairABytes, &tmA, fbar, kb * BK, arow, pol_a);
-                    ptx::tma_load_2d_cta2(sB + stage * kPairBBytes, &tmB, fbar, kb * BK, brow, pol_b);
-                    if (++stage == S) {
-                        stage = 0;
-                        phase ^= 1u;
-                    }
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (leader && lane == 0) {
-            // ---------------------------------------------------- MMA issuer (leader only)
-            constexpr uint32_t idesc = ptx::umma_idesc_bf16(PM, BN);
-            int stage = 0;
-            uint32_t phase = 0;
-            int it = 0;
-            for (int tile = pair; tile < total; tile += npairs, ++it) {
-                const int acc = it & 1;
-                const uint32_t aphase = (it >> 1) & 1;
-                ptx::mbar_wait(&tempty[acc], aphase ^ 1u);
-                ptx::tc_fence_after();
-                const uint32_t d = tmem_base + acc * BN;
-                for (int kb = 0; kb < num_kb; ++kb) {
-                    ptx::mbar_wait(&full[stage], phase);
-                    ptx::tc_fence_after();
-                    const uint32_t a0 = ptx::smem_u32(sA + stage * kPairABytes);
-                    const uint32_t b0 = ptx::smem_u32(sB + stage * kPairBBytes);
-#pragma unroll
-                    for (int kk = 0; kk < BK / 16; ++kk)
-                        ptx::umma_bf16_cta2(d, ptx::umma_desc_sw128_kmajor(a0 + kk * 32),
-                                            ptx::umma_desc_sw128_kmajor(b0 + kk * 32), idesc,
-                                            (kb | kk) != 0 ? 1u : 0u);
-                    ptx::umma_commit_cta2_mc(&empty[stage], 0x3);
-                    if (++stage == S) {
-                        stage = 0;
-                        phase ^= 1u;
-                    }
-                }
-                ptx::umma_commit_cta2_mc(&tfull[acc], 0x3);
-            }
-        }
-    } else if (warp >= 4) {
-        // -------------------------------------------------------- epilogue (both CTAs)
-        const int q = warp - 4;
-        const uint32_t tempty0 = ptx::mapa_shared(&tempty[0], 0);
-        int it = 0;
-        for (int tile = pair; tile < total; tile += npairs, ++it) {
-            const int acc = it & 1;
-            const uint32_t aphase = (it >> 1) & 1;
-            int m, n, local;
-            const int gi = batch_locate(bi, tile, local);
-            tile_coords(local, bi->m_tiles[gi], n_tiles, group_m, m, n);
-            ptx::mbar_wait(&tfull[acc], aphase);
-            ptx::tc_fence_after();
-            const int arow = bi->a_begin[gi] + m * PM + (int)rank * 128 + q * 32 + lane;
-            const bool valid = arow < bi->a_end[gi];
-            const int64_t orow = (int64_t)bi->out_base[gi] + (arow - bi->a_begin[gi]);
-            const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-            epilogue_row<BN, MODE>(taddr, valid, out + orow * ldo,
-                                   resid ? resid + orow * ldo : nullptr, n);
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_cluster(tempty0 + acc * 8);
-        }
-    }
-    ptx::tc_fence_before();
-    ptx::cluster_sync();
-    if (warp == 2) {
-        ptx::tc_fence_after();
-        ptx::tmem_dealloc_cta2<2 * BN>(tmem_base);
-    }
+    clk.stop(batch);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -630,6 +592,256 @@ __device__ __forceinline__ void swap_epilogue(uint32_t taddr, int lane, int ncol
             __syncwarp();
         }
     }
+}
+
+// ------------------------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of 2 CTAs on one TPC computes 256 x 256 tiles.
+// Each CTA stages its own 128 rows of A and half (128 rows) of the B tile per K step (32 KB, 6
+// stages), the leader issues tcgen05.mma.cta_group::2 (M=256) reading both CTAs' smem, and each
+// CTA's TMEM holds its 128 rows of the fp32 accumulator.  Per SM this halves the B bytes moved
+// per MMA and doubles the bytes in flight (6 x 32 KB vs 4 x 48 KB), for large expert groups.
+// Barrier protocol: full[s] (leader; arrivals: leader expect_tx + peer remote arrive; TMA bytes
+// of both CTAs), empty[s] (both; MMA commit multicast), tfull[a] (both; multicast), tempty[a]
+// (leader; 4 epilogue warps x 2 CTAs).
+// Tail swap (batch.tail_swap): a group's last partial tile of r <= 128 rows is a swap-AB tile
+// instead -- the stage's B buffer takes the weight tile exactly as for a full tile, the A buffer
+// only the r tail tokens (nc/2 rows per CTA, nc = ceil(r/32)*32), and the leader issues
+// D^T[256 x nc] = W X^T with the operand descriptors swapped, so the tile moves ~half the bytes
+// and does nc/256 of the MMA work of a padded 256-row tile.  Its epilogue (TMEM lane = weight row)
+// transposes through shared memory (swap_epilogue).  Schedule: TailSched.
+constexpr int kPairStages = 6;
+constexpr uint32_t kPairABytes = 128 * BK * 2;   // per CTA
+constexpr uint32_t kPairBBytes = 128 * BK * 2;   // per CTA (half of a 256-row B tile)
+constexpr size_t kPairSmem =
+    1024 + kPairStages * (kPairABytes + kPairBBytes) + kSwapEpiBytes + kBatchReserve + 256;
+
+// One tile of the pair kernel's sequence: a full (or padded) 256 x 256 tile (nc == 0) of group gi
+// at M tile m, weight tile n; or a swap tail (nc > 0): token columns [m*256, m*256 + nc).
+struct PairTile {
+    int gi, m, n, nc;
+};
+struct PairSched {
+    int t, P, F, n_tiles, group_m;
+    TailSched ts;
+    __device__ __forceinline__ void init(const BatchInfo* bi, int pair, int npairs, int nt,
+                                         int gm, float cost) {
+        t = pair; P = npairs; F = bi->total; n_tiles = nt; group_m = gm;
+        ts.init(F, bi->n_tail_grp * nt, npairs, pair, cost);
+    }
+    __device__ __forceinline__ bool next(const BatchInfo* bi, PairTile& o) {
+        if (t < F) {
+            int local;
+            o.gi = batch_locate(bi, t, local);
+            tile_coords(local, bi->m_tiles[o.gi], n_tiles, group_m, o.m, o.n);
+            o.nc = 0;
+            t += P;
+            return true;
+        }
+        int tj;
+        if (!ts.next(tj)) return false;
+        o.gi = bi->tail_grp[tj / n_tiles];
+        o.n = n_tiles - 1 - tj % n_tiles;     // descending: the most recently used weights first
+        o.m = bi->m_tiles[o.gi];
+        o.nc = bi->tail_nc[o.gi];
+        return true;
+    }
+};
+
+template <int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+expert_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
+                        const __grid_constant__ CUtensorMap tmB,
+                        const __grid_constant__ TokenMaps tmT,
+                        const __grid_constant__ PairBMaps tmAlt,
+                        const __grid_constant__ GemmBatch batch, int N, int K,
+                        __nv_bfloat16* __restrict__ out, int ldo,
+                        const __nv_bfloat16* __restrict__ resid) {
+    constexpr int PM = 256, S = kPairStages, kAccCols = 256;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + S * kPairABytes;
+    float* sE = reinterpret_cast<float*>(sB + S * kPairBBytes);
+    BatchInfo* bi = reinterpret_cast<BatchInfo*>(sB + S * kPairBBytes + kSwapEpiBytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(bi) + kBatchSmem);
+    uint64_t* empty = full + S;
+    uint64_t* tfull = empty + S;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const uint32_t rank = ptx::cluster_ctarank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    ClkProbe clk;
+    clk.start(batch);
+    if (threadIdx.x == 0) {
+        batch_load(bi, batch);
+        // tile width: 256, or 224 / 192 when that needs fewer waves; 0 = the single-CTA kernel
+        // of this launch runs it (select), -1 = nothing to do
+        const int plan = batch.select
+            ? plan_tiles(bi, N, batch.select, batch.bn_single, true, true, batch.alt_ok != 0)
+            : plan_tiles(bi, N, gridDim.x, 0, false, true, batch.alt_ok != 0);
+        bi->plan = plan;
+        if (plan > 0) batch_tiles(bi, PM, N / plan, batch.tail_swap != 0 && plan == 256);
+    }
+    __syncthreads();
+    if (bi->plan <= 0) return;                   // uniform over the grid
+    const int BN = bi->plan;
+    const int n_tiles = N / BN;
+    const CUtensorMap* mB = BN == 256 ? &tmB : (BN == 224 ? &tmAlt.b224 : &tmAlt.b192);
+    const int num_kb = K / BK;
+    const int group_m = g_group_m > 0 ? g_group_m : ((K <= 8192) ? 16 : 4);  // 256-row tiles
+    PairSched sched0;
+    sched0.init(bi, pair, npairs, n_tiles, group_m, batch.tail_cost);
+    {
+        PairSched probe = sched0;
+        PairTile pt;
+        if (!probe.next(bi, pt)) return;         // identical in both CTAs: the pair leaves together
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(mB);
+        for (int s = 0; s < S; ++s) {
+            ptx::mbar_init(&full[s], 2);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], 8);
+        }
+        ptx::fence_barrier_init();
+        ptx::fence_proxy_async();
+    }
+    if (warp == 2) ptx::tmem_alloc_cta2<2 * kAccCols>(tmem_slot);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------------------------------------------- TMA producer (both CTAs)
+            const uint64_t pol_a = l2_policy_a();
+            const uint64_t pol_b = l2_policy_b();
+            const uint32_t full0 = ptx::mapa_shared(&full[0], 0);  // leader's full[0]
+            int stage = 0;
+            uint32_t phase = 0;
+            PairSched sc = sched0;
+            PairTile pt;
+            while (sc.next(bi, pt)) {
+                const int brow = bi->b_row[pt.gi] + pt.n * BN + (int)rank * (BN / 2);
+                const int half = pt.nc >> 1;   // swap tail: token rows of this CTA
+                const int arow = bi->a_begin[pt.gi] + pt.m * PM + (int)rank * (pt.nc ? half : 128);
+                const uint32_t tx = pt.nc ? 2 * kPairBBytes + (uint32_t)pt.nc * BK * 2
+                                          : 2 * kPairABytes + (uint32_t)BN * BK * 2;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1u);
+                    const uint32_t fbar = full0 + stage * 8;
+                    if (leader) ptx::mbar_arrive_expect_tx(&full[stage], tx);
+                    else ptx::mbar_arrive_cluster(fbar);
+                    ptx::tma_load_2d_cta2(sB + stage * kPairBBytes, mB, fbar, kb * BK, brow, pol_b);
+                    if (!pt.nc) {
+                        ptx::tma_load_2d_cta2(sA + stage * kPairABytes, &tmA, fbar, kb * BK, arow, pol_a);
+                    } else {
+                        uint8_t* a = sA + stage * kPairABytes;
+                        for (int i = 1, r = 0; i < 4; ++i) {   // boxes of 64, 32, 16 rows
+                            const int box = 128 >> i;
+                            if (half - r >= box) {
+                                ptx::tma_load_2d_cta2(a + r * (BK * 2), &tmT.box[i], fbar, kb * BK,
+                                                      arow + r, pol_a);
+                                r += box;
+                            }
+                        }
+                    }
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {
+            // ---------------------------------------------------- MMA issuer (leader only)
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            PairSched sc = sched0;
+            PairTile pt;
+            while (sc.next(bi, pt)) {
+                const uint32_t idesc = ptx::umma_idesc_bf16(PM, pt.nc ? (uint32_t)pt.nc : (uint32_t)BN);
+                const int acc = it & 1;
+                const uint32_t aphase = (it >> 1) & 1;
+                ptx::mbar_wait(&tempty[acc], aphase ^ 1u);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem_base + acc * kAccCols;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a0 = ptx::smem_u32(sA + stage * kPairABytes);
+                    const uint32_t b0 = ptx::smem_u32(sB + stage * kPairBBytes);
+                    // swap tail: the weights (B buffer) are the MMA's A operand
+                    const uint32_t x0 = pt.nc ? b0 : a0, y0 = pt.nc ? a0 : b0;
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk)
+                        ptx::umma_bf16_cta2(d, ptx::umma_desc_sw128_kmajor(x0 + kk * 32),
+                                            ptx::umma_desc_sw128_kmajor(y0 + kk * 32), idesc,
+                                            (kb | kk) != 0 ? 1u : 0u);
+                    ptx::umma_commit_cta2_mc(&empty[stage], 0x3);
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+                ptx::umma_commit_cta2_mc(&tfull[acc], 0x3);
+                ++it;
+            }
+        }
+    } else if (warp >= 4) {
+        // -------------------------------------------------------- epilogue (both CTAs)
+        const int q = warp - 4;
+        const uint32_t tempty0 = ptx::mapa_shared(&tempty[0], 0);
+        int it = 0;
+        PairSched sc = sched0;
+        PairTile pt;
+        while (sc.next(bi, pt)) {
+            const int acc = it & 1;
+            const uint32_t aphase = (it >> 1) & 1;
+            ptx::mbar_wait(&tfull[acc], aphase);
+            ptx::tc_fence_after();
+            const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
+            const int gi = pt.gi;
+            if (!pt.nc) {
+                const int arow = bi->a_begin[gi] + pt.m * PM + (int)rank * 128 + q * 32 + lane;
+                const bool valid = arow < bi->a_end[gi];
+                const int64_t orow = (int64_t)bi->out_base[gi] + (arow - bi->a_begin[gi]);
+                epilogue_row<MODE>(taddr, valid, out + orow * ldo,
+                                   resid ? resid + orow * ldo : nullptr, pt.n, BN);
+            } else {
+                // TMEM lane = weight row n*256 + rank*128 + q*32 + lane, column = tail token
+                const int tok0 = pt.m * PM;
+                const int fcol = (MODE == kGemmSwiGLU) ? pt.n * 128 + (int)rank * 64 + q * 16
+                                                       : pt.n * 256 + (int)rank * 128 + q * 32;
+                swap_epilogue<MODE>(taddr, lane, pt.nc, tok0, bi->a_end[gi] - bi->a_begin[gi],
+                                    (int64_t)bi->out_base[gi] + tok0, out, ldo, fcol, resid,
+                                    sE + q * (32 * 33));
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster(tempty0 + acc * 8);
+            ++it;
+        }
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc_cta2<2 * kAccCols>(tmem_base);
+    }
+    clk.stop(batch);
 }
 
 // tmW: weights [M, K] (box 64 x 128); tmX: group tokens [*, K] (TokenMaps); M = 2 h_i (SwiGLU)
@@ -804,17 +1016,22 @@ cudaError_t launch_swap(const CUtensorMap* tmW, const TokenMaps* tmX, const Gemm
 }
 
 template <int MODE>
-cudaError_t launch_pair(const CUtensorMap* tmA, const CUtensorMap* tmB, const GemmBatch& batch,
-                        int N, int K, __nv_bfloat16* out, int ldo, const __nv_bfloat16* resid,
-                        int grid, cudaStream_t st) {
+cudaError_t launch_pair(const CUtensorMap* tmA, const CUtensorMap* tmB, const TokenMaps* tmT,
+                        const PairBMaps* alt, const GemmBatch& batch, int N, int K,
+                        __nv_bfloat16* out, int ldo, const __nv_bfloat16* resid, int grid,
+                        cudaStream_t st) {
     // Set on every launch: the attribute is per device context, contexts may be driven from
     // several host threads (MOE_FLAG_LOCAL_EP), and the call is a cheap host-side update.
     cudaError_t e = cudaFuncSetAttribute(expert_gemm_pair_kernel<MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kPairSmem);
     if (e != cudaSuccess) return e;
-    expert_gemm_pair_kernel<MODE><<<grid & ~1, kThreads, kPairSmem, st>>>(*tmA, *tmB, batch, N, K,
-                                                                          out, ldo, resid);
+    TokenMaps none{};
+    PairBMaps no_alt{};
+    GemmBatch b = batch;
+    if (!alt) b.alt_ok = 0;
+    expert_gemm_pair_kernel<MODE><<<grid & ~1, kThreads, kPairSmem, st>>>(
+        *tmA, *tmB, tmT ? *tmT : none, alt ? *alt : no_alt, b, N, K, out, ldo, resid);
     return cudaGetLastError();
 }
 
@@ -843,6 +1060,27 @@ cudaError_t launch_expert_gemm_swap(int mode, const CUtensorMap* tmW, const Toke
     return launch_swap<kGemmPlain>(tmW, tmX, batch, M, K, out, ldo, resid, grid, st);
 }
 
+double pair_makespan(const int64_t* rows, int n, int n_tiles, int npairs, bool tail_swap,
+                     float tail_cost) {
+    int64_t F = 0, R = 0;
+    for (int i = 0; i < n; ++i) {
+        const int r = (int)std::max<int64_t>(0, rows[i]);
+        const int nc = tail_cols(r, tail_swap);
+        F += (int64_t)(nc ? r / kPairRows : (r + kPairRows - 1) / kPairRows) * n_tiles;
+        if (nc) R += n_tiles;
+    }
+    double worst = 0.0;
+    for (int p = 0; p < npairs; ++p) {
+        TailSched ts;
+        ts.init((int)F, (int)R, npairs, p, tail_cost);
+        int tails = 0, tj;
+        while (ts.next(tj)) ++tails;
+        const double load = (double)(F / npairs + (p < F % npairs ? 1 : 0)) + tail_cost * tails;
+        worst = std::max(worst, load);
+    }
+    return worst;
+}
+
 int gemm_bn_for(int mode, int N) {
     if (mode == kGemmSwiGLU) return (N % 256 == 0) ? 256 : 0;
     if (N % 256 == 0) return 256;
@@ -853,14 +1091,16 @@ int gemm_bn_for(int mode, int N) {
 cudaError_t launch_expert_gemm(int mode, int bn, bool pair, const CUtensorMap* tmA,
                                const CUtensorMap* tmB, const GemmBatch& batch, int N, int K,
                                __nv_bfloat16* out, int ldo, const __nv_bfloat16* resid, int grid,
-                               cudaStream_t st) {
+                               cudaStream_t st, const TokenMaps* tmT, const PairBMaps* alt) {
     if ((mode == kGemmResidual) != (resid != nullptr) || batch.n < 1 || batch.n > kMaxBatch)
         return cudaErrorInvalidValue;
     if (pair) {
-        if (bn != 256) return cudaErrorInvalidValue;
-        if (mode == kGemmSwiGLU) return launch_pair<kGemmSwiGLU>(tmA, tmB, batch, N, K, out, ldo, resid, grid, st);
-        if (mode == kGemmResidual) return launch_pair<kGemmResidual>(tmA, tmB, batch, N, K, out, ldo, resid, grid, st);
-        return launch_pair<kGemmPlain>(tmA, tmB, batch, N, K, out, ldo, resid, grid, st);
+        if (bn != 256 || (batch.tail_swap && (!tmT || batch.part != 0 || !(batch.tail_cost > 0.f))))
+            return cudaErrorInvalidValue;
+        if (batch.select && batch.alt_ok && !alt) return cudaErrorInvalidValue;  // plans must agree
+        if (mode == kGemmSwiGLU) return launch_pair<kGemmSwiGLU>(tmA, tmB, tmT, alt, batch, N, K, out, ldo, resid, grid, st);
+        if (mode == kGemmResidual) return launch_pair<kGemmResidual>(tmA, tmB, tmT, alt, batch, N, K, out, ldo, resid, grid, st);
+        return launch_pair<kGemmPlain>(tmA, tmB, tmT, alt, batch, N, K, out, ldo, resid, grid, st);
     }
     if (mode == kGemmSwiGLU) {
         if (bn == 256) return launch_one<256, kGemmSwiGLU>(tmA, tmB, batch, N, K, out, ldo, resid, grid, st);

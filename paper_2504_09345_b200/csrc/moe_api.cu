@@ -95,6 +95,12 @@ namespace {
 
 using moe::set_err;
 
+// B maps of the CTA-pair kernel's 224- and 192-wide tiles (per-CTA boxes of 112 / 96 rows).
+bool make_alt_maps(moe::PairBMaps* a, const void* base, uint64_t rows, uint64_t cols) {
+    return moe::make_tmap(&a->b224, base, rows, cols, 112) &&
+           moe::make_tmap(&a->b192, base, rows, cols, 96);
+}
+
 moe_status check_cfg(const moe_config* cfg) {
     if (!cfg) return MOE_E_INVAL;
     if (cfg->hidden <= 0 || cfg->ffn <= 0 || cfg->num_experts <= 0 || cfg->top_k <= 0 ||
@@ -256,45 +262,67 @@ moe_status request_copy(moe_ctx c, const void* const* experts, int i, uint64_t q
 // shared-memory bandwidth bound, but half the M granularity and twice the concurrent tiles),
 // by a wave model: time ~ ceil(tiles / concurrent tiles) / tensor efficiency.
 // (rows: the expected rows of each of the launch's n groups; their tiles share the waves.)
+// swap-AB tail tiles in the pair kernel (not combined with the tail-split experiment)
+bool tail_swap_on(moe_ctx c) { return c->tail_swap && !c->tail_split; }
+
 bool pick_pair(moe_ctx c, const int64_t* rows, int n, int bn, int N) {
     if (bn != 256 || c->pair_mode == 0) return false;
-    if (c->pair_mode == 1) return true;
+    if (c->pair_mode != -1) return true;   // 1: always; 2: the device decides (GemmBatch::select)
     const int sms = c->num_sms;
     const int64_t nt = N / 256;
-    int64_t t1 = 0, t2 = 0;
-    for (int i = 0; i < n; ++i) {
-        if (rows[i] <= 0) continue;
-        t1 += ((rows[i] + 127) / 128) * nt;
-        t2 += ((rows[i] + 255) / 256) * nt;
-    }
+    int64_t t1 = 0;
+    for (int i = 0; i < n; ++i)
+        if (rows[i] > 0) t1 += ((rows[i] + 127) / 128) * nt;
     if (t1 == 0) return false;
     const double w1 = (double)((t1 + sms - 1) / sms) / 0.76;
-    const double w2 = (double)((t2 + sms / 2 - 1) / (sms / 2)) / 0.97;
+    const double w2 = moe::pair_makespan(rows, n, (int)nt, sms / 2, tail_swap_on(c), c->tail_cost) / 0.97;
     return w2 < w1;
 }
 
-// One expert-GEMM step over a batch of groups on `st`.  With the CTA-pair kernel and tail split
-// on, the pair kernel covers the whole 256-row tiles and the single-CTA kernel the < 256-row
-// remainders, concurrently on tail_stream (fork/join events: the tail needs the same inputs and
-// `st` continues only after both).
+// One expert-GEMM step over a batch of groups on `st`.
+//  * device selection (MOE_GEMM_PAIR=device) and the pair kernel possible: the CTA-pair kernel
+//    and the single-CTA kernel are both launched; each evaluates plan_tiles on the actual group
+//    sizes and the loser exits at once (GemmBatch::select) -- the tile shape follows the real
+//    routing without a host sync (but the extra launch costs ~10 us; off by default).
+//  * tail split (experiment): the pair kernel covers the whole 256-row tiles and the single-CTA
+//    kernel the < 256-row remainders, concurrently on tail_stream (fork/join events).
+//  * otherwise one launch of the kernel `pair` names (swap-AB tail tiles if tail_swap is on).
 moe_status launch_grouped(moe_ctx c, int mode, int bn, bool pair, const CUtensorMap* tmA,
                           const CUtensorMap* tmB, const CUtensorMap* tmB_pair,
+                          const moe::PairBMaps* alt, const moe::TokenMaps* tmT,
                           moe::GemmBatch batch, int N, int K, __nv_bfloat16* out, int ldo,
-                          cudaStream_t st) {
+                          cudaStream_t st, const __nv_bfloat16* resid = nullptr) {
     const int grid = c->num_sms;
+    if (!c->alt_tiles) alt = nullptr;
+    batch.bn_single = bn;
+    batch.alt_ok = alt ? 1 : 0;
+    if (pair && c->pair_mode == 2 && !c->tail_split) {
+        batch.select = grid;
+        batch.tail_swap = tail_swap_on(c) ? 1 : 0;
+        batch.tail_cost = c->tail_cost;
+        MOE_CUDA(c, moe::launch_expert_gemm(mode, bn, true, tmA, tmB_pair, batch, N, K, out, ldo,
+                                            resid, grid, st, tmT, alt));
+        batch.tail_swap = 0;
+        MOE_CUDA(c, moe::launch_expert_gemm(mode, bn, false, tmA, tmB, batch, N, K, out, ldo,
+                                            resid, grid, st));
+        c->stats.kernel_launches += 1;
+        return MOE_OK;
+    }
     if (!pair || !c->tail_split) {
+        batch.tail_swap = pair && tail_swap_on(c) ? 1 : 0;
+        batch.tail_cost = c->tail_cost;
         MOE_CUDA(c, moe::launch_expert_gemm(mode, bn, pair, tmA, pair ? tmB_pair : tmB, batch, N,
-                                            K, out, ldo, nullptr, grid, st));
+                                            K, out, ldo, resid, grid, st, tmT, alt));
         return MOE_OK;
     }
     MOE_CUDA(c, cudaEventRecord(c->fork_ev, st));
     batch.part = 1;
     MOE_CUDA(c, moe::launch_expert_gemm(mode, bn, true, tmA, tmB_pair, batch, N, K, out, ldo,
-                                        nullptr, grid, st));
+                                        resid, grid, st, nullptr, alt));
     batch.part = 2;
     MOE_CUDA(c, cudaStreamWaitEvent(c->tail_stream, c->fork_ev, 0));
     MOE_CUDA(c, moe::launch_expert_gemm(mode, bn, false, tmA, tmB, batch, N, K, out, ldo,
-                                        nullptr, grid, c->tail_stream));
+                                        resid, grid, c->tail_stream));
     MOE_CUDA(c, cudaEventRecord(c->join_ev, c->tail_stream));
     MOE_CUDA(c, cudaStreamWaitEvent(st, c->join_ev, 0));
     c->stats.kernel_launches += 1;
@@ -365,6 +393,10 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         if (use_swap(2 * hi) || use_swap(h)) nb = 1;   // the swap kernel takes one group
         moe::GemmBatch b1{}, b2{};
         b1.table = g1;
+        if (c->clk_acc) {
+            b1.clk = c->clk_acc;
+            b2.clk = c->clk_acc + 2;
+        }
         b2.table = g2;
         b1.n = b2.n = nb;
         int64_t rows[moe::kMaxBatch];
@@ -386,7 +418,9 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
                 const bool pr = pick_pair(c, rows, nb, c->bn1, 2 * hi);
                 moe_status gs = launch_grouped(c, moe::kGemmSwiGLU, c->bn1, pr,
                                                shared ? &tm_x : tmA_routed, &c->tm_w13,
-                                               &c->tm_w13_pair, b1, 2 * hi, h, c->h_act, hi, st);
+                                               &c->tm_w13_pair, &c->tm_w13_alt,
+                                               shared ? &tm_x_t : tmT_routed,
+                                               b1, 2 * hi, h, c->h_act, hi, st);
                 if (gs != MOE_OK) return gs;
             }
             p.end();
@@ -403,7 +437,8 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
             } else {
                 const bool pr = pick_pair(c, rows, nb, c->bn2, h);
                 moe_status gs = launch_grouped(c, moe::kGemmPlain, c->bn2, pr, &c->tm_h,
-                                               &c->tm_w2, &c->tm_w2_pair, b2, h, hi,
+                                               &c->tm_w2, &c->tm_w2_pair, &c->tm_w2_alt,
+                                               &c->tm_h_t, b2, h, hi,
                                                shared ? c->y_perm : y_routed, h, st);
                 if (gs != MOE_OK) return gs;
             }
@@ -589,6 +624,7 @@ moe_status taskb_resources(moe_ctx c) {
     for (int i = 0; i < 2; ++i) {  // Wo [h, h]: N = h output rows, K = h
         tm &= moe::make_tmap(&c->tm_wo[i], c->lw_slot[i], (uint64_t)h, (uint64_t)h, (uint32_t)c->bn2);
         tm &= moe::make_tmap(&c->tm_wo_pair[i], c->lw_slot[i], (uint64_t)h, (uint64_t)h, 128);
+        tm &= make_alt_maps(&c->tm_wo_alt[i], c->lw_slot[i], (uint64_t)h, (uint64_t)h);
     }
     if (!tm) return set_err(c, MOE_E_CUDA, "cuTensorMapEncodeTiled failed for Wo");
     return MOE_OK;
@@ -632,19 +668,20 @@ moe_status taskb_impl(moe_ctx c, const __nv_bfloat16* attn, const __nv_bfloat16*
         moe::GemmBatch ob{};
         ob.table = c->oproj_grp;
         ob.n = 1;   // idx[0] = 0, b_row[0] = 0: Wo is the whole map
+        moe::TokenMaps tm_attn_t;
+        if (!moe::make_token_maps(&tm_attn_t, attn, (uint64_t)T, (uint64_t)h))
+            return set_err(c, MOE_E_CUDA, "cuTensorMapEncodeTiled failed for attn");
         if (c->swap_mode == 1 && h % 256 == 0) {
-            moe::TokenMaps tm_attn_t;
-            if (!moe::make_token_maps(&tm_attn_t, attn, (uint64_t)T, (uint64_t)h))
-                return set_err(c, MOE_E_CUDA, "cuTensorMapEncodeTiled failed for attn");
             MOE_CUDA(c, moe::launch_expert_gemm_swap(moe::kGemmResidual, &c->tm_wo_pair[b],
                                                      &tm_attn_t, ob, h, h, c->h1_ws, h,
                                                      resid, c->num_sms, st));
         } else {
             const int64_t rows = T;
             const bool pr = pick_pair(c, &rows, 1, c->bn2, h);
-            MOE_CUDA(c, moe::launch_expert_gemm(moe::kGemmResidual, c->bn2, pr, &tm_attn,
-                                                pr ? &c->tm_wo_pair[b] : &c->tm_wo[b], ob, h, h,
-                                                c->h1_ws, h, resid, c->num_sms, st));
+            moe_status gs = launch_grouped(c, moe::kGemmResidual, c->bn2, pr, &tm_attn,
+                                           &c->tm_wo[b], &c->tm_wo_pair[b], &c->tm_wo_alt[b],
+                                           &tm_attn_t, ob, h, h, c->h1_ws, h, st, resid);
+            if (gs != MOE_OK) return gs;
         }
         p.end();
     }
@@ -767,8 +804,11 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
             ok &= cudaStreamCreateWithPriority(&c->token_stream, cudaStreamNonBlocking, greatest) ==
                   cudaSuccess;
         }
-        if (cfg->flags & MOE_FLAG_PROFILE)
+        if (cfg->flags & MOE_FLAG_PROFILE) {
             ok &= cudaStreamCreateWithFlags(&c->clock_stream, cudaStreamNonBlocking) == cudaSuccess;
+            ok &= cudaMalloc((void**)&c->clk_acc, 4 * sizeof(unsigned long long)) == cudaSuccess &&
+                  cudaMemset(c->clk_acc, 0, 4 * sizeof(unsigned long long)) == cudaSuccess;
+        }
         ok &= cudaEventCreateWithFlags(&c->done_ev, cudaEventDisableTiming) == cudaSuccess;
         if (const char* e = getenv("MOE_GEMM_TAILSPLIT")) c->tail_split = atoi(e) != 0;
         if (c->tail_split) {
@@ -814,14 +854,23 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
         const uint64_t r13 = 3ull * hi * c->nslots, r2 = 3ull * h * c->nslots;
         tm &= moe::make_tmap(&c->tm_w13, c->slot_base, r13, h, (uint32_t)c->bn1);
         tm &= moe::make_tmap(&c->tm_w13_pair, c->slot_base, r13, h, 128);
+        tm &= make_alt_maps(&c->tm_w13_alt, c->slot_base, r13, h);
         tm &= moe::make_tmap(&c->tm_w2, c->slot_base, r2, hi, (uint32_t)c->bn2);
         tm &= moe::make_tmap(&c->tm_w2_pair, c->slot_base, r2, hi, 128);
+        tm &= make_alt_maps(&c->tm_w2_alt, c->slot_base, r2, hi);
     }
     if (!tm) return fail(MOE_E_CUDA);
     if (const char* e = getenv("MOE_GEMM_SWAP")) c->swap_mode = atoi(e) != 0;
+    if (const char* e = getenv("MOE_GEMM_TAILSWAP")) c->tail_swap = atoi(e) != 0;
+    if (const char* e = getenv("MOE_GEMM_ALT")) c->alt_tiles = atoi(e) != 0;
+    if (const char* e = getenv("MOE_GEMM_TAILCOST")) {
+        const float v = (float)atof(e);
+        if (v > 0.f && v <= 4.f) c->tail_cost = v;
+    }
     if (const char* e = getenv("MOE_GEMM_PAIR")) {
         if (!strcmp(e, "0")) c->pair_mode = 0;
         else if (!strcmp(e, "1")) c->pair_mode = 1;
+        else if (!strcmp(e, "2") || !strcmp(e, "device")) c->pair_mode = 2;
         else if (!strcmp(e, "auto")) c->pair_mode = -1;
     }
     {
@@ -1026,6 +1075,14 @@ moe_status moe_get_stats(moe_ctx ctx, moe_stats* out) {
         MOE_CUDA(ctx, cudaStreamSynchronize(ctx->copy_stream));
         ctx->stats.comm_bytes = b;
     }
+    if (ctx->clk_acc) {   // SM clock during the expert GEMMs (in-kernel clock64 / globaltimer)
+        unsigned long long v[4] = {};
+        MOE_CUDA(ctx, cudaMemcpyAsync(v, ctx->clk_acc, sizeof v, cudaMemcpyDeviceToHost,
+                                      ctx->copy_stream));
+        MOE_CUDA(ctx, cudaStreamSynchronize(ctx->copy_stream));
+        ctx->stats.gemm1_sm_mhz = v[1] ? 1e3 * (double)v[0] / (double)v[1] : 0.0;
+        ctx->stats.gemm2_sm_mhz = v[3] ? 1e3 * (double)v[2] / (double)v[3] : 0.0;
+    }
     *out = ctx->stats;
     return MOE_OK;
 }
@@ -1035,6 +1092,11 @@ moe_status moe_reset_stats(moe_ctx ctx) {
     moe_stats tmp;
     moe_status s = moe_get_stats(ctx, &tmp);
     ctx->stats = moe_stats{};
+    if (ctx->clk_acc && s == MOE_OK) {
+        MOE_CUDA(ctx, cudaMemsetAsync(ctx->clk_acc, 0, 4 * sizeof(unsigned long long),
+                                      ctx->copy_stream));
+        MOE_CUDA(ctx, cudaStreamSynchronize(ctx->copy_stream));
+    }
     return s;
 }
 
@@ -1089,7 +1151,7 @@ moe_status moe_destroy(moe_ctx c) {
     }
     void* bufs[] = {c->idx_ws, c->gates_ws, c->tile_counts, c->tile_prefix, c->offsets, c->counts,
                     c->grp1, c->grp2, c->shared_grp, c->pos, c->x_perm, c->h_act, c->y_perm,
-                    c->h1_ws, c->u_ws, c->oproj_grp};
+                    c->h1_ws, c->u_ws, c->oproj_grp, c->clk_acc};
     for (void* p : bufs) cudaFree(p);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->token_stream) cudaStreamDestroy(c->token_stream);

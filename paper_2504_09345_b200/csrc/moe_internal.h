@@ -32,6 +32,11 @@ struct GemmGroup {
 // part: 0 = every row of each group; 1 = the head (the largest multiple of 256 rows -- whole
 // CTA-pair tiles); 2 = the tail (the remaining < 256 rows), so a pair-kernel launch on the head
 // and a concurrent 128-row-tile launch on the tail split a group without padding it to 256.
+// tail_swap (CTA-pair kernel only): a group's last partial tile of <= 128 rows runs swap-AB
+// inside the same launch -- weights as the 256-row M side, the r tail tokens as an N =
+// ceil(r/32)*32 side -- instead of a 256-row tile that is mostly padding; those tail tiles are
+// scheduled after the full tiles onto the least-loaded CTA pairs, at an estimated `tail_cost`
+// (time of a tail tile / time of a full 256x256 tile).
 constexpr int kMaxBatch = 16;
 constexpr int kPairRows = 256;
 struct GemmBatch {
@@ -40,6 +45,23 @@ struct GemmBatch {
     int32_t b_row[kMaxBatch];
     int32_t n;
     int32_t part;
+    int32_t tail_swap;
+    float tail_cost;
+    // select > 0: the host launched BOTH the CTA-pair and the single-CTA kernel for this batch,
+    // sized for `select` SMs; each evaluates the same wave model (plan_tiles, gemm.cu) on the
+    // ACTUAL group sizes (device memory, no host sync) and the one not chosen exits at once.
+    // bn_single: the single-CTA kernel's tile width; alt_ok: the pair launch has PairBMaps.
+    int32_t select;
+    int32_t bn_single;
+    int32_t alt_ok;
+    // clk: if non-null, CTA 0 adds its SM cycles (clock64) and elapsed ns (globaltimer) from
+    // kernel entry to exit to clk[0] / clk[1] (the SM clock under power management).
+    unsigned long long* clk;
+};
+// Extra B maps of the CTA-pair kernel: per-CTA boxes of 112 and 96 rows for 224- and 192-wide
+// tiles (chosen on the device when N divides and fewer waves result, e.g. 28672 = 128 x 224).
+struct PairBMaps {
+    CUtensorMap b224, b192;
 };
 
 // ------------------------------------------------------------ expert parallelism, P2P transport
@@ -142,15 +164,23 @@ enum GemmMode { kGemmSwiGLU = 0, kGemmPlain = 1, kGemmResidual = 2 };
 //   batch: the launch's expert groups (GemmBatch below): ONE persistent launch covers up to
 //   kMaxBatch experts -- their tiles are scheduled together, so small experts no longer pay a
 //   partial last wave each.
-cudaError_t launch_expert_gemm(int mode, int bn, bool pair, const CUtensorMap* tmA,
-                               const CUtensorMap* tmB, const GemmBatch& batch, int N, int K,
-                               __nv_bfloat16* out, int ldo, const __nv_bfloat16* resid, int grid,
-                               cudaStream_t st);
 // Token operand of the swap-AB kernel: the same [rows, K] bf16 tensor with 64-column boxes of
 // 128, 64, 32 and 16 rows, so a CTA's N/2 token rows (a multiple of 16) load in <= 4 TMA ops.
 struct TokenMaps {
     CUtensorMap box[4];
 };
+//   tmT: tmA's tensor as TokenMaps -- the token operand of swap-AB tail tiles (pair kernel with
+//   batch.tail_swap; may be nullptr otherwise).
+cudaError_t launch_expert_gemm(int mode, int bn, bool pair, const CUtensorMap* tmA,
+                               const CUtensorMap* tmB, const GemmBatch& batch, int N, int K,
+                               __nv_bfloat16* out, int ldo, const __nv_bfloat16* resid, int grid,
+                               cudaStream_t st, const TokenMaps* tmT = nullptr,
+                               const PairBMaps* alt = nullptr);
+// Host model of the pair kernel's schedule (the same rule the kernel applies): the makespan in
+// units of one full 256x256 tile time of a launch whose groups have rows[i] rows, N/256 weight
+// tiles, on npairs CTA pairs.
+double pair_makespan(const int64_t* rows, int n, int n_tiles, int npairs, bool tail_swap,
+                     float tail_cost);
 bool make_token_maps(TokenMaps* t, const void* base, uint64_t rows, uint64_t cols);  // moe_api.cu
 // Swap-AB CTA-pair kernel (gemm.cu): weights are the 256-row M side (tmW: box 64 x 128, M rows
 // = 2 h_i for SwiGLU, h otherwise, M % 256 == 0), the group's tokens the N side, N = 32..256

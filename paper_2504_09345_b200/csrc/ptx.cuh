@@ -252,5 +252,11 @@ __device__ __forceinline__ int4 ld_nc_v4(const void* p) {
     return r;
 }
 
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 }  // namespace ptx
 }  // namespace moe

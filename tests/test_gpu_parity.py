@@ -276,21 +276,50 @@ def test_ep_path_one_rank_nccl_matches_oracle_and_single_gpu(shape):
 
 
 # ------------------------------------------------------------- CTA-pair (cta_group::2) GEMM
-@pytest.mark.parametrize("mode", ["1", "0", "split"])
+@pytest.mark.parametrize("mode", ["1", "1-tailswap", "1-alt", "device", "0", "split"])
 @pytest.mark.parametrize("shape", [
     dict(hidden=256, ffn=384, num_experts=8, top_k=2, tokens=1500),
     dict(hidden=512, ffn=640, num_experts=4, top_k=2, tokens=2100, num_shared=1),
     dict(hidden=256, ffn=256, num_experts=64, top_k=6, tokens=333),     # many tiny groups
+    dict(hidden=768, ffn=1792, num_experts=8, top_k=2, tokens=1700),    # 224 / 192-wide tiles
 ])
 def test_gemm_tile_variants(shape, mode, monkeypatch):
     """MOE_GEMM_PAIR=1 forces the 256x256 CTA-pair kernel (tcgen05.mma.cta_group::2, 2-CTA TMA)
-    for every bn=256 GEMM; 0 forces the 128-row kernel; split = pair kernel on whole 256-row
-    tiles + a concurrent 128-row launch on the remainders (MOE_GEMM_TAILSPLIT).  All must match
-    the oracle."""
-    monkeypatch.setenv("MOE_GEMM_PAIR", "1" if mode == "split" else mode)
+    for every bn=256 GEMM: with padded 256-row group tails (1), with tails of <= 128 rows as
+    swap-AB tail tiles (1-tailswap, MOE_GEMM_TAILSWAP=1), or with 224 / 192-wide tiles where
+    they divide N (1-alt, MOE_GEMM_ALT=1); device = both kernels launched, the device picks on the
+    actual group sizes and the other exits; 0 forces the 128-row kernel; split = pair kernel on
+    whole 256-row tiles + a concurrent 128-row launch on the remainders (MOE_GEMM_TAILSPLIT).
+    All must match the oracle."""
+    monkeypatch.setenv("MOE_GEMM_PAIR", {"0": "0", "device": "device"}.get(mode, "1"))
     if mode == "split":
         monkeypatch.setenv("MOE_GEMM_TAILSPLIT", "1")
+    if mode == "1-tailswap":
+        monkeypatch.setenv("MOE_GEMM_TAILSWAP", "1")
+    if mode in ("1-alt", "device"):
+        monkeypatch.setenv("MOE_GEMM_ALT", "1")
     cfg = synth.MoEConfig("custom", 14, shape["hidden"], shape["ffn"], shape["num_experts"],
+                          shape["top_k"], shape["tokens"], shape.get("num_shared", 0))
+    inp = synth.gen_inputs(cfg)
+    run, out, *_ = _check_full(inp)
+    run.close()
+
+
+@pytest.mark.parametrize("cost", ["0.05", "0.6", "3.0"])
+@pytest.mark.parametrize("shape", [
+    dict(hidden=256, ffn=512, num_experts=8, top_k=2, tokens=1100),     # tails 1..128 rows
+    dict(hidden=512, ffn=384, num_experts=16, top_k=4, tokens=700, num_shared=2),
+    dict(hidden=256, ffn=768, num_experts=2, top_k=1, tokens=40),       # tail-only groups
+    dict(hidden=768, ffn=1280, num_experts=8, top_k=2, tokens=9000),    # many tiles per pair
+])
+def test_gemm_pair_tail_swap_schedules(shape, cost, monkeypatch):
+    """Pair kernel with swap-AB tail tiles (MOE_GEMM_TAILSWAP=1, opt-in) under tail costs that drive the static schedule
+    (TailSched, gemm.cu) through light-only, mixed and heavy-first rounds: every tile must be
+    computed exactly once whatever the assignment."""
+    monkeypatch.setenv("MOE_GEMM_PAIR", "1")
+    monkeypatch.setenv("MOE_GEMM_TAILSWAP", "1")
+    monkeypatch.setenv("MOE_GEMM_TAILCOST", cost)
+    cfg = synth.MoEConfig("custom", 16, shape["hidden"], shape["ffn"], shape["num_experts"],
                           shape["top_k"], shape["tokens"], shape.get("num_shared", 0))
     inp = synth.gen_inputs(cfg)
     run, out, *_ = _check_full(inp)

@@ -119,6 +119,29 @@ def test_taskb_staged_parity(shape, force_ep, swap, monkeypatch):
         r.close()
 
 
+@pytest.mark.parametrize("shape", [
+    dict(hidden=256, ffn=384, ne=8, k=2, T=300),
+    dict(hidden=768, ffn=1792, ne=8, k=2, T=1100, S=1),
+])
+@pytest.mark.parametrize("variant", ["tailswap", "alt", "device"])
+def test_taskb_gemm_variants(shape, variant, monkeypatch):
+    """The residual-epilogue O-projection (and the expert GEMMs) through the opt-in GEMM paths:
+    swap-AB tail tiles, 224 / 192-wide pair tiles, device-side kernel selection."""
+    monkeypatch.setenv("MOE_GEMM_PAIR", "device" if variant == "device" else "1")
+    if variant == "tailswap":
+        monkeypatch.setenv("MOE_GEMM_TAILSWAP", "1")
+    else:
+        monkeypatch.setenv("MOE_GEMM_ALT", "1")
+    inp, tb = _inputs(shape["hidden"], shape["ffn"], shape["ne"], shape["k"], shape["T"],
+                      shape.get("S", 0))
+    r = TaskBRun(inp, tb)
+    try:
+        out, idx, gates, h1, u = r.forward()
+        _check_staged(inp, tb, out, idx, gates, h1, u)
+    finally:
+        r.close()
+
+
 def test_taskb_end_to_end_vs_pure_oracle():
     """From (attn, resid) alone: the whole oracle Task B vs the CUDA path."""
     inp, tb = _inputs(512, 640, 16, 4, 700, S=1)
