@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--layers", type=int, default=2)
     ap.add_argument("--packet-mb", type=float, default=0.0)
+    ap.add_argument("--mover", action="store_true",
+                    help="expert copies through the library's data-mover thread (MOE_FLAG_MOVER)")
     ap.add_argument("--slots", type=int, default=0, help="expert staging slots (0 = auto)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -289,7 +291,7 @@ def run_ours(args):
         try:
             layer = moe.MoELayer(cfg.hidden, cfg.ffn, cfg.num_experts, cfg.top_k, Tr,
                                  num_shared=cfg.num_shared, device=local, profile=True,
-                                 packet_bytes=int(args.packet_mb * 2 ** 20), world_size=world,
+                                 packet_bytes=int(args.packet_mb * 2 ** 20), mover=args.mover, world_size=world,
                                  rank=rank, num_slots=args.slots, ipc_ep=True)
             handles = [None] * world
             dist.all_gather_object(handles, layer.ipc_handle())
@@ -311,7 +313,7 @@ def run_ours(args):
     if layer is None:
         layer = moe.MoELayer(cfg.hidden, cfg.ffn, cfg.num_experts, cfg.top_k, Tr,
                              num_shared=cfg.num_shared, device=local, profile=True,
-                             packet_bytes=int(args.packet_mb * 2 ** 20), world_size=world,
+                             packet_bytes=int(args.packet_mb * 2 ** 20), mover=args.mover, world_size=world,
                              rank=rank, nccl_unique_id=uid, num_slots=args.slots)
     stream = torch.cuda.Stream()
     sh = stream.cuda_stream
@@ -496,7 +498,7 @@ def run_ours(args):
                        "experts_per_rank": nl, "top_k": cfg.top_k, "num_shared": cfg.num_shared,
                        "layers_cycled": args.layers, "staging_slots": st["num_slots"],
                        "experts_streamed_per_call": nl + cfg.num_shared,
-                       "packet_mb": args.packet_mb,
+                       "packet_mb": args.packet_mb, "mover": bool(args.mover),
                        "l2": "inputs larger than L2: all expert weights re-streamed from host each step",
                        "parallelism": f"ep{world}", "ep_transport": transport},
             "roofline": roofline, "roofline_step": roofline_step,

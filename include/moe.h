@@ -66,6 +66,14 @@ typedef enum {
                                 buffers are shared with CUDA IPC -- call moe_ep_ipc_handle on
                                 every rank, all-gather the handles, then moe_ep_ipc_connect
                                 before the first forward call.  Takes precedence over NCCL.      */
+#define MOE_FLAG_MOVER 16u   /* the Contiguous Data Mover: expert copies are cut
+                                into packets of packet_bytes (0 = 100 MB) and issued by a
+                                library thread with at most one packet in flight (
+                                MOE_MOVER_INFLIGHT=n for n), so a caller's token copy
+                                (moe_layer_forward_host) waits behind one packet, not behind
+                                every expert copy already requested.  The copies and the GEMMs
+                                are ordered by device counters (stream memory operations);
+                                MOE_E_UNSUPPORTED if the driver lacks them.                      */
 
 /*
  * Layer configuration.  Envelope of the sm_100a kernels (MOE_E_UNSUPPORTED otherwise):

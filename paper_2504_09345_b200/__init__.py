@@ -38,6 +38,7 @@ EXPORTED = ["moe_packed_expert_bytes", "moe_pack_expert", "moe_host_alloc", "moe
             "moe_taskb_forward_host", "moe_ep_ipc_handle", "moe_ep_ipc_connect",
             "moe_ep_ipc_selftest"]
 MOE_FLAG_IPC_EP = 8
+MOE_FLAG_MOVER = 16
 MOE_IPC_HANDLE_BYTES = 256
 
 
@@ -357,13 +358,15 @@ class MoELayer:
                  world_size: int = 1, rank: int = 0, packet_bytes: int = 0,
                  profile: bool = False, nccl_unique_id: Optional[bytes] = None,
                  force_ep: bool = False, num_slots: int = 0, local_ep: bool = False,
-                 ipc_ep: bool = False):
+                 ipc_ep: bool = False, mover: bool = False):
         """local_ep: in-process expert parallelism over peer memory (MOE_FLAG_LOCAL_EP);
         nccl_unique_id is then the 128-byte group key shared by the `world_size` contexts (one
         host thread each).  ipc_ep: the same transport across processes (MOE_FLAG_IPC_EP): call
-        ipc_connect(all ranks' ipc_handle()) before the first forward."""
+        ipc_connect(all ranks' ipc_handle()) before the first forward.  mover: expert copies in
+        packets through the library's data-mover thread (MOE_FLAG_MOVER)."""
         flags = ((MOE_FLAG_PROFILE if profile else 0) | (MOE_FLAG_FORCE_EP if force_ep else 0) |
-                 (MOE_FLAG_LOCAL_EP if local_ep else 0) | (MOE_FLAG_IPC_EP if ipc_ep else 0))
+                 (MOE_FLAG_LOCAL_EP if local_ep else 0) | (MOE_FLAG_IPC_EP if ipc_ep else 0) |
+                 (MOE_FLAG_MOVER if mover else 0))
         self.cfg = moe_config(hidden, ffn, num_experts, top_k, num_shared, max_tokens,
                               int(renormalize), device, world_size, rank, None, packet_bytes,
                               flags, num_slots)

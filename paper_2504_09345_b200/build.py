@@ -18,7 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "libmoe_b200.so")
-SOURCES = ["moe_api.cu", "ep.cu", "ep_p2p.cu", "route.cu", "gemm.cu", "taskb.cu"]
+SOURCES = ["moe_api.cu", "ep.cu", "ep_p2p.cu", "route.cu", "gemm.cu", "taskb.cu", "mover.cu"]
 HEADERS = ["ptx.cuh", "moe_internal.h", "engine.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

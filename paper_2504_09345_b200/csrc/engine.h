@@ -47,6 +47,10 @@ const NcclApi* nccl_api();  // nullptr if libnccl cannot be found
 
 }  // namespace moe
 
+namespace moe {
+struct Mover;   // mover.cu: the Contiguous Data Mover thread (MOE_FLAG_MOVER)
+}
+
 struct moe_ctx_s {
     moe_config cfg{};
     int n_local = 0;       // routed experts owned by this rank
@@ -82,6 +86,9 @@ struct moe_ctx_s {
     cudaEvent_t ready13[moe::kMaxSlots] = {}, ready2[moe::kMaxSlots] = {};
     cudaEvent_t slot_free[moe::kMaxSlots] = {};
     uint64_t seq = 0;  // streamed-item counter across calls: item q uses slot q % nslots
+    // MOE_FLAG_MOVER: expert copies go through the mover thread (mover.cu) in packets, ordered
+    // against the GEMMs by device counters instead of the ready13 / ready2 / slot_free events.
+    moe::Mover* mover = nullptr;
     // The staging buffer seen as one W13 matrix [nslots * 3 h_i, h] and one W2 matrix
     // [nslots * 3 h, h_i]: slot s's W13 starts at row 3 h_i s, its W2 at row 3 h s + 2 h, so one
     // GEMM launch can cover experts in different slots (GemmBatch::b_row).
@@ -248,6 +255,15 @@ struct Prof {
         }
     }
 };
+
+// Contiguous Data Mover (mover.cu, MOE_FLAG_MOVER)
+moe_status mover_start(moe_ctx c);
+void mover_stop(moe_ctx c);                      // drains, joins, frees
+moe_status mover_drain(moe_ctx c);               // every queued packet issued; mover errors
+moe_status mover_push(moe_ctx c, uint64_t q0, int n, const char* src, char* dst);
+moe_status mover_wait(moe_ctx c, cudaStream_t st, int which, uint64_t value);  // 0 r13, 1 r2
+moe_status mover_mark_free(moe_ctx c, cudaStream_t st, uint64_t value);
+double mover_take_h2d_ms(moe_ctx c, int64_t* packets);
 
 // expert parallelism (ep.cu)
 moe_status ep_init(moe_ctx c);

@@ -183,6 +183,15 @@ moe_status flush_copies(moe_ctx c) {
     if (c->pend_n == 0) return MOE_OK;
     const int n = c->pend_n;
     const int s0 = (int)(c->pend_q0 % (uint64_t)c->nslots);
+    if (c->mover) {   // the mover thread packetises and orders it by device counters
+        for (int j = 0; j < n; ++j) {
+            c->batch_q0[s0 + j] = c->pend_q0;
+            c->batch_n[s0 + j] = n;
+        }
+        c->stats.h2d_weight_bytes += (int64_t)n * c->blob_bytes;
+        c->pend_n = 0;
+        return moe::mover_push(c, c->pend_q0, n, c->pend_src, static_cast<char*>(c->slot[s0]));
+    }
     for (int j = 0; j < n; ++j)  // each slot must have been released by its previous item's GEMMs
         MOE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->slot_free[s0 + j], 0));
     const char* src = c->pend_src;
@@ -341,6 +350,10 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     float* gates = topk_w ? topk_w : c->gates_ws;
     const uint64_t q0 = c->seq;
 
+    // With the mover, the slot counters assume one compute order: a call on another stream
+    // than the previous one first waits for it (a no-op on the same stream).
+    if (c->mover) MOE_CUDA(c, cudaStreamWaitEvent(st, c->done_ev, 0));
+
     // A operand of the shared experts is the hidden batch itself (per-call tensor map).
     // (T == 0 only happens under EP: the rank serves other ranks' tokens; its shared-expert
     // groups are then empty and never touch the map.)
@@ -400,9 +413,16 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         b2.table = g2;
         b1.n = b2.n = nb;
         int64_t rows[moe::kMaxBatch];
+        if (c->mover) {
+            if (getenv("MOE_MOVER_TRACE"))
+                fprintf(stderr, "[api] GEMMs of items [%llu, %llu): wait r13 >= %llu\n",
+                        (unsigned long long)q, (unsigned long long)(q + nb), (unsigned long long)(q + nb));
+            moe_status ws = moe::mover_wait(c, st, 0, q + nb);
+            if (ws != MOE_OK) return ws;
+        }
         for (int j = 0; j < nb; ++j) {
             const int sj = (int)((q + j) % (uint64_t)ns), e = expert_of(i + j);
-            MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready13[sj], 0));
+            if (!c->mover) MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready13[sj], 0));
             b1.idx[j] = b2.idx[j] = e;
             b1.b_row[j] = 3 * hi * sj;           // W13 of slot sj in tm_w13*
             b2.b_row[j] = 3 * h * sj + 2 * h;    // W2 of slot sj in tm_w2*
@@ -425,8 +445,13 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
             }
             p.end();
         }
-        for (int j = 0; j < nb; ++j)
-            MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready2[(q + j) % (uint64_t)ns], 0));
+        if (c->mover) {
+            moe_status ws = moe::mover_wait(c, st, 1, q + nb);
+            if (ws != MOE_OK) return ws;
+        } else {
+            for (int j = 0; j < nb; ++j)
+                MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready2[(q + j) % (uint64_t)ns], 0));
+        }
         {
             Prof p(c, moe::kRecGemm2, st);
             if (use_swap(h)) {
@@ -447,8 +472,13 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         c->stats.kernel_launches += 2;
         c->stats.gemm1_launches += 1;
         c->stats.gemm2_launches += 1;
-        for (int j = 0; j < nb; ++j)
-            MOE_CUDA(c, cudaEventRecord(c->slot_free[(q + j) % (uint64_t)ns], st));
+        if (c->mover) {
+            moe_status ms = moe::mover_mark_free(c, st, q + nb);
+            if (ms != MOE_OK) return ms;
+        } else {
+            for (int j = 0; j < nb; ++j)
+                MOE_CUDA(c, cudaEventRecord(c->slot_free[(q + j) % (uint64_t)ns], st));
+        }
         for (int j = 0; j < nb; ++j) {   // the freed slots take the items ns ahead
             if (i + j + ns < c->n_all) {
                 moe_status s2 = request_copy(c, experts, expert_of(i + j + ns), q + j + ns);
@@ -884,6 +914,10 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
         moe_status es = moe::ep_init(c);
         if (es != MOE_OK) return fail(es);
     }
+    if (cfg->flags & MOE_FLAG_MOVER) {
+        moe_status ms = moe::mover_start(c);
+        if (ms != MOE_OK) return fail(ms);
+    }
     if (cudaDeviceSynchronize() != cudaSuccess) return fail(MOE_E_CUDA);
     *out = c;
     return MOE_OK;
@@ -1036,6 +1070,10 @@ moe_status moe_sync(moe_ctx ctx) {
                        ctx->p2p_diag_h[2], ctx->p2p_diag_h[3], ctx->p2p_diag_h[4]);
     }
     MOE_CUDA(ctx, cudaSetDevice(ctx->cfg.device));
+    if (ctx->mover) {   // every packet issued before the streams are waited on
+        moe_status ms = moe::mover_drain(ctx);
+        if (ms != MOE_OK) return ms;
+    }
     MOE_CUDA(ctx, cudaEventSynchronize(ctx->done_ev));     // the last call (see engine.h)
     MOE_CUDA(ctx, cudaStreamSynchronize(ctx->copy_stream));
     if (ctx->token_stream) MOE_CUDA(ctx, cudaStreamSynchronize(ctx->token_stream));
@@ -1066,6 +1104,7 @@ moe_status moe_get_stats(moe_ctx ctx, moe_stats* out) {
         ctx->ev_pool.push_back(r.b);
     }
     ctx->pending.clear();
+    if (ctx->mover) ctx->stats.h2d_ms += moe::mover_take_h2d_ms(ctx, nullptr);
     ctx->stats.num_slots = ctx->nslots;
     ctx->stats.comm_bytes = ctx->comm_bytes;
     if (ctx->p2p && ctx->p2p_bytes) {   // P2P transport: counted on the device by the plan kernel
@@ -1128,6 +1167,7 @@ moe_status moe_debug_buffers(moe_ctx ctx, moe_debug_view* out) {
 moe_status moe_destroy(moe_ctx c) {
     if (!c) return MOE_OK;
     cudaSetDevice(c->cfg.device);
+    moe::mover_stop(c);
     cudaDeviceSynchronize();
     moe::ep_destroy(c);
     for (const moe::Rec& r : c->pending) {

@@ -22,13 +22,13 @@ class GpuRun:
     """One context + pinned experts for a set of inputs."""
 
     def __init__(self, inp: synth.MoEInputs, max_tokens=None, profile=False, packet_bytes=0,
-                 renormalize=True, force_ep=False):
+                 renormalize=True, force_ep=False, mover=False, num_slots=0):
         cfg = inp.cfg
         self.inp = inp
         self.layer = MoELayer(cfg.hidden, cfg.ffn, cfg.num_experts, cfg.top_k,
                               max_tokens or max(1, inp.x.shape[0]), num_shared=cfg.num_shared,
                               renormalize=renormalize, profile=profile, packet_bytes=packet_bytes,
-                              force_ep=force_ep)
+                              force_ep=force_ep, mover=mover, num_slots=num_slots)
         self.experts = HostExperts(cfg.hidden, cfg.ffn, inp.w1, inp.w3, inp.w2)
         self.router = bf16_tensor(inp.router)
 
