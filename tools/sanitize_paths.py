@@ -1,6 +1,7 @@
 """Small runs of every engine path for compute-sanitizer (memcheck / racecheck / synccheck):
 tiny MoE layer, GPU Task B, grouped launches over many small experts, CTA-pair + tail split,
-and in-process P2P expert parallelism (W = 2)."""
+in-process P2P expert parallelism (W = 2), the opt-in GEMM variants (swap-AB tail tiles,
+224/192-wide pair tiles, device-side kernel choice) and the Contiguous Data Mover."""
 import os, sys, threading
 sys.path.insert(0, "."); sys.path.insert(0, "tests")
 import numpy as np, torch
@@ -57,4 +58,24 @@ th = [threading.Thread(target=work, args=(q,)) for q in range(W)]
 for l in ly: l.close()
 for e in ex: e.close()
 full.close()
+# 5. GEMM variants: swap-AB tail tiles, 224/192-wide tiles, device-side kernel choice
+cfg = synth.MoEConfig("custom", 24, 768, 1792, 8, 2, 700, 1)
+inp = synth.gen_inputs(cfg)
+for env in ({"MOE_GEMM_PAIR": "1", "MOE_GEMM_TAILSWAP": "1"},
+            {"MOE_GEMM_PAIR": "1", "MOE_GEMM_ALT": "1"},
+            {"MOE_GEMM_PAIR": "device", "MOE_GEMM_ALT": "1"}):
+    os.environ.update(env)
+    r = GpuRun(inp); r.run(); r.close()
+    for k in env: del os.environ[k]
+# 6. the data mover: small packets, 2 slots, back-to-back calls + Task B
+cfg = synth.MoEConfig("custom", 25, 256, 384, 8, 2, 300)
+inp = synth.gen_inputs(cfg)
+r = GpuRun(inp, mover=True, packet_bytes=64 << 10, num_slots=2)
+r.run(); r.run()
+tb = synth.gen_taskb(cfg, inp.x)
+hl = HostLayer(cfg.hidden, tb.wo, tb.gamma)
+a, res = bf16_tensor(tb.attn), bf16_tensor(tb.resid)
+o = torch.empty_like(a)
+r.layer.taskb_forward(a, res, hl, tb.eps, r.router, r.experts, o)
+r.layer.sync(); torch.cuda.synchronize(); hl.close(); r.close()
 print("sanitize paths done")
