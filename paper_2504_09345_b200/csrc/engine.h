@@ -110,6 +110,11 @@ struct moe_ctx_s {
     // kernel's idle last wave.
     bool tail_split = false;
     bool alt_tiles = false;   // MOE_GEMM_ALT=1: pair kernel may pick 224/192-wide tiles
+    // MOE_GEMM_STREAMK: the pair kernel's partial last wave as K-chunks (GemmBatch::streamk);
+    // sk_ws = num_sms/2 chunks x 256 KB of fp32 partials, sk_flags = [num_sms/2][2] counters.
+    bool streamk_default = false;
+    float* sk_ws = nullptr;
+    int* sk_flags = nullptr;
     cudaStream_t tail_stream = nullptr;
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
 

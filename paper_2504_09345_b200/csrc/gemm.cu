@@ -164,6 +164,7 @@ __device__ __forceinline__ void epilogue_row(uint32_t taddr, bool valid, __nv_bf
 // the tail tiles of all such groups are numbered after the full tiles (TailSched below).
 struct BatchInfo {
     int n, total, n_tail_grp, plan;
+    int sk_L, sk_S;            // stream-K: the last sk_L full tiles run as sk_S K-chunks each
     int first[kMaxBatch + 1];
     int m_tiles[kMaxBatch];
     int a_begin[kMaxBatch], a_end[kMaxBatch], out_base[kMaxBatch], b_row[kMaxBatch];
@@ -211,10 +212,29 @@ __device__ __forceinline__ void batch_tiles(BatchInfo* bi, int bm, int n_tiles, 
     }
     bi->first[bi->n] = t;
     bi->total = t;
+    bi->sk_L = 0;
+    bi->sk_S = 1;
     int nt = 0;
     for (int i = bi->n - 1; i >= 0; --i)
         if (bi->tail_nc[i]) bi->tail_grp[nt++] = i;
     bi->n_tail_grp = nt;
+}
+
+// Stream-K plan of the pair kernel's partial last wave (GemmBatch::streamk; the host model in
+// pair_makespan mirrors it): F full tiles on P pairs leave L = F % P tiles for a last wave in
+// which P - L pairs would idle.  If F > P and 0 < L <= P / 2, each of those L tiles is cut into
+// S = the largest power of two <= min(P / L, 4) that divides num_kb (S >= 2) K-chunks.
+__host__ __device__ __forceinline__ void streamk_plan(int F, int P, int num_kb, int& L, int& S) {
+    L = 0;
+    S = 1;
+    if (F <= P) return;
+    const int l = F % P;
+    if (l == 0 || l > P / 2) return;
+    int s2 = 1;   // at most 4 chunks: the owner's read of the others' partials stays short
+    while (s2 * 2 <= P / l && s2 * 2 <= 4 && num_kb % (s2 * 2) == 0) s2 *= 2;
+    if (s2 < 2) return;
+    L = l;
+    S = s2;
 }
 
 __device__ __forceinline__ void batch_init(BatchInfo* bi, const GemmBatch& b, int bm,
@@ -615,26 +635,45 @@ constexpr uint32_t kPairBBytes = 128 * BK * 2;   // per CTA (half of a 256-row B
 constexpr size_t kPairSmem =
     1024 + kPairStages * (kPairABytes + kPairBBytes) + kSwapEpiBytes + kBatchReserve + 256;
 
-// One tile of the pair kernel's sequence: a full (or padded) 256 x 256 tile (nc == 0) of group gi
-// at M tile m, weight tile n; or a swap tail (nc > 0): token columns [m*256, m*256 + nc).
+// One tile of the pair kernel's sequence: a full (or padded) 256 x BN tile (nc == 0) of group gi
+// at M tile m, weight tile n, over k-blocks [kb0, kb1); or a swap tail (nc > 0): token columns
+// [m*256, m*256 + nc).  Stream-K chunks have unit >= 0: split tile lidx, chunk `chunk`.
 struct PairTile {
-    int gi, m, n, nc;
+    int gi, m, n, nc, kb0, kb1, unit, chunk, lidx;
 };
 struct PairSched {
-    int t, P, F, n_tiles, group_m;
+    int t, P, Ffull, n_tiles, group_m, num_kb, pair, L, S;
+    bool unit_done;
     TailSched ts;
-    __device__ __forceinline__ void init(const BatchInfo* bi, int pair, int npairs, int nt,
-                                         int gm, float cost) {
-        t = pair; P = npairs; F = bi->total; n_tiles = nt; group_m = gm;
-        ts.init(F, bi->n_tail_grp * nt, npairs, pair, cost);
+    __device__ __forceinline__ void init(const BatchInfo* bi, int pair_, int npairs, int nt,
+                                         int gm, float cost, int nkb) {
+        t = pair_; P = npairs; n_tiles = nt; group_m = gm; num_kb = nkb; pair = pair_;
+        L = bi->sk_L; S = bi->sk_S;
+        Ffull = bi->total - L;
+        unit_done = false;
+        ts.init(bi->total, bi->n_tail_grp * nt, npairs, pair_, cost);
+    }
+    __device__ __forceinline__ void coords(const BatchInfo* bi, int tile, PairTile& o) const {
+        int local;
+        o.gi = batch_locate(bi, tile, local);
+        tile_coords(local, bi->m_tiles[o.gi], n_tiles, group_m, o.m, o.n);
     }
     __device__ __forceinline__ bool next(const BatchInfo* bi, PairTile& o) {
-        if (t < F) {
-            int local;
-            o.gi = batch_locate(bi, t, local);
-            tile_coords(local, bi->m_tiles[o.gi], n_tiles, group_m, o.m, o.n);
-            o.nc = 0;
+        o.nc = 0; o.kb0 = 0; o.kb1 = num_kb; o.unit = -1; o.chunk = 0; o.lidx = 0;
+        if (t < Ffull) {
+            coords(bi, t, o);
             t += P;
+            return true;
+        }
+        if (!unit_done && pair < L * S) {   // this pair's stream-K chunk (one per pair at most)
+            unit_done = true;
+            o.unit = pair;
+            o.lidx = pair / S;
+            o.chunk = pair % S;
+            coords(bi, Ffull + o.lidx, o);
+            const int per = num_kb / S;
+            o.kb0 = o.chunk * per;
+            o.kb1 = o.kb0 + per;
             return true;
         }
         int tj;
@@ -683,7 +722,12 @@ expert_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
             ? plan_tiles(bi, N, batch.select, batch.bn_single, true, true, batch.alt_ok != 0)
             : plan_tiles(bi, N, gridDim.x, 0, false, true, batch.alt_ok != 0);
         bi->plan = plan;
-        if (plan > 0) batch_tiles(bi, PM, N / plan, batch.tail_swap != 0 && plan == 256);
+        if (plan > 0) {
+            const bool tails = batch.tail_swap != 0 && plan == 256;
+            batch_tiles(bi, PM, N / plan, tails);
+            if (batch.streamk && !tails && batch.sk_ws && batch.sk_flags)
+                streamk_plan(bi->total, (int)gridDim.x / 2, K / BK, bi->sk_L, bi->sk_S);
+        }
     }
     __syncthreads();
     if (bi->plan <= 0) return;                   // uniform over the grid
@@ -693,7 +737,7 @@ expert_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
     const int num_kb = K / BK;
     const int group_m = g_group_m > 0 ? g_group_m : ((K <= 8192) ? 16 : 4);  // 256-row tiles
     PairSched sched0;
-    sched0.init(bi, pair, npairs, n_tiles, group_m, batch.tail_cost);
+    sched0.init(bi, pair, npairs, n_tiles, group_m, batch.tail_cost, num_kb);
     {
         PairSched probe = sched0;
         PairTile pt;
@@ -737,7 +781,7 @@ expert_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                 const int arow = bi->a_begin[pt.gi] + pt.m * PM + (int)rank * (pt.nc ? half : 128);
                 const uint32_t tx = pt.nc ? 2 * kPairBBytes + (uint32_t)pt.nc * BK * 2
                                           : 2 * kPairABytes + (uint32_t)BN * BK * 2;
-                for (int kb = 0; kb < num_kb; ++kb) {
+                for (int kb = pt.kb0; kb < pt.kb1; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1u);
                     const uint32_t fbar = full0 + stage * 8;
                     if (leader) ptx::mbar_arrive_expect_tx(&full[stage], tx);
@@ -778,7 +822,7 @@ expert_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                 ptx::mbar_wait(&tempty[acc], aphase ^ 1u);
                 ptx::tc_fence_after();
                 const uint32_t d = tmem_base + acc * kAccCols;
-                for (int kb = 0; kb < num_kb; ++kb) {
+                for (int kb = pt.kb0; kb < pt.kb1; ++kb) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
                     const uint32_t a0 = ptx::smem_u32(sA + stage * kPairABytes);
@@ -789,7 +833,7 @@ expert_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                     for (int kk = 0; kk < BK / 16; ++kk)
                         ptx::umma_bf16_cta2(d, ptx::umma_desc_sw128_kmajor(x0 + kk * 32),
                                             ptx::umma_desc_sw128_kmajor(y0 + kk * 32), idesc,
-                                            (kb | kk) != 0 ? 1u : 0u);
+                                            (kb != pt.kb0 || kk != 0) ? 1u : 0u);
                     ptx::umma_commit_cta2_mc(&empty[stage], 0x3);
                     if (++stage == S) {
                         stage = 0;
@@ -814,7 +858,67 @@ expert_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
             ptx::tc_fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
             const int gi = pt.gi;
-            if (!pt.nc) {
+            if (pt.unit >= 0 && pt.chunk != 0) {
+                // stream-K chunk: fp32 partial of this CTA's 128 rows -> sk_ws, then count it
+                const int row = (int)rank * 128 + q * 32 + lane;
+                float* ws = batch.sk_ws + (int64_t)pt.unit * kStreamKUnitFloats;
+#pragma unroll 1
+                for (int c = 0; c < BN; c += 32) {
+                    uint32_t v[32];
+                    ptx::tmem_ld_32x32b_x32(taddr + c, v);
+                    ptx::tmem_ld_wait();
+                    float4* dst = reinterpret_cast<float4*>(ws + ((int64_t)(c / 32) * 256 + row) * 32);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                             __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+                }
+                ptx::named_bar_sync(1, 128);
+                if (q == 0 && lane == 0) {
+                    __threadfence();
+                    ptx::red_release_gpu_add(batch.sk_flags + pt.lidx * 2 + (int)rank, 1);
+                }
+            } else if (!pt.nc) {
+                if (pt.unit >= 0) {
+                    // stream-K owner (chunk 0): wait for the other S-1 chunks' partials of these
+                    // rows, add them into the TMEM accumulator, then the usual epilogue
+                    const int S = bi->sk_S;
+                    int* flag = batch.sk_flags + pt.lidx * 2 + (int)rank;
+                    if (q == 0 && lane == 0)
+                        while (ptx::ld_acquire_gpu(flag) < S - 1) __nanosleep(64);
+                    ptx::named_bar_sync(1, 128);
+                    const int row = (int)rank * 128 + q * 32 + lane;
+#pragma unroll 1
+                    for (int c = 0; c < BN; c += 32) {
+                        uint32_t v[32];
+                        ptx::tmem_ld_32x32b_x32(taddr + c, v);
+                        ptx::tmem_ld_wait();
+                        // all (S-1) x 8 loads of this 32-column chunk in flight at once; fixed
+                        // summation order (chunk 1, 2, 3) keeps the result deterministic
+                        const float4* src = reinterpret_cast<const float4*>(
+                            batch.sk_ws + (int64_t)pt.unit * kStreamKUnitFloats +
+                            ((int64_t)(c / 32) * 256 + row) * 32);
+                        constexpr int64_t kUnit4 = kStreamKUnitFloats / 4;
+                        float4 p4[3][8];
+#pragma unroll
+                        for (int sc = 1; sc < 4; ++sc)
+#pragma unroll
+                            for (int i = 0; i < 8; ++i)
+                                p4[sc - 1][i] = sc < S ? __ldcg(src + sc * kUnit4 + i)
+                                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const float4 a = p4[0][i], b = p4[1][i], d4 = p4[2][i];
+                            v[4 * i] = __float_as_uint(__uint_as_float(v[4 * i]) + ((a.x + b.x) + d4.x));
+                            v[4 * i + 1] = __float_as_uint(__uint_as_float(v[4 * i + 1]) + ((a.y + b.y) + d4.y));
+                            v[4 * i + 2] = __float_as_uint(__uint_as_float(v[4 * i + 2]) + ((a.z + b.z) + d4.z));
+                            v[4 * i + 3] = __float_as_uint(__uint_as_float(v[4 * i + 3]) + ((a.w + b.w) + d4.w));
+                        }
+                        ptx::tmem_st_32x32b_x32(taddr + c, v);
+                    }
+                    ptx::tmem_st_wait();
+                    if (q == 0 && lane == 0) *flag = 0;   // ready for the next launch
+                }
                 const int arow = bi->a_begin[gi] + pt.m * PM + (int)rank * 128 + q * 32 + lane;
                 const bool valid = arow < bi->a_end[gi];
                 const int64_t orow = (int64_t)bi->out_base[gi] + (arow - bi->a_begin[gi]);
@@ -1061,13 +1165,19 @@ cudaError_t launch_expert_gemm_swap(int mode, const CUtensorMap* tmW, const Toke
 }
 
 double pair_makespan(const int64_t* rows, int n, int n_tiles, int npairs, bool tail_swap,
-                     float tail_cost) {
+                     float tail_cost, bool streamk, int num_kb) {
     int64_t F = 0, R = 0;
     for (int i = 0; i < n; ++i) {
         const int r = (int)std::max<int64_t>(0, rows[i]);
         const int nc = tail_cols(r, tail_swap);
         F += (int64_t)(nc ? r / kPairRows : (r + kPairRows - 1) / kPairRows) * n_tiles;
         if (nc) R += n_tiles;
+    }
+    if (streamk && !tail_swap) {
+        int L, S;
+        streamk_plan((int)F, npairs, num_kb, L, S);
+        if (L > 0)   // q full waves + one 1/S-long chunk + the partial-sum fixup (~0.1 tile)
+            return (double)(F / npairs) + 1.0 / S + 0.1;
     }
     double worst = 0.0;
     for (int p = 0; p < npairs; ++p) {

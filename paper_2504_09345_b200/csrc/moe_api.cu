@@ -274,7 +274,7 @@ moe_status request_copy(moe_ctx c, const void* const* experts, int i, uint64_t q
 // swap-AB tail tiles in the pair kernel (not combined with the tail-split experiment)
 bool tail_swap_on(moe_ctx c) { return c->tail_swap && !c->tail_split; }
 
-bool pick_pair(moe_ctx c, const int64_t* rows, int n, int bn, int N) {
+bool pick_pair(moe_ctx c, const int64_t* rows, int n, int bn, int N, int K) {
     if (bn != 256 || c->pair_mode == 0) return false;
     if (c->pair_mode != -1) return true;   // 1: always; 2: the device decides (GemmBatch::select)
     const int sms = c->num_sms;
@@ -284,7 +284,8 @@ bool pick_pair(moe_ctx c, const int64_t* rows, int n, int bn, int N) {
         if (rows[i] > 0) t1 += ((rows[i] + 127) / 128) * nt;
     if (t1 == 0) return false;
     const double w1 = (double)((t1 + sms - 1) / sms) / 0.76;
-    const double w2 = moe::pair_makespan(rows, n, (int)nt, sms / 2, tail_swap_on(c), c->tail_cost) / 0.97;
+    const double w2 = moe::pair_makespan(rows, n, (int)nt, sms / 2, tail_swap_on(c), c->tail_cost,
+                                         c->sk_ws != nullptr, K / 64) / 0.97;
     return w2 < w1;
 }
 
@@ -305,6 +306,11 @@ moe_status launch_grouped(moe_ctx c, int mode, int bn, bool pair, const CUtensor
     if (!c->alt_tiles) alt = nullptr;
     batch.bn_single = bn;
     batch.alt_ok = alt ? 1 : 0;
+    if (c->sk_ws && !c->tail_split) {   // stream-K last wave (pair kernel only)
+        batch.streamk = 1;
+        batch.sk_ws = c->sk_ws;
+        batch.sk_flags = c->sk_flags;
+    }
     if (pair && c->pair_mode == 2 && !c->tail_split) {
         batch.select = grid;
         batch.tail_swap = tail_swap_on(c) ? 1 : 0;
@@ -435,7 +441,7 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
                                                          shared ? &tm_x_t : tmT_routed, b1,
                                                          2 * hi, h, c->h_act, hi, nullptr, grid, st));
             } else {
-                const bool pr = pick_pair(c, rows, nb, c->bn1, 2 * hi);
+                const bool pr = pick_pair(c, rows, nb, c->bn1, 2 * hi, h);
                 moe_status gs = launch_grouped(c, moe::kGemmSwiGLU, c->bn1, pr,
                                                shared ? &tm_x : tmA_routed, &c->tm_w13,
                                                &c->tm_w13_pair, &c->tm_w13_alt,
@@ -460,7 +466,7 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
                                                          shared ? c->y_perm : y_routed, h,
                                                          nullptr, grid, st));
             } else {
-                const bool pr = pick_pair(c, rows, nb, c->bn2, h);
+                const bool pr = pick_pair(c, rows, nb, c->bn2, h, hi);
                 moe_status gs = launch_grouped(c, moe::kGemmPlain, c->bn2, pr, &c->tm_h,
                                                &c->tm_w2, &c->tm_w2_pair, &c->tm_w2_alt,
                                                &c->tm_h_t, b2, h, hi,
@@ -707,7 +713,7 @@ moe_status taskb_impl(moe_ctx c, const __nv_bfloat16* attn, const __nv_bfloat16*
                                                      resid, c->num_sms, st));
         } else {
             const int64_t rows = T;
-            const bool pr = pick_pair(c, &rows, 1, c->bn2, h);
+            const bool pr = pick_pair(c, &rows, 1, c->bn2, h, h);
             moe_status gs = launch_grouped(c, moe::kGemmResidual, c->bn2, pr, &tm_attn,
                                            &c->tm_wo[b], &c->tm_wo_pair[b], &c->tm_wo_alt[b],
                                            &tm_attn_t, ob, h, h, c->h1_ws, h, st, resid);
@@ -893,6 +899,17 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     if (const char* e = getenv("MOE_GEMM_SWAP")) c->swap_mode = atoi(e) != 0;
     if (const char* e = getenv("MOE_GEMM_TAILSWAP")) c->tail_swap = atoi(e) != 0;
     if (const char* e = getenv("MOE_GEMM_ALT")) c->alt_tiles = atoi(e) != 0;
+    {   // stream-K last wave of the pair kernel (MOE_GEMM_STREAMK)
+        bool sk = c->streamk_default;
+        if (const char* e = getenv("MOE_GEMM_STREAMK")) sk = atoi(e) != 0;
+        if (sk) {
+            const size_t units = (size_t)std::max(1, c->num_sms / 2);
+            if (cudaMalloc((void**)&c->sk_ws, units * moe::kStreamKUnitFloats * sizeof(float)) != cudaSuccess ||
+                cudaMalloc((void**)&c->sk_flags, units * 2 * sizeof(int)) != cudaSuccess ||
+                cudaMemset(c->sk_flags, 0, units * 2 * sizeof(int)) != cudaSuccess)
+                return fail(MOE_E_NOMEM);
+        }
+    }
     if (const char* e = getenv("MOE_GEMM_TAILCOST")) {
         const float v = (float)atof(e);
         if (v > 0.f && v <= 4.f) c->tail_cost = v;
@@ -1191,7 +1208,7 @@ moe_status moe_destroy(moe_ctx c) {
     }
     void* bufs[] = {c->idx_ws, c->gates_ws, c->tile_counts, c->tile_prefix, c->offsets, c->counts,
                     c->grp1, c->grp2, c->shared_grp, c->pos, c->x_perm, c->h_act, c->y_perm,
-                    c->h1_ws, c->u_ws, c->oproj_grp, c->clk_acc};
+                    c->h1_ws, c->u_ws, c->oproj_grp, c->clk_acc, c->sk_ws, c->sk_flags};
     for (void* p : bufs) cudaFree(p);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->token_stream) cudaStreamDestroy(c->token_stream);

@@ -57,7 +57,16 @@ struct GemmBatch {
     // clk: if non-null, CTA 0 adds its SM cycles (clock64) and elapsed ns (globaltimer) from
     // kernel entry to exit to clk[0] / clk[1] (the SM clock under power management).
     unsigned long long* clk;
+    // Stream-K last wave (CTA-pair kernel, streamk != 0): when the full tiles leave a partial
+    // last wave of L <= P/2 tiles on P pairs, those L tiles are cut along K into S chunks that
+    // run on S*L <= P pairs at once; chunk 0's pair sums the other chunks' fp32 partials
+    // (sk_ws: kStreamKUnitFloats per chunk, P chunks) after their per-CTA counters in sk_flags
+    // ([P][2], zero between launches) reach S - 1, then runs the usual epilogue.
+    int32_t streamk;
+    float* sk_ws;
+    int* sk_flags;
 };
+constexpr int64_t kStreamKUnitFloats = 8ll * 256 * 32;   // 256 rows x 256 fp32 columns
 // Extra B maps of the CTA-pair kernel: per-CTA boxes of 112 and 96 rows for 224- and 192-wide
 // tiles (chosen on the device when N divides and fewer waves result, e.g. 28672 = 128 x 224).
 struct PairBMaps {
@@ -180,7 +189,7 @@ cudaError_t launch_expert_gemm(int mode, int bn, bool pair, const CUtensorMap* t
 // units of one full 256x256 tile time of a launch whose groups have rows[i] rows, N/256 weight
 // tiles, on npairs CTA pairs.
 double pair_makespan(const int64_t* rows, int n, int n_tiles, int npairs, bool tail_swap,
-                     float tail_cost);
+                     float tail_cost, bool streamk = false, int num_kb = 64);
 bool make_token_maps(TokenMaps* t, const void* base, uint64_t rows, uint64_t cols);  // moe_api.cu
 // Swap-AB CTA-pair kernel (gemm.cu): weights are the 256-row M side (tmW: box 64 x 128, M rows
 // = 2 h_i for SwiGLU, h otherwise, M % 256 == 0), the group's tokens the N side, N = 32..256

@@ -326,6 +326,29 @@ def test_gemm_pair_tail_swap_schedules(shape, cost, monkeypatch):
     run.close()
 
 
+@pytest.mark.parametrize("shape", [
+    dict(hidden=1024, ffn=2560, num_experts=1, top_k=1, tokens=1000),   # GEMM1: 80 tiles, L=6, S=8
+    dict(hidden=512, ffn=4864, num_experts=2, top_k=1, tokens=1500),    # 2 ragged groups, 228 tiles
+    dict(hidden=4096, ffn=1024, num_experts=1, top_k=1, tokens=1100),   # GEMM2: 80 tiles, L=6
+])
+def test_gemm_pair_streamk_last_wave(shape, monkeypatch):
+    """MOE_GEMM_STREAMK=1: the pair kernel's partial last wave runs as K-chunks on otherwise idle
+    SM pairs; chunk 0 adds the other chunks' fp32 partials before its epilogue.  Must match the
+    oracle, and back-to-back calls must stay bitwise stable (the chunk counters reset)."""
+    monkeypatch.setenv("MOE_GEMM_PAIR", "1")
+    monkeypatch.setenv("MOE_GEMM_STREAMK", "1")
+    cfg = synth.MoEConfig("custom", 17, shape["hidden"], shape["ffn"], shape["num_experts"],
+                          shape["top_k"], shape["tokens"], 0)
+    inp = synth.gen_inputs(cfg)
+    run, out, *_ = _check_full(inp)
+    try:
+        for _ in range(3):
+            out2, _, _ = run.run()
+            assert torch.equal(out2, out)
+    finally:
+        run.close()
+
+
 # ------------------------------------------------------------ swap-AB (weights as M) GEMM
 @pytest.mark.parametrize("shape", [
     dict(hidden=256, ffn=384, num_experts=8, top_k=2, tokens=1500),

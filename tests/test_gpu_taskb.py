@@ -122,14 +122,17 @@ def test_taskb_staged_parity(shape, force_ep, swap, monkeypatch):
 @pytest.mark.parametrize("shape", [
     dict(hidden=256, ffn=384, ne=8, k=2, T=300),
     dict(hidden=768, ffn=1792, ne=8, k=2, T=1100, S=1),
+    dict(hidden=4096, ffn=256, ne=2, k=1, T=1100),     # O-projection: 80 pair tiles (stream-K)
 ])
-@pytest.mark.parametrize("variant", ["tailswap", "alt", "device"])
+@pytest.mark.parametrize("variant", ["tailswap", "alt", "device", "streamk"])
 def test_taskb_gemm_variants(shape, variant, monkeypatch):
     """The residual-epilogue O-projection (and the expert GEMMs) through the opt-in GEMM paths:
     swap-AB tail tiles, 224 / 192-wide pair tiles, device-side kernel selection."""
     monkeypatch.setenv("MOE_GEMM_PAIR", "device" if variant == "device" else "1")
     if variant == "tailswap":
         monkeypatch.setenv("MOE_GEMM_TAILSWAP", "1")
+    elif variant == "streamk":
+        monkeypatch.setenv("MOE_GEMM_STREAMK", "1")
     else:
         monkeypatch.setenv("MOE_GEMM_ALT", "1")
     inp, tb = _inputs(shape["hidden"], shape["ffn"], shape["ne"], shape["k"], shape["T"],
