@@ -36,19 +36,27 @@ SHAPES = _shapes()
 _REF = {}
 
 
-@pytest.mark.parametrize("mode", ["auto", "pair0", "pair1", "swap"])
+MODES = {"auto": {}, "pair0": {"MOE_GEMM_PAIR": "0"}, "pair1": {"MOE_GEMM_PAIR": "1"},
+         "swap": {"MOE_GEMM_SWAP": "1"},
+         # the opt-in variants: every one must stay exact on every shape
+         "tailswap": {"MOE_GEMM_PAIR": "1", "MOE_GEMM_TAILSWAP": "1"},
+         "alt": {"MOE_GEMM_PAIR": "1", "MOE_GEMM_ALT": "1"},
+         "device": {"MOE_GEMM_PAIR": "device", "MOE_GEMM_ALT": "1"},
+         "streamk": {"MOE_GEMM_PAIR": "1", "MOE_GEMM_STREAMK": "1"},
+         "mover": {}}
+
+
+@pytest.mark.parametrize("mode", list(MODES))
 @pytest.mark.parametrize("case", range(len(SHAPES)))
 def test_random_shapes(case, mode, monkeypatch):
     shape = SHAPES[case]
-    env = {"auto": {}, "pair0": {"MOE_GEMM_PAIR": "0"}, "pair1": {"MOE_GEMM_PAIR": "1"},
-           "swap": {"MOE_GEMM_SWAP": "1"}}[mode]
-    for k_, v in env.items():
+    for k_, v in MODES[mode].items():
         monkeypatch.setenv(k_, v)
     cfg = synth.MoEConfig("custom", 100 + case, shape["hidden"], shape["ffn"],
                           shape["num_experts"], shape["top_k"], shape["tokens"],
                           shape["num_shared"])
     inp = synth.gen_inputs(cfg)
-    run = GpuRun(inp)
+    run = GpuRun(inp, mover=(mode == "mover"), packet_bytes=(256 << 10) if mode == "mover" else 0)
     try:
         out, idx, gates = run.run()
         if case not in _REF:   # the oracle result does not depend on the tiling mode
