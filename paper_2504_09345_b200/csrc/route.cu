@@ -9,6 +9,7 @@
 //   * token positions inside an expert group are ascending in t (R12), computed from per-tile
 //     counts (no atomics on the data path).
 #include <cfloat>
+#include <cstdlib>
 #include <cmath>
 
 #include "moe_internal.h"
@@ -418,9 +419,15 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
     const int n_tiles = (T + kRouteTile - 1) / kRouteTile;
     if (n_tiles == 0) return cudaSuccess;
     // EPT experts per warp: few experts -> fewer per warp, so a 32-token tile still spreads over
-    // several warps (C1's 4096 tokens are only 128 tiles); many experts -> 8 per warp (16 regs
-    // of accumulators, 1 x load per 8 DFMAs).
-    const int ept = ne <= 8 ? 1 : (ne <= 16 ? 2 : 8);
+    // several warps (C1's 4096 tokens are only 128 tiles); more experts -> more per warp (fewer
+    // x loads per DFMA).  Measured per call (profiles/r01/router_ept): N_e = 8 (C1): EPT 1 / 2
+    // 0.15 ms, 4 0.18, 8 0.44; N_e = 16 (DBRX): EPT 2 0.64 ms, 4 0.52, 8 0.70.
+    int ept = ne <= 8 ? 1 : (ne <= 16 ? 4 : 8);
+    if (const char* e = getenv("MOE_ROUTER_EPT")) {   // experiments: 1, 2, 4 or 8
+        const int v = atoi(e);
+        const int bound = v >= 8 ? 512 : 256;          // the kernel's __launch_bounds__
+        if ((v == 1 || v == 2 || v == 4 || v == 8) && ((ne + v - 1) / v) * 32 <= bound) ept = v;
+    }
     const int nw = (ne + ept - 1) / ept;
     const int ne_pad = nw * ept;
     const size_t dyn = sizeof(double) * (size_t)(kChunk * kXsPitch + kChunk * ne_pad);
@@ -435,6 +442,7 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
     } while (0)
     if (ept == 1) MOE_ROUTER(1);
     else if (ept == 2) MOE_ROUTER(2);
+    else if (ept == 4) MOE_ROUTER(4);
     else MOE_ROUTER(8);
 #undef MOE_ROUTER
     return cudaGetLastError();

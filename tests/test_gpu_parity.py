@@ -349,6 +349,18 @@ def test_gemm_pair_streamk_last_wave(shape, monkeypatch):
         run.close()
 
 
+@pytest.mark.parametrize("ept", ["1", "2", "4", "8"])
+@pytest.mark.parametrize("ne,k", [(5, 2), (8, 2), (16, 4)])
+def test_router_experts_per_warp_variants(ne, k, ept, monkeypatch):
+    """Every router_topk_kernel<EPT> instantiation (MOE_ROUTER_EPT; the default picks by N_e)
+    gives the same bit-exact selection and gates (one fp64 FMA chain per logit either way)."""
+    monkeypatch.setenv("MOE_ROUTER_EPT", ept)
+    cfg = synth.MoEConfig("custom", 19, 384, 256, ne, k, 777, 0)
+    inp = synth.gen_inputs(cfg)
+    run, *_ = _check_full(inp)
+    run.close()
+
+
 # ------------------------------------------------------------ swap-AB (weights as M) GEMM
 @pytest.mark.parametrize("shape", [
     dict(hidden=256, ffn=384, num_experts=8, top_k=2, tokens=1500),
