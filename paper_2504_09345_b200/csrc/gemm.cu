@@ -15,6 +15,10 @@
 //
 // Kernels: expert_gemm_kernel (1 CTA, M = 128), expert_gemm_pair_kernel (CTA pair,
 // cta_group::2, M = 256), expert_gemm_swap_kernel (weights as M, tokens as N; experimental).
+// Opt-in variants of the pair kernel, each parity-tested and measured (none beat
+// the default in-bench): swap-AB tail tiles (GemmBatch::tail_swap), 224/192-wide tiles
+// (PairBMaps), device-side choice between the two kernels (GemmBatch::select), stream-K last
+// wave (GemmBatch::streamk).  Every launch can report its SM clock (GemmBatch::clk).
 // Structure of the first (persistent, one CTA per SM, 256 threads):
 //   warp 0     TMA producer: A tile 128x64 and B tile BNx64 per stage, 128B swizzle
 //   warp 1     MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M=128, N=BN, K=16 per instr
