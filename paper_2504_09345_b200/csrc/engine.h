@@ -89,6 +89,7 @@ struct moe_ctx_s {
     // MOE_FLAG_MOVER: expert copies go through the mover thread (mover.cu) in packets, ordered
     // against the GEMMs by device counters instead of the ready13 / ready2 / slot_free events.
     moe::Mover* mover = nullptr;
+    bool mover_trace = false;   // MOE_MOVER_TRACE=1: one stderr line per GEMM wait / mover job
     // The staging buffer seen as one W13 matrix [nslots * 3 h_i, h] and one W2 matrix
     // [nslots * 3 h, h_i]: slot s's W13 starts at row 3 h_i s, its W2 at row 3 h s + 2 h, so one
     // GEMM launch can cover experts in different slots (GemmBatch::b_row).

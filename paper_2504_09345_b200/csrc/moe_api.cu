@@ -420,7 +420,7 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         b1.n = b2.n = nb;
         int64_t rows[moe::kMaxBatch];
         if (c->mover) {
-            if (getenv("MOE_MOVER_TRACE"))
+            if (c->mover_trace)
                 fprintf(stderr, "[api] GEMMs of items [%llu, %llu): wait r13 >= %llu\n",
                         (unsigned long long)q, (unsigned long long)(q + nb), (unsigned long long)(q + nb));
             moe_status ws = moe::mover_wait(c, st, 0, q + nb);
@@ -932,6 +932,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
         if (es != MOE_OK) return fail(es);
     }
     if (cfg->flags & MOE_FLAG_MOVER) {
+        c->mover_trace = getenv("MOE_MOVER_TRACE") && atoi(getenv("MOE_MOVER_TRACE")) != 0;
         moe_status ms = moe::mover_start(c);
         if (ms != MOE_OK) return fail(ms);
     }
