@@ -20,7 +20,6 @@ namespace moe {
 namespace {
 
 constexpr int kChunk = 64;  // channels staged per iteration (one 16-byte vector per thread of x)
-constexpr int kXsPitch = kRouteTile + 1;  // padded row (doubles): conflict-free transposed stores
 
 __device__ __forceinline__ bool ranks_above(double la, int a, double lb, int b) {
     const bool na = isnan(la), nb = isnan(lb);
@@ -40,36 +39,45 @@ __device__ __forceinline__ void bf16x8_to_f64(const int4& v, double (&o)[8]) {
     }
 }
 
-// Router: one block = kRouteTile (32) tokens; warp w owns experts [w*EPT, (w+1)*EPT) for all 32
-// tokens (lane = token).  Every (token, expert) logit is ONE fp64 FMA chain over the channels in
-// ascending order -- the definition's order (reading R6) -- so selection is bit-exact.  Per
-// channel a lane reads its x value (fp64, transposed tile) and its EPT router weights as EPT/2
-// double2 broadcasts from a [channel][expert] tile zero-padded to a multiple of EPT experts:
-// 1 + EPT/2 shared-memory wavefront groups per EPT DFMAs and no branches in the inner loop.
-// 64-channel chunks are staged with 16-byte loads prefetched into registers one chunk ahead.
-template <int EPT>
-__global__ void __launch_bounds__(EPT >= 8 ? 512 : 256)
+// Router: one block = TPT x kRouteTile (32) tokens; warp w owns experts [w*EPT, (w+1)*EPT) for all
+// of them (lane = token, TPT tokens per lane).  Every (token, expert) logit is ONE fp64 FMA chain
+// over the channels in ascending order -- the definition's order (reading R6) -- so selection is
+// bit-exact.  Per channel a lane reads its TPT x values (fp64, transposed tile) and its EPT router
+// weights as EPT/2 double2 broadcasts from a [channel][expert] tile zero-padded to a multiple of
+// EPT experts: TPT + EPT/2 shared-memory wavefront groups per TPT*EPT DFMAs and no branches in
+// the inner loop (TPT = 2 for many experts: the kernel is shared-memory bound there -- ncu at C4:
+// 70% of the smem pipe, short-scoreboard stalls -- and a second token per lane reuses every
+// weight broadcast).  64-channel chunks are staged with 16-byte loads prefetched into registers
+// one chunk ahead.
+template <int EPT, int TPT>
+__global__ void __launch_bounds__((EPT >= 8 && TPT == 1) ? 512 : 256)
 router_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
                    const __nv_bfloat16* __restrict__ wr, int ne, int k, int renorm,
                    int32_t* __restrict__ idx_out, float* __restrict__ gate_out,
                    int32_t* __restrict__ tile_counts) {
+    constexpr int kTok = kRouteTile * TPT;      // tokens per block
+    constexpr int kPitch = kTok + 1;            // padded row (doubles): conflict-free stores
     extern __shared__ __align__(16) double dyn[];
-    __shared__ int cnt[kMaxExperts];
+    __shared__ int cnt[TPT][kMaxExperts];
     const int nw = blockDim.x >> 5;            // warps = ne_pad / EPT
     const int ne_pad = nw * EPT;
-    double* xs = dyn;                           // [kChunk][kXsPitch]
-    double* ws = dyn + kChunk * kXsPitch;       // [kChunk][ne_pad], later logits [32][ne_pad]
+    double* xs = dyn;                           // [kChunk][kPitch]
+    double* ws = dyn + kChunk * kPitch;         // [kChunk][ne_pad], later logits [kTok][ne_pad]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
-    const int t0 = blockIdx.x * kRouteTile;
-    for (int e = tid; e < kMaxExperts; e += nthr) cnt[e] = 0;
+    const int t0 = blockIdx.x * kTok;
+    for (int e = tid; e < TPT * kMaxExperts; e += nthr) cnt[e / kMaxExperts][e % kMaxExperts] = 0;
 
-    double acc[EPT];
+    double acc[TPT][EPT];
 #pragma unroll
-    for (int i = 0; i < EPT; ++i) acc[i] = 0.0;
+    for (int p = 0; p < TPT; ++p)
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) acc[p][i] = 0.0;
 
-    constexpr int kXV = kRouteTile * (kChunk / 8) / 32;  // x vectors per thread (1 warp) = 8
+    // x vectors per thread: the TPT = 2 variant runs with >= 3 warps (N_e > 16)
+    constexpr int kMinThreads = TPT == 2 ? 96 : 32;
+    constexpr int kXV = (kTok * (kChunk / 8) + kMinThreads - 1) / kMinThreads;
     constexpr int kWV = (EPT * (kChunk / 8) + 31) / 32;  // router vectors per thread
-    const int n_xv = kRouteTile * (kChunk / 8);
+    const int n_xv = kTok * (kChunk / 8);
     const int n_wv = ne_pad * (kChunk / 8);
     int4 xr[kXV], wv[kWV];
     // Staging maps consecutive lanes to consecutive TOKENS (x) / EXPERTS (router) at a fixed
@@ -80,7 +88,7 @@ router_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
         for (int j = 0; j < kXV; ++j) {
             const int v = tid + j * nthr;
             if (v < n_xv) {
-                const int t = v & 31, cc = (v >> 5) * 8;
+                const int t = v % kTok, cc = (v / kTok) * 8;
                 xr[j] = (t0 + t < T) ? ptx::ld_nc_v4(x + (size_t)(t0 + t) * h + c0 + cc)
                                      : make_int4(0, 0, 0, 0);
             }
@@ -101,10 +109,10 @@ router_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
         for (int j = 0; j < kXV; ++j) {
             const int v = tid + j * nthr;
             if (v < n_xv) {
-                const int t = v & 31, cc = (v >> 5) * 8;
+                const int t = v % kTok, cc = (v / kTok) * 8;
                 bf16x8_to_f64(xr[j], d);
 #pragma unroll
-                for (int q = 0; q < 8; ++q) xs[(cc + q) * kXsPitch + t] = d[q];
+                for (int q = 0; q < 8; ++q) xs[(cc + q) * kPitch + t] = d[q];
             }
         }
 #pragma unroll
@@ -127,29 +135,38 @@ router_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
         if (c0 + kChunk < h) load(c0 + kChunk);   // next chunk in flight during the FMAs
 #pragma unroll 8
         for (int c = 0; c < kChunk; ++c) {
-            const double xv = xs[c * kXsPitch + lane];
+            double xv[TPT];
+#pragma unroll
+            for (int p = 0; p < TPT; ++p) xv[p] = xs[c * kPitch + p * 32 + lane];
             if constexpr (EPT == 1) {
-                acc[0] = fma(xv, wbase[c * ne_pad], acc[0]);
+                const double w = wbase[c * ne_pad];
+#pragma unroll
+                for (int p = 0; p < TPT; ++p) acc[p][0] = fma(xv[p], w, acc[p][0]);
             } else {
                 const double2* w2 = reinterpret_cast<const double2*>(wbase + c * ne_pad);
 #pragma unroll
                 for (int i = 0; i < EPT / 2; ++i) {
                     const double2 w = w2[i];
-                    acc[2 * i] = fma(xv, w.x, acc[2 * i]);
-                    acc[2 * i + 1] = fma(xv, w.y, acc[2 * i + 1]);
+#pragma unroll
+                    for (int p = 0; p < TPT; ++p) {
+                        acc[p][2 * i] = fma(xv[p], w.x, acc[p][2 * i]);
+                        acc[p][2 * i + 1] = fma(xv[p], w.y, acc[p][2 * i + 1]);
+                    }
                 }
             }
         }
         __syncthreads();
     }
-    // logits -> shared [32][ne_pad]
+    // logits -> shared [kTok][ne_pad] (kTok <= kChunk: fits the router tile's space)
     double* lg = ws;
 #pragma unroll
-    for (int i = 0; i < EPT; ++i) lg[lane * ne_pad + warp * EPT + i] = acc[i];
+    for (int p = 0; p < TPT; ++p)
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) lg[(p * 32 + lane) * ne_pad + warp * EPT + i] = acc[p][i];
     __syncthreads();
 
-    // warp-shuffle top-k: warp w handles tokens w, w+nw, ... of the tile
-    for (int tt = warp; tt < kRouteTile; tt += nw) {
+    // warp-shuffle top-k: warp w handles tokens w, w+nw, ... of the block
+    for (int tt = warp; tt < kTok; tt += nw) {
         const int t = t0 + tt;
         if (t >= T) break;
         double v[kMaxExperts / 32];
@@ -217,11 +234,17 @@ router_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
                 }
             idx_out[(size_t)t * k + lane] = me;
             gate_out[(size_t)t * k + lane] = (float)(exp(mine - m) / z);
-            atomicAdd(&cnt[me], 1);
+            atomicAdd(&cnt[tt / kRouteTile][me], 1);
         }
     }
     __syncthreads();
-    for (int e = tid; e < ne; e += nthr) tile_counts[(size_t)blockIdx.x * ne + e] = cnt[e];
+    const int n_tiles = (T + kRouteTile - 1) / kRouteTile;
+#pragma unroll
+    for (int p = 0; p < TPT; ++p) {   // one row per 32-token routing tile (scan / permute grain)
+        const int tile = blockIdx.x * TPT + p;
+        if (tile < n_tiles)
+            for (int e = tid; e < ne; e += nthr) tile_counts[(size_t)tile * ne + e] = cnt[p][e];
+    }
 }
 
 // Single block of 1024 threads.  Warp w scans experts w, w+32, ... over the tiles.
@@ -430,20 +453,25 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
     }
     const int nw = (ne + ept - 1) / ept;
     const int ne_pad = nw * ept;
-    const size_t dyn = sizeof(double) * (size_t)(kChunk * kXsPitch + kChunk * ne_pad);
-    const int smem_max = (int)(sizeof(double) * (kChunk * kXsPitch + kChunk * kMaxExperts));
-#define MOE_ROUTER(E)                                                                        \
+    // two tokens per lane where the kernel is shared-memory bound (8 experts per warp, 3..8 warps:
+    // the staging of the 64-token x tile is sized for >= 96 threads, kMinThreads)
+    const int tpt = (ept == 8 && nw >= 3 && nw <= 8) ? 2 : 1;
+    const size_t dyn = sizeof(double) * (size_t)(kChunk * (kRouteTile * tpt + 1) + kChunk * ne_pad);
+    const int smem_max = (int)(sizeof(double) * (kChunk * (2 * kRouteTile + 1) + kChunk * kMaxExperts));
+    const int blocks = (T + kRouteTile * tpt - 1) / (kRouteTile * tpt);
+#define MOE_ROUTER(E, P)                                                                     \
     do {                                                                                     \
-        cudaError_t e_ = cudaFuncSetAttribute(router_topk_kernel<E>,                         \
+        cudaError_t e_ = cudaFuncSetAttribute(router_topk_kernel<E, P>,                      \
             cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);                          \
         if (e_ != cudaSuccess) return e_;                                                    \
-        router_topk_kernel<E><<<n_tiles, nw * 32, dyn, st>>>(x, T, h, wr, ne, k, renorm, idx, \
-                                                              gates, tile_counts);           \
+        router_topk_kernel<E, P><<<blocks, nw * 32, dyn, st>>>(x, T, h, wr, ne, k, renorm,   \
+                                                               idx, gates, tile_counts);     \
     } while (0)
-    if (ept == 1) MOE_ROUTER(1);
-    else if (ept == 2) MOE_ROUTER(2);
-    else if (ept == 4) MOE_ROUTER(4);
-    else MOE_ROUTER(8);
+    if (ept == 1) MOE_ROUTER(1, 1);
+    else if (ept == 2) MOE_ROUTER(2, 1);
+    else if (ept == 4) MOE_ROUTER(4, 1);
+    else if (tpt == 2) MOE_ROUTER(8, 2);
+    else MOE_ROUTER(8, 1);
 #undef MOE_ROUTER
     return cudaGetLastError();
 }

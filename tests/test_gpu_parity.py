@@ -350,7 +350,7 @@ def test_gemm_pair_streamk_last_wave(shape, monkeypatch):
 
 
 @pytest.mark.parametrize("ept", ["1", "2", "4", "8"])
-@pytest.mark.parametrize("ne,k", [(5, 2), (8, 2), (16, 4)])
+@pytest.mark.parametrize("ne,k", [(5, 2), (8, 2), (16, 4), (40, 6)])   # 40: 2 tokens per lane
 def test_router_experts_per_warp_variants(ne, k, ept, monkeypatch):
     """Every router_topk_kernel<EPT> instantiation (MOE_ROUTER_EPT; the default picks by N_e)
     gives the same bit-exact selection and gates (one fp64 FMA chain per logit either way)."""
