@@ -74,7 +74,7 @@ router_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
         for (int i = 0; i < EPT; ++i) acc[p][i] = 0.0;
 
     // x vectors per thread: the TPT = 2 variant runs with >= 3 warps (N_e > 16)
-    constexpr int kMinThreads = TPT == 2 ? 96 : 32;
+    constexpr int kMinThreads = TPT >= 2 ? 96 : 32;
     constexpr int kXV = (kTok * (kChunk / 8) + kMinThreads - 1) / kMinThreads;
     constexpr int kWV = (EPT * (kChunk / 8) + 31) / 32;  // router vectors per thread
     const int n_xv = kTok * (kChunk / 8);
@@ -157,8 +157,9 @@ router_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
         }
         __syncthreads();
     }
-    // logits -> shared [kTok][ne_pad] (kTok <= kChunk: fits the router tile's space)
-    double* lg = ws;
+    // logits -> shared [kTok][ne_pad]: the router tile's space when kTok <= kChunk, else the x
+    // tile's (kTok * ne_pad <= kChunk * kPitch for ne_pad <= 64, which TPT = 4 requires)
+    double* lg = kTok <= kChunk ? ws : xs;
 #pragma unroll
     for (int p = 0; p < TPT; ++p)
 #pragma unroll
@@ -455,6 +456,7 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
     const int ne_pad = nw * ept;
     // two tokens per lane where the kernel is shared-memory bound (8 experts per warp, 3..8 warps:
     // the staging of the 64-token x tile is sized for >= 96 threads, kMinThreads)
+    // (4 tokens per lane measured slower at C4: 0.84 vs 0.79 ms -- 180 registers, fewer warps)
     const int tpt = (ept == 8 && nw >= 3 && nw <= 8) ? 2 : 1;
     const size_t dyn = sizeof(double) * (size_t)(kChunk * (kRouteTile * tpt + 1) + kChunk * ne_pad);
     const int smem_max = (int)(sizeof(double) * (kChunk * (2 * kRouteTile + 1) + kChunk * kMaxExperts));
