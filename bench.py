@@ -488,6 +488,25 @@ def run_ours(args):
         os.sched_setaffinity(0, all_cpus)   # the oracle gets every host core
         cpu = cpu_baseline(full, args.cpu_seconds)
 
+    # Per-expert rows of the last call on this rank (the load histogram goes with
+    # every result; it is what makes DeepSeek-V2-Lite's grouped GEMMs uneven).
+    routing = None
+    try:
+        layer.sync()
+        dbg = layer.debug()
+
+        class _Cai:
+            def __init__(self, ptr, n):
+                self.__cuda_array_interface__ = {"data": (int(ptr), False), "shape": (n,),
+                                                 "typestr": "<i4", "version": 3}
+        rows = torch.as_tensor(_Cai(dbg.counts, nl), device=f"cuda:{local}").cpu().tolist()
+        mean = sum(rows) / max(1, len(rows))
+        routing = {"rows_per_local_expert_last_call": rows,
+                   "max_over_mean": max(rows) / mean if mean else None,
+                   "min_over_mean": min(rows) / mean if mean else None}
+    except Exception as e:  # noqa: BLE001 -- diagnostics only
+        routing = {"error": str(e)}
+
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
@@ -508,7 +527,7 @@ def run_ours(args):
             "gpu_launches_per_step": launches / args.steps,
             "ms_per_step_dist_rank0": step_dist,
             "single_call_latency_ms": latency_ms,
-            "host_affinity": affinity}
+            "host_affinity": affinity, "routing_rank0": routing}
     if rank == 0:
         print(json.dumps(line), flush=True)
     layer.sync()
