@@ -142,10 +142,22 @@ def cpu_baseline(inp, seconds: float) -> dict:
         rounds += 1
         if elapsed < seconds / 8:
             n *= 2
+    # one host thread on a small sample: the scaling of the oracle itself
+    one = None
+    try:
+        oracle.set_num_threads(1)
+        n1 = min(8, inp.x.shape[0])
+        t0 = time.perf_counter()
+        oracle.forward(inp.x[:n1], inp.router, inp.w1, inp.w3, inp.w2, cfg.top_k, cfg.num_shared)
+        dt = time.perf_counter() - t0
+        one = {"value": n1 / dt, "unit": "tokens/s", "cores": 1,
+               "sample": f"{n1} tokens of the {cfg.name} layer, 1 OpenMP thread ({dt:.2f} s)"}
+    finally:
+        oracle.set_num_threads(cores)
     return {"value": done / elapsed, "unit": "tokens/s", "cores": cores, "kind": "oracle",
             "sample": f"{done} of {cfg.tokens} tokens of the {cfg.name} layer ({rounds} calls, "
                       f"{elapsed:.1f} s, fp64 router + fp32 experts, OpenMP)",
-            "host": host_cpu_info()}
+            "one_thread": one, "host": host_cpu_info()}
 
 
 def host_cpu_info() -> dict:

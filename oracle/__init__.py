@@ -54,6 +54,7 @@ def _load():
         lib.moe_ref_forward.argtypes = [P, i64, i32, P, i32, i32, i32, P, P, P, i32, i32, P, P, P, P]
         lib.moe_ref_forward.restype = ctypes.c_int
         lib.moe_ref_num_threads.restype = ctypes.c_int
+        lib.moe_ref_set_num_threads.argtypes = [ctypes.c_int]
         _lib = lib
     return _lib
 
@@ -70,6 +71,11 @@ def _u16(a) -> np.ndarray:
 
 def num_threads() -> int:
     return _load().moe_ref_num_threads()
+
+
+def set_num_threads(n: int) -> None:
+    """OpenMP threads of the following oracle calls (timing only; results do not depend on it)."""
+    _load().moe_ref_set_num_threads(int(n))
 
 
 def router_logits(x: np.ndarray, router: np.ndarray) -> np.ndarray:

@@ -44,6 +44,16 @@ int moe_ref_num_threads(void) {
 #endif
 }
 
+/* Thread count of the following calls (bench.py's one-thread baseline); the
+ * arithmetic is per output element and does not depend on it. */
+void moe_ref_set_num_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 /* Step 1: router logits, fp64 accumulation in ascending c.  logits: [T, n_experts]. */
 void moe_ref_router_logits(const uint16_t* x, int64_t T, int32_t h, const uint16_t* router,
                            int32_t n_experts, double* logits) {
