@@ -422,9 +422,10 @@ def run_ours(args):
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(cfg.name, {}).get("gemm1_dram_bytes_per_launch")
     # Peak: the BURST cuBLAS figure.  The kernel runs inside a long step, but the step is
-    # host-link bound and the GPU idles between expert GEMMs, so it runs at full boost clock
-    # (see `clocks`), not at the power-capped clock of the sustained figure; the burst peak is
-    # the conservative denominator here.  The sustained-peak fraction is reported beside it.
+    # host-link bound and the GPU idles between expert GEMMs (~0.2-ms bursts, nvidia-smi sees
+    # boost clock, `clocks`), so the burst peak is the conservative denominator; the sustained-peak
+    # fraction is reported beside it, and so is the SM clock measured INSIDE the kernel (power
+    # management still lowers it during the burst: ~1.5 GHz, `sm_mhz_in_kernel`).
     roofline = {"kernel": "expert GEMM1 + fused SwiGLU (a5): tcgen05 expert_gemm_pair_kernel / "
                           "expert_gemm_kernel<256,0>, chosen per launch by the wave model",
                 "bound": "tensor",
@@ -495,10 +496,9 @@ def run_ours(args):
         e2e["matches_device_path"] = bool(allmax(0.0 if torch.equal(oh[last].cuda(), outs[last]) else 1.0) == 0.0)
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
-        full = synth.gen_inputs(cfg, layer=0) if world > 1 else layers[0]
+    if rank == 0 and world == 1 and not args.no_cpu:   # the oracle baseline: N = 1 only
         os.sched_setaffinity(0, all_cpus)   # the oracle gets every host core
-        cpu = cpu_baseline(full, args.cpu_seconds)
+        cpu = cpu_baseline(layers[0], args.cpu_seconds)
 
     # Per-expert rows of the last call on this rank (the load histogram goes with
     # every result; it is what makes DeepSeek-V2-Lite's grouped GEMMs uneven).
