@@ -93,3 +93,19 @@ def test_config_validation_without_gpu(lib, kw, status):
 def test_status_strings(lib):
     for s in range(8):
         assert moe.status_string(s).startswith("MOE_")
+
+
+def test_header_compiles_as_plain_c99(tmp_path):
+    """include/moe.h is a C ABI: it must compile as C99 with no C++ or CUDA types."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        import pytest
+        pytest.skip("no gcc")
+    src = tmp_path / "t.c"
+    src.write_text('#include "moe.h"\nint main(void) { moe_stats s; moe_config c; (void)s; (void)c;'
+                   ' return (int)MOE_FLAG_MOVER + (int)MOE_OK; }\n')
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-Werror", "-pedantic",
+                        "-fsyntax-only", "-I", inc, str(src)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
