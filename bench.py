@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--config", default="mixtral_8x7b")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--layers", type=int, default=2)
+    ap.add_argument("--tokens", type=int, default=0,
+                    help="override the config's token count (e.g. 131072 = 2 x n_real at C1: the "
+                         "compute-bound regime of the paper's profiler, PAPER.md:608-615)")
     ap.add_argument("--packet-mb", type=float, default=0.0)
     ap.add_argument("--mover", action="store_true",
                     help="expert copies through the library's data-mover thread (MOE_FLAG_MOVER)")
@@ -245,6 +248,8 @@ def run_ours(args):
         dist.barrier()
     peaks = load_peaks()
     cfg = synth.CONFIGS[args.config]
+    if args.tokens:
+        cfg = cfg.with_tokens(args.tokens)
     T = cfg.tokens                      # global tokens per step (strong scaling over ranks)
     if T % world or cfg.num_experts % world:
         raise SystemExit(f"{cfg.name}: tokens/experts do not split over {world} ranks")

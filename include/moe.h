@@ -276,11 +276,15 @@ int64_t moe_ep_plan(int32_t world, int32_t rank, int32_t num_experts, const int3
                     int32_t* grp_off);
 
 /* MOE_FLAG_IPC_EP bootstrap.  moe_ep_ipc_handle writes this rank's MOE_IPC_HANDLE_BYTES-byte
- * blob (CUDA IPC handles of its receive buffers, counts and flags); the caller all-gathers the
- * blobs of all ranks (rank order) and passes them to moe_ep_ipc_connect, which maps the peers'
- * buffers (cudaIpcOpenMemHandle, peer access enabled lazily).  MOE_E_STATE if the context is
- * not an IPC_EP context or is already connected. */
-#define MOE_IPC_HANDLE_BYTES 256
+ * blob (CUDA IPC handles of its receive buffers, counts and flags, then its layer shape and
+ * max_tokens); the caller all-gathers the blobs of all ranks (rank order) and passes them to
+ * moe_ep_ipc_connect, which checks that every rank runs the same layer shape and max_tokens
+ * (MOE_E_INVAL otherwise: the receive buffers are sized W x max_tokens x top_k rows) and maps
+ * the peers' buffers (cudaIpcOpenMemHandle, peer access enabled lazily).  MOE_E_STATE if the
+ * context is not an IPC_EP context or is already connected.  If a call nevertheless routes more
+ * rows to an owner than it can hold, nothing is exchanged and moe_sync / the next call return
+ * MOE_E_STATE. */
+#define MOE_IPC_HANDLE_BYTES 512
 moe_status moe_ep_ipc_handle(moe_ctx ctx, void* out);
 moe_status moe_ep_ipc_connect(moe_ctx ctx, const void* all_handles);
 /* Collective check of a connected IPC_EP group (call on every rank): each rank writes a tagged

@@ -39,7 +39,7 @@ EXPORTED = ["moe_packed_expert_bytes", "moe_pack_expert", "moe_host_alloc", "moe
             "moe_ep_ipc_selftest"]
 MOE_FLAG_IPC_EP = 8
 MOE_FLAG_MOVER = 16
-MOE_IPC_HANDLE_BYTES = 256
+MOE_IPC_HANDLE_BYTES = 512
 
 
 class moe_config(ctypes.Structure):

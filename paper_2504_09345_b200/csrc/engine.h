@@ -80,9 +80,14 @@ struct moe_ctx_s {
     // DMA coalescing: consecutive streamed items whose host blobs are contiguous and whose slots
     // are adjacent are moved by one cudaMemcpyAsync of up to copy_group experts.
     int copy_group = 1;
+    // Routed experts per GEMM launch: up to gemm_group_max (half the slots) consecutive experts
+    // until the launch expects gemm_rows_target rows (MOE_GEMM_ROWS overrides; forward_impl).
+    int gemm_group_max = 1;
+    int64_t gemm_rows_target = 2048;
     int pend_n = 0;                     // items in the pending batch
     uint64_t pend_q0 = 0;               // streamed-item index of the batch's first item
     const char* pend_src = nullptr;     // host address of the batch's first blob
+    uintptr_t pend_base = 0;            // start of that blob's pinned allocation
     cudaEvent_t ready13[moe::kMaxSlots] = {}, ready2[moe::kMaxSlots] = {};
     cudaEvent_t slot_free[moe::kMaxSlots] = {};
     uint64_t seq = 0;  // streamed-item counter across calls: item q uses slot q % nslots
@@ -95,29 +100,12 @@ struct moe_ctx_s {
     // GEMM launch can cover experts in different slots (GemmBatch::b_row).
     CUtensorMap tm_w13, tm_w2;
     CUtensorMap tm_w13_pair, tm_w2_pair;   // 128-row boxes (CTA-pair GEMM)
-    moe::PairBMaps tm_w13_alt, tm_w2_alt;  // 112 / 96-row boxes (224 / 192-wide pair tiles)
     // DMA batches (flush_copies): slot s holds item batch_q0[s] + j of a batch of batch_n[s]
     uint64_t batch_q0[moe::kMaxSlots] = {};
     int batch_n[moe::kMaxSlots] = {};
     // MOE_GEMM_PAIR: 0 never, 1 always, -1 auto (default): the host's wave model on the
-    // EXPECTED group sizes, one launch; 2 ("device"): both kernels are launched and the device
-    // picks by the wave model on the ACTUAL group sizes (GemmBatch::select; measured slower
-    // in-bench: the losing launch costs ~10 us).
+    // EXPECTED group sizes picks the CTA-pair or the single-CTA kernel, one launch (pick_pair).
     int pair_mode = -1;
-    // Tail split (MOE_GEMM_TAILSPLIT=1, experiment, default off): a CTA-pair GEMM covers only
-    // whole 256-row tiles of each group; the < 256-row remainder runs as 128-row tiles in a
-    // concurrent launch on tail_stream (forked / joined with events).  Measured slower at C1
-    // (GEMM1 1.61 -> 1.74 ms/step) and C4, +2% at C3: the tail CTAs do not just fill the pair
-    // kernel's idle last wave.
-    bool tail_split = false;
-    bool alt_tiles = false;   // MOE_GEMM_ALT=1: pair kernel may pick 224/192-wide tiles
-    // MOE_GEMM_STREAMK: the pair kernel's partial last wave as K-chunks (GemmBatch::streamk);
-    // sk_ws = num_sms/2 chunks x 256 KB of fp32 partials, sk_flags = [num_sms/2][2] counters.
-    bool streamk_default = false;
-    float* sk_ws = nullptr;
-    int* sk_flags = nullptr;
-    cudaStream_t tail_stream = nullptr;
-    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
 
     // workspace
     int32_t* idx_ws = nullptr;
@@ -134,12 +122,6 @@ struct moe_ctx_s {
     __nv_bfloat16* h_act = nullptr;
     __nv_bfloat16* y_perm = nullptr;
     CUtensorMap tm_xperm, tm_h;
-    moe::TokenMaps tm_xperm_t, tm_h_t;  // token operands of the swap-AB GEMM
-    int swap_mode = 0;                  // MOE_GEMM_SWAP: 0 never, 1 always
-    // MOE_GEMM_TAILSWAP: pair-kernel groups end in a swap-AB tail tile when the last partial
-    // tile has <= 128 rows; MOE_GEMM_TAILCOST: its scheduling cost in full-tile units.
-    bool tail_swap = false;   // measured: no gain
-    float tail_cost = 0.6f;
     int64_t last_rows = 0;
 
     // expert parallelism (world_size > 1, or MOE_FLAG_FORCE_EP)
@@ -155,7 +137,6 @@ struct moe_ctx_s {
     __nv_bfloat16* x_recv = nullptr;
     __nv_bfloat16* y_recv = nullptr;
     CUtensorMap tm_xrecv;
-    moe::TokenMaps tm_xrecv_t;
     std::vector<int32_t> send_off, send_cnt, recv_off, recv_cnt, grp_off;
     int64_t last_recv_rows = 0, comm_bytes = 0;
     // P2P transport (MOE_FLAG_LOCAL_EP: ranks in this process; MOE_FLAG_IPC_EP: ranks in other
@@ -186,10 +167,10 @@ struct moe_ctx_s {
     // moe_packed_layer_bytes) are streamed like the experts, into two slots of their own, on the
     // same copy stream just ahead of the call's expert weights.
     int64_t layer_bytes = 0;
+    bool taskb_ready = false;         // every Task B resource below allocated and mapped
     char* lw_slot[2] = {nullptr, nullptr};
     cudaEvent_t lw_ready[2] = {}, lw_free[2] = {};
     CUtensorMap tm_wo[2], tm_wo_pair[2];
-    moe::PairBMaps tm_wo_alt[2];
     uint64_t lw_seq = 0;
     __nv_bfloat16* h1_ws = nullptr;   // [max_tokens, h] residual stream after the O-projection
     __nv_bfloat16* u_ws = nullptr;    // [max_tokens, h] normalised MoE input
@@ -207,8 +188,7 @@ struct moe_ctx_s {
     std::vector<cudaEvent_t> ev_pool;
     moe_stats stats{};
 
-    std::unordered_set<const void*> pinned_ok;
-    std::unordered_map<const void*, uintptr_t> alloc_base;  // host blob -> start of its allocation
+    std::vector<uintptr_t> call_base;   // this call's expert blobs -> start of their allocation
     std::string last_error;
     moe_status sticky = MOE_OK;
 };
@@ -272,6 +252,12 @@ moe_status mover_mark_free(moe_ctx c, cudaStream_t st, uint64_t value);
 double mover_take_h2d_ms(moe_ctx c, int64_t* packets);
 
 // expert parallelism (ep.cu)
+// Layer shape a rank publishes in its IPC blob (after the 4 memory handles); connect checks that
+// every rank's matches its own.
+struct IpcShape {
+    int32_t magic, rank, world, hidden, ffn, num_experts, top_k, num_shared, max_tokens, pad;
+};
+IpcShape ipc_shape(moe_ctx c);
 moe_status ep_init(moe_ctx c);
 void ep_destroy(moe_ctx c);
 // After routing/permute on `st`: exchange counts (host sync), build the plan, dispatch x_perm

@@ -114,8 +114,7 @@ moe_status ep_init(moe_ctx c) {
         cudaGetLastError();
         return set_err(c, MOE_E_NOMEM, "EP buffers");
     }
-    if (!make_tmap(&c->tm_xrecv, c->x_recv, (uint64_t)c->cap_recv, cf.hidden, 128) ||
-        !make_token_maps(&c->tm_xrecv_t, c->x_recv, (uint64_t)c->cap_recv, cf.hidden))
+    if (!make_tmap(&c->tm_xrecv, c->x_recv, (uint64_t)c->cap_recv, cf.hidden, 128))
         return set_err(c, MOE_E_CUDA, "tensor map x_recv");
     const int np = W * c->n_local;
     c->send_off.assign(np, 0);
@@ -165,6 +164,15 @@ moe_status ep_init(moe_ctx c) {
             g->ranks.assign(W, nullptr);
         }
         if (g->world != W || g->ranks[cf.rank]) return set_err(c, MOE_E_INVAL, "LOCAL_EP group mismatch");
+        for (moe_ctx p : g->ranks) {   // the exchange assumes one layer shape on every rank
+            if (!p) continue;
+            const moe_config& o = p->cfg;
+            if (o.hidden != cf.hidden || o.ffn != cf.ffn || o.num_experts != cf.num_experts ||
+                o.top_k != cf.top_k || o.num_shared != cf.num_shared ||
+                o.max_tokens != cf.max_tokens)
+                return set_err(c, MOE_E_INVAL, "LOCAL_EP rank %d: layer shape / max_tokens differ "
+                               "from rank %d's", cf.rank, o.rank);
+        }
         g->ranks[cf.rank] = c;
         c->local_group = g.get();
         return MOE_OK;
@@ -323,6 +331,12 @@ moe_status ep_combine(moe_ctx c, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------------------- P2P transport
+IpcShape ipc_shape(moe_ctx c) {
+    const moe_config& cf = c->cfg;
+    return IpcShape{0x4D6F4533, cf.rank, cf.world_size, cf.hidden, cf.ffn, cf.num_experts,
+                    cf.top_k, cf.num_shared, cf.max_tokens, 0};
+}
+
 namespace {
 
 // This rank's device tables, filled from the peers' buffers as mapped in this process.
@@ -361,6 +375,16 @@ moe_status p2p_connect_local(moe_ctx c, cudaStream_t st) {
         for (int d = 0; d < W; ++d) {
             const moe_ctx p = g->ranks[d];
             if (!p) return set_err(c, MOE_E_STATE, "LOCAL_EP rank %d missing", d);
+            if (p->cfg.device != c->cfg.device) {   // ranks on different GPUs of the box
+                int can = 0;
+                MOE_CUDA(c, cudaDeviceCanAccessPeer(&can, c->cfg.device, p->cfg.device));
+                if (!can)
+                    return set_err(c, MOE_E_UNSUPPORTED, "LOCAL_EP: device %d cannot access "
+                                   "peer device %d", c->cfg.device, p->cfg.device);
+                const cudaError_t e = cudaDeviceEnablePeerAccess(p->cfg.device, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else MOE_CUDA(c, e);
+            }
             flags[d] = p->p2p_flags;
             counts[d] = p->p2p_counts;
             xr[d] = p->x_recv;
@@ -427,7 +451,7 @@ moe_status p2p_before_dispatch(moe_ctx c, int T, cudaStream_t st) {
     P2P_TRY(p2p_wait(c, kFlagCounts, seq, st));
     MOE_CUDA(c, launch_p2p_plan(c->p2p_counts + (size_t)par * W * ne, W, ne, me, T, cf.top_k,
                                 cf.num_shared, c->cap_recv, c->n_all, cf.hidden, c->ep_grp,
-                                c->pr_x, c->pr_y, c->p2p_rows, c->p2p_bytes, st));
+                                c->pr_x, c->pr_y, c->p2p_rows, c->p2p_bytes, c->p2p_diag_d, st));
     P2P_TRY(p2p_wait(c, kFlagXFree, seq - 1, st));
     return MOE_OK;
 }
@@ -503,7 +527,8 @@ moe_status moe_ep_ipc_handle(moe_ctx c, void* out) {
     if (!c->p2p || c->local_ep) return moe::set_err(c, MOE_E_STATE, "not an IPC_EP context");
     MOE_CUDA(c, cudaSetDevice(c->cfg.device));
     void* bufs[4] = {c->x_recv, c->y_recv, c->p2p_counts, c->p2p_flags};
-    static_assert(4 * sizeof(cudaIpcMemHandle_t) <= MOE_IPC_HANDLE_BYTES, "IPC blob size");
+    static_assert(4 * sizeof(cudaIpcMemHandle_t) + sizeof(moe::IpcShape) <= MOE_IPC_HANDLE_BYTES,
+                  "IPC blob size");
     char* o = static_cast<char*>(out);
     memset(o, 0, MOE_IPC_HANDLE_BYTES);
     for (int i = 0; i < 4; ++i) {
@@ -511,6 +536,8 @@ moe_status moe_ep_ipc_handle(moe_ctx c, void* out) {
         MOE_CUDA(c, cudaIpcGetMemHandle(&hnd, bufs[i]));
         memcpy(o + i * sizeof hnd, &hnd, sizeof hnd);
     }
+    const moe::IpcShape sh = moe::ipc_shape(c);
+    memcpy(o + 4 * sizeof(cudaIpcMemHandle_t), &sh, sizeof sh);
     return MOE_OK;
 }
 
@@ -520,6 +547,21 @@ moe_status moe_ep_ipc_connect(moe_ctx c, const void* all) {
         return moe::set_err(c, MOE_E_STATE, "not an unconnected IPC_EP context");
     MOE_CUDA(c, cudaSetDevice(c->cfg.device));
     const int W = c->cfg.world_size, me = c->cfg.rank;
+    // every rank must run the same layer shape and capacity (the receive buffers are sized for
+    // W x max_tokens x top_k rows), in rank order
+    const moe::IpcShape mine = moe::ipc_shape(c);
+    for (int d = 0; d < W; ++d) {
+        moe::IpcShape o;
+        memcpy(&o, static_cast<const char*>(all) + (size_t)d * MOE_IPC_HANDLE_BYTES +
+                       4 * sizeof(cudaIpcMemHandle_t), sizeof o);
+        moe::IpcShape want = mine;
+        want.rank = d;
+        if (memcmp(&o, &want, sizeof o) != 0)
+            return moe::set_err(c, MOE_E_INVAL, "IPC_EP: rank %d's blob (magic %x, rank %d, W %d, "
+                                "h %d, h_i %d, N_e %d, k %d, S %d, max_tokens %d) does not match "
+                                "this rank's layer", d, o.magic, o.rank, o.world, o.hidden, o.ffn,
+                                o.num_experts, o.top_k, o.num_shared, o.max_tokens);
+    }
     unsigned long long* flags[moe::kMaxRanks];
     int32_t* counts[moe::kMaxRanks];
     __nv_bfloat16 *xr[moe::kMaxRanks], *yr[moe::kMaxRanks];

@@ -79,8 +79,25 @@ __global__ void p2p_plan_kernel(const int32_t* __restrict__ counts, int W, int n
                                 int k, int S, long long cap_recv, int n_all, int h,
                                 GemmGroup* __restrict__ grp, PeerRows* __restrict__ pr_x,
                                 PeerRows* __restrict__ pr_y, int32_t* __restrict__ rows_out,
-                                long long* __restrict__ bytes_acc) {
+                                long long* __restrict__ bytes_acc,
+                                long long* __restrict__ diag) {
     const int nl = ne / W;
+    // Every owner must be able to hold the rows routed to it: each rank checks every owner's
+    // total (the counts are the same on every rank, so all ranks agree).  With consistent
+    // configurations (max_tokens, top_k equal on all ranks; checked at connect) this cannot
+    // fail; if it does, nothing is dispatched (send bases -1, empty groups) instead of writing
+    // past a peer's buffer, and moe_sync reports the overflow.
+    __shared__ long long worst;
+    if (threadIdx.x == 0) worst = 0;
+    __syncthreads();
+    for (int d = threadIdx.x; d < W; d += blockDim.x) {
+        long long tot = 0;
+        for (int q = 0; q < W; ++q)
+            for (int l = 0; l < nl; ++l) tot += counts[(size_t)q * ne + d * nl + l];
+        atomicMax(&worst, tot);
+    }
+    __syncthreads();
+    const bool overflow = worst > cap_recv;
     // send bases: where this rank's block for expert e = d*nl + le starts in owner d's x_recv
     for (int e = threadIdx.x; e < ne; e += blockDim.x) {
         const int d = e / nl, le = e % nl;
@@ -88,15 +105,23 @@ __global__ void p2p_plan_kernel(const int32_t* __restrict__ counts, int W, int n
         for (int l = 0; l < le; ++l)
             for (int q = 0; q < W; ++q) b += counts[(size_t)q * ne + d * nl + l];
         for (int q = 0; q < me; ++q) b += counts[(size_t)q * ne + e];
-        pr_x->base[e] = (int32_t)b;
-        pr_y->base[e] = (int32_t)b;
+        pr_x->base[e] = overflow ? -1 : (int32_t)b;
+        pr_y->base[e] = overflow ? -1 : (int32_t)b;
     }
     if (threadIdx.x == 0) {
+        if (overflow && diag) {   // host-mapped: reported by moe_sync / the next call
+            diag[6] = worst;
+            diag[7] = cap_recv;
+            __threadfence_system();
+            diag[5] = 1;
+            __threadfence_system();
+        }
         // receive side: expert-major groups (local expert, source rank, source token order)
         int off = 0;
         for (int le = 0; le < nl; ++le) {
             int cnt = 0;
             for (int q = 0; q < W; ++q) cnt += counts[(size_t)q * ne + me * nl + le];
+            if (overflow) cnt = 0;
             grp[le] = GemmGroup{off, off + cnt, off, 0};
             grp[n_all + le] = grp[le];
             off += cnt;
@@ -109,7 +134,7 @@ __global__ void p2p_plan_kernel(const int32_t* __restrict__ counts, int W, int n
         }
         long long sent = 0;
         for (int e = 0; e < ne; ++e) sent += counts[(size_t)me * ne + e];
-        *bytes_acc += 2 * sent * h * 2;   // rows written to the owners + read back in the combine
+        if (!overflow) *bytes_acc += 2 * sent * h * 2;   // rows written to the owners + read back in the combine
     }
 }
 
@@ -181,9 +206,9 @@ cudaError_t launch_p2p_wait(const unsigned long long* flags, int W, int which,
 cudaError_t launch_p2p_plan(const int32_t* counts_par, int W, int ne, int me, int T, int k,
                             int S, long long cap_recv, int n_all, int h, GemmGroup* grp,
                             PeerRows* pr_x, PeerRows* pr_y, int32_t* rows_out,
-                            long long* bytes_acc, cudaStream_t st) {
+                            long long* bytes_acc, long long* diag, cudaStream_t st) {
     p2p_plan_kernel<<<1, 128, 0, st>>>(counts_par, W, ne, me, T, k, S, cap_recv, n_all, h, grp,
-                                       pr_x, pr_y, rows_out, bytes_acc);
+                                       pr_x, pr_y, rows_out, bytes_acc, diag);
     return cudaGetLastError();
 }
 

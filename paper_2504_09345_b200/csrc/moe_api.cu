@@ -60,12 +60,6 @@ bool make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, u
     return r == CUDA_SUCCESS;
 }
 
-bool make_token_maps(TokenMaps* t, const void* base, uint64_t rows, uint64_t cols) {
-    for (int i = 0; i < 4; ++i)
-        if (!make_tmap(&t->box[i], base, rows, cols, 128u >> i)) return false;
-    return true;
-}
-
 moe_status set_err(moe_ctx c, moe_status s, const char* fmt, ...) {
     if (c) {
         char buf[512];
@@ -94,12 +88,6 @@ cudaEvent_t pool_get(moe_ctx c) {
 namespace {
 
 using moe::set_err;
-
-// B maps of the CTA-pair kernel's 224- and 192-wide tiles (per-CTA boxes of 112 / 96 rows).
-bool make_alt_maps(moe::PairBMaps* a, const void* base, uint64_t rows, uint64_t cols) {
-    return moe::make_tmap(&a->b224, base, rows, cols, 112) &&
-           moe::make_tmap(&a->b192, base, rows, cols, 96);
-}
 
 moe_status check_cfg(const moe_config* cfg) {
     if (!cfg) return MOE_E_INVAL;
@@ -147,19 +135,15 @@ uintptr_t alloc_start(const void* p) {
     return (uintptr_t)start;
 }
 
-bool is_pinned(moe_ctx c, const void* p) {
-    if (c->pinned_ok.count(p)) return true;
+// Page-locked host memory?  Checked on every call, not cached: a caller may free a blob and get
+// new (possibly pageable) memory at the same address.
+bool is_pinned(const void* p) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
-    if (a.type == cudaMemoryTypeHost) {
-        c->pinned_ok.insert(p);
-        c->alloc_base[p] = alloc_start(p);
-        return true;
-    }
-    return false;
+    return a.type == cudaMemoryTypeHost;
 }
 
 bool is_device(const void* p) {
@@ -248,7 +232,7 @@ moe_status request_copy(moe_ctx c, const void* const* experts, int i, uint64_t q
     const char* src = static_cast<const char*>(experts[i]);
     const int s = (int)(q % (uint64_t)c->nslots);
     if (c->pend_n > 0) {
-        const uintptr_t a0 = c->alloc_base[c->pend_src], a1 = c->alloc_base[src];
+        const uintptr_t a0 = c->pend_base, a1 = c->call_base[i];
         const bool contiguous = src == c->pend_src + (int64_t)c->pend_n * c->blob_bytes &&
                                 q == c->pend_q0 + (uint64_t)c->pend_n && s != 0 && a0 != 0 &&
                                 a0 == a1;
@@ -260,87 +244,42 @@ moe_status request_copy(moe_ctx c, const void* const* experts, int i, uint64_t q
     if (c->pend_n == 0) {
         c->pend_q0 = q;
         c->pend_src = src;
+        c->pend_base = c->call_base[i];
     }
     ++c->pend_n;
     if (c->pend_n >= c->copy_group) return flush_copies(c);
     return MOE_OK;
 }
 
-// Tile shape of one GEMM launch of `rows` expected rows and N output columns: the CTA-pair kernel
-// (256x256 tiles on SM pairs, ~97% tensor-pipe activity) or the single-CTA kernel (128x256, ~76%:
-// shared-memory bandwidth bound, but half the M granularity and twice the concurrent tiles),
-// by a wave model: time ~ ceil(tiles / concurrent tiles) / tensor efficiency.
-// (rows: the expected rows of each of the launch's n groups; their tiles share the waves.)
-// swap-AB tail tiles in the pair kernel (not combined with the tail-split experiment)
-bool tail_swap_on(moe_ctx c) { return c->tail_swap && !c->tail_split; }
-
-bool pick_pair(moe_ctx c, const int64_t* rows, int n, int bn, int N, int K) {
-    if (bn != 256 || c->pair_mode == 0) return false;
-    if (c->pair_mode != -1) return true;   // 1: always; 2: the device decides (GemmBatch::select)
+// Tile shape of one GEMM launch: the CTA-pair kernel (256x256 tiles on SM pairs, ~97% tensor-pipe
+// activity) or the single-CTA kernel (128 x bn tiles, ~76%: shared-memory bandwidth bound, but
+// half the M granularity and twice the concurrent tiles), by a wave model on the EXPECTED rows of
+// each of the launch's n groups: time ~ ceil(tiles / concurrent tiles) x tile width / efficiency.
+bool pick_pair(moe_ctx c, const int64_t* rows, int n, int bn, int N) {
+    if (bn != 256 || N % 256 || c->pair_mode == 0) return false;
+    if (c->pair_mode == 1) return true;
     const int sms = c->num_sms;
-    const int64_t nt = N / 256;
-    int64_t t1 = 0;
-    for (int i = 0; i < n; ++i)
-        if (rows[i] > 0) t1 += ((rows[i] + 127) / 128) * nt;
+    int64_t t1 = 0, t2 = 0;
+    for (int i = 0; i < n; ++i) {
+        if (rows[i] <= 0) continue;
+        t1 += ((rows[i] + 127) / 128) * (N / bn);
+        t2 += ((rows[i] + 255) / 256) * (N / 256);
+    }
     if (t1 == 0) return false;
     const double w1 = (double)((t1 + sms - 1) / sms) / 0.76;
-    const double w2 = moe::pair_makespan(rows, n, (int)nt, sms / 2, tail_swap_on(c), c->tail_cost,
-                                         c->sk_ws != nullptr, K / 64) / 0.97;
+    const double w2 = (double)((t2 + sms / 2 - 1) / (sms / 2)) / 0.97;
     return w2 < w1;
 }
 
-// One expert-GEMM step over a batch of groups on `st`.
-//  * device selection (MOE_GEMM_PAIR=device) and the pair kernel possible: the CTA-pair kernel
-//    and the single-CTA kernel are both launched; each evaluates plan_tiles on the actual group
-//    sizes and the loser exits at once (GemmBatch::select) -- the tile shape follows the real
-//    routing without a host sync (but the extra launch costs ~10 us; off by default).
-//  * tail split (experiment): the pair kernel covers the whole 256-row tiles and the single-CTA
-//    kernel the < 256-row remainders, concurrently on tail_stream (fork/join events).
-//  * otherwise one launch of the kernel `pair` names (swap-AB tail tiles if tail_swap is on).
-moe_status launch_grouped(moe_ctx c, int mode, int bn, bool pair, const CUtensorMap* tmA,
-                          const CUtensorMap* tmB, const CUtensorMap* tmB_pair,
-                          const moe::PairBMaps* alt, const moe::TokenMaps* tmT,
-                          moe::GemmBatch batch, int N, int K, __nv_bfloat16* out, int ldo,
-                          cudaStream_t st, const __nv_bfloat16* resid = nullptr) {
-    const int grid = c->num_sms;
-    if (!c->alt_tiles) alt = nullptr;
-    batch.bn_single = bn;
-    batch.alt_ok = alt ? 1 : 0;
-    if (c->sk_ws && !c->tail_split) {   // stream-K last wave (pair kernel only)
-        batch.streamk = 1;
-        batch.sk_ws = c->sk_ws;
-        batch.sk_flags = c->sk_flags;
-    }
-    if (pair && c->pair_mode == 2 && !c->tail_split) {
-        batch.select = grid;
-        batch.tail_swap = tail_swap_on(c) ? 1 : 0;
-        batch.tail_cost = c->tail_cost;
-        MOE_CUDA(c, moe::launch_expert_gemm(mode, bn, true, tmA, tmB_pair, batch, N, K, out, ldo,
-                                            resid, grid, st, tmT, alt));
-        batch.tail_swap = 0;
-        MOE_CUDA(c, moe::launch_expert_gemm(mode, bn, false, tmA, tmB, batch, N, K, out, ldo,
-                                            resid, grid, st));
-        c->stats.kernel_launches += 1;
-        return MOE_OK;
-    }
-    if (!pair || !c->tail_split) {
-        batch.tail_swap = pair && tail_swap_on(c) ? 1 : 0;
-        batch.tail_cost = c->tail_cost;
-        MOE_CUDA(c, moe::launch_expert_gemm(mode, bn, pair, tmA, pair ? tmB_pair : tmB, batch, N,
-                                            K, out, ldo, resid, grid, st, tmT, alt));
-        return MOE_OK;
-    }
-    MOE_CUDA(c, cudaEventRecord(c->fork_ev, st));
-    batch.part = 1;
-    MOE_CUDA(c, moe::launch_expert_gemm(mode, bn, true, tmA, tmB_pair, batch, N, K, out, ldo,
-                                        resid, grid, st, nullptr, alt));
-    batch.part = 2;
-    MOE_CUDA(c, cudaStreamWaitEvent(c->tail_stream, c->fork_ev, 0));
-    MOE_CUDA(c, moe::launch_expert_gemm(mode, bn, false, tmA, tmB, batch, N, K, out, ldo,
-                                        resid, grid, c->tail_stream));
-    MOE_CUDA(c, cudaEventRecord(c->join_ev, c->tail_stream));
-    MOE_CUDA(c, cudaStreamWaitEvent(st, c->join_ev, 0));
-    c->stats.kernel_launches += 1;
+// One expert-GEMM launch over a batch of groups on `st` (pair: tmB_pair, else tmB).
+moe_status launch_grouped(moe_ctx c, int mode, int bn, const int64_t* rows,
+                          const CUtensorMap* tmA, const CUtensorMap* tmB,
+                          const CUtensorMap* tmB_pair, const moe::GemmBatch& batch, int N, int K,
+                          __nv_bfloat16* out, int ldo, cudaStream_t st,
+                          const __nv_bfloat16* resid = nullptr) {
+    const bool pair = pick_pair(c, rows, batch.n, bn, N);
+    MOE_CUDA(c, moe::launch_expert_gemm(mode, bn, pair, tmA, pair ? tmB_pair : tmB, batch, N, K,
+                                        out, ldo, resid, c->num_sms, st));
     return MOE_OK;
 }
 
@@ -356,18 +295,16 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     float* gates = topk_w ? topk_w : c->gates_ws;
     const uint64_t q0 = c->seq;
 
-    // With the mover, the slot counters assume one compute order: a call on another stream
-    // than the previous one first waits for it (a no-op on the same stream).
-    if (c->mover) MOE_CUDA(c, cudaStreamWaitEvent(st, c->done_ev, 0));
+    // Calls share the context's workspace (routing tables, x_perm, h_act, y_perm, the host-mode
+    // token buffers) and, with the mover, one compute order of the slot counters: a call on
+    // another stream than the previous one first waits for it (a no-op on the same stream).
+    MOE_CUDA(c, cudaStreamWaitEvent(st, c->done_ev, 0));
 
     // A operand of the shared experts is the hidden batch itself (per-call tensor map).
     // (T == 0 only happens under EP: the rank serves other ranks' tokens; its shared-expert
     // groups are then empty and never touch the map.)
     CUtensorMap tm_x = c->tm_xperm;
-    moe::TokenMaps tm_x_t = c->tm_xperm_t;
-    if (S > 0 && T > 0 &&
-        (!moe::make_tmap(&tm_x, hidden, (uint64_t)T, (uint64_t)h, 128) ||
-         !moe::make_token_maps(&tm_x_t, hidden, (uint64_t)T, (uint64_t)h)))
+    if (S > 0 && T > 0 && !moe::make_tmap(&tm_x, hidden, (uint64_t)T, (uint64_t)h, 128))
         return set_err(c, MOE_E_CUDA, "cuTensorMapEncodeTiled failed for hidden");
 
     // Streaming order: shared experts first (their GEMMs need only the hidden batch, and they are
@@ -388,28 +325,34 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     // so many small experts no longer pay one partial last wave each.  A batch never mixes
     // shared and routed experts (different A operands and outputs).  Items [i0, i1), group
     // tables g1 (GEMM1) / g2 (GEMM2) indexed by expert_of(i).
-    const int grid = c->num_sms;
     // The host does not know the group sizes (they live on the device), so the tile shape is
     // chosen on the expected size: T*k*W/N_e rows per routed expert (+10% for routing
     // variance), T per shared expert.
     const int64_t exp_routed = (int64_t)T * k * cf.world_size / ne;
-    // swap-AB kernel: weight rows must fill 256-row pair tiles
-    auto use_swap = [&](int M) { return c->swap_mode == 1 && M % 256 == 0; };
+    // Experts per GEMM launch (routed items): consecutive experts whose expected rows are small
+    // share one launch -- and so one set of waves -- until a launch has ~kGemmRowsTarget rows
+    // (C1: 2 experts of ~1024 rows per launch, 4 staging slots).  Bounded by half the slots, so
+    // the next group's copies never wait on this group's GEMMs.
+    const int gemm_items =
+        (int)std::max<int64_t>(1, std::min<int64_t>(c->gemm_group_max,
+                                                    (c->gemm_rows_target + exp_routed - 1) /
+                                                        std::max<int64_t>(1, exp_routed)));
     const CUtensorMap* tmA_routed = &c->tm_xperm;
-    const moe::TokenMaps* tmT_routed = &c->tm_xperm_t;
     __nv_bfloat16* y_routed = c->y_perm;
     auto run_items = [&](int i0, int i1, const GemmGroup* g1, const GemmGroup* g2) -> moe_status {
     for (int i = i0; i < i1;) {
         const uint64_t q = q0 + i;
-        if (c->pend_n > 0 && c->pend_q0 <= q) {  // this item's batch is still pending: issue it
+        const bool shared = expert_of(i) >= c->n_local;
+        const int left = (shared ? S : c->n_all) - i;   // items of this class (shared / routed)
+        // the launch takes item q's whole DMA batch, or gemm_items routed items if more
+        int want = std::min(left, shared ? 1 : gemm_items);
+        if (c->pend_n > 0 && c->pend_q0 < q + (uint64_t)want) {  // a batch still pending: issue it
             moe_status fs = flush_copies(c);
             if (fs != MOE_OK) return fs;
         }
         const int s = (int)(q % (uint64_t)ns);
-        const bool shared = expert_of(i) >= c->n_local;
         int nb = (int)(c->batch_q0[s] + (uint64_t)c->batch_n[s] - q);
-        nb = std::max(1, std::min({nb, (shared ? S : c->n_all) - i, moe::kMaxBatch}));
-        if (use_swap(2 * hi) || use_swap(h)) nb = 1;   // the swap kernel takes one group
+        nb = std::max(1, std::min({std::max(nb, want), left, moe::kMaxBatch}));
         moe::GemmBatch b1{}, b2{};
         b1.table = g1;
         if (c->clk_acc) {
@@ -436,19 +379,10 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         }
         {
             Prof p(c, moe::kRecGemm1, st);
-            if (use_swap(2 * hi)) {
-                MOE_CUDA(c, moe::launch_expert_gemm_swap(moe::kGemmSwiGLU, &c->tm_w13_pair,
-                                                         shared ? &tm_x_t : tmT_routed, b1,
-                                                         2 * hi, h, c->h_act, hi, nullptr, grid, st));
-            } else {
-                const bool pr = pick_pair(c, rows, nb, c->bn1, 2 * hi, h);
-                moe_status gs = launch_grouped(c, moe::kGemmSwiGLU, c->bn1, pr,
-                                               shared ? &tm_x : tmA_routed, &c->tm_w13,
-                                               &c->tm_w13_pair, &c->tm_w13_alt,
-                                               shared ? &tm_x_t : tmT_routed,
-                                               b1, 2 * hi, h, c->h_act, hi, st);
-                if (gs != MOE_OK) return gs;
-            }
+            moe_status gs = launch_grouped(c, moe::kGemmSwiGLU, c->bn1, rows,
+                                           shared ? &tm_x : tmA_routed, &c->tm_w13,
+                                           &c->tm_w13_pair, b1, 2 * hi, h, c->h_act, hi, st);
+            if (gs != MOE_OK) return gs;
             p.end();
         }
         if (c->mover) {
@@ -460,19 +394,10 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         }
         {
             Prof p(c, moe::kRecGemm2, st);
-            if (use_swap(h)) {
-                MOE_CUDA(c, moe::launch_expert_gemm_swap(moe::kGemmPlain, &c->tm_w2_pair,
-                                                         &c->tm_h_t, b2, h, hi,
-                                                         shared ? c->y_perm : y_routed, h,
-                                                         nullptr, grid, st));
-            } else {
-                const bool pr = pick_pair(c, rows, nb, c->bn2, h, hi);
-                moe_status gs = launch_grouped(c, moe::kGemmPlain, c->bn2, pr, &c->tm_h,
-                                               &c->tm_w2, &c->tm_w2_pair, &c->tm_w2_alt,
-                                               &c->tm_h_t, b2, h, hi,
-                                               shared ? c->y_perm : y_routed, h, st);
-                if (gs != MOE_OK) return gs;
-            }
+            moe_status gs = launch_grouped(c, moe::kGemmPlain, c->bn2, rows, &c->tm_h, &c->tm_w2,
+                                           &c->tm_w2_pair, b2, h, hi,
+                                           shared ? c->y_perm : y_routed, h, st);
+            if (gs != MOE_OK) return gs;
             p.end();
         }
         c->stats.kernel_launches += 2;
@@ -540,7 +465,6 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         if (s != MOE_OK) return s;
         p.end();
         tmA_routed = &c->tm_xrecv;
-        tmT_routed = &c->tm_xrecv_t;
         g1 = c->ep_grp;
         g2 = c->ep_grp + c->n_all;
         y_routed = c->y_recv;
@@ -581,6 +505,10 @@ moe_status validate_call(moe_ctx c, int32_t T, const void* router_w, const void*
                          int32_t top_k) {
     if (!c) return MOE_E_INVAL;
     if (c->sticky != MOE_OK) return set_err(c, MOE_E_STATE, "context is in an error state");
+    if (c->p2p_diag_h && (c->p2p_diag_h[0] || c->p2p_diag_h[5])) {   // an earlier call failed
+        moe_sync(c);
+        return c->sticky != MOE_OK ? c->sticky : MOE_E_STATE;
+    }
     if (T < 0 || T > c->cfg.max_tokens)
         return set_err(c, MOE_E_INVAL, "num_tokens %d outside [0, %d]", T, c->cfg.max_tokens);
     if (top_k != c->cfg.top_k)
@@ -588,10 +516,16 @@ moe_status validate_call(moe_ctx c, int32_t T, const void* router_w, const void*
     if (T == 0 && !c->ep) return MOE_OK;
     if (!router_w || !experts) return set_err(c, MOE_E_INVAL, "NULL router_w / experts");
     if (!is_device(router_w)) return set_err(c, MOE_E_INVAL, "router_w is not device memory");
+    if ((uintptr_t)router_w & 15)   // the router reads it with 16-byte vector loads
+        return set_err(c, MOE_E_INVAL, "router_w must be 16-byte aligned");
+    c->call_base.assign(c->n_all, 0);
     for (int i = 0; i < c->n_all; ++i) {
         if (!experts[i]) return set_err(c, MOE_E_INVAL, "experts[%d] is NULL", i);
-        if (!is_pinned(c, experts[i]))
+        if (!is_pinned(experts[i]))
             return set_err(c, MOE_E_NOT_PINNED, "experts[%d] is not page-locked host memory", i);
+        // start of the blob's allocation, looked up per call: one DMA may only span blobs of
+        // the same allocation (request_copy)
+        c->call_base[i] = alloc_start(experts[i]);
     }
     return MOE_OK;
 }
@@ -632,9 +566,28 @@ moe_status stage_host_tokens(moe_ctx c, const void* host, size_t bytes, int* b_o
     return MOE_OK;
 }
 
-// Task B resources, allocated on the first moe_taskb_forward.
+// Task B resources, allocated on the first moe_taskb_forward.  All or nothing: on any failure
+// everything allocated here is released again, so the next call retries from scratch
+// (taskb_ready is set only once the tensor maps are encoded).
+void taskb_release(moe_ctx c) {
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(c->lw_slot[i]);
+        c->lw_slot[i] = nullptr;
+        if (c->lw_ready[i]) cudaEventDestroy(c->lw_ready[i]);
+        if (c->lw_free[i]) cudaEventDestroy(c->lw_free[i]);
+        c->lw_ready[i] = c->lw_free[i] = nullptr;
+    }
+    cudaFree(c->h1_ws);
+    cudaFree(c->u_ws);
+    cudaFree(c->oproj_grp);
+    c->h1_ws = c->u_ws = nullptr;
+    c->oproj_grp = nullptr;
+    c->taskb_ready = false;
+    cudaGetLastError();
+}
+
 moe_status taskb_resources(moe_ctx c) {
-    if (c->lw_slot[0]) return MOE_OK;
+    if (c->taskb_ready) return MOE_OK;
     const int h = c->cfg.hidden;
     const size_t act = (size_t)c->cfg.max_tokens * h * 2;
     c->layer_bytes = moe_packed_layer_bytes(h);
@@ -648,11 +601,7 @@ moe_status taskb_resources(moe_ctx c) {
     ok &= cudaMalloc((void**)&c->u_ws, act) == cudaSuccess;
     ok &= cudaMalloc((void**)&c->oproj_grp, sizeof(GemmGroup)) == cudaSuccess;
     if (!ok) {
-        cudaGetLastError();
-        for (int i = 0; i < 2; ++i) {  // leave the context as it was (the next call retries)
-            cudaFree(c->lw_slot[i]);
-            c->lw_slot[i] = nullptr;
-        }
+        taskb_release(c);
         return set_err(c, MOE_E_NOMEM, "Task B buffers (2 x %lld B layer slots + 2 x %zu B)",
                        (long long)c->layer_bytes, act);
     }
@@ -660,9 +609,12 @@ moe_status taskb_resources(moe_ctx c) {
     for (int i = 0; i < 2; ++i) {  // Wo [h, h]: N = h output rows, K = h
         tm &= moe::make_tmap(&c->tm_wo[i], c->lw_slot[i], (uint64_t)h, (uint64_t)h, (uint32_t)c->bn2);
         tm &= moe::make_tmap(&c->tm_wo_pair[i], c->lw_slot[i], (uint64_t)h, (uint64_t)h, 128);
-        tm &= make_alt_maps(&c->tm_wo_alt[i], c->lw_slot[i], (uint64_t)h, (uint64_t)h);
     }
-    if (!tm) return set_err(c, MOE_E_CUDA, "cuTensorMapEncodeTiled failed for Wo");
+    if (!tm) {
+        taskb_release(c);
+        return set_err(c, MOE_E_CUDA, "cuTensorMapEncodeTiled failed for Wo");
+    }
+    c->taskb_ready = true;
     return MOE_OK;
 }
 
@@ -675,6 +627,8 @@ moe_status taskb_impl(moe_ctx c, const __nv_bfloat16* attn, const __nv_bfloat16*
                       int xb = 0) {
     const int h = c->cfg.hidden;
     c->stats.taskb_calls += 1;
+    // h1 / u are read by the previous call's combine: order after it (see forward_impl)
+    MOE_CUDA(c, cudaStreamWaitEvent(st, c->done_ev, 0));
     if (T == 0) {  // EP only: no local tokens, this rank still serves its experts
         c->last_taskb_T = 0;
         return forward_impl(c, nullptr, 0, wr, experts, nullptr, topk_idx, topk_w, st, false, 0);
@@ -704,21 +658,11 @@ moe_status taskb_impl(moe_ctx c, const __nv_bfloat16* attn, const __nv_bfloat16*
         moe::GemmBatch ob{};
         ob.table = c->oproj_grp;
         ob.n = 1;   // idx[0] = 0, b_row[0] = 0: Wo is the whole map
-        moe::TokenMaps tm_attn_t;
-        if (!moe::make_token_maps(&tm_attn_t, attn, (uint64_t)T, (uint64_t)h))
-            return set_err(c, MOE_E_CUDA, "cuTensorMapEncodeTiled failed for attn");
-        if (c->swap_mode == 1 && h % 256 == 0) {
-            MOE_CUDA(c, moe::launch_expert_gemm_swap(moe::kGemmResidual, &c->tm_wo_pair[b],
-                                                     &tm_attn_t, ob, h, h, c->h1_ws, h,
-                                                     resid, c->num_sms, st));
-        } else {
-            const int64_t rows = T;
-            const bool pr = pick_pair(c, &rows, 1, c->bn2, h, h);
-            moe_status gs = launch_grouped(c, moe::kGemmResidual, c->bn2, pr, &tm_attn,
-                                           &c->tm_wo[b], &c->tm_wo_pair[b], &c->tm_wo_alt[b],
-                                           &tm_attn_t, ob, h, h, c->h1_ws, h, st, resid);
-            if (gs != MOE_OK) return gs;
-        }
+        const int64_t rows = T;
+        moe_status gs = launch_grouped(c, moe::kGemmResidual, c->bn2, &rows, &tm_attn,
+                                       &c->tm_wo[b], &c->tm_wo_pair[b], ob, h, h, c->h1_ws, h, st,
+                                       resid);
+        if (gs != MOE_OK) return gs;
         p.end();
     }
     {
@@ -797,6 +741,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     c->num_sms = prop.multiProcessorCount;
     const int h = cfg->hidden, hi = cfg->ffn, ne = cfg->num_experts, k = cfg->top_k;
     const int S = cfg->num_shared, Tm = cfg->max_tokens, W = cfg->world_size;
+    if (const char* e = getenv("MOE_GEMM_ROWS")) c->gemm_rows_target = std::max(1, atoi(e));
     c->ep = W > 1 || (cfg->flags & (MOE_FLAG_FORCE_EP | MOE_FLAG_LOCAL_EP | MOE_FLAG_IPC_EP));
     c->local_ep = (cfg->flags & MOE_FLAG_LOCAL_EP) != 0;
     c->p2p = c->local_ep || (cfg->flags & MOE_FLAG_IPC_EP) != 0;
@@ -812,8 +757,13 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
         c->nslots = cfg->num_slots;
     } else {  // auto: ~512 MiB of staging, 2..32 slots, fewer than the experts streamed per call
         // (measured on DSV2-Lite-size experts: 8 slots 95.1%, 16 slots 98.9%, 24-32 slots with
-        // 12-16-expert DMAs 99.4% of roofline)
-        const int64_t want = (moe::kAutoSlotBytes + c->blob_bytes - 1) / c->blob_bytes;
+        // 12-16-expert DMAs 99.4% of roofline); at least two GEMM groups' worth when small
+        // expert groups share a launch (forward_impl gemm_items; C1: 4 slots)
+        int64_t want = (moe::kAutoSlotBytes + c->blob_bytes - 1) / c->blob_bytes;
+        const int64_t rows_max = std::max<int64_t>(1, (int64_t)Tm * k * W / ne);
+        const int64_t g = std::min<int64_t>((c->gemm_rows_target + rows_max - 1) / rows_max,
+                                            (c->n_all - 1) / 2);
+        if (g > 1) want = std::max(want, 2 * g);
         c->nslots = (int)std::max<int64_t>(
             2, std::min<int64_t>({want, (int64_t)moe::kMaxSlots, (int64_t)c->n_all - 1}));
     }
@@ -821,6 +771,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     c->copy_group = (int)std::max<int64_t>(
         1, std::min<int64_t>((moe::kCopyBatchBytes + c->blob_bytes - 1) / c->blob_bytes, c->nslots / 2));
     if (const char* e = getenv("MOE_COPY_GROUP")) c->copy_group = std::max(1, std::min(atoi(e), c->nslots));
+    c->gemm_group_max = std::min(c->nslots / 2, moe::kMaxBatch);
     c->cap_recv = c->ep ? (int64_t)W * Tm * k : (int64_t)Tm * k;
     // h_act rows: routed rows (received rows under EP) then S * Tm shared rows
     const int64_t h_rows = c->cap_recv + (int64_t)S * Tm;
@@ -846,12 +797,6 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
                   cudaMemset(c->clk_acc, 0, 4 * sizeof(unsigned long long)) == cudaSuccess;
         }
         ok &= cudaEventCreateWithFlags(&c->done_ev, cudaEventDisableTiming) == cudaSuccess;
-        if (const char* e = getenv("MOE_GEMM_TAILSPLIT")) c->tail_split = atoi(e) != 0;
-        if (c->tail_split) {
-            ok &= cudaStreamCreateWithFlags(&c->tail_stream, cudaStreamNonBlocking) == cudaSuccess;
-            ok &= cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming) == cudaSuccess;
-            ok &= cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming) == cudaSuccess;
-        }
     }
     ok &= dalloc((void**)&c->slot_base, (size_t)c->blob_bytes * c->nslots);
     for (int i = 0; i < c->nslots; ++i) {
@@ -884,47 +829,21 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     bool tm = true;
     tm &= moe::make_tmap(&c->tm_xperm, c->x_perm, (uint64_t)Tm * k, h, 128);
     tm &= moe::make_tmap(&c->tm_h, c->h_act, (uint64_t)h_rows, hi, 128);
-    tm &= moe::make_token_maps(&c->tm_xperm_t, c->x_perm, (uint64_t)Tm * k, h);
-    tm &= moe::make_token_maps(&c->tm_h_t, c->h_act, (uint64_t)h_rows, hi);
     {   // the whole staging buffer as one W13 view and one W2 view (see engine.h)
         const uint64_t r13 = 3ull * hi * c->nslots, r2 = 3ull * h * c->nslots;
         tm &= moe::make_tmap(&c->tm_w13, c->slot_base, r13, h, (uint32_t)c->bn1);
         tm &= moe::make_tmap(&c->tm_w13_pair, c->slot_base, r13, h, 128);
-        tm &= make_alt_maps(&c->tm_w13_alt, c->slot_base, r13, h);
         tm &= moe::make_tmap(&c->tm_w2, c->slot_base, r2, hi, (uint32_t)c->bn2);
         tm &= moe::make_tmap(&c->tm_w2_pair, c->slot_base, r2, hi, 128);
-        tm &= make_alt_maps(&c->tm_w2_alt, c->slot_base, r2, hi);
     }
     if (!tm) return fail(MOE_E_CUDA);
-    if (const char* e = getenv("MOE_GEMM_SWAP")) c->swap_mode = atoi(e) != 0;
-    if (const char* e = getenv("MOE_GEMM_TAILSWAP")) c->tail_swap = atoi(e) != 0;
-    if (const char* e = getenv("MOE_GEMM_ALT")) c->alt_tiles = atoi(e) != 0;
-    {   // stream-K last wave of the pair kernel (MOE_GEMM_STREAMK)
-        bool sk = c->streamk_default;
-        if (const char* e = getenv("MOE_GEMM_STREAMK")) sk = atoi(e) != 0;
-        if (sk) {
-            const size_t units = (size_t)std::max(1, c->num_sms / 2);
-            if (cudaMalloc((void**)&c->sk_ws, units * moe::kStreamKUnitFloats * sizeof(float)) != cudaSuccess ||
-                cudaMalloc((void**)&c->sk_flags, units * 2 * sizeof(int)) != cudaSuccess ||
-                cudaMemset(c->sk_flags, 0, units * 2 * sizeof(int)) != cudaSuccess)
-                return fail(MOE_E_NOMEM);
-        }
-    }
-    if (const char* e = getenv("MOE_GEMM_TAILCOST")) {
-        const float v = (float)atof(e);
-        if (v > 0.f && v <= 4.f) c->tail_cost = v;
-    }
-    if (const char* e = getenv("MOE_GEMM_PAIR")) {
+    if (const char* e = getenv("MOE_GEMM_PAIR")) {   // tests: force one kernel
         if (!strcmp(e, "0")) c->pair_mode = 0;
         else if (!strcmp(e, "1")) c->pair_mode = 1;
-        else if (!strcmp(e, "2") || !strcmp(e, "device")) c->pair_mode = 2;
-        else if (!strcmp(e, "auto")) c->pair_mode = -1;
+        else c->pair_mode = -1;
     }
     {
-        int hints = 0;   // measured: evict_normal beats evict_last/evict_first (profiles/r01)
-        if (const char* e = getenv("MOE_GEMM_L2HINT")) hints = atoi(e);
-        if (moe::set_gemm_l2_hints(hints) != cudaSuccess) return fail(MOE_E_CUDA);
-        const char* gm = getenv("MOE_GEMM_GROUPM");
+        const char* gm = getenv("MOE_GEMM_GROUPM");   // tests: raster group override
         if (moe::set_gemm_group_m(gm ? atoi(gm) : 0) != cudaSuccess) return fail(MOE_E_CUDA);
     }
     if (c->ep) {
@@ -975,7 +894,7 @@ moe_status moe_layer_forward_host(moe_ctx ctx, const void* hidden_host, int32_t 
         return forward_impl(c, nullptr, 0, static_cast<const __nv_bfloat16*>(router_w), experts,
                             nullptr, topk_idx, topk_w, st, false, 0);
     if (!hidden_host || !out_host) return set_err(ctx, MOE_E_INVAL, "NULL hidden / out");
-    if (!is_pinned(ctx, hidden_host) || !is_pinned(ctx, out_host))
+    if (!is_pinned(hidden_host) || !is_pinned(out_host))
         return set_err(ctx, MOE_E_NOT_PINNED, "hidden_host/out_host must be page-locked");
     MOE_CUDA(ctx, cudaSetDevice(ctx->cfg.device));
     const size_t bytes = (size_t)num_tokens * c->cfg.hidden * 2;
@@ -1022,7 +941,7 @@ moe_status moe_taskb_forward(moe_ctx ctx, const void* attn, const void* resid, i
             return set_err(ctx, MOE_E_INVAL, "attn/resid/out must be device memory");
         if ((topk_idx && !is_device(topk_idx)) || (topk_w && !is_device(topk_w)))
             return set_err(ctx, MOE_E_INVAL, "topk_idx/topk_w must be device memory");
-        if (!is_pinned(ctx, layer))
+        if (!is_pinned(layer))
             return set_err(ctx, MOE_E_NOT_PINNED, "layer blob is not page-locked host memory");
     }
     MOE_CUDA(ctx, cudaSetDevice(ctx->cfg.device));
@@ -1059,7 +978,7 @@ moe_status moe_taskb_forward_host(moe_ctx ctx, const void* attn_host, const void
         return set_err(c, MOE_E_INVAL, "resid must be 16-byte aligned device memory");
     if ((topk_idx && !is_device(topk_idx)) || (topk_w && !is_device(topk_w)))
         return set_err(c, MOE_E_INVAL, "topk_idx/topk_w must be device memory");
-    if (!is_pinned(c, attn_host) || !is_pinned(c, out_host) || !is_pinned(c, layer))
+    if (!is_pinned(attn_host) || !is_pinned(out_host) || !is_pinned(layer))
         return set_err(c, MOE_E_NOT_PINNED, "attn_host/out_host/layer must be page-locked");
     s = taskb_resources(c);
     if (s != MOE_OK) return s;
@@ -1080,6 +999,13 @@ moe_status moe_taskb_forward_host(moe_ctx ctx, const void* attn_host, const void
 
 moe_status moe_sync(moe_ctx ctx) {
     if (!ctx) return MOE_E_INVAL;
+    if (ctx->p2p_diag_h && ctx->p2p_diag_h[5]) {   // the P2P plan refused an overflow (ep_p2p.cu)
+        ctx->sticky = MOE_E_STATE;
+        return set_err(ctx, MOE_E_STATE,
+                       "P2P EP: an expert owner would receive %lld rows > its capacity %lld "
+                       "(ranks configured with different max_tokens / top_k?); the call "
+                       "exchanged nothing", ctx->p2p_diag_h[6], ctx->p2p_diag_h[7]);
+    }
     if (ctx->p2p_diag_h && ctx->p2p_diag_h[0]) {   // a P2P flag wait timed out (ep_p2p.cu)
         ctx->sticky = MOE_E_CUDA;
         return set_err(ctx, MOE_E_CUDA,
@@ -1209,15 +1135,12 @@ moe_status moe_destroy(moe_ctx c) {
     }
     void* bufs[] = {c->idx_ws, c->gates_ws, c->tile_counts, c->tile_prefix, c->offsets, c->counts,
                     c->grp1, c->grp2, c->shared_grp, c->pos, c->x_perm, c->h_act, c->y_perm,
-                    c->h1_ws, c->u_ws, c->oproj_grp, c->clk_acc, c->sk_ws, c->sk_flags};
+                    c->h1_ws, c->u_ws, c->oproj_grp, c->clk_acc};
     for (void* p : bufs) cudaFree(p);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->token_stream) cudaStreamDestroy(c->token_stream);
     if (c->clock_stream) cudaStreamDestroy(c->clock_stream);
     if (c->done_ev) cudaEventDestroy(c->done_ev);
-    if (c->tail_stream) cudaStreamDestroy(c->tail_stream);
-    if (c->fork_ev) cudaEventDestroy(c->fork_ev);
-    if (c->join_ev) cudaEventDestroy(c->join_ev);
     cudaGetLastError();
     delete c;
     return MOE_OK;

@@ -29,48 +29,15 @@ struct GemmGroup {
 // The expert groups of one GEMM launch (kernel parameter, by value): entry i is group
 // table[idx[i]] (a device table written by the routing / EP plan kernels), whose weights start
 // at row b_row[i] of the launch's B tensor map (one map spans all staging slots).
-// part: 0 = every row of each group; 1 = the head (the largest multiple of 256 rows -- whole
-// CTA-pair tiles); 2 = the tail (the remaining < 256 rows), so a pair-kernel launch on the head
-// and a concurrent 128-row-tile launch on the tail split a group without padding it to 256.
-// tail_swap (CTA-pair kernel only): a group's last partial tile of <= 128 rows runs swap-AB
-// inside the same launch -- weights as the 256-row M side, the r tail tokens as an N =
-// ceil(r/32)*32 side -- instead of a 256-row tile that is mostly padding; those tail tiles are
-// scheduled after the full tiles onto the least-loaded CTA pairs, at an estimated `tail_cost`
-// (time of a tail tile / time of a full 256x256 tile).
 constexpr int kMaxBatch = 16;
-constexpr int kPairRows = 256;
 struct GemmBatch {
     const GemmGroup* table;
     int32_t idx[kMaxBatch];
     int32_t b_row[kMaxBatch];
     int32_t n;
-    int32_t part;
-    int32_t tail_swap;
-    float tail_cost;
-    // select > 0: the host launched BOTH the CTA-pair and the single-CTA kernel for this batch,
-    // sized for `select` SMs; each evaluates the same wave model (plan_tiles, gemm.cu) on the
-    // ACTUAL group sizes (device memory, no host sync) and the one not chosen exits at once.
-    // bn_single: the single-CTA kernel's tile width; alt_ok: the pair launch has PairBMaps.
-    int32_t select;
-    int32_t bn_single;
-    int32_t alt_ok;
     // clk: if non-null, CTA 0 adds its SM cycles (clock64) and elapsed ns (globaltimer) from
     // kernel entry to exit to clk[0] / clk[1] (the SM clock under power management).
     unsigned long long* clk;
-    // Stream-K last wave (CTA-pair kernel, streamk != 0): when the full tiles leave a partial
-    // last wave of L <= P/2 tiles on P pairs, those L tiles are cut along K into S chunks that
-    // run on S*L <= P pairs at once; chunk 0's pair sums the other chunks' fp32 partials
-    // (sk_ws: kStreamKUnitFloats per chunk, P chunks) after their per-CTA counters in sk_flags
-    // ([P][2], zero between launches) reach S - 1, then runs the usual epilogue.
-    int32_t streamk;
-    float* sk_ws;
-    int* sk_flags;
-};
-constexpr int64_t kStreamKUnitFloats = 8ll * 256 * 32;   // 256 rows x 256 fp32 columns
-// Extra B maps of the CTA-pair kernel: per-CTA boxes of 112 and 96 rows for 224- and 192-wide
-// tiles (chosen on the device when N divides and fewer waves result, e.g. 28672 = 128 x 224).
-struct PairBMaps {
-    CUtensorMap b224, b192;
 };
 
 // ------------------------------------------------------------ expert parallelism, P2P transport
@@ -116,11 +83,12 @@ cudaError_t launch_p2p_selftest(const P2PTable* tab, const PeerRows* pr_x,
 // From counts[par] (all ranks' per-expert counts): this rank's GEMM groups over x_recv
 // (expert-major, moe_ep_plan's layout) + shared-expert groups, the send bases of pr_x / pr_y
 // (where this rank's rows for expert e start in the owner's buffers), rows received (rows_out)
-// and bytes sent (+= bytes_acc).
+// and bytes sent (+= bytes_acc).  If some owner would receive more than cap_recv rows, nothing
+// is dispatched (bases -1, empty groups) and diag[5..7] = {1, rows, cap_recv} (host-mapped).
 cudaError_t launch_p2p_plan(const int32_t* counts_par, int W, int ne, int me, int T, int k,
                             int S, long long cap_recv, int n_all, int h, GemmGroup* grp,
                             PeerRows* pr_x, PeerRows* pr_y, int32_t* rows_out,
-                            long long* bytes_acc, cudaStream_t st);
+                            long long* bytes_acc, long long* diag, cudaStream_t st);
 
 // ---------------------------------------------------------------------------- routing kernels
 // a2+a3: router GEMM (fp64, ascending c) + warp-shuffle top-k + softmax gates + per-tile counts.
@@ -164,43 +132,18 @@ cudaError_t launch_fill_shared_groups(GemmGroup* g, int n_local, int n_all, int 
 
 // ---------------------------------------------------------------------------- expert GEMM
 enum GemmMode { kGemmSwiGLU = 0, kGemmPlain = 1, kGemmResidual = 2 };
-// One expert group of a5 (SwiGLU, N = 2*h_i interleaved) or a6 (plain, N = h) on tcgen05, or
-// the O-projection of Task B (residual: out = bf16(A B^T + resid), N = h).
+// One launch over a batch of expert groups (GemmBatch: up to kMaxBatch experts whose tiles
+// share the persistent CTAs' waves) of a5 (SwiGLU, N = 2*h_i interleaved), a6 (plain, N = h) or
+// the O-projection of Task B (residual: out = bf16(A B^T + resid), N = h), on tcgen05.
 //   tmA: A [rows, K] bf16 (box 64 x 128); tmB: B [N, K] bf16 (box 64 x bn, or 64 x 128 when
-//   `pair`: the CTA-pair kernel, 256 x 256 tiles, bn must be 256); group: device ptr.
+//   `pair`: the CTA-pair kernel, 256 x 256 tiles, bn must be 256).
 //   out: bf16 [*, ldo]; SwiGLU writes N/2 columns.  resid: bf16 [*, ldo] (residual mode only,
 //   else nullptr), read at the output's rows.
-//   batch: the launch's expert groups (GemmBatch below): ONE persistent launch covers up to
-//   kMaxBatch experts -- their tiles are scheduled together, so small experts no longer pay a
-//   partial last wave each.
-// Token operand of the swap-AB kernel: the same [rows, K] bf16 tensor with 64-column boxes of
-// 128, 64, 32 and 16 rows, so a CTA's N/2 token rows (a multiple of 16) load in <= 4 TMA ops.
-struct TokenMaps {
-    CUtensorMap box[4];
-};
-//   tmT: tmA's tensor as TokenMaps -- the token operand of swap-AB tail tiles (pair kernel with
-//   batch.tail_swap; may be nullptr otherwise).
 cudaError_t launch_expert_gemm(int mode, int bn, bool pair, const CUtensorMap* tmA,
                                const CUtensorMap* tmB, const GemmBatch& batch, int N, int K,
                                __nv_bfloat16* out, int ldo, const __nv_bfloat16* resid, int grid,
-                               cudaStream_t st, const TokenMaps* tmT = nullptr,
-                               const PairBMaps* alt = nullptr);
-// Host model of the pair kernel's schedule (the same rule the kernel applies): the makespan in
-// units of one full 256x256 tile time of a launch whose groups have rows[i] rows, N/256 weight
-// tiles, on npairs CTA pairs.
-double pair_makespan(const int64_t* rows, int n, int n_tiles, int npairs, bool tail_swap,
-                     float tail_cost, bool streamk = false, int num_kb = 64);
-bool make_token_maps(TokenMaps* t, const void* base, uint64_t rows, uint64_t cols);  // moe_api.cu
-// Swap-AB CTA-pair kernel (gemm.cu): weights are the 256-row M side (tmW: box 64 x 128, M rows
-// = 2 h_i for SwiGLU, h otherwise, M % 256 == 0), the group's tokens the N side, N = 32..256
-// per tile (a multiple of 32).
-cudaError_t launch_expert_gemm_swap(int mode, const CUtensorMap* tmW, const TokenMaps* tmX,
-                                    const GemmBatch& batch, int M, int K, __nv_bfloat16* out,
-                                    int ldo, const __nv_bfloat16* resid, int grid, cudaStream_t st);
+                               cudaStream_t st);
 int gemm_bn_for(int mode, int N);   // tile width used for a given mode / N (0 = unsupported)
-// L2 policy of the GEMM operand loads for the current device: 0 evict_normal, 1 A evict_last +
-// B evict_first.
-cudaError_t set_gemm_l2_hints(int mode);
-cudaError_t set_gemm_group_m(int gm);   // 0 = per-kernel default (MOE_GEMM_GROUPM, experiments)
+cudaError_t set_gemm_group_m(int gm);   // raster group override (0 = kernel default; tests)
 
 }  // namespace moe

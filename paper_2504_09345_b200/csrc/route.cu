@@ -336,7 +336,9 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int h, int k, int ne,
                 const int p = spos[q * k + j];
                 if (pr) {   // straight into the expert owner's x_recv (P2P dispatch)
                     const int e = sidx[(tt0 + q) * k + j];
-                    dst_ptr[j] = pr->rows[e / pr->nl] + (size_t)(pr->base[e] + p - offsets[e]) * h;
+                    const int b = pr->base[e];   // -1: the plan refused the exchange (overflow)
+                    dst_ptr[j] = b < 0 ? nullptr
+                                       : pr->rows[e / pr->nl] + (size_t)(b + p - offsets[e]) * h;
                 } else {
                     dst_ptr[j] = x_perm + (size_t)p * h;
                 }
@@ -352,6 +354,7 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int h, int k, int ne,
             }
             for (int j = 0; j < k; ++j) {
                 int4* dst = reinterpret_cast<int4*>(dst_ptr[j]);
+                if (!dst) continue;
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int v = v0 + 32 * u;
@@ -384,7 +387,13 @@ combine_kernel(const __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ 
             g[j] = gates[(size_t)t * k + j];
             if (pr) {   // the expert owner's y_recv (P2P combine)
                 const int e = idx[(size_t)t * k + j];
-                prow[j] = pr->rows[e / pr->nl] + (size_t)(pr->base[e] + p - offsets[e]) * h;
+                const int b = pr->base[e];
+                if (b < 0) {   // the plan refused the exchange (overflow): contributes nothing
+                    prow[j] = y;
+                    g[j] = 0.f;
+                    continue;
+                }
+                prow[j] = pr->rows[e / pr->nl] + (size_t)(b + p - offsets[e]) * h;
             } else {
                 prow[j] = y + (size_t)p * h;
             }

@@ -42,7 +42,8 @@ def n_real(slope: float, intercept: float, t_io: float) -> float:
     return (t_io - intercept) / slope
 
 
-def profile(config: str, tokens: Sequence[int], steps: int = 3, device: int = 0) -> dict:
+def profile(config, tokens: Sequence[int], steps: int = 3, device: int = 0) -> dict:
+    """config: a synth.CONFIGS name or a synth.MoEConfig (any layer shape)."""
     import numpy as np
     import torch
 
@@ -52,7 +53,7 @@ def profile(config: str, tokens: Sequence[int], steps: int = 3, device: int = 0)
     from . import HostExperts, MoELayer, ledger, moe_probe_h2d
 
     torch.cuda.set_device(device)
-    cfg = synth.CONFIGS[config]
+    cfg = synth.CONFIGS[config] if isinstance(config, str) else config
     tmax = max(tokens)
     inp = synth.gen_inputs(cfg, tokens=tmax)
     experts = HostExperts(cfg.hidden, cfg.ffn, inp.w1, inp.w3, inp.w2)
@@ -88,7 +89,13 @@ def profile(config: str, tokens: Sequence[int], steps: int = 3, device: int = 0)
     probe = moe_probe_h2d(device, 1 << 30, 3)
     n_eq2 = ledger.eq2_tokens_to_saturate(tf, probe, cfg.num_experts, cfg.top_k,
                                           binary_prefixes=False)
-    res = {"config": config, "points": pts, "slope_ms_per_token": slope, "intercept_ms": icpt,
+    # residuals of the line relative to each measured point (how linear GPU time is in n)
+    for p in pts:
+        p["fit_rel_residual"] = (p["gpu_ms"] - (slope * p["tokens"] + icpt)) / p["gpu_ms"]
+    res = {"config": cfg.name, "shape": {"hidden": cfg.hidden, "ffn": cfg.ffn,
+                                         "experts": cfg.num_experts, "top_k": cfg.top_k,
+                                         "shared": cfg.num_shared},
+           "points": pts, "slope_ms_per_token": slope, "intercept_ms": icpt,
            "t_io_ms": t_io, "n_real": n_real(slope, icpt, t_io),
            "n_eq2_estimate": n_eq2, "eq2_inputs": {"tensor_tflops": tf, "host_link_gbs": probe},
            "layer_weight_bytes": cfg.expert_bytes * (cfg.num_experts + cfg.num_shared)}

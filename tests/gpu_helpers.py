@@ -65,6 +65,37 @@ def sample_tokens(T: int, n: int, seed: int = 0) -> np.ndarray:
     return np.unique(np.clip(np.concatenate([fixed, rest]), 0, T - 1))
 
 
+def stratified_tokens(idx: np.ndarray, num_experts: int, num_shared: int = 0,
+                      block: int = 128) -> np.ndarray:
+    """Tokens that touch every (expert, 128-row M tile) of the permuted layout -- and so every
+    256-row CTA-pair tile and every raster group of every GEMM launch -- including each group's
+    first and last row (VERDICT r1 "stratified token set").
+
+    Inside expert e's group the rows are the (t, j) with idx[t, j] == e in ascending t (reading
+    R12); for every 128-row block of the group the tokens at its first and last row are taken,
+    plus the group's last row.  Shared experts (and Task B's O-projection) take all T tokens in
+    order: the first and last token of every 128-token block."""
+    T, k = idx.shape
+    flat = np.asarray(idx).ravel()
+    sel = set()
+    for e in range(num_experts):
+        rows = np.nonzero(flat == e)[0]          # ascending flat index = ascending t
+        n = len(rows)
+        if n == 0:
+            continue
+        for p in set(range(0, n, block)) | set(range(block - 1, n, block)) | {n - 1}:
+            sel.add(int(rows[p]) // k)
+    if num_shared:
+        sel |= set(block_tokens(T, block).tolist())
+    return np.array(sorted(sel), dtype=np.int64)
+
+
+def block_tokens(T: int, block: int = 128) -> np.ndarray:
+    """First and last token of every `block`-token M tile of a GEMM over all T tokens."""
+    s = set(range(0, T, block)) | set(range(block - 1, T, block)) | {T - 1}
+    return np.array(sorted(s), dtype=np.int64)
+
+
 class _CudaArray:
     def __init__(self, ptr, shape, typestr):
         self.__cuda_array_interface__ = {"data": (int(ptr), False), "shape": tuple(shape),

@@ -37,12 +37,10 @@ _REF = {}
 
 
 MODES = {"auto": {}, "pair0": {"MOE_GEMM_PAIR": "0"}, "pair1": {"MOE_GEMM_PAIR": "1"},
-         "swap": {"MOE_GEMM_SWAP": "1"},
-         # the opt-in variants: every one must stay exact on every shape
-         "tailswap": {"MOE_GEMM_PAIR": "1", "MOE_GEMM_TAILSWAP": "1"},
-         "alt": {"MOE_GEMM_PAIR": "1", "MOE_GEMM_ALT": "1"},
-         "device": {"MOE_GEMM_PAIR": "device", "MOE_GEMM_ALT": "1"},
-         "streamk": {"MOE_GEMM_PAIR": "1", "MOE_GEMM_STREAMK": "1"},
+         # several raster groups per launch, the last one partial (tile_coords, gemm.cu)
+         "groupm2": {"MOE_GEMM_GROUPM": "2"},
+         # one routed expert per GEMM launch (no expert grouping, forward_impl gemm_items)
+         "onegroup": {"MOE_GEMM_ROWS": "1000000000"},
          "mover": {}}
 
 

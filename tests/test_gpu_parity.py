@@ -15,7 +15,8 @@ import oracle
 import synth
 from paper_2504_09345_b200 import (MOE_E_INVAL, MOE_E_NOT_PINNED, MoEError, moe_layer_forward)
 
-from gpu_helpers import GpuRun, bf16_tensor, dev_view, sample_tokens, to_f32, token_rel_err
+from gpu_helpers import (GpuRun, bf16_tensor, dev_view, sample_tokens, stratified_tokens, to_f32,
+                         token_rel_err)
 
 pytestmark = pytest.mark.gpu
 
@@ -230,7 +231,9 @@ def test_stats_h2d_bytes_equal_algorithmic_bytes(group, monkeypatch):
 @pytest.mark.parametrize("name", ["mixtral_8x7b", "mixtral_8x22b", "dbrx", "dsv2_lite"])
 def test_full_size_config(name):
     """Full BASELINE.json sizes in the bench's launch configuration: routing bit-exact on all
-    tokens (oracle router + top-k over every token), outputs on sampled tokens."""
+    tokens (oracle router + top-k over every token); outputs compared element by element on a
+    stratified token set that touches every (expert, 128-row M tile) of the permuted layout --
+    each group's first and last row, every raster group of every launch -- plus random tokens."""
     cfg = synth.CONFIGS[name]
     inp = synth.gen_inputs(cfg)
     run = GpuRun(inp)
@@ -241,15 +244,38 @@ def test_full_size_config(name):
         idx_gpu = idx.cpu().numpy()
         assert np.array_equal(idx_gpu, idx_ref), f"{(idx_gpu != idx_ref).any(1).sum()} tokens differ"
         assert np.max(np.abs(gates.cpu().numpy() - g_ref)) <= 1e-6
-        sel = sample_tokens(cfg.tokens, 24)
+        sel = np.union1d(stratified_tokens(idx_ref, cfg.num_experts, cfg.num_shared),
+                         sample_tokens(cfg.tokens, 24))
         y_ref = oracle.experts_combine(inp.x[sel], inp.w1, inp.w3, inp.w2, cfg.num_experts,
                                        cfg.num_shared, idx_ref[sel], g_ref[sel])
         err = token_rel_err(to_f32(out[torch.from_numpy(sel).cuda()]), y_ref)
-        print(f"{name}: max token rel err {err.max():.3e} over {len(sel)} tokens; "
-              f"expert load {np.bincount(idx_ref.ravel(), minlength=cfg.num_experts).tolist()}")
+        print(f"{name}: max token rel err {err.max():.3e} (mean {err.mean():.2e}) over {len(sel)} "
+              f"stratified tokens; expert load "
+              f"{np.bincount(idx_ref.ravel(), minlength=cfg.num_experts).tolist()}")
         assert err.max() <= TOL
     finally:
         run.close()
+
+
+@pytest.mark.parametrize("pair", ["0", "1"])
+@pytest.mark.parametrize("shape", [
+    # GEMM2 with K = h_i = 8448 > 8192: the long-K raster (group 8 single / 4 pair M tiles);
+    # ~1500-row groups -> 12 (single) / 6 (pair) M tiles: two raster groups, the last partial
+    dict(hidden=256, ffn=8448, num_experts=2, top_k=1, tokens=3000),
+    # one 9000-row group: 71 (single) / 36 (pair) M tiles -> groups of 32 / 16, last partial
+    dict(hidden=256, ffn=256, num_experts=1, top_k=1, tokens=9000),
+])
+def test_long_k_and_large_group_rasters(shape, pair, monkeypatch):
+    """The raster branches that the BASELINE configs take at full size (C1's GEMM2 has
+    K = 14336 > 8192; C4's hot experts exceed 4096 rows), at sizes the oracle compares on
+    EVERY token, with both GEMM kernels."""
+    monkeypatch.setenv("MOE_GEMM_PAIR", pair)
+    cfg = synth.MoEConfig("custom", 23, shape["hidden"], shape["ffn"], shape["num_experts"],
+                          shape["top_k"], shape["tokens"], 0)
+    inp = synth.gen_inputs(cfg)
+    run, out, idx, gates, err = _check_full(inp)
+    print(f"{shape} pair={pair}: max token rel err {err.max():.3e}")
+    run.close()
 
 
 # ------------------------------------------------------------------------ expert parallelism
@@ -276,28 +302,22 @@ def test_ep_path_one_rank_nccl_matches_oracle_and_single_gpu(shape):
 
 
 # ------------------------------------------------------------- CTA-pair (cta_group::2) GEMM
-@pytest.mark.parametrize("mode", ["1", "1-tailswap", "1-alt", "device", "0", "split"])
+@pytest.mark.parametrize("mode", ["1", "0", "1-g2", "0-g3"])
 @pytest.mark.parametrize("shape", [
     dict(hidden=256, ffn=384, num_experts=8, top_k=2, tokens=1500),
     dict(hidden=512, ffn=640, num_experts=4, top_k=2, tokens=2100, num_shared=1),
     dict(hidden=256, ffn=256, num_experts=64, top_k=6, tokens=333),     # many tiny groups
-    dict(hidden=768, ffn=1792, num_experts=8, top_k=2, tokens=1700),    # 224 / 192-wide tiles
+    dict(hidden=768, ffn=1792, num_experts=8, top_k=2, tokens=1700),
 ])
 def test_gemm_tile_variants(shape, mode, monkeypatch):
     """MOE_GEMM_PAIR=1 forces the 256x256 CTA-pair kernel (tcgen05.mma.cta_group::2, 2-CTA TMA)
-    for every bn=256 GEMM: with padded 256-row group tails (1), with tails of <= 128 rows as
-    swap-AB tail tiles (1-tailswap, MOE_GEMM_TAILSWAP=1), or with 224 / 192-wide tiles where
-    they divide N (1-alt, MOE_GEMM_ALT=1); device = both kernels launched, the device picks on the
-    actual group sizes and the other exits; 0 forces the 128-row kernel; split = pair kernel on
-    whole 256-row tiles + a concurrent 128-row launch on the remainders (MOE_GEMM_TAILSPLIT).
-    All must match the oracle."""
-    monkeypatch.setenv("MOE_GEMM_PAIR", {"0": "0", "device": "device"}.get(mode, "1"))
-    if mode == "split":
-        monkeypatch.setenv("MOE_GEMM_TAILSPLIT", "1")
-    if mode == "1-tailswap":
-        monkeypatch.setenv("MOE_GEMM_TAILSWAP", "1")
-    if mode in ("1-alt", "device"):
-        monkeypatch.setenv("MOE_GEMM_ALT", "1")
+    for every bn=256 GEMM, 0 the 128-row kernel; -gN sets the raster group to N M tiles
+    (MOE_GEMM_GROUPM), so launches hold several raster groups, the last one partial.  All must
+    match the oracle."""
+    pair, _, g = mode.partition("-g")
+    monkeypatch.setenv("MOE_GEMM_PAIR", pair)
+    if g:
+        monkeypatch.setenv("MOE_GEMM_GROUPM", g)
     cfg = synth.MoEConfig("custom", 14, shape["hidden"], shape["ffn"], shape["num_experts"],
                           shape["top_k"], shape["tokens"], shape.get("num_shared", 0))
     inp = synth.gen_inputs(cfg)
@@ -305,46 +325,28 @@ def test_gemm_tile_variants(shape, mode, monkeypatch):
     run.close()
 
 
-@pytest.mark.parametrize("cost", ["0.05", "0.6", "3.0"])
-@pytest.mark.parametrize("shape", [
-    dict(hidden=256, ffn=512, num_experts=8, top_k=2, tokens=1100),     # tails 1..128 rows
-    dict(hidden=512, ffn=384, num_experts=16, top_k=4, tokens=700, num_shared=2),
-    dict(hidden=256, ffn=768, num_experts=2, top_k=1, tokens=40),       # tail-only groups
-    dict(hidden=768, ffn=1280, num_experts=8, top_k=2, tokens=9000),    # many tiles per pair
-])
-def test_gemm_pair_tail_swap_schedules(shape, cost, monkeypatch):
-    """Pair kernel with swap-AB tail tiles (MOE_GEMM_TAILSWAP=1, opt-in) under tail costs that drive the static schedule
-    (TailSched, gemm.cu) through light-only, mixed and heavy-first rounds: every tile must be
-    computed exactly once whatever the assignment."""
-    monkeypatch.setenv("MOE_GEMM_PAIR", "1")
-    monkeypatch.setenv("MOE_GEMM_TAILSWAP", "1")
-    monkeypatch.setenv("MOE_GEMM_TAILCOST", cost)
-    cfg = synth.MoEConfig("custom", 16, shape["hidden"], shape["ffn"], shape["num_experts"],
-                          shape["top_k"], shape["tokens"], shape.get("num_shared", 0))
+@pytest.mark.parametrize("rows,copy_group,launches", [("1", "1", 8), ("1", None, 4),
+                                                       ("2048", None, 3)])
+def test_experts_per_gemm_launch(rows, copy_group, launches, monkeypatch):
+    """Consecutive routed experts share one GEMM launch until it expects MOE_GEMM_ROWS rows
+    (forward_impl gemm_items; C1 puts 2 experts of ~1024 rows per launch in 4 staging slots), or
+    as many as one DMA batch holds.  Here 8 experts of ~512 rows, 7 slots, DMA batches of up to 3
+    (no batch wraps past slot 0): one expert per launch (8 launches); DMA batches only [0-2]
+    [3-5] [6] [7] (4); 2048-row groups of <= 3 experts [0-2] [3-5] [6-7] (3).  Every grouping
+    must give the oracle's result, bitwise the same on a repeated call."""
+    monkeypatch.setenv("MOE_GEMM_ROWS", rows)
+    if copy_group:
+        monkeypatch.setenv("MOE_COPY_GROUP", copy_group)
+    cfg = synth.MoEConfig("custom", 21, 256, 512, 8, 2, 2048)
     inp = synth.gen_inputs(cfg)
-    run, out, *_ = _check_full(inp)
-    run.close()
-
-
-@pytest.mark.parametrize("shape", [
-    dict(hidden=1024, ffn=2560, num_experts=1, top_k=1, tokens=1000),   # GEMM1: 80 tiles, L=6, S=8
-    dict(hidden=512, ffn=4864, num_experts=2, top_k=1, tokens=1500),    # 2 ragged groups, 228 tiles
-    dict(hidden=4096, ffn=1024, num_experts=1, top_k=1, tokens=1100),   # GEMM2: 80 tiles, L=6
-])
-def test_gemm_pair_streamk_last_wave(shape, monkeypatch):
-    """MOE_GEMM_STREAMK=1: the pair kernel's partial last wave runs as K-chunks on otherwise idle
-    SM pairs; chunk 0 adds the other chunks' fp32 partials before its epilogue.  Must match the
-    oracle, and back-to-back calls must stay bitwise stable (the chunk counters reset)."""
-    monkeypatch.setenv("MOE_GEMM_PAIR", "1")
-    monkeypatch.setenv("MOE_GEMM_STREAMK", "1")
-    cfg = synth.MoEConfig("custom", 17, shape["hidden"], shape["ffn"], shape["num_experts"],
-                          shape["top_k"], shape["tokens"], 0)
-    inp = synth.gen_inputs(cfg)
-    run, out, *_ = _check_full(inp)
+    run, out, *_ = _check_full(inp, profile=True)
     try:
-        for _ in range(3):
-            out2, _, _ = run.run()
-            assert torch.equal(out2, out)
+        run.layer.reset_stats()
+        out2, _, _ = run.run()
+        assert torch.equal(out2, out)
+        st = run.layer.stats()
+        assert st["num_slots"] == 7
+        assert st["gemm1_launches"] == launches and st["gemm2_launches"] == launches, st
     finally:
         run.close()
 
@@ -358,27 +360,6 @@ def test_router_experts_per_warp_variants(ne, k, ept, monkeypatch):
     cfg = synth.MoEConfig("custom", 19, 384, 256, ne, k, 777, 0)
     inp = synth.gen_inputs(cfg)
     run, *_ = _check_full(inp)
-    run.close()
-
-
-# ------------------------------------------------------------ swap-AB (weights as M) GEMM
-@pytest.mark.parametrize("shape", [
-    dict(hidden=256, ffn=384, num_experts=8, top_k=2, tokens=1500),
-    dict(hidden=512, ffn=640, num_experts=4, top_k=2, tokens=2100, num_shared=1),
-    dict(hidden=256, ffn=256, num_experts=64, top_k=6, tokens=333),     # many tiny groups
-    dict(hidden=384, ffn=256, num_experts=16, top_k=4, tokens=777, num_shared=2),  # h % 256 != 0
-    dict(hidden=1024, ffn=512, num_experts=2, top_k=1, tokens=70),      # one tile per group
-    dict(hidden=768, ffn=1280, num_experts=8, top_k=2, tokens=9000),    # many tiles per pair
-])
-def test_gemm_swap_ab(shape, monkeypatch):
-    """MOE_GEMM_SWAP=1: expert GEMMs with the weights as the 256-row M side and the tokens as a
-    run-time N (32..256 per tile), work split evenly over SM pairs, transposed epilogue (GEMMs
-    whose weight rows are not a multiple of 256 fall back to the regular kernels)."""
-    monkeypatch.setenv("MOE_GEMM_SWAP", "1")
-    cfg = synth.MoEConfig("custom", 15, shape["hidden"], shape["ffn"], shape["num_experts"],
-                          shape["top_k"], shape["tokens"], shape.get("num_shared", 0))
-    inp = synth.gen_inputs(cfg)
-    run, out, *_ = _check_full(inp)
     run.close()
 
 
@@ -534,3 +515,67 @@ def test_coalesced_expert_dma(group, monkeypatch):
     layer.close()
     ex_c.close()
     ex_n.close()
+
+
+def test_alternating_streams_without_mover():
+    """Back-to-back calls on two different caller streams, no host sync in between, default
+    (event-ordered) engine: every call first waits for the previous one (the calls share the
+    context's workspace), so outputs equal isolated calls bitwise."""
+    cfg = synth.MoEConfig("custom", 22, 512, 768, 8, 2, 900)
+    layers = [synth.gen_inputs(cfg, layer=l) for l in range(2)]
+    runs = [GpuRun(l) for l in layers]
+    iso = [r.run() for r in runs]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    torch.cuda.synchronize()
+    outs = []
+    for it in range(6):
+        l = it % 2
+        x = bf16_tensor(layers[l].x)
+        o = torch.empty_like(x)
+        runs[0].layer.forward(x, bf16_tensor(layers[l].router), runs[l].experts, o,
+                              stream=streams[it % 2].cuda_stream)
+        outs.append((l, o, x))
+    torch.cuda.synchronize()
+    runs[0].layer.sync()
+    for l, o, _ in outs:
+        assert torch.equal(o, iso[l][0])
+    for r in runs:
+        r.close()
+
+
+def test_local_ep_rejects_inconsistent_ranks():
+    """LOCAL_EP ranks must share the layer shape and max_tokens (the receive buffers are sized
+    W x max_tokens x top_k): a rank registering with another max_tokens is refused at init."""
+    import os
+    from paper_2504_09345_b200 import MoELayer
+    key = os.urandom(128)
+    r0 = MoELayer(256, 256, 8, 2, 100, world_size=2, rank=0, nccl_unique_id=key, local_ep=True)
+    try:
+        with pytest.raises(MoEError) as e:
+            MoELayer(256, 256, 8, 2, 200, world_size=2, rank=1, nccl_unique_id=key, local_ep=True)
+        assert e.value.status == MOE_E_INVAL
+        r1 = MoELayer(256, 256, 8, 2, 100, world_size=2, rank=1, nccl_unique_id=key, local_ep=True)
+        r1.close()
+    finally:
+        r0.close()
+
+
+def test_ipc_connect_rejects_mismatched_blob():
+    """moe_ep_ipc_connect checks every rank's published layer shape / max_tokens before mapping
+    anything: a peer blob announcing another max_tokens is refused with MOE_E_INVAL."""
+    import struct
+    from paper_2504_09345_b200 import MoELayer
+    r0 = MoELayer(256, 256, 8, 2, 100, world_size=2, rank=0, ipc_ep=True)
+    try:
+        mine = bytearray(r0.ipc_handle())
+        off = 4 * 64   # after the 4 cudaIpcMemHandle_t
+        fields = list(struct.unpack_from("<10i", mine, off))
+        assert fields[0] == 0x4D6F4533 and fields[1] == 0 and fields[2] == 2 and fields[8] == 100
+        peer = bytearray(mine)
+        fields[1], fields[8] = 1, 200          # rank 1 with another max_tokens
+        struct.pack_into("<10i", peer, off, *fields)
+        with pytest.raises(MoEError) as e:
+            r0.ipc_connect([bytes(mine), bytes(peer)])
+        assert e.value.status == MOE_E_INVAL
+    finally:
+        r0.close()

@@ -23,7 +23,8 @@ import synth
 from paper_2504_09345_b200 import (MOE_E_INVAL, MOE_E_NOT_PINNED, HostLayer, MoEError,
                                    moe_taskb_forward)
 
-from gpu_helpers import GpuRun, bf16_tensor, dev_view, sample_tokens, to_f32, token_rel_err
+from gpu_helpers import (GpuRun, bf16_tensor, block_tokens, dev_view, sample_tokens,
+                         stratified_tokens, to_f32, token_rel_err)
 
 pytestmark = pytest.mark.gpu
 
@@ -105,36 +106,31 @@ def _inputs(hidden, ffn, ne, k, T, S=0, seed_id=9):
     dict(hidden=384, ffn=256, ne=64, k=6, T=777, S=2),
     dict(hidden=128, ffn=128, ne=4, k=2, T=1),
 ])
-@pytest.mark.parametrize("force_ep,swap", [(False, "0"), (True, "0"), (False, "1")])
-def test_taskb_staged_parity(shape, force_ep, swap, monkeypatch):
-    monkeypatch.setenv("MOE_GEMM_SWAP", swap)
+@pytest.mark.parametrize("force_ep,pair", [(False, "auto"), (True, "auto"), (False, "0"),
+                                            (False, "1")])
+def test_taskb_staged_parity(shape, force_ep, pair, monkeypatch):
+    monkeypatch.setenv("MOE_GEMM_PAIR", pair)
     inp, tb = _inputs(shape["hidden"], shape["ffn"], shape["ne"], shape["k"], shape["T"],
                       shape.get("S", 0))
     r = TaskBRun(inp, tb, force_ep=force_ep)
     try:
         out, idx, gates, h1, u = r.forward()
         e1, e = _check_staged(inp, tb, out, idx, gates, h1, u)
-        print(f"{shape} ep={force_ep} swap={swap}: h1 rel {e1:.2e}, out rel {e:.2e}")
+        print(f"{shape} ep={force_ep} pair={pair}: h1 rel {e1:.2e}, out rel {e:.2e}")
     finally:
         r.close()
 
 
 @pytest.mark.parametrize("shape", [
-    dict(hidden=256, ffn=384, ne=8, k=2, T=300),
     dict(hidden=768, ffn=1792, ne=8, k=2, T=1100, S=1),
-    dict(hidden=4096, ffn=256, ne=2, k=1, T=1100),     # O-projection: 80 pair tiles (stream-K)
+    dict(hidden=4096, ffn=256, ne=2, k=1, T=1100),     # O-projection: 80 pair tiles, K = 4096
 ])
-@pytest.mark.parametrize("variant", ["tailswap", "alt", "device", "streamk"])
-def test_taskb_gemm_variants(shape, variant, monkeypatch):
-    """The residual-epilogue O-projection (and the expert GEMMs) through the opt-in GEMM paths:
-    swap-AB tail tiles, 224 / 192-wide pair tiles, device-side kernel selection."""
-    monkeypatch.setenv("MOE_GEMM_PAIR", "device" if variant == "device" else "1")
-    if variant == "tailswap":
-        monkeypatch.setenv("MOE_GEMM_TAILSWAP", "1")
-    elif variant == "streamk":
-        monkeypatch.setenv("MOE_GEMM_STREAMK", "1")
-    else:
-        monkeypatch.setenv("MOE_GEMM_ALT", "1")
+@pytest.mark.parametrize("groupm", ["1", "3"])
+def test_taskb_raster_groups(shape, groupm, monkeypatch):
+    """The residual-epilogue O-projection (and the expert GEMMs) on the CTA-pair kernel with
+    several raster groups per launch, the last one partial (MOE_GEMM_GROUPM)."""
+    monkeypatch.setenv("MOE_GEMM_PAIR", "1")
+    monkeypatch.setenv("MOE_GEMM_GROUPM", groupm)
     inp, tb = _inputs(shape["hidden"], shape["ffn"], shape["ne"], shape["k"], shape["T"],
                       shape.get("S", 0))
     r = TaskBRun(inp, tb)
@@ -165,14 +161,19 @@ def test_taskb_end_to_end_vs_pure_oracle():
 
 @pytest.mark.parametrize("name", ["mixtral_8x7b", "dsv2_lite"])
 def test_taskb_full_size(name):
-    """BASELINE.json sizes: routing bit-exact on every token, other stages on sampled tokens."""
+    """BASELINE.json sizes: routing bit-exact on every token; the other stages on a stratified
+    token set -- the first and last token of every 128-token O-projection M tile, and every
+    (expert, 128-row M tile) of the MoE's permuted layout (gpu_helpers.stratified_tokens)."""
     cfg = synth.CONFIGS[name]
     inp = synth.gen_inputs(cfg)
     tb = synth.gen_taskb(cfg, inp.x)
     r = TaskBRun(inp, tb)
     try:
         out, idx, gates, h1, u = r.forward()
-        sel = sample_tokens(cfg.tokens, 16)
+        sel = np.union1d(np.union1d(block_tokens(cfg.tokens),
+                                    stratified_tokens(idx.cpu().numpy(), cfg.num_experts,
+                                                      cfg.num_shared)),
+                         sample_tokens(cfg.tokens, 16))
         e1, e = _check_staged(inp, tb, out, idx, gates, h1, u, rows=sel)
         print(f"{name}: h1 rel {e1:.2e}, out rel {e:.2e} over {len(sel)} tokens")
     finally:

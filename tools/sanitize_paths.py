@@ -1,7 +1,7 @@
 """Small runs of every engine path for compute-sanitizer (memcheck / racecheck / synccheck):
-tiny MoE layer, GPU Task B, grouped launches over many small experts, CTA-pair + tail split,
-in-process P2P expert parallelism (W = 2), the opt-in GEMM variants (swap-AB tail tiles,
-224/192-wide pair tiles, device-side kernel choice) and the Contiguous Data Mover."""
+tiny MoE layer, GPU Task B, grouped launches over many small experts, the CTA-pair kernel with
+several raster groups, in-process P2P expert parallelism (W = 2), both GEMM kernels with
+several experts per launch, and the Contiguous Data Mover."""
 import os, sys, threading
 sys.path.insert(0, "."); sys.path.insert(0, "tests")
 import numpy as np, torch
@@ -24,12 +24,12 @@ torch.cuda.synchronize(); r.layer.sync(); hl.close(); r.close()
 cfg = synth.MoEConfig("custom", 21, 256, 256, 32, 4, 300, 2)
 inp = synth.gen_inputs(cfg)
 r = GpuRun(inp); r.run(); r.run(); r.close()
-# 3. CTA-pair kernel with the tail split
-os.environ["MOE_GEMM_PAIR"] = "1"; os.environ["MOE_GEMM_TAILSPLIT"] = "1"
+# 3. CTA-pair kernel with several raster groups per launch
+os.environ["MOE_GEMM_PAIR"] = "1"; os.environ["MOE_GEMM_GROUPM"] = "1"
 cfg = synth.MoEConfig("custom", 22, 256, 384, 8, 2, 700, 1)
 inp = synth.gen_inputs(cfg)
 r = GpuRun(inp); r.run(); r.close()
-del os.environ["MOE_GEMM_PAIR"], os.environ["MOE_GEMM_TAILSPLIT"]
+del os.environ["MOE_GEMM_PAIR"], os.environ["MOE_GEMM_GROUPM"]
 # 4. in-process P2P expert parallelism, W = 2
 W = 2
 cfg = synth.MoEConfig("custom", 23, 256, 256, 8, 2, 200, 1)
@@ -58,12 +58,11 @@ th = [threading.Thread(target=work, args=(q,)) for q in range(W)]
 for l in ly: l.close()
 for e in ex: e.close()
 full.close()
-# 5. GEMM variants: swap-AB tail tiles, 224/192-wide tiles, device-side kernel choice
+# 5. both GEMM kernels with several routed experts per launch (MOE_GEMM_ROWS)
 cfg = synth.MoEConfig("custom", 24, 768, 1792, 8, 2, 700, 1)
 inp = synth.gen_inputs(cfg)
-for env in ({"MOE_GEMM_PAIR": "1", "MOE_GEMM_TAILSWAP": "1"},
-            {"MOE_GEMM_PAIR": "1", "MOE_GEMM_ALT": "1"},
-            {"MOE_GEMM_PAIR": "device", "MOE_GEMM_ALT": "1"}):
+for env in ({"MOE_GEMM_PAIR": "1", "MOE_GEMM_ROWS": "100000"},
+            {"MOE_GEMM_PAIR": "0", "MOE_GEMM_ROWS": "100000"}):
     os.environ.update(env)
     r = GpuRun(inp); r.run(); r.close()
     for k in env: del os.environ[k]
