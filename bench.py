@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--taskb", action="store_true",
                     help="time GPU Task B (O-projection + RMSNorm + MoE layer, streamed Wo) "
                          "instead of the MoE layer alone (no cpu leg)")
+    ap.add_argument("--partitions", type=int, default=1, choices=[1, 2],
+                    help="--taskb e2e: 2 = VSLPipe's alpha / beta token partitions through one "
+                         "stream of the layer's weights (moe_taskb_forward2_host, PAPER.md:795-801)")
     ap.add_argument("--ep-transport", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1: p2p = fused dispatch/combine over peer memory (CUDA IPC), "
                          "falling back to NCCL if the peers cannot be mapped; nccl = NCCL "
@@ -354,7 +357,7 @@ def run_ours(args):
             return
         layer.forward(xs[l], routers[l], experts[l], outs[l], idxs[l], gws[l], stream=sh)
 
-    def timed(fn, sampler=None):
+    def timed(fn, sampler=None, fence=None):
         for i in range(args.warmup):
             fn(i)
         torch.cuda.synchronize()
@@ -368,6 +371,8 @@ def run_ours(args):
         evs[0].record(stream)
         for i in range(args.steps):
             fn(args.warmup + i)
+            if fence is not None and i == args.steps - 1:
+                fence()          # the last step's result copy (library D2H stream) is in the region
             evs[i + 1].record(stream)
         torch.cuda.synchronize()
         if sampler is not None:
@@ -479,24 +484,43 @@ def run_ours(args):
 
         if args.taskb:   # attention output from host memory (the paper's CPU attention)
             xh = [a.cpu().pin_memory() for a in attns]
+        half = Tr // 2   # --partitions 2: alpha = the first half of the rank's tokens
+        if args.partitions == 2:
+            if not args.taskb:
+                raise SystemExit("--partitions 2 needs --taskb (VSLPipe's partitions are Task B's)")
+            xh2 = [[x[:half], x[half:]] for x in xh]
+            oh2 = [[o[:half], o[half:]] for o in oh]
+            rs2 = [[r[:half], r[half:]] for r in resids]
 
         def step_h(i):
             l = i % args.layers
+            if args.taskb and args.partitions == 2:
+                layer.taskb_forward2_host(xh2[l], rs2[l], hls[l], tbs[l].eps, routers[l],
+                                          experts[l], oh2[l], stream=sh)
+                return
             if args.taskb:
                 layer.taskb_forward_host(xh[l], resids[l], hls[l], tbs[l].eps, routers[l],
                                          experts[l], oh[l], stream=sh)
                 return
             layer.forward_host(xh[l], routers[l], experts[l], oh[l], stream=sh)
 
-        ems = timed(step_h)
+        ems = timed(step_h, fence=lambda: layer.wait_output(sh))
+        est = layer.stats()
         tok_bytes = T * cfg.hidden * 2
         e2e = {"value": T / (ems / 1e3), "unit": "tokens/s", "ms_per_step": ems,
                "h2d_bytes_per_step": tok_bytes + step_weight_bytes,
                "h2d_token_bytes_per_step": tok_bytes, "h2d_weight_bytes_per_step": step_weight_bytes,
                "d2h_bytes_per_step": tok_bytes,
-               "api": ("moe_taskb_forward_host (pinned host attention output / result, device "
+               "api": ("moe_taskb_forward2_host (two token partitions alpha/beta, one weight "
+                       "stream)" if args.taskb and args.partitions == 2 else
+                       "moe_taskb_forward_host (pinned host attention output / result, device "
                        "residual)" if args.taskb else
-                       "moe_layer_forward_host (pinned host hidden/out)")}
+                       "moe_layer_forward_host (pinned host hidden/out)"),
+               "token_copy_latency_ms": {
+                   "per_partition": [est["part_latency_ms"][p] / max(1, est["part_copies"][p])
+                                     for p in range(2)],
+                   "copies": est["part_copies"],
+                   "note": "enqueue -> resident of each host token copy (partition 1 = beta)"}}
         last = (args.warmup + args.steps - 1) % args.layers
         e2e["matches_device_path"] = bool(allmax(0.0 if torch.equal(oh[last].cuda(), outs[last]) else 1.0) == 0.0)
 

@@ -153,8 +153,11 @@ moe_status moe_layer_forward(moe_ctx ctx, const void* hidden, int32_t num_tokens
 /*
  * Same as moe_layer_forward with HOST token buffers: hidden_host (pinned bf16 [T,h]) is copied
  * to the device on the copy stream ahead of the call's expert weights, and the result is copied
- * back into out_host (pinned bf16 [T,h]); both copies are ordered on `stream`.  topk_* are
- * optional DEVICE buffers as above.  End-to-end entry point (bench "e2e").
+ * back into out_host (pinned bf16 [T,h]) on the library's result-copy stream once the call's
+ * combine has run -- work enqueued on `stream` after the call does NOT wait for that copy.
+ * out_host is complete when moe_sync() returns, or once `stream` passes a moe_wait_output()
+ * issued after the call.  topk_* are optional DEVICE buffers as above (written in `stream`
+ * order).  End-to-end entry point (bench "e2e").
  */
 moe_status moe_layer_forward_host(moe_ctx ctx, const void* hidden_host, int32_t num_tokens,
                                   const void* router_w, const void* const* experts, int32_t top_k,
@@ -208,6 +211,35 @@ moe_status moe_taskb_forward_host(moe_ctx ctx, const void* attn_host, const void
                                   const void* router_w, const void* const* experts, int32_t top_k,
                                   void* out_host, int32_t* topk_idx, float* topk_w, void* stream);
 
+/* Enqueue on `stream` a wait for the result copies (into out_host) of every host-buffer call
+ * issued so far on this context; `stream` may be any stream of the context's device. */
+moe_status moe_wait_output(moe_ctx ctx, void* stream);
+
+/*
+ * GPU Task B over TWO token partitions through ONE stream of the layer's weights -- VSLPipe's
+ * alpha / beta groups ("partitions them into two groups, alpha and beta ... In
+ * each phase, CPU-side attention computations for one partition run concurrently with GPU-side
+ * GEMM operations for the other"; the data mover keeps the attention transfers from being
+ * head-of-line blocked by weight packets).  Partition p in {0 = alpha,
+ * 1 = beta} has num_tokens[p] >= 0 tokens; attn_host[p] (pinned bf16 [T_p, h]), resid[p] (device
+ * bf16 [T_p, h]) and out_host[p] (pinned bf16 [T_p, h]) as moe_taskb_forward_host.  Order:
+ *   alpha's attention copy; Wo|gamma (streamed once); alpha's O-projection + norm; the call's first
+ *   expert copies; THEN beta's attention copy (with MOE_FLAG_MOVER it waits behind at most one
+ *   weight packet, else behind those expert copies); beta's O-projection + norm; routing over
+ *   T_0 + T_1 tokens; every expert streamed once, its GEMMs covering both partitions' rows;
+ *   alpha's rows combined first and copied back while beta's rows are combined.
+ * topk_idx / topk_w: optional device [T_0 + T_1, k], alpha's rows then beta's.  The outputs are
+ * bitwise those of moe_taskb_forward_host on each partition in turn, for one layer's weight
+ * traffic.  T_0 + T_1 <= max_tokens; either may be 0 (then this is moe_taskb_forward_host).
+ * Per-partition token-copy latencies: moe_stats.part_latency_ms (MOE_FLAG_PROFILE).
+ */
+moe_status moe_taskb_forward2_host(moe_ctx ctx, const void* const attn_host[2],
+                                   const void* const resid[2], const int32_t num_tokens[2],
+                                   const void* layer, float eps, const void* router_w,
+                                   const void* const* experts, int32_t top_k,
+                                   void* const out_host[2], int32_t* topk_idx, float* topk_w,
+                                   void* stream);
+
 /* Block until all work of the context is done; returns the first pending async error. */
 moe_status moe_sync(moe_ctx ctx);
 
@@ -224,7 +256,7 @@ typedef struct {
     double route_ms, permute_ms, gemm1_ms, gemm2_ms, combine_ms, comm_ms;
     int64_t num_slots;            /* expert staging slots in use                              */
     int64_t comm_bytes;           /* bytes this rank sent in EP dispatch + combine            */
-    int64_t host_calls;           /* moe_layer_forward_host calls                             */
+    int64_t host_calls;           /* host-buffer calls (moe_*_host)                            */
     double token_latency_ms;      /* sum over host calls: enqueue -> tokens resident on the GPU */
     int64_t taskb_calls;          /* moe_taskb_forward calls (each also counts in `calls`)    */
     double oproj_ms, norm_ms;     /* Task B: O-projection GEMM, RMSNorm                       */
@@ -232,6 +264,11 @@ typedef struct {
      * ns of CTA 0 from its first to its last instruction, summed over launches -- the clock the
      * tensor-core roofline of those kernels must be scaled to (power management).  0 = none. */
     double gemm1_sm_mhz, gemm2_sm_mhz;
+    /* Host token copies per partition (0: the only / alpha partition, 1: beta of
+     * moe_taskb_forward2_host) and their summed enqueue -> resident latency (MOE_FLAG_PROFILE);
+     * token_latency_ms is their total. */
+    int64_t part_copies[2];
+    double part_latency_ms[2];
 } moe_stats;
 
 moe_status moe_get_stats(moe_ctx ctx, moe_stats* out);   /* synchronises the context */

@@ -36,7 +36,7 @@ EXPORTED = ["moe_packed_expert_bytes", "moe_pack_expert", "moe_host_alloc", "moe
             "moe_last_error", "moe_probe_h2d", "moe_ep_plan", "moe_nccl_unique_id",
             "moe_packed_layer_bytes", "moe_pack_layer", "moe_taskb_forward",
             "moe_taskb_forward_host", "moe_ep_ipc_handle", "moe_ep_ipc_connect",
-            "moe_ep_ipc_selftest"]
+            "moe_ep_ipc_selftest", "moe_wait_output", "moe_taskb_forward2_host"]
 MOE_FLAG_IPC_EP = 8
 MOE_FLAG_MOVER = 16
 MOE_IPC_HANDLE_BYTES = 512
@@ -64,10 +64,14 @@ class moe_stats(ctypes.Structure):
                 ("host_calls", ctypes.c_int64), ("token_latency_ms", ctypes.c_double),
                 ("taskb_calls", ctypes.c_int64), ("oproj_ms", ctypes.c_double),
                 ("norm_ms", ctypes.c_double), ("gemm1_sm_mhz", ctypes.c_double),
-                ("gemm2_sm_mhz", ctypes.c_double)]
+                ("gemm2_sm_mhz", ctypes.c_double), ("part_copies", ctypes.c_int64 * 2),
+                ("part_latency_ms", ctypes.c_double * 2)]
 
     def as_dict(self):
-        return {f: getattr(self, f) for f, _ in self._fields_}
+        d = {f: getattr(self, f) for f, _ in self._fields_}
+        for f in ("part_copies", "part_latency_ms"):
+            d[f] = list(d[f])
+        return d
 
 
 class moe_debug_view(ctypes.Structure):
@@ -126,6 +130,8 @@ def load(path: str = LIB_PATH):
     lib.moe_ep_ipc_handle.argtypes = [P, P]
     lib.moe_ep_ipc_connect.argtypes = [P, P]
     lib.moe_ep_ipc_selftest.argtypes = [P, ctypes.c_double]
+    lib.moe_wait_output.argtypes = [P, P]
+    lib.moe_taskb_forward2_host.argtypes = [P, P, P, P, P, ctypes.c_float, P, P, i32, P, P, P, P]
     for name in EXPORTED:
         if name not in ("moe_packed_expert_bytes", "moe_status_string", "moe_last_error",
                         "moe_ep_plan", "moe_packed_layer_bytes"):
@@ -211,6 +217,24 @@ def moe_taskb_forward_host(ctx: int, attn_host: int, resid: int, num_tokens: int
                                          layer or None, eps, router_w, experts, top_k,
                                          out_host or None, topk_idx or None, topk_w or None,
                                          stream or None), ctx)
+
+
+def moe_taskb_forward2_host(ctx: int, attn_host: Sequence[int], resid: Sequence[int],
+                            num_tokens: Sequence[int], layer: int, eps: float, router_w: int,
+                            experts, top_k: int, out_host: Sequence[int], topk_idx: int = 0,
+                            topk_w: int = 0, stream: int = 0) -> None:
+    """Two token partitions (alpha, beta) through one stream of the layer's weights."""
+    a = (ctypes.c_void_p * 2)(*[p or None for p in attn_host])
+    r = (ctypes.c_void_p * 2)(*[p or None for p in resid])
+    n = (ctypes.c_int32 * 2)(*num_tokens)
+    o = (ctypes.c_void_p * 2)(*[p or None for p in out_host])
+    _check(load().moe_taskb_forward2_host(ctx, a, r, n, layer or None, eps, router_w, experts,
+                                          top_k, o, topk_idx or None, topk_w or None,
+                                          stream or None), ctx)
+
+
+def moe_wait_output(ctx: int, stream: int = 0) -> None:
+    _check(load().moe_wait_output(ctx, stream or None), ctx)
 
 
 def moe_ep_ipc_handle(ctx: int) -> bytes:
@@ -415,6 +439,23 @@ class MoELayer:
                                out_host.data_ptr() if T else 0,
                                topk_idx.data_ptr() if topk_idx is not None else 0,
                                topk_w.data_ptr() if topk_w is not None else 0, stream)
+
+    def taskb_forward2_host(self, attn_host, resid, layer: HostLayer, eps: float, router_w,
+                            experts: HostExperts, out_host, topk_idx=None, topk_w=None,
+                            stream: int = 0):
+        """GPU Task B over two partitions (sequences of 2 pinned host attention outputs, 2 device
+        residuals, 2 pinned host outputs) with the layer's weights streamed once."""
+        moe_taskb_forward2_host(
+            self.ctx, [a.data_ptr() if a.shape[0] else 0 for a in attn_host],
+            [r.data_ptr() if r.shape[0] else 0 for r in resid], [a.shape[0] for a in attn_host],
+            layer.ptr, eps, router_w.data_ptr(), experts.array, self.top_k,
+            [o.data_ptr() if o.shape[0] else 0 for o in out_host],
+            topk_idx.data_ptr() if topk_idx is not None else 0,
+            topk_w.data_ptr() if topk_w is not None else 0, stream)
+
+    def wait_output(self, stream: int = 0):
+        """Make `stream` wait for the result copies of the host-buffer calls issued so far."""
+        moe_wait_output(self.ctx, stream)
 
     def ipc_handle(self) -> bytes:
         return moe_ep_ipc_handle(self.ctx)

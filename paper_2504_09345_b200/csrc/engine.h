@@ -13,8 +13,9 @@
 
 namespace moe {
 
+// kRecTokenA / B: enqueue -> resident latency of a host token copy of partition 0 / 1
 enum RecKind { kRecH2D = 0, kRecRoute, kRecPermute, kRecGemm1, kRecGemm2, kRecCombine, kRecComm,
-               kRecTokenLatency, kRecOproj, kRecNorm, kRecKinds };
+               kRecTokenA, kRecTokenB, kRecOproj, kRecNorm, kRecKinds };
 
 struct Rec {
     int kind;
@@ -181,6 +182,15 @@ struct moe_ctx_s {
     __nv_bfloat16* x_dev[2] = {nullptr, nullptr};
     __nv_bfloat16* out_dev[2] = {nullptr, nullptr};
     cudaEvent_t xbuf_free[2] = {}, x_ready[2] = {};
+    cudaEvent_t x_ready_b[2] = {};      // [parity] partition 1's tokens resident (2-partition Task B)
+    // Result copies (device -> pinned host) run on their own stream, so the caller's stream never
+    // waits for them (the next call's shared-expert GEMMs and routing start at once):
+    // comb_ev[p] = partition p combined (recorded on the caller's stream); d2h_done[b] = the copy
+    // out of out_dev[b] finished (the call reusing out_dev[b] waits for it); out_ev = the last
+    // result copy finished (moe_wait_output, moe_sync).
+    cudaStream_t d2h_stream = nullptr;
+    cudaEvent_t comb_ev[2] = {}, d2h_done[2] = {};
+    cudaEvent_t out_ev = nullptr;
     int host_parity = 0;
 
     // profiling

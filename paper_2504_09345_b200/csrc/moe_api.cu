@@ -15,6 +15,7 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <mutex>
 
 #include "engine.h"
@@ -283,11 +284,25 @@ moe_status launch_grouped(moe_ctx c, int mode, int bn, const int64_t* rows,
     return MOE_OK;
 }
 
+// Optional parts of a call (GPU Task B with two token partitions, moe_taskb_forward2_host):
+//   pre_route   runs after the call's first weight copies are requested and before any routing
+//               (the late partition's token copy + O-projection + norm go there, so its copy
+//               queues behind this call's weight requests -- the head-of-line case the data
+//               mover is for);
+//   split_at    0 < split_at < T: the combine runs as rows [0, split_at) then [split_at, T), with
+//               split_ev recorded between them (the first partition's result copy starts while
+//               the second is still being combined).
+struct FwdExtra {
+    std::function<moe_status()> pre_route;
+    int split_at = 0;
+    cudaEvent_t split_ev = nullptr;
+};
+
 // resid (Task B): added to every output row in the combine (nullptr for the plain MoE layer).
 moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __nv_bfloat16* wr,
                         const void* const* experts, __nv_bfloat16* out, int32_t* topk_idx,
                         float* topk_w, cudaStream_t st, bool hidden_on_copy_stream, int xb,
-                        const __nv_bfloat16* resid = nullptr) {
+                        const __nv_bfloat16* resid = nullptr, const FwdExtra* ex = nullptr) {
     const moe_config& cf = c->cfg;
     const int h = cf.hidden, hi = cf.ffn, ne = cf.num_experts, k = cf.top_k, S = cf.num_shared;
     const int n_tiles = (T + moe::kRouteTile - 1) / moe::kRouteTile;
@@ -319,6 +334,10 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         if (s != MOE_OK) return s;
     }
     if (hidden_on_copy_stream) MOE_CUDA(c, cudaStreamWaitEvent(st, c->x_ready[xb], 0));
+    if (ex && ex->pre_route) {
+        moe_status s = ex->pre_route();
+        if (s != MOE_OK) return s;
+    }
 
     // One GEMM1 + one GEMM2 launch per DMA batch (flush_copies): the batch's experts sit in
     // adjacent slots of the staging buffer and their tiles are scheduled together (GemmBatch),
@@ -484,11 +503,28 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     }
     {
         Prof p(c, moe::kRecCombine, st);
-        MOE_CUDA(c, moe::launch_combine(c->y_perm, c->pos, gates, T, h, k, S, (int64_t)T * k,
-                                        resid, out, idx, c->offsets,
-                                        c->p2p ? c->pr_y : nullptr, st));
+        // rows [r0, r1) of the call's tokens (two launches when the call is split, FwdExtra)
+        auto combine = [&](int r0, int r1) -> moe_status {
+            MOE_CUDA(c, moe::launch_combine(c->y_perm, c->pos + (int64_t)r0 * k, gates + (int64_t)r0 * k,
+                                            r1 - r0, h, k, S, (int64_t)T * k + r0, T,
+                                            resid ? resid + (int64_t)r0 * h : nullptr,
+                                            out + (int64_t)r0 * h, idx + (int64_t)r0 * k, c->offsets,
+                                            c->p2p ? c->pr_y : nullptr, st));
+            c->stats.kernel_launches += 1;
+            return MOE_OK;
+        };
+        const int split = (ex && ex->split_at > 0 && ex->split_at < T) ? ex->split_at : 0;
+        if (split) {
+            moe_status cs = combine(0, split);
+            if (cs != MOE_OK) return cs;
+            if (ex->split_ev) MOE_CUDA(c, cudaEventRecord(ex->split_ev, st));
+            cs = combine(split, T);
+            if (cs != MOE_OK) return cs;
+        } else if (T > 0) {
+            moe_status cs = combine(0, T);
+            if (cs != MOE_OK) return cs;
+        }
         p.end();
-        c->stats.kernel_launches += 1;
     }
     if (c->p2p) {
         moe_status s = moe::p2p_after_combine(c, st);
@@ -530,10 +566,9 @@ moe_status validate_call(moe_ctx c, int32_t T, const void* router_w, const void*
     return MOE_OK;
 }
 
-// Host-buffer entry points: copy `bytes` of pinned host tokens into device buffer x_dev[*b] (two
-// buffers alternate between calls) on the weight stream, just ahead of the call's weights (see
-// engine.h token_lane); x_ready[*b] marks them resident.  Allocates the buffers on first use.
-moe_status stage_host_tokens(moe_ctx c, const void* host, size_t bytes, int* b_out) {
+// Host-buffer entry points.  Two device token buffers x_dev / out_dev alternate between calls
+// (parity b = host_buffer()); allocated on first use.
+moe_status host_buffer(moe_ctx c, int* b_out) {
     if (!c->x_dev[0]) {
         const size_t cap = (size_t)c->cfg.max_tokens * c->cfg.hidden * 2;
         for (int i = 0; i < 2; ++i) {
@@ -543,8 +578,16 @@ moe_status stage_host_tokens(moe_ctx c, const void* host, size_t bytes, int* b_o
             }
         }
     }
-    const int b = c->host_parity;
+    *b_out = c->host_parity;
     c->host_parity ^= 1;
+    return MOE_OK;
+}
+
+// Copy `bytes` of pinned host tokens into x_dev[b] at byte offset `off` on the weight stream, in
+// enqueue order with the weight copies (see engine.h token_lane), and record `ready` there.
+// part: 0 / 1 -- the partition whose enqueue -> resident latency the stats attribute it to.
+moe_status stage_tokens(moe_ctx c, int b, const void* host, size_t bytes, size_t off,
+                        cudaEvent_t ready, int part) {
     cudaStream_t ts = c->token_lane ? c->token_stream : c->copy_stream;
     cudaEvent_t t0 = nullptr;
     const bool prof = (c->cfg.flags & MOE_FLAG_PROFILE) != 0;
@@ -553,16 +596,38 @@ moe_status stage_host_tokens(moe_ctx c, const void* host, size_t bytes, int* b_o
         MOE_CUDA(c, cudaEventRecord(t0, c->clock_stream));
     }
     MOE_CUDA(c, cudaStreamWaitEvent(ts, c->xbuf_free[b], 0));
-    MOE_CUDA(c, cudaMemcpyAsync(c->x_dev[b], host, bytes, cudaMemcpyHostToDevice, ts));
-    MOE_CUDA(c, cudaEventRecord(c->x_ready[b], ts));
+    MOE_CUDA(c, cudaMemcpyAsync(reinterpret_cast<char*>(c->x_dev[b]) + off, host, bytes,
+                                cudaMemcpyHostToDevice, ts));
+    MOE_CUDA(c, cudaEventRecord(ready, ts));
     if (prof) {
         cudaEvent_t t1 = moe::pool_get(c);
         MOE_CUDA(c, cudaEventRecord(t1, ts));
-        c->pending.push_back(moe::Rec{moe::kRecTokenLatency, t0, t1});
+        c->pending.push_back(moe::Rec{part ? moe::kRecTokenB : moe::kRecTokenA, t0, t1});
     }
     c->stats.h2d_token_bytes += (int64_t)bytes;
-    c->stats.host_calls += 1;
-    *b_out = b;
+    c->stats.host_calls += part == 0 ? 1 : 0;
+    c->stats.part_copies[part] += 1;
+    return MOE_OK;
+}
+
+// Result copies of a host-buffer call into pinned host memory, on the context's D2H stream: part
+// p (rows [row0[p], row0[p] + rows[p]) of out_dev[b]) starts once ev[p] -- recorded on the caller's
+// stream after that part's combine -- has passed, so the copy overlaps whatever the caller's
+// stream runs next (the next call's shared-expert GEMMs and routing; the second partition's
+// combine).  d2h_done[b] guards out_dev[b] against the call that reuses it; out_ev is the
+// completion moe_wait_output / moe_sync wait on.
+moe_status copy_results(moe_ctx c, int b, int np, void* const* host, const int* row0,
+                        const int* rows, const cudaEvent_t* ev) {
+    const size_t rb = (size_t)c->cfg.hidden * 2;
+    for (int p = 0; p < np; ++p) {
+        if (rows[p] <= 0) continue;
+        MOE_CUDA(c, cudaStreamWaitEvent(c->d2h_stream, ev[p], 0));
+        MOE_CUDA(c, cudaMemcpyAsync(host[p], reinterpret_cast<char*>(c->out_dev[b]) + row0[p] * rb,
+                                    rows[p] * rb, cudaMemcpyDeviceToHost, c->d2h_stream));
+        c->stats.d2h_token_bytes += (int64_t)rows[p] * (int64_t)rb;
+    }
+    MOE_CUDA(c, cudaEventRecord(c->d2h_done[b], c->d2h_stream));
+    MOE_CUDA(c, cudaEventRecord(c->out_ev, c->d2h_stream));
     return MOE_OK;
 }
 
@@ -599,7 +664,7 @@ moe_status taskb_resources(moe_ctx c) {
     }
     ok &= cudaMalloc((void**)&c->h1_ws, act) == cudaSuccess;
     ok &= cudaMalloc((void**)&c->u_ws, act) == cudaSuccess;
-    ok &= cudaMalloc((void**)&c->oproj_grp, sizeof(GemmGroup)) == cudaSuccess;
+    ok &= cudaMalloc((void**)&c->oproj_grp, 2 * sizeof(GemmGroup)) == cudaSuccess;   // 2 partitions
     if (!ok) {
         taskb_release(c);
         return set_err(c, MOE_E_NOMEM, "Task B buffers (2 x %lld B layer slots + 2 x %zu B)",
@@ -618,14 +683,66 @@ moe_status taskb_resources(moe_ctx c) {
     return MOE_OK;
 }
 
-// b1 O-projection + residual, b2 RMSNorm, then the MoE layer on u with h1 as the combine's
-// residual (R19-R21).
-moe_status taskb_impl(moe_ctx c, const __nv_bfloat16* attn, const __nv_bfloat16* resid, int T,
+// One token partition of a Task B call: its attention output (rows [base, base + T) of the
+// A operand `tm_attn` maps), its residual rows, and the event that marks its attention output
+// resident (nullptr: already on the device, in stream order).
+struct TbPart {
+    const __nv_bfloat16* resid;
+    int T, base;
+    cudaEvent_t ready;
+};
+
+// b1 O-projection + residual and b2 RMSNorm of one partition (rows [base, base + T) of h1 / u).
+moe_status taskb_front(moe_ctx c, const CUtensorMap& tm_attn, const TbPart& pt, int lb, float eps,
+                       cudaStream_t st) {
+    const int h = c->cfg.hidden;
+    if (pt.T == 0) return MOE_OK;
+    const int gi = pt.base == 0 ? 0 : 1;   // oproj_grp entry of this partition
+    MOE_CUDA(c, moe::launch_fill_group(c->oproj_grp + gi, pt.base, pt.base + pt.T, 0, st));
+    if (pt.ready) MOE_CUDA(c, cudaStreamWaitEvent(st, pt.ready, 0));
+    MOE_CUDA(c, cudaStreamWaitEvent(st, c->lw_ready[lb], 0));
+    __nv_bfloat16* h1 = c->h1_ws + (int64_t)pt.base * h;
+    {
+        Prof p(c, moe::kRecOproj, st);
+        moe::GemmBatch ob{};
+        ob.table = c->oproj_grp + gi;
+        ob.n = 1;   // idx[0] = 0, b_row[0] = 0: Wo is the whole map
+        const int64_t rows = pt.T;
+        moe_status gs = launch_grouped(c, moe::kGemmResidual, c->bn2, &rows, &tm_attn,
+                                       &c->tm_wo[lb], &c->tm_wo_pair[lb], ob, h, h, h1, h, st,
+                                       pt.resid);
+        if (gs != MOE_OK) return gs;
+        p.end();
+    }
+    {
+        Prof p(c, moe::kRecNorm, st);
+        const __nv_bfloat16* gamma =
+            reinterpret_cast<const __nv_bfloat16*>(c->lw_slot[lb] + 2ll * h * h);
+        MOE_CUDA(c, moe::launch_rmsnorm(h1, gamma, pt.T, h, eps, c->u_ws + (int64_t)pt.base * h, st));
+        p.end();
+    }
+    c->stats.kernel_launches += 3;
+    return MOE_OK;
+}
+
+// GPU Task B over one or two token partitions (R19-R21): b1 O-projection
+// + residual, b2 RMSNorm, then the MoE layer on u with h1 as the combine's residual.  The layer
+// blob and the experts are streamed ONCE for all partitions.  Partition 0's front runs as soon as
+// its attention output and Wo are resident; partition 1's (`late`, the two-partition host call)
+// runs after the call's first expert copies are requested -- its token copy is issued there by
+// late->stage -- and the combine is split so partition 0's result can leave first (VSLPipe's
+// alpha / beta).
+struct TbLate {
+    TbPart part;
+    std::function<moe_status()> stage;   // issues partition 1's token copy
+};
+
+moe_status taskb_impl(moe_ctx c, const __nv_bfloat16* attn, const TbPart& p0, const TbLate* late,
                       const void* layer, float eps, const __nv_bfloat16* wr,
                       const void* const* experts, __nv_bfloat16* out, int32_t* topk_idx,
-                      float* topk_w, cudaStream_t st, bool attn_on_copy_stream = false,
-                      int xb = 0) {
+                      float* topk_w, cudaStream_t st, cudaEvent_t split_ev = nullptr) {
     const int h = c->cfg.hidden;
+    const int T = p0.T + (late ? late->part.T : 0);
     c->stats.taskb_calls += 1;
     // h1 / u are read by the previous call's combine: order after it (see forward_impl)
     MOE_CUDA(c, cudaStreamWaitEvent(st, c->done_ev, 0));
@@ -638,44 +755,38 @@ moe_status taskb_impl(moe_ctx c, const __nv_bfloat16* attn, const __nv_bfloat16*
         return set_err(c, MOE_E_CUDA, "cuTensorMapEncodeTiled failed for attn");
     // The layer weights ride the copy stream just ahead of this call's expert weights (nothing
     // is pending between calls: forward_impl flushes at its end).
-    const int b = (int)(c->lw_seq & 1);
+    const int lb = (int)(c->lw_seq & 1);
     c->lw_seq += 1;
-    MOE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->lw_free[b], 0));
+    MOE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->lw_free[lb], 0));
     {
         Prof p(c, moe::kRecH2D, c->copy_stream);
-        MOE_CUDA(c, cudaMemcpyAsync(c->lw_slot[b], layer, (size_t)c->layer_bytes,
+        MOE_CUDA(c, cudaMemcpyAsync(c->lw_slot[lb], layer, (size_t)c->layer_bytes,
                                     cudaMemcpyHostToDevice, c->copy_stream));
         p.end();
     }
-    MOE_CUDA(c, cudaEventRecord(c->lw_ready[b], c->copy_stream));
+    MOE_CUDA(c, cudaEventRecord(c->lw_ready[lb], c->copy_stream));
     c->stats.h2d_weight_bytes += c->layer_bytes;
 
-    MOE_CUDA(c, moe::launch_fill_group(c->oproj_grp, 0, T, 0, st));
-    if (attn_on_copy_stream) MOE_CUDA(c, cudaStreamWaitEvent(st, c->x_ready[xb], 0));
-    MOE_CUDA(c, cudaStreamWaitEvent(st, c->lw_ready[b], 0));
-    {
-        Prof p(c, moe::kRecOproj, st);
-        moe::GemmBatch ob{};
-        ob.table = c->oproj_grp;
-        ob.n = 1;   // idx[0] = 0, b_row[0] = 0: Wo is the whole map
-        const int64_t rows = T;
-        moe_status gs = launch_grouped(c, moe::kGemmResidual, c->bn2, &rows, &tm_attn,
-                                       &c->tm_wo[b], &c->tm_wo_pair[b], ob, h, h, c->h1_ws, h, st,
-                                       resid);
-        if (gs != MOE_OK) return gs;
-        p.end();
+    moe_status s = taskb_front(c, tm_attn, p0, lb, eps, st);
+    if (s != MOE_OK) return s;
+    FwdExtra ex;
+    if (late && late->part.T > 0) {
+        ex.pre_route = [&]() -> moe_status {
+            moe_status ls = late->stage();
+            if (ls != MOE_OK) return ls;
+            ls = taskb_front(c, tm_attn, late->part, lb, eps, st);
+            if (ls != MOE_OK) return ls;
+            MOE_CUDA(c, cudaEventRecord(c->lw_free[lb], st));
+            return MOE_OK;
+        };
+        ex.split_at = p0.T;
+        ex.split_ev = split_ev;
+    } else {
+        MOE_CUDA(c, cudaEventRecord(c->lw_free[lb], st));
     }
-    {
-        Prof p(c, moe::kRecNorm, st);
-        const __nv_bfloat16* gamma =
-            reinterpret_cast<const __nv_bfloat16*>(c->lw_slot[b] + 2ll * h * h);
-        MOE_CUDA(c, moe::launch_rmsnorm(c->h1_ws, gamma, T, h, eps, c->u_ws, st));
-        p.end();
-    }
-    MOE_CUDA(c, cudaEventRecord(c->lw_free[b], st));
-    c->stats.kernel_launches += 3;
     c->last_taskb_T = T;
-    return forward_impl(c, c->u_ws, T, wr, experts, out, topk_idx, topk_w, st, false, 0, c->h1_ws);
+    return forward_impl(c, c->u_ws, T, wr, experts, out, topk_idx, topk_w, st, false, 0, c->h1_ws,
+                        &ex);
 }
 
 }  // namespace
@@ -797,6 +908,8 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
                   cudaMemset(c->clk_acc, 0, 4 * sizeof(unsigned long long)) == cudaSuccess;
         }
         ok &= cudaEventCreateWithFlags(&c->done_ev, cudaEventDisableTiming) == cudaSuccess;
+        ok &= cudaEventCreateWithFlags(&c->out_ev, cudaEventDisableTiming) == cudaSuccess;
+        ok &= cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking) == cudaSuccess;
     }
     ok &= dalloc((void**)&c->slot_base, (size_t)c->blob_bytes * c->nslots);
     for (int i = 0; i < c->nslots; ++i) {
@@ -808,6 +921,9 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     for (int i = 0; i < 2; ++i) {
         ok &= cudaEventCreateWithFlags(&c->xbuf_free[i], cudaEventDisableTiming) == cudaSuccess;
         ok &= cudaEventCreateWithFlags(&c->x_ready[i], cudaEventDisableTiming) == cudaSuccess;
+        ok &= cudaEventCreateWithFlags(&c->x_ready_b[i], cudaEventDisableTiming) == cudaSuccess;
+        ok &= cudaEventCreateWithFlags(&c->d2h_done[i], cudaEventDisableTiming) == cudaSuccess;
+        ok &= cudaEventCreateWithFlags(&c->comb_ev[i], cudaEventDisableTiming) == cudaSuccess;
     }
     ok &= dalloc((void**)&c->idx_ws, sizeof(int32_t) * (size_t)Tm * k);
     ok &= dalloc((void**)&c->gates_ws, sizeof(float) * (size_t)Tm * k);
@@ -899,16 +1015,19 @@ moe_status moe_layer_forward_host(moe_ctx ctx, const void* hidden_host, int32_t 
     MOE_CUDA(ctx, cudaSetDevice(ctx->cfg.device));
     const size_t bytes = (size_t)num_tokens * c->cfg.hidden * 2;
     int b = 0;
-    s = stage_host_tokens(c, hidden_host, bytes, &b);
+    s = host_buffer(c, &b);
     if (s != MOE_OK) return s;
+    s = stage_tokens(c, b, hidden_host, bytes, 0, c->x_ready[b], 0);
+    if (s != MOE_OK) return s;
+    // out_dev[b] is rewritten by this call's combine: the result copy of two calls ago must be out
+    MOE_CUDA(c, cudaStreamWaitEvent(st, c->d2h_done[b], 0));
     s = forward_impl(c, c->x_dev[b], num_tokens, static_cast<const __nv_bfloat16*>(router_w),
                      experts, c->out_dev[b], topk_idx, topk_w, st, true, b);
     if (s != MOE_OK) return s;
     MOE_CUDA(c, cudaEventRecord(c->xbuf_free[b], st));
-    MOE_CUDA(c, cudaMemcpyAsync(out_host, c->out_dev[b], bytes, cudaMemcpyDeviceToHost, st));
-    c->stats.d2h_token_bytes += (int64_t)bytes;
-    MOE_CUDA(c, cudaEventRecord(c->done_ev, st));   // moe_sync covers the result copy
-    return MOE_OK;
+    MOE_CUDA(c, cudaEventRecord(c->comb_ev[0], st));
+    const int r0 = 0, rows = num_tokens;
+    return copy_results(c, b, 1, &out_host, &r0, &rows, c->comb_ev);
 }
 
 int64_t moe_packed_layer_bytes(int32_t hidden) {
@@ -947,8 +1066,8 @@ moe_status moe_taskb_forward(moe_ctx ctx, const void* attn, const void* resid, i
     MOE_CUDA(ctx, cudaSetDevice(ctx->cfg.device));
     s = taskb_resources(ctx);
     if (s != MOE_OK) return s;
-    return taskb_impl(ctx, static_cast<const __nv_bfloat16*>(attn),
-                      static_cast<const __nv_bfloat16*>(resid), num_tokens, layer, eps,
+    const TbPart p0{static_cast<const __nv_bfloat16*>(resid), num_tokens, 0, nullptr};
+    return taskb_impl(ctx, static_cast<const __nv_bfloat16*>(attn), p0, nullptr, layer, eps,
                       static_cast<const __nv_bfloat16*>(router_w), experts,
                       static_cast<__nv_bfloat16*>(out), topk_idx, topk_w,
                       static_cast<cudaStream_t>(stream));
@@ -958,42 +1077,86 @@ moe_status moe_taskb_forward_host(moe_ctx ctx, const void* attn_host, const void
                                   int32_t num_tokens, const void* layer, float eps,
                                   const void* router_w, const void* const* experts, int32_t top_k,
                                   void* out_host, int32_t* topk_idx, float* topk_w, void* stream) {
-    moe_status s = validate_call(ctx, num_tokens, router_w, experts, top_k);
-    if (s != MOE_OK || (num_tokens == 0 && !ctx->ep)) return s;
+    const void* a[2] = {attn_host, nullptr};
+    const void* r[2] = {resid, nullptr};
+    const int32_t n[2] = {num_tokens, 0};
+    void* o[2] = {out_host, nullptr};
+    return moe_taskb_forward2_host(ctx, a, r, n, layer, eps, router_w, experts, top_k, o, topk_idx,
+                                   topk_w, stream);
+}
+
+moe_status moe_taskb_forward2_host(moe_ctx ctx, const void* const attn_host[2],
+                                   const void* const resid[2], const int32_t num_tokens[2],
+                                   const void* layer, float eps, const void* router_w,
+                                   const void* const* experts, int32_t top_k,
+                                   void* const out_host[2], int32_t* topk_idx, float* topk_w,
+                                   void* stream) {
+    if (!ctx || !attn_host || !resid || !num_tokens || !out_host) return MOE_E_INVAL;
+    if (num_tokens[0] < 0 || num_tokens[1] < 0)
+        return set_err(ctx, MOE_E_INVAL, "negative partition size");
+    const int T = num_tokens[0] + num_tokens[1];
+    moe_status s = validate_call(ctx, T, router_w, experts, top_k);
+    if (s != MOE_OK || (T == 0 && !ctx->ep)) return s;
     if (!(eps >= 0.0f) || !std::isfinite(eps))
         return set_err(ctx, MOE_E_INVAL, "eps must be finite and >= 0");
     moe_ctx c = ctx;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     MOE_CUDA(c, cudaSetDevice(c->cfg.device));
-    if (num_tokens == 0) {  // EP: this rank still serves the other ranks' tokens
+    if (!layer) return set_err(c, MOE_E_INVAL, "NULL layer");
+    if (!is_pinned(layer)) return set_err(c, MOE_E_NOT_PINNED, "layer must be page-locked");
+    if (T == 0) {  // EP: this rank still serves the other ranks' tokens
         s = taskb_resources(c);
         if (s != MOE_OK) return s;
-        return taskb_impl(c, nullptr, nullptr, 0, layer, eps,
+        const TbPart none{nullptr, 0, 0, nullptr};
+        return taskb_impl(c, nullptr, none, nullptr, layer, eps,
                           static_cast<const __nv_bfloat16*>(router_w), experts, nullptr, topk_idx,
                           topk_w, st);
     }
-    if (!attn_host || !resid || !out_host || !layer)
-        return set_err(c, MOE_E_INVAL, "NULL attn_host / resid / out_host / layer");
-    if (((uintptr_t)resid & 15) || !is_device(resid))
-        return set_err(c, MOE_E_INVAL, "resid must be 16-byte aligned device memory");
+    for (int p = 0; p < 2; ++p) {
+        if (num_tokens[p] == 0) continue;
+        if (!attn_host[p] || !resid[p] || !out_host[p])
+            return set_err(c, MOE_E_INVAL, "NULL attn_host / resid / out_host of partition %d", p);
+        if (((uintptr_t)resid[p] & 15) || !is_device(resid[p]))
+            return set_err(c, MOE_E_INVAL, "resid[%d] must be 16-byte aligned device memory", p);
+        if (!is_pinned(attn_host[p]) || !is_pinned(out_host[p]))
+            return set_err(c, MOE_E_NOT_PINNED, "attn_host/out_host[%d] must be page-locked", p);
+    }
     if ((topk_idx && !is_device(topk_idx)) || (topk_w && !is_device(topk_w)))
         return set_err(c, MOE_E_INVAL, "topk_idx/topk_w must be device memory");
-    if (!is_pinned(attn_host) || !is_pinned(out_host) || !is_pinned(layer))
-        return set_err(c, MOE_E_NOT_PINNED, "attn_host/out_host/layer must be page-locked");
     s = taskb_resources(c);
     if (s != MOE_OK) return s;
-    const size_t bytes = (size_t)num_tokens * c->cfg.hidden * 2;
+    const size_t rb = (size_t)c->cfg.hidden * 2;
     int b = 0;
-    s = stage_host_tokens(c, attn_host, bytes, &b);   // attention output: ahead of Wo + experts
+    s = host_buffer(c, &b);
     if (s != MOE_OK) return s;
-    s = taskb_impl(c, c->x_dev[b], static_cast<const __nv_bfloat16*>(resid), num_tokens, layer,
-                   eps, static_cast<const __nv_bfloat16*>(router_w), experts, c->out_dev[b],
-                   topk_idx, topk_w, st, true, b);
+    // the first non-empty partition is "alpha": its attention output goes ahead of Wo + experts
+    const int pa = num_tokens[0] > 0 ? 0 : 1, pb = 1 - pa;
+    const int Ta = num_tokens[pa], Tb = pa == 0 ? num_tokens[1] : 0;
+    s = stage_tokens(c, b, attn_host[pa], (size_t)Ta * rb, 0, c->x_ready[b], 0);
+    if (s != MOE_OK) return s;
+    MOE_CUDA(c, cudaStreamWaitEvent(st, c->d2h_done[b], 0));   // out_dev[b] free (see forward)
+    const TbPart p0{static_cast<const __nv_bfloat16*>(resid[pa]), Ta, 0, c->x_ready[b]};
+    TbLate late;
+    late.part = TbPart{static_cast<const __nv_bfloat16*>(resid[pb]), Tb, Ta, c->x_ready_b[b]};
+    late.stage = [&]() {   // beta's attention output: queued behind this call's weight requests
+        return stage_tokens(c, b, attn_host[pb], (size_t)Tb * rb, (size_t)Ta * rb,
+                            c->x_ready_b[b], 1);
+    };
+    s = taskb_impl(c, c->x_dev[b], p0, Tb > 0 ? &late : nullptr, layer, eps,
+                   static_cast<const __nv_bfloat16*>(router_w), experts, c->out_dev[b], topk_idx,
+                   topk_w, st, c->comb_ev[0]);
     if (s != MOE_OK) return s;
     MOE_CUDA(c, cudaEventRecord(c->xbuf_free[b], st));
-    MOE_CUDA(c, cudaMemcpyAsync(out_host, c->out_dev[b], bytes, cudaMemcpyDeviceToHost, st));
-    c->stats.d2h_token_bytes += (int64_t)bytes;
-    MOE_CUDA(c, cudaEventRecord(c->done_ev, st));   // moe_sync covers the result copy
+    MOE_CUDA(c, cudaEventRecord(c->comb_ev[Tb > 0 ? 1 : 0], st));
+    void* const hosts[2] = {out_host[pa], Tb > 0 ? out_host[pb] : nullptr};
+    const int row0[2] = {0, Ta}, rows[2] = {Ta, Tb};
+    return copy_results(c, b, 2, hosts, row0, rows, c->comb_ev);
+}
+
+moe_status moe_wait_output(moe_ctx ctx, void* stream) {
+    if (!ctx) return MOE_E_INVAL;
+    MOE_CUDA(ctx, cudaSetDevice(ctx->cfg.device));
+    MOE_CUDA(ctx, cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), ctx->out_ev, 0));
     return MOE_OK;
 }
 
@@ -1019,6 +1182,7 @@ moe_status moe_sync(moe_ctx ctx) {
         if (ms != MOE_OK) return ms;
     }
     MOE_CUDA(ctx, cudaEventSynchronize(ctx->done_ev));     // the last call (see engine.h)
+    MOE_CUDA(ctx, cudaEventSynchronize(ctx->out_ev));      // its result copy (host-buffer calls)
     MOE_CUDA(ctx, cudaStreamSynchronize(ctx->copy_stream));
     if (ctx->token_stream) MOE_CUDA(ctx, cudaStreamSynchronize(ctx->token_stream));
     if (ctx->comm && moe::nccl_api()) {
@@ -1038,12 +1202,18 @@ moe_status moe_get_stats(moe_ctx ctx, moe_stats* out) {
     if (s != MOE_OK) return s;
     double* bucket[moe::kRecKinds] = {&ctx->stats.h2d_ms,   &ctx->stats.route_ms,   &ctx->stats.permute_ms,
                                       &ctx->stats.gemm1_ms, &ctx->stats.gemm2_ms,   &ctx->stats.combine_ms,
-                                      &ctx->stats.comm_ms,  &ctx->stats.token_latency_ms,
+                                      &ctx->stats.comm_ms,  &ctx->stats.part_latency_ms[0],
+                                      &ctx->stats.part_latency_ms[1],
                                       &ctx->stats.oproj_ms, &ctx->stats.norm_ms};
     for (const moe::Rec& r : ctx->pending) {
         float ms = 0.f;
-        if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) *bucket[r.kind] += ms;
-        else cudaGetLastError();
+        if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+            *bucket[r.kind] += ms;
+            if (r.kind == moe::kRecTokenA || r.kind == moe::kRecTokenB)
+                ctx->stats.token_latency_ms += ms;
+        } else {
+            cudaGetLastError();
+        }
         ctx->ev_pool.push_back(r.a);
         ctx->ev_pool.push_back(r.b);
     }
@@ -1128,7 +1298,8 @@ moe_status moe_destroy(moe_ctx c) {
     for (int i = 0; i < 2; ++i) {
         cudaFree(c->x_dev[i]);
         cudaFree(c->out_dev[i]);
-        cudaEvent_t evs[] = {c->xbuf_free[i], c->x_ready[i], c->lw_ready[i], c->lw_free[i]};
+        cudaEvent_t evs[] = {c->xbuf_free[i], c->x_ready[i], c->lw_ready[i], c->lw_free[i],
+                             c->x_ready_b[i], c->d2h_done[i], c->comb_ev[i]};
         for (cudaEvent_t e : evs)
             if (e) cudaEventDestroy(e);
         cudaFree(c->lw_slot[i]);
@@ -1141,6 +1312,8 @@ moe_status moe_destroy(moe_ctx c) {
     if (c->token_stream) cudaStreamDestroy(c->token_stream);
     if (c->clock_stream) cudaStreamDestroy(c->clock_stream);
     if (c->done_ev) cudaEventDestroy(c->done_ev);
+    if (c->out_ev) cudaEventDestroy(c->out_ev);
+    if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
     cudaGetLastError();
     delete c;
     return MOE_OK;

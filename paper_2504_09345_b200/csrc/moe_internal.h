@@ -108,12 +108,14 @@ cudaError_t launch_permute(const __nv_bfloat16* x, int T, int h, int k, int ne,
                            const int32_t* idx, const int32_t* tile_prefix,
                            const int32_t* offsets, __nv_bfloat16* x_perm, int32_t* pos,
                            const PeerRows* pr, cudaStream_t st);
-// a7: out[t] = sum_j g[t,j] * Y[pos[t,j]] + sum_s Y[R + s*T + t] (+ resid[t] if resid != NULL)
-//     (fp32, fixed order) -> bf16.  pr != NULL (P2P expert parallelism): routed rows are read
-//     from their owners' y_recv (PeerRows; needs idx and offsets), shared rows from y_perm.
+// a7: out[t] = sum_j g[t,j] * Y[pos[t,j]] + sum_s Y[R + s*stride + t] (+ resid[t] if resid !=
+//     NULL) (fp32, fixed order) -> bf16, for the T rows starting at the given pointers (a row
+//     range of a call: R = shared_base is then offset by the range's first row, stride = the
+//     call's T).  pr != NULL (P2P expert parallelism): routed rows are read from their owners'
+//     y_recv (PeerRows; needs idx and offsets), shared rows from y_perm.
 cudaError_t launch_combine(const __nv_bfloat16* y_perm, const int32_t* pos, const float* gates,
                            int T, int h, int k, int num_shared, int64_t shared_base,
-                           const __nv_bfloat16* resid, __nv_bfloat16* out,
+                           int64_t shared_stride, const __nv_bfloat16* resid, __nv_bfloat16* out,
                            const int32_t* idx, const int32_t* offsets, const PeerRows* pr,
                            cudaStream_t st);
 // Task B (b2): u[t] = RMSNorm(h1[t]) * gamma, reading R21:

@@ -370,7 +370,7 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int h, int k, int ne,
 __global__ void __launch_bounds__(256)
 combine_kernel(const __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ pos,
                const float* __restrict__ gates, int T, int h, int k, int num_shared,
-               int64_t shared_base, const __nv_bfloat16* __restrict__ resid,
+               int64_t shared_base, int64_t shared_stride, const __nv_bfloat16* __restrict__ resid,
                __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ idx,
                const int32_t* __restrict__ offsets, const PeerRows* __restrict__ pr) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -415,7 +415,7 @@ combine_kernel(const __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ 
             }
         }
         for (int s = 0; s < num_shared; ++s) {
-            const int64_t row = shared_base + (int64_t)s * T + t;
+            const int64_t row = shared_base + (int64_t)s * shared_stride + t;
             const int4 raw = ptx::ld_nc_v4(reinterpret_cast<const int4*>(y + (size_t)row * h) + v);
             const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
@@ -508,12 +508,13 @@ cudaError_t launch_permute(const __nv_bfloat16* x, int T, int h, int k, int ne,
 
 cudaError_t launch_combine(const __nv_bfloat16* y_perm, const int32_t* pos, const float* gates,
                            int T, int h, int k, int num_shared, int64_t shared_base,
-                           const __nv_bfloat16* resid, __nv_bfloat16* out,
+                           int64_t shared_stride, const __nv_bfloat16* resid, __nv_bfloat16* out,
                            const int32_t* idx, const int32_t* offsets, const PeerRows* pr,
                            cudaStream_t st) {
     if (T == 0) return cudaSuccess;
     combine_kernel<<<(T + 7) / 8, 256, 0, st>>>(y_perm, pos, gates, T, h, k, num_shared,
-                                                shared_base, resid, out, idx, offsets, pr);
+                                                shared_base, shared_stride, resid, out, idx,
+                                                offsets, pr);
     return cudaGetLastError();
 }
 

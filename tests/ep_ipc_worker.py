@@ -30,7 +30,8 @@ def run_rank(rank, world, port, cfg_tuple, calls, device, q):
         ids = list(range(rank * nl, (rank + 1) * nl)) + [ne + s for s in range(S)]
         experts = HostExperts(cfg.hidden, cfg.ffn, [inp.w1[i] for i in ids],
                               [inp.w3[i] for i in ids], [inp.w2[i] for i in ids])
-        layer = MoELayer(cfg.hidden, cfg.ffn, ne, cfg.top_k, max(1, hi - lo), num_shared=S,
+        cap = max(1, -(-T // world))   # one capacity on every rank (checked at connect)
+        layer = MoELayer(cfg.hidden, cfg.ffn, ne, cfg.top_k, cap, num_shared=S,
                          device=device, world_size=world, rank=rank, ipc_ep=True)
         handles = [None] * world
         dist.all_gather_object(handles, layer.ipc_handle())

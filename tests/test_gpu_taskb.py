@@ -37,9 +37,9 @@ def _bits(t: torch.Tensor) -> np.ndarray:
 
 
 class TaskBRun:
-    def __init__(self, inp, tb, force_ep=False, profile=False, max_tokens=None):
+    def __init__(self, inp, tb, force_ep=False, profile=False, max_tokens=None, **kw):
         self.inp, self.tb = inp, tb
-        self.run = GpuRun(inp, force_ep=force_ep, profile=profile, max_tokens=max_tokens)
+        self.run = GpuRun(inp, force_ep=force_ep, profile=profile, max_tokens=max_tokens, **kw)
         self.layer = HostLayer(inp.cfg.hidden, tb.wo, tb.gamma)
 
     def forward(self, attn_bits=None, resid_bits=None, out_alias=None, layer=None):
@@ -297,7 +297,7 @@ def test_taskb_local_expert_parallel_matches_single_gpu():
             ids = list(range(q * nl, (q + 1) * nl)) + [ne + s for s in range(S)]
             exps.append(HostExperts(cfg.hidden, cfg.ffn, [inp.w1[i] for i in ids],
                                     [inp.w3[i] for i in ids], [inp.w2[i] for i in ids]))
-            lays.append(MoELayer(cfg.hidden, cfg.ffn, ne, cfg.top_k, bounds[q + 1] - bounds[q],
+            lays.append(MoELayer(cfg.hidden, cfg.ffn, ne, cfg.top_k, max(1, -(-T // world)),
                                  num_shared=S, world_size=world, rank=q, nccl_unique_id=key,
                                  local_ep=True))
             a = bf16_tensor(tb.attn[bounds[q]:bounds[q + 1]])
@@ -375,3 +375,120 @@ def test_taskb_chained_layers():
         for e in experts[1:]:
             e.close()
         run.close()
+
+
+# ------------------------------------------------- VSLPipe alpha / beta partitions (NEXT-3)
+def _two_partition_run(r, tb, split, mover_note=""):
+    """moe_taskb_forward2_host on rows [0, split) (alpha) and [split, T) (beta)."""
+    T = tb.attn.shape[0]
+    k = r.inp.cfg.top_k
+    attn = [bf16_tensor(tb.attn[:split], device="cpu").pin_memory(),
+            bf16_tensor(tb.attn[split:], device="cpu").pin_memory()]
+    resid = [bf16_tensor(tb.resid[:split]), bf16_tensor(tb.resid[split:])]
+    outs = [torch.empty_like(a).pin_memory() for a in attn]
+    idx = torch.empty((T, k), dtype=torch.int32, device="cuda")
+    gates = torch.empty((T, k), dtype=torch.float32, device="cuda")
+    s = torch.cuda.current_stream()
+    r.run.layer.taskb_forward2_host(attn, resid, r.layer, tb.eps, r.run.router, r.run.experts,
+                                    outs, idx, gates, stream=s.cuda_stream)
+    r.run.layer.wait_output(s.cuda_stream)
+    s.synchronize()
+    r.run.layer.sync()
+    return outs, idx, gates
+
+
+@pytest.mark.parametrize("mover", [False, True])
+@pytest.mark.parametrize("split", [400, 0, 900, 1])
+def test_taskb_two_partitions_bitwise_equal_single_calls(split, mover):
+    """VSLPipe's alpha / beta through ONE stream of the layer's weights
+    (moe_taskb_forward2_host): each partition's output and routing are bitwise those of
+    moe_taskb_forward_host on that partition alone, while the layer blob and every expert are
+    copied once per call (H2D weight bytes = one layer), with and without the data mover.
+    split 0 / T: one empty partition; 1: a one-token alpha."""
+    inp, tb = _inputs(512, 640, 16, 4, 900, S=1)
+    r = TaskBRun(inp, tb, profile=True, mover=mover, packet_bytes=1 << 20)
+    try:
+        T = 900
+        # reference: each partition alone through the single-partition host entry point
+        ref_out, ref_idx = [], []
+        s = torch.cuda.current_stream()
+        for lo, hi in ((0, split), (split, T)):
+            if hi == lo:
+                ref_out.append(None)
+                continue
+            a = bf16_tensor(tb.attn[lo:hi], device="cpu").pin_memory()
+            o = torch.empty_like(a).pin_memory()
+            idx = torch.empty((hi - lo, 4), dtype=torch.int32, device="cuda")
+            r.run.layer.taskb_forward_host(a, bf16_tensor(tb.resid[lo:hi]), r.layer, tb.eps,
+                                           r.run.router, r.run.experts, o, idx,
+                                           stream=s.cuda_stream)
+            r.run.layer.sync()
+            ref_out.append(o.clone())
+            ref_idx.append(idx.clone())
+        r.run.layer.reset_stats()
+        outs, idx, gates = _two_partition_run(r, tb, split)
+        st = r.run.layer.stats()
+        blob = 6 * 512 * 640
+        assert st["h2d_weight_bytes"] == 17 * blob + (2 * 512 * 512 + 2 * 512), st
+        assert st["taskb_calls"] == 1
+        for p, (lo, hi) in enumerate(((0, split), (split, T))):
+            if hi == lo:
+                continue
+            assert torch.equal(outs[p], ref_out[p]), f"partition {p} differs"
+        assert torch.equal(idx, torch.cat(ref_idx))
+        # and the whole two-partition call against the oracle, stage by stage
+        out_all = torch.cat([o for o in outs if o.shape[0]]).cuda()
+        dbg = r.run.layer.debug()
+        h1 = _bits(dev_view(dbg.h1, (T, 512), "<i2").clone().view(torch.int16))
+        u = _bits(dev_view(dbg.moe_in, (T, 512), "<i2").clone().view(torch.int16))
+        _check_staged(inp, tb, out_all, idx, gates, h1, u)
+    finally:
+        r.close()
+
+
+def test_taskb_two_partitions_beta_copy_latency_mover_vs_events():
+    """Beta's attention copy is issued after the call's first expert copies were requested (its
+    CPU attention finishes during alpha's GPU phase).  With the event-ordered engine it queues
+    behind those expert DMAs; with the data mover (one packet in flight) it
+    waits behind at most one packet -- the head-of-line blocking the mover exists to avoid.
+    Measured per partition (moe_stats.part_latency_ms) over back-to-back calls; outputs equal."""
+    cfg = synth.MoEConfig("custom", 41, 1024, 4096, 8, 2, 1024)   # 25 MB experts
+    inp = synth.gen_inputs(cfg)
+    tb = synth.gen_taskb(cfg, inp.x)
+    from paper_2504_09345_b200 import HostExperts, MoELayer
+    experts = HostExperts(cfg.hidden, cfg.ffn, inp.w1, inp.w3, inp.w2)
+    hl = HostLayer(cfg.hidden, tb.wo, tb.gamma)
+    router = bf16_tensor(inp.router)
+    split = 512
+    attn = [bf16_tensor(tb.attn[:split], device="cpu").pin_memory(),
+            bf16_tensor(tb.attn[split:], device="cpu").pin_memory()]
+    resid = [bf16_tensor(tb.resid[:split]), bf16_tensor(tb.resid[split:])]
+    lat, res = {}, {}
+    try:
+        for mover in (False, True):
+            layer = MoELayer(cfg.hidden, cfg.ffn, cfg.num_experts, cfg.top_k, cfg.tokens,
+                             profile=True, mover=mover, packet_bytes=4 << 20)
+            outs = [[torch.empty_like(a).pin_memory() for a in attn] for _ in range(3)]
+            s = torch.cuda.current_stream()
+            layer.taskb_forward2_host(attn, resid, hl, tb.eps, router, experts, outs[0],
+                                      stream=s.cuda_stream)   # warm-up
+            layer.sync()
+            layer.reset_stats()
+            for o in outs:
+                layer.taskb_forward2_host(attn, resid, hl, tb.eps, router, experts, o,
+                                          stream=s.cuda_stream)
+            layer.sync()
+            st = layer.stats()
+            assert st["part_copies"] == [3, 3], st["part_copies"]
+            lat[mover] = [st["part_latency_ms"][p] / 3 for p in range(2)]
+            res[mover] = [o.clone() for o in outs[-1]]
+            for o in outs[:-1]:
+                assert all(torch.equal(x, y) for x, y in zip(o, outs[-1]))
+            layer.close()
+        print(f"beta token-copy latency: events {lat[False][1]:.3f} ms, mover {lat[True][1]:.3f} ms;"
+              f" alpha: events {lat[False][0]:.3f} ms, mover {lat[True][0]:.3f} ms")
+        assert all(torch.equal(x, y) for x, y in zip(res[False], res[True]))
+        assert lat[True][1] < lat[False][1]
+    finally:
+        hl.close()
+        experts.close()

@@ -17,7 +17,7 @@ for r in range(W):
     ids = list(range(r * nl, (r + 1) * nl)) + [ne + s for s in range(S)]
     ex.append(HostExperts(h, hi, [inp.w1[i] for i in ids], [inp.w3[i] for i in ids], [inp.w2[i] for i in ids]))
 for r in range(W):
-    ly.append(MoELayer(h, hi, ne, k, max(1, bounds[r+1]-bounds[r]), num_shared=S, world_size=W, rank=r, nccl_unique_id=key, local_ep=True))
+    ly.append(MoELayer(h, hi, ne, k, max(1, -(-T // W)), num_shared=S, world_size=W, rank=r, nccl_unique_id=key, local_ep=True))
     x = bf16_tensor(inp.x[bounds[r]:bounds[r+1]].reshape(-1, h))
     bufs.append((torch.cuda.Stream(), x, torch.empty_like(x)))
 torch.cuda.synchronize()
