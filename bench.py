@@ -335,6 +335,10 @@ def run_ours(args):
                              num_shared=cfg.num_shared, device=local, profile=True,
                              packet_bytes=int(args.packet_mb * 2 ** 20), mover=args.mover, world_size=world,
                              rank=rank, nccl_unique_id=uid, num_slots=args.slots)
+    comm_nranks = layer.group_size()
+    if world > 1:
+        print(f"[bench] rank {rank}: expert-parallel transport {transport}, group size "
+              f"{comm_nranks} (NCCL: ncclCommCount)", file=sys.stderr, flush=True)
     stream = torch.cuda.Stream()
     sh = stream.cuda_stream
     layer_bytes = 0
@@ -418,7 +422,11 @@ def run_ours(args):
     rank_bytes = (nl + cfg.num_shared) * ledger.expert_bytes(cfg.hidden, cfg.ffn) + layer_bytes
     step_weight_bytes = work.weight_bytes + world * layer_bytes
     oproj_flops = 2.0 * T * cfg.hidden * cfg.hidden if args.taskb else 0.0
-    t_io = allmax(rank_bytes / (probe_gbs * 1e9))                  # slowest rank's host link
+    # Host-link roofline on ALGORITHMIC bytes: the layer's weights once, split over W links
+    # -- shared experts (and Task B's Wo) replicated on every rank are charged
+    # against us, not credited.  The slowest rank's probe is the link bandwidth.
+    alg_rank_bytes = (work.weight_bytes + layer_bytes) / world
+    t_io = alg_rank_bytes / (-allmax(-probe_gbs) * 1e9)
     t_tc = (work.expert_flops + oproj_flops) / world / (peaks["bf16_tflops_sustained"] * 1e12)
     t_roof = max(t_io, t_tc)
     # dominant kernel: GEMM1 (+SwiGLU).  FLOPs per launch over all ranks / avg launch time.
@@ -468,6 +476,7 @@ def run_ours(args):
                      "h2d_aggregate_gbs_over_step": step_weight_bytes / (ms * 1e-3) / 1e9,
                      "weight_bytes_per_step": step_weight_bytes,
                      "weight_bytes_per_rank": rank_bytes,
+                     "algorithmic_weight_bytes_per_rank": alg_rank_bytes,
                      "expert_flops_per_step": work.expert_flops,
                      "oproj_flops_per_step": oproj_flops,
                      "tensor_peak_tflops": peaks["bf16_tflops_sustained"]}
@@ -516,6 +525,9 @@ def run_ours(args):
                        "moe_taskb_forward_host (pinned host attention output / result, device "
                        "residual)" if args.taskb else
                        "moe_layer_forward_host (pinned host hidden/out)"),
+               "copy_stream_ms_per_step": {
+                   "weights": est["h2d_ms"] / args.steps, "tokens": est["h2d_token_ms"] / args.steps,
+                   "note": "summed CUDA-event durations of the H2D copies (link busy time)"},
                "token_copy_latency_ms": {
                    "per_partition": [est["part_latency_ms"][p] / max(1, est["part_copies"][p])
                                      for p in range(2)],
@@ -560,7 +572,8 @@ def run_ours(args):
                        "experts_streamed_per_call": nl + cfg.num_shared,
                        "packet_mb": args.packet_mb, "mover": bool(args.mover),
                        "l2": "inputs larger than L2: all expert weights re-streamed from host each step",
-                       "parallelism": f"ep{world}", "ep_transport": transport},
+                       "parallelism": f"ep{world}", "ep_transport": transport,
+                       "ep_comm_nranks": comm_nranks},
             "roofline": roofline, "roofline_step": roofline_step,
             "per_kernel_ms_per_step_rank0": per_kernel_ms,
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,

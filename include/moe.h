@@ -269,6 +269,7 @@ typedef struct {
      * token_latency_ms is their total. */
     int64_t part_copies[2];
     double part_latency_ms[2];
+    double h2d_token_ms;          /* sum of host token copy durations (MOE_FLAG_PROFILE)        */
 } moe_stats;
 
 moe_status moe_get_stats(moe_ctx ctx, moe_stats* out);   /* synchronises the context */
@@ -330,6 +331,10 @@ moe_status moe_ep_ipc_connect(moe_ctx ctx, const void* all_handles);
  * moe_last_error) if any peer did not signal or its data did not arrive -- the caller can then
  * fall back to the NCCL transport with a new context. */
 moe_status moe_ep_ipc_selftest(moe_ctx ctx, double timeout_s);
+
+/* Ranks of the context's expert-parallel group as its transport sees them: ncclCommCount of the
+ * NCCL communicator, world_size for the P2P transports, 1 without expert parallelism. */
+moe_status moe_ep_group_size(moe_ctx ctx, int32_t* nranks);
 
 /* 128-byte ncclUniqueId for moe_config.nccl_unique_id (call on one rank, broadcast to all).
  * MOE_E_NCCL if libnccl.so.2 cannot be loaded. */

@@ -36,7 +36,8 @@ EXPORTED = ["moe_packed_expert_bytes", "moe_pack_expert", "moe_host_alloc", "moe
             "moe_last_error", "moe_probe_h2d", "moe_ep_plan", "moe_nccl_unique_id",
             "moe_packed_layer_bytes", "moe_pack_layer", "moe_taskb_forward",
             "moe_taskb_forward_host", "moe_ep_ipc_handle", "moe_ep_ipc_connect",
-            "moe_ep_ipc_selftest", "moe_wait_output", "moe_taskb_forward2_host"]
+            "moe_ep_ipc_selftest", "moe_wait_output", "moe_taskb_forward2_host",
+            "moe_ep_group_size"]
 MOE_FLAG_IPC_EP = 8
 MOE_FLAG_MOVER = 16
 MOE_IPC_HANDLE_BYTES = 512
@@ -65,7 +66,7 @@ class moe_stats(ctypes.Structure):
                 ("taskb_calls", ctypes.c_int64), ("oproj_ms", ctypes.c_double),
                 ("norm_ms", ctypes.c_double), ("gemm1_sm_mhz", ctypes.c_double),
                 ("gemm2_sm_mhz", ctypes.c_double), ("part_copies", ctypes.c_int64 * 2),
-                ("part_latency_ms", ctypes.c_double * 2)]
+                ("part_latency_ms", ctypes.c_double * 2), ("h2d_token_ms", ctypes.c_double)]
 
     def as_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_}
@@ -131,6 +132,7 @@ def load(path: str = LIB_PATH):
     lib.moe_ep_ipc_connect.argtypes = [P, P]
     lib.moe_ep_ipc_selftest.argtypes = [P, ctypes.c_double]
     lib.moe_wait_output.argtypes = [P, P]
+    lib.moe_ep_group_size.argtypes = [P, ctypes.POINTER(ctypes.c_int32)]
     lib.moe_taskb_forward2_host.argtypes = [P, P, P, P, P, ctypes.c_float, P, P, i32, P, P, P, P]
     for name in EXPORTED:
         if name not in ("moe_packed_expert_bytes", "moe_status_string", "moe_last_error",
@@ -452,6 +454,12 @@ class MoELayer:
             [o.data_ptr() if o.shape[0] else 0 for o in out_host],
             topk_idx.data_ptr() if topk_idx is not None else 0,
             topk_w.data_ptr() if topk_w is not None else 0, stream)
+
+    def group_size(self) -> int:
+        """Ranks of the expert-parallel group as the transport sees them (NCCL: ncclCommCount)."""
+        n = ctypes.c_int32()
+        _check(load().moe_ep_group_size(self.ctx, ctypes.byref(n)), self.ctx)
+        return n.value
 
     def wait_output(self, stream: int = 0):
         """Make `stream` wait for the result copies of the host-buffer calls issued so far."""

@@ -15,7 +15,7 @@ namespace moe {
 
 // kRecTokenA / B: enqueue -> resident latency of a host token copy of partition 0 / 1
 enum RecKind { kRecH2D = 0, kRecRoute, kRecPermute, kRecGemm1, kRecGemm2, kRecCombine, kRecComm,
-               kRecTokenA, kRecTokenB, kRecOproj, kRecNorm, kRecKinds };
+               kRecTokenA, kRecTokenB, kRecOproj, kRecNorm, kRecH2DTok, kRecKinds };
 
 struct Rec {
     int kind;
@@ -43,6 +43,7 @@ struct NcclApi {
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;   // optional
 };
 const NcclApi* nccl_api();  // nullptr if libnccl cannot be found
 

@@ -60,6 +60,7 @@ const NcclApi* nccl_api() {
         LOAD(GroupStart, "ncclGroupStart");
         LOAD(GroupEnd, "ncclGroupEnd");
         LOAD(GetErrorString, "ncclGetErrorString");
+        LOAD(CommCount, "ncclCommCount");
 #undef LOAD
         ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.CommGetAsyncError &&
              api.AllGather && api.Send && api.Recv && api.GroupStart && api.GroupEnd &&
@@ -519,6 +520,17 @@ moe_status moe_nccl_unique_id(void* out128) {
     moe::ncclUniqueId id;
     if (n->GetUniqueId(&id) != 0) return MOE_E_NCCL;
     memcpy(out128, &id, sizeof id);
+    return MOE_OK;
+}
+
+moe_status moe_ep_group_size(moe_ctx c, int32_t* nranks) {
+    if (!c || !nranks) return MOE_E_INVAL;
+    *nranks = c->ep ? c->cfg.world_size : 1;
+    if (c->comm && moe::nccl_api() && moe::nccl_api()->CommCount) {
+        int n = 0;
+        MOE_NCCL(c, moe::nccl_api()->CommCount(c->comm, &n));
+        *nranks = n;
+    }
     return MOE_OK;
 }
 

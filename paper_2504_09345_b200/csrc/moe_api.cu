@@ -596,8 +596,10 @@ moe_status stage_tokens(moe_ctx c, int b, const void* host, size_t bytes, size_t
         MOE_CUDA(c, cudaEventRecord(t0, c->clock_stream));
     }
     MOE_CUDA(c, cudaStreamWaitEvent(ts, c->xbuf_free[b], 0));
+    Prof pc(c, moe::kRecH2DTok, ts);   // the copy's own duration
     MOE_CUDA(c, cudaMemcpyAsync(reinterpret_cast<char*>(c->x_dev[b]) + off, host, bytes,
                                 cudaMemcpyHostToDevice, ts));
+    pc.end();
     MOE_CUDA(c, cudaEventRecord(ready, ts));
     if (prof) {
         cudaEvent_t t1 = moe::pool_get(c);
@@ -1204,7 +1206,8 @@ moe_status moe_get_stats(moe_ctx ctx, moe_stats* out) {
                                       &ctx->stats.gemm1_ms, &ctx->stats.gemm2_ms,   &ctx->stats.combine_ms,
                                       &ctx->stats.comm_ms,  &ctx->stats.part_latency_ms[0],
                                       &ctx->stats.part_latency_ms[1],
-                                      &ctx->stats.oproj_ms, &ctx->stats.norm_ms};
+                                      &ctx->stats.oproj_ms, &ctx->stats.norm_ms,
+                                      &ctx->stats.h2d_token_ms};
     for (const moe::Rec& r : ctx->pending) {
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {

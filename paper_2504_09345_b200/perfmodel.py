@@ -171,6 +171,37 @@ def validate_against_profiler(prof: Dict) -> Dict:
             "mean_accuracy": sum(r["accuracy"] for r in rows) / len(rows)}
 
 
+def predict_expert_parallel(hidden: int, ffn: int, num_experts: int, top_k: int,
+                            num_shared: int, tokens: int, world: int, link_gbs: float,
+                            host_dram_gbs: float, tensor_tflops: float,
+                            gemm_efficiency: float = 0.8, nvlink_gbs: float = 900.0) -> Dict:
+    """Predicted step time / tokens per second of ONE streamed MoE layer under expert
+    parallelism over `world` GPUs of one box (BASELINE.json's 1/2/4/8 B200s).
+
+    Each rank streams its N_e / W routed experts plus the replicated shared ones over its own
+    host link; all W links draw on one host's DRAM at once (Eq. 5's logic: host
+    memory must feed every stream), so a link delivers min(link, host_dram / W).  Each rank's
+    expert GEMMs do 1/W of the layer's FLOPs (plus its own shared-expert work), at
+    `gemm_efficiency` of the tensor peak; the token exchange (dispatch + combine, bf16 rows, the
+    (W-1)/W of them that leave the rank) goes over NVLink.  The step is the slowest of the three
+    pipelined streams (weights, GEMMs, exchange): step = max(t_link, t_gemm, t_a2a)."""
+    if world < 1 or num_experts % world:
+        raise ValueError("world must divide num_experts")
+    eb = ledger.expert_bytes(hidden, ffn)
+    rank_bytes = (num_experts // world + num_shared) * eb
+    per_link = min(link_gbs, host_dram_gbs / world)
+    t_link = rank_bytes / (per_link * 1e9)
+    flops = 6.0 * hidden * ffn * tokens * (top_k / world + num_shared / world)
+    t_gemm = flops / (gemm_efficiency * tensor_tflops * 1e12)
+    a2a_bytes = 2 * (tokens / world) * top_k * hidden * 2 * (world - 1) / world
+    t_a2a = a2a_bytes / (nvlink_gbs * 1e9) if world > 1 else 0.0
+    step = max(t_link, t_gemm, t_a2a)
+    return {"world": world, "rank_weight_bytes": rank_bytes, "per_link_gbs": per_link,
+            "t_link_ms": t_link * 1e3, "t_gemm_ms": t_gemm * 1e3, "t_a2a_ms": t_a2a * 1e3,
+            "step_ms": step * 1e3, "tokens_per_s": tokens / step,
+            "bound": "host_link" if step == t_link else ("tensor" if step == t_gemm else "nvlink")}
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     sub = ap.add_subparsers(dest="cmd", required=True)

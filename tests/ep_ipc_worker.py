@@ -23,13 +23,13 @@ def run_rank(rank, world, port, cfg_tuple, calls, device, q):
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
         torch.cuda.set_device(device)
-        cfg = synth.MoEConfig(*cfg_tuple)
-        inp = synth.gen_inputs(cfg)
+        # a BASELINE config by name (its token structure included), or a custom shape tuple
+        cfg = synth.CONFIGS[cfg_tuple] if isinstance(cfg_tuple, str) else synth.MoEConfig(*cfg_tuple)
         ne, nl, S, T = cfg.num_experts, cfg.num_experts // world, cfg.num_shared, cfg.tokens
         lo, hi = T * rank // world, T * (rank + 1) // world
         ids = list(range(rank * nl, (rank + 1) * nl)) + [ne + s for s in range(S)]
-        experts = HostExperts(cfg.hidden, cfg.ffn, [inp.w1[i] for i in ids],
-                              [inp.w3[i] for i in ids], [inp.w2[i] for i in ids])
+        inp = synth.gen_inputs(cfg, expert_ids=ids)   # only this rank's experts
+        experts = HostExperts(cfg.hidden, cfg.ffn, inp.w1, inp.w3, inp.w2)
         cap = max(1, -(-T // world))   # one capacity on every rank (checked at connect)
         layer = MoELayer(cfg.hidden, cfg.ffn, ne, cfg.top_k, cap, num_shared=S,
                          device=device, world_size=world, rank=rank, ipc_ep=True)

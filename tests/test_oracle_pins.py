@@ -303,3 +303,83 @@ def test_whole_layer_c4_slice_vs_torch_fp64():
         ref += _dense_swiglu_fp64(inp.x, inp.w1[e], inp.w3[e], inp.w2[e])
     ref = ref.numpy()
     assert np.max(np.abs(y - ref)) <= 1e-5 * np.max(np.abs(ref))
+
+
+def _rank_count_mask(logits, k):
+    """Vectorised rank-count definition (numpy, independent of the oracle's C selection):
+    e in S_t  <=>  #{e' : l_e' > l_e  or (l_e' == l_e and e' < e)} < k."""
+    l = logits[:, None, :]          # [T, 1, e']
+    m = logits[:, :, None]          # [T, e, 1]
+    ne = logits.shape[1]
+    lower = np.arange(ne)[None, None, :] < np.arange(ne)[None, :, None]
+    above = (l > m) | ((l == m) & lower)
+    return above.sum(axis=2) < k    # [T, e]
+
+
+@pytest.mark.parametrize("name,k_override", [
+    ("tiny", None), ("mixtral_8x7b", None), ("mixtral_8x22b", None), ("dbrx", None),
+    ("dsv2_lite", None),                       # (N_e, k) = (64, 6): the C4 shape
+    ("envelope_128x8", None),                  # (128, 8): the envelope maximum
+])
+def test_topk_on_config_logits(name, k_override):
+    """Routing on REAL config logits (a token sample of every BASELINE workload's structure, plus
+    the envelope maximum N_e = 128, k = 8) by two routes other than the oracle's selection loop:
+    (1) the rank-count definition (PAPER.md:269 'top-N_k of N_e', reading R5's order), vectorised;
+    (2) Python's sorted() with key (-logit, index) -- which also fixes the listed ORDER.  Where
+    C(N_e, k) is small, (3) exhaustive subset enumeration on the first tokens as well.  Some rows
+    get duplicated router rows so exact ties occur."""
+    if name == "envelope_128x8":
+        cfg = synth.MoEConfig("envelope_128x8", 50, 1024, 128, 128, 8, 1024)
+    else:
+        cfg = synth.CONFIGS[name]
+    T = min(cfg.tokens, 1024)
+    inp = synth.gen_inputs(cfg, tokens=T, experts=False)
+    router = inp.router.copy()
+    router[cfg.num_experts - 1] = router[0]           # exact ties between experts 0 and N_e - 1
+    logits = oracle.router_logits(inp.x, router)
+    k = cfg.top_k
+    idx, gates = oracle.topk_gates(logits, k)
+    mask = _rank_count_mask(logits, k)
+    for t in range(T):
+        assert sorted(idx[t].tolist()) == np.nonzero(mask[t])[0].tolist(), t
+        ref = sorted(range(cfg.num_experts), key=lambda e: (-logits[t, e], e))[:k]
+        assert idx[t].tolist() == ref, t
+    if math.comb(cfg.num_experts, k) <= 2000:
+        for t in range(min(T, 64)):
+            assert sorted(idx[t].tolist()) == _enumerate_best_subset(logits[t], k)
+    assert np.allclose(gates.astype(np.float64).sum(1), 1.0, atol=1e-6)
+
+
+@pytest.mark.parametrize("name,tokens", [("mixtral_8x7b", 2), ("mixtral_8x22b", 2), ("dbrx", 1)])
+def test_whole_layer_full_shape_slice_vs_torch_fp64(name, tokens):
+    """SURVEY §8(c.3) 'whole layer' at the C1-C3 shapes: an independent torch fp64 layer on a
+    token slice -- fp64 router matmul, selection by a stable sort on (-logit, index), softmax over
+    the k selected logits, SwiGLU experts W2 (silu(W1 x) * W3 x) in fp64, gate-weighted sum
+    (readings R1-R3, R5) -- against the oracle: idx equal, y within 1e-5 of the largest output.
+    Only the routed experts' weights are generated (each expert's draw is independent of the
+    others, synth.gen_inputs(expert_ids=...))."""
+    cfg = synth.CONFIGS[name]
+    head = synth.gen_inputs(cfg, tokens=tokens, experts=False)
+    x = _t64(head.x)
+    logits = x @ _t64(head.router).T
+    order = [sorted(range(cfg.num_experts), key=lambda e: (-float(logits[t, e]), e))[:cfg.top_k]
+             for t in range(tokens)]
+    used = sorted({e for row in order for e in row})
+    sub = synth.gen_inputs(cfg, tokens=tokens, expert_ids=used)
+    assert np.array_equal(sub.x, head.x)
+    w = {e: (sub.w1[i], sub.w3[i], sub.w2[i]) for i, e in enumerate(used)}
+    ref = torch.zeros(tokens, cfg.hidden, dtype=torch.float64)
+    for t in range(tokens):
+        sel = torch.tensor([float(logits[t, e]) for e in order[t]], dtype=torch.float64)
+        p = torch.softmax(sel, dim=0)
+        for j, e in enumerate(order[t]):
+            ref[t] += p[j] * _dense_swiglu_fp64(head.x[t:t + 1], *w[e])[0]
+    # the oracle on the same tokens, routed by its own router + top-k; it reads only the routed
+    # experts' weights (unrouted experts are given a stand-in that is never read)
+    lg = oracle.router_logits(head.x, head.router)
+    idx, g = oracle.topk_gates(lg, cfg.top_k)
+    assert idx.tolist() == order
+    mats = [[w.get(e, w[used[0]])[m] for e in range(cfg.num_experts)] for m in range(3)]
+    y = oracle.experts_combine(head.x, mats[0], mats[1], mats[2], cfg.num_experts, 0, idx, g)
+    ref = ref.numpy()
+    assert np.max(np.abs(y - ref)) <= 1e-5 * np.max(np.abs(ref))

@@ -169,3 +169,32 @@ def test_b200_layer_model_predicts_measured_step_times():
                                                   prof["eq2_inputs"]["host_link_gbs"], 8, 2,
                                                   binary_prefixes=False)
         assert (0.5 if mixtral else 0.3) * n_eq2 < v["n_real"] < 1.2 * n_eq2, (f, v)
+
+
+def test_expert_parallel_prediction_closed_forms():
+    """predict_expert_parallel: at W = 1 the Mixtral-8x7B layer is host-link bound at exactly
+    (8 x 352.3 MB) / link; each doubling of W halves the per-rank bytes while host DRAM keeps up
+    (tokens/s doubles); once W links exceed host DRAM, per-link bandwidth is host_dram / W and
+    the step stops shrinking (Eq. 5's logic).  Shared experts are replicated:
+    C4 at W = 8 streams 8 + 2 experts per rank."""
+    from paper_2504_09345_b200 import perfmodel as pm
+    kw = dict(hidden=4096, ffn=14336, num_experts=8, top_k=2, num_shared=0, tokens=4096,
+              link_gbs=55.6, tensor_tflops=1385.5)
+    p1 = pm.predict_expert_parallel(world=1, host_dram_gbs=1e9, **kw)
+    assert p1["bound"] == "host_link"
+    assert p1["step_ms"] == pytest.approx(8 * 352_321_536 / 55.6e9 * 1e3)
+    prev = p1
+    for w in (2, 4, 8):
+        p = pm.predict_expert_parallel(world=w, host_dram_gbs=1e9, **kw)
+        assert p["tokens_per_s"] == pytest.approx(2 * prev["tokens_per_s"])
+        prev = p
+    capped = pm.predict_expert_parallel(world=8, host_dram_gbs=222.4, **kw)   # 4 links' worth
+    half = pm.predict_expert_parallel(world=4, host_dram_gbs=1e9, **kw)
+    assert capped["per_link_gbs"] == pytest.approx(27.8)
+    assert capped["step_ms"] == pytest.approx(half["step_ms"])
+    c4 = pm.predict_expert_parallel(hidden=2048, ffn=1408, num_experts=64, top_k=6, num_shared=2,
+                                    tokens=32768, world=8, link_gbs=55.6, host_dram_gbs=1e9,
+                                    tensor_tflops=1385.5)
+    assert c4["rank_weight_bytes"] == 10 * 6 * 2048 * 1408
+    with pytest.raises(ValueError):
+        pm.predict_expert_parallel(world=3, host_dram_gbs=1e9, **kw)
