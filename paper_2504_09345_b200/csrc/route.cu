@@ -8,6 +8,7 @@
 //   * top-k breaks ties toward the lower expert index (R5); NaN ranks last;
 //   * token positions inside an expert group are ascending in t (R12), computed from per-tile
 //     counts (no atomics on the data path).
+#include <algorithm>
 #include <cfloat>
 #include <cstdlib>
 #include <cmath>
@@ -36,6 +37,88 @@ __device__ __forceinline__ void bf16x8_to_f64(const int4& v, double (&o)[8]) {
         const float2 f = __bfloat1622float2(b[i]);  // exact
         o[2 * i] = (double)f.x;
         o[2 * i + 1] = (double)f.y;
+    }
+}
+
+// Warp-shuffle top-k of one block's tokens from their fp64 logits lg[kTok][ne_pad] (shared):
+// warp w handles tokens w, w+nw, ...; selection by (logit desc, index asc) with NaN last (R5,
+// R13); gates = fp64 softmax over the k selected (or all N_e) logits (R3); per-tile counts.
+template <int TPT>
+__device__ __forceinline__ void topk_tile(const double* lg, int ne_pad, int t0, int T, int ne,
+                                          int k, int renorm, int32_t* __restrict__ idx_out,
+                                          float* __restrict__ gate_out,
+                                          int (*cnt)[kMaxExperts], int warp, int nw, int lane) {
+    constexpr int kTok = kRouteTile * TPT;
+    for (int tt = warp; tt < kTok; tt += nw) {
+        const int t = t0 + tt;
+        if (t >= T) break;
+        double v[kMaxExperts / 32];
+#pragma unroll
+        for (int i = 0; i < kMaxExperts / 32; ++i) {
+            const int e = lane + 32 * i;
+            v[i] = (e < ne) ? lg[tt * ne_pad + e] : 0.0;
+        }
+        uint32_t taken = 0;
+        double sel_l[kMaxTopK];
+        int sel_e[kMaxTopK];
+        for (int j = 0; j < k; ++j) {
+            bool have = false;
+            double bv = 0.0;
+            int be = 0x7fffffff;
+#pragma unroll
+            for (int i = 0; i < kMaxExperts / 32; ++i) {
+                const int e = lane + 32 * i;
+                if (e < ne && !((taken >> i) & 1u)) {
+                    if (!have || ranks_above(v[i], e, bv, be)) {
+                        bv = v[i];
+                        be = e;
+                        have = true;
+                    }
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+                const int oe = __shfl_xor_sync(0xffffffffu, be, off);
+                const int oh = __shfl_xor_sync(0xffffffffu, (int)have, off);
+                if (oh && (!have || ranks_above(ov, oe, bv, be))) {
+                    bv = ov;
+                    be = oe;
+                    have = true;
+                }
+            }
+            if ((be & 31) == lane) taken |= 1u << (be >> 5);
+            sel_l[j] = bv;
+            sel_e[j] = be;
+        }
+        // softmax gates in fp64 (R3): renormalised over the k selected, or over all N_e
+        const double m = sel_l[0];
+        double z = 0.0;
+        if (renorm) {
+            for (int j = 0; j < k; ++j) z += exp(sel_l[j] - m);
+        } else {
+            double part = 0.0;
+#pragma unroll
+            for (int i = 0; i < kMaxExperts / 32; ++i) {
+                const int e = lane + 32 * i;
+                if (e < ne) part += exp(v[i] - m);
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+            z = part;
+        }
+        if (lane < k) {
+            double mine = sel_l[0];
+            int me = sel_e[0];
+            for (int j = 1; j < k; ++j)
+                if (j == lane) {
+                    mine = sel_l[j];
+                    me = sel_e[j];
+                }
+            idx_out[(size_t)t * k + lane] = me;
+            gate_out[(size_t)t * k + lane] = (float)(exp(mine - m) / z);
+            atomicAdd(&cnt[tt / kRouteTile][me], 1);
+        }
     }
 }
 
@@ -166,82 +249,145 @@ router_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
         for (int i = 0; i < EPT; ++i) lg[(p * 32 + lane) * ne_pad + warp * EPT + i] = acc[p][i];
     __syncthreads();
 
-    // warp-shuffle top-k: warp w handles tokens w, w+nw, ... of the block
-    for (int tt = warp; tt < kTok; tt += nw) {
-        const int t = t0 + tt;
-        if (t >= T) break;
-        double v[kMaxExperts / 32];
-#pragma unroll
-        for (int i = 0; i < kMaxExperts / 32; ++i) {
-            const int e = lane + 32 * i;
-            v[i] = (e < ne) ? lg[tt * ne_pad + e] : 0.0;
-        }
-        uint32_t taken = 0;
-        double sel_l[kMaxTopK];
-        int sel_e[kMaxTopK];
-        for (int j = 0; j < k; ++j) {
-            bool have = false;
-            double bv = 0.0;
-            int be = 0x7fffffff;
-#pragma unroll
-            for (int i = 0; i < kMaxExperts / 32; ++i) {
-                const int e = lane + 32 * i;
-                if (e < ne && !((taken >> i) & 1u)) {
-                    if (!have || ranks_above(v[i], e, bv, be)) {
-                        bv = v[i];
-                        be = e;
-                        have = true;
-                    }
-                }
-            }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
-                const int oe = __shfl_xor_sync(0xffffffffu, be, off);
-                const int oh = __shfl_xor_sync(0xffffffffu, (int)have, off);
-                if (oh && (!have || ranks_above(ov, oe, bv, be))) {
-                    bv = ov;
-                    be = oe;
-                    have = true;
-                }
-            }
-            if ((be & 31) == lane) taken |= 1u << (be >> 5);
-            sel_l[j] = bv;
-            sel_e[j] = be;
-        }
-        // softmax gates in fp64 (R3): renormalised over the k selected, or over all N_e
-        const double m = sel_l[0];
-        double z = 0.0;
-        if (renorm) {
-            for (int j = 0; j < k; ++j) z += exp(sel_l[j] - m);
-        } else {
-            double part = 0.0;
-#pragma unroll
-            for (int i = 0; i < kMaxExperts / 32; ++i) {
-                const int e = lane + 32 * i;
-                if (e < ne) part += exp(v[i] - m);
-            }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
-            z = part;
-        }
-        if (lane < k) {
-            double mine = sel_l[0];
-            int me = sel_e[0];
-            for (int j = 1; j < k; ++j)
-                if (j == lane) {
-                    mine = sel_l[j];
-                    me = sel_e[j];
-                }
-            idx_out[(size_t)t * k + lane] = me;
-            gate_out[(size_t)t * k + lane] = (float)(exp(mine - m) / z);
-            atomicAdd(&cnt[tt / kRouteTile][me], 1);
-        }
-    }
+    topk_tile<TPT>(lg, ne_pad, t0, T, ne, k, renorm, idx_out, gate_out, cnt, warp, nw, lane);
     __syncthreads();
     const int n_tiles = (T + kRouteTile - 1) / kRouteTile;
 #pragma unroll
     for (int p = 0; p < TPT; ++p) {   // one row per 32-token routing tile (scan / permute grain)
+        const int tile = blockIdx.x * TPT + p;
+        if (tile < n_tiles)
+            for (int e = tid; e < ne; e += nthr) tile_counts[(size_t)tile * ne + e] = cnt[p][e];
+    }
+}
+
+// Router v4: the same one-FMA-chain-per-logit arithmetic (reading R6), restructured for latency:
+//   * x is read by the lane that owns the token, straight from global memory (16-byte vectors of 8
+//     channels, prefetched two vectors ahead in registers) and widened to fp64 in registers --
+//     no shared-memory staging of x, no barrier per x tile;
+//   * the router weights are staged once per block into shared memory as fp64, in chunks of CW
+//     channels x ne_pad experts, double-buffered: chunk j+1 is loaded into registers while chunk
+//     j is consumed and stored into the other buffer at its end -- ONE __syncthreads per chunk;
+//   * warp w owns experts [w*EPT, (w+1)*EPT) of the block's 32*TPT tokens; per channel a lane
+//     reads EPT/2 double2 broadcasts and runs TPT*EPT independent chains.
+// Few experts (C1: 8) -> EPT = 2, 4 warps per 32 tokens: 16k warps' worth of chains spread over
+// every SM; many experts (C4: 64) -> EPT = 8, TPT = 2 (each broadcast feeds 16 DFMAs).
+template <int EPT, int TPT>
+__global__ void __launch_bounds__(512)
+router_v4_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
+                 const __nv_bfloat16* __restrict__ wr, int ne, int k, int renorm, int cw,
+                 int32_t* __restrict__ idx_out, float* __restrict__ gate_out,
+                 int32_t* __restrict__ tile_counts) {
+    constexpr int kTok = kRouteTile * TPT;
+    extern __shared__ __align__(16) double dyn[];
+    __shared__ int cnt[TPT][kMaxExperts];
+    const int nw = blockDim.x >> 5;
+    const int ne_pad = nw * EPT;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
+    const int t0 = blockIdx.x * kTok;
+    for (int e = tid; e < TPT * kMaxExperts; e += nthr) cnt[e / kMaxExperts][e % kMaxExperts] = 0;
+
+    // router chunk staging: vector v of a chunk = 8 channels of expert v % ne_pad
+    const int n_wv = (cw / 8) * ne_pad;
+    constexpr int kMaxWV = 4;   // n_wv <= 4 * nthr (host: cw * EPT <= 1024)
+    auto wload = [&](int c0, int4 (&wv)[kMaxWV]) {
+#pragma unroll
+        for (int j = 0; j < kMaxWV; ++j) {
+            const int v = tid + j * nthr;
+            if (v < n_wv) {
+                const int e = v % ne_pad, cc = (v / ne_pad) * 8;
+                wv[j] = (e < ne) ? ptx::ld_nc_v4(wr + (size_t)e * h + c0 + cc) : make_int4(0, 0, 0, 0);
+            }
+        }
+    };
+    auto wstore = [&](double* ws, const int4 (&wv)[kMaxWV]) {
+        double d[8];
+#pragma unroll
+        for (int j = 0; j < kMaxWV; ++j) {
+            const int v = tid + j * nthr;
+            if (v < n_wv) {
+                const int e = v % ne_pad, cc = (v / ne_pad) * 8;
+                bf16x8_to_f64(wv[j], d);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) ws[(cc + q) * ne_pad + e] = d[q];
+            }
+        }
+    };
+    int4 wv[kMaxWV];
+    wload(0, wv);
+    wstore(dyn, wv);
+    __syncthreads();
+
+    // this lane's token rows
+    const int4* xrow[TPT];
+    bool live[TPT];
+#pragma unroll
+    for (int p = 0; p < TPT; ++p) {
+        const int t = t0 + p * 32 + lane;
+        live[p] = t < T;
+        xrow[p] = reinterpret_cast<const int4*>(x + (size_t)(live[p] ? t : 0) * h);
+    }
+    double acc[TPT][EPT];
+#pragma unroll
+    for (int p = 0; p < TPT; ++p)
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) acc[p][i] = 0.0;
+    const int nvec = h / 8;
+    int4 xa[TPT], xb[TPT];   // vectors v and v + 1 in flight
+#pragma unroll
+    for (int p = 0; p < TPT; ++p) {
+        xa[p] = live[p] ? ptx::ld_nc_v4(xrow[p]) : make_int4(0, 0, 0, 0);
+        xb[p] = (live[p] && nvec > 1) ? ptx::ld_nc_v4(xrow[p] + 1) : make_int4(0, 0, 0, 0);
+    }
+    const int vpc = cw / 8;   // x vectors per chunk
+    int buf = 0;
+    for (int v = 0; v < nvec; ++v) {
+        const int vin = v % vpc;
+        if (vin == 0 && v + vpc < nvec) wload((v + vpc) * 8, wv);   // next chunk in flight
+        double xd[TPT][8];
+#pragma unroll
+        for (int p = 0; p < TPT; ++p) {
+            bf16x8_to_f64(xa[p], xd[p]);
+            xa[p] = xb[p];
+            xb[p] = (live[p] && v + 2 < nvec) ? ptx::ld_nc_v4(xrow[p] + v + 2) : make_int4(0, 0, 0, 0);
+        }
+        const double* wrow = dyn + (size_t)buf * cw * ne_pad + (size_t)(vin * 8) * ne_pad + warp * EPT;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if constexpr (EPT == 1) {
+                const double w = wrow[q * ne_pad];
+#pragma unroll
+                for (int p = 0; p < TPT; ++p) acc[p][0] = fma(xd[p][q], w, acc[p][0]);
+            } else {
+                const double2* w2 = reinterpret_cast<const double2*>(wrow + q * ne_pad);
+#pragma unroll
+                for (int i = 0; i < EPT / 2; ++i) {
+                    const double2 w = w2[i];
+#pragma unroll
+                    for (int p = 0; p < TPT; ++p) {
+                        acc[p][2 * i] = fma(xd[p][q], w.x, acc[p][2 * i]);
+                        acc[p][2 * i + 1] = fma(xd[p][q], w.y, acc[p][2 * i + 1]);
+                    }
+                }
+            }
+        }
+        if (vin == vpc - 1 && v + 1 < nvec) {   // end of a chunk: publish the next one
+            wstore(dyn + (size_t)(buf ^ 1) * cw * ne_pad, wv);
+            __syncthreads();
+            buf ^= 1;
+        }
+    }
+    __syncthreads();   // every lane done with the router chunks: the space takes the logits
+    double* lg = dyn;  // [kTok][ne_pad] (host sizes dyn for max(2 chunks, logits))
+#pragma unroll
+    for (int p = 0; p < TPT; ++p)
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) lg[(p * 32 + lane) * ne_pad + warp * EPT + i] = acc[p][i];
+    __syncthreads();
+    topk_tile<TPT>(lg, ne_pad, t0, T, ne, k, renorm, idx_out, gate_out, cnt, warp, nw, lane);
+    __syncthreads();
+    const int n_tiles = (T + kRouteTile - 1) / kRouteTile;
+#pragma unroll
+    for (int p = 0; p < TPT; ++p) {
         const int tile = blockIdx.x * TPT + p;
         if (tile < n_tiles)
             for (int e = tid; e < ne; e += nthr) tile_counts[(size_t)tile * ne + e] = cnt[p][e];
@@ -446,9 +592,10 @@ combine_kernel(const __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ 
 
 }  // namespace
 
-cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_bfloat16* wr,
-                               int ne, int k, int renorm, int32_t* idx, float* gates,
-                               int32_t* tile_counts, cudaStream_t st) {
+// Router v3 (round 1; MOE_ROUTER=3 for comparison): x and router tiles staged in shared memory.
+cudaError_t launch_router_v3(const __nv_bfloat16* x, int T, int h, const __nv_bfloat16* wr,
+                            int ne, int k, int renorm, int32_t* idx, float* gates,
+                            int32_t* tile_counts, cudaStream_t st) {
     const int n_tiles = (T + kRouteTile - 1) / kRouteTile;
     if (n_tiles == 0) return cudaSuccess;
     // EPT experts per warp: few experts -> fewer per warp, so a 32-token tile still spreads over
@@ -484,6 +631,45 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
     else if (tpt == 2) MOE_ROUTER(8, 2);
     else MOE_ROUTER(8, 1);
 #undef MOE_ROUTER
+    return cudaGetLastError();
+}
+
+cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_bfloat16* wr,
+                               int ne, int k, int renorm, int32_t* idx, float* gates,
+                               int32_t* tile_counts, cudaStream_t st) {
+    const int n_tiles = (T + kRouteTile - 1) / kRouteTile;
+    if (n_tiles == 0) return cudaSuccess;
+    const char* ver = getenv("MOE_ROUTER");   // 3: round 1's kernel (comparison)
+    if (ver && atoi(ver) == 3) return launch_router_v3(x, T, h, wr, ne, k, renorm, idx, gates, tile_counts, st);
+    // experts per warp: few experts -> 2 per warp (C1: 4 warps per 32 tokens, parallel chains on
+    // every SM); 16 -> 4; more -> 8 with two tokens per lane (every broadcast feeds 16 DFMAs)
+    int ept = ne <= 8 ? 2 : (ne <= 16 ? 4 : 8);
+    if (const char* e = getenv("MOE_ROUTER_EPT")) {   // experiments: 1, 2, 4 or 8
+        const int v = atoi(e);
+        if ((v == 1 || v == 2 || v == 4 || v == 8) && ((ne + v - 1) / v) * 32 <= 512) ept = v;
+    }
+    const int nw = (ne + ept - 1) / ept;
+    const int ne_pad = nw * ept;
+    int tpt = (ept == 8 && nw >= 3 && nw <= 8) ? 2 : 1;
+    if (const char* e = getenv("MOE_ROUTER_TPT")) tpt = atoi(e) == 2 ? 2 : 1;
+    int cw = 128;   // router channels per staged chunk: 2 chunks of fp64 <= 32 KB
+    while (cw > 8 && 2 * cw * ne_pad > 4096) cw >>= 1;
+    const size_t dyn = sizeof(double) * (size_t)std::max(2 * cw * ne_pad, kRouteTile * tpt * ne_pad);
+    const int blocks = (T + kRouteTile * tpt - 1) / (kRouteTile * tpt);
+#define MOE_ROUTER4(E, P)                                                                    \
+    do {                                                                                     \
+        cudaError_t e_ = cudaFuncSetAttribute(router_v4_kernel<E, P>,                        \
+            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);                          \
+        if (e_ != cudaSuccess) return e_;                                                    \
+        router_v4_kernel<E, P><<<blocks, nw * 32, dyn, st>>>(x, T, h, wr, ne, k, renorm, cw,  \
+                                                             idx, gates, tile_counts);       \
+    } while (0)
+    if (ept == 1) MOE_ROUTER4(1, 1);
+    else if (ept == 2) { if (tpt == 2) MOE_ROUTER4(2, 2); else MOE_ROUTER4(2, 1); }
+    else if (ept == 4) { if (tpt == 2) MOE_ROUTER4(4, 2); else MOE_ROUTER4(4, 1); }
+    else if (tpt == 2) MOE_ROUTER4(8, 2);
+    else MOE_ROUTER4(8, 1);
+#undef MOE_ROUTER4
     return cudaGetLastError();
 }
 

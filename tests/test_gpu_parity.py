@@ -352,12 +352,18 @@ def test_experts_per_gemm_launch(rows, copy_group, launches, monkeypatch):
         run.close()
 
 
-@pytest.mark.parametrize("ept", ["1", "2", "4", "8"])
+@pytest.mark.parametrize("variant", ["v3-1", "v3-2", "v3-4", "v3-8", "v4-1", "v4-2", "v4-4",
+                                     "v4-8", "v4-2-tpt2", "v4-4-tpt2", "v4-8-tpt1"])
 @pytest.mark.parametrize("ne,k", [(5, 2), (8, 2), (16, 4), (40, 6)])   # 40: 2 tokens per lane
-def test_router_experts_per_warp_variants(ne, k, ept, monkeypatch):
-    """Every router_topk_kernel<EPT> instantiation (MOE_ROUTER_EPT; the default picks by N_e)
-    gives the same bit-exact selection and gates (one fp64 FMA chain per logit either way)."""
+def test_router_experts_per_warp_variants(ne, k, variant, monkeypatch):
+    """Every router kernel instantiation -- round 1's router_topk_kernel<EPT> (MOE_ROUTER=3) and
+    router_v4_kernel<EPT, TPT> (default; MOE_ROUTER_EPT / MOE_ROUTER_TPT) -- gives the same
+    bit-exact selection and gates (one fp64 FMA chain per logit, ascending channels, either way)."""
+    ver, ept, *rest = variant.split("-")
+    monkeypatch.setenv("MOE_ROUTER", ver[1])
     monkeypatch.setenv("MOE_ROUTER_EPT", ept)
+    if rest:
+        monkeypatch.setenv("MOE_ROUTER_TPT", rest[0][3])
     cfg = synth.MoEConfig("custom", 19, 384, 256, ne, k, 777, 0)
     inp = synth.gen_inputs(cfg)
     run, *_ = _check_full(inp)
