@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-one-thread-tokens", type=int, default=8,
+                    help="tokens of the one-thread oracle sample (SURVEY §8(d): 64 = all of C0, "
+                         "256 = a C1 slice)")
     ap.add_argument("--taskb", action="store_true",
                     help="time GPU Task B (O-projection + RMSNorm + MoE layer, streamed Wo) "
                          "instead of the MoE layer alone (no cpu leg)")
@@ -131,7 +134,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------------------
-def cpu_baseline(inp, seconds: float) -> dict:
+def cpu_baseline(inp, seconds: float, one_thread_tokens: int = 8) -> dict:
     """The oracle as it stands, on a bounded token sample of the same workload (rank 0 only)."""
     import oracle
     cfg = inp.cfg
@@ -152,12 +155,14 @@ def cpu_baseline(inp, seconds: float) -> dict:
     one = None
     try:
         oracle.set_num_threads(1)
-        n1 = min(8, inp.x.shape[0])
+        n1 = min(max(1, one_thread_tokens), inp.x.shape[0])
         t0 = time.perf_counter()
         oracle.forward(inp.x[:n1], inp.router, inp.w1, inp.w3, inp.w2, cfg.top_k, cfg.num_shared)
         dt = time.perf_counter() - t0
         one = {"value": n1 / dt, "unit": "tokens/s", "cores": 1,
-               "sample": f"{n1} tokens of the {cfg.name} layer, 1 OpenMP thread ({dt:.2f} s)"}
+               "sample": f"{n1} tokens of the {cfg.name} layer, 1 OpenMP thread ({dt:.2f} s)",
+               "extrapolated_full_layer_s": cfg.tokens * dt / n1,
+               "extrapolated_note": f"all {cfg.tokens} tokens at the sample's rate (extrapolated)"}
     finally:
         oracle.set_num_threads(cores)
     return {"value": done / elapsed, "unit": "tokens/s", "cores": cores, "kind": "oracle",
@@ -304,41 +309,47 @@ def run_ours(args):
     if world > 1:
         dist.barrier()   # all ranks probe their host links at the same time (shared host DRAM)
     probe_gbs = moe.moe_probe_h2d(local, 1 << 30, 5)   # paper's method: 1 GB pinned H2D copies
-    uid = None
-    transport = "single" if world == 1 else args.ep_transport
-    layer = None
-    if transport == "p2p":   # CUDA IPC peer mapping; every rank must succeed, else NCCL
-        try:
+    transport0 = "single" if world == 1 else args.ep_transport
+
+    def make_layer(profile):
+        """This rank's context: the P2P transport over CUDA IPC when asked and every rank can map
+        its peers (checked by a self-test), else NCCL.  Returns (layer, transport)."""
+        transport, layer, uid = transport0, None, None
+        mk = dict(num_shared=cfg.num_shared, device=local, profile=profile,
+                  packet_bytes=int(args.packet_mb * 2 ** 20), mover=args.mover, world_size=world,
+                  rank=rank, num_slots=args.slots)
+        if transport == "p2p":   # CUDA IPC peer mapping; every rank must succeed, else NCCL
+            try:
+                layer = moe.MoELayer(cfg.hidden, cfg.ffn, cfg.num_experts, cfg.top_k, Tr,
+                                     ipc_ep=True, **mk)
+                handles = [None] * world
+                dist.all_gather_object(handles, layer.ipc_handle())
+                layer.ipc_connect(handles)
+                layer.ipc_selftest(5.0)   # flags + rows through the mapping, before trusting it
+                ok = 1.0
+            except Exception as e:  # noqa: BLE001 -- reported, then the NCCL transport
+                print(f"[bench] rank {rank}: P2P transport unavailable ({e}); using NCCL",
+                      file=sys.stderr, flush=True)
+                ok = 0.0
+            if allmax(1.0 - ok) > 0:
+                if layer is not None:
+                    layer.close()
+                layer, transport = None, "nccl"
+        if world > 1 and transport == "nccl":
+            obj = [moe.moe_nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            uid = obj[0]
+        if layer is None:
             layer = moe.MoELayer(cfg.hidden, cfg.ffn, cfg.num_experts, cfg.top_k, Tr,
-                                 num_shared=cfg.num_shared, device=local, profile=True,
-                                 packet_bytes=int(args.packet_mb * 2 ** 20), mover=args.mover, world_size=world,
-                                 rank=rank, num_slots=args.slots, ipc_ep=True)
-            handles = [None] * world
-            dist.all_gather_object(handles, layer.ipc_handle())
-            layer.ipc_connect(handles)
-            layer.ipc_selftest(5.0)   # flags + rows through the mapping, before trusting it
-            ok = 1.0
-        except Exception as e:  # noqa: BLE001 -- reported, then the NCCL transport
-            print(f"[bench] rank {rank}: P2P transport unavailable ({e}); using NCCL",
-                  file=sys.stderr, flush=True)
-            ok = 0.0
-        if allmax(1.0 - ok) > 0:
-            if layer is not None:
-                layer.close()
-            layer, transport = None, "nccl"
-    if world > 1 and transport == "nccl":
-        obj = [moe.moe_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        uid = obj[0]
-    if layer is None:
-        layer = moe.MoELayer(cfg.hidden, cfg.ffn, cfg.num_experts, cfg.top_k, Tr,
-                             num_shared=cfg.num_shared, device=local, profile=True,
-                             packet_bytes=int(args.packet_mb * 2 ** 20), mover=args.mover, world_size=world,
-                             rank=rank, nccl_unique_id=uid, num_slots=args.slots)
-    comm_nranks = layer.group_size()
-    if world > 1:
-        print(f"[bench] rank {rank}: expert-parallel transport {transport}, group size "
-              f"{comm_nranks} (NCCL: ncclCommCount)", file=sys.stderr, flush=True)
+                                 nccl_unique_id=uid, **mk)
+        return layer, transport
+
+    def drop_layer(layer):
+        layer.sync()
+        if world > 1:
+            dist.barrier()   # P2P: peers may read this rank's buffers until their combine ends
+        layer.close()
+
     stream = torch.cuda.Stream()
     sh = stream.cuda_stream
     layer_bytes = 0
@@ -360,6 +371,32 @@ def run_ours(args):
                                 outs[l], idxs[l], gws[l], stream=sh)
             return
         layer.forward(xs[l], routers[l], experts[l], outs[l], idxs[l], gws[l], stream=sh)
+
+    # e2e inputs: host token buffers through the host-buffer entry points (H2D tokens + D2H out)
+    if not args.no_e2e:
+        xh = [torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).pin_memory() for x in xslice]
+        oh = [torch.empty_like(x).pin_memory() for x in xh]
+        if args.taskb:   # attention output from host memory (the paper's CPU attention)
+            xh = [a.cpu().pin_memory() for a in attns]
+        half = Tr // 2   # --partitions 2: alpha = the first half of the rank's tokens
+        if args.partitions == 2:
+            if not args.taskb:
+                raise SystemExit("--partitions 2 needs --taskb (VSLPipe's partitions are Task B's)")
+            xh2 = [[x[:half], x[half:]] for x in xh]
+            oh2 = [[o[:half], o[half:]] for o in oh]
+            rs2 = [[r[:half], r[half:]] for r in resids]
+
+    def step_h(i):
+        l = i % args.layers
+        if args.taskb and args.partitions == 2:
+            layer.taskb_forward2_host(xh2[l], rs2[l], hls[l], tbs[l].eps, routers[l],
+                                      experts[l], oh2[l], stream=sh)
+            return
+        if args.taskb:
+            layer.taskb_forward_host(xh[l], resids[l], hls[l], tbs[l].eps, routers[l],
+                                     experts[l], oh[l], stream=sh)
+            return
+        layer.forward_host(xh[l], routers[l], experts[l], oh[l], stream=sh)
 
     def timed(fn, sampler=None, fence=None):
         for i in range(args.warmup):
@@ -388,17 +425,23 @@ def run_ours(args):
         timed.dist = {"p10": q(0.1), "p50": q(0.5), "p90": q(0.9)}
         return allmax(evs[0].elapsed_time(evs[-1])) / args.steps
 
+    # ---- pass 1 (the headline): the library's default configuration, MOE_FLAG_PROFILE off --
+    # no event brackets or clock probes in the timed region
+    layer, transport = make_layer(False)
+    comm_nranks = layer.group_size()
+    if world > 1:
+        print(f"[bench] rank {rank}: expert-parallel transport {transport}, group size "
+              f"{comm_nranks} (NCCL: ncclCommCount)", file=sys.stderr, flush=True)
     clocks = ClockSampler(local)
     ms = timed(step, clocks)
     step_dist = dict(timed.dist)
     clk = clocks.result
-    st = layer.stats()
     value = T / (ms / 1e3)
-    # every expert is re-streamed every call: fewer staging slots than experts per call (the
-    # library enforces it for explicit slot counts; asserted here for the run's auto choice)
-    assert st["num_slots"] == 2 or st["num_slots"] < nl + cfg.num_shared, st["num_slots"]
-    assert st["h2d_weight_bytes"] >= args.steps * (nl + cfg.num_shared) * \
-        ledger.expert_bytes(cfg.hidden, cfg.ffn), "weights were not re-streamed every step"
+    ems = None
+    if not args.no_e2e:
+        ems = timed(step_h, fence=lambda: layer.wait_output(sh))
+        last = (args.warmup + args.steps - 1) % args.layers
+        e2e_match = bool(allmax(0.0 if torch.equal(oh[last].cuda(), outs[last]) else 1.0) == 0.0)
     # single-call latency: one isolated call (no cross-call prefetch), all ranks together
     if world > 1:
         dist.barrier()
@@ -409,6 +452,22 @@ def run_ours(args):
     l1.record(stream)
     torch.cuda.synchronize()
     latency_ms = allmax(l0.elapsed_time(l1))
+    drop_layer(layer)
+
+    # ---- pass 2 (the explanation): MOE_FLAG_PROFILE on -- per-kernel CUDA-event times, the
+    # dominant kernel's roofline, the in-kernel SM clock, copy-stream busy time
+    layer, _ = make_layer(True)
+    ms_prof = timed(step)
+    st = layer.stats()
+    est = None
+    if not args.no_e2e:
+        timed(step_h, fence=lambda: layer.wait_output(sh))
+        est = layer.stats()
+    # every expert is re-streamed every call: fewer staging slots than experts per call (the
+    # library enforces it for explicit slot counts; asserted here for the run's auto choice)
+    assert st["num_slots"] == 2 or st["num_slots"] < nl + cfg.num_shared, st["num_slots"]
+    assert st["h2d_weight_bytes"] >= args.steps * (nl + cfg.num_shared) * \
+        ledger.expert_bytes(cfg.hidden, cfg.ffn), "weights were not re-streamed every step"
 
     # ---- work ledger (experts hit: from the routing of the timed layers, all ranks)
     cnt = torch.zeros(cfg.num_experts, dtype=torch.int64, device="cuda")
@@ -435,10 +494,16 @@ def run_ours(args):
     g1_flops_launch = g1_flops_total / max(1.0, g1_n)
     g1_launch_ms = g1_ms / max(1.0, g1_n)
     achieved_tf = g1_flops_launch / (g1_launch_ms * 1e-3) / 1e12 if g1_launch_ms > 0 else 0.0
-    traffic = None
+    # DRAM bytes per GEMM1 launch from one `ncu --set full` capture (dram__bytes_read.sum +
+    # dram__bytes_write.sum) of the committed build, kept in profiles/ncu_traffic.json with its
+    # provenance (round, capture command) -- ncu cannot run inside the timed bench
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(cfg.name, {}).get("gemm1_dram_bytes_per_launch")
+        tj = json.load(open(tp))
+        key = cfg.name + ("@%d" % T if args.tokens else "")
+        traffic = tj.get(key, {}).get("gemm1_dram_bytes_per_launch")
+        traffic_src = tj.get(key, {}).get("source", tj.get("source"))
     # Peak: the BURST cuBLAS figure.  The kernel runs inside a long step, but the step is
     # host-link bound and the GPU idles between expert GEMMs (~0.2-ms bursts, nvidia-smi sees
     # boost clock, `clocks`), so the burst peak is the conservative denominator; the sustained-peak
@@ -451,6 +516,7 @@ def run_ours(args):
                 "unit": "TFLOP/s", "frac": achieved_tf / peaks["bf16_tflops"],
                 "frac_of_sustained_peak": achieved_tf / peaks["bf16_tflops_sustained"],
                 "traffic": traffic if world == 1 else None,
+                "traffic_source": traffic_src if world == 1 else None,
                 "peak_source": peaks["source"] + " bf16_tflops (burst)",
                 "flops_per_launch": g1_flops_launch, "avg_launch_ms": g1_launch_ms}
     # The SM clock the GEMM1 launches actually ran at (in-kernel clock64 / globaltimer, CTA 0,
@@ -485,36 +551,9 @@ def run_ours(args):
                       "comm_ms", "oproj_ms", "norm_ms")}
     launches = allsum(st["kernel_launches"])
 
-    # ---- e2e: host token buffers through moe_layer_forward_host (H2D tokens + D2H output)
+    # ---- e2e (pass 1's time; pass 2's copy-stream diagnostics)
     e2e = None
     if not args.no_e2e:
-        xh = [torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).pin_memory() for x in xslice]
-        oh = [torch.empty_like(x).pin_memory() for x in xh]
-
-        if args.taskb:   # attention output from host memory (the paper's CPU attention)
-            xh = [a.cpu().pin_memory() for a in attns]
-        half = Tr // 2   # --partitions 2: alpha = the first half of the rank's tokens
-        if args.partitions == 2:
-            if not args.taskb:
-                raise SystemExit("--partitions 2 needs --taskb (VSLPipe's partitions are Task B's)")
-            xh2 = [[x[:half], x[half:]] for x in xh]
-            oh2 = [[o[:half], o[half:]] for o in oh]
-            rs2 = [[r[:half], r[half:]] for r in resids]
-
-        def step_h(i):
-            l = i % args.layers
-            if args.taskb and args.partitions == 2:
-                layer.taskb_forward2_host(xh2[l], rs2[l], hls[l], tbs[l].eps, routers[l],
-                                          experts[l], oh2[l], stream=sh)
-                return
-            if args.taskb:
-                layer.taskb_forward_host(xh[l], resids[l], hls[l], tbs[l].eps, routers[l],
-                                         experts[l], oh[l], stream=sh)
-                return
-            layer.forward_host(xh[l], routers[l], experts[l], oh[l], stream=sh)
-
-        ems = timed(step_h, fence=lambda: layer.wait_output(sh))
-        est = layer.stats()
         tok_bytes = T * cfg.hidden * 2
         e2e = {"value": T / (ems / 1e3), "unit": "tokens/s", "ms_per_step": ems,
                "h2d_bytes_per_step": tok_bytes + step_weight_bytes,
@@ -525,21 +564,20 @@ def run_ours(args):
                        "moe_taskb_forward_host (pinned host attention output / result, device "
                        "residual)" if args.taskb else
                        "moe_layer_forward_host (pinned host hidden/out)"),
-               "copy_stream_ms_per_step": {
+               "copy_stream_ms_per_step_profile_pass": {
                    "weights": est["h2d_ms"] / args.steps, "tokens": est["h2d_token_ms"] / args.steps,
                    "note": "summed CUDA-event durations of the H2D copies (link busy time)"},
-               "token_copy_latency_ms": {
+               "token_copy_latency_ms_profile_pass": {
                    "per_partition": [est["part_latency_ms"][p] / max(1, est["part_copies"][p])
                                      for p in range(2)],
                    "copies": est["part_copies"],
-                   "note": "enqueue -> resident of each host token copy (partition 1 = beta)"}}
-        last = (args.warmup + args.steps - 1) % args.layers
-        e2e["matches_device_path"] = bool(allmax(0.0 if torch.equal(oh[last].cuda(), outs[last]) else 1.0) == 0.0)
+                   "note": "enqueue -> resident of each host token copy (partition 1 = beta)"},
+               "matches_device_path": e2e_match}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:   # the oracle baseline: N = 1 only
         os.sched_setaffinity(0, all_cpus)   # the oracle gets every host core
-        cpu = cpu_baseline(layers[0], args.cpu_seconds)
+        cpu = cpu_baseline(layers[0], args.cpu_seconds, args.cpu_one_thread_tokens)
 
     # Per-expert rows of the last call on this rank (the load histogram goes with
     # every result; it is what makes DeepSeek-V2-Lite's grouped GEMMs uneven).
@@ -574,6 +612,7 @@ def run_ours(args):
                        "l2": "inputs larger than L2: all expert weights re-streamed from host each step",
                        "parallelism": f"ep{world}", "ep_transport": transport,
                        "ep_comm_nranks": comm_nranks},
+            "ms_per_step_profile_pass": ms_prof,
             "roofline": roofline, "roofline_step": roofline_step,
             "per_kernel_ms_per_step_rank0": per_kernel_ms,
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
@@ -584,10 +623,7 @@ def run_ours(args):
             "host_affinity": affinity, "routing_rank0": routing}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    layer.sync()
-    if world > 1:
-        dist.barrier()   # P2P: peers may read this rank's buffers until their last combine ends
-    layer.close()
+    drop_layer(layer)
     for e in experts:
         e.close()
     if args.taskb:

@@ -254,31 +254,36 @@ moe_status request_copy(moe_ctx c, const void* const* experts, int i, uint64_t q
 
 // Tile shape of one GEMM launch: the CTA-pair kernel (256x256 tiles on SM pairs, ~97% tensor-pipe
 // activity) or the single-CTA kernel (128 x bn tiles, ~76%: shared-memory bandwidth bound, but
-// half the M granularity and twice the concurrent tiles), by a wave model on the EXPECTED rows of
-// each of the launch's n groups: time ~ ceil(tiles / concurrent tiles) x tile width / efficiency.
-bool pick_pair(moe_ctx c, const int64_t* rows, int n, int bn, int N) {
+// half the M granularity and twice the concurrent tiles), by a wave model on the EXPECTED tiles
+// of the launch's n groups: time ~ ceil(tiles / concurrent tiles) x tile width / efficiency.
+// rows[i]: a group's expected rows; `routed`: the counts are a routing outcome (mean rows[i],
+// spread ~ sqrt), so a group's last M tile is on average half full -- expected tiles = rows/BM
+// + 1/2 -- else (shared experts, the O-projection: exactly rows[i]) tiles = ceil(rows/BM).
+// (Round 1 used rows + 10% instead, which at C1 predicted 3 waves of CTA-pair tiles for GEMM2
+// of two 1024-row experts where the actual routing gives 2, and so chose the slower kernel.)
+bool pick_pair(moe_ctx c, const int64_t* rows, int n, int bn, int N, bool routed) {
     if (bn != 256 || N % 256 || c->pair_mode == 0) return false;
     if (c->pair_mode == 1) return true;
     const int sms = c->num_sms;
-    int64_t t1 = 0, t2 = 0;
+    double t1 = 0, t2 = 0;
     for (int i = 0; i < n; ++i) {
         if (rows[i] <= 0) continue;
-        t1 += ((rows[i] + 127) / 128) * (N / bn);
-        t2 += ((rows[i] + 255) / 256) * (N / 256);
+        t1 += (routed ? rows[i] / 128.0 + 0.5 : (double)((rows[i] + 127) / 128)) * (N / bn);
+        t2 += (routed ? rows[i] / 256.0 + 0.5 : (double)((rows[i] + 255) / 256)) * (N / 256);
     }
     if (t1 == 0) return false;
-    const double w1 = (double)((t1 + sms - 1) / sms) / 0.76;
-    const double w2 = (double)((t2 + sms / 2 - 1) / (sms / 2)) / 0.97;
+    const double w1 = std::ceil(t1 / sms - 1e-9) / 0.76;
+    const double w2 = std::ceil(t2 / (sms / 2) - 1e-9) / 0.97;
     return w2 < w1;
 }
 
 // One expert-GEMM launch over a batch of groups on `st` (pair: tmB_pair, else tmB).
-moe_status launch_grouped(moe_ctx c, int mode, int bn, const int64_t* rows,
+moe_status launch_grouped(moe_ctx c, int mode, int bn, const int64_t* rows, bool routed,
                           const CUtensorMap* tmA, const CUtensorMap* tmB,
                           const CUtensorMap* tmB_pair, const moe::GemmBatch& batch, int N, int K,
                           __nv_bfloat16* out, int ldo, cudaStream_t st,
                           const __nv_bfloat16* resid = nullptr) {
-    const bool pair = pick_pair(c, rows, batch.n, bn, N);
+    const bool pair = pick_pair(c, rows, batch.n, bn, N, routed);
     MOE_CUDA(c, moe::launch_expert_gemm(mode, bn, pair, tmA, pair ? tmB_pair : tmB, batch, N, K,
                                         out, ldo, resid, c->num_sms, st));
     return MOE_OK;
@@ -394,11 +399,11 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
             b1.idx[j] = b2.idx[j] = e;
             b1.b_row[j] = 3 * hi * sj;           // W13 of slot sj in tm_w13*
             b2.b_row[j] = 3 * h * sj + 2 * h;    // W2 of slot sj in tm_w2*
-            rows[j] = shared ? (int64_t)T : exp_routed + exp_routed / 10;
+            rows[j] = shared ? (int64_t)T : exp_routed;
         }
         {
             Prof p(c, moe::kRecGemm1, st);
-            moe_status gs = launch_grouped(c, moe::kGemmSwiGLU, c->bn1, rows,
+            moe_status gs = launch_grouped(c, moe::kGemmSwiGLU, c->bn1, rows, !shared,
                                            shared ? &tm_x : tmA_routed, &c->tm_w13,
                                            &c->tm_w13_pair, b1, 2 * hi, h, c->h_act, hi, st);
             if (gs != MOE_OK) return gs;
@@ -413,7 +418,7 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         }
         {
             Prof p(c, moe::kRecGemm2, st);
-            moe_status gs = launch_grouped(c, moe::kGemmPlain, c->bn2, rows, &c->tm_h, &c->tm_w2,
+            moe_status gs = launch_grouped(c, moe::kGemmPlain, c->bn2, rows, !shared, &c->tm_h, &c->tm_w2,
                                            &c->tm_w2_pair, b2, h, hi,
                                            shared ? c->y_perm : y_routed, h, st);
             if (gs != MOE_OK) return gs;
@@ -710,7 +715,7 @@ moe_status taskb_front(moe_ctx c, const CUtensorMap& tm_attn, const TbPart& pt, 
         ob.table = c->oproj_grp + gi;
         ob.n = 1;   // idx[0] = 0, b_row[0] = 0: Wo is the whole map
         const int64_t rows = pt.T;
-        moe_status gs = launch_grouped(c, moe::kGemmResidual, c->bn2, &rows, &tm_attn,
+        moe_status gs = launch_grouped(c, moe::kGemmResidual, c->bn2, &rows, false, &tm_attn,
                                        &c->tm_wo[lb], &c->tm_wo_pair[lb], ob, h, h, h1, h, st,
                                        pt.resid);
         if (gs != MOE_OK) return gs;

@@ -260,20 +260,29 @@ router_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
     }
 }
 
-// Router v4: the same one-FMA-chain-per-logit arithmetic (reading R6), restructured for latency:
-//   * x is read by the lane that owns the token, straight from global memory (16-byte vectors of 8
-//     channels, prefetched two vectors ahead in registers) and widened to fp64 in registers --
-//     no shared-memory staging of x, no barrier per x tile;
-//   * the router weights are staged once per block into shared memory as fp64, in chunks of CW
-//     channels x ne_pad experts, double-buffered: chunk j+1 is loaded into registers while chunk
-//     j is consumed and stored into the other buffer at its end -- ONE __syncthreads per chunk;
-//   * warp w owns experts [w*EPT, (w+1)*EPT) of the block's 32*TPT tokens; per channel a lane
-//     reads EPT/2 double2 broadcasts and runs TPT*EPT independent chains.
-// Few experts (C1: 8) -> EPT = 2, 4 warps per 32 tokens: 16k warps' worth of chains spread over
-// every SM; many experts (C4: 64) -> EPT = 8, TPT = 2 (each broadcast feeds 16 DFMAs).
+// cp.async of 16 bytes global -> shared; src_bytes = 0 zero-fills the destination.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(ptx::smem_u32(smem)),
+                 "l"(gmem), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Router v5: the same one-FMA-chain-per-logit arithmetic (reading R6), restructured so shared
+// memory stops being the bottleneck and each chunk costs one barrier:
+//   * channels are consumed in chunks of CW; per chunk the block's token rows (bf16, cp.async,
+//     coalesced, rows padded by 16 B so the per-lane 16-byte row reads are conflict-free) and the
+//     router rows (widened to fp64 once, [channel][expert]) are staged into the other half of a
+//     double buffer while the current chunk is consumed -- ONE __syncthreads per chunk;
+//   * a lane owns TPT tokens and EPT experts (warp w: experts [w*EPT, (w+1)*EPT)); per 8
+//     channels it reads each token's 16-byte row slice once (widened to fp64 in registers) and
+//     EPT/2 double2 broadcasts of router weights per channel, feeding TPT*EPT independent chains.
+// Per warp and 8 channels: TPT x (4 wavefronts of row reads) + 4 EPT broadcast wavefronts for
+// 8 TPT EPT warp-DFMAs; with EPT >= 4 the fp64 pipe (not shared memory) is the limit.
 template <int EPT, int TPT>
 __global__ void __launch_bounds__(512)
-router_v4_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
+router_v5_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
                  const __nv_bfloat16* __restrict__ wr, int ne, int k, int renorm, int cw,
                  int32_t* __restrict__ idx_out, float* __restrict__ gate_out,
                  int32_t* __restrict__ tile_counts) {
@@ -284,12 +293,16 @@ router_v4_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
     const int ne_pad = nw * EPT;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
     const int t0 = blockIdx.x * kTok;
+    const int xpitch = cw + 8;   // bf16 per staged row (16 B of padding)
+    double* wbuf = dyn;                                                       // [2][cw][ne_pad]
+    __nv_bfloat16* xbuf = reinterpret_cast<__nv_bfloat16*>(dyn + 2 * (size_t)cw * ne_pad);  // [2][kTok][xpitch]
     for (int e = tid; e < TPT * kMaxExperts; e += nthr) cnt[e / kMaxExperts][e % kMaxExperts] = 0;
 
-    // router chunk staging: vector v of a chunk = 8 channels of expert v % ne_pad
+    // router chunk: vector v = 8 channels of expert v % ne_pad, through registers (widened)
+    constexpr int kMaxWV = 4;   // (cw / 8) * ne_pad <= 4 * nthr  (host: cw * EPT <= 1024)
     const int n_wv = (cw / 8) * ne_pad;
-    constexpr int kMaxWV = 4;   // n_wv <= 4 * nthr (host: cw * EPT <= 1024)
-    auto wload = [&](int c0, int4 (&wv)[kMaxWV]) {
+    int4 wv[kMaxWV];
+    auto wload = [&](int c0) {
 #pragma unroll
         for (int j = 0; j < kMaxWV; ++j) {
             const int v = tid + j * nthr;
@@ -299,7 +312,8 @@ router_v4_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
             }
         }
     };
-    auto wstore = [&](double* ws, const int4 (&wv)[kMaxWV]) {
+    auto wstore = [&](int b) {
+        double* ws = wbuf + (size_t)b * cw * ne_pad;
         double d[8];
 #pragma unroll
         for (int j = 0; j < kMaxWV; ++j) {
@@ -312,72 +326,76 @@ router_v4_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
             }
         }
     };
-    int4 wv[kMaxWV];
-    wload(0, wv);
-    wstore(dyn, wv);
+    // token chunk: row r's channels [c0, c0 + cw) -> xbuf[b][r][0 .. cw), 16 B per cp.async
+    const int n_xv = kTok * (cw / 8);
+    auto xstage = [&](int c0, int b) {
+        __nv_bfloat16* xs = xbuf + (size_t)b * kTok * xpitch;
+        for (int v = tid; v < n_xv; v += nthr) {
+            const int r = v / (cw / 8), cc = (v % (cw / 8)) * 8;
+            const int t = t0 + r;
+            cp_async16(xs + (size_t)r * xpitch + cc, x + (size_t)(t < T ? t : 0) * h + c0 + cc,
+                       t < T ? 16 : 0);
+        }
+        cp_async_commit();
+    };
+
+    xstage(0, 0);
+    wload(0);
+    wstore(0);
+    cp_async_wait_all();
     __syncthreads();
 
-    // this lane's token rows
-    const int4* xrow[TPT];
-    bool live[TPT];
-#pragma unroll
-    for (int p = 0; p < TPT; ++p) {
-        const int t = t0 + p * 32 + lane;
-        live[p] = t < T;
-        xrow[p] = reinterpret_cast<const int4*>(x + (size_t)(live[p] ? t : 0) * h);
-    }
     double acc[TPT][EPT];
 #pragma unroll
     for (int p = 0; p < TPT; ++p)
 #pragma unroll
         for (int i = 0; i < EPT; ++i) acc[p][i] = 0.0;
-    const int nvec = h / 8;
-    int4 xa[TPT], xb[TPT];   // vectors v and v + 1 in flight
-#pragma unroll
-    for (int p = 0; p < TPT; ++p) {
-        xa[p] = live[p] ? ptx::ld_nc_v4(xrow[p]) : make_int4(0, 0, 0, 0);
-        xb[p] = (live[p] && nvec > 1) ? ptx::ld_nc_v4(xrow[p] + 1) : make_int4(0, 0, 0, 0);
-    }
-    const int vpc = cw / 8;   // x vectors per chunk
-    int buf = 0;
-    for (int v = 0; v < nvec; ++v) {
-        const int vin = v % vpc;
-        if (vin == 0 && v + vpc < nvec) wload((v + vpc) * 8, wv);   // next chunk in flight
-        double xd[TPT][8];
-#pragma unroll
-        for (int p = 0; p < TPT; ++p) {
-            bf16x8_to_f64(xa[p], xd[p]);
-            xa[p] = xb[p];
-            xb[p] = (live[p] && v + 2 < nvec) ? ptx::ld_nc_v4(xrow[p] + v + 2) : make_int4(0, 0, 0, 0);
+    const int n_chunks = h / cw;
+    for (int ch = 0; ch < n_chunks; ++ch) {
+        const int b = ch & 1;
+        const bool more = ch + 1 < n_chunks;
+        if (more) {   // the next chunk in flight while this one is consumed
+            xstage((ch + 1) * cw, b ^ 1);
+            wload((ch + 1) * cw);
         }
-        const double* wrow = dyn + (size_t)buf * cw * ne_pad + (size_t)(vin * 8) * ne_pad + warp * EPT;
+        const __nv_bfloat16* xs = xbuf + (size_t)b * kTok * xpitch;
+        const double* ws = wbuf + (size_t)b * cw * ne_pad + warp * EPT;
+#pragma unroll 1
+        for (int c8 = 0; c8 < cw; c8 += 8) {
+            double xd[TPT][8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            if constexpr (EPT == 1) {
-                const double w = wrow[q * ne_pad];
+            for (int p = 0; p < TPT; ++p) {
+                const int4 raw = *reinterpret_cast<const int4*>(xs + (size_t)(p * 32 + lane) * xpitch + c8);
+                bf16x8_to_f64(raw, xd[p]);
+            }
 #pragma unroll
-                for (int p = 0; p < TPT; ++p) acc[p][0] = fma(xd[p][q], w, acc[p][0]);
-            } else {
-                const double2* w2 = reinterpret_cast<const double2*>(wrow + q * ne_pad);
+            for (int q = 0; q < 8; ++q) {
+                const double* wrow = ws + (size_t)(c8 + q) * ne_pad;
+                if constexpr (EPT == 1) {
+                    const double w = wrow[0];
 #pragma unroll
-                for (int i = 0; i < EPT / 2; ++i) {
-                    const double2 w = w2[i];
+                    for (int p = 0; p < TPT; ++p) acc[p][0] = fma(xd[p][q], w, acc[p][0]);
+                } else {
+                    const double2* w2 = reinterpret_cast<const double2*>(wrow);
 #pragma unroll
-                    for (int p = 0; p < TPT; ++p) {
-                        acc[p][2 * i] = fma(xd[p][q], w.x, acc[p][2 * i]);
-                        acc[p][2 * i + 1] = fma(xd[p][q], w.y, acc[p][2 * i + 1]);
+                    for (int i = 0; i < EPT / 2; ++i) {
+                        const double2 w = w2[i];
+#pragma unroll
+                        for (int p = 0; p < TPT; ++p) {
+                            acc[p][2 * i] = fma(xd[p][q], w.x, acc[p][2 * i]);
+                            acc[p][2 * i + 1] = fma(xd[p][q], w.y, acc[p][2 * i + 1]);
+                        }
                     }
                 }
             }
         }
-        if (vin == vpc - 1 && v + 1 < nvec) {   // end of a chunk: publish the next one
-            wstore(dyn + (size_t)(buf ^ 1) * cw * ne_pad, wv);
-            __syncthreads();
-            buf ^= 1;
+        if (more) {
+            wstore(b ^ 1);
+            cp_async_wait_all();
         }
+        __syncthreads();   // next chunk visible; this chunk's buffers free for chunk + 2
     }
-    __syncthreads();   // every lane done with the router chunks: the space takes the logits
-    double* lg = dyn;  // [kTok][ne_pad] (host sizes dyn for max(2 chunks, logits))
+    double* lg = dyn;  // [kTok][ne_pad] logits (host sizes dyn for it)
 #pragma unroll
     for (int p = 0; p < TPT; ++p)
 #pragma unroll
@@ -641,8 +659,8 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
     if (n_tiles == 0) return cudaSuccess;
     const char* ver = getenv("MOE_ROUTER");   // 3: round 1's kernel (comparison)
     if (ver && atoi(ver) == 3) return launch_router_v3(x, T, h, wr, ne, k, renorm, idx, gates, tile_counts, st);
-    // experts per warp: few experts -> 2 per warp (C1: 4 warps per 32 tokens, parallel chains on
-    // every SM); 16 -> 4; more -> 8 with two tokens per lane (every broadcast feeds 16 DFMAs)
+    // experts per warp: few experts -> 2 per warp (C1: 4 warps per 32 tokens, parallel chains
+    // on every SM); 16 -> 4; more -> 8 with two tokens per lane (every broadcast feeds 16 DFMAs)
     int ept = ne <= 8 ? 2 : (ne <= 16 ? 4 : 8);
     if (const char* e = getenv("MOE_ROUTER_EPT")) {   // experiments: 1, 2, 4 or 8
         const int v = atoi(e);
@@ -652,24 +670,27 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
     const int ne_pad = nw * ept;
     int tpt = (ept == 8 && nw >= 3 && nw <= 8) ? 2 : 1;
     if (const char* e = getenv("MOE_ROUTER_TPT")) tpt = atoi(e) == 2 ? 2 : 1;
-    int cw = 128;   // router channels per staged chunk: 2 chunks of fp64 <= 32 KB
-    while (cw > 8 && 2 * cw * ne_pad > 4096) cw >>= 1;
-    const size_t dyn = sizeof(double) * (size_t)std::max(2 * cw * ne_pad, kRouteTile * tpt * ne_pad);
-    const int blocks = (T + kRouteTile * tpt - 1) / (kRouteTile * tpt);
-#define MOE_ROUTER4(E, P)                                                                    \
+    const int ktok = kRouteTile * tpt;
+    int cw = 128;   // channels per staged chunk: 2 fp64 router chunks <= 32 KB, <= 4 vectors/thread
+    while (cw > 8 && (2 * cw * ne_pad > 4096 || cw * ept > 1024)) cw >>= 1;
+    const size_t wbytes = sizeof(double) * 2 * (size_t)cw * ne_pad;
+    const size_t xbytes = 2 * 2 * (size_t)ktok * (cw + 8);
+    const size_t dyn = std::max(wbytes + xbytes, sizeof(double) * (size_t)ktok * ne_pad);
+    const int blocks = (T + ktok - 1) / ktok;
+#define MOE_ROUTER5(E, P)                                                                    \
     do {                                                                                     \
-        cudaError_t e_ = cudaFuncSetAttribute(router_v4_kernel<E, P>,                        \
+        cudaError_t e_ = cudaFuncSetAttribute(router_v5_kernel<E, P>,                        \
             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);                          \
         if (e_ != cudaSuccess) return e_;                                                    \
-        router_v4_kernel<E, P><<<blocks, nw * 32, dyn, st>>>(x, T, h, wr, ne, k, renorm, cw,  \
+        router_v5_kernel<E, P><<<blocks, nw * 32, dyn, st>>>(x, T, h, wr, ne, k, renorm, cw,  \
                                                              idx, gates, tile_counts);       \
     } while (0)
-    if (ept == 1) MOE_ROUTER4(1, 1);
-    else if (ept == 2) { if (tpt == 2) MOE_ROUTER4(2, 2); else MOE_ROUTER4(2, 1); }
-    else if (ept == 4) { if (tpt == 2) MOE_ROUTER4(4, 2); else MOE_ROUTER4(4, 1); }
-    else if (tpt == 2) MOE_ROUTER4(8, 2);
-    else MOE_ROUTER4(8, 1);
-#undef MOE_ROUTER4
+    if (ept == 1) { if (tpt == 2) MOE_ROUTER5(1, 2); else MOE_ROUTER5(1, 1); }
+    else if (ept == 2) { if (tpt == 2) MOE_ROUTER5(2, 2); else MOE_ROUTER5(2, 1); }
+    else if (ept == 4) { if (tpt == 2) MOE_ROUTER5(4, 2); else MOE_ROUTER5(4, 1); }
+    else if (tpt == 2) MOE_ROUTER5(8, 2);
+    else MOE_ROUTER5(8, 1);
+#undef MOE_ROUTER5
     return cudaGetLastError();
 }
 

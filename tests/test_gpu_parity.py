@@ -352,12 +352,12 @@ def test_experts_per_gemm_launch(rows, copy_group, launches, monkeypatch):
         run.close()
 
 
-@pytest.mark.parametrize("variant", ["v3-1", "v3-2", "v3-4", "v3-8", "v4-1", "v4-2", "v4-4",
-                                     "v4-8", "v4-2-tpt2", "v4-4-tpt2", "v4-8-tpt1"])
+@pytest.mark.parametrize("variant", ["v3-1", "v3-2", "v3-4", "v3-8", "v5-1", "v5-2", "v5-4",
+                                     "v5-8", "v5-2-tpt2", "v5-4-tpt2", "v5-8-tpt1"])
 @pytest.mark.parametrize("ne,k", [(5, 2), (8, 2), (16, 4), (40, 6)])   # 40: 2 tokens per lane
 def test_router_experts_per_warp_variants(ne, k, variant, monkeypatch):
     """Every router kernel instantiation -- round 1's router_topk_kernel<EPT> (MOE_ROUTER=3) and
-    router_v4_kernel<EPT, TPT> (default; MOE_ROUTER_EPT / MOE_ROUTER_TPT) -- gives the same
+    router_v5_kernel<EPT, TPT> (default; MOE_ROUTER_EPT / MOE_ROUTER_TPT) -- gives the same
     bit-exact selection and gates (one fp64 FMA chain per logit, ascending channels, either way)."""
     ver, ept, *rest = variant.split("-")
     monkeypatch.setenv("MOE_ROUTER", ver[1])

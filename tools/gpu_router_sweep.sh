@@ -1,4 +1,4 @@
-# Router kernel sweep (v3 = round 1, v4 = register-x / double-buffered router chunks) on the
+# Router kernel sweep (v3 = round 1, v5 = cp.async token rows + double-buffered fp64 router chunks) on the
 # BASELINE shapes + the 131k-token C1 regime.  usage: bash tools/gpu_router_sweep.sh <outdir>
 O=${1:-gpurun_out/router}
 cd ${GRAFT_REPO_ROOT:-.}

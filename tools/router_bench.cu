@@ -43,7 +43,7 @@ int main(int argc, char** argv) {
     cudaEventElapsedTime(&ms, e0, e1);
     const double dfma = (double)T * ne * h;
     printf("router T=%d h=%d N_e=%d k=%d [MOE_ROUTER=%s EPT=%s TPT=%s]: %.1f us  %.2f TFLOP/s fp64 (%s)\n",
-           T, h, ne, k, getenv("MOE_ROUTER") ? getenv("MOE_ROUTER") : "4",
+           T, h, ne, k, getenv("MOE_ROUTER") ? getenv("MOE_ROUTER") : "5",
            getenv("MOE_ROUTER_EPT") ? getenv("MOE_ROUTER_EPT") : "auto",
            getenv("MOE_ROUTER_TPT") ? getenv("MOE_ROUTER_TPT") : "auto", 1e3 * ms / iters,
            2 * dfma / (ms / iters * 1e-3) / 1e12, cudaGetErrorString(err));
