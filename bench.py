@@ -62,6 +62,10 @@ def parse():
     ap.add_argument("--partitions", type=int, default=1, choices=[1, 2],
                     help="--taskb e2e: 2 = VSLPipe's alpha / beta token partitions through one "
                          "stream of the layer's weights (moe_taskb_forward2_host, PAPER.md:795-801)")
+    ap.add_argument("--shared", default="auto", choices=["auto", "replicated", "sharded"],
+                    help="shared experts under EP: sharded by intermediate columns across the "
+                         "ranks (MOE_FLAG_SHARD_SHARED, P2P transport) or replicated on every "
+                         "rank; auto = sharded when N > 1 with the p2p transport")
     ap.add_argument("--ep-transport", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1: p2p = fused dispatch/combine over peer memory (CUDA IPC), "
                          "falling back to NCCL if the peers cannot be mapped; nccl = NCCL "
@@ -264,6 +268,10 @@ def run_ours(args):
     Tr = T // world
     nl = cfg.num_experts // world
     ids = list(range(rank * nl, (rank + 1) * nl)) + [cfg.num_experts + s for s in range(cfg.num_shared)]
+    shard = (cfg.num_shared > 0 and world > 1 and
+             (args.shared == "sharded" or (args.shared == "auto" and args.ep_transport == "p2p")))
+    if shard and (args.ep_transport != "p2p" or args.mover):
+        raise SystemExit("--shared sharded needs the p2p transport and no --mover")
 
     def allmax(v):
         if world == 1:
@@ -298,7 +306,13 @@ def run_ours(args):
 
     # ---- inputs: L layers; this rank's token slice and only its own experts (pinned, packed)
     layers = [synth.gen_inputs(cfg, layer=l, expert_ids=ids) for l in range(args.layers)]
-    experts = [moe.HostExperts(cfg.hidden, cfg.ffn, l.w1, l.w3, l.w2) for l in layers]
+    if shard:   # routed experts + this rank's column slice of the concatenated shared FFN
+        experts = [moe.HostExperts(cfg.hidden, cfg.ffn, l.w1[:nl], l.w3[:nl], l.w2[:nl],
+                                   slice_=moe.shared_slice_weights(cfg.ffn, l.w1[nl:], l.w3[nl:],
+                                                                   l.w2[nl:], world, rank))
+                   for l in layers]
+    else:
+        experts = [moe.HostExperts(cfg.hidden, cfg.ffn, l.w1, l.w3, l.w2) for l in layers]
     xslice = [np.ascontiguousarray(l.x[rank * Tr:(rank + 1) * Tr]) for l in layers]
     xs = [torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).cuda() for x in xslice]
     routers = [torch.from_numpy(l.router.view(np.int16)).view(torch.bfloat16).cuda() for l in layers]
@@ -317,7 +331,7 @@ def run_ours(args):
         transport, layer, uid = transport0, None, None
         mk = dict(num_shared=cfg.num_shared, device=local, profile=profile,
                   packet_bytes=int(args.packet_mb * 2 ** 20), mover=args.mover, world_size=world,
-                  rank=rank, num_slots=args.slots)
+                  rank=rank, num_slots=args.slots, shard_shared=shard)
         if transport == "p2p":   # CUDA IPC peer mapping; every rank must succeed, else NCCL
             try:
                 layer = moe.MoELayer(cfg.hidden, cfg.ffn, cfg.num_experts, cfg.top_k, Tr,
@@ -334,6 +348,9 @@ def run_ours(args):
             if allmax(1.0 - ok) > 0:
                 if layer is not None:
                     layer.close()
+                if shard:
+                    raise SystemExit("P2P transport unavailable: sharded shared experts need it "
+                                     "(run with --shared replicated)")
                 layer, transport = None, "nccl"
         if world > 1 and transport == "nccl":
             obj = [moe.moe_nccl_unique_id() if rank == 0 else None]
@@ -453,6 +470,13 @@ def run_ours(args):
     torch.cuda.synchronize()
     latency_ms = allmax(l0.elapsed_time(l1))
     drop_layer(layer)
+    # the link probe again, after the headline pass: a shared host's other traffic makes single
+    # probes vary by ~10% from box to box; the roofline takes the better of the two (the
+    # bandwidth the link demonstrably has), both are reported
+    if world > 1:
+        dist.barrier()
+    probe_after = moe.moe_probe_h2d(local, 1 << 30, 5)
+    probe_before, probe_gbs = probe_gbs, max(probe_gbs, probe_after)
 
     # ---- pass 2 (the explanation): MOE_FLAG_PROFILE on -- per-kernel CUDA-event times, the
     # dominant kernel's roofline, the in-kernel SM clock, copy-stream busy time
@@ -465,9 +489,10 @@ def run_ours(args):
         est = layer.stats()
     # every expert is re-streamed every call: fewer staging slots than experts per call (the
     # library enforces it for explicit slot counts; asserted here for the run's auto choice)
-    assert st["num_slots"] == 2 or st["num_slots"] < nl + cfg.num_shared, st["num_slots"]
-    assert st["h2d_weight_bytes"] >= args.steps * (nl + cfg.num_shared) * \
-        ledger.expert_bytes(cfg.hidden, cfg.ffn), "weights were not re-streamed every step"
+    streamed = nl + (int(experts[0].slice_bytes > 0) if shard else cfg.num_shared)
+    assert st["num_slots"] == 2 or st["num_slots"] < streamed, st["num_slots"]
+    assert st["h2d_weight_bytes"] >= args.steps * experts[0].nbytes, \
+        "weights were not re-streamed every step"
 
     # ---- work ledger (experts hit: from the routing of the timed layers, all ranks)
     cnt = torch.zeros(cfg.num_experts, dtype=torch.int64, device="cuda")
@@ -478,7 +503,7 @@ def run_ours(args):
     hit = int((cnt > 0).sum().item())
     work = ledger.layer_work(T, cfg.hidden, cfg.ffn, cfg.num_experts, cfg.top_k, cfg.num_shared,
                              experts_hit=hit)
-    rank_bytes = (nl + cfg.num_shared) * ledger.expert_bytes(cfg.hidden, cfg.ffn) + layer_bytes
+    rank_bytes = experts[0].nbytes + layer_bytes
     step_weight_bytes = work.weight_bytes + world * layer_bytes
     oproj_flops = 2.0 * T * cfg.hidden * cfg.hidden if args.taskb else 0.0
     # Host-link roofline on ALGORITHMIC bytes: the layer's weights once, split over W links
@@ -538,6 +563,7 @@ def run_ours(args):
                      "roofline_tokens_per_s": T / t_roof,
                      "host_link_probe_gbs_rank0": probe_gbs,
                      "host_link_probe_gbs_min": -allmax(-probe_gbs),
+                     "host_link_probe_gbs_rank0_before_after": [probe_before, probe_after],
                      "h2d_achieved_gbs_in_copies_rank0": h2d_gbs,
                      "h2d_aggregate_gbs_over_step": step_weight_bytes / (ms * 1e-3) / 1e9,
                      "weight_bytes_per_step": step_weight_bytes,
@@ -607,7 +633,8 @@ def run_ours(args):
                        "hidden": cfg.hidden, "ffn": cfg.ffn, "experts": cfg.num_experts,
                        "experts_per_rank": nl, "top_k": cfg.top_k, "num_shared": cfg.num_shared,
                        "layers_cycled": args.layers, "staging_slots": st["num_slots"],
-                       "experts_streamed_per_call": nl + cfg.num_shared,
+                       "experts_streamed_per_call": streamed,
+                       "shared_experts": ("sharded" if shard else "replicated") if cfg.num_shared else None,
                        "packet_mb": args.packet_mb, "mover": bool(args.mover),
                        "l2": "inputs larger than L2: all expert weights re-streamed from host each step",
                        "parallelism": f"ep{world}", "ep_transport": transport,

@@ -74,13 +74,30 @@ typedef enum {
                                 every expert copy already requested.  The copies and the GEMMs
                                 are ordered by device counters (stream memory operations);
                                 MOE_E_UNSUPPORTED if the driver lacks them.                      */
+#define MOE_FLAG_SHARD_SHARED 32u /* shared experts SHARDED across the expert-parallel group
+                                 instead of replicated on every rank.  Needs
+                                the P2P transport (LOCAL_EP / IPC_EP), world_size > 1 and
+                                1 <= num_shared <= world_size; not with MOE_FLAG_MOVER.  The S
+                                shared experts are one FFN of width S*ffn (their concatenation,
+                                DESIGN.md reading R10) and a SwiGLU FFN is a sum over blocks of
+                                its intermediate columns:  W2 (silu(W1 x) * W3 x) =
+                                sum_B W2[:,B] (silu(W1[B] x) * W3[B] x).  Rank r streams only
+                                the column slice moe_shared_slice() gives it (~S*ffn/W wide, so
+                                the per-rank host bytes are the algorithmic total / W); the
+                                permute kernel also writes every local token row into every
+                                slice owner (the all-gather, over peer memory), each owner runs
+                                its slice over all ranks' tokens, and the combine kernel of the
+                                token's rank adds the owners' partial rows in rank order (fp32)
+                                -- the reduce-scatter.  Output differs from the replicated
+                                layout by summation order only (within the same 2e-2 bar).      */
 
 /*
  * Layer configuration.  Envelope of the sm_100a kernels (MOE_E_UNSUPPORTED otherwise):
  *   hidden % 128 == 0, ffn % 128 == 0, 1 <= num_experts <= 128, 1 <= top_k <= min(num_experts, 8),
  *   0 <= num_shared <= 8, max_tokens >= 1.
  * Multi-GPU expert parallelism (world_size > 1): num_experts % world_size == 0; rank r owns the
- * routed experts [r*N_e/W, (r+1)*N_e/W); shared experts are replicated on every rank.
+ * routed experts [r*N_e/W, (r+1)*N_e/W); shared experts are replicated on every rank, or
+ * sharded by intermediate columns with MOE_FLAG_SHARD_SHARED.
  */
 typedef struct {
     int32_t hidden;           /* h                                          */
@@ -119,6 +136,20 @@ int64_t moe_packed_expert_bytes(int32_t hidden, int32_t ffn);
 moe_status moe_pack_expert(int32_t hidden, int32_t ffn, const void* w1, const void* w3,
                            const void* w2, void* dst);
 
+/* MOE_FLAG_SHARD_SHARED: the columns [*col0, *col0 + *width) of the concatenated shared
+ * intermediate dimension (num_shared * ffn wide; shared expert s holds columns [s*ffn,
+ * (s+1)*ffn)) that rank `rank` of `world` serves.  The concatenation's B = num_shared*ffn/128
+ * blocks of 128 columns are split evenly in rank order: rank r takes blocks
+ * [floor(r*B/W), floor((r+1)*B/W)), so widths differ by at most 128 and may be 0.
+ * The rank's slice blob is moe_pack_expert(hidden, *width, W1s, W3s, W2s) with W1s / W3s = rows
+ * [col0, col0 + width) of the shared experts' row-stacked W1 / W3 ([S*ffn, h]) and W2s = columns
+ * [col0, col0 + width) of their column-concatenated W2 ([h, S*ffn]); it is the last entry of the
+ * rank's `experts` array (no entry when *width == 0).  Host-only, synchronous.
+ * MOE_E_INVAL on NULL outputs, ffn % 128 != 0, num_shared < 1, world < 1 or rank outside
+ * [0, world). */
+moe_status moe_shared_slice(int32_t ffn, int32_t num_shared, int32_t world, int32_t rank,
+                            int32_t* col0, int32_t* width);
+
 /* Pinned host allocation helpers (cudaHostAlloc, portable).  The blobs passed to
  * moe_layer_forward must be page-locked; these are one way to get such memory. */
 moe_status moe_host_alloc(size_t bytes, void** ptr);
@@ -138,7 +169,9 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out);
  *   num_tokens  0 <= T <= max_tokens (0 = no-op).
  *   router_w    device bf16 [N_e, h] row-major (all routed experts, on every rank).
  *   experts     host array of (N_e/W + num_shared) pointers to PINNED packed blobs: this rank's
- *               routed experts in increasing expert id, then the shared experts.
+ *               routed experts in increasing expert id, then the shared experts.  With
+ *               MOE_FLAG_SHARD_SHARED: N_e/W routed blobs, then the rank's shared slice blob
+ *               (moe_shared_slice) if its width is not 0.
  *   top_k       must equal cfg->top_k.
  *   out         device bf16 [num_tokens, h].
  *   topk_idx    optional device int32 [num_tokens, top_k] (NULL = not returned): the selected

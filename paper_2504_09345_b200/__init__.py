@@ -37,9 +37,10 @@ EXPORTED = ["moe_packed_expert_bytes", "moe_pack_expert", "moe_host_alloc", "moe
             "moe_packed_layer_bytes", "moe_pack_layer", "moe_taskb_forward",
             "moe_taskb_forward_host", "moe_ep_ipc_handle", "moe_ep_ipc_connect",
             "moe_ep_ipc_selftest", "moe_wait_output", "moe_taskb_forward2_host",
-            "moe_ep_group_size"]
+            "moe_ep_group_size", "moe_shared_slice"]
 MOE_FLAG_IPC_EP = 8
 MOE_FLAG_MOVER = 16
+MOE_FLAG_SHARD_SHARED = 32
 MOE_IPC_HANDLE_BYTES = 512
 
 
@@ -134,6 +135,8 @@ def load(path: str = LIB_PATH):
     lib.moe_wait_output.argtypes = [P, P]
     lib.moe_ep_group_size.argtypes = [P, ctypes.POINTER(ctypes.c_int32)]
     lib.moe_taskb_forward2_host.argtypes = [P, P, P, P, P, ctypes.c_float, P, P, i32, P, P, P, P]
+    lib.moe_shared_slice.argtypes = [i32, i32, i32, i32, ctypes.POINTER(ctypes.c_int32),
+                                     ctypes.POINTER(ctypes.c_int32)]
     for name in EXPORTED:
         if name not in ("moe_packed_expert_bytes", "moe_status_string", "moe_last_error",
                         "moe_ep_plan", "moe_packed_layer_bytes"):
@@ -162,6 +165,27 @@ def moe_pack_expert(hidden: int, ffn: int, w1: np.ndarray, w3: np.ndarray, w2: n
     for a in (w1, w3, w2):
         assert a.dtype == np.uint16 and a.flags.c_contiguous
     _check(load().moe_pack_expert(hidden, ffn, w1.ctypes.data, w3.ctypes.data, w2.ctypes.data, dst))
+
+
+def moe_shared_slice(ffn: int, num_shared: int, world: int, rank: int) -> tuple:
+    """(col0, width): rank's columns of the concatenated shared FFN (MOE_FLAG_SHARD_SHARED)."""
+    c0, w = ctypes.c_int32(), ctypes.c_int32()
+    _check(load().moe_shared_slice(ffn, num_shared, world, rank, ctypes.byref(c0), ctypes.byref(w)))
+    return c0.value, w.value
+
+
+def shared_slice_weights(ffn: int, w1s: Sequence[np.ndarray], w3s: Sequence[np.ndarray],
+                         w2s: Sequence[np.ndarray], world: int, rank: int):
+    """The rank's slice of the shared experts (canonical bf16 bit patterns), or None if its width
+    is 0: rows [col0, col0 + width) of the row-stacked W1 / W3 and the same columns of the
+    column-concatenated W2 (include/moe.h, moe_shared_slice) -- array slicing only."""
+    c0, w = moe_shared_slice(ffn, len(w1s), world, rank)
+    if w == 0:
+        return None
+    w1 = np.ascontiguousarray(np.concatenate(list(w1s), axis=0)[c0:c0 + w])
+    w3 = np.ascontiguousarray(np.concatenate(list(w3s), axis=0)[c0:c0 + w])
+    w2 = np.ascontiguousarray(np.concatenate(list(w2s), axis=1)[:, c0:c0 + w])
+    return w1, w3, w2
 
 
 def moe_host_alloc(nbytes: int) -> int:
@@ -309,13 +333,16 @@ class HostExperts:
     """Pinned, packed expert blobs of one layer (this rank's routed experts, then shared)."""
 
     def __init__(self, hidden: int, ffn: int, w1: Sequence[np.ndarray], w3: Sequence[np.ndarray],
-                 w2: Sequence[np.ndarray], contiguous: bool = True):
+                 w2: Sequence[np.ndarray], contiguous: bool = True, slice_=None):
         """contiguous: one pinned region holding every blob back to back (the library then
-        moves consecutive small experts with one DMA); else one allocation per expert."""
+        moves consecutive small experts with one DMA); else one allocation per expert.
+        slice_: (w1, w3, w2) of a shared-FFN slice (shared_slice_weights) appended as the last
+        blob, in an allocation of its own (MOE_FLAG_SHARD_SHARED)."""
         self.hidden, self.ffn = hidden, ffn
         self.blob_bytes = moe_packed_expert_bytes(hidden, ffn)
         self.ptrs: List[int] = []
         self._allocs: List[int] = []
+        self.slice_bytes = 0
         n = len(w1)
         try:
             if contiguous and n > 0:
@@ -329,6 +356,15 @@ class HostExperts:
             for p, a, b, c in zip(self.ptrs, w1, w3, w2):
                 moe_pack_expert(hidden, ffn, np.ascontiguousarray(a), np.ascontiguousarray(b),
                                 np.ascontiguousarray(c), p)
+            if slice_ is not None:
+                a, b, c = slice_
+                width = a.shape[0]
+                self.slice_bytes = moe_packed_expert_bytes(hidden, width)
+                p = moe_host_alloc(self.slice_bytes)
+                self._allocs.append(p)
+                self.ptrs.append(p)
+                moe_pack_expert(hidden, width, np.ascontiguousarray(a), np.ascontiguousarray(b),
+                                np.ascontiguousarray(c), p)
         except Exception:
             self.close()
             raise
@@ -336,7 +372,8 @@ class HostExperts:
 
     @property
     def nbytes(self) -> int:
-        return self.blob_bytes * len(self.ptrs)
+        n = len(self.ptrs) - (1 if self.slice_bytes else 0)
+        return self.blob_bytes * n + self.slice_bytes
 
     def close(self):
         for p in self._allocs:
@@ -384,15 +421,18 @@ class MoELayer:
                  world_size: int = 1, rank: int = 0, packet_bytes: int = 0,
                  profile: bool = False, nccl_unique_id: Optional[bytes] = None,
                  force_ep: bool = False, num_slots: int = 0, local_ep: bool = False,
-                 ipc_ep: bool = False, mover: bool = False):
+                 ipc_ep: bool = False, mover: bool = False, shard_shared: bool = False):
         """local_ep: in-process expert parallelism over peer memory (MOE_FLAG_LOCAL_EP);
         nccl_unique_id is then the 128-byte group key shared by the `world_size` contexts (one
         host thread each).  ipc_ep: the same transport across processes (MOE_FLAG_IPC_EP): call
         ipc_connect(all ranks' ipc_handle()) before the first forward.  mover: expert copies in
-        packets through the library's data-mover thread (MOE_FLAG_MOVER)."""
+        packets through the library's data-mover thread (MOE_FLAG_MOVER).  shard_shared: the
+        shared experts sharded by intermediate columns across the EP group
+        (MOE_FLAG_SHARD_SHARED; pass HostExperts(..., slice_=shared_slice_weights(...)))."""
         flags = ((MOE_FLAG_PROFILE if profile else 0) | (MOE_FLAG_FORCE_EP if force_ep else 0) |
                  (MOE_FLAG_LOCAL_EP if local_ep else 0) | (MOE_FLAG_IPC_EP if ipc_ep else 0) |
-                 (MOE_FLAG_MOVER if mover else 0))
+                 (MOE_FLAG_MOVER if mover else 0) |
+                 (MOE_FLAG_SHARD_SHARED if shard_shared else 0))
         self.cfg = moe_config(hidden, ffn, num_experts, top_k, num_shared, max_tokens,
                               int(renormalize), device, world_size, rank, None, packet_bytes,
                               flags, num_slots)

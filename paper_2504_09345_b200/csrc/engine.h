@@ -56,7 +56,18 @@ struct Mover;   // mover.cu: the Contiguous Data Mover thread (MOE_FLAG_MOVER)
 struct moe_ctx_s {
     moe_config cfg{};
     int n_local = 0;       // routed experts owned by this rank
-    int n_all = 0;         // n_local + num_shared (items streamed per call)
+    int n_all = 0;         // n_local + s_items (items streamed per call)
+    int s_items = 0;       // shared items streamed per call: num_shared, or 0/1 (sharded)
+    // MOE_FLAG_SHARD_SHARED: this rank streams one slice of the concatenated
+    // shared FFN, shard_w columns wide (0 = none), run over every rank's tokens.  Its W2 part
+    // ([h, shard_w]) is read through tm_w2s*, a view of the staging buffer with shard_w columns
+    // per row (slot s = rows [s * slice_slot_rows, ...)).
+    bool shard = false;
+    int shard_w = 0;
+    uint32_t shard_mask = 0;          // ranks whose slice is not empty
+    int64_t slice_bytes = 0;
+    int64_t slice_slot_rows = 0;
+    CUtensorMap tm_w2s, tm_w2s_pair;
     int64_t blob_bytes = 0, w13_bytes = 0;
     int num_sms = 148;
     int bn1 = 256, bn2 = 256;
@@ -89,6 +100,7 @@ struct moe_ctx_s {
     int pend_n = 0;                     // items in the pending batch
     uint64_t pend_q0 = 0;               // streamed-item index of the batch's first item
     const char* pend_src = nullptr;     // host address of the batch's first blob
+    int64_t pend_item = 0, pend_w13 = 0; // bytes per item of the batch / of its W13 part
     uintptr_t pend_base = 0;            // start of that blob's pinned allocation
     cudaEvent_t ready13[moe::kMaxSlots] = {}, ready2[moe::kMaxSlots] = {};
     cudaEvent_t slot_free[moe::kMaxSlots] = {};
@@ -266,7 +278,8 @@ double mover_take_h2d_ms(moe_ctx c, int64_t* packets);
 // Layer shape a rank publishes in its IPC blob (after the 4 memory handles); connect checks that
 // every rank's matches its own.
 struct IpcShape {
-    int32_t magic, rank, world, hidden, ffn, num_experts, top_k, num_shared, max_tokens, pad;
+    int32_t magic, rank, world, hidden, ffn, num_experts, top_k, num_shared, max_tokens;
+    int32_t shard;   // MOE_FLAG_SHARD_SHARED bit: all ranks must agree
 };
 IpcShape ipc_shape(moe_ctx c);
 moe_status ep_init(moe_ctx c);

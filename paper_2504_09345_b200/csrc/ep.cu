@@ -109,13 +109,16 @@ moe_status ep_init(moe_ctx c) {
     ok &= cudaHostAlloc((void**)&c->counts_all_h, sizeof(int32_t) * (size_t)W * ne, 0) == cudaSuccess;
     ok &= cudaMalloc((void**)&c->ep_grp, sizeof(GemmGroup) * 2 * (size_t)c->n_all) == cudaSuccess;
     ok &= cudaHostAlloc((void**)&c->ep_grp_h, sizeof(GemmGroup) * 2 * (size_t)c->n_all, 0) == cudaSuccess;
-    ok &= cudaMalloc((void**)&c->x_recv, 2 * (size_t)c->cap_recv * cf.hidden) == cudaSuccess;
-    ok &= cudaMalloc((void**)&c->y_recv, 2 * (size_t)c->cap_recv * cf.hidden) == cudaSuccess;
+    // MOE_FLAG_SHARD_SHARED: W * max_tokens more rows for every rank's tokens (x_recv) and the
+    // shared slice's partial outputs for them (y_recv), both read / written by peers
+    const int64_t rows = c->cap_recv + (c->shard ? (int64_t)W * cf.max_tokens : 0);
+    ok &= cudaMalloc((void**)&c->x_recv, 2 * (size_t)rows * cf.hidden) == cudaSuccess;
+    ok &= cudaMalloc((void**)&c->y_recv, 2 * (size_t)rows * cf.hidden) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
         return set_err(c, MOE_E_NOMEM, "EP buffers");
     }
-    if (!make_tmap(&c->tm_xrecv, c->x_recv, (uint64_t)c->cap_recv, cf.hidden, 128))
+    if (!make_tmap(&c->tm_xrecv, c->x_recv, (uint64_t)rows, cf.hidden, 128))
         return set_err(c, MOE_E_CUDA, "tensor map x_recv");
     const int np = W * c->n_local;
     c->send_off.assign(np, 0);
@@ -170,9 +173,10 @@ moe_status ep_init(moe_ctx c) {
             const moe_config& o = p->cfg;
             if (o.hidden != cf.hidden || o.ffn != cf.ffn || o.num_experts != cf.num_experts ||
                 o.top_k != cf.top_k || o.num_shared != cf.num_shared ||
-                o.max_tokens != cf.max_tokens)
+                o.max_tokens != cf.max_tokens ||
+                (o.flags & MOE_FLAG_SHARD_SHARED) != (cf.flags & MOE_FLAG_SHARD_SHARED))
                 return set_err(c, MOE_E_INVAL, "LOCAL_EP rank %d: layer shape / max_tokens differ "
-                               "from rank %d's", cf.rank, o.rank);
+                               "(or MOE_FLAG_SHARD_SHARED) from rank %d's", cf.rank, o.rank);
         }
         g->ranks[cf.rank] = c;
         c->local_group = g.get();
@@ -335,7 +339,8 @@ moe_status ep_combine(moe_ctx c, cudaStream_t st) {
 IpcShape ipc_shape(moe_ctx c) {
     const moe_config& cf = c->cfg;
     return IpcShape{0x4D6F4533, cf.rank, cf.world_size, cf.hidden, cf.ffn, cf.num_experts,
-                    cf.top_k, cf.num_shared, cf.max_tokens, 0};
+                    cf.top_k, cf.num_shared, cf.max_tokens,
+                    (int32_t)(cf.flags & MOE_FLAG_SHARD_SHARED)};
 }
 
 namespace {
@@ -355,6 +360,8 @@ moe_status p2p_upload(moe_ctx c, unsigned long long* const* flags, int32_t* cons
         py.rows[d] = yr[d];
     }
     px.nl = py.nl = c->n_local;
+    px.shard_row = py.shard_row = -1;   // set per call by the plan kernel when sharded
+    px.shard_mask = py.shard_mask = c->shard ? c->shard_mask : 0u;
     MOE_CUDA(c, cudaMemcpyAsync(c->p2p_tab, &tab, sizeof tab, cudaMemcpyHostToDevice, st));
     MOE_CUDA(c, cudaMemcpyAsync(c->pr_x, &px, sizeof px, cudaMemcpyHostToDevice, st));
     MOE_CUDA(c, cudaMemcpyAsync(c->pr_y, &py, sizeof py, cudaMemcpyHostToDevice, st));
@@ -452,7 +459,8 @@ moe_status p2p_before_dispatch(moe_ctx c, int T, cudaStream_t st) {
     P2P_TRY(p2p_wait(c, kFlagCounts, seq, st));
     MOE_CUDA(c, launch_p2p_plan(c->p2p_counts + (size_t)par * W * ne, W, ne, me, T, cf.top_k,
                                 cf.num_shared, c->cap_recv, c->n_all, cf.hidden, c->ep_grp,
-                                c->pr_x, c->pr_y, c->p2p_rows, c->p2p_bytes, c->p2p_diag_d, st));
+                                c->pr_x, c->pr_y, c->p2p_rows, c->p2p_bytes, c->p2p_diag_d,
+                                c->shard ? c->n_local : -1, st));
     P2P_TRY(p2p_wait(c, kFlagXFree, seq - 1, st));
     return MOE_OK;
 }
@@ -570,9 +578,10 @@ moe_status moe_ep_ipc_connect(moe_ctx c, const void* all) {
         want.rank = d;
         if (memcmp(&o, &want, sizeof o) != 0)
             return moe::set_err(c, MOE_E_INVAL, "IPC_EP: rank %d's blob (magic %x, rank %d, W %d, "
-                                "h %d, h_i %d, N_e %d, k %d, S %d, max_tokens %d) does not match "
-                                "this rank's layer", d, o.magic, o.rank, o.world, o.hidden, o.ffn,
-                                o.num_experts, o.top_k, o.num_shared, o.max_tokens);
+                                "h %d, h_i %d, N_e %d, k %d, S %d, max_tokens %d, shard %d) does "
+                                "not match this rank's layer", d, o.magic, o.rank, o.world,
+                                o.hidden, o.ffn, o.num_experts, o.top_k, o.num_shared,
+                                o.max_tokens, o.shard);
     }
     unsigned long long* flags[moe::kMaxRanks];
     int32_t* counts[moe::kMaxRanks];

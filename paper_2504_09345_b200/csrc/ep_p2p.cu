@@ -80,7 +80,7 @@ __global__ void p2p_plan_kernel(const int32_t* __restrict__ counts, int W, int n
                                 GemmGroup* __restrict__ grp, PeerRows* __restrict__ pr_x,
                                 PeerRows* __restrict__ pr_y, int32_t* __restrict__ rows_out,
                                 long long* __restrict__ bytes_acc,
-                                long long* __restrict__ diag) {
+                                long long* __restrict__ diag, int shard_item) {
     const int nl = ne / W;
     // Every owner must be able to hold the rows routed to it: each rank checks every owner's
     // total (the counts are the same on every rank, so all ranks agree).  With consistent
@@ -127,14 +127,36 @@ __global__ void p2p_plan_kernel(const int32_t* __restrict__ counts, int W, int n
             off += cnt;
         }
         *rows_out = off;
-        for (int s = 0; s < S; ++s) {   // shared experts: the local tokens
-            const int hb = (int)(cap_recv + (long long)s * T);
-            grp[nl + s] = GemmGroup{0, T, hb, 0};
-            grp[n_all + nl + s] = GemmGroup{hb, hb + T, T * k + s * T, 0};
+        long long shard_rows = 0;
+        if (shard_item >= 0) {
+            // MOE_FLAG_SHARD_SHARED: rank q's tokens sit at rows cap_recv + P_q of every slice
+            // owner's x_recv / y_recv (P_q = sum of the earlier ranks' T; T_q = its routed rows
+            // / k, read from the counts every rank already has)
+            long long P = 0, tot = 0;
+            for (int q = 0; q < W; ++q) {
+                long long rq = 0;
+                for (int e = 0; e < ne; ++e) rq += counts[(size_t)q * ne + e];
+                if (q < me) P += rq / k;
+                tot += rq / k;
+            }
+            pr_x->shard_row = pr_y->shard_row = (int32_t)(cap_recv + P);
+            if ((pr_x->shard_mask >> me) & 1u) {   // this rank's slice over all W ranks' tokens
+                const int hb = (int)cap_recv;
+                grp[shard_item] = GemmGroup{hb, (int)(hb + tot), hb, 0};
+                grp[n_all + shard_item] = GemmGroup{hb, (int)(hb + tot), hb, 0};
+            }
+            shard_rows = (long long)__popc(pr_x->shard_mask) * T;
+        } else {
+            for (int s = 0; s < S; ++s) {   // shared experts (replicated): the local tokens
+                const int hb = (int)(cap_recv + (long long)s * T);
+                grp[nl + s] = GemmGroup{0, T, hb, 0};
+                grp[n_all + nl + s] = GemmGroup{hb, hb + T, T * k + s * T, 0};
+            }
         }
         long long sent = 0;
         for (int e = 0; e < ne; ++e) sent += counts[(size_t)me * ne + e];
-        if (!overflow) *bytes_acc += 2 * sent * h * 2;   // rows written to the owners + read back in the combine
+        // rows written to the owners + read back in the combine (and the shared gather / sum)
+        if (!overflow) *bytes_acc += 2 * (sent + shard_rows) * h * 2;
     }
 }
 
@@ -206,9 +228,10 @@ cudaError_t launch_p2p_wait(const unsigned long long* flags, int W, int which,
 cudaError_t launch_p2p_plan(const int32_t* counts_par, int W, int ne, int me, int T, int k,
                             int S, long long cap_recv, int n_all, int h, GemmGroup* grp,
                             PeerRows* pr_x, PeerRows* pr_y, int32_t* rows_out,
-                            long long* bytes_acc, long long* diag, cudaStream_t st) {
+                            long long* bytes_acc, long long* diag, int shard_item,
+                            cudaStream_t st) {
     p2p_plan_kernel<<<1, 128, 0, st>>>(counts_par, W, ne, me, T, k, S, cap_recv, n_all, h, grp,
-                                       pr_x, pr_y, rows_out, bytes_acc, diag);
+                                       pr_x, pr_y, rows_out, bytes_acc, diag, shard_item);
     return cudaGetLastError();
 }
 

@@ -90,6 +90,15 @@ namespace {
 
 using moe::set_err;
 
+// MOE_FLAG_SHARD_SHARED: rank r's columns of the concatenated shared FFN (include/moe.h,
+// moe_shared_slice): blocks [floor(r B / W), floor((r+1) B / W)) of B = S h_i / 128.
+void shared_slice_cols(int ffn, int S, int W, int r, int* col0, int* width) {
+    const int64_t B = (int64_t)S * ffn / 128;
+    const int64_t b0 = B * r / W, b1 = B * (r + 1) / W;
+    *col0 = (int)(b0 * 128);
+    *width = (int)((b1 - b0) * 128);
+}
+
 moe_status check_cfg(const moe_config* cfg) {
     if (!cfg) return MOE_E_INVAL;
     if (cfg->hidden <= 0 || cfg->ffn <= 0 || cfg->num_experts <= 0 || cfg->top_k <= 0 ||
@@ -105,10 +114,24 @@ moe_status check_cfg(const moe_config* cfg) {
         return MOE_E_INVAL;
     if (cfg->num_slots < 0 || cfg->num_slots == 1 || cfg->num_slots > moe::kMaxSlots)
         return MOE_E_INVAL;
-    if (cfg->num_slots > 2 && cfg->num_slots >= cfg->num_experts / cfg->world_size + cfg->num_shared)
+    int s_items = cfg->num_shared;
+    if (cfg->flags & MOE_FLAG_SHARD_SHARED) {
+        // P2P transport only (the gather / partial sums ride the peer-memory permute / combine);
+        // a slice must fit one expert slot (S <= W) and the slot must hold whole rows of the
+        // slice's W2 view (tm_w2s); the mover's packets assume one blob size
+        if (cfg->world_size < 2 || !(cfg->flags & (MOE_FLAG_LOCAL_EP | MOE_FLAG_IPC_EP)) ||
+            cfg->num_shared < 1 || cfg->num_shared > cfg->world_size ||
+            (cfg->flags & MOE_FLAG_MOVER))
+            return MOE_E_UNSUPPORTED;
+        int c0 = 0, w = 0;
+        shared_slice_cols(cfg->ffn, cfg->num_shared, cfg->world_size, cfg->rank, &c0, &w);
+        if (w > 0 && (3ll * cfg->hidden * cfg->ffn) % w) return MOE_E_UNSUPPORTED;
+        s_items = w > 0 ? 1 : 0;
+    }
+    if (cfg->num_slots > 2 && cfg->num_slots >= cfg->num_experts / cfg->world_size + s_items)
         return MOE_E_INVAL;  // more slots than streamed experts would let weights stay resident
     const int64_t rows = (int64_t)cfg->max_tokens * cfg->world_size * cfg->top_k +
-                         (int64_t)cfg->max_tokens * cfg->num_shared;
+                         (int64_t)cfg->max_tokens * std::max(cfg->num_shared, cfg->world_size);
     if (rows >= (1ll << 31)) return MOE_E_UNSUPPORTED;
     return MOE_OK;
 }
@@ -168,6 +191,7 @@ moe_status flush_copies(moe_ctx c) {
     if (c->pend_n == 0) return MOE_OK;
     const int n = c->pend_n;
     const int s0 = (int)(c->pend_q0 % (uint64_t)c->nslots);
+    const int64_t ib = c->pend_item, i13 = c->pend_w13;   // bytes per item / its W13 part
     if (c->mover) {   // the mover thread packetises and orders it by device counters
         for (int j = 0; j < n; ++j) {
             c->batch_q0[s0 + j] = c->pend_q0;
@@ -197,7 +221,7 @@ moe_status flush_copies(moe_ctx c) {
         // microseconds of idle link (measured: separate W13/W2 copies lost ~0.4% of the C1 step,
         // 17 MB per-expert copies ran at 54.0 of 55.6 GB/s).  GEMM1 then starts after the
         // batch landed -- still long before the next batch's copy ends.
-        moe_status st = copy_range(0, (int64_t)n * c->blob_bytes);
+        moe_status st = copy_range(0, (int64_t)n * ib);
         if (st != MOE_OK) return st;
         for (int j = 0; j < n; ++j) {
             MOE_CUDA(c, cudaEventRecord(c->ready13[s0 + j], c->copy_stream));
@@ -205,11 +229,11 @@ moe_status flush_copies(moe_ctx c) {
         }
     } else {  // packetised: W13 first so GEMM1 can start early
         for (int j = 0; j < n; ++j) {
-            const int64_t b = (int64_t)j * c->blob_bytes;
-            moe_status st = copy_range(b, b + c->w13_bytes);
+            const int64_t b = (int64_t)j * ib;
+            moe_status st = copy_range(b, b + i13);
             if (st != MOE_OK) return st;
             MOE_CUDA(c, cudaEventRecord(c->ready13[s0 + j], c->copy_stream));
-            st = copy_range(b + c->w13_bytes, b + c->blob_bytes);
+            st = copy_range(b + i13, b + ib);
             if (st != MOE_OK) return st;
             MOE_CUDA(c, cudaEventRecord(c->ready2[s0 + j], c->copy_stream));
         }
@@ -219,7 +243,7 @@ moe_status flush_copies(moe_ctx c) {
         c->batch_q0[s0 + j] = c->pend_q0;
         c->batch_n[s0 + j] = n;
     }
-    c->stats.h2d_weight_bytes += (int64_t)n * c->blob_bytes;
+    c->stats.h2d_weight_bytes += (int64_t)n * ib;
     c->pend_n = 0;
     return MOE_OK;
 }
@@ -232,9 +256,13 @@ moe_status flush_copies(moe_ctx c) {
 moe_status request_copy(moe_ctx c, const void* const* experts, int i, uint64_t q) {
     const char* src = static_cast<const char*>(experts[i]);
     const int s = (int)(q % (uint64_t)c->nslots);
+    // the shared slice (MOE_FLAG_SHARD_SHARED) is smaller than an expert: a batch of its own
+    const bool slice = c->shard && i >= c->n_local;
+    const int64_t ib = slice ? c->slice_bytes : c->blob_bytes;
     if (c->pend_n > 0) {
         const uintptr_t a0 = c->pend_base, a1 = c->call_base[i];
-        const bool contiguous = src == c->pend_src + (int64_t)c->pend_n * c->blob_bytes &&
+        const bool contiguous = !slice && c->pend_item == ib &&
+                                src == c->pend_src + (int64_t)c->pend_n * c->blob_bytes &&
                                 q == c->pend_q0 + (uint64_t)c->pend_n && s != 0 && a0 != 0 &&
                                 a0 == a1;
         if (!contiguous || c->pend_n >= c->copy_group) {
@@ -246,9 +274,11 @@ moe_status request_copy(moe_ctx c, const void* const* experts, int i, uint64_t q
         c->pend_q0 = q;
         c->pend_src = src;
         c->pend_base = c->call_base[i];
+        c->pend_item = ib;
+        c->pend_w13 = slice ? 4ll * c->cfg.hidden * c->shard_w : c->w13_bytes;
     }
     ++c->pend_n;
-    if (c->pend_n >= c->copy_group) return flush_copies(c);
+    if (c->pend_n >= c->copy_group || slice) return flush_copies(c);
     return MOE_OK;
 }
 
@@ -324,14 +354,15 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     // (T == 0 only happens under EP: the rank serves other ranks' tokens; its shared-expert
     // groups are then empty and never touch the map.)
     CUtensorMap tm_x = c->tm_xperm;
-    if (S > 0 && T > 0 && !moe::make_tmap(&tm_x, hidden, (uint64_t)T, (uint64_t)h, 128))
+    const int Si = c->s_items;   // shared items streamed (S, or this rank's slice: 0 / 1)
+    if (S > 0 && !c->shard && T > 0 && !moe::make_tmap(&tm_x, hidden, (uint64_t)T, (uint64_t)h, 128))
         return set_err(c, MOE_E_CUDA, "cuTensorMapEncodeTiled failed for hidden");
 
     // Streaming order: shared experts first (their GEMMs need only the hidden batch, and they are
     // the longest GEMMs -- T rows each -- so they must not sit at the end of a call where they
     // would hold slots the next call's first copies wait on), then the routed experts.
     // expert_of(i) is the index into `experts` / the group tables of streamed item i.
-    auto expert_of = [&](int i) { return i < S ? c->n_local + i : i - S; };
+    auto expert_of = [&](int i) { return i < Si ? c->n_local + i : i - Si; };
     // the first nslots weight copies go ahead of routing (cross-call prefetch)
     const int ns = c->nslots;
     for (int i = 0; i < std::min(ns, c->n_all); ++i) {
@@ -367,7 +398,10 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     for (int i = i0; i < i1;) {
         const uint64_t q = q0 + i;
         const bool shared = expert_of(i) >= c->n_local;
-        const int left = (shared ? S : c->n_all) - i;   // items of this class (shared / routed)
+        // the rank's shared-FFN slice (MOE_FLAG_SHARD_SHARED): every rank's tokens gathered in
+        // x_recv from row cap_recv, shard_w columns, partial rows into y_recv (peers read them)
+        const bool slice = shared && c->shard;
+        const int left = (shared ? Si : c->n_all) - i;   // items of this class (shared / routed)
         // the launch takes item q's whole DMA batch, or gemm_items routed items if more
         int want = std::min(left, shared ? 1 : gemm_items);
         if (c->pend_n > 0 && c->pend_q0 < q + (uint64_t)want) {  // a batch still pending: issue it
@@ -398,14 +432,16 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
             if (!c->mover) MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready13[sj], 0));
             b1.idx[j] = b2.idx[j] = e;
             b1.b_row[j] = 3 * hi * sj;           // W13 of slot sj in tm_w13*
-            b2.b_row[j] = 3 * h * sj + 2 * h;    // W2 of slot sj in tm_w2*
-            rows[j] = shared ? (int64_t)T : exp_routed;
+            b2.b_row[j] = slice ? (int32_t)(c->slice_slot_rows * sj + 2 * h)   // in tm_w2s*
+                                : 3 * h * sj + 2 * h;    // W2 of slot sj in tm_w2*
+            rows[j] = slice ? (int64_t)T * cf.world_size : shared ? (int64_t)T : exp_routed;
         }
         {
             Prof p(c, moe::kRecGemm1, st);
             moe_status gs = launch_grouped(c, moe::kGemmSwiGLU, c->bn1, rows, !shared,
-                                           shared ? &tm_x : tmA_routed, &c->tm_w13,
-                                           &c->tm_w13_pair, b1, 2 * hi, h, c->h_act, hi, st);
+                                           slice ? &c->tm_xrecv : shared ? &tm_x : tmA_routed,
+                                           &c->tm_w13, &c->tm_w13_pair, b1,
+                                           2 * (slice ? c->shard_w : hi), h, c->h_act, hi, st);
             if (gs != MOE_OK) return gs;
             p.end();
         }
@@ -418,9 +454,12 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         }
         {
             Prof p(c, moe::kRecGemm2, st);
-            moe_status gs = launch_grouped(c, moe::kGemmPlain, c->bn2, rows, !shared, &c->tm_h, &c->tm_w2,
-                                           &c->tm_w2_pair, b2, h, hi,
-                                           shared ? c->y_perm : y_routed, h, st);
+            moe_status gs = launch_grouped(c, moe::kGemmPlain, c->bn2, rows, !shared, &c->tm_h,
+                                           slice ? &c->tm_w2s : &c->tm_w2,
+                                           slice ? &c->tm_w2s_pair : &c->tm_w2_pair, b2, h,
+                                           slice ? c->shard_w : hi,
+                                           slice ? c->y_recv : shared ? c->y_perm : y_routed, h,
+                                           st);
             if (gs != MOE_OK) return gs;
             p.end();
         }
@@ -448,12 +487,12 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
     // Shared experts first, BEFORE routing: they need only the hidden batch, so their GEMMs run
     // while the router works and their slots are free for the next copies early (the copy
     // engine never waits on the router).  Their group tables are written here (not by scan).
-    if (S > 0) {
+    if (Si > 0 && !c->shard) {
         const int hbase = (int)(c->ep ? c->cap_recv : (int64_t)T * k);
         MOE_CUDA(c, moe::launch_fill_shared_groups(c->shared_grp, c->n_local, c->n_all, S, T,
                                                    hbase, T * k, st));
         c->stats.kernel_launches += 1;
-        const moe_status ss = run_items(0, S, c->shared_grp, c->shared_grp + c->n_all);
+        const moe_status ss = run_items(0, Si, c->shared_grp, c->shared_grp + c->n_all);
         if (ss != MOE_OK) return ss;
     }
 
@@ -493,8 +532,12 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         g2 = c->ep_grp + c->n_all;
         y_routed = c->y_recv;
     }
+    if (c->shard && Si > 0) {   // the shared slice, once every rank's tokens have arrived
+        const moe_status ss = run_items(0, Si, g1, g2);
+        if (ss != MOE_OK) return ss;
+    }
 
-    const moe_status rs = run_items(S, c->n_all, g1, g2);   // the routed experts
+    const moe_status rs = run_items(Si, c->n_all, g1, g2);   // the routed experts
     if (rs != MOE_OK) return rs;
     {
         moe_status fs = flush_copies(c);  // nothing may stay pending across calls
@@ -514,7 +557,7 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
                                             r1 - r0, h, k, S, (int64_t)T * k + r0, T,
                                             resid ? resid + (int64_t)r0 * h : nullptr,
                                             out + (int64_t)r0 * h, idx + (int64_t)r0 * k, c->offsets,
-                                            c->p2p ? c->pr_y : nullptr, st));
+                                            c->p2p ? c->pr_y : nullptr, c->shard ? r0 : -1, st));
             c->stats.kernel_launches += 1;
             return MOE_OK;
         };
@@ -805,6 +848,18 @@ int64_t moe_packed_expert_bytes(int32_t hidden, int32_t ffn) {
     return 6ll * hidden * ffn;
 }
 
+moe_status moe_shared_slice(int32_t ffn, int32_t num_shared, int32_t world, int32_t rank,
+                            int32_t* col0, int32_t* width) {
+    if (!col0 || !width || ffn <= 0 || ffn % 128 || num_shared < 1 || world < 1 || rank < 0 ||
+        rank >= world)
+        return MOE_E_INVAL;
+    int c0 = 0, w = 0;
+    shared_slice_cols(ffn, num_shared, world, rank, &c0, &w);
+    *col0 = c0;
+    *width = w;
+    return MOE_OK;
+}
+
 moe_status moe_pack_expert(int32_t hidden, int32_t ffn, const void* w1, const void* w3,
                            const void* w2, void* dst) {
     if (!w1 || !w3 || !w2 || !dst || hidden <= 0 || ffn <= 0) return MOE_E_INVAL;
@@ -865,7 +920,21 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     c->p2p = c->local_ep || (cfg->flags & MOE_FLAG_IPC_EP) != 0;
     if (W > moe::kMaxRanks && c->p2p) return fail(MOE_E_UNSUPPORTED);
     c->n_local = ne / W;
-    c->n_all = c->n_local + S;
+    c->shard = (cfg->flags & MOE_FLAG_SHARD_SHARED) != 0;   // check_cfg: P2P, W > 1, S <= W
+    c->s_items = S;
+    if (c->shard) {
+        int c0 = 0;
+        for (int r = 0; r < W; ++r) {
+            int w = 0;
+            shared_slice_cols(hi, S, W, r, &c0, &w);
+            if (w > 0) c->shard_mask |= 1u << r;
+            if (r == cfg->rank) c->shard_w = w;
+        }
+        c->s_items = c->shard_w > 0 ? 1 : 0;
+        c->slice_bytes = c->shard_w > 0 ? moe_packed_expert_bytes(h, c->shard_w) : 0;
+        c->slice_slot_rows = c->shard_w > 0 ? 3ll * h * hi / c->shard_w : 0;
+    }
+    c->n_all = c->n_local + c->s_items;
     c->w13_bytes = 4ll * h * hi;
     c->blob_bytes = moe_packed_expert_bytes(h, hi);
     c->bn1 = moe::gemm_bn_for(moe::kGemmSwiGLU, 2 * hi);
@@ -891,8 +960,9 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     if (const char* e = getenv("MOE_COPY_GROUP")) c->copy_group = std::max(1, std::min(atoi(e), c->nslots));
     c->gemm_group_max = std::min(c->nslots / 2, moe::kMaxBatch);
     c->cap_recv = c->ep ? (int64_t)W * Tm * k : (int64_t)Tm * k;
-    // h_act rows: routed rows (received rows under EP) then S * Tm shared rows
-    const int64_t h_rows = c->cap_recv + (int64_t)S * Tm;
+    // h_act rows: routed rows (received rows under EP) then S * Tm shared rows (sharded: the
+    // slice's rows for all W ranks' tokens, W * Tm)
+    const int64_t h_rows = c->cap_recv + (int64_t)(c->shard ? W : S) * Tm;
     c->rows_cap = (int64_t)Tm * (k + S);  // y_perm rows
     const int n_tiles = (Tm + moe::kRouteTile - 1) / moe::kRouteTile;
 
@@ -958,6 +1028,11 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
         tm &= moe::make_tmap(&c->tm_w13_pair, c->slot_base, r13, h, 128);
         tm &= moe::make_tmap(&c->tm_w2, c->slot_base, r2, hi, (uint32_t)c->bn2);
         tm &= moe::make_tmap(&c->tm_w2_pair, c->slot_base, r2, hi, 128);
+        if (c->shard_w > 0) {   // the slice's W2 [h, shard_w] at row 2h of its slot
+            const uint64_t rs = (uint64_t)c->slice_slot_rows * c->nslots;
+            tm &= moe::make_tmap(&c->tm_w2s, c->slot_base, rs, c->shard_w, (uint32_t)c->bn2);
+            tm &= moe::make_tmap(&c->tm_w2s_pair, c->slot_base, rs, c->shard_w, 128);
+        }
     }
     if (!tm) return fail(MOE_E_CUDA);
     if (const char* e = getenv("MOE_GEMM_PAIR")) {   // tests: force one kernel

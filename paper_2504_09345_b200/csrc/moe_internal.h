@@ -46,10 +46,16 @@ constexpr int kMaxRanks = 8;         // EP group size (one B200 box)
 // every call): routed row (t, j) of expert e lives in rank e / nl's buffer at row
 // base[e] + (pos[t, j] - offsets[e]) -- base[e] is where this rank's block for expert e starts
 // in the owner's expert-major layout (moe_ep_plan's recv_off).
+// MOE_FLAG_SHARD_SHARED: every rank in shard_mask also holds a shared-FFN slice; the rows from
+// cap_recv on of its x_recv / y_recv hold all ranks' tokens (rank-major, rank q's T_q tokens
+// from row cap_recv + P_q, P_q = sum_{q'<q} T_q') and the slice's partial outputs for them.
+// shard_row = cap_recv + P_me of THIS rank (written by the plan kernel every call), -1 = off.
 struct PeerRows {
     __nv_bfloat16* rows[kMaxRanks];
     int32_t base[kMaxExperts];
     int32_t nl;
+    int32_t shard_row;
+    uint32_t shard_mask;
 };
 
 // Per-call synchronisation of the P2P transport: each rank owns flags[kP2PFlags][kMaxRanks]
@@ -85,16 +91,24 @@ cudaError_t launch_p2p_selftest(const P2PTable* tab, const PeerRows* pr_x,
 // (where this rank's rows for expert e start in the owner's buffers), rows received (rows_out)
 // and bytes sent (+= bytes_acc).  If some owner would receive more than cap_recv rows, nothing
 // is dispatched (bases -1, empty groups) and diag[5..7] = {1, rows, cap_recv} (host-mapped).
+// shard_item >= 0 (MOE_FLAG_SHARD_SHARED): group entry of this rank's shared slice, run over
+// every rank's tokens (x_recv rows cap_recv + [0, sum_q T_q)), and pr_x / pr_y->shard_row set;
+// -1 = shared experts replicated (groups over the local tokens) or none.
 cudaError_t launch_p2p_plan(const int32_t* counts_par, int W, int ne, int me, int T, int k,
                             int S, long long cap_recv, int n_all, int h, GemmGroup* grp,
                             PeerRows* pr_x, PeerRows* pr_y, int32_t* rows_out,
-                            long long* bytes_acc, long long* diag, cudaStream_t st);
+                            long long* bytes_acc, long long* diag, int shard_item,
+                            cudaStream_t st);
 
 // ---------------------------------------------------------------------------- routing kernels
 // a2+a3: router GEMM (fp64, ascending c) + warp-shuffle top-k + softmax gates + per-tile counts.
 cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_bfloat16* wr,
                                int ne, int k, int renorm, int32_t* idx, float* gates,
                                int32_t* tile_counts, cudaStream_t st);
+// Round 1's router kernel (comparison only: tools/router_bench.cu, MOE_ROUTER=3).
+cudaError_t launch_router_v3(const __nv_bfloat16* x, int T, int h, const __nv_bfloat16* wr,
+                             int ne, int k, int renorm, int32_t* idx, float* gates,
+                             int32_t* tile_counts, cudaStream_t st);
 // a4 (scan): tile prefix per expert, expert offsets, per-expert counts and GEMM group tables.
 //   expert_lo..expert_lo+n_local-1 are the experts whose groups are built (all of them at W=1).
 cudaError_t launch_scan(const int32_t* tile_counts, int n_tiles, int ne, int T, int k,
@@ -112,12 +126,14 @@ cudaError_t launch_permute(const __nv_bfloat16* x, int T, int h, int k, int ne,
 //     NULL) (fp32, fixed order) -> bf16, for the T rows starting at the given pointers (a row
 //     range of a call: R = shared_base is then offset by the range's first row, stride = the
 //     call's T).  pr != NULL (P2P expert parallelism): routed rows are read from their owners'
-//     y_recv (PeerRows; needs idx and offsets), shared rows from y_perm.
+//     y_recv (PeerRows; needs idx and offsets), shared rows from y_perm.  shard_t0 >= 0
+//     (MOE_FLAG_SHARD_SHARED; num_shared is then ignored): the shared part is the sum, in rank
+//     order over pr->shard_mask, of row pr->shard_row + shard_t0 + t of every owner's y_recv.
 cudaError_t launch_combine(const __nv_bfloat16* y_perm, const int32_t* pos, const float* gates,
                            int T, int h, int k, int num_shared, int64_t shared_base,
                            int64_t shared_stride, const __nv_bfloat16* resid, __nv_bfloat16* out,
                            const int32_t* idx, const int32_t* offsets, const PeerRows* pr,
-                           cudaStream_t st);
+                           int shard_t0, cudaStream_t st);
 // Task B (b2): u[t] = RMSNorm(h1[t]) * gamma, reading R21:
 //   r = 1 / sqrt(sum_c h1[t,c]^2 / h + eps)  (fp64),  n = bf16(float(h1 * r)),
 //   u = bf16(float(gamma) * float(n))  (fp32 multiply).

@@ -412,6 +412,153 @@ router_v5_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
     }
 }
 
+// Router v6: the same one-FMA-chain-per-logit arithmetic (reading R6); every operand is widened
+// to fp64 ONCE per block, when its chunk is staged, so the inner loop is shared-memory loads and
+// DFMAs only (v5 re-widened each token's x in every warp: ~12 instructions per channel per warp,
+// ncu at C1: issue-bound at 28% slot use with 4 warps per SM).
+//   * a block = TPT x 32 tokens and NW warps; warp w owns experts [w*EPT, (w+1)*EPT) (zero rows
+//     pad N_e to NW*EPT), lane l owns tokens l, l+32, ...: TPT*EPT independent chains per lane;
+//   * channels are consumed in chunks of CW: x as [channel pair][token] double2 (one 16-byte
+//     read gives a lane two channels of one token, conflict-free), the router rows as
+//     [channel][expert] fp64 (double2 broadcasts), both double-buffered; the next chunk is
+//     loaded from global memory into registers during the current chunk's DFMAs and widened into
+//     the other buffer after them -- one __syncthreads per chunk;
+//   * per channel pair and warp: TPT x-reads (4 wavefronts each) + EPT double2 broadcasts for
+//     2*TPT*EPT DFMAs.
+// Channels per chunk: the largest power of two <= 128 whose double-buffered fp64 x + router
+// tiles (16 B per channel per token / expert) fit 96 KB -- two blocks per SM.
+constexpr int router_v6_cw(int rows) {
+    int cw = 128;
+    while (cw > 8 && 16 * cw * rows > 96 * 1024) cw >>= 1;
+    return cw;
+}
+
+template <int EPT, int TPT, int NW, int CW>
+__global__ void __launch_bounds__(NW * 32, 16 / NW)
+router_v6_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
+                 const __nv_bfloat16* __restrict__ wr, int ne, int k, int renorm,
+                 int32_t* __restrict__ idx_out, float* __restrict__ gate_out,
+                 int32_t* __restrict__ tile_counts) {
+    static_assert(EPT % 2 == 0 && CW % 8 == 0, "shape");
+    constexpr int kTok = kRouteTile * TPT;
+    constexpr int kThr = NW * 32;
+    constexpr int kNePad = NW * EPT;
+    constexpr int kNXV = kTok * (CW / 8);              // 16-byte x vectors per chunk
+    constexpr int kNWV = kNePad * (CW / 8);            // 16-byte router vectors per chunk
+    constexpr int kXV = (kNXV + kThr - 1) / kThr;
+    constexpr int kWV = (kNWV + kThr - 1) / kThr;
+    extern __shared__ __align__(16) double dyn[];
+    __shared__ int cnt[TPT][kMaxExperts];
+    double2* xs = reinterpret_cast<double2*>(dyn);                 // [2][CW/2][kTok]
+    double* ws = dyn + 2 * CW * kTok;                              // [2][CW][kNePad]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int t0 = blockIdx.x * kTok;
+    for (int e = tid; e < TPT * kMaxExperts; e += kThr) cnt[e / kMaxExperts][e % kMaxExperts] = 0;
+
+    // staging: consecutive threads take consecutive TOKENS (x) / EXPERTS (router) at one 8-channel
+    // group, so the widened stores hit consecutive shared-memory words
+    int4 xr[kXV], wv[kWV];
+    auto load = [&](int c0) {
+#pragma unroll
+        for (int j = 0; j < kXV; ++j) {
+            const int v = tid + j * kThr;
+            if (v < kNXV) {
+                const int t = v % kTok, cc = (v / kTok) * 8;
+                xr[j] = (t0 + t < T) ? ptx::ld_nc_v4(x + (size_t)(t0 + t) * h + c0 + cc)
+                                     : make_int4(0, 0, 0, 0);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kWV; ++j) {
+            const int v = tid + j * kThr;
+            if (v < kNWV) {
+                const int e = v % kNePad, cc = (v / kNePad) * 8;
+                wv[j] = (e < ne) ? ptx::ld_nc_v4(wr + (size_t)e * h + c0 + cc)
+                                 : make_int4(0, 0, 0, 0);
+            }
+        }
+    };
+    auto store = [&](int b) {
+        double2* xb = xs + (size_t)b * (CW / 2) * kTok;
+        double* wb = ws + (size_t)b * CW * kNePad;
+        double d[8];
+#pragma unroll
+        for (int j = 0; j < kXV; ++j) {
+            const int v = tid + j * kThr;
+            if (v < kNXV) {
+                const int t = v % kTok, c2 = (v / kTok) * 4;
+                bf16x8_to_f64(xr[j], d);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) xb[(c2 + q) * kTok + t] = make_double2(d[2 * q], d[2 * q + 1]);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kWV; ++j) {
+            const int v = tid + j * kThr;
+            if (v < kNWV) {
+                const int e = v % kNePad, cc = (v / kNePad) * 8;
+                bf16x8_to_f64(wv[j], d);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) wb[(cc + q) * kNePad + e] = d[q];
+            }
+        }
+    };
+
+    load(0);
+    store(0);
+    __syncthreads();
+    double acc[TPT][EPT];
+#pragma unroll
+    for (int p = 0; p < TPT; ++p)
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) acc[p][i] = 0.0;
+    const int n_chunks = h / CW;
+    for (int ch = 0; ch < n_chunks; ++ch) {
+        const int b = ch & 1;
+        const bool more = ch + 1 < n_chunks;
+        if (more) load((ch + 1) * CW);   // in flight during this chunk's DFMAs
+        const double2* xb = xs + (size_t)b * (CW / 2) * kTok + lane;
+        const double* wb = ws + (size_t)b * CW * kNePad + warp * EPT;
+#pragma unroll
+        for (int c2 = 0; c2 < CW / 2; ++c2) {
+            double2 xv[TPT];
+#pragma unroll
+            for (int p = 0; p < TPT; ++p) xv[p] = xb[c2 * kTok + p * 32];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {   // channel 2*c2 + q: ascending order in every chain
+                const double2* w2 = reinterpret_cast<const double2*>(wb + (2 * c2 + q) * kNePad);
+#pragma unroll
+                for (int i = 0; i < EPT / 2; ++i) {
+                    const double2 w = w2[i];
+#pragma unroll
+                    for (int p = 0; p < TPT; ++p) {
+                        const double xq = q ? xv[p].y : xv[p].x;
+                        acc[p][2 * i] = fma(xq, w.x, acc[p][2 * i]);
+                        acc[p][2 * i + 1] = fma(xq, w.y, acc[p][2 * i + 1]);
+                    }
+                }
+            }
+        }
+        if (more) store(b ^ 1);   // chunk b ^ 1 was consumed before the previous barrier
+        __syncthreads();
+    }
+    double* lg = dyn;   // [kTok][kNePad] logits (the x buffers, all reads done)
+#pragma unroll
+    for (int p = 0; p < TPT; ++p)
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) lg[(p * 32 + lane) * kNePad + warp * EPT + i] = acc[p][i];
+    __syncthreads();
+    topk_tile<TPT>(lg, kNePad, t0, T, ne, k, renorm, idx_out, gate_out, cnt, warp, NW, lane);
+    __syncthreads();
+    const int n_tiles = (T + kRouteTile - 1) / kRouteTile;
+#pragma unroll
+    for (int p = 0; p < TPT; ++p) {
+        const int tile = blockIdx.x * TPT + p;
+        if (tile < n_tiles)
+            for (int e = tid; e < ne; e += kThr) tile_counts[(size_t)tile * ne + e] = cnt[p][e];
+    }
+}
+
 // Single block of 1024 threads.  Warp w scans experts w, w+32, ... over the tiles.
 __global__ void __launch_bounds__(1024)
 scan_kernel(const int32_t* __restrict__ tile_counts, int n_tiles, int ne, int T, int k,
@@ -508,6 +655,8 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int h, int k, int ne,
                 }
             }
         }
+        // MOE_FLAG_SHARD_SHARED: the row also goes to every shared-slice owner (the gather)
+        const uint32_t smask = (pr && pr->shard_row >= 0) ? pr->shard_mask : 0u;
         constexpr int U = 4;
         for (int v0 = lane; v0 < nvec; v0 += 32 * U) {
             int4 buf[U];
@@ -525,6 +674,15 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int h, int k, int ne,
                     if (v < nvec) dst[v] = buf[u];
                 }
             }
+            for (uint32_t m = smask; m; m &= m - 1) {
+                const int d = __ffs(m) - 1;
+                int4* dst = reinterpret_cast<int4*>(pr->rows[d] + (size_t)(pr->shard_row + t) * h);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int v = v0 + 32 * u;
+                    if (v < nvec) dst[v] = buf[u];
+                }
+            }
         }
     }
     if (pr) __threadfence_system();   // peer stores performed before the dispatch flag release
@@ -536,7 +694,8 @@ combine_kernel(const __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ 
                const float* __restrict__ gates, int T, int h, int k, int num_shared,
                int64_t shared_base, int64_t shared_stride, const __nv_bfloat16* __restrict__ resid,
                __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ idx,
-               const int32_t* __restrict__ offsets, const PeerRows* __restrict__ pr) {
+               const int32_t* __restrict__ offsets, const PeerRows* __restrict__ pr,
+               int shard_t0) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int t = blockIdx.x * 8 + warp;
     if (t >= T) return;
@@ -578,7 +737,21 @@ combine_kernel(const __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ 
                 acc[2 * i + 1] = fmaf(g[j], f.y, acc[2 * i + 1]);
             }
         }
-        for (int s = 0; s < num_shared; ++s) {
+        if (shard_t0 >= 0) {   // sharded shared experts: the owners' partial rows, rank order
+            for (uint32_t m = pr->shard_mask; m; m &= m - 1) {
+                const __nv_bfloat16* row =
+                    pr->rows[__ffs(m) - 1] + (size_t)(pr->shard_row + shard_t0 + t) * h;
+                const int4 raw = ptx::ld_nc_v4(reinterpret_cast<const int4*>(row) + v);
+                const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float2 f = __bfloat1622float2(b[i]);
+                    acc[2 * i] += f.x;
+                    acc[2 * i + 1] += f.y;
+                }
+            }
+        }
+        for (int s = 0; s < (shard_t0 >= 0 ? 0 : num_shared); ++s) {
             const int64_t row = shared_base + (int64_t)s * shared_stride + t;
             const int4 raw = ptx::ld_nc_v4(reinterpret_cast<const int4*>(y + (size_t)row * h) + v);
             const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&raw);
@@ -659,6 +832,47 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
     if (n_tiles == 0) return cudaSuccess;
     const char* ver = getenv("MOE_ROUTER");   // 3: round 1's kernel (comparison)
     if (ver && atoi(ver) == 3) return launch_router_v3(x, T, h, wr, ne, k, renorm, idx, gates, tile_counts, st);
+    if (!ver || atoi(ver) == 6) {
+        // v6 buckets: N_e padded to NW * EPT; tokens per lane TPT (MOE_ROUTER_TPT = 1/2/4):
+        // few experts -> 1 token per lane (C1: latency-bound chains, as many warps as possible),
+        // many -> 4 (each router broadcast feeds 8 DFMAs)
+        int tpt = ne <= 8 ? 1 : (ne <= 16 ? 2 : 4);
+        if (const char* e = getenv("MOE_ROUTER_TPT")) {
+            const int v = atoi(e);
+            if (v == 1 || v == 2 || v == 4) tpt = v;
+        }
+        const int ktok = kRouteTile * tpt;
+        const int blocks = (T + ktok - 1) / ktok;
+        cudaError_t err = cudaSuccess;
+#define MOE_ROUTER6(E, P, N)                                                                 \
+    do {                                                                                     \
+        constexpr int cw_ = router_v6_cw(kRouteTile * P + N * E);                            \
+        const size_t dyn_ = sizeof(double) * std::max<size_t>(                               \
+            2 * (size_t)cw_ * (kRouteTile * P) + 2 * (size_t)cw_ * (N * E),                  \
+            (size_t)(kRouteTile * P) * (N * E));                                             \
+        if (h % cw_) return cudaErrorInvalidValue;                                           \
+        err = cudaFuncSetAttribute(router_v6_kernel<E, P, N, cw_>,                           \
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_);  \
+        if (err != cudaSuccess) return err;                                                  \
+        router_v6_kernel<E, P, N, cw_><<<blocks, N * 32, dyn_, st>>>(x, T, h, wr, ne, k,     \
+                                                                    renorm, idx, gates,      \
+                                                                    tile_counts);            \
+    } while (0)
+#define MOE_ROUTER6_TPT(E, N)                                                                \
+    do {                                                                                     \
+        if (tpt == 1) MOE_ROUTER6(E, 1, N);                                                  \
+        else if (tpt == 2) MOE_ROUTER6(E, 2, N);                                             \
+        else MOE_ROUTER6(E, 4, N);                                                           \
+    } while (0)
+        if (ne <= 8) MOE_ROUTER6_TPT(2, 4);
+        else if (ne <= 16) MOE_ROUTER6_TPT(4, 4);
+        else if (ne <= 32) MOE_ROUTER6_TPT(8, 4);
+        else if (ne <= 64) MOE_ROUTER6_TPT(8, 8);
+        else MOE_ROUTER6_TPT(8, 16);
+#undef MOE_ROUTER6_TPT
+#undef MOE_ROUTER6
+        return cudaGetLastError();
+    }
     // experts per warp: few experts -> 2 per warp (C1: 4 warps per 32 tokens, parallel chains
     // on every SM); 16 -> 4; more -> 8 with two tokens per lane (every broadcast feeds 16 DFMAs)
     int ept = ne <= 8 ? 2 : (ne <= 16 ? 4 : 8);
@@ -717,11 +931,12 @@ cudaError_t launch_combine(const __nv_bfloat16* y_perm, const int32_t* pos, cons
                            int T, int h, int k, int num_shared, int64_t shared_base,
                            int64_t shared_stride, const __nv_bfloat16* resid, __nv_bfloat16* out,
                            const int32_t* idx, const int32_t* offsets, const PeerRows* pr,
-                           cudaStream_t st) {
+                           int shard_t0, cudaStream_t st) {
     if (T == 0) return cudaSuccess;
+    if (shard_t0 >= 0 && !pr) return cudaErrorInvalidValue;
     combine_kernel<<<(T + 7) / 8, 256, 0, st>>>(y_perm, pos, gates, T, h, k, num_shared,
                                                 shared_base, shared_stride, resid, out, idx,
-                                                offsets, pr);
+                                                offsets, pr, shard_t0);
     return cudaGetLastError();
 }
 

@@ -8,7 +8,7 @@ import os
 import sys
 
 
-def run_rank(rank, world, port, cfg_tuple, calls, device, q):
+def run_rank(rank, world, port, cfg_tuple, calls, device, q, shard=False):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     if root not in sys.path:
         sys.path.insert(0, root)
@@ -18,7 +18,7 @@ def run_rank(rank, world, port, cfg_tuple, calls, device, q):
         import torch.distributed as dist
 
         import synth
-        from paper_2504_09345_b200 import HostExperts, MoELayer
+        from paper_2504_09345_b200 import HostExperts, MoELayer, shared_slice_weights
 
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -29,10 +29,16 @@ def run_rank(rank, world, port, cfg_tuple, calls, device, q):
         lo, hi = T * rank // world, T * (rank + 1) // world
         ids = list(range(rank * nl, (rank + 1) * nl)) + [ne + s for s in range(S)]
         inp = synth.gen_inputs(cfg, expert_ids=ids)   # only this rank's experts
-        experts = HostExperts(cfg.hidden, cfg.ffn, inp.w1, inp.w3, inp.w2)
+        if shard:   # MOE_FLAG_SHARD_SHARED: routed experts + this rank's shared-FFN slice
+            sl = shared_slice_weights(cfg.ffn, inp.w1[nl:], inp.w3[nl:], inp.w2[nl:], world, rank)
+            experts = HostExperts(cfg.hidden, cfg.ffn, inp.w1[:nl], inp.w3[:nl], inp.w2[:nl],
+                                  slice_=sl)
+        else:
+            experts = HostExperts(cfg.hidden, cfg.ffn, inp.w1, inp.w3, inp.w2)
         cap = max(1, -(-T // world))   # one capacity on every rank (checked at connect)
         layer = MoELayer(cfg.hidden, cfg.ffn, ne, cfg.top_k, cap, num_shared=S,
-                         device=device, world_size=world, rank=rank, ipc_ep=True)
+                         device=device, world_size=world, rank=rank, ipc_ep=True,
+                         shard_shared=shard)
         handles = [None] * world
         dist.all_gather_object(handles, layer.ipc_handle())
         layer.ipc_connect(handles)
@@ -48,8 +54,8 @@ def run_rank(rank, world, port, cfg_tuple, calls, device, q):
         s.synchronize()
         layer.sync()
         st = layer.stats()
-        q.put((rank, idx.cpu().numpy(), out.view(torch.int16).cpu().numpy(), st["comm_bytes"],
-               None))
+        q.put((rank, idx.cpu().numpy(), out.view(torch.int16).cpu().numpy(),
+               (st["comm_bytes"], st["h2d_weight_bytes"]), None))
         dist.barrier()          # peers may still read this rank's y_recv until they are done
         layer.close()
         experts.close()

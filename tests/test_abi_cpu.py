@@ -109,3 +109,67 @@ def test_header_compiles_as_plain_c99(tmp_path):
     r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-Werror", "-pedantic",
                         "-fsyntax-only", "-I", inc, str(src)], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+# ------------------------------------------------ MOE_FLAG_SHARD_SHARED host logic
+@pytest.mark.parametrize("ffn,S,W", [(1408, 2, 8), (1408, 1, 8), (256, 2, 8), (384, 1, 8),
+                                     (14336, 1, 2), (1408, 2, 2), (1408, 3, 4), (128, 1, 8)])
+def test_shared_slice_partitions_the_concatenated_ffn(lib, ffn, S, W):
+    """Slices of all ranks tile [0, S*ffn) in rank order with 128-column blocks, widths differ
+    by at most one block (so every rank's slice fits one expert slot when S <= W)."""
+    spans = [moe.moe_shared_slice(ffn, S, W, r) for r in range(W)]
+    pos = 0
+    for c0, w in spans:
+        assert c0 == pos and w % 128 == 0 and w >= 0
+        pos += w
+    assert pos == S * ffn
+    widths = [w for _, w in spans]
+    assert max(widths) - min(widths) <= 128
+    if S <= W:
+        assert max(widths) <= ffn
+
+
+def test_shared_slice_rejects_bad_arguments(lib):
+    for args in ((1408, 0, 8, 0), (1408, 2, 0, 0), (1408, 2, 8, 8), (1408, 2, 8, -1),
+                 (100, 2, 8, 0)):
+        with pytest.raises(moe.MoEError) as ei:
+            moe.moe_shared_slice(*args)
+        assert ei.value.status == moe.MOE_E_INVAL
+
+
+def test_shared_slices_sum_to_the_shared_ffns():
+    """The math the sharded layout relies on (include/moe.h MOE_FLAG_SHARD_SHARED): the sum over
+    ranks of the SwiGLU FFN of each rank's slice (shared_slice_weights) equals the sum of the
+    S shared experts' FFNs, in fp64 on bf16 weights -- pins the slicing (rows of W1/W3, columns
+    of W2, expert boundaries crossed by a slice) against whole experts."""
+    import synth
+    from paper_2504_09345_b200 import shared_slice_weights
+    cfg = synth.MoEConfig("custom", 19, 256, 384, 4, 2, 8, 3)
+    inp = synth.gen_inputs(cfg)
+    f64 = lambda a: synth.bf16_bits_to_f32(a).astype(np.float64)
+    x = f64(inp.x)
+
+    def ffn(w1, w3, w2):
+        a, b = x @ f64(w1).T, x @ f64(w3).T
+        return (a / (1 + np.exp(-a)) * b) @ f64(w2).T
+
+    ne = cfg.num_experts
+    want = sum(ffn(inp.w1[ne + s], inp.w3[ne + s], inp.w2[ne + s]) for s in range(cfg.num_shared))
+    for W in (3, 4, 8):
+        parts = [shared_slice_weights(cfg.ffn, inp.w1[ne:], inp.w3[ne:], inp.w2[ne:], W, r)
+                 for r in range(W)]
+        got = sum(ffn(*p) for p in parts if p is not None)
+        np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-12)
+
+
+def test_shard_shared_rejected_outside_its_envelope(lib):
+    """MOE_FLAG_SHARD_SHARED needs the P2P transport, W > 1 and 1 <= num_shared <= W, and not
+    the mover; moe_init refuses anything else before touching CUDA."""
+    for kw in (dict(world_size=1, local_ep=True, num_shared=1),
+               dict(world_size=2, local_ep=True, num_shared=3),
+               dict(world_size=2, local_ep=True, num_shared=0),
+               dict(world_size=2, local_ep=True, num_shared=1, mover=True),
+               dict(world_size=2, num_shared=1)):               # NCCL transport
+        with pytest.raises(moe.MoEError) as ei:
+            moe.MoELayer(256, 256, 8, 2, 64, nccl_unique_id=b"k" * 128, shard_shared=True, **kw)
+        assert ei.value.status == moe.MOE_E_UNSUPPORTED, kw

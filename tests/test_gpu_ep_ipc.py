@@ -72,15 +72,15 @@ def test_ep_ipc_processes(world, shape):
         assert np.array_equal(out.reshape(hi - lo, -1), out_full[lo:hi]), f"rank {r} differs"
         y = torch.from_numpy(out.reshape(hi - lo, -1)).view(torch.bfloat16)
         assert token_rel_err(to_f32(y), y_ref[lo:hi]).max() <= 2e-2
-    assert sum(results[r][2] for r in range(world)) == 3 * 2 * T * cfg.top_k * cfg.hidden * 2
+    assert sum(results[r][2][0] for r in range(world)) == 3 * 2 * T * cfg.top_k * cfg.hidden * 2
     assert all(p.exitcode == 0 for p in procs)
 
 
-def _run_ranks(world, cfg_arg, calls, timeout=900):
+def _run_ranks(world, cfg_arg, calls, timeout=900, shard=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=run_rank, args=(r, world, port, cfg_arg, calls, 0, q))
+    procs = [ctx.Process(target=run_rank, args=(r, world, port, cfg_arg, calls, 0, q, shard))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -136,4 +136,38 @@ def test_ep_ipc_full_size(name, world):
     err = token_rel_err(to_f32(y), y_ref)
     print(f"{name} W={world}: max token rel err {err.max():.3e} over {len(sel)} stratified tokens")
     assert err.max() <= 2e-2
-    assert sum(results[r][2] for r in range(world)) == 2 * 2 * T * cfg.top_k * cfg.hidden * 2
+    assert sum(results[r][2][0] for r in range(world)) == 2 * 2 * T * cfg.top_k * cfg.hidden * 2
+
+
+def test_ep_ipc_full_size_sharded_shared():
+    """C4 (DeepSeek-V2-Lite shape: 64 routed experts top-6 + 2 shared) at W = 8 processes with
+    the shared experts SHARDED (MOE_FLAG_SHARD_SHARED): each rank streams its 8
+    routed experts and a 352-column slice of the 2816-wide concatenated shared FFN (17.3 MB x 8 +
+    4.3 MB, vs 17.3 MB x 10 replicated), every token is gathered to every slice owner and the
+    partial rows are summed in the token's rank.  Bar: routing bit-exact on every token; the
+    stratified token set within 2e-2 of the oracle; host bytes summed over ranks = the
+    algorithmic bytes of one layer per call (no replication)."""
+    from gpu_helpers import sample_tokens, stratified_tokens
+    cfg = synth.CONFIGS["dsv2_lite"]
+    world = 8
+    inp = synth.gen_inputs(cfg)
+    logits = oracle.router_logits(inp.x, inp.router)
+    idx_ref, g_ref = oracle.topk_gates(logits, cfg.top_k)
+    results = _run_ranks(world, "dsv2_lite", 2, shard=True)
+    T = cfg.tokens
+    out_ep = np.empty((T, cfg.hidden), dtype=np.int16)
+    for r in range(world):
+        lo, hi = T * r // world, T * (r + 1) // world
+        idx, out, _ = results[r]
+        assert np.array_equal(idx, idx_ref[lo:hi]), f"rank {r}: routing differs"
+        out_ep[lo:hi] = out.reshape(hi - lo, -1)
+    sel = np.union1d(stratified_tokens(idx_ref, cfg.num_experts, cfg.num_shared),
+                     sample_tokens(T, 16))
+    y_ref = oracle.experts_combine(inp.x[sel], inp.w1, inp.w3, inp.w2, cfg.num_experts,
+                                   cfg.num_shared, idx_ref[sel], g_ref[sel])
+    y = torch.from_numpy(out_ep[sel]).view(torch.bfloat16)
+    err = token_rel_err(to_f32(y), y_ref)
+    print(f"dsv2_lite W=8 sharded shared: max token rel err {err.max():.3e} over {len(sel)} tokens")
+    assert err.max() <= 2e-2
+    layer_bytes = (cfg.num_experts + cfg.num_shared) * 6 * cfg.hidden * cfg.ffn
+    assert sum(results[r][2][1] for r in range(world)) == 2 * layer_bytes

@@ -352,16 +352,20 @@ def test_experts_per_gemm_launch(rows, copy_group, launches, monkeypatch):
         run.close()
 
 
-@pytest.mark.parametrize("variant", ["v3-1", "v3-2", "v3-4", "v3-8", "v5-1", "v5-2", "v5-4",
-                                     "v5-8", "v5-2-tpt2", "v5-4-tpt2", "v5-8-tpt1"])
-@pytest.mark.parametrize("ne,k", [(5, 2), (8, 2), (16, 4), (40, 6)])   # 40: 2 tokens per lane
+@pytest.mark.parametrize("variant", ["v3-1", "v3-2", "v3-4", "v3-8", "v5-2", "v5-8-tpt1",
+                                     "v6-0-tpt1", "v6-0-tpt2", "v6-0-tpt4"])
+@pytest.mark.parametrize("ne,k", [(5, 2), (8, 2), (16, 4), (40, 6), (128, 8)])
 def test_router_experts_per_warp_variants(ne, k, variant, monkeypatch):
-    """Every router kernel instantiation -- round 1's router_topk_kernel<EPT> (MOE_ROUTER=3) and
-    router_v5_kernel<EPT, TPT> (default; MOE_ROUTER_EPT / MOE_ROUTER_TPT) -- gives the same
-    bit-exact selection and gates (one fp64 FMA chain per logit, ascending channels, either way)."""
+    """Every router kernel instantiation -- round 1's router_topk_kernel<EPT> (MOE_ROUTER=3),
+    router_v5_kernel<EPT, TPT> (MOE_ROUTER=5) and router_v6_kernel<EPT, TPT, NW, CW> (default;
+    every N_e bucket x MOE_ROUTER_TPT = 1 / 2 / 4) -- gives the same bit-exact selection and gates
+    as the oracle (one fp64 FMA chain per logit, ascending channels, in every kernel)."""
     ver, ept, *rest = variant.split("-")
+    if ne == 128 and ver != "v6":
+        pytest.skip("128 experts: v6 buckets only")
     monkeypatch.setenv("MOE_ROUTER", ver[1])
-    monkeypatch.setenv("MOE_ROUTER_EPT", ept)
+    if ept != "0":
+        monkeypatch.setenv("MOE_ROUTER_EPT", ept)
     if rest:
         monkeypatch.setenv("MOE_ROUTER_TPT", rest[0][3])
     cfg = synth.MoEConfig("custom", 19, 384, 256, ne, k, 777, 0)
@@ -489,6 +493,91 @@ def test_ep_local_transport_world_ranks(world, shape):
     for e in experts:
         e.close()
     full.close()
+
+
+@pytest.mark.parametrize("world,shape", [
+    (2, dict(hidden=256, ffn=384, num_experts=8, top_k=2, tokens=600, num_shared=1)),
+    (4, dict(hidden=256, ffn=256, num_experts=16, top_k=4, tokens=1000, num_shared=2)),
+    # 4 blocks of 128 columns over 8 ranks: ranks 0, 2, 4, 6 serve no slice
+    (8, dict(hidden=384, ffn=256, num_experts=64, top_k=6, tokens=804, num_shared=2)),
+    (8, dict(hidden=256, ffn=384, num_experts=8, top_k=2, tokens=5, num_shared=1)),  # empty ranks
+])
+def test_ep_local_sharded_shared_experts(world, shape):
+    """MOE_FLAG_SHARD_SHARED over the LOCAL_EP transport: rank r streams only
+    its column slice of the concatenated shared FFN (moe_shared_slice), the permute gathers every
+    rank's tokens into the slice owners, the combine sums their partial rows.  Bar: routing
+    bit-exact; every token within 2e-2 of the oracle (shared experts as whole FFNs, R10);
+    three calls reuse every buffer; the ranks together stream each weight byte exactly once
+    per call (routed experts + the slices = the algorithmic bytes, no replication)."""
+    import os
+    import threading
+    from paper_2504_09345_b200 import HostExperts, MoELayer, shared_slice_weights
+    cfg = synth.MoEConfig("custom", 18, shape["hidden"], shape["ffn"], shape["num_experts"],
+                          shape["top_k"], shape["tokens"], shape["num_shared"])
+    inp = synth.gen_inputs(cfg)
+    y_ref, idx_ref, _ = oracle.forward(inp.x, inp.router, inp.w1, inp.w3, inp.w2, cfg.top_k,
+                                       cfg.num_shared)
+    ne, nl, S = cfg.num_experts, cfg.num_experts // world, cfg.num_shared
+    T, h = cfg.tokens, cfg.hidden
+    bounds = [T * r // world for r in range(world + 1)]
+    key = os.urandom(128)
+    router = bf16_tensor(inp.router)
+    layers, experts, outs, idxs, errors = [], [], [None] * world, [None] * world, []
+    for r in range(world):
+        ids = list(range(r * nl, (r + 1) * nl))
+        sl = shared_slice_weights(cfg.ffn, inp.w1[ne:], inp.w3[ne:], inp.w2[ne:], world, r)
+        experts.append(HostExperts(h, cfg.ffn, [inp.w1[i] for i in ids], [inp.w3[i] for i in ids],
+                                   [inp.w2[i] for i in ids], slice_=sl))
+    for r in range(world):
+        layers.append(MoELayer(h, cfg.ffn, ne, cfg.top_k, max(1, -(-T // world)), num_shared=S,
+                               world_size=world, rank=r, nccl_unique_id=key, local_ep=True,
+                               shard_shared=True))
+    bufs = []
+    for r in range(world):
+        x = bf16_tensor(inp.x[bounds[r]:bounds[r + 1]].reshape(-1, h))
+        bufs.append((torch.cuda.Stream(), x, torch.empty_like(x),
+                     torch.empty((x.shape[0], cfg.top_k), dtype=torch.int32, device="cuda")))
+    torch.cuda.synchronize()
+
+    def work(r):
+        try:
+            s, x, o, idx = bufs[r]
+            for _ in range(3):
+                layers[r].forward(x, router, experts[r], o, idx, stream=s.cuda_stream)
+            s.synchronize()
+            outs[r], idxs[r] = o, idx
+        except Exception as e:
+            msg = repr(e)[:300]
+            try:
+                layers[r].sync()
+            except Exception as e2:
+                msg += f" | sync: {e2!r}"[:300]
+            errors.append((r, msg))
+
+    threads = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=300)
+    assert not errors, "\n".join(f"rank {r}: {str(e)[:300]}" for r, e in errors)
+    worst = 0.0
+    for r in range(world):
+        lo, hi = bounds[r], bounds[r + 1]
+        if hi == lo:
+            continue
+        assert np.array_equal(idxs[r].cpu().numpy(), idx_ref[lo:hi])
+        worst = max(worst, float(token_rel_err(to_f32(outs[r]), y_ref[lo:hi]).max()))
+    assert worst <= TOL, worst
+    st = [l.stats() for l in layers]
+    assert sum(s["h2d_weight_bytes"] for s in st) == 3 * (ne + S) * 6 * h * cfg.ffn
+    served = sum(1 for r in range(world) if experts[r].slice_bytes)
+    assert served == min(world, S * cfg.ffn // 128)
+    # routed rows out and back, plus every token to each slice owner and its partial row back
+    assert sum(s["comm_bytes"] for s in st) == 3 * 2 * (T * cfg.top_k + served * T) * h * 2
+    for l in layers:
+        l.close()
+    for e in experts:
+        e.close()
 
 
 @pytest.mark.parametrize("group", ["1", "3", "4"])

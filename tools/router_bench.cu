@@ -5,6 +5,7 @@
 //        tools/router_bench.cu -L paper_2504_09345_b200 -lmoe_b200 -o build/router_bench
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "moe_internal.h"
@@ -41,11 +42,26 @@ int main(int argc, char** argv) {
     cudaError_t err = cudaEventSynchronize(e1);
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
+    // bitwise check against round 1's kernel (v3) on the same inputs
+    int32_t* idx3;
+    float* g3;
+    cudaMalloc(&idx3, (size_t)T * k * 4);
+    cudaMalloc(&g3, (size_t)T * k * 4);
+    moe::launch_router_v3(x, T, h, w, ne, k, 1, idx3, g3, tc, 0);
+    cudaDeviceSynchronize();
+    std::vector<int32_t> a((size_t)T * k), b((size_t)T * k);
+    std::vector<float> ga((size_t)T * k), gb((size_t)T * k);
+    cudaMemcpy(a.data(), idx, a.size() * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(b.data(), idx3, b.size() * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(ga.data(), g, ga.size() * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(gb.data(), g3, gb.size() * 4, cudaMemcpyDeviceToHost);
+    size_t bad = 0;
+    for (size_t i = 0; i < a.size(); ++i) bad += (a[i] != b[i]) || (memcmp(&ga[i], &gb[i], 4) != 0);
     const double dfma = (double)T * ne * h;
-    printf("router T=%d h=%d N_e=%d k=%d [MOE_ROUTER=%s EPT=%s TPT=%s]: %.1f us  %.2f TFLOP/s fp64 (%s)\n",
-           T, h, ne, k, getenv("MOE_ROUTER") ? getenv("MOE_ROUTER") : "5",
+    printf("router T=%d h=%d N_e=%d k=%d [MOE_ROUTER=%s EPT=%s TPT=%s]: %.1f us  %.2f TFLOP/s fp64 (%s; %zu of %zu idx/gates differ from v3)\n",
+           T, h, ne, k, getenv("MOE_ROUTER") ? getenv("MOE_ROUTER") : "6",
            getenv("MOE_ROUTER_EPT") ? getenv("MOE_ROUTER_EPT") : "auto",
            getenv("MOE_ROUTER_TPT") ? getenv("MOE_ROUTER_TPT") : "auto", 1e3 * ms / iters,
-           2 * dfma / (ms / iters * 1e-3) / 1e12, cudaGetErrorString(err));
+           2 * dfma / (ms / iters * 1e-3) / 1e12, cudaGetErrorString(err), bad, a.size());
     return 0;
 }
