@@ -268,149 +268,8 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-// Router v5: the same one-FMA-chain-per-logit arithmetic (reading R6), restructured so shared
-// memory stops being the bottleneck and each chunk costs one barrier:
-//   * channels are consumed in chunks of CW; per chunk the block's token rows (bf16, cp.async,
-//     coalesced, rows padded by 16 B so the per-lane 16-byte row reads are conflict-free) and the
-//     router rows (widened to fp64 once, [channel][expert]) are staged into the other half of a
-//     double buffer while the current chunk is consumed -- ONE __syncthreads per chunk;
-//   * a lane owns TPT tokens and EPT experts (warp w: experts [w*EPT, (w+1)*EPT)); per 8
-//     channels it reads each token's 16-byte row slice once (widened to fp64 in registers) and
-//     EPT/2 double2 broadcasts of router weights per channel, feeding TPT*EPT independent chains.
-// Per warp and 8 channels: TPT x (4 wavefronts of row reads) + 4 EPT broadcast wavefronts for
-// 8 TPT EPT warp-DFMAs; with EPT >= 4 the fp64 pipe (not shared memory) is the limit.
-template <int EPT, int TPT>
-__global__ void __launch_bounds__(512)
-router_v5_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
-                 const __nv_bfloat16* __restrict__ wr, int ne, int k, int renorm, int cw,
-                 int32_t* __restrict__ idx_out, float* __restrict__ gate_out,
-                 int32_t* __restrict__ tile_counts) {
-    constexpr int kTok = kRouteTile * TPT;
-    extern __shared__ __align__(16) double dyn[];
-    __shared__ int cnt[TPT][kMaxExperts];
-    const int nw = blockDim.x >> 5;
-    const int ne_pad = nw * EPT;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
-    const int t0 = blockIdx.x * kTok;
-    const int xpitch = cw + 8;   // bf16 per staged row (16 B of padding)
-    double* wbuf = dyn;                                                       // [2][cw][ne_pad]
-    __nv_bfloat16* xbuf = reinterpret_cast<__nv_bfloat16*>(dyn + 2 * (size_t)cw * ne_pad);  // [2][kTok][xpitch]
-    for (int e = tid; e < TPT * kMaxExperts; e += nthr) cnt[e / kMaxExperts][e % kMaxExperts] = 0;
-
-    // router chunk: vector v = 8 channels of expert v % ne_pad, through registers (widened)
-    constexpr int kMaxWV = 4;   // (cw / 8) * ne_pad <= 4 * nthr  (host: cw * EPT <= 1024)
-    const int n_wv = (cw / 8) * ne_pad;
-    int4 wv[kMaxWV];
-    auto wload = [&](int c0) {
-#pragma unroll
-        for (int j = 0; j < kMaxWV; ++j) {
-            const int v = tid + j * nthr;
-            if (v < n_wv) {
-                const int e = v % ne_pad, cc = (v / ne_pad) * 8;
-                wv[j] = (e < ne) ? ptx::ld_nc_v4(wr + (size_t)e * h + c0 + cc) : make_int4(0, 0, 0, 0);
-            }
-        }
-    };
-    auto wstore = [&](int b) {
-        double* ws = wbuf + (size_t)b * cw * ne_pad;
-        double d[8];
-#pragma unroll
-        for (int j = 0; j < kMaxWV; ++j) {
-            const int v = tid + j * nthr;
-            if (v < n_wv) {
-                const int e = v % ne_pad, cc = (v / ne_pad) * 8;
-                bf16x8_to_f64(wv[j], d);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) ws[(cc + q) * ne_pad + e] = d[q];
-            }
-        }
-    };
-    // token chunk: row r's channels [c0, c0 + cw) -> xbuf[b][r][0 .. cw), 16 B per cp.async
-    const int n_xv = kTok * (cw / 8);
-    auto xstage = [&](int c0, int b) {
-        __nv_bfloat16* xs = xbuf + (size_t)b * kTok * xpitch;
-        for (int v = tid; v < n_xv; v += nthr) {
-            const int r = v / (cw / 8), cc = (v % (cw / 8)) * 8;
-            const int t = t0 + r;
-            cp_async16(xs + (size_t)r * xpitch + cc, x + (size_t)(t < T ? t : 0) * h + c0 + cc,
-                       t < T ? 16 : 0);
-        }
-        cp_async_commit();
-    };
-
-    xstage(0, 0);
-    wload(0);
-    wstore(0);
-    cp_async_wait_all();
-    __syncthreads();
-
-    double acc[TPT][EPT];
-#pragma unroll
-    for (int p = 0; p < TPT; ++p)
-#pragma unroll
-        for (int i = 0; i < EPT; ++i) acc[p][i] = 0.0;
-    const int n_chunks = h / cw;
-    for (int ch = 0; ch < n_chunks; ++ch) {
-        const int b = ch & 1;
-        const bool more = ch + 1 < n_chunks;
-        if (more) {   // the next chunk in flight while this one is consumed
-            xstage((ch + 1) * cw, b ^ 1);
-            wload((ch + 1) * cw);
-        }
-        const __nv_bfloat16* xs = xbuf + (size_t)b * kTok * xpitch;
-        const double* ws = wbuf + (size_t)b * cw * ne_pad + warp * EPT;
-#pragma unroll 1
-        for (int c8 = 0; c8 < cw; c8 += 8) {
-            double xd[TPT][8];
-#pragma unroll
-            for (int p = 0; p < TPT; ++p) {
-                const int4 raw = *reinterpret_cast<const int4*>(xs + (size_t)(p * 32 + lane) * xpitch + c8);
-                bf16x8_to_f64(raw, xd[p]);
-            }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const double* wrow = ws + (size_t)(c8 + q) * ne_pad;
-                if constexpr (EPT == 1) {
-                    const double w = wrow[0];
-#pragma unroll
-                    for (int p = 0; p < TPT; ++p) acc[p][0] = fma(xd[p][q], w, acc[p][0]);
-                } else {
-                    const double2* w2 = reinterpret_cast<const double2*>(wrow);
-#pragma unroll
-                    for (int i = 0; i < EPT / 2; ++i) {
-                        const double2 w = w2[i];
-#pragma unroll
-                        for (int p = 0; p < TPT; ++p) {
-                            acc[p][2 * i] = fma(xd[p][q], w.x, acc[p][2 * i]);
-                            acc[p][2 * i + 1] = fma(xd[p][q], w.y, acc[p][2 * i + 1]);
-                        }
-                    }
-                }
-            }
-        }
-        if (more) {
-            wstore(b ^ 1);
-            cp_async_wait_all();
-        }
-        __syncthreads();   // next chunk visible; this chunk's buffers free for chunk + 2
-    }
-    double* lg = dyn;  // [kTok][ne_pad] logits (host sizes dyn for it)
-#pragma unroll
-    for (int p = 0; p < TPT; ++p)
-#pragma unroll
-        for (int i = 0; i < EPT; ++i) lg[(p * 32 + lane) * ne_pad + warp * EPT + i] = acc[p][i];
-    __syncthreads();
-    topk_tile<TPT>(lg, ne_pad, t0, T, ne, k, renorm, idx_out, gate_out, cnt, warp, nw, lane);
-    __syncthreads();
-    const int n_tiles = (T + kRouteTile - 1) / kRouteTile;
-#pragma unroll
-    for (int p = 0; p < TPT; ++p) {
-        const int tile = blockIdx.x * TPT + p;
-        if (tile < n_tiles)
-            for (int e = tid; e < ne; e += nthr) tile_counts[(size_t)tile * ne + e] = cnt[p][e];
-    }
-}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // Router v6: the same one-FMA-chain-per-logit arithmetic (reading R6); every operand is widened
 // to fp64 ONCE per block, when its chunk is staged, so the inner loop is shared-memory loads and
@@ -418,130 +277,177 @@ router_v5_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
 // ncu at C1: issue-bound at 28% slot use with 4 warps per SM).
 //   * a block = TPT x 32 tokens and NW warps; warp w owns experts [w*EPT, (w+1)*EPT) (zero rows
 //     pad N_e to NW*EPT), lane l owns tokens l, l+32, ...: TPT*EPT independent chains per lane;
-//   * channels are consumed in chunks of CW: x as [channel pair][token] double2 (one 16-byte
-//     read gives a lane two channels of one token, conflict-free), the router rows as
-//     [channel][expert] fp64 (double2 broadcasts), both double-buffered; the next chunk is
-//     loaded from global memory into registers during the current chunk's DFMAs and widened into
-//     the other buffer after them -- one __syncthreads per chunk;
+//   * channels are consumed in chunks of CW.  Raw bf16 chunks arrive by cp.async into a
+//     kStages-deep ring, kStages-1 chunks ahead (at C1 a chunk's DFMAs take less than a DRAM
+//     round trip, so one chunk of look-ahead left every chunk waiting on memory: ncu
+//     long-scoreboard); each thread widens the vectors IT copied (no barrier between the copy and
+//     the widening) into a double-buffered fp64 tile -- x as [channel pair][token] double2 (one
+//     16-byte read gives a lane two channels of one token, conflict-free), the router rows as
+//     [channel][expert] (double2 broadcasts) -- one __syncthreads per chunk;
 //   * per channel pair and warp: TPT x-reads (4 wavefronts each) + EPT double2 broadcasts for
 //     2*TPT*EPT DFMAs.
-// Channels per chunk: the largest power of two <= 128 whose double-buffered fp64 x + router
-// tiles (16 B per channel per token / expert) fit 96 KB -- two blocks per SM.
+constexpr int kRouterStages = 4;
+
+// Channels per chunk: the largest power of two <= 128 whose fp64 double buffer (16 B per channel
+// per token / expert) + raw bf16 ring (kRouterStages x 2 B) fit 96 KB -- two blocks per SM.
 constexpr int router_v6_cw(int rows) {
     int cw = 128;
-    while (cw > 8 && 16 * cw * rows > 96 * 1024) cw >>= 1;
+    while (cw > 8 && (16 + 2 * kRouterStages) * cw * rows > 96 * 1024) cw >>= 1;
     return cw;
 }
 
-template <int EPT, int TPT, int NW, int CW>
+// Channel pairs of operands prefetched into registers: ~48 registers' worth (x: 4 TPT, router:
+// 4 max(EPT, 2) per pair), at least 1.
+constexpr int router_v6_prefetch(int ept, int tpt) {
+    const int per = 4 * tpt + 4 * (ept >= 2 ? ept : 2);
+    const int d = 48 / per;
+    return d < 1 ? 1 : (d > 4 ? 4 : d);
+}
+
+template <int EPT, int TPT, int NW, int CW, int kPf>
 __global__ void __launch_bounds__(NW * 32, 16 / NW)
 router_v6_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
                  const __nv_bfloat16* __restrict__ wr, int ne, int k, int renorm,
                  int32_t* __restrict__ idx_out, float* __restrict__ gate_out,
                  int32_t* __restrict__ tile_counts) {
-    static_assert(EPT % 2 == 0 && CW % 8 == 0, "shape");
+    static_assert((EPT == 1 || EPT % 2 == 0) && CW % 8 == 0 && kPf >= 1, "shape");
     constexpr int kTok = kRouteTile * TPT;
     constexpr int kThr = NW * 32;
     constexpr int kNePad = NW * EPT;
     constexpr int kNXV = kTok * (CW / 8);              // 16-byte x vectors per chunk
     constexpr int kNWV = kNePad * (CW / 8);            // 16-byte router vectors per chunk
-    constexpr int kXV = (kNXV + kThr - 1) / kThr;
-    constexpr int kWV = (kNWV + kThr - 1) / kThr;
+    constexpr int kNV = kNXV + kNWV;
+    constexpr int kVT = (kNV + kThr - 1) / kThr;       // vectors per thread
     extern __shared__ __align__(16) double dyn[];
     __shared__ int cnt[TPT][kMaxExperts];
     double2* xs = reinterpret_cast<double2*>(dyn);                 // [2][CW/2][kTok]
     double* ws = dyn + 2 * CW * kTok;                              // [2][CW][kNePad]
+    int4* raw = reinterpret_cast<int4*>(ws + 2 * CW * kNePad);     // [kRouterStages][kNV]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int t0 = blockIdx.x * kTok;
     for (int e = tid; e < TPT * kMaxExperts; e += kThr) cnt[e / kMaxExperts][e % kMaxExperts] = 0;
 
-    // staging: consecutive threads take consecutive TOKENS (x) / EXPERTS (router) at one 8-channel
-    // group, so the widened stores hit consecutive shared-memory words
-    int4 xr[kXV], wv[kWV];
-    auto load = [&](int c0) {
+    // vector v < kNXV: token v % kTok, channels (v / kTok)*8 ..; else router row (v - kNXV) %
+    // kNePad.  Consecutive threads take consecutive tokens / experts at one 8-channel group, so
+    // the widened stores hit consecutive shared-memory words.
+    auto issue = [&](int c0, int stage) {
+        int4* rs = raw + (size_t)stage * kNV;
 #pragma unroll
-        for (int j = 0; j < kXV; ++j) {
+        for (int j = 0; j < kVT; ++j) {
             const int v = tid + j * kThr;
             if (v < kNXV) {
-                const int t = v % kTok, cc = (v / kTok) * 8;
-                xr[j] = (t0 + t < T) ? ptx::ld_nc_v4(x + (size_t)(t0 + t) * h + c0 + cc)
-                                     : make_int4(0, 0, 0, 0);
+                const int t = t0 + v % kTok, cc = (v / kTok) * 8;
+                cp_async16(rs + v, x + (size_t)(t < T ? t : 0) * h + c0 + cc, t < T ? 16 : 0);
+            } else if (v < kNV) {
+                const int u = v - kNXV, e = u % kNePad, cc = (u / kNePad) * 8;
+                cp_async16(rs + v, wr + (size_t)(e < ne ? e : 0) * h + c0 + cc, e < ne ? 16 : 0);
             }
         }
-#pragma unroll
-        for (int j = 0; j < kWV; ++j) {
-            const int v = tid + j * kThr;
-            if (v < kNWV) {
-                const int e = v % kNePad, cc = (v / kNePad) * 8;
-                wv[j] = (e < ne) ? ptx::ld_nc_v4(wr + (size_t)e * h + c0 + cc)
-                                 : make_int4(0, 0, 0, 0);
-            }
-        }
+        cp_async_commit();
     };
-    auto store = [&](int b) {
+    auto widen = [&](int stage, int b) {   // this thread's own vectors: no barrier needed
+        const int4* rs = raw + (size_t)stage * kNV;
         double2* xb = xs + (size_t)b * (CW / 2) * kTok;
         double* wb = ws + (size_t)b * CW * kNePad;
         double d[8];
 #pragma unroll
-        for (int j = 0; j < kXV; ++j) {
+        for (int j = 0; j < kVT; ++j) {
             const int v = tid + j * kThr;
             if (v < kNXV) {
                 const int t = v % kTok, c2 = (v / kTok) * 4;
-                bf16x8_to_f64(xr[j], d);
+                bf16x8_to_f64(rs[v], d);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) xb[(c2 + q) * kTok + t] = make_double2(d[2 * q], d[2 * q + 1]);
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < kWV; ++j) {
-            const int v = tid + j * kThr;
-            if (v < kNWV) {
-                const int e = v % kNePad, cc = (v / kNePad) * 8;
-                bf16x8_to_f64(wv[j], d);
+            } else if (v < kNV) {
+                const int u = v - kNXV, e = u % kNePad, cc = (u / kNePad) * 8;
+                bf16x8_to_f64(rs[v], d);
 #pragma unroll
                 for (int q = 0; q < 8; ++q) wb[(cc + q) * kNePad + e] = d[q];
             }
         }
     };
 
-    load(0);
-    store(0);
+    const int n_chunks = h / CW;
+#pragma unroll
+    for (int c = 0; c < kRouterStages - 1; ++c) {
+        if (c < n_chunks) issue(c * CW, c);
+        else cp_async_commit();   // empty group: the wait counts below stay uniform
+    }
+    cp_async_wait<kRouterStages - 2>();   // chunk 0 landed
+    widen(0, 0);
     __syncthreads();
     double acc[TPT][EPT];
 #pragma unroll
     for (int p = 0; p < TPT; ++p)
 #pragma unroll
         for (int i = 0; i < EPT; ++i) acc[p][i] = 0.0;
-    const int n_chunks = h / CW;
     for (int ch = 0; ch < n_chunks; ++ch) {
         const int b = ch & 1;
-        const bool more = ch + 1 < n_chunks;
-        if (more) load((ch + 1) * CW);   // in flight during this chunk's DFMAs
+        // chunk ch + kStages - 1 into the ring slot chunk ch - 1 used (widened last iteration)
+        if (ch + kRouterStages - 1 < n_chunks)
+            issue((ch + kRouterStages - 1) * CW, (ch + kRouterStages - 1) % kRouterStages);
+        else
+            cp_async_commit();
         const double2* xb = xs + (size_t)b * (CW / 2) * kTok + lane;
         const double* wb = ws + (size_t)b * CW * kNePad + warp * EPT;
+        // operands of channel pair c2 + kPf are loaded while pair c2's DFMAs issue (explicit
+        // register prefetch: at C1 one warp per SM sub-partition otherwise waited a shared-memory
+        // round trip per channel -- ncu short-scoreboard / wait stalls, ~37 cycles per channel)
+        constexpr int kWP = EPT >= 2 ? EPT / 2 : 1;   // router loads per channel
+        double2 xv[kPf][TPT];
+        double2 wv[kPf][2][kWP];
+        auto fetch = [&](int c2, int slot) {
+#pragma unroll
+            for (int p = 0; p < TPT; ++p) xv[slot][p] = xb[c2 * kTok + p * 32];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const double* wrow = wb + (2 * c2 + q) * kNePad;
+                if constexpr (EPT == 1) {
+                    wv[slot][q][0].x = wrow[0];
+                } else {
+#pragma unroll
+                    for (int i = 0; i < kWP; ++i) wv[slot][q][i] = reinterpret_cast<const double2*>(wrow)[i];
+                }
+            }
+        };
+#pragma unroll
+        for (int c2 = 0; c2 < kPf && c2 < CW / 2; ++c2) fetch(c2, c2);
 #pragma unroll
         for (int c2 = 0; c2 < CW / 2; ++c2) {
-            double2 xv[TPT];
+            const int slot = c2 % kPf;
+            double2 xc[TPT];
+            double2 wc[2][kWP];
 #pragma unroll
-            for (int p = 0; p < TPT; ++p) xv[p] = xb[c2 * kTok + p * 32];
+            for (int p = 0; p < TPT; ++p) xc[p] = xv[slot][p];
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+#pragma unroll
+                for (int i = 0; i < kWP; ++i) wc[q][i] = wv[slot][q][i];
+            if (c2 + kPf < CW / 2) fetch(c2 + kPf, slot);
 #pragma unroll
             for (int q = 0; q < 2; ++q) {   // channel 2*c2 + q: ascending order in every chain
-                const double2* w2 = reinterpret_cast<const double2*>(wb + (2 * c2 + q) * kNePad);
 #pragma unroll
-                for (int i = 0; i < EPT / 2; ++i) {
-                    const double2 w = w2[i];
+                for (int i = 0; i < kWP; ++i) {
 #pragma unroll
                     for (int p = 0; p < TPT; ++p) {
-                        const double xq = q ? xv[p].y : xv[p].x;
-                        acc[p][2 * i] = fma(xq, w.x, acc[p][2 * i]);
-                        acc[p][2 * i + 1] = fma(xq, w.y, acc[p][2 * i + 1]);
+                        const double xq = q ? xc[p].y : xc[p].x;
+                        if constexpr (EPT == 1) {
+                            acc[p][0] = fma(xq, wc[q][0].x, acc[p][0]);
+                        } else {
+                            acc[p][2 * i] = fma(xq, wc[q][i].x, acc[p][2 * i]);
+                            acc[p][2 * i + 1] = fma(xq, wc[q][i].y, acc[p][2 * i + 1]);
+                        }
                     }
                 }
             }
         }
-        if (more) store(b ^ 1);   // chunk b ^ 1 was consumed before the previous barrier
+        if (ch + 1 < n_chunks) {   // fp64 buffer b ^ 1 was consumed before the last barrier
+            cp_async_wait<kRouterStages - 2>();   // chunk ch + 1 landed
+            widen((ch + 1) % kRouterStages, b ^ 1);
+        }
         __syncthreads();
     }
+    cp_async_wait<0>();
     double* lg = dyn;   // [kTok][kNePad] logits (the x buffers, all reads done)
 #pragma unroll
     for (int p = 0; p < TPT; ++p)
@@ -688,7 +594,10 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int h, int k, int ne,
     if (pr) __threadfence_system();   // peer stores performed before the dispatch flag release
 }
 
-// Warp per token; lane handles 8 consecutive columns per 16-byte vector.
+// Warp per (token, 256-column chunk); lane = 8 consecutive columns (one 16-byte vector).  Every
+// lane issues its k row loads (+ shared / residual rows) back to back: one vector per lane keeps
+// the most loads in flight per SM (a warp per whole token row held only ~28 KB in flight per SM
+// at C1's 4096 tokens -- 0.66 of HBM bandwidth in ncu).
 __global__ void __launch_bounds__(256)
 combine_kernel(const __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ pos,
                const float* __restrict__ gates, int T, int h, int k, int num_shared,
@@ -697,8 +606,12 @@ combine_kernel(const __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ 
                const int32_t* __restrict__ offsets, const PeerRows* __restrict__ pr,
                int shard_t0) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int t = blockIdx.x * 8 + warp;
-    if (t >= T) return;
+    const int nvec = h / 8;
+    const int cpt = (nvec + 31) / 32;   // 256-column chunks per token
+    const int64_t gw = (int64_t)blockIdx.x * 8 + warp;
+    const int t = (int)(gw / cpt);
+    const int v = (int)(gw % cpt) * 32 + lane;
+    if (t >= T || v >= nvec) return;
     const __nv_bfloat16* prow[kMaxTopK];
     float g[kMaxTopK];
 #pragma unroll
@@ -722,56 +635,44 @@ combine_kernel(const __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ 
             }
         }
     }
-    const int nvec = h / 8;
-    for (int v = lane; v < nvec; v += 32) {
+    {
+        int4 raw[kMaxTopK];
+#pragma unroll
+        for (int j = 0; j < kMaxTopK; ++j)
+            if (j < k) raw[j] = ptx::ld_nc_v4(reinterpret_cast<const int4*>(prow[j]) + v);
         float acc[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] = 0.f;
-        for (int j = 0; j < k; ++j) {
-            const int4 raw = ptx::ld_nc_v4(reinterpret_cast<const int4*>(prow[j]) + v);
-            const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const float2 f = __bfloat1622float2(b[i]);
-                acc[2 * i] = fmaf(g[j], f.x, acc[2 * i]);
-                acc[2 * i + 1] = fmaf(g[j], f.y, acc[2 * i + 1]);
-            }
-        }
-        if (shard_t0 >= 0) {   // sharded shared experts: the owners' partial rows, rank order
-            for (uint32_t m = pr->shard_mask; m; m &= m - 1) {
-                const __nv_bfloat16* row =
-                    pr->rows[__ffs(m) - 1] + (size_t)(pr->shard_row + shard_t0 + t) * h;
-                const int4 raw = ptx::ld_nc_v4(reinterpret_cast<const int4*>(row) + v);
-                const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&raw);
+        for (int j = 0; j < kMaxTopK; ++j) {   // fixed j order (R10)
+            if (j < k) {
+                const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&raw[j]);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const float2 f = __bfloat1622float2(b[i]);
-                    acc[2 * i] += f.x;
-                    acc[2 * i + 1] += f.y;
+                    acc[2 * i] = fmaf(g[j], f.x, acc[2 * i]);
+                    acc[2 * i + 1] = fmaf(g[j], f.y, acc[2 * i + 1]);
                 }
             }
         }
-        for (int s = 0; s < (shard_t0 >= 0 ? 0 : num_shared); ++s) {
-            const int64_t row = shared_base + (int64_t)s * shared_stride + t;
-            const int4 raw = ptx::ld_nc_v4(reinterpret_cast<const int4*>(y + (size_t)row * h) + v);
-            const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&raw);
+        auto add_row = [&](const __nv_bfloat16* row) {   // weight-1 terms, in call order
+            const int4 r = ptx::ld_nc_v4(reinterpret_cast<const int4*>(row) + v);
+            const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&r);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const float2 f = __bfloat1622float2(b[i]);
                 acc[2 * i] += f.x;
                 acc[2 * i + 1] += f.y;
             }
+        };
+        if (shard_t0 >= 0) {   // sharded shared experts: the owners' partial rows, rank order
+            for (uint32_t m = pr->shard_mask; m; m &= m - 1)
+                add_row(pr->rows[__ffs(m) - 1] + (size_t)(pr->shard_row + shard_t0 + t) * h);
+        } else {
+            for (int s = 0; s < num_shared; ++s)
+                add_row(y + (size_t)(shared_base + (int64_t)s * shared_stride + t) * h);
         }
-        if (resid) {  // Task B: the block's residual connection around the MoE layer
-            const int4 raw = ptx::ld_nc_v4(reinterpret_cast<const int4*>(resid + (size_t)t * h) + v);
-            const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&raw);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const float2 f = __bfloat1622float2(b[i]);
-                acc[2 * i] += f.x;
-                acc[2 * i + 1] += f.y;
-            }
-        }
+        if (resid) add_row(resid + (size_t)t * h);   // Task B: the block's residual connection
         int4 o;
         o.x = (int)ptx::pack_bf16x2(acc[0], acc[1]);
         o.y = (int)ptx::pack_bf16x2(acc[2], acc[3]);
@@ -830,13 +731,22 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
                                int32_t* tile_counts, cudaStream_t st) {
     const int n_tiles = (T + kRouteTile - 1) / kRouteTile;
     if (n_tiles == 0) return cudaSuccess;
-    const char* ver = getenv("MOE_ROUTER");   // 3: round 1's kernel (comparison)
+    const char* ver = getenv("MOE_ROUTER");   // 3: round 1's kernel (comparison); 6 / unset: v6
     if (ver && atoi(ver) == 3) return launch_router_v3(x, T, h, wr, ne, k, renorm, idx, gates, tile_counts, st);
     if (!ver || atoi(ver) == 6) {
-        // v6 buckets: N_e padded to NW * EPT; tokens per lane TPT (MOE_ROUTER_TPT = 1/2/4):
-        // few experts -> 1 token per lane (C1: latency-bound chains, as many warps as possible),
-        // many -> 4 (each router broadcast feeds 8 DFMAs)
-        int tpt = ne <= 8 ? 1 : (ne <= 16 ? 2 : 4);
+        // v6 buckets: N_e padded to NW * EPT; tokens per lane TPT (MOE_ROUTER_TPT = 1/2/4): the
+        // most tokens per lane (each router broadcast feeds 2 TPT DFMAs) that still leaves every
+        // SM a block -- below that the chains are latency-bound and want more warps instead
+        // (measured, profiles/r02/router: C1 4096 tokens TPT 1 80 us vs 2 133; C4 TPT 4 551 us
+        // vs 1 783; DBRX TPT 2 344 vs 1 449; 131k x 8 experts TPT 4 1005 vs 1 1375)
+        int sms = 148;
+        {
+            int dev = 0;
+            if (cudaGetDevice(&dev) == cudaSuccess)
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        }
+        int tpt = 4;
+        while (tpt > 1 && (T + kRouteTile * tpt - 1) / (kRouteTile * tpt) < sms) tpt >>= 1;
         if (const char* e = getenv("MOE_ROUTER_TPT")) {
             const int v = atoi(e);
             if (v == 1 || v == 2 || v == 4) tpt = v;
@@ -847,16 +757,17 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
 #define MOE_ROUTER6(E, P, N)                                                                 \
     do {                                                                                     \
         constexpr int cw_ = router_v6_cw(kRouteTile * P + N * E);                            \
-        const size_t dyn_ = sizeof(double) * std::max<size_t>(                               \
-            2 * (size_t)cw_ * (kRouteTile * P) + 2 * (size_t)cw_ * (N * E),                  \
-            (size_t)(kRouteTile * P) * (N * E));                                             \
+        const size_t dyn_ = std::max<size_t>(                                                \
+            (size_t)(16 + 2 * kRouterStages) * cw_ * (kRouteTile * P + N * E),               \
+            sizeof(double) * (size_t)(kRouteTile * P) * (N * E));                            \
         if (h % cw_) return cudaErrorInvalidValue;                                           \
-        err = cudaFuncSetAttribute(router_v6_kernel<E, P, N, cw_>,                           \
+        constexpr int pf_ = router_v6_prefetch(E, P);                                        \
+        err = cudaFuncSetAttribute(router_v6_kernel<E, P, N, cw_, pf_>,                      \
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_);  \
         if (err != cudaSuccess) return err;                                                  \
-        router_v6_kernel<E, P, N, cw_><<<blocks, N * 32, dyn_, st>>>(x, T, h, wr, ne, k,     \
-                                                                    renorm, idx, gates,      \
-                                                                    tile_counts);            \
+        router_v6_kernel<E, P, N, cw_, pf_><<<blocks, N * 32, dyn_, st>>>(x, T, h, wr, ne,   \
+                                                                         k, renorm, idx,     \
+                                                                         gates, tile_counts);\
     } while (0)
 #define MOE_ROUTER6_TPT(E, N)                                                                \
     do {                                                                                     \
@@ -864,7 +775,9 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
         else if (tpt == 2) MOE_ROUTER6(E, 2, N);                                             \
         else MOE_ROUTER6(E, 4, N);                                                           \
     } while (0)
-        if (ne <= 8) MOE_ROUTER6_TPT(2, 4);
+        const char* ev = getenv("MOE_ROUTER_EPT");
+        if (ne <= 8 && ev && atoi(ev) == 1) MOE_ROUTER6_TPT(1, 8);   // one chain per lane
+        else if (ne <= 8) MOE_ROUTER6_TPT(2, 4);
         else if (ne <= 16) MOE_ROUTER6_TPT(4, 4);
         else if (ne <= 32) MOE_ROUTER6_TPT(8, 4);
         else if (ne <= 64) MOE_ROUTER6_TPT(8, 8);
@@ -873,39 +786,7 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
 #undef MOE_ROUTER6
         return cudaGetLastError();
     }
-    // experts per warp: few experts -> 2 per warp (C1: 4 warps per 32 tokens, parallel chains
-    // on every SM); 16 -> 4; more -> 8 with two tokens per lane (every broadcast feeds 16 DFMAs)
-    int ept = ne <= 8 ? 2 : (ne <= 16 ? 4 : 8);
-    if (const char* e = getenv("MOE_ROUTER_EPT")) {   // experiments: 1, 2, 4 or 8
-        const int v = atoi(e);
-        if ((v == 1 || v == 2 || v == 4 || v == 8) && ((ne + v - 1) / v) * 32 <= 512) ept = v;
-    }
-    const int nw = (ne + ept - 1) / ept;
-    const int ne_pad = nw * ept;
-    int tpt = (ept == 8 && nw >= 3 && nw <= 8) ? 2 : 1;
-    if (const char* e = getenv("MOE_ROUTER_TPT")) tpt = atoi(e) == 2 ? 2 : 1;
-    const int ktok = kRouteTile * tpt;
-    int cw = 128;   // channels per staged chunk: 2 fp64 router chunks <= 32 KB, <= 4 vectors/thread
-    while (cw > 8 && (2 * cw * ne_pad > 4096 || cw * ept > 1024)) cw >>= 1;
-    const size_t wbytes = sizeof(double) * 2 * (size_t)cw * ne_pad;
-    const size_t xbytes = 2 * 2 * (size_t)ktok * (cw + 8);
-    const size_t dyn = std::max(wbytes + xbytes, sizeof(double) * (size_t)ktok * ne_pad);
-    const int blocks = (T + ktok - 1) / ktok;
-#define MOE_ROUTER5(E, P)                                                                    \
-    do {                                                                                     \
-        cudaError_t e_ = cudaFuncSetAttribute(router_v5_kernel<E, P>,                        \
-            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);                          \
-        if (e_ != cudaSuccess) return e_;                                                    \
-        router_v5_kernel<E, P><<<blocks, nw * 32, dyn, st>>>(x, T, h, wr, ne, k, renorm, cw,  \
-                                                             idx, gates, tile_counts);       \
-    } while (0)
-    if (ept == 1) { if (tpt == 2) MOE_ROUTER5(1, 2); else MOE_ROUTER5(1, 1); }
-    else if (ept == 2) { if (tpt == 2) MOE_ROUTER5(2, 2); else MOE_ROUTER5(2, 1); }
-    else if (ept == 4) { if (tpt == 2) MOE_ROUTER5(4, 2); else MOE_ROUTER5(4, 1); }
-    else if (tpt == 2) MOE_ROUTER5(8, 2);
-    else MOE_ROUTER5(8, 1);
-#undef MOE_ROUTER5
-    return cudaGetLastError();
+    return cudaErrorInvalidValue;   // MOE_ROUTER=<unknown>
 }
 
 cudaError_t launch_scan(const int32_t* tile_counts, int n_tiles, int ne, int T, int k,
@@ -934,7 +815,8 @@ cudaError_t launch_combine(const __nv_bfloat16* y_perm, const int32_t* pos, cons
                            int shard_t0, cudaStream_t st) {
     if (T == 0) return cudaSuccess;
     if (shard_t0 >= 0 && !pr) return cudaErrorInvalidValue;
-    combine_kernel<<<(T + 7) / 8, 256, 0, st>>>(y_perm, pos, gates, T, h, k, num_shared,
+    const int64_t warps = (int64_t)T * ((h / 8 + 31) / 32);   // one per (token, 256 columns)
+    combine_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(y_perm, pos, gates, T, h, k, num_shared,
                                                 shared_base, shared_stride, resid, out, idx,
                                                 offsets, pr, shard_t0);
     return cudaGetLastError();

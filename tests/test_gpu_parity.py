@@ -352,14 +352,14 @@ def test_experts_per_gemm_launch(rows, copy_group, launches, monkeypatch):
         run.close()
 
 
-@pytest.mark.parametrize("variant", ["v3-1", "v3-2", "v3-4", "v3-8", "v5-2", "v5-8-tpt1",
-                                     "v6-0-tpt1", "v6-0-tpt2", "v6-0-tpt4"])
+@pytest.mark.parametrize("variant", ["v3-1", "v3-2", "v3-4", "v3-8",
+                                     "v6-0-tpt1", "v6-0-tpt2", "v6-0-tpt4", "v6-1-tpt1", "v6-1-tpt2"])
 @pytest.mark.parametrize("ne,k", [(5, 2), (8, 2), (16, 4), (40, 6), (128, 8)])
 def test_router_experts_per_warp_variants(ne, k, variant, monkeypatch):
-    """Every router kernel instantiation -- round 1's router_topk_kernel<EPT> (MOE_ROUTER=3),
-    router_v5_kernel<EPT, TPT> (MOE_ROUTER=5) and router_v6_kernel<EPT, TPT, NW, CW> (default;
-    every N_e bucket x MOE_ROUTER_TPT = 1 / 2 / 4) -- gives the same bit-exact selection and gates
-    as the oracle (one fp64 FMA chain per logit, ascending channels, in every kernel)."""
+    """Every router kernel instantiation -- round 1's router_topk_kernel<EPT> (MOE_ROUTER=3) and
+    router_v6_kernel<EPT, TPT, NW, CW, PF> (default; every N_e bucket x MOE_ROUTER_TPT = 1 / 2 / 4,
+    one chain per lane with MOE_ROUTER_EPT=1) -- gives the same bit-exact selection and gates as
+    the oracle (one fp64 FMA chain per logit, ascending channels, in every kernel)."""
     ver, ept, *rest = variant.split("-")
     if ne == 128 and ver != "v6":
         pytest.skip("128 experts: v6 buckets only")

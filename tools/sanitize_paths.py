@@ -1,6 +1,7 @@
 """Small runs of every engine path for compute-sanitizer (memcheck / racecheck / synccheck):
 tiny MoE layer, GPU Task B, grouped launches over many small experts, the CTA-pair kernel with
-several raster groups, in-process P2P expert parallelism (W = 2), both GEMM kernels with
+several raster groups, in-process P2P expert parallelism (W = 2; W = 4 with sharded shared
+experts), both GEMM kernels with
 several experts per launch, and the Contiguous Data Mover."""
 import os, sys, threading
 sys.path.insert(0, "."); sys.path.insert(0, "tests")
@@ -53,6 +54,32 @@ def work(q):
     for _ in range(2):
         ly[q].forward(x, full.router, ex[q], o, stream=s.cuda_stream)
     s.synchronize()
+th = [threading.Thread(target=work, args=(q,)) for q in range(W)]
+[t.start() for t in th]; [t.join(300) for t in th]
+for l in ly: l.close()
+for e in ex: e.close()
+full.close()
+# 4b. sharded shared experts (MOE_FLAG_SHARD_SHARED) over the same transport, W = 4: two ranks
+# serve a slice, two serve none
+from paper_2504_09345_b200 import shared_slice_weights
+W = 4
+cfg = synth.MoEConfig("custom", 26, 256, 256, 8, 2, 200, 1)
+inp = synth.gen_inputs(cfg)
+full = GpuRun(inp)
+nl, S, T, ne = cfg.num_experts // W, cfg.num_shared, cfg.tokens, cfg.num_experts
+bounds = [T * q // W for q in range(W + 1)]
+key = os.urandom(128)
+ex, ly, bufs = [], [], []
+for q in range(W):
+    ids = list(range(q * nl, (q + 1) * nl))
+    sl = shared_slice_weights(cfg.ffn, inp.w1[ne:], inp.w3[ne:], inp.w2[ne:], W, q)
+    ex.append(HostExperts(cfg.hidden, cfg.ffn, [inp.w1[i] for i in ids], [inp.w3[i] for i in ids],
+                          [inp.w2[i] for i in ids], slice_=sl))
+    ly.append(MoELayer(cfg.hidden, cfg.ffn, ne, cfg.top_k, max(1, -(-T // W)), num_shared=S,
+                       world_size=W, rank=q, nccl_unique_id=key, local_ep=True, shard_shared=True))
+    x = bf16_tensor(inp.x[bounds[q]:bounds[q + 1]])
+    bufs.append((torch.cuda.Stream(), x, torch.empty_like(x)))
+torch.cuda.synchronize()
 th = [threading.Thread(target=work, args=(q,)) for q in range(W)]
 [t.start() for t in th]; [t.join(300) for t in th]
 for l in ly: l.close()
