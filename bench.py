@@ -528,7 +528,7 @@ def run_ours(args):
         tj = json.load(open(tp))
         key = cfg.name + ("@%d" % T if args.tokens else "")
         traffic = tj.get(key, {}).get("gemm1_dram_bytes_per_launch")
-        traffic_src = tj.get(key, {}).get("source", tj.get("source"))
+        traffic_src = tj.get(key, {}).get("source", tj.get("source")) if traffic else None
     # Peak: the BURST cuBLAS figure.  The kernel runs inside a long step, but the step is
     # host-link bound and the GPU idles between expert GEMMs (~0.2-ms bursts, nvidia-smi sees
     # boost clock, `clocks`), so the burst peak is the conservative denominator; the sustained-peak
@@ -581,6 +581,36 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         tok_bytes = T * cfg.hidden * 2
+        # The e2e step also moves its result device -> host while weights and the next tokens
+        # stream in; on a shared host the two directions interfere.  Duplex probe: 1 GB H2D
+        # with a concurrent D2H of the step's D2H : H2D ratio, best of 3 (CUDA events on the
+        # H2D stream) -- the link bandwidth the e2e step can have.
+        h2d_step = tok_bytes / world + step_weight_bytes / world
+        ratio = (tok_bytes / world) / max(1.0, h2d_step)
+        nb = 1 << 30
+        hsrc = torch.empty(nb, dtype=torch.uint8).pin_memory()
+        dbuf = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        nd = max(1 << 20, int(nb * ratio)) & ~15
+        dsrc = torch.empty(nd, dtype=torch.uint8, device="cuda")
+        hdst = torch.empty(nd, dtype=torch.uint8).pin_memory()
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        duplex = 0.0
+        for _ in range(3):
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(s_out):
+                hdst.copy_(dsrc, non_blocking=True)
+            with torch.cuda.stream(s_in):
+                a.record(s_in)
+                dbuf.copy_(hsrc, non_blocking=True)
+                b.record(s_in)
+            torch.cuda.synchronize()
+            duplex = max(duplex, nb / (a.elapsed_time(b) * 1e-3) / 1e9)
+        del hsrc, dbuf, dsrc, hdst
+        duplex = -allmax(-duplex)
+        e2e_ideal_ms = h2d_step / (duplex * 1e9) * 1e3
         e2e = {"value": T / (ems / 1e3), "unit": "tokens/s", "ms_per_step": ems,
                "h2d_bytes_per_step": tok_bytes + step_weight_bytes,
                "h2d_token_bytes_per_step": tok_bytes, "h2d_weight_bytes_per_step": step_weight_bytes,
@@ -598,7 +628,12 @@ def run_ours(args):
                                      for p in range(2)],
                    "copies": est["part_copies"],
                    "note": "enqueue -> resident of each host token copy (partition 1 = beta)"},
-               "matches_device_path": e2e_match}
+               "matches_device_path": e2e_match,
+               "link_roofline": {"h2d_gbs_duplex_probe": duplex, "d2h_to_h2d_ratio": ratio,
+                                 "ideal_ms_per_step": e2e_ideal_ms,
+                                 "frac": e2e_ideal_ms / ems,
+                                 "note": "H2D bytes per rank / the H2D bandwidth measured with the "
+                                         "step's share of D2H running concurrently"}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:   # the oracle baseline: N = 1 only

@@ -594,35 +594,37 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int h, int k, int ne,
     if (pr) __threadfence_system();   // peer stores performed before the dispatch flag release
 }
 
-// Warp per (token, 256-column chunk); lane = 8 consecutive columns (one 16-byte vector).  Every
-// lane issues its k row loads (+ shared / residual rows) back to back: one vector per lane keeps
-// the most loads in flight per SM (a warp per whole token row held only ~28 KB in flight per SM
-// at C1's 4096 tokens -- 0.66 of HBM bandwidth in ncu).
+// Warp per (token, 1/split of its row); lane = 8 consecutive columns per 16-byte vector, two
+// vectors per iteration with all their row loads issued first.  split (host) makes >= ~8k warps
+// so small calls still keep enough loads in flight (C1: 4096 tokens -> half rows); a warp per
+// 256 columns was measured slower at C1 (32 vs 23 us: each warp paid the pos -> row dependent
+// round trips for a single vector per lane).
+template <int K>   // top_k (compile time: the row loads of a batch sit in K * 2 registers x4)
 __global__ void __launch_bounds__(256)
 combine_kernel(const __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ pos,
-               const float* __restrict__ gates, int T, int h, int k, int num_shared,
+               const float* __restrict__ gates, int T, int h, int num_shared,
                int64_t shared_base, int64_t shared_stride, const __nv_bfloat16* __restrict__ resid,
                __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ idx,
                const int32_t* __restrict__ offsets, const PeerRows* __restrict__ pr,
-               int shard_t0) {
+               int shard_t0, int split) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nvec = h / 8;
-    const int cpt = (nvec + 31) / 32;   // 256-column chunks per token
     const int64_t gw = (int64_t)blockIdx.x * 8 + warp;
-    const int t = (int)(gw / cpt);
-    const int v = (int)(gw % cpt) * 32 + lane;
-    if (t >= T || v >= nvec) return;
-    const __nv_bfloat16* prow[kMaxTopK];
-    float g[kMaxTopK];
+    const int t = (int)(gw / split);
+    if (t >= T) return;
+    const int per = nvec / split;               // vectors of this warp's part of the row
+    const int v0 = (int)(gw % split) * per;
+    const __nv_bfloat16* prow[K];
+    float g[K];
 #pragma unroll
-    for (int j = 0; j < kMaxTopK; ++j) {
+    for (int j = 0; j < K; ++j) {
         prow[j] = y;
         g[j] = 0.f;
-        if (j < k) {
-            const int p = pos[(size_t)t * k + j];
-            g[j] = gates[(size_t)t * k + j];
+        {
+            const int p = pos[(size_t)t * K + j];
+            g[j] = gates[(size_t)t * K + j];
             if (pr) {   // the expert owner's y_recv (P2P combine)
-                const int e = idx[(size_t)t * k + j];
+                const int e = idx[(size_t)t * K + j];
                 const int b = pr->base[e];
                 if (b < 0) {   // the plan refused the exchange (overflow): contributes nothing
                     prow[j] = y;
@@ -635,50 +637,61 @@ combine_kernel(const __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ 
             }
         }
     }
-    {
-        int4 raw[kMaxTopK];
+    constexpr int U = 2;
+    for (int vb = v0 + lane; vb < v0 + per; vb += 32 * U) {
+        int4 raw[U][K];
 #pragma unroll
-        for (int j = 0; j < kMaxTopK; ++j)
-            if (j < k) raw[j] = ptx::ld_nc_v4(reinterpret_cast<const int4*>(prow[j]) + v);
-        float acc[8];
+        for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+            for (int j = 0; j < K; ++j)
+                if (vb + 32 * u < v0 + per)
+                    raw[u][j] = ptx::ld_nc_v4(reinterpret_cast<const int4*>(prow[j]) + vb + 32 * u);
 #pragma unroll
-        for (int j = 0; j < kMaxTopK; ++j) {   // fixed j order (R10)
-            if (j < k) {
-                const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&raw[j]);
+        for (int u = 0; u < U; ++u) {
+            const int v = vb + 32 * u;
+            if (v >= v0 + per) break;
+            float acc[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+#pragma unroll
+            for (int j = 0; j < K; ++j) {   // fixed j order (R10)
+                {
+                    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&raw[u][j]);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const float2 f = __bfloat1622float2(b[i]);
+                        acc[2 * i] = fmaf(g[j], f.x, acc[2 * i]);
+                        acc[2 * i + 1] = fmaf(g[j], f.y, acc[2 * i + 1]);
+                    }
+                }
+            }
+            // weight-1 rows after the routed terms, in call order: shared experts (or their
+            // sharded partial rows, rank order), then Task B's residual
+            auto add_row = [&](const __nv_bfloat16* row) {
+                const int4 r = ptx::ld_nc_v4(reinterpret_cast<const int4*>(row) + v);
+                const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&r);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const float2 f = __bfloat1622float2(b[i]);
-                    acc[2 * i] = fmaf(g[j], f.x, acc[2 * i]);
-                    acc[2 * i + 1] = fmaf(g[j], f.y, acc[2 * i + 1]);
+                    acc[2 * i] += f.x;
+                    acc[2 * i + 1] += f.y;
                 }
+            };
+            if (shard_t0 >= 0) {
+                for (uint32_t m = pr->shard_mask; m; m &= m - 1)
+                    add_row(pr->rows[__ffs(m) - 1] + (size_t)(pr->shard_row + shard_t0 + t) * h);
+            } else {
+                for (int s2 = 0; s2 < num_shared; ++s2)
+                    add_row(y + (size_t)(shared_base + (int64_t)s2 * shared_stride + t) * h);
             }
+            if (resid) add_row(resid + (size_t)t * h);
+            int4 o;
+            o.x = (int)ptx::pack_bf16x2(acc[0], acc[1]);
+            o.y = (int)ptx::pack_bf16x2(acc[2], acc[3]);
+            o.z = (int)ptx::pack_bf16x2(acc[4], acc[5]);
+            o.w = (int)ptx::pack_bf16x2(acc[6], acc[7]);
+            reinterpret_cast<int4*>(out + (size_t)t * h)[v] = o;
         }
-        auto add_row = [&](const __nv_bfloat16* row) {   // weight-1 terms, in call order
-            const int4 r = ptx::ld_nc_v4(reinterpret_cast<const int4*>(row) + v);
-            const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&r);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const float2 f = __bfloat1622float2(b[i]);
-                acc[2 * i] += f.x;
-                acc[2 * i + 1] += f.y;
-            }
-        };
-        if (shard_t0 >= 0) {   // sharded shared experts: the owners' partial rows, rank order
-            for (uint32_t m = pr->shard_mask; m; m &= m - 1)
-                add_row(pr->rows[__ffs(m) - 1] + (size_t)(pr->shard_row + shard_t0 + t) * h);
-        } else {
-            for (int s = 0; s < num_shared; ++s)
-                add_row(y + (size_t)(shared_base + (int64_t)s * shared_stride + t) * h);
-        }
-        if (resid) add_row(resid + (size_t)t * h);   // Task B: the block's residual connection
-        int4 o;
-        o.x = (int)ptx::pack_bf16x2(acc[0], acc[1]);
-        o.y = (int)ptx::pack_bf16x2(acc[2], acc[3]);
-        o.z = (int)ptx::pack_bf16x2(acc[4], acc[5]);
-        o.w = (int)ptx::pack_bf16x2(acc[6], acc[7]);
-        reinterpret_cast<int4*>(out + (size_t)t * h)[v] = o;
     }
 }
 
@@ -815,10 +828,27 @@ cudaError_t launch_combine(const __nv_bfloat16* y_perm, const int32_t* pos, cons
                            int shard_t0, cudaStream_t st) {
     if (T == 0) return cudaSuccess;
     if (shard_t0 >= 0 && !pr) return cudaErrorInvalidValue;
-    const int64_t warps = (int64_t)T * ((h / 8 + 31) / 32);   // one per (token, 256 columns)
-    combine_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(y_perm, pos, gates, T, h, k, num_shared,
-                                                shared_base, shared_stride, resid, out, idx,
-                                                offsets, pr, shard_t0);
+    // parts per row: >= ~8k warps in flight, each part a multiple of 32 vectors
+    int split = 1;
+    while (split < 8 && (int64_t)T * split < 8192 && (h / 8) % (64 * split) == 0) split *= 2;
+    const int64_t warps = (int64_t)T * split;
+    const unsigned blocks = (unsigned)((warps + 7) / 8);
+#define MOE_COMBINE(KK)                                                                      \
+    combine_kernel<KK><<<blocks, 256, 0, st>>>(y_perm, pos, gates, T, h, num_shared,         \
+                                               shared_base, shared_stride, resid, out, idx,  \
+                                               offsets, pr, shard_t0, split)
+    switch (k) {
+        case 1: MOE_COMBINE(1); break;
+        case 2: MOE_COMBINE(2); break;
+        case 3: MOE_COMBINE(3); break;
+        case 4: MOE_COMBINE(4); break;
+        case 5: MOE_COMBINE(5); break;
+        case 6: MOE_COMBINE(6); break;
+        case 7: MOE_COMBINE(7); break;
+        case 8: MOE_COMBINE(8); break;
+        default: return cudaErrorInvalidValue;
+    }
+#undef MOE_COMBINE
     return cudaGetLastError();
 }
 

@@ -174,12 +174,13 @@ def validate_against_profiler(prof: Dict) -> Dict:
 def predict_expert_parallel(hidden: int, ffn: int, num_experts: int, top_k: int,
                             num_shared: int, tokens: int, world: int, link_gbs: float,
                             host_dram_gbs: float, tensor_tflops: float,
-                            gemm_efficiency: float = 0.8, nvlink_gbs: float = 900.0) -> Dict:
+                            gemm_efficiency: float = 0.8, nvlink_gbs: float = 900.0,
+                            shard_shared: bool = False) -> Dict:
     """Predicted step time / tokens per second of ONE streamed MoE layer under expert
     parallelism over `world` GPUs of one box (BASELINE.json's 1/2/4/8 B200s).
 
-    Each rank streams its N_e / W routed experts plus the replicated shared ones over its own
-    host link; all W links draw on one host's DRAM at once (Eq. 5's logic: host
+    Each rank streams its N_e / W routed experts plus the replicated shared ones (or, with
+    shard_shared, its column slice of them) over its own host link; all W links draw on one host's DRAM at once (Eq. 5's logic: host
     memory must feed every stream), so a link delivers min(link, host_dram / W).  Each rank's
     expert GEMMs do 1/W of the layer's FLOPs (plus its own shared-expert work), at
     `gemm_efficiency` of the tensor peak; the token exchange (dispatch + combine, bf16 rows, the
@@ -188,7 +189,13 @@ def predict_expert_parallel(hidden: int, ffn: int, num_experts: int, top_k: int,
     if world < 1 or num_experts % world:
         raise ValueError("world must divide num_experts")
     eb = ledger.expert_bytes(hidden, ffn)
-    rank_bytes = (num_experts // world + num_shared) * eb
+    if shard_shared and world > 1 and num_shared:
+        # MOE_FLAG_SHARD_SHARED: the slowest rank holds ceil(B / W) of the B = S h_i / 128
+        # column blocks of the concatenated shared FFN (include/moe.h, moe_shared_slice)
+        blocks = num_shared * ffn // 128
+        rank_bytes = (num_experts // world) * eb + -(-blocks // world) * 128 * 6 * hidden
+    else:
+        rank_bytes = (num_experts // world + num_shared) * eb
     per_link = min(link_gbs, host_dram_gbs / world)
     t_link = rank_bytes / (per_link * 1e9)
     flops = 6.0 * hidden * ffn * tokens * (top_k / world + num_shared / world)

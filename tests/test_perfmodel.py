@@ -198,3 +198,21 @@ def test_expert_parallel_prediction_closed_forms():
     assert c4["rank_weight_bytes"] == 10 * 6 * 2048 * 1408
     with pytest.raises(ValueError):
         pm.predict_expert_parallel(world=3, host_dram_gbs=1e9, **kw)
+
+
+def test_expert_parallel_sharded_shared_bytes():
+    """MOE_FLAG_SHARD_SHARED: the slowest rank streams its N_e/W routed experts plus ceil(B/W)
+    128-column blocks of the concatenated shared FFN (C4 at W = 8: 22 blocks -> 3 on the
+    slowest rank) instead of both shared experts."""
+    from paper_2504_09345_b200 import ledger
+    h, hi = 2048, 1408
+    eb = ledger.expert_bytes(h, hi)
+    rep = pm.predict_expert_parallel(h, hi, 64, 6, 2, 32768, 8, 55.6, 1e9, 1361.0)
+    shd = pm.predict_expert_parallel(h, hi, 64, 6, 2, 32768, 8, 55.6, 1e9, 1361.0,
+                                            shard_shared=True)
+    assert rep["rank_weight_bytes"] == 10 * eb
+    assert shd["rank_weight_bytes"] == 8 * eb + 3 * 128 * 6 * h
+    # W = 1 is unaffected by the flag
+    one = pm.predict_expert_parallel(h, hi, 64, 6, 2, 32768, 1, 55.6, 1e9, 1361.0,
+                                            shard_shared=True)
+    assert one["rank_weight_bytes"] == 66 * eb
