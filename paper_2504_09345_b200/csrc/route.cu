@@ -300,8 +300,7 @@ constexpr int router_v6_cw(int rows) {
 // 4 max(EPT, 2) per pair), at least 1.
 constexpr int router_v6_prefetch(int ept, int tpt) {
     const int per = 4 * tpt + 4 * (ept >= 2 ? ept : 2);
-    const int d = 48 / per;
-    return d < 1 ? 1 : (d > 4 ? 4 : d);
+    return 48 / per >= 4 ? 4 : (48 / per >= 2 ? 2 : 1);   // a power of two: divides CW / 2
 }
 
 template <int EPT, int TPT, int NW, int CW, int kPf>
@@ -411,34 +410,32 @@ router_v6_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
             }
         };
 #pragma unroll
-        for (int c2 = 0; c2 < kPf && c2 < CW / 2; ++c2) fetch(c2, c2);
+        for (int j = 0; j < kPf; ++j) fetch(j, j);
+        // pairs c2 + j live in slot j: consumed, then refilled with pair c2 + j + kPf; fully
+        // unrolled, so the slots are static registers (no rotation copies: a rotating prefetch
+        // cost ~6 moves per channel) and the refill bound is resolved at compile time (a rolled
+        // loop was measured slower: C1 90 vs 80 us)
 #pragma unroll
-        for (int c2 = 0; c2 < CW / 2; ++c2) {
-            const int slot = c2 % kPf;
-            double2 xc[TPT];
-            double2 wc[2][kWP];
+        for (int c2 = 0; c2 < CW / 2; c2 += kPf) {
 #pragma unroll
-            for (int p = 0; p < TPT; ++p) xc[p] = xv[slot][p];
+            for (int j = 0; j < kPf; ++j) {
 #pragma unroll
-            for (int q = 0; q < 2; ++q)
+                for (int q = 0; q < 2; ++q) {   // channel 2*(c2+j) + q: ascending in every chain
 #pragma unroll
-                for (int i = 0; i < kWP; ++i) wc[q][i] = wv[slot][q][i];
-            if (c2 + kPf < CW / 2) fetch(c2 + kPf, slot);
+                    for (int i = 0; i < kWP; ++i) {
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {   // channel 2*c2 + q: ascending order in every chain
-#pragma unroll
-                for (int i = 0; i < kWP; ++i) {
-#pragma unroll
-                    for (int p = 0; p < TPT; ++p) {
-                        const double xq = q ? xc[p].y : xc[p].x;
-                        if constexpr (EPT == 1) {
-                            acc[p][0] = fma(xq, wc[q][0].x, acc[p][0]);
-                        } else {
-                            acc[p][2 * i] = fma(xq, wc[q][i].x, acc[p][2 * i]);
-                            acc[p][2 * i + 1] = fma(xq, wc[q][i].y, acc[p][2 * i + 1]);
+                        for (int p = 0; p < TPT; ++p) {
+                            const double xq = q ? xv[j][p].y : xv[j][p].x;
+                            if constexpr (EPT == 1) {
+                                acc[p][0] = fma(xq, wv[j][q][0].x, acc[p][0]);
+                            } else {
+                                acc[p][2 * i] = fma(xq, wv[j][q][i].x, acc[p][2 * i]);
+                                acc[p][2 * i + 1] = fma(xq, wv[j][q][i].y, acc[p][2 * i + 1]);
+                            }
                         }
                     }
                 }
+                if (c2 + j + kPf < CW / 2) fetch(c2 + j + kPf, j);
             }
         }
         if (ch + 1 < n_chunks) {   // fp64 buffer b ^ 1 was consumed before the last barrier
