@@ -58,10 +58,11 @@ int main(int argc, char** argv) {
     size_t bad = 0;
     for (size_t i = 0; i < a.size(); ++i) bad += (a[i] != b[i]) || (memcmp(&ga[i], &gb[i], 4) != 0);
     const double dfma = (double)T * ne * h;
-    printf("router T=%d h=%d N_e=%d k=%d [MOE_ROUTER=%s EPT=%s TPT=%s]: %.1f us  %.2f TFLOP/s fp64 (%s; %zu of %zu idx/gates differ from v3)\n",
+    printf("router T=%d h=%d N_e=%d k=%d [MOE_ROUTER=%s EPT=%s TPT=%s LANES=%s]: %.1f us  %.2f TFLOP/s fp64 (%s; %zu of %zu idx/gates differ from v3)\n",
            T, h, ne, k, getenv("MOE_ROUTER") ? getenv("MOE_ROUTER") : "6",
            getenv("MOE_ROUTER_EPT") ? getenv("MOE_ROUTER_EPT") : "auto",
-           getenv("MOE_ROUTER_TPT") ? getenv("MOE_ROUTER_TPT") : "auto", 1e3 * ms / iters,
+           getenv("MOE_ROUTER_TPT") ? getenv("MOE_ROUTER_TPT") : "auto",
+           getenv("MOE_ROUTER_LANES") ? getenv("MOE_ROUTER_LANES") : "auto", 1e3 * ms / iters,
            2 * dfma / (ms / iters * 1e-3) / 1e12, cudaGetErrorString(err), bad, a.size());
     return 0;
 }
