@@ -66,6 +66,16 @@ def test_ragged_shapes_parity(shape):
     run.close()
 
 
+@pytest.mark.parametrize("k", range(1, 9))
+def test_every_top_k(k):
+    """Every top_k the envelope allows (1..8): the combine kernel is instantiated per top_k
+    (combine_kernel<K>), the router's top-k loop and the scan / permute run k rows per token;
+    all tokens compared, with shared experts and a ragged token count."""
+    run, *_ = _check_full(synth.gen_inputs(synth.MoEConfig("custom", 30 + k, 256, 384,
+                                                           max(8, k + 3), k, 333, 1)))
+    run.close()
+
+
 def test_full_softmax_gates_mode():
     inp = synth.gen_inputs(synth.MoEConfig("custom", 8, 256, 256, 8, 2, 200))
     run, *_ = _check_full(inp, renormalize=False)
