@@ -78,6 +78,40 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
+def spread_devices(world: int):
+    """The W GPUs a run uses when it has fewer ranks than the box has GPUs (spread
+    W = 2 / 4 over PCIe switches and sockets, so ranks do not share a host uplink): greedy --
+    GPU 0 first, then repeatedly the GPU whose closest already-chosen GPU is topologically
+    farthest (NVML common-ancestor level: system > NUMA node > host bridge > PCIe switches), ties
+    to the lowest index.  Deterministic, so every rank computes the same list.  Identity when
+    every visible GPU is used, NVML is missing, or MOE_BENCH_SPREAD=0."""
+    import torch
+    n = torch.cuda.device_count()
+    if world >= n or os.environ.get("MOE_BENCH_SPREAD") == "0":
+        return list(range(world)), "identity"
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        hs = []
+        for d in range(n):
+            p = torch.cuda.get_device_properties(d)
+            busid = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            hs.append(pynvml.nvmlDeviceGetHandleByPciBusId(busid))
+        chosen = [0]
+        while len(chosen) < world:
+            best, best_lvl = None, -1
+            for d in range(n):
+                if d in chosen:
+                    continue
+                lvl = min(pynvml.nvmlDeviceGetTopologyCommonAncestor(hs[d], hs[c]) for c in chosen)
+                if lvl > best_lvl:
+                    best, best_lvl = d, lvl
+            chosen.append(best)
+        return sorted(chosen), "nvml topology spread"
+    except Exception as e:  # noqa: BLE001 -- fall back to a stride over the visible GPUs
+        return [r * (n // world) for r in range(world)], f"stride ({str(e)[:60]})"
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -246,8 +280,12 @@ def run_ours(args):
     # gloo group for the bench's own plumbing -- exercises the N > 1 code path on a 1-GPU box
     # with the P2P transport (NCCL refuses two ranks on one GPU).
     share = os.environ.get("MOE_BENCH_SHARE_GPU") == "1"
+    placement = "shared GPU 0 (path check)" if share else "identity"
     if share:
         local = 0
+    elif world > 1 and int(os.environ.get("LOCAL_WORLD_SIZE", world)) == world:
+        devs, placement = spread_devices(world)   # single node: spread the ranks' GPUs
+        local = devs[local]
     torch.cuda.set_device(local)
     if world > 1:
         if share:
@@ -673,6 +711,7 @@ def run_ours(args):
                        "packet_mb": args.packet_mb, "mover": bool(args.mover),
                        "l2": "inputs larger than L2: all expert weights re-streamed from host each step",
                        "parallelism": f"ep{world}", "ep_transport": transport,
+                       "gpu_placement": placement,
                        "ep_comm_nranks": comm_nranks},
             "ms_per_step_profile_pass": ms_prof,
             "roofline": roofline, "roofline_step": roofline_step,
