@@ -371,18 +371,31 @@ def run_ours(args):
                   packet_bytes=int(args.packet_mb * 2 ** 20), mover=args.mover, world_size=world,
                   rank=rank, num_slots=args.slots, shard_shared=shard)
         if transport == "p2p":   # CUDA IPC peer mapping; every rank must succeed, else NCCL
+            # Every rank reaches the same collectives whatever fails locally (a rank that cannot
+            # build its context still joins the handle exchange with None), so a local failure
+            # never leaves the others waiting in a collective it skipped.
+            err, hnd = None, None
             try:
                 layer = moe.MoELayer(cfg.hidden, cfg.ffn, cfg.num_experts, cfg.top_k, Tr,
                                      ipc_ep=True, **mk)
-                handles = [None] * world
-                dist.all_gather_object(handles, layer.ipc_handle())
-                layer.ipc_connect(handles)
-                layer.ipc_selftest(5.0)   # flags + rows through the mapping, before trusting it
-                ok = 1.0
-            except Exception as e:  # noqa: BLE001 -- reported, then the NCCL transport
-                print(f"[bench] rank {rank}: P2P transport unavailable ({e}); using NCCL",
+                hnd = layer.ipc_handle()
+            except Exception as e:  # noqa: BLE001 -- reported below, then the NCCL transport
+                err = e
+            handles = [None] * world
+            dist.all_gather_object(handles, hnd)
+            ok = 0.0
+            if err is None and all(x is not None for x in handles):
+                try:
+                    layer.ipc_connect(handles)
+                    layer.ipc_selftest(5.0)   # flags + rows through the mapping (peers time out
+                    ok = 1.0                  # instead of hanging if one rank could not connect)
+                except Exception as e:  # noqa: BLE001
+                    err = e
+            elif err is None:
+                err = RuntimeError("a peer could not build its IPC context")
+            if err is not None:
+                print(f"[bench] rank {rank}: P2P transport unavailable ({err}); using NCCL",
                       file=sys.stderr, flush=True)
-                ok = 0.0
             if allmax(1.0 - ok) > 0:
                 if layer is not None:
                     layer.close()

@@ -60,14 +60,13 @@ struct moe_ctx_s {
     int s_items = 0;       // shared items streamed per call: num_shared, or 0/1 (sharded)
     // MOE_FLAG_SHARD_SHARED: this rank streams one slice of the concatenated
     // shared FFN, shard_w columns wide (0 = none), run over every rank's tokens.  Its W2 part
-    // ([h, shard_w]) is read through tm_w2s*, a view of the staging buffer with shard_w columns
-    // per row (slot s = rows [s * slice_slot_rows, ...)).
+    // ([h, shard_w]) is read through tm_w2s*[s], a view of slot s's W2 part with shard_w columns
+    // per row (any width: no divisibility of the slot by the row pitch is needed).
     bool shard = false;
     int shard_w = 0;
     uint32_t shard_mask = 0;          // ranks whose slice is not empty
     int64_t slice_bytes = 0;
-    int64_t slice_slot_rows = 0;
-    CUtensorMap tm_w2s, tm_w2s_pair;
+    CUtensorMap tm_w2s[moe::kMaxSlots], tm_w2s_pair[moe::kMaxSlots];
     int64_t blob_bytes = 0, w13_bytes = 0;
     int num_sms = 148;
     int bn1 = 256, bn2 = 256;

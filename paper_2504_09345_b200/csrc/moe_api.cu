@@ -117,15 +117,14 @@ moe_status check_cfg(const moe_config* cfg) {
     int s_items = cfg->num_shared;
     if (cfg->flags & MOE_FLAG_SHARD_SHARED) {
         // P2P transport only (the gather / partial sums ride the peer-memory permute / combine);
-        // a slice must fit one expert slot (S <= W) and the slot must hold whole rows of the
-        // slice's W2 view (tm_w2s); the mover's packets assume one blob size
+        // a slice must fit one expert slot (S <= W: at most ceil(S h_i / 128 / W) <= h_i / 128
+        // blocks); the mover's packets assume one blob size
         if (cfg->world_size < 2 || !(cfg->flags & (MOE_FLAG_LOCAL_EP | MOE_FLAG_IPC_EP)) ||
             cfg->num_shared < 1 || cfg->num_shared > cfg->world_size ||
             (cfg->flags & MOE_FLAG_MOVER))
             return MOE_E_UNSUPPORTED;
         int c0 = 0, w = 0;
         shared_slice_cols(cfg->ffn, cfg->num_shared, cfg->world_size, cfg->rank, &c0, &w);
-        if (w > 0 && (3ll * cfg->hidden * cfg->ffn) % w) return MOE_E_UNSUPPORTED;
         s_items = w > 0 ? 1 : 0;
     }
     if (cfg->num_slots > 2 && cfg->num_slots >= cfg->num_experts / cfg->world_size + s_items)
@@ -432,7 +431,7 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
             if (!c->mover) MOE_CUDA(c, cudaStreamWaitEvent(st, c->ready13[sj], 0));
             b1.idx[j] = b2.idx[j] = e;
             b1.b_row[j] = 3 * hi * sj;           // W13 of slot sj in tm_w13*
-            b2.b_row[j] = slice ? (int32_t)(c->slice_slot_rows * sj + 2 * h)   // in tm_w2s*
+            b2.b_row[j] = slice ? 0                        // tm_w2s*[sj] starts at the W2 part
                                 : 3 * h * sj + 2 * h;    // W2 of slot sj in tm_w2*
             rows[j] = slice ? (int64_t)T * cf.world_size : shared ? (int64_t)T : exp_routed;
         }
@@ -455,8 +454,9 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
         {
             Prof p(c, moe::kRecGemm2, st);
             moe_status gs = launch_grouped(c, moe::kGemmPlain, c->bn2, rows, !shared, &c->tm_h,
-                                           slice ? &c->tm_w2s : &c->tm_w2,
-                                           slice ? &c->tm_w2s_pair : &c->tm_w2_pair, b2, h,
+                                           slice ? &c->tm_w2s[q % (uint64_t)ns] : &c->tm_w2,
+                                           slice ? &c->tm_w2s_pair[q % (uint64_t)ns] : &c->tm_w2_pair,
+                                           b2, h,
                                            slice ? c->shard_w : hi,
                                            slice ? c->y_recv : shared ? c->y_perm : y_routed, h,
                                            st);
@@ -932,7 +932,6 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
         }
         c->s_items = c->shard_w > 0 ? 1 : 0;
         c->slice_bytes = c->shard_w > 0 ? moe_packed_expert_bytes(h, c->shard_w) : 0;
-        c->slice_slot_rows = c->shard_w > 0 ? 3ll * h * hi / c->shard_w : 0;
     }
     c->n_all = c->n_local + c->s_items;
     c->w13_bytes = 4ll * h * hi;
@@ -1028,10 +1027,12 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
         tm &= moe::make_tmap(&c->tm_w13_pair, c->slot_base, r13, h, 128);
         tm &= moe::make_tmap(&c->tm_w2, c->slot_base, r2, hi, (uint32_t)c->bn2);
         tm &= moe::make_tmap(&c->tm_w2_pair, c->slot_base, r2, hi, 128);
-        if (c->shard_w > 0) {   // the slice's W2 [h, shard_w] at row 2h of its slot
-            const uint64_t rs = (uint64_t)c->slice_slot_rows * c->nslots;
-            tm &= moe::make_tmap(&c->tm_w2s, c->slot_base, rs, c->shard_w, (uint32_t)c->bn2);
-            tm &= moe::make_tmap(&c->tm_w2s_pair, c->slot_base, rs, c->shard_w, 128);
+        // the slice's W2 [h, shard_w] after its W13 [2 shard_w, h], one view per slot (the
+        // slice has its own launch, so the map is chosen per launch)
+        for (int i = 0; c->shard_w > 0 && i < c->nslots; ++i) {
+            const char* w2 = c->slot_base + (size_t)i * c->blob_bytes + 4ll * h * c->shard_w;
+            tm &= moe::make_tmap(&c->tm_w2s[i], w2, (uint64_t)h, c->shard_w, (uint32_t)c->bn2);
+            tm &= moe::make_tmap(&c->tm_w2s_pair[i], w2, (uint64_t)h, c->shard_w, 128);
         }
     }
     if (!tm) return fail(MOE_E_CUDA);

@@ -511,6 +511,9 @@ def test_ep_local_transport_world_ranks(world, shape):
     # 4 blocks of 128 columns over 8 ranks: ranks 0, 2, 4, 6 serve no slice
     (8, dict(hidden=384, ffn=256, num_experts=64, top_k=6, tokens=804, num_shared=2)),
     (8, dict(hidden=256, ffn=384, num_experts=8, top_k=2, tokens=5, num_shared=1)),  # empty ranks
+    # C4's h_i = 1408 with 2 shared experts at W = 4: 22 blocks -> slices of 640 / 768 columns
+    # (widths that divide no slot evenly: the slice's W2 view is per slot)
+    (4, dict(hidden=256, ffn=1408, num_experts=8, top_k=2, tokens=400, num_shared=2)),
 ])
 def test_ep_local_sharded_shared_experts(world, shape):
     """MOE_FLAG_SHARD_SHARED over the LOCAL_EP transport: rank r streams only
