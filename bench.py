@@ -65,7 +65,7 @@ def parse():
     ap.add_argument("--shared", default="auto", choices=["auto", "replicated", "sharded"],
                     help="shared experts under EP: sharded by intermediate columns across the "
                          "ranks (MOE_FLAG_SHARD_SHARED, P2P transport) or replicated on every "
-                         "rank; auto = sharded when N > 1 with the p2p transport (and no --mover)")
+                         "rank; auto = sharded when N > 1 with the p2p transport")
     ap.add_argument("--ep-transport", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1: p2p = fused dispatch/combine over peer memory (CUDA IPC), "
                          "falling back to NCCL if the peers cannot be mapped; nccl = NCCL "
@@ -307,10 +307,9 @@ def run_ours(args):
     nl = cfg.num_experts // world
     ids = list(range(rank * nl, (rank + 1) * nl)) + [cfg.num_experts + s for s in range(cfg.num_shared)]
     shard = (cfg.num_shared > 0 and world > 1 and
-             (args.shared == "sharded" or
-              (args.shared == "auto" and args.ep_transport == "p2p" and not args.mover)))
-    if shard and (args.ep_transport != "p2p" or args.mover):
-        raise SystemExit("--shared sharded needs the p2p transport and no --mover")
+             (args.shared == "sharded" or (args.shared == "auto" and args.ep_transport == "p2p")))
+    if shard and args.ep_transport != "p2p":
+        raise SystemExit("--shared sharded needs the p2p transport")
 
     def allmax(v):
         if world == 1:

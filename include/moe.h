@@ -77,7 +77,7 @@ typedef enum {
 #define MOE_FLAG_SHARD_SHARED 32u /* shared experts SHARDED across the expert-parallel group
                                  instead of replicated on every rank.  Needs
                                 the P2P transport (LOCAL_EP / IPC_EP), world_size > 1 and
-                                1 <= num_shared <= world_size; not with MOE_FLAG_MOVER.  The S
+                                1 <= num_shared <= world_size.  The S
                                 shared experts are one FFN of width S*ffn (their concatenation,
                                 DESIGN.md reading R10) and a SwiGLU FFN is a sum over blocks of
                                 its intermediate columns:  W2 (silu(W1 x) * W3 x) =

@@ -268,7 +268,8 @@ struct Prof {
 moe_status mover_start(moe_ctx c);
 void mover_stop(moe_ctx c);                      // drains, joins, frees
 moe_status mover_drain(moe_ctx c);               // every queued packet issued; mover errors
-moe_status mover_push(moe_ctx c, uint64_t q0, int n, const char* src, char* dst);
+moe_status mover_push(moe_ctx c, uint64_t q0, int n, const char* src, char* dst, int64_t item,
+                      int64_t w13);   // n items of `item` bytes (W13 part: the first w13)
 moe_status mover_wait(moe_ctx c, cudaStream_t st, int which, uint64_t value);  // 0 r13, 1 r2
 moe_status mover_mark_free(moe_ctx c, cudaStream_t st, uint64_t value);
 double mover_take_h2d_ms(moe_ctx c, int64_t* packets);

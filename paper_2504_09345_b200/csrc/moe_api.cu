@@ -118,10 +118,9 @@ moe_status check_cfg(const moe_config* cfg) {
     if (cfg->flags & MOE_FLAG_SHARD_SHARED) {
         // P2P transport only (the gather / partial sums ride the peer-memory permute / combine);
         // a slice must fit one expert slot (S <= W: at most ceil(S h_i / 128 / W) <= h_i / 128
-        // blocks); the mover's packets assume one blob size
+        // blocks)
         if (cfg->world_size < 2 || !(cfg->flags & (MOE_FLAG_LOCAL_EP | MOE_FLAG_IPC_EP)) ||
-            cfg->num_shared < 1 || cfg->num_shared > cfg->world_size ||
-            (cfg->flags & MOE_FLAG_MOVER))
+            cfg->num_shared < 1 || cfg->num_shared > cfg->world_size)
             return MOE_E_UNSUPPORTED;
         int c0 = 0, w = 0;
         shared_slice_cols(cfg->ffn, cfg->num_shared, cfg->world_size, cfg->rank, &c0, &w);
@@ -196,9 +195,10 @@ moe_status flush_copies(moe_ctx c) {
             c->batch_q0[s0 + j] = c->pend_q0;
             c->batch_n[s0 + j] = n;
         }
-        c->stats.h2d_weight_bytes += (int64_t)n * c->blob_bytes;
+        c->stats.h2d_weight_bytes += (int64_t)n * ib;
         c->pend_n = 0;
-        return moe::mover_push(c, c->pend_q0, n, c->pend_src, static_cast<char*>(c->slot[s0]));
+        return moe::mover_push(c, c->pend_q0, n, c->pend_src, static_cast<char*>(c->slot[s0]), ib,
+                               i13);
     }
     for (int j = 0; j < n; ++j)  // each slot must have been released by its previous item's GEMMs
         MOE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->slot_free[s0 + j], 0));

@@ -75,6 +75,7 @@ struct Job {
     int n;
     const char* src;
     char* dst;
+    int64_t item, w13;   // bytes per item / of its W13 part (a shared-FFN slice is smaller)
 };
 }  // namespace
 
@@ -170,15 +171,15 @@ struct Mover {
         // The job's items are contiguous in host memory and in the staging buffer: one byte range
         // cut into packets regardless of item boundaries (small experts share packets); after each
         // packet the counters advance over the items whose W13 part / whole blob it completed.
-        const int64_t total = (int64_t)j.n * blob;
+        const int64_t total = (int64_t)j.n * j.item;
         int done13 = 0, done2 = 0;
         for (int64_t o = 0; o < total;) {
             const int64_t e = std::min(total, o + packet);
             if (!issue(j.dst + o, j.src + o, e - o)) return false;
             o = e;
             int n13 = done13, n2 = done2;
-            while (n13 < j.n && (int64_t)n13 * blob + w13 <= e) ++n13;
-            while (n2 < j.n && (int64_t)(n2 + 1) * blob <= e) ++n2;
+            while (n13 < j.n && (int64_t)n13 * j.item + j.w13 <= e) ++n13;
+            while (n2 < j.n && (int64_t)(n2 + 1) * j.item <= e) ++n2;
             if (n13 > done13 && !write_flag(0, j.q0 + n13)) return false;
             if (n2 > done2 && !write_flag(1, j.q0 + n2)) return false;
             done13 = n13;
@@ -286,7 +287,8 @@ void mover_stop(moe_ctx c) {
     c->mover = nullptr;
 }
 
-moe_status mover_push(moe_ctx c, uint64_t q0, int n, const char* src, char* dst) {
+moe_status mover_push(moe_ctx c, uint64_t q0, int n, const char* src, char* dst, int64_t item,
+                      int64_t w13) {
     Mover* m = c->mover;
     {
         std::lock_guard<std::mutex> g(m->mu);
@@ -294,7 +296,7 @@ moe_status mover_push(moe_ctx c, uint64_t q0, int n, const char* src, char* dst)
             c->sticky = m->err;
             return set_err(c, m->err, "%s", m->err_msg.c_str());
         }
-        m->queue.push_back(Job{q0, n, src, dst});
+        m->queue.push_back(Job{q0, n, src, dst, item, w13});
     }
     m->cv.notify_one();
     return MOE_OK;

@@ -163,12 +163,11 @@ def test_shared_slices_sum_to_the_shared_ffns():
 
 
 def test_shard_shared_rejected_outside_its_envelope(lib):
-    """MOE_FLAG_SHARD_SHARED needs the P2P transport, W > 1 and 1 <= num_shared <= W, and not
-    the mover; moe_init refuses anything else before touching CUDA."""
+    """MOE_FLAG_SHARD_SHARED needs the P2P transport, W > 1 and 1 <= num_shared <= W; moe_init
+    refuses anything else before touching CUDA."""
     for kw in (dict(world_size=1, local_ep=True, num_shared=1),
                dict(world_size=2, local_ep=True, num_shared=3),
                dict(world_size=2, local_ep=True, num_shared=0),
-               dict(world_size=2, local_ep=True, num_shared=1, mover=True),
                dict(world_size=2, num_shared=1)):               # NCCL transport
         with pytest.raises(moe.MoEError) as ei:
             moe.MoELayer(256, 256, 8, 2, 64, nccl_unique_id=b"k" * 128, shard_shared=True, **kw)

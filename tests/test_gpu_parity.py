@@ -515,13 +515,15 @@ def test_ep_local_transport_world_ranks(world, shape):
     # (widths that divide no slot evenly: the slice's W2 view is per slot)
     (4, dict(hidden=256, ffn=1408, num_experts=8, top_k=2, tokens=400, num_shared=2)),
 ])
-def test_ep_local_sharded_shared_experts(world, shape):
+@pytest.mark.parametrize("mover", [False, True])
+def test_ep_local_sharded_shared_experts(world, shape, mover):
     """MOE_FLAG_SHARD_SHARED over the LOCAL_EP transport: rank r streams only
     its column slice of the concatenated shared FFN (moe_shared_slice), the permute gathers every
     rank's tokens into the slice owners, the combine sums their partial rows.  Bar: routing
     bit-exact; every token within 2e-2 of the oracle (shared experts as whole FFNs, R10);
     three calls reuse every buffer; the ranks together stream each weight byte exactly once
-    per call (routed experts + the slices = the algorithmic bytes, no replication)."""
+    per call (routed experts + the slices = the algorithmic bytes, no replication); with the
+    data mover the slice (a smaller blob) is packetised like any expert."""
     import os
     import threading
     from paper_2504_09345_b200 import HostExperts, MoELayer, shared_slice_weights
@@ -544,7 +546,8 @@ def test_ep_local_sharded_shared_experts(world, shape):
     for r in range(world):
         layers.append(MoELayer(h, cfg.ffn, ne, cfg.top_k, max(1, -(-T // world)), num_shared=S,
                                world_size=world, rank=r, nccl_unique_id=key, local_ep=True,
-                               shard_shared=True))
+                               shard_shared=True, mover=mover,
+                               packet_bytes=(64 << 10) if mover else 0))
     bufs = []
     for r in range(world):
         x = bf16_tensor(inp.x[bounds[r]:bounds[r + 1]].reshape(-1, h))
