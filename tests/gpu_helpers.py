@@ -105,3 +105,70 @@ class _CudaArray:
 def dev_view(ptr: int, shape, typestr: str) -> torch.Tensor:
     """Read-only torch view of a raw device pointer owned by the library (debug buffers)."""
     return torch.as_tensor(_CudaArray(ptr, shape, typestr), device="cuda")
+
+
+def run_local_ep(inp: synth.MoEInputs, world: int, shard: bool = False, mover: bool = False,
+                 calls: int = 2, key: bytes = None, stream_per_rank: bool = True):
+    """MOE_FLAG_LOCAL_EP: `world` contexts on this GPU, one host thread each, every rank owning
+    T / W tokens and N_e / W experts (+ the shared ones, or its column slice with `shard`).
+    Returns (per-rank (out, idx) device tensors, per-rank stats, token bounds)."""
+    import os
+    import threading
+    from paper_2504_09345_b200 import shared_slice_weights
+    cfg = inp.cfg
+    ne, nl, S, T, h = cfg.num_experts, cfg.num_experts // world, cfg.num_shared, cfg.tokens, cfg.hidden
+    bounds = [T * r // world for r in range(world + 1)]
+    key = key or os.urandom(128)
+    router = bf16_tensor(inp.router)
+    experts, layers = [], []
+    try:
+        for r in range(world):
+            if shard:
+                ids = list(range(r * nl, (r + 1) * nl))
+                sl = shared_slice_weights(cfg.ffn, inp.w1[ne:], inp.w3[ne:], inp.w2[ne:], world, r)
+            else:
+                ids = list(range(r * nl, (r + 1) * nl)) + [ne + s for s in range(S)]
+                sl = None
+            experts.append(HostExperts(h, cfg.ffn, [inp.w1[i] for i in ids],
+                                       [inp.w3[i] for i in ids], [inp.w2[i] for i in ids],
+                                       slice_=sl))
+        for r in range(world):
+            layers.append(MoELayer(h, cfg.ffn, ne, cfg.top_k, max(1, -(-T // world)),
+                                   num_shared=S, world_size=world, rank=r, nccl_unique_id=key,
+                                   local_ep=True, shard_shared=shard, mover=mover,
+                                   packet_bytes=(64 << 10) if mover else 0))
+        bufs = []
+        for r in range(world):
+            x = bf16_tensor(inp.x[bounds[r]:bounds[r + 1]].reshape(-1, h))
+            bufs.append((torch.cuda.Stream(), x, torch.empty_like(x),
+                         torch.empty((x.shape[0], cfg.top_k), dtype=torch.int32, device="cuda")))
+        torch.cuda.synchronize()
+        errors = []
+
+        def work(r):
+            try:
+                s, x, o, idx = bufs[r]
+                for _ in range(calls):
+                    layers[r].forward(x, router, experts[r], o, idx, stream=s.cuda_stream)
+                s.synchronize()
+            except Exception as e:  # noqa: BLE001 -- reported below
+                msg = repr(e)[:300]
+                try:
+                    layers[r].sync()
+                except Exception as e2:  # noqa: BLE001
+                    msg += f" | sync: {e2!r}"[:300]
+                errors.append((r, msg))
+
+        threads = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join(timeout=300)
+        assert not errors, "\n".join(f"rank {r}: {e}" for r, e in errors)
+        stats = [l.stats() for l in layers]
+        return [(b[2], b[3]) for b in bufs], stats, bounds
+    finally:
+        for l in layers:
+            l.close()
+        for e in experts:
+            e.close()
