@@ -172,3 +172,23 @@ def test_shard_shared_rejected_outside_its_envelope(lib):
         with pytest.raises(moe.MoEError) as ei:
             moe.MoELayer(256, 256, 8, 2, 64, nccl_unique_id=b"k" * 128, shard_shared=True, **kw)
         assert ei.value.status == moe.MOE_E_UNSUPPORTED, kw
+
+
+def build_c_example(tmpdir) -> str:
+    """examples/moe_layer.c: the C ABI from plain C99 (no Python) -- compiled and linked here;
+    tests/test_gpu_parity.py runs it on the GPU against the oracle."""
+    import subprocess
+    exe = os.path.join(str(tmpdir), "moe_layer")
+    pkg = os.path.join(ROOT, "paper_2504_09345_b200")
+    cmd = ["gcc", "-std=c99", "-O2", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+           "-I", "/usr/local/cuda/include", os.path.join(ROOT, "examples", "moe_layer.c"),
+           "-L", pkg, "-lmoe_b200", "-Wl,-rpath," + pkg, "-L", "/usr/local/cuda/lib64", "-lcudart",
+           "-Wl,-rpath,/usr/local/cuda/lib64", "-o", exe]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_c_example_builds(lib, tmp_path):
+    exe = build_c_example(tmp_path)
+    assert os.path.exists(exe)

@@ -6,6 +6,7 @@ Bar (BASELINE.json north_star):
   * outputs: per-token max-abs error / max-abs reference <= 2e-2.
 """
 import dataclasses
+import os
 
 import numpy as np
 import pytest
@@ -74,6 +75,34 @@ def test_every_top_k(k):
     run, *_ = _check_full(synth.gen_inputs(synth.MoEConfig("custom", 30 + k, 256, 384,
                                                            max(8, k + 3), k, 333, 1)))
     run.close()
+
+
+def test_c_example_against_oracle(tmp_path):
+    """examples/moe_layer.c -- the C ABI driven from plain C99 (no Python in the process): it
+    packs the experts, runs moe_layer_forward_host on pinned host tokens and writes the result;
+    idx bit-exact and outputs within 2e-2 of the oracle (a tiny layer with a shared expert)."""
+    import subprocess
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from test_abi_cpu import build_c_example
+    exe = build_c_example(tmp_path)
+    cfg = synth.MoEConfig("custom", 60, 256, 384, 8, 2, 200, 1)
+    inp = synth.gen_inputs(cfg)
+    inp.x.tofile(tmp_path / "x.bin")
+    inp.router.tofile(tmp_path / "router.bin")
+    with open(tmp_path / "experts.bin", "wb") as f:
+        for a, b, c in zip(inp.w1, inp.w3, inp.w2):
+            f.write(np.ascontiguousarray(a).tobytes())
+            f.write(np.ascontiguousarray(b).tobytes())
+            f.write(np.ascontiguousarray(c).tobytes())
+    r = subprocess.run([exe, str(tmp_path), "256", "384", "8", "2", "1", "200"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    out = np.fromfile(tmp_path / "out.bin", dtype=np.uint16).reshape(200, 256)
+    idx = np.fromfile(tmp_path / "idx.bin", dtype=np.int32).reshape(200, 2)
+    y_ref, idx_ref, _ = oracle.forward(inp.x, inp.router, inp.w1, inp.w3, inp.w2, 2, 1)
+    assert np.array_equal(idx, idx_ref)
+    assert token_rel_err(synth.bf16_bits_to_f32(out), y_ref).max() <= TOL
 
 
 def test_full_softmax_gates_mode():
