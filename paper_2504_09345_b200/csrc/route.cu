@@ -462,6 +462,222 @@ router_v6_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
     }
 }
 
+// Top-k of one token per thread from its fp64 logits (row of lg, shared): insertion of experts
+// 0..ne-1 in ascending order into a k-deep list ranked by (logit desc, index asc), NaN last (R5,
+// R13) -- the same selection and the same fp64 gate arithmetic as topk_tile (R3), without the
+// warp shuffles (a warp-per-token selection costs k x 5 dependent shuffle rounds per token).
+template <int TPT>
+__device__ __forceinline__ void topk_rows(const double* lg, int pitch, int t0, int T, int ne,
+                                          int k, int renorm, int32_t* __restrict__ idx_out,
+                                          float* __restrict__ gate_out,
+                                          int (*cnt)[kMaxExperts], int tid, int nthr) {
+    constexpr int kTok = kRouteTile * TPT;
+    for (int tt = tid; tt < kTok; tt += nthr) {
+        const int t = t0 + tt;
+        if (t >= T) break;
+        const double* row = lg + tt * pitch;
+        double sl[kMaxTopK];
+        int se[kMaxTopK];
+#pragma unroll
+        for (int j = 0; j < kMaxTopK; ++j) {
+            sl[j] = 0.0;
+            se[j] = -1;   // empty slot
+        }
+        for (int e = 0; e < ne; ++e) {
+            double cv = row[e];
+            int ce = e;
+#pragma unroll
+            for (int j = 0; j < kMaxTopK; ++j) {
+                if (j < k && (se[j] < 0 || ranks_above(cv, ce, sl[j], se[j]))) {
+                    const double tv = sl[j];
+                    const int te = se[j];
+                    sl[j] = cv;
+                    se[j] = ce;
+                    cv = tv;
+                    ce = te;
+                }
+            }
+        }
+        const double m = sl[0];
+        double ex[kMaxTopK];
+        double z = 0.0;
+#pragma unroll
+        for (int j = 0; j < kMaxTopK; ++j) {
+            ex[j] = 0.0;
+            if (j < k) {
+                ex[j] = exp(sl[j] - m);
+                if (renorm) z += ex[j];
+            }
+        }
+        if (!renorm)
+            for (int e = 0; e < ne; ++e) z += exp(row[e] - m);
+#pragma unroll
+        for (int j = 0; j < kMaxTopK; ++j) {
+            if (j < k) {
+                idx_out[(size_t)t * k + j] = se[j];
+                gate_out[(size_t)t * k + j] = (float)(ex[j] / z);
+                atomicAdd(&cnt[tt / kRouteTile][se[j]], 1);
+            }
+        }
+    }
+}
+
+// Router v7: the same one-FMA-chain-per-logit arithmetic (R6) with the per-chunk staging taken off
+// the compute warps.  A producer warp runs a S-deep mbarrier ring: per chunk of CW channels it
+// issues one 1-D bulk copy (cp.async.bulk, TMA engine) per token row -- raw bf16, rows at a
+// 16-byte-padded pitch so the lanes' 16-byte reads are conflict-free -- and widens the router rows
+// to fp64 [channel][expert] itself; the NW compute warps only wait on full[s], run their chains
+// and release the stage (empty[s]).  x is widened in registers at the point of use (an exact
+// bf16 -> fp32 shift and F2F.F64.F32) instead of being stored and re-read as fp64: per channel a
+// lane reads 2 B of x instead of 8 and no compute warp ever takes a block-wide barrier inside
+// the channel loop (v6 at C1: one __syncthreads + a widening pass per 64 channels, ~28 cycles
+// per channel step for one warp per SM sub-partition).
+//   * block = TPT x 32 tokens (lane l: tokens l, l+32, ...), warp w < NW owns experts
+//     [w*EPT, (w+1)*EPT) (zero rows pad N_e to NW*EPT), warp NW is the producer;
+//   * per channel and compute warp: TPT conversions + EPT/2 double2 broadcasts for TPT*EPT DFMAs;
+//   * top-k per thread (topk_rows).
+template <int EPT, int TPT, int NW, int CW>
+struct RouterV7Cfg {
+    static constexpr int kTok = kRouteTile * TPT;
+    static constexpr int kNePad = NW * EPT;
+    static constexpr int kXP = CW * 2 + 16;                 // bytes per staged x row
+    static constexpr int kXBytes = kTok * kXP;
+    static constexpr int kStage = kXBytes + CW * kNePad * 8;
+    static constexpr int kStages = (110 * 1024 / kStage) < 2 ? 2 : ((110 * 1024 / kStage) > 8 ? 8 : 110 * 1024 / kStage);
+    static constexpr int kLgPitch = kNePad + 1;              // odd pitch: conflict-free row reads
+    static constexpr size_t kSmem = (size_t)kStages * kStage > (size_t)kTok * kLgPitch * 8
+                                        ? (size_t)kStages * kStage
+                                        : (size_t)kTok * kLgPitch * 8;
+};
+
+template <int EPT, int TPT, int NW, int CW>
+__global__ void __launch_bounds__((NW + 1) * 32)
+router_v7_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
+                 const __nv_bfloat16* __restrict__ wr, int ne, int k, int renorm,
+                 int32_t* __restrict__ idx_out, float* __restrict__ gate_out,
+                 int32_t* __restrict__ tile_counts) {
+    using C = RouterV7Cfg<EPT, TPT, NW, CW>;
+    static_assert((EPT == 1 || EPT % 2 == 0) && CW % 8 == 0, "shape");
+    constexpr int S = C::kStages, kTok = C::kTok, kNePad = C::kNePad, kXP = C::kXP;
+    constexpr int kThr = (NW + 1) * 32;
+    extern __shared__ __align__(128) uint8_t dyn7[];
+    __shared__ uint64_t full[S], empty[S];
+    __shared__ int cnt[TPT][kMaxExperts];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int t0 = blockIdx.x * kTok;
+    const int n_chunks = h / CW;
+    for (int e = tid; e < TPT * kMaxExperts; e += kThr) cnt[e / kMaxExperts][e % kMaxExperts] = 0;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            ptx::mbar_init(&full[s], 32);   // the producer's 32 lanes (+ the rows' bytes)
+            ptx::mbar_init(&empty[s], NW);  // one arrive per compute warp
+        }
+        ptx::fence_barrier_init();
+    }
+    __syncthreads();
+
+    double acc[TPT][EPT];
+#pragma unroll
+    for (int p = 0; p < TPT; ++p)
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) acc[p][i] = 0.0;
+
+    if (warp == NW) {
+        // ---------------------------------------------------------------- producer warp
+        const int nvalid = min(kTok, T - t0);
+        for (int ch = 0; ch < n_chunks; ++ch) {
+            const int s = ch % S;
+            ptx::mbar_wait(&empty[s], ((ch / S) & 1) ^ 1u);
+            uint8_t* st = dyn7 + (size_t)s * C::kStage;
+            const int c0 = ch * CW;
+            if (lane == 0) ptx::mbar_expect_tx(&full[s], (uint32_t)(nvalid * CW * 2));
+            __syncwarp();
+            for (int r = lane; r < nvalid; r += 32)
+                ptx::bulk_g2s(st + r * kXP, x + (size_t)(t0 + r) * h + c0, CW * 2, &full[s]);
+            double* ws = reinterpret_cast<double*>(st + C::kXBytes);   // [CW][kNePad]
+            constexpr int kWV = kNePad * (CW / 8);
+#pragma unroll 1
+            for (int v = lane; v < kWV; v += 32) {
+                const int e = v % kNePad, g = v / kNePad;
+                double d[8];
+                if (e < ne) {
+                    bf16x8_to_f64(ptx::ld_nc_v4(wr + (size_t)e * h + c0 + 8 * g), d);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) d[q] = 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) ws[(8 * g + q) * kNePad + e] = d[q];
+            }
+            ptx::mbar_arrive(&full[s]);   // release: this lane's router stores
+        }
+    } else {
+        // ---------------------------------------------------------------- compute warps
+        for (int ch = 0; ch < n_chunks; ++ch) {
+            const int s = ch % S;
+            ptx::mbar_wait(&full[s], (ch / S) & 1);
+            const uint8_t* st = dyn7 + (size_t)s * C::kStage;
+            const uint8_t* xr = st + lane * kXP;
+            const double* wc = reinterpret_cast<const double*>(st + C::kXBytes) + warp * EPT;
+#pragma unroll
+            for (int g = 0; g < CW / 8; ++g) {
+                int4 xv[TPT];
+#pragma unroll
+                for (int p = 0; p < TPT; ++p)
+                    xv[p] = *reinterpret_cast<const int4*>(xr + p * 32 * kXP + g * 16);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {   // channel c0 + 8g + q: ascending in every chain
+                    double xd[TPT];
+#pragma unroll
+                    for (int p = 0; p < TPT; ++p) {
+                        const uint32_t w32 = (q >> 1) == 0 ? (uint32_t)xv[p].x
+                                           : (q >> 1) == 1 ? (uint32_t)xv[p].y
+                                           : (q >> 1) == 2 ? (uint32_t)xv[p].z
+                                                           : (uint32_t)xv[p].w;
+                        xd[p] = (double)__uint_as_float((q & 1) ? (w32 & 0xffff0000u) : (w32 << 16));
+                    }
+                    const double* wrow = wc + (8 * g + q) * kNePad;
+                    if constexpr (EPT == 1) {
+                        const double w0 = wrow[0];
+#pragma unroll
+                        for (int p = 0; p < TPT; ++p) acc[p][0] = fma(xd[p], w0, acc[p][0]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < EPT / 2; ++i) {
+                            const double2 wv = reinterpret_cast<const double2*>(wrow)[i];
+#pragma unroll
+                            for (int p = 0; p < TPT; ++p) {
+                                acc[p][2 * i] = fma(xd[p], wv.x, acc[p][2 * i]);
+                                acc[p][2 * i + 1] = fma(xd[p], wv.y, acc[p][2 * i + 1]);
+                            }
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&empty[s]);
+        }
+    }
+    __syncthreads();   // every stage consumed: the ring's memory holds the logits now
+    double* lg = reinterpret_cast<double*>(dyn7);   // [kTok][kLgPitch]
+    if (warp < NW) {
+#pragma unroll
+        for (int p = 0; p < TPT; ++p)
+#pragma unroll
+            for (int i = 0; i < EPT; ++i) lg[(p * 32 + lane) * C::kLgPitch + warp * EPT + i] = acc[p][i];
+    }
+    __syncthreads();
+    topk_rows<TPT>(lg, C::kLgPitch, t0, T, ne, k, renorm, idx_out, gate_out, cnt, tid, kThr);
+    __syncthreads();
+    const int n_tiles = (T + kRouteTile - 1) / kRouteTile;
+#pragma unroll
+    for (int p = 0; p < TPT; ++p) {
+        const int tile = blockIdx.x * TPT + p;
+        if (tile < n_tiles)
+            for (int e = tid; e < ne; e += kThr) tile_counts[(size_t)tile * ne + e] = cnt[p][e];
+    }
+}
+
 // Single block of 1024 threads.  Warp w scans experts w, w+32, ... over the tiles.
 __global__ void __launch_bounds__(1024)
 scan_kernel(const int32_t* __restrict__ tile_counts, int n_tiles, int ne, int T, int k,
@@ -743,6 +959,53 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
     if (n_tiles == 0) return cudaSuccess;
     const char* ver = getenv("MOE_ROUTER");   // 3: round 1's kernel (comparison); 6 / unset: v6
     if (ver && atoi(ver) == 3) return launch_router_v3(x, T, h, wr, ne, k, renorm, idx, gates, tile_counts, st);
+    int sms7 = 148;
+    {
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess)
+            cudaDeviceGetAttribute(&sms7, cudaDevAttrMultiProcessorCount, dev);
+    }
+    if (ver && atoi(ver) == 7) {
+        int tpt = 4;
+        while (tpt > 1 && (T + kRouteTile * tpt - 1) / (kRouteTile * tpt) < sms7) tpt >>= 1;
+        if (const char* e = getenv("MOE_ROUTER_TPT")) {
+            const int v = atoi(e);
+            if (v == 1 || v == 2 || v == 4) tpt = v;
+        }
+        const int blocks = (T + kRouteTile * tpt - 1) / (kRouteTile * tpt);
+        cudaError_t err = cudaSuccess;
+#define MOE_ROUTER7(E, P, N, CW_)                                                            \
+    do {                                                                                     \
+        using C7 = RouterV7Cfg<E, P, N, CW_>;                                                \
+        if (h % CW_) return cudaErrorInvalidValue;                                           \
+        err = cudaFuncSetAttribute(router_v7_kernel<E, P, N, CW_>,                           \
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,              \
+                                   (int)C7::kSmem);                                          \
+        if (err != cudaSuccess) return err;                                                  \
+        router_v7_kernel<E, P, N, CW_><<<blocks, (N + 1) * 32, C7::kSmem, st>>>(             \
+            x, T, h, wr, ne, k, renorm, idx, gates, tile_counts);                            \
+    } while (0)
+#define MOE_ROUTER7_TPT(E, N, CW_)                                                           \
+    do {                                                                                     \
+        if (tpt == 1) MOE_ROUTER7(E, 1, N, CW_);                                             \
+        else if (tpt == 2) MOE_ROUTER7(E, 2, N, CW_);                                        \
+        else MOE_ROUTER7(E, 4, N, CW_);                                                      \
+    } while (0)
+        const char* ev = getenv("MOE_ROUTER_EPT");
+        const int ept = ev ? atoi(ev) : 0;
+        if (ne <= 8 && ept == 1) MOE_ROUTER7_TPT(1, 8, 64);
+        else if (ne <= 8 && ept == 4) MOE_ROUTER7_TPT(4, 2, 64);
+        else if (ne <= 8 && ept == 8) MOE_ROUTER7_TPT(8, 1, 64);
+        else if (ne <= 8) MOE_ROUTER7_TPT(2, 4, 64);
+        else if (ne <= 16 && ept == 8) MOE_ROUTER7_TPT(8, 2, 64);
+        else if (ne <= 16) MOE_ROUTER7_TPT(4, 4, 64);
+        else if (ne <= 32) MOE_ROUTER7_TPT(8, 4, 64);
+        else if (ne <= 64) MOE_ROUTER7_TPT(8, 8, 32);
+        else MOE_ROUTER7_TPT(8, 16, 32);
+#undef MOE_ROUTER7_TPT
+#undef MOE_ROUTER7
+        return cudaGetLastError();
+    }
     if (!ver || atoi(ver) == 6) {
         // v6 buckets: N_e padded to NW * EPT; tokens per lane TPT (MOE_ROUTER_TPT = 1/2/4): the
         // most tokens per lane (each router broadcast feeds 2 TPT DFMAs) that still leaves every

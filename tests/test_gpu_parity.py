@@ -392,16 +392,19 @@ def test_experts_per_gemm_launch(rows, copy_group, launches, monkeypatch):
 
 
 @pytest.mark.parametrize("variant", ["v3-1", "v3-2", "v3-4", "v3-8",
-                                     "v6-0-tpt1", "v6-0-tpt2", "v6-0-tpt4", "v6-1-tpt1", "v6-1-tpt2"])
+                                     "v6-0-tpt1", "v6-0-tpt2", "v6-0-tpt4", "v6-1-tpt1", "v6-1-tpt2",
+                                     "v7-0-tpt1", "v7-0-tpt2", "v7-0-tpt4", "v7-1-tpt1", "v7-4-tpt2",
+                                     "v7-8-tpt4"])
 @pytest.mark.parametrize("ne,k", [(5, 2), (8, 2), (16, 4), (40, 6), (128, 8)])
 def test_router_experts_per_warp_variants(ne, k, variant, monkeypatch):
     """Every router kernel instantiation -- round 1's router_topk_kernel<EPT> (MOE_ROUTER=3) and
-    router_v6_kernel<EPT, TPT, NW, CW, PF> (default; every N_e bucket x MOE_ROUTER_TPT = 1 / 2 / 4,
-    one chain per lane with MOE_ROUTER_EPT=1) -- gives the same bit-exact selection and gates as
+    router_v6_kernel<EPT, TPT, NW, CW, PF> (every N_e bucket x MOE_ROUTER_TPT = 1 / 2 / 4, one
+    chain per lane with MOE_ROUTER_EPT=1) and router_v7_kernel<EPT, TPT, NW, CW> (MOE_ROUTER=7:
+    producer-warp bulk-copy ring, per-thread top-k; the EPT overrides 1 / 4 / 8) -- gives the same bit-exact selection and gates as
     the oracle (one fp64 FMA chain per logit, ascending channels, in every kernel)."""
     ver, ept, *rest = variant.split("-")
-    if ne == 128 and ver != "v6":
-        pytest.skip("128 experts: v6 buckets only")
+    if ne == 128 and ver == "v3":
+        pytest.skip("128 experts: v6 / v7 buckets only")
     monkeypatch.setenv("MOE_ROUTER", ver[1])
     if ept != "0":
         monkeypatch.setenv("MOE_ROUTER_EPT", ept)

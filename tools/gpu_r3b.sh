@@ -1,0 +1,2 @@
+bash tools/gpu_router_v7.sh gpurun_out/router7
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -k "router_experts_per_warp" > gpurun_out/router7/tests.log 2>&1; tail -3 gpurun_out/router7/tests.log

