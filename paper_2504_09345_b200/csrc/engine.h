@@ -124,6 +124,7 @@ struct moe_ctx_s {
     int32_t* idx_ws = nullptr;
     float* gates_ws = nullptr;
     int32_t* tile_counts = nullptr;
+    double* wr64 = nullptr;   // router rows widened to fp64 (router workspace)
     int32_t* tile_prefix = nullptr;
     int32_t* offsets = nullptr;
     int32_t* counts = nullptr;

@@ -498,12 +498,13 @@ moe_status forward_impl(moe_ctx c, const __nv_bfloat16* hidden, int T, const __n
 
     {
         Prof p(c, moe::kRecRoute, st);
+        int nl = 0;
         MOE_CUDA(c, moe::launch_router_topk(hidden, T, h, wr, ne, k, cf.renormalize, idx, gates,
-                                            c->tile_counts, st));
+                                            c->tile_counts, c->wr64, &nl, st));
         MOE_CUDA(c, moe::launch_scan(c->tile_counts, n_tiles, ne, T, k, S, c->tile_prefix,
                                      c->offsets, c->counts, c->grp1, c->grp2, st));
         p.end();
-        c->stats.kernel_launches += 2;
+        c->stats.kernel_launches += nl + 1;
     }
     if (c->p2p) {   // P2P EP: counts exchange + plan before the permute writes into the owners
         Prof p(c, moe::kRecComm, st);
@@ -1004,6 +1005,7 @@ moe_status moe_init(const moe_config* cfg, moe_ctx* out) {
     ok &= dalloc((void**)&c->idx_ws, sizeof(int32_t) * (size_t)Tm * k);
     ok &= dalloc((void**)&c->gates_ws, sizeof(float) * (size_t)Tm * k);
     ok &= dalloc((void**)&c->tile_counts, sizeof(int32_t) * (size_t)n_tiles * ne);
+    ok &= dalloc((void**)&c->wr64, sizeof(double) * moe::router_ws_doubles(h, ne));
     ok &= dalloc((void**)&c->tile_prefix, sizeof(int32_t) * (size_t)n_tiles * ne);
     ok &= dalloc((void**)&c->offsets, sizeof(int32_t) * (size_t)(ne + 1));
     ok &= dalloc((void**)&c->counts, sizeof(int32_t) * (size_t)(ne + S));
@@ -1388,7 +1390,7 @@ moe_status moe_destroy(moe_ctx c) {
             if (e) cudaEventDestroy(e);
         cudaFree(c->lw_slot[i]);
     }
-    void* bufs[] = {c->idx_ws, c->gates_ws, c->tile_counts, c->tile_prefix, c->offsets, c->counts,
+    void* bufs[] = {c->idx_ws, c->gates_ws, c->tile_counts, c->wr64, c->tile_prefix, c->offsets, c->counts,
                     c->grp1, c->grp2, c->shared_grp, c->pos, c->x_perm, c->h_act, c->y_perm,
                     c->h1_ws, c->u_ws, c->oproj_grp, c->clk_acc};
     for (void* p : bufs) cudaFree(p);

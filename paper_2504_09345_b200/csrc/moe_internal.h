@@ -102,9 +102,15 @@ cudaError_t launch_p2p_plan(const int32_t* counts_par, int W, int ne, int me, in
 
 // ---------------------------------------------------------------------------- routing kernels
 // a2+a3: router GEMM (fp64, ascending c) + warp-shuffle top-k + softmax gates + per-tile counts.
+//   wr64: device workspace of router_ws_doubles(h, ne) doubles (the router rows widened to fp64
+//   by the router's own first launch); *launches += the kernels enqueued.
 cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_bfloat16* wr,
                                int ne, int k, int renorm, int32_t* idx, float* gates,
-                               int32_t* tile_counts, cudaStream_t st);
+                               int32_t* tile_counts, double* wr64, int* launches,
+                               cudaStream_t st);
+size_t router_ws_doubles(int h, int ne);
+// Router v7 block 0: SM clock at entry, cycles to the end of the channel loop / to exit, exit ns.
+cudaError_t router_probe(unsigned long long out[4]);
 // Round 1's router kernel (comparison only: tools/router_bench.cu, MOE_ROUTER=3).
 cudaError_t launch_router_v3(const __nv_bfloat16* x, int T, int h, const __nv_bfloat16* wr,
                              int ne, int k, int renorm, int32_t* idx, float* gates,

@@ -462,6 +462,23 @@ router_v6_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
     }
 }
 
+// Block 0's SM clock at kernel entry / end of the channel loop (compute warp 0) / exit, and the
+// entry-to-exit %globaltimer ns (router_probe(): tools only).
+__device__ unsigned long long g_router_probe[4];
+
+// Router rows widened to fp64 for router v7: wr64[c * ne_pad + e] = (double)wr[e][c] (exact), zero
+// for the padding experts e >= ne.
+__global__ void __launch_bounds__(256)
+router_widen_kernel(const __nv_bfloat16* __restrict__ wr, int h, int ne, int ne_pad,
+                    double* __restrict__ wr64) {
+    const int64_t n = (int64_t)h * ne_pad;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int e = (int)(i % ne_pad), c = (int)(i / ne_pad);
+        wr64[i] = e < ne ? (double)__bfloat162float(wr[(size_t)e * h + c]) : 0.0;
+    }
+}
+
 // Top-k of one token per thread from its fp64 logits (row of lg, shared): insertion of experts
 // 0..ne-1 in ascending order into a k-deep list ranked by (logit desc, index asc), NaN last (R5,
 // R13) -- the same selection and the same fp64 gate arithmetic as topk_tile (R3), without the
@@ -523,11 +540,14 @@ __device__ __forceinline__ void topk_rows(const double* lg, int pitch, int t0, i
 }
 
 // Router v7: the same one-FMA-chain-per-logit arithmetic (R6) with the per-chunk staging taken off
-// the compute warps.  A producer warp runs a S-deep mbarrier ring: per chunk of CW channels it
-// issues one 1-D bulk copy (cp.async.bulk, TMA engine) per token row -- raw bf16, rows at a
-// 16-byte-padded pitch so the lanes' 16-byte reads are conflict-free -- and widens the router rows
-// to fp64 [channel][expert] itself; the NW compute warps only wait on full[s], run their chains
-// and release the stage (empty[s]).  x is widened in registers at the point of use (an exact
+// the compute warps.  The router rows are widened once per call into an fp64 [channel][expert]
+// workspace (router_widen_kernel, zero rows pad N_e); a producer warp runs a S-deep mbarrier ring
+// of 1-D bulk copies (cp.async.bulk, TMA engine) -- per chunk of CW channels one copy per token
+// row (raw bf16, rows at a 16-byte-padded pitch so the lanes' 16-byte reads are conflict-free)
+// and one copy of the chunk's fp64 router rows -- so it never waits on a load itself (a first
+// version widened the router chunk in the producer from global loads: two dependent L2 round
+// trips per chunk, 110 us at C1 whatever the chain count); the NW compute warps only wait on
+// full[s], run their chains and release the stage (empty[s]).  x is widened in registers at the point of use (an exact
 // bf16 -> fp32 shift and F2F.F64.F32) instead of being stored and re-read as fp64: per channel a
 // lane reads 2 B of x instead of 8 and no compute warp ever takes a block-wide barrier inside
 // the channel loop (v6 at C1: one __syncthreads + a widening pass per 64 channels, ~28 cycles
@@ -553,12 +573,13 @@ struct RouterV7Cfg {
 template <int EPT, int TPT, int NW, int CW>
 __global__ void __launch_bounds__((NW + 1) * 32)
 router_v7_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
-                 const __nv_bfloat16* __restrict__ wr, int ne, int k, int renorm,
+                 const double* __restrict__ wr64, int ne, int k, int renorm,
                  int32_t* __restrict__ idx_out, float* __restrict__ gate_out,
                  int32_t* __restrict__ tile_counts) {
     using C = RouterV7Cfg<EPT, TPT, NW, CW>;
     static_assert((EPT == 1 || EPT % 2 == 0) && CW % 8 == 0, "shape");
     constexpr int S = C::kStages, kTok = C::kTok, kNePad = C::kNePad, kXP = C::kXP;
+    constexpr uint32_t kWBytes = CW * kNePad * 8;
     constexpr int kThr = (NW + 1) * 32;
     extern __shared__ __align__(128) uint8_t dyn7[];
     __shared__ uint64_t full[S], empty[S];
@@ -566,10 +587,16 @@ router_v7_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int t0 = blockIdx.x * kTok;
     const int n_chunks = h / CW;
+    const bool probe = blockIdx.x == 0 && tid == 0;
+    uint64_t clk0 = 0, ns0 = 0;
+    if (probe) {
+        clk0 = clock64();
+        ns0 = ptx::globaltimer_ns();
+    }
     for (int e = tid; e < TPT * kMaxExperts; e += kThr) cnt[e / kMaxExperts][e % kMaxExperts] = 0;
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
-            ptx::mbar_init(&full[s], 32);   // the producer's 32 lanes (+ the rows' bytes)
+            ptx::mbar_init(&full[s], 1);    // the producer's expect_tx (+ the copies' bytes)
             ptx::mbar_init(&empty[s], NW);  // one arrive per compute warp
         }
         ptx::fence_barrier_init();
@@ -590,73 +617,88 @@ router_v7_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
             ptx::mbar_wait(&empty[s], ((ch / S) & 1) ^ 1u);
             uint8_t* st = dyn7 + (size_t)s * C::kStage;
             const int c0 = ch * CW;
-            if (lane == 0) ptx::mbar_expect_tx(&full[s], (uint32_t)(nvalid * CW * 2));
+            if (lane == 0) {
+                ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)(nvalid * CW * 2 + kWBytes));
+                ptx::bulk_g2s(st + C::kXBytes, wr64 + (size_t)c0 * kNePad, kWBytes, &full[s]);
+            }
             __syncwarp();
             for (int r = lane; r < nvalid; r += 32)
                 ptx::bulk_g2s(st + r * kXP, x + (size_t)(t0 + r) * h + c0, CW * 2, &full[s]);
-            double* ws = reinterpret_cast<double*>(st + C::kXBytes);   // [CW][kNePad]
-            constexpr int kWV = kNePad * (CW / 8);
-#pragma unroll 1
-            for (int v = lane; v < kWV; v += 32) {
-                const int e = v % kNePad, g = v / kNePad;
-                double d[8];
-                if (e < ne) {
-                    bf16x8_to_f64(ptx::ld_nc_v4(wr + (size_t)e * h + c0 + 8 * g), d);
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) d[q] = 0.0;
-                }
-#pragma unroll
-                for (int q = 0; q < 8; ++q) ws[(8 * g + q) * kNePad + e] = d[q];
-            }
-            ptx::mbar_arrive(&full[s]);   // release: this lane's router stores
         }
     } else {
         // ---------------------------------------------------------------- compute warps
+        // Explicit register pipeline inside a chunk (fully unrolled, so every ring index is a
+        // compile-time constant): router operands kWD channels ahead, x one 8-channel group
+        // ahead, each channel's x widened one channel ahead.  Left to the compiler, the router
+        // loads were issued one channel ahead and every channel step waited a shared-memory
+        // round trip (measured 34 cycles per channel at C1).
+        constexpr int kWP = EPT >= 2 ? EPT / 2 : 1;      // double2 (or double) loads per channel
+        constexpr int kWD = 4;                            // router channels in flight
         for (int ch = 0; ch < n_chunks; ++ch) {
             const int s = ch % S;
             ptx::mbar_wait(&full[s], (ch / S) & 1);
             const uint8_t* st = dyn7 + (size_t)s * C::kStage;
             const uint8_t* xr = st + lane * kXP;
             const double* wc = reinterpret_cast<const double*>(st + C::kXBytes) + warp * EPT;
+            double2 wv[kWD][kWP];
+            auto loadw = [&](int c, int slot) {
+                const double* wrow = wc + c * kNePad;
 #pragma unroll
-            for (int g = 0; g < CW / 8; ++g) {
-                int4 xv[TPT];
+                for (int i = 0; i < kWP; ++i) {
+                    if constexpr (EPT == 1) wv[slot][i].x = wrow[0];
+                    else wv[slot][i] = reinterpret_cast<const double2*>(wrow)[i];
+                }
+            };
+            constexpr int kXG = 3;                            // x groups (8 channels) in flight
+            constexpr int kXL = 4;                            // channels widened ahead
+            int4 xv[kXG][TPT];
+            auto loadx = [&](int g, int slot) {
 #pragma unroll
                 for (int p = 0; p < TPT; ++p)
-                    xv[p] = *reinterpret_cast<const int4*>(xr + p * 32 * kXP + g * 16);
+                    xv[slot][p] = *reinterpret_cast<const int4*>(xr + p * 32 * kXP + g * 16);
+            };
+            double xd[kXL + 1][TPT];
+            auto widen = [&](int c, int slot) {   // exact: bf16 -> fp32 (shift) -> fp64
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {   // channel c0 + 8g + q: ascending in every chain
-                    double xd[TPT];
+                for (int p = 0; p < TPT; ++p) {
+                    const int4& v = xv[(c >> 3) % kXG][p];
+                    const int qq = c & 7;
+                    const uint32_t w32 = (qq >> 1) == 0 ? (uint32_t)v.x
+                                       : (qq >> 1) == 1 ? (uint32_t)v.y
+                                       : (qq >> 1) == 2 ? (uint32_t)v.z
+                                                        : (uint32_t)v.w;
+                    xd[slot][p] = (double)__uint_as_float((qq & 1) ? (w32 & 0xffff0000u) : (w32 << 16));
+                }
+            };
+            loadx(0, 0);
+            if (CW > 8) loadx(1, 1);
+#pragma unroll
+            for (int c = 0; c < kWD; ++c) loadw(c, c);
+#pragma unroll
+            for (int c = 0; c < kXL; ++c) widen(c, c);
+#pragma unroll
+            for (int c = 0; c < CW; ++c) {   // channel c0 + c: ascending in every chain
+                if ((c & 7) == 0 && c + 16 < CW) loadx((c >> 3) + 2, ((c >> 3) + 2) % kXG);
+                if (c + kXL < CW) widen(c + kXL, (c + kXL) % (kXL + 1));
+                const int xs = c % (kXL + 1);
+#pragma unroll
+                for (int i = 0; i < kWP; ++i) {
 #pragma unroll
                     for (int p = 0; p < TPT; ++p) {
-                        const uint32_t w32 = (q >> 1) == 0 ? (uint32_t)xv[p].x
-                                           : (q >> 1) == 1 ? (uint32_t)xv[p].y
-                                           : (q >> 1) == 2 ? (uint32_t)xv[p].z
-                                                           : (uint32_t)xv[p].w;
-                        xd[p] = (double)__uint_as_float((q & 1) ? (w32 & 0xffff0000u) : (w32 << 16));
-                    }
-                    const double* wrow = wc + (8 * g + q) * kNePad;
-                    if constexpr (EPT == 1) {
-                        const double w0 = wrow[0];
-#pragma unroll
-                        for (int p = 0; p < TPT; ++p) acc[p][0] = fma(xd[p], w0, acc[p][0]);
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < EPT / 2; ++i) {
-                            const double2 wv = reinterpret_cast<const double2*>(wrow)[i];
-#pragma unroll
-                            for (int p = 0; p < TPT; ++p) {
-                                acc[p][2 * i] = fma(xd[p], wv.x, acc[p][2 * i]);
-                                acc[p][2 * i + 1] = fma(xd[p], wv.y, acc[p][2 * i + 1]);
-                            }
+                        if constexpr (EPT == 1) {
+                            acc[p][0] = fma(xd[xs][p], wv[c % kWD][0].x, acc[p][0]);
+                        } else {
+                            acc[p][2 * i] = fma(xd[xs][p], wv[c % kWD][i].x, acc[p][2 * i]);
+                            acc[p][2 * i + 1] = fma(xd[xs][p], wv[c % kWD][i].y, acc[p][2 * i + 1]);
                         }
                     }
                 }
+                if (c + kWD < CW) loadw(c + kWD, c % kWD);
             }
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&empty[s]);
         }
+        if (probe) g_router_probe[1] = clock64() - clk0;
     }
     __syncthreads();   // every stage consumed: the ring's memory holds the logits now
     double* lg = reinterpret_cast<double*>(dyn7);   // [kTok][kLgPitch]
@@ -675,6 +717,11 @@ router_v7_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
         const int tile = blockIdx.x * TPT + p;
         if (tile < n_tiles)
             for (int e = tid; e < ne; e += kThr) tile_counts[(size_t)tile * ne + e] = cnt[p][e];
+    }
+    if (probe) {
+        g_router_probe[0] = clk0;
+        g_router_probe[2] = clock64() - clk0;
+        g_router_probe[3] = ptx::globaltimer_ns() - ns0;
     }
 }
 
@@ -952,13 +999,32 @@ cudaError_t launch_router_v3(const __nv_bfloat16* x, int T, int h, const __nv_bf
     return cudaGetLastError();
 }
 
+// N_e padded to the v7 bucket's NW * EPT (every EPT override of a bucket pads to the same width)
+static int router_ne_pad(int ne) {
+    int p = 8;
+    while (p < ne) p *= 2;
+    return p;
+}
+
+size_t router_ws_doubles(int h, int ne) { return (size_t)h * router_ne_pad(ne); }
+
+cudaError_t router_probe(unsigned long long out[4]) {
+    return cudaMemcpyFromSymbol(out, g_router_probe, 4 * sizeof(unsigned long long));
+}
+
 cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_bfloat16* wr,
                                int ne, int k, int renorm, int32_t* idx, float* gates,
-                               int32_t* tile_counts, cudaStream_t st) {
+                               int32_t* tile_counts, double* wr64, int* launches,
+                               cudaStream_t st) {
     const int n_tiles = (T + kRouteTile - 1) / kRouteTile;
     if (n_tiles == 0) return cudaSuccess;
     const char* ver = getenv("MOE_ROUTER");   // 3: round 1's kernel (comparison); 6 / unset: v6
-    if (ver && atoi(ver) == 3) return launch_router_v3(x, T, h, wr, ne, k, renorm, idx, gates, tile_counts, st);
+    int none = 0;
+    if (!launches) launches = &none;
+    if (ver && atoi(ver) == 3) {
+        *launches += 1;
+        return launch_router_v3(x, T, h, wr, ne, k, renorm, idx, gates, tile_counts, st);
+    }
     int sms7 = 148;
     {
         int dev = 0;
@@ -977,13 +1043,13 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
 #define MOE_ROUTER7(E, P, N, CW_)                                                            \
     do {                                                                                     \
         using C7 = RouterV7Cfg<E, P, N, CW_>;                                                \
-        if (h % CW_) return cudaErrorInvalidValue;                                           \
+        if (h % CW_ || C7::kNePad != ne_pad) return cudaErrorInvalidValue;                  \
         err = cudaFuncSetAttribute(router_v7_kernel<E, P, N, CW_>,                           \
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,              \
                                    (int)C7::kSmem);                                          \
         if (err != cudaSuccess) return err;                                                  \
         router_v7_kernel<E, P, N, CW_><<<blocks, (N + 1) * 32, C7::kSmem, st>>>(             \
-            x, T, h, wr, ne, k, renorm, idx, gates, tile_counts);                            \
+            x, T, h, wr64, ne, k, renorm, idx, gates, tile_counts);                            \
     } while (0)
 #define MOE_ROUTER7_TPT(E, N, CW_)                                                           \
     do {                                                                                     \
@@ -991,6 +1057,11 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
         else if (tpt == 2) MOE_ROUTER7(E, 2, N, CW_);                                        \
         else MOE_ROUTER7(E, 4, N, CW_);                                                      \
     } while (0)
+        if (!wr64) return cudaErrorInvalidValue;
+        const int ne_pad = router_ne_pad(ne);
+        router_widen_kernel<<<(int)std::min<int64_t>(((int64_t)h * ne_pad + 255) / 256, 1184), 256, 0, st>>>(
+            wr, h, ne, ne_pad, wr64);
+        *launches += 2;
         const char* ev = getenv("MOE_ROUTER_EPT");
         const int ept = ev ? atoi(ev) : 0;
         if (ne <= 8 && ept == 1) MOE_ROUTER7_TPT(1, 8, 64);
@@ -1007,6 +1078,7 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
         return cudaGetLastError();
     }
     if (!ver || atoi(ver) == 6) {
+        *launches += 1;
         // v6 buckets: N_e padded to NW * EPT; tokens per lane TPT (MOE_ROUTER_TPT = 1/2/4): the
         // most tokens per lane (each router broadcast feeds 2 TPT DFMAs) that still leaves every
         // SM a block -- below that the chains are latency-bound and want more warps instead

@@ -10,7 +10,7 @@ export LD_LIBRARY_PATH=paper_2504_09345_b200:$LD_LIBRARY_PATH
 for shape in "4096 4096 8 2" "512 4096 8 2" "8192 6144 8 2" "16384 6144 16 4" "32768 2048 64 6" "131072 4096 8 2" "4000 2048 128 1" "1000 512 40 3" "64 128 8 2"; do
   timeout 60 ./build/router_bench $shape
   for t in auto 1 2 4; do
-    for e in auto 1 4 8; do
+    for e in auto 4 8; do
       if [ $t = auto ]; then unset MOE_ROUTER_TPT; else export MOE_ROUTER_TPT=$t; fi
       if [ $e = auto ]; then unset MOE_ROUTER_EPT; else export MOE_ROUTER_EPT=$e; fi
       MOE_ROUTER=7 timeout 60 ./build/router_bench $shape

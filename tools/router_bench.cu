@@ -30,6 +30,9 @@ int main(int argc, char** argv) {
     cudaMalloc(&idx, (size_t)T * k * 4);
     cudaMalloc(&g, (size_t)T * k * 4);
     cudaMalloc(&tc, (size_t)((T + 31) / 32) * ne * 4);
+    double* wr64;
+    cudaMalloc(&wr64, sizeof(double) * moe::router_ws_doubles(h, ne));
+    int nl = 0;
     fill<<<1024, 256>>>(x, (size_t)T * h, 1, 3.f);
     fill<<<64, 256>>>(w, (size_t)ne * h, 2, 0.03f);
     cudaEvent_t e0, e1;
@@ -38,11 +41,11 @@ int main(int argc, char** argv) {
     // launches captured in a CUDA graph: the timing excludes the host-side launch path
     cudaStream_t s;
     cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-    for (int i = 0; i < 3; ++i) moe::launch_router_topk(x, T, h, w, ne, k, 1, idx, g, tc, s);
+    for (int i = 0; i < 3; ++i) moe::launch_router_topk(x, T, h, w, ne, k, 1, idx, g, tc, wr64, &nl, s);
     cudaGraph_t graph;
     cudaGraphExec_t exec;
     cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
-    for (int i = 0; i < iters; ++i) moe::launch_router_topk(x, T, h, w, ne, k, 1, idx, g, tc, s);
+    for (int i = 0; i < iters; ++i) moe::launch_router_topk(x, T, h, w, ne, k, 1, idx, g, tc, wr64, &nl, s);
     cudaStreamEndCapture(s, &graph);
     cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphLaunch(exec, s);
@@ -76,5 +79,9 @@ int main(int argc, char** argv) {
            getenv("MOE_ROUTER_TPT") ? getenv("MOE_ROUTER_TPT") : "auto",
            getenv("MOE_ROUTER_LANES") ? getenv("MOE_ROUTER_LANES") : "auto", 1e3 * ms / iters,
            2 * dfma / (ms / iters * 1e-3) / 1e12, cudaGetErrorString(err), bad, a.size());
+    unsigned long long pr[4] = {0, 0, 0, 0};
+    if (getenv("MOE_ROUTER") && atoi(getenv("MOE_ROUTER")) == 7 && moe::router_probe(pr) == cudaSuccess && pr[3])
+        printf("    block 0: %llu cycles (loop %llu = %.1f per channel), %.2f us, %.0f MHz\n", pr[2], pr[1],
+               (double)pr[1] / h, pr[3] * 1e-3, (double)pr[2] / pr[3] * 1e3);
     return 0;
 }
