@@ -47,18 +47,26 @@ PFN_encodeTiled_t get_encode_fn() {
 }
 }  // namespace
 
-// bf16 [rows, cols] row-major, box = 64 columns (128 B, one swizzle atom) x box_rows rows.
-bool make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+// bf16 [rows, cols] row-major, box = box_cols columns (box_cols * 2 bytes = the swizzle span:
+// 128 or 64) x box_rows rows; rows past `rows` read as zeros.
+bool make_tmap_box(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_cols,
+                   uint32_t box_rows) {
     PFN_encodeTiled_t enc = get_encode_fn();
-    if (!enc || rows == 0) return false;
+    if (!enc || rows == 0 || (box_cols != 64 && box_cols != 32)) return false;
     cuuint64_t dims[2] = {cols, rows};
     cuuint64_t strides[1] = {cols * 2};
-    cuuint32_t box[2] = {64, box_rows};
+    cuuint32_t box[2] = {box_cols, box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     box_cols == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
+}
+
+// box = 64 columns (128 B, one swizzle atom) x box_rows rows.
+bool make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+    return make_tmap_box(m, base, rows, cols, 64, box_rows);
 }
 
 moe_status set_err(moe_ctx c, moe_status s, const char* fmt, ...) {

@@ -109,6 +109,10 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
                                int32_t* tile_counts, double* wr64, int* launches,
                                cudaStream_t st);
 size_t router_ws_doubles(int h, int ne);
+// Tensor map of a bf16 [rows, cols] row-major array: box_cols (64 -> 128B swizzle, 32 -> 64B
+// swizzle) x box_rows, rows past `rows` read as zeros (moe_api.cu).
+bool make_tmap_box(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_cols,
+                   uint32_t box_rows);
 // Router v7 block 0: SM clock at entry, cycles to the end of the channel loop / to exit, exit ns.
 cudaError_t router_probe(unsigned long long out[4]);
 // Round 1's router kernel (comparison only: tools/router_bench.cu, MOE_ROUTER=3).

@@ -500,8 +500,11 @@ __device__ __forceinline__ void topk_rows(const double* lg, int pitch, int t0, i
             sl[j] = 0.0;
             se[j] = -1;   // empty slot
         }
+        double kv = 0.0;   // the current k-th entry (valid once k experts are in the list)
+        int ke = -1;
         for (int e = 0; e < ne; ++e) {
             double cv = row[e];
+            if (e >= k && !ranks_above(cv, e, kv, ke)) continue;   // below the k-th: no change
             int ce = e;
 #pragma unroll
             for (int j = 0; j < kMaxTopK; ++j) {
@@ -514,6 +517,12 @@ __device__ __forceinline__ void topk_rows(const double* lg, int pitch, int t0, i
                     ce = te;
                 }
             }
+#pragma unroll
+            for (int j = 0; j < kMaxTopK; ++j)
+                if (j == k - 1) {
+                    kv = sl[j];
+                    ke = se[j];
+                }
         }
         const double m = sl[0];
         double ex[kMaxTopK];
@@ -558,21 +567,22 @@ __device__ __forceinline__ void topk_rows(const double* lg, int pitch, int t0, i
 //   * top-k per thread (topk_rows).
 template <int EPT, int TPT, int NW, int CW>
 struct RouterV7Cfg {
+    static_assert(CW == 64 || CW == 32, "x chunk = one 128-B (64 ch) or 64-B (32 ch) swizzle span");
     static constexpr int kTok = kRouteTile * TPT;
     static constexpr int kNePad = NW * EPT;
-    static constexpr int kXP = CW * 2 + 16;                 // bytes per staged x row
+    static constexpr int kXP = CW * 2;                       // bytes per staged x row (swizzled)
     static constexpr int kXBytes = kTok * kXP;
-    static constexpr int kStage = kXBytes + CW * kNePad * 8;
+    static constexpr int kStage = (kXBytes + CW * kNePad * 8 + 1023) / 1024 * 1024;
     static constexpr int kStages = (110 * 1024 / kStage) < 2 ? 2 : ((110 * 1024 / kStage) > 8 ? 8 : 110 * 1024 / kStage);
     static constexpr int kLgPitch = kNePad + 1;              // odd pitch: conflict-free row reads
-    static constexpr size_t kSmem = (size_t)kStages * kStage > (size_t)kTok * kLgPitch * 8
-                                        ? (size_t)kStages * kStage
-                                        : (size_t)kTok * kLgPitch * 8;
+    static constexpr size_t kSmem = 1024 + ((size_t)kStages * kStage > (size_t)kTok * kLgPitch * 8
+                                                ? (size_t)kStages * kStage
+                                                : (size_t)kTok * kLgPitch * 8);
 };
 
 template <int EPT, int TPT, int NW, int CW>
 __global__ void __launch_bounds__((NW + 1) * 32)
-router_v7_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
+router_v7_kernel(const __grid_constant__ CUtensorMap tmX, int T, int h,
                  const double* __restrict__ wr64, int ne, int k, int renorm,
                  int32_t* __restrict__ idx_out, float* __restrict__ gate_out,
                  int32_t* __restrict__ tile_counts) {
@@ -581,7 +591,11 @@ router_v7_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
     constexpr int S = C::kStages, kTok = C::kTok, kNePad = C::kNePad, kXP = C::kXP;
     constexpr uint32_t kWBytes = CW * kNePad * 8;
     constexpr int kThr = (NW + 1) * 32;
-    extern __shared__ __align__(128) uint8_t dyn7[];
+    extern __shared__ uint8_t dyn7_raw[];
+    // 1024-byte aligned (the TMA swizzle span) by an OFFSET from the shared array, so the compiler
+    // still knows every operand pointer is shared memory (LDS); an aligned pointer rebuilt from an
+    // integer made every operand read a generic LD (ncu: long-scoreboard stalls on the DFMAs).
+    uint8_t* dyn7 = dyn7_raw + ((1024u - (ptx::smem_u32(dyn7_raw) & 1023u)) & 1023u);
     __shared__ uint64_t full[S], empty[S];
     __shared__ int cnt[TPT][kMaxExperts];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -610,20 +624,18 @@ router_v7_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
         for (int i = 0; i < EPT; ++i) acc[p][i] = 0.0;
 
     if (warp == NW) {
-        // ---------------------------------------------------------------- producer warp
-        const int nvalid = min(kTok, T - t0);
-        for (int ch = 0; ch < n_chunks; ++ch) {
-            const int s = ch % S;
-            ptx::mbar_wait(&empty[s], ((ch / S) & 1) ^ 1u);
-            uint8_t* st = dyn7 + (size_t)s * C::kStage;
-            const int c0 = ch * CW;
-            if (lane == 0) {
-                ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)(nvalid * CW * 2 + kWBytes));
+        // ---------------------------------------------------------------- producer (1 thread)
+        if (lane == 0) {
+            ptx::prefetch_tmap(&tmX);
+            for (int ch = 0; ch < n_chunks; ++ch) {
+                const int s = ch % S;
+                ptx::mbar_wait(&empty[s], ((ch / S) & 1) ^ 1u);
+                uint8_t* st = dyn7 + (size_t)s * C::kStage;
+                const int c0 = ch * CW;
+                ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)(C::kXBytes + kWBytes));
+                ptx::tma_load_2d(st, &tmX, &full[s], c0, t0);   // rows >= T read as zeros
                 ptx::bulk_g2s(st + C::kXBytes, wr64 + (size_t)c0 * kNePad, kWBytes, &full[s]);
             }
-            __syncwarp();
-            for (int r = lane; r < nvalid; r += 32)
-                ptx::bulk_g2s(st + r * kXP, x + (size_t)(t0 + r) * h + c0, CW * 2, &full[s]);
         }
     } else {
         // ---------------------------------------------------------------- compute warps
@@ -633,11 +645,13 @@ router_v7_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
         // loads were issued one channel ahead and every channel step waited a shared-memory
         // round trip (measured 34 cycles per channel at C1).
         constexpr int kWP = EPT >= 2 ? EPT / 2 : 1;      // double2 (or double) loads per channel
-        constexpr int kWD = 4;                            // router channels in flight
+        constexpr int kWD = EPT >= 8 ? 2 : 4;             // router channels in flight
         for (int ch = 0; ch < n_chunks; ++ch) {
             const int s = ch % S;
             ptx::mbar_wait(&full[s], (ch / S) & 1);
             const uint8_t* st = dyn7 + (size_t)s * C::kStage;
+            // x tile: token row r at r * kXP, its 16-byte group g at (g ^ swz(r)) * 16 (the TMA
+            // swizzle: 128B span -> r & 7, 64B span -> (r >> 1) & 3): lanes hit 8 distinct groups
             const uint8_t* xr = st + lane * kXP;
             const double* wc = reinterpret_cast<const double*>(st + C::kXBytes) + warp * EPT;
             double2 wv[kWD][kWP];
@@ -650,13 +664,14 @@ router_v7_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
                 }
             };
             constexpr int kXG = 3;                            // x groups (8 channels) in flight
-            constexpr int kXL = 4;                            // channels widened ahead
             int4 xv[kXG][TPT];
             auto loadx = [&](int g, int slot) {
 #pragma unroll
                 for (int p = 0; p < TPT; ++p)
-                    xv[slot][p] = *reinterpret_cast<const int4*>(xr + p * 32 * kXP + g * 16);
+                    xv[slot][p] = *reinterpret_cast<const int4*>(
+                        xr + p * 32 * kXP + ((g ^ (CW == 64 ? (lane & 7) : ((lane >> 1) & 3))) * 16));
             };
+            constexpr int kXL = 4;                            // channels widened ahead
             double xd[kXL + 1][TPT];
             auto widen = [&](int c, int slot) {   // exact: bf16 -> fp32 (shift) -> fp64
 #pragma unroll
@@ -1018,7 +1033,8 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
                                cudaStream_t st) {
     const int n_tiles = (T + kRouteTile - 1) / kRouteTile;
     if (n_tiles == 0) return cudaSuccess;
-    const char* ver = getenv("MOE_ROUTER");   // 3: round 1's kernel (comparison); 6 / unset: v6
+    // MOE_ROUTER: unset / 7 = v7 (N_e <= 64; v6 above), 6 = v6, 3 = round 1's kernel (comparisons)
+    const char* ver = getenv("MOE_ROUTER");
     int none = 0;
     if (!launches) launches = &none;
     if (ver && atoi(ver) == 3) {
@@ -1031,39 +1047,43 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
         if (cudaGetDevice(&dev) == cudaSuccess)
             cudaDeviceGetAttribute(&sms7, cudaDevAttrMultiProcessorCount, dev);
     }
-    if (ver && atoi(ver) == 7) {
+    if ((!ver || atoi(ver) == 7) && ne <= 64) {   // default for N_e <= 64 (v6 above)
+        const char* ev = getenv("MOE_ROUTER_EPT");
+        const int ept = ev ? atoi(ev) : 0;
         int tpt = 4;
         while (tpt > 1 && (T + kRouteTile * tpt - 1) / (kRouteTile * tpt) < sms7) tpt >>= 1;
         if (const char* e = getenv("MOE_ROUTER_TPT")) {
             const int v = atoi(e);
             if (v == 1 || v == 2 || v == 4) tpt = v;
         }
+        if (tpt == 4 && (ne > 16 || ept == 8)) tpt = 2;   // 4 tokens x 8 experts per lane spill
         const int blocks = (T + kRouteTile * tpt - 1) / (kRouteTile * tpt);
         cudaError_t err = cudaSuccess;
 #define MOE_ROUTER7(E, P, N, CW_)                                                            \
     do {                                                                                     \
         using C7 = RouterV7Cfg<E, P, N, CW_>;                                                \
         if (h % CW_ || C7::kNePad != ne_pad) return cudaErrorInvalidValue;                  \
+        CUtensorMap tmX;                                                                     \
+        if (!make_tmap_box(&tmX, x, (uint64_t)T, (uint64_t)h, CW_, C7::kTok))                \
+            return cudaErrorInvalidValue;                                                    \
         err = cudaFuncSetAttribute(router_v7_kernel<E, P, N, CW_>,                           \
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,              \
                                    (int)C7::kSmem);                                          \
         if (err != cudaSuccess) return err;                                                  \
         router_v7_kernel<E, P, N, CW_><<<blocks, (N + 1) * 32, C7::kSmem, st>>>(             \
-            x, T, h, wr64, ne, k, renorm, idx, gates, tile_counts);                            \
+            tmX, T, h, wr64, ne, k, renorm, idx, gates, tile_counts);                            \
     } while (0)
 #define MOE_ROUTER7_TPT(E, N, CW_)                                                           \
     do {                                                                                     \
         if (tpt == 1) MOE_ROUTER7(E, 1, N, CW_);                                             \
         else if (tpt == 2) MOE_ROUTER7(E, 2, N, CW_);                                        \
-        else MOE_ROUTER7(E, 4, N, CW_);                                                      \
+        else if constexpr (E < 8) MOE_ROUTER7(E, 4, N, CW_);                                 \
     } while (0)
         if (!wr64) return cudaErrorInvalidValue;
         const int ne_pad = router_ne_pad(ne);
         router_widen_kernel<<<(int)std::min<int64_t>(((int64_t)h * ne_pad + 255) / 256, 1184), 256, 0, st>>>(
             wr, h, ne, ne_pad, wr64);
         *launches += 2;
-        const char* ev = getenv("MOE_ROUTER_EPT");
-        const int ept = ev ? atoi(ev) : 0;
         if (ne <= 8 && ept == 1) MOE_ROUTER7_TPT(1, 8, 64);
         else if (ne <= 8 && ept == 4) MOE_ROUTER7_TPT(4, 2, 64);
         else if (ne <= 8 && ept == 8) MOE_ROUTER7_TPT(8, 1, 64);
@@ -1071,13 +1091,12 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
         else if (ne <= 16 && ept == 8) MOE_ROUTER7_TPT(8, 2, 64);
         else if (ne <= 16) MOE_ROUTER7_TPT(4, 4, 64);
         else if (ne <= 32) MOE_ROUTER7_TPT(8, 4, 64);
-        else if (ne <= 64) MOE_ROUTER7_TPT(8, 8, 32);
-        else MOE_ROUTER7_TPT(8, 16, 32);
+        else MOE_ROUTER7_TPT(8, 8, 32);
 #undef MOE_ROUTER7_TPT
 #undef MOE_ROUTER7
         return cudaGetLastError();
     }
-    if (!ver || atoi(ver) == 6) {
+    if (!ver || atoi(ver) == 6 || atoi(ver) == 7) {   // v7 covers N_e <= 64
         *launches += 1;
         // v6 buckets: N_e padded to NW * EPT; tokens per lane TPT (MOE_ROUTER_TPT = 1/2/4): the
         // most tokens per lane (each router broadcast feeds 2 TPT DFMAs) that still leaves every
