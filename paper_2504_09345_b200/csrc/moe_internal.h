@@ -113,8 +113,9 @@ size_t router_ws_doubles(int h, int ne);
 // swizzle) x box_rows, rows past `rows` read as zeros (moe_api.cu).
 bool make_tmap_box(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_cols,
                    uint32_t box_rows);
-// Router v7 block 0: SM clock at entry, cycles to the end of the channel loop / to exit, exit ns.
-cudaError_t router_probe(unsigned long long out[4]);
+// Router v7 block 0: SM clock at entry, cycles to the end of compute warp 0's channel loop / to
+// exit, exit ns, cycles to the last compute warp's loop end, cycles to the end of the top-k.
+cudaError_t router_probe(unsigned long long out[6]);
 // Round 1's router kernel (comparison only: tools/router_bench.cu, MOE_ROUTER=3).
 cudaError_t launch_router_v3(const __nv_bfloat16* x, int T, int h, const __nv_bfloat16* wr,
                              int ne, int k, int renorm, int32_t* idx, float* gates,

@@ -464,7 +464,7 @@ router_v6_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
 
 // Block 0's SM clock at kernel entry / end of the channel loop (compute warp 0) / exit, and the
 // entry-to-exit %globaltimer ns (router_probe(): tools only).
-__device__ unsigned long long g_router_probe[4];
+__device__ unsigned long long g_router_probe[8];
 
 // Router rows widened to fp64 for router v7: wr64[c * ne_pad + e] = (double)wr[e][c] (exact), zero
 // for the padding experts e >= ne.
@@ -479,10 +479,24 @@ router_widen_kernel(const __nv_bfloat16* __restrict__ wr, int h, int ne, int ne_
     }
 }
 
+// Order-preserving 64-bit key of an fp64 logit: larger key = larger logit; -0 and +0 share a key
+// (they compare equal), every NaN maps to 0 -- below -inf, so NaN ranks last (R13) and NaNs tie.
+__device__ __forceinline__ uint64_t logit_key(double l) {
+    uint64_t b = (uint64_t)__double_as_longlong(l);
+    if (b == 0x8000000000000000ull) b = 0;                   // -0 -> +0
+    b = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+    return isnan(l) ? 0ull : b;
+}
+__device__ __forceinline__ double key_logit(uint64_t k) {   // inverse (NaN for key 0)
+    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+
 // Top-k of one token per thread from its fp64 logits (row of lg, shared): insertion of experts
-// 0..ne-1 in ascending order into a k-deep list ranked by (logit desc, index asc), NaN last (R5,
-// R13) -- the same selection and the same fp64 gate arithmetic as topk_tile (R3), without the
-// warp shuffles (a warp-per-token selection costs k x 5 dependent shuffle rounds per token).
+// 0..ne-1 in ascending order into a k-deep list ranked by (key desc, index asc) -- the order
+// ranks_above defines (R5, R13) -- on 64-bit integer keys, every list index a compile-time
+// constant (registers only).  Gates from the selected fp64 logits exactly as in topk_tile (R3).
+// (A warp-per-token shuffle selection with fp64 compares and dynamically indexed lists, and a
+// token-per-thread scan with fp64 compares, both took as long as the channel loop at C4.)
 template <int TPT>
 __device__ __forceinline__ void topk_rows(const double* lg, int pitch, int t0, int T, int ne,
                                           int k, int renorm, int32_t* __restrict__ idx_out,
@@ -493,45 +507,35 @@ __device__ __forceinline__ void topk_rows(const double* lg, int pitch, int t0, i
         const int t = t0 + tt;
         if (t >= T) break;
         const double* row = lg + tt * pitch;
-        double sl[kMaxTopK];
+        uint64_t sk[kMaxTopK];
         int se[kMaxTopK];
 #pragma unroll
         for (int j = 0; j < kMaxTopK; ++j) {
-            sl[j] = 0.0;
-            se[j] = -1;   // empty slot
+            sk[j] = 0ull;
+            se[j] = 0x7fffffff;   // empty: below every expert, NaN included
         }
-        double kv = 0.0;   // the current k-th entry (valid once k experts are in the list)
-        int ke = -1;
         for (int e = 0; e < ne; ++e) {
-            double cv = row[e];
-            if (e >= k && !ranks_above(cv, e, kv, ke)) continue;   // below the k-th: no change
+            uint64_t ck = logit_key(row[e]);
             int ce = e;
 #pragma unroll
             for (int j = 0; j < kMaxTopK; ++j) {
-                if (j < k && (se[j] < 0 || ranks_above(cv, ce, sl[j], se[j]))) {
-                    const double tv = sl[j];
-                    const int te = se[j];
-                    sl[j] = cv;
-                    se[j] = ce;
-                    cv = tv;
-                    ce = te;
-                }
+                const bool up = j < k && (ck > sk[j] || (ck == sk[j] && ce < se[j]));
+                const uint64_t tk = sk[j];
+                const int te = se[j];
+                sk[j] = up ? ck : tk;
+                se[j] = up ? ce : te;
+                ck = up ? tk : ck;
+                ce = up ? te : ce;
             }
-#pragma unroll
-            for (int j = 0; j < kMaxTopK; ++j)
-                if (j == k - 1) {
-                    kv = sl[j];
-                    ke = se[j];
-                }
         }
-        const double m = sl[0];
+        const double m = key_logit(sk[0]);
         double ex[kMaxTopK];
         double z = 0.0;
 #pragma unroll
         for (int j = 0; j < kMaxTopK; ++j) {
             ex[j] = 0.0;
             if (j < k) {
-                ex[j] = exp(sl[j] - m);
+                ex[j] = exp(key_logit(sk[j]) - m);
                 if (renorm) z += ex[j];
             }
         }
@@ -606,6 +610,7 @@ router_v7_kernel(const __grid_constant__ CUtensorMap tmX, int T, int h,
     if (probe) {
         clk0 = clock64();
         ns0 = ptx::globaltimer_ns();
+        g_router_probe[4] = 0;
     }
     for (int e = tid; e < TPT * kMaxExperts; e += kThr) cnt[e / kMaxExperts][e % kMaxExperts] = 0;
     if (tid == 0) {
@@ -714,6 +719,7 @@ router_v7_kernel(const __grid_constant__ CUtensorMap tmX, int T, int h,
             if (lane == 0) ptx::mbar_arrive(&empty[s]);
         }
         if (probe) g_router_probe[1] = clock64() - clk0;
+        if (blockIdx.x == 0 && lane == 0) atomicMax(&g_router_probe[4], (unsigned long long)clock64());
     }
     __syncthreads();   // every stage consumed: the ring's memory holds the logits now
     double* lg = reinterpret_cast<double*>(dyn7);   // [kTok][kLgPitch]
@@ -726,6 +732,7 @@ router_v7_kernel(const __grid_constant__ CUtensorMap tmX, int T, int h,
     __syncthreads();
     topk_rows<TPT>(lg, C::kLgPitch, t0, T, ne, k, renorm, idx_out, gate_out, cnt, tid, kThr);
     __syncthreads();
+    if (probe) g_router_probe[5] = clock64() - clk0;
     const int n_tiles = (T + kRouteTile - 1) / kRouteTile;
 #pragma unroll
     for (int p = 0; p < TPT; ++p) {
@@ -734,6 +741,7 @@ router_v7_kernel(const __grid_constant__ CUtensorMap tmX, int T, int h,
             for (int e = tid; e < ne; e += kThr) tile_counts[(size_t)tile * ne + e] = cnt[p][e];
     }
     if (probe) {
+        g_router_probe[4] -= clk0;
         g_router_probe[0] = clk0;
         g_router_probe[2] = clock64() - clk0;
         g_router_probe[3] = ptx::globaltimer_ns() - ns0;
@@ -1024,7 +1032,7 @@ static int router_ne_pad(int ne) {
 size_t router_ws_doubles(int h, int ne) { return (size_t)h * router_ne_pad(ne); }
 
 cudaError_t router_probe(unsigned long long out[4]) {
-    return cudaMemcpyFromSymbol(out, g_router_probe, 4 * sizeof(unsigned long long));
+    return cudaMemcpyFromSymbol(out, g_router_probe, 6 * sizeof(unsigned long long));
 }
 
 cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_bfloat16* wr,

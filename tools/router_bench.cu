@@ -79,9 +79,9 @@ int main(int argc, char** argv) {
            getenv("MOE_ROUTER_TPT") ? getenv("MOE_ROUTER_TPT") : "auto",
            getenv("MOE_ROUTER_LANES") ? getenv("MOE_ROUTER_LANES") : "auto", 1e3 * ms / iters,
            2 * dfma / (ms / iters * 1e-3) / 1e12, cudaGetErrorString(err), bad, a.size());
-    unsigned long long pr[4] = {0, 0, 0, 0};
+    unsigned long long pr[6] = {0, 0, 0, 0, 0, 0};
     if (getenv("MOE_ROUTER") && atoi(getenv("MOE_ROUTER")) == 7 && moe::router_probe(pr) == cudaSuccess && pr[3])
-        printf("    block 0: %llu cycles (loop %llu = %.1f per channel), %.2f us, %.0f MHz\n", pr[2], pr[1],
-               (double)pr[1] / h, pr[3] * 1e-3, (double)pr[2] / pr[3] * 1e3);
+        printf("    block 0: %llu cycles (loop %llu = %.1f per channel, last warp %llu, top-k done %llu), %.2f us, %.0f MHz\n",
+               pr[2], pr[1], (double)pr[1] / h, pr[4], pr[5], pr[3] * 1e-3, (double)pr[2] / pr[3] * 1e3);
     return 0;
 }
