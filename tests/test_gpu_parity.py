@@ -723,3 +723,40 @@ def test_ipc_connect_rejects_mismatched_blob():
         assert e.value.status == MOE_E_INVAL
     finally:
         r0.close()
+
+
+@pytest.mark.parametrize("ver", ["6", "7"])
+def test_router_special_values(ver, monkeypatch):
+    """Routing on inputs with special bf16 values (R5, R13): all-zero rows (every logit ties ->
+    experts 0..k-1), -0.0, subnormals, +-inf (logits +-inf or NaN -> NaN ranks last), and a NaN
+    channel.  idx must equal the oracle's bit for bit on every token, gates wherever the oracle's
+    are finite (router v7's integer keys and v6's fp64 compares implement the same order)."""
+    monkeypatch.setenv("MOE_ROUTER", ver)
+    cfg = synth.MoEConfig("custom", 23, 128, 256, 8, 2, 64)
+    inp = synth.gen_inputs(cfg)
+    x = inp.x.copy()                      # uint16 bf16 bits [T, h]
+    x[0] = 0                              # +0 row: all logits 0
+    x[1] = 0x8000                         # -0 row
+    x[2, ::2] = 0x8000                    # half the channels -0
+    x[3] = (np.arange(x.shape[1]) % 127 + 1).astype(np.uint16)            # subnormals
+    x[4] = x[4] | 0x8000                  # all negative
+    x[5, 7] = 0x7F80                      # +inf in one channel
+    x[6, 9] = 0xFF80                      # -inf in one channel
+    x[7, 11] = 0x7FC0                     # NaN in one channel
+    x[8, :] = x[9, :]                     # duplicate tokens
+    r = inp.router.copy()
+    r[6] = r[2]                           # duplicate router rows: lower index wins the tie
+    inp2 = dataclasses.replace(inp, x=x, router=r)
+    run = GpuRun(inp2)
+    try:
+        out, idx, gates = run.run()
+        _, idx_ref, g_ref = oracle.forward(inp2.x, inp2.router, inp2.w1, inp2.w3, inp2.w2,
+                                           cfg.top_k, cfg.num_shared)
+        assert np.array_equal(idx.cpu().numpy(), idx_ref)
+        assert (idx_ref[0] == [0, 1]).all() and (idx_ref[1] == [0, 1]).all()
+        g = gates.cpu().numpy()
+        fin = np.isfinite(g_ref)
+        assert np.array_equal(np.isfinite(g), fin)
+        assert np.max(np.abs(g[fin] - g_ref[fin])) <= 1e-6
+    finally:
+        run.close()

@@ -74,13 +74,13 @@ int main(int argc, char** argv) {
     for (size_t i = 0; i < a.size(); ++i) bad += (a[i] != b[i]) || (memcmp(&ga[i], &gb[i], 4) != 0);
     const double dfma = (double)T * ne * h;
     printf("router T=%d h=%d N_e=%d k=%d [MOE_ROUTER=%s EPT=%s TPT=%s LANES=%s]: %.1f us  %.2f TFLOP/s fp64 (%s; %zu of %zu idx/gates differ from v3)\n",
-           T, h, ne, k, getenv("MOE_ROUTER") ? getenv("MOE_ROUTER") : "6",
+           T, h, ne, k, getenv("MOE_ROUTER") ? getenv("MOE_ROUTER") : "default",
            getenv("MOE_ROUTER_EPT") ? getenv("MOE_ROUTER_EPT") : "auto",
            getenv("MOE_ROUTER_TPT") ? getenv("MOE_ROUTER_TPT") : "auto",
            getenv("MOE_ROUTER_LANES") ? getenv("MOE_ROUTER_LANES") : "auto", 1e3 * ms / iters,
            2 * dfma / (ms / iters * 1e-3) / 1e12, cudaGetErrorString(err), bad, a.size());
     unsigned long long pr[6] = {0, 0, 0, 0, 0, 0};
-    if (getenv("MOE_ROUTER") && atoi(getenv("MOE_ROUTER")) == 7 && moe::router_probe(pr) == cudaSuccess && pr[3])
+    if ((!getenv("MOE_ROUTER") || atoi(getenv("MOE_ROUTER")) == 7) && ne <= 64 && moe::router_probe(pr) == cudaSuccess && pr[3])
         printf("    block 0: %llu cycles (loop %llu = %.1f per channel, last warp %llu, top-k done %llu), %.2f us, %.0f MHz\n",
                pr[2], pr[1], (double)pr[1] / h, pr[4], pr[5], pr[3] * 1e-3, (double)pr[2] / pr[3] * 1e3);
     return 0;
