@@ -497,15 +497,31 @@ __device__ __forceinline__ double key_logit(uint64_t k) {   // inverse (NaN for 
 // constant (registers only).  Gates from the selected fp64 logits exactly as in topk_tile (R3).
 // (A warp-per-token shuffle selection with fp64 compares and dynamically indexed lists, and a
 // token-per-thread scan with fp64 compares, both took as long as the channel loop at C4.)
-template <int TPT>
+template <int TPT, int G>
 __device__ __forceinline__ void topk_rows(const double* lg, int pitch, int t0, int T, int ne,
                                           int k, int renorm, int32_t* __restrict__ idx_out,
                                           float* __restrict__ gate_out,
                                           int (*cnt)[kMaxExperts], int tid, int nthr) {
+    // G threads (adjacent lanes) per token: thread `sub` scans experts sub, sub + G, ... into its
+    // own list, then the G lists merge by xor shuffles (the order is total, so any partition of
+    // the experts merges to the same top-k).  nthr and kTok * G are multiples of 32: every lane
+    // of a warp runs the same trip count (full-mask shuffles).
     constexpr int kTok = kRouteTile * TPT;
-    for (int tt = tid; tt < kTok; tt += nthr) {
+    auto insert = [&](uint64_t (&sk)[kMaxTopK], int (&se)[kMaxTopK], uint64_t ck, int ce) {
+#pragma unroll
+        for (int j = 0; j < kMaxTopK; ++j) {
+            const bool up = j < k && (ck > sk[j] || (ck == sk[j] && ce < se[j]));
+            const uint64_t tk = sk[j];
+            const int te = se[j];
+            sk[j] = up ? ck : tk;
+            se[j] = up ? ce : te;
+            ck = up ? tk : ck;
+            ce = up ? te : ce;
+        }
+    };
+    for (int u = tid; u < kTok * G; u += nthr) {
+        const int tt = u / G, sub = u % G;
         const int t = t0 + tt;
-        if (t >= T) break;
         const double* row = lg + tt * pitch;
         uint64_t sk[kMaxTopK];
         int se[kMaxTopK];
@@ -514,20 +530,22 @@ __device__ __forceinline__ void topk_rows(const double* lg, int pitch, int t0, i
             sk[j] = 0ull;
             se[j] = 0x7fffffff;   // empty: below every expert, NaN included
         }
-        for (int e = 0; e < ne; ++e) {
-            uint64_t ck = logit_key(row[e]);
-            int ce = e;
+        for (int e = sub; e < ne; e += G) insert(sk, se, logit_key(row[e]), e);
+        if constexpr (G > 1) {
 #pragma unroll
-            for (int j = 0; j < kMaxTopK; ++j) {
-                const bool up = j < k && (ck > sk[j] || (ck == sk[j] && ce < se[j]));
-                const uint64_t tk = sk[j];
-                const int te = se[j];
-                sk[j] = up ? ck : tk;
-                se[j] = up ? ce : te;
-                ck = up ? tk : ck;
-                ce = up ? te : ce;
+            for (int off = 1; off < G; off <<= 1) {
+                uint64_t pk[kMaxTopK];
+                int pe[kMaxTopK];
+#pragma unroll
+                for (int j = 0; j < kMaxTopK; ++j) {
+                    pk[j] = __shfl_xor_sync(0xffffffffu, sk[j], off);
+                    pe[j] = __shfl_xor_sync(0xffffffffu, se[j], off);
+                }
+#pragma unroll
+                for (int j = 0; j < kMaxTopK; ++j) insert(sk, se, pk[j], pe[j]);
             }
         }
+        if (t >= T || sub != 0) continue;
         const double m = key_logit(sk[0]);
         double ex[kMaxTopK];
         double z = 0.0;
@@ -552,23 +570,22 @@ __device__ __forceinline__ void topk_rows(const double* lg, int pitch, int t0, i
     }
 }
 
-// Router v7: the same one-FMA-chain-per-logit arithmetic (R6) with the per-chunk staging taken off
-// the compute warps.  The router rows are widened once per call into an fp64 [channel][expert]
-// workspace (router_widen_kernel, zero rows pad N_e); a producer warp runs a S-deep mbarrier ring
-// of 1-D bulk copies (cp.async.bulk, TMA engine) -- per chunk of CW channels one copy per token
-// row (raw bf16, rows at a 16-byte-padded pitch so the lanes' 16-byte reads are conflict-free)
-// and one copy of the chunk's fp64 router rows -- so it never waits on a load itself (a first
-// version widened the router chunk in the producer from global loads: two dependent L2 round
-// trips per chunk, 110 us at C1 whatever the chain count); the NW compute warps only wait on
-// full[s], run their chains and release the stage (empty[s]).  x is widened in registers at the point of use (an exact
-// bf16 -> fp32 shift and F2F.F64.F32) instead of being stored and re-read as fp64: per channel a
-// lane reads 2 B of x instead of 8 and no compute warp ever takes a block-wide barrier inside
-// the channel loop (v6 at C1: one __syncthreads + a widening pass per 64 channels, ~28 cycles
-// per channel step for one warp per SM sub-partition).
-//   * block = TPT x 32 tokens (lane l: tokens l, l+32, ...), warp w < NW owns experts
-//     [w*EPT, (w+1)*EPT) (zero rows pad N_e to NW*EPT), warp NW is the producer;
-//   * per channel and compute warp: TPT conversions + EPT/2 double2 broadcasts for TPT*EPT DFMAs;
-//   * top-k per thread (topk_rows).
+// Router v7: the same one-FMA-chain-per-logit arithmetic (R6) with the staging taken off the
+// compute warps (DESIGN.md §6 has the measurements behind each choice).
+//   * the router rows are widened once per call into an fp64 [channel][N_e padded] workspace
+//     (router_widen_kernel, zero rows pad N_e);
+//   * one producer thread runs an S-deep mbarrier ring: per chunk of CW channels ONE 2-D TMA box
+//     of x ([kTok tokens][CW channels] bf16, 128-B / 64-B swizzle, rows >= T read as zeros) and
+//     ONE bulk copy of the chunk's fp64 router rows (a copy per token row made the TMA engine's
+//     per-copy cost the limit: ~33 cycles per channel at C1);
+//   * NW compute warps (lane = token, TPT tokens per lane; warp w = experts [w*EPT, (w+1)*EPT))
+//     wait on full[s], run their chains and release the stage (empty[s]); no block barrier in
+//     the channel loop.  x stays bf16 in shared memory (2 B per token-channel instead of v6's 8)
+//     and is widened in registers (exact bf16 -> fp32 shift, F2F.F64.F32); router operands are
+//     read kWD channels ahead, x one 8-channel group ahead;
+//   * the stage pointer is aligned by an offset from the shared array so operand reads stay LDS
+//     (an integer-rebuilt pointer compiled to generic LD: 22 vs 16 cycles per channel at C1);
+//   * top-k per thread on 64-bit integer keys (topk_rows; 4 threads per token above 16 experts).
 template <int EPT, int TPT, int NW, int CW>
 struct RouterV7Cfg {
     static_assert(CW == 64 || CW == 32, "x chunk = one 128-B (64 ch) or 64-B (32 ch) swizzle span");
@@ -730,7 +747,10 @@ router_v7_kernel(const __grid_constant__ CUtensorMap tmX, int T, int h,
             for (int i = 0; i < EPT; ++i) lg[(p * 32 + lane) * C::kLgPitch + warp * EPT + i] = acc[p][i];
     }
     __syncthreads();
-    topk_rows<TPT>(lg, C::kLgPitch, t0, T, ne, k, renorm, idx_out, gate_out, cnt, tid, kThr);
+    if (ne > 16)   // 4 threads per token: a serial scan of 64 experts took 19% of C4's block time
+        topk_rows<TPT, 4>(lg, C::kLgPitch, t0, T, ne, k, renorm, idx_out, gate_out, cnt, tid, kThr);
+    else
+        topk_rows<TPT, 1>(lg, C::kLgPitch, t0, T, ne, k, renorm, idx_out, gate_out, cnt, tid, kThr);
     __syncthreads();
     if (probe) g_router_probe[5] = clock64() - clk0;
     const int n_tiles = (T + kRouteTile - 1) / kRouteTile;
