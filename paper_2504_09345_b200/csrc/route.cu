@@ -1075,7 +1075,8 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
         if (cudaGetDevice(&dev) == cudaSuccess)
             cudaDeviceGetAttribute(&sms7, cudaDevAttrMultiProcessorCount, dev);
     }
-    if ((!ver || atoi(ver) == 7) && ne <= 64) {   // default for N_e <= 64 (v6 above)
+    const int v7_max = getenv("MOE_ROUTER_V7_MAX") ? atoi(getenv("MOE_ROUTER_V7_MAX")) : 64;
+    if ((!ver || atoi(ver) == 7) && ne <= v7_max) {   // default for N_e <= 64 (v6 above)
         const char* ev = getenv("MOE_ROUTER_EPT");
         const int ept = ev ? atoi(ev) : 0;
         int tpt = 4;
@@ -1119,7 +1120,8 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
         else if (ne <= 16 && ept == 8) MOE_ROUTER7_TPT(8, 2, 64);
         else if (ne <= 16) MOE_ROUTER7_TPT(4, 4, 64);
         else if (ne <= 32) MOE_ROUTER7_TPT(8, 4, 64);
-        else MOE_ROUTER7_TPT(8, 8, 32);
+        else if (ne <= 64) MOE_ROUTER7_TPT(8, 8, 32);
+        else MOE_ROUTER7_TPT(8, 16, 32);
 #undef MOE_ROUTER7_TPT
 #undef MOE_ROUTER7
         return cudaGetLastError();
