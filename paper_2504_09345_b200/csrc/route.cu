@@ -260,208 +260,6 @@ router_topk_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
     }
 }
 
-// cp.async of 16 bytes global -> shared; src_bytes = 0 zero-fills the destination.
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(ptx::smem_u32(smem)),
-                 "l"(gmem), "r"(src_bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// Router v6: the same one-FMA-chain-per-logit arithmetic (reading R6); every operand is widened
-// to fp64 ONCE per block, when its chunk is staged, so the inner loop is shared-memory loads and
-// DFMAs only (v5 re-widened each token's x in every warp: ~12 instructions per channel per warp,
-// ncu at C1: issue-bound at 28% slot use with 4 warps per SM).
-//   * a block = TPT x 32 tokens and NW warps; warp w owns experts [w*EPT, (w+1)*EPT) (zero rows
-//     pad N_e to NW*EPT), lane l owns tokens l, l+32, ...: TPT*EPT independent chains per lane;
-//   * channels are consumed in chunks of CW.  Raw bf16 chunks arrive by cp.async into a
-//     kStages-deep ring, kStages-1 chunks ahead (at C1 a chunk's DFMAs take less than a DRAM
-//     round trip, so one chunk of look-ahead left every chunk waiting on memory: ncu
-//     long-scoreboard); each thread widens the vectors IT copied (no barrier between the copy and
-//     the widening) into a double-buffered fp64 tile -- x as [channel pair][token] double2 (one
-//     16-byte read gives a lane two channels of one token, conflict-free), the router rows as
-//     [channel][expert] (double2 broadcasts) -- one __syncthreads per chunk;
-//   * per channel pair and warp: TPT x-reads (4 wavefronts each) + EPT double2 broadcasts for
-//     2*TPT*EPT DFMAs.
-constexpr int kRouterStages = 4;
-
-// Channels per chunk: the largest power of two <= 128 whose fp64 double buffer (16 B per channel
-// per token / expert) + raw bf16 ring (kRouterStages x 2 B) fit 96 KB -- two blocks per SM.
-constexpr int router_v6_cw(int rows) {
-    int cw = 128;
-    while (cw > 8 && (16 + 2 * kRouterStages) * cw * rows > 96 * 1024) cw >>= 1;
-    return cw;
-}
-
-// Channel pairs of operands prefetched into registers: ~48 registers' worth (x: 4 TPT, router:
-// 4 max(EPT, 2) per pair), at least 1.
-constexpr int router_v6_prefetch(int ept, int tpt) {
-    const int per = 4 * tpt + 4 * (ept >= 2 ? ept : 2);
-    return 48 / per >= 4 ? 4 : (48 / per >= 2 ? 2 : 1);   // a power of two: divides CW / 2
-}
-
-template <int EPT, int TPT, int NW, int CW, int kPf>
-__global__ void __launch_bounds__(NW * 32, 16 / NW)
-router_v6_kernel(const __nv_bfloat16* __restrict__ x, int T, int h,
-                 const __nv_bfloat16* __restrict__ wr, int ne, int k, int renorm,
-                 int32_t* __restrict__ idx_out, float* __restrict__ gate_out,
-                 int32_t* __restrict__ tile_counts) {
-    static_assert((EPT == 1 || EPT % 2 == 0) && CW % 8 == 0 && kPf >= 1, "shape");
-    constexpr int kTok = kRouteTile * TPT;
-    constexpr int kThr = NW * 32;
-    constexpr int kNePad = NW * EPT;
-    constexpr int kNXV = kTok * (CW / 8);              // 16-byte x vectors per chunk
-    constexpr int kNWV = kNePad * (CW / 8);            // 16-byte router vectors per chunk
-    constexpr int kNV = kNXV + kNWV;
-    constexpr int kVT = (kNV + kThr - 1) / kThr;       // vectors per thread
-    extern __shared__ __align__(16) double dyn[];
-    __shared__ int cnt[TPT][kMaxExperts];
-    double2* xs = reinterpret_cast<double2*>(dyn);                 // [2][CW/2][kTok]
-    double* ws = dyn + 2 * CW * kTok;                              // [2][CW][kNePad]
-    int4* raw = reinterpret_cast<int4*>(ws + 2 * CW * kNePad);     // [kRouterStages][kNV]
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int t0 = blockIdx.x * kTok;
-    for (int e = tid; e < TPT * kMaxExperts; e += kThr) cnt[e / kMaxExperts][e % kMaxExperts] = 0;
-
-    // vector v < kNXV: token v % kTok, channels (v / kTok)*8 ..; else router row (v - kNXV) %
-    // kNePad.  Consecutive threads take consecutive tokens / experts at one 8-channel group, so
-    // the widened stores hit consecutive shared-memory words.
-    auto issue = [&](int c0, int stage) {
-        int4* rs = raw + (size_t)stage * kNV;
-#pragma unroll
-        for (int j = 0; j < kVT; ++j) {
-            const int v = tid + j * kThr;
-            if (v < kNXV) {
-                const int t = t0 + v % kTok, cc = (v / kTok) * 8;
-                cp_async16(rs + v, x + (size_t)(t < T ? t : 0) * h + c0 + cc, t < T ? 16 : 0);
-            } else if (v < kNV) {
-                const int u = v - kNXV, e = u % kNePad, cc = (u / kNePad) * 8;
-                cp_async16(rs + v, wr + (size_t)(e < ne ? e : 0) * h + c0 + cc, e < ne ? 16 : 0);
-            }
-        }
-        cp_async_commit();
-    };
-    auto widen = [&](int stage, int b) {   // this thread's own vectors: no barrier needed
-        const int4* rs = raw + (size_t)stage * kNV;
-        double2* xb = xs + (size_t)b * (CW / 2) * kTok;
-        double* wb = ws + (size_t)b * CW * kNePad;
-        double d[8];
-#pragma unroll
-        for (int j = 0; j < kVT; ++j) {
-            const int v = tid + j * kThr;
-            if (v < kNXV) {
-                const int t = v % kTok, c2 = (v / kTok) * 4;
-                bf16x8_to_f64(rs[v], d);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) xb[(c2 + q) * kTok + t] = make_double2(d[2 * q], d[2 * q + 1]);
-            } else if (v < kNV) {
-                const int u = v - kNXV, e = u % kNePad, cc = (u / kNePad) * 8;
-                bf16x8_to_f64(rs[v], d);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) wb[(cc + q) * kNePad + e] = d[q];
-            }
-        }
-    };
-
-    const int n_chunks = h / CW;
-#pragma unroll
-    for (int c = 0; c < kRouterStages - 1; ++c) {
-        if (c < n_chunks) issue(c * CW, c);
-        else cp_async_commit();   // empty group: the wait counts below stay uniform
-    }
-    cp_async_wait<kRouterStages - 2>();   // chunk 0 landed
-    widen(0, 0);
-    __syncthreads();
-    double acc[TPT][EPT];
-#pragma unroll
-    for (int p = 0; p < TPT; ++p)
-#pragma unroll
-        for (int i = 0; i < EPT; ++i) acc[p][i] = 0.0;
-    for (int ch = 0; ch < n_chunks; ++ch) {
-        const int b = ch & 1;
-        // chunk ch + kStages - 1 into the ring slot chunk ch - 1 used (widened last iteration)
-        if (ch + kRouterStages - 1 < n_chunks)
-            issue((ch + kRouterStages - 1) * CW, (ch + kRouterStages - 1) % kRouterStages);
-        else
-            cp_async_commit();
-        const double2* xb = xs + (size_t)b * (CW / 2) * kTok + lane;
-        const double* wb = ws + (size_t)b * CW * kNePad + warp * EPT;
-        // operands of channel pair c2 + kPf are loaded while pair c2's DFMAs issue (explicit
-        // register prefetch: at C1 one warp per SM sub-partition otherwise waited a shared-memory
-        // round trip per channel -- ncu short-scoreboard / wait stalls, ~37 cycles per channel)
-        constexpr int kWP = EPT >= 2 ? EPT / 2 : 1;   // router loads per channel
-        double2 xv[kPf][TPT];
-        double2 wv[kPf][2][kWP];
-        auto fetch = [&](int c2, int slot) {
-#pragma unroll
-            for (int p = 0; p < TPT; ++p) xv[slot][p] = xb[c2 * kTok + p * 32];
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const double* wrow = wb + (2 * c2 + q) * kNePad;
-                if constexpr (EPT == 1) {
-                    wv[slot][q][0].x = wrow[0];
-                } else {
-#pragma unroll
-                    for (int i = 0; i < kWP; ++i) wv[slot][q][i] = reinterpret_cast<const double2*>(wrow)[i];
-                }
-            }
-        };
-#pragma unroll
-        for (int j = 0; j < kPf; ++j) fetch(j, j);
-        // pairs c2 + j live in slot j: consumed, then refilled with pair c2 + j + kPf; fully
-        // unrolled, so the slots are static registers (no rotation copies: a rotating prefetch
-        // cost ~6 moves per channel) and the refill bound is resolved at compile time (a rolled
-        // loop was measured slower: C1 90 vs 80 us)
-#pragma unroll
-        for (int c2 = 0; c2 < CW / 2; c2 += kPf) {
-#pragma unroll
-            for (int j = 0; j < kPf; ++j) {
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {   // channel 2*(c2+j) + q: ascending in every chain
-#pragma unroll
-                    for (int i = 0; i < kWP; ++i) {
-#pragma unroll
-                        for (int p = 0; p < TPT; ++p) {
-                            const double xq = q ? xv[j][p].y : xv[j][p].x;
-                            if constexpr (EPT == 1) {
-                                acc[p][0] = fma(xq, wv[j][q][0].x, acc[p][0]);
-                            } else {
-                                acc[p][2 * i] = fma(xq, wv[j][q][i].x, acc[p][2 * i]);
-                                acc[p][2 * i + 1] = fma(xq, wv[j][q][i].y, acc[p][2 * i + 1]);
-                            }
-                        }
-                    }
-                }
-                if (c2 + j + kPf < CW / 2) fetch(c2 + j + kPf, j);
-            }
-        }
-        if (ch + 1 < n_chunks) {   // fp64 buffer b ^ 1 was consumed before the last barrier
-            cp_async_wait<kRouterStages - 2>();   // chunk ch + 1 landed
-            widen((ch + 1) % kRouterStages, b ^ 1);
-        }
-        __syncthreads();
-    }
-    cp_async_wait<0>();
-    double* lg = dyn;   // [kTok][kNePad] logits (the x buffers, all reads done)
-#pragma unroll
-    for (int p = 0; p < TPT; ++p)
-#pragma unroll
-        for (int i = 0; i < EPT; ++i) lg[(p * 32 + lane) * kNePad + warp * EPT + i] = acc[p][i];
-    __syncthreads();
-    topk_tile<TPT>(lg, kNePad, t0, T, ne, k, renorm, idx_out, gate_out, cnt, warp, NW, lane);
-    __syncthreads();
-    const int n_tiles = (T + kRouteTile - 1) / kRouteTile;
-#pragma unroll
-    for (int p = 0; p < TPT; ++p) {
-        const int tile = blockIdx.x * TPT + p;
-        if (tile < n_tiles)
-            for (int e = tid; e < ne; e += kThr) tile_counts[(size_t)tile * ne + e] = cnt[p][e];
-    }
-}
-
 // Block 0's SM clock at kernel entry / end of the channel loop (compute warp 0) / exit, and the
 // entry-to-exit %globaltimer ns (router_probe(): tools only).
 __device__ unsigned long long g_router_probe[8];
@@ -580,7 +378,7 @@ __device__ __forceinline__ void topk_rows(const double* lg, int pitch, int t0, i
 //     per-copy cost the limit: ~33 cycles per channel at C1);
 //   * NW compute warps (lane = token, TPT tokens per lane; warp w = experts [w*EPT, (w+1)*EPT))
 //     wait on full[s], run their chains and release the stage (empty[s]); no block barrier in
-//     the channel loop.  x stays bf16 in shared memory (2 B per token-channel instead of v6's 8)
+//     the channel loop.  x stays bf16 in shared memory (2 B per token-channel instead of the 8 of round 2's v6 kernel)
 //     and is widened in registers (exact bf16 -> fp32 shift, F2F.F64.F32); router operands are
 //     read kWD channels ahead, x one 8-channel group ahead;
 //   * the stage pointer is aligned by an offset from the shared array so operand reads stay LDS
@@ -1061,7 +859,7 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
                                cudaStream_t st) {
     const int n_tiles = (T + kRouteTile - 1) / kRouteTile;
     if (n_tiles == 0) return cudaSuccess;
-    // MOE_ROUTER: unset / 7 = v7 (N_e <= 64; v6 above), 6 = v6, 3 = round 1's kernel (comparisons)
+    // MOE_ROUTER: unset / 7 = v7, 3 = round 1's kernel (comparisons; N_e <= 64)
     const char* ver = getenv("MOE_ROUTER");
     int none = 0;
     if (!launches) launches = &none;
@@ -1069,18 +867,17 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
         *launches += 1;
         return launch_router_v3(x, T, h, wr, ne, k, renorm, idx, gates, tile_counts, st);
     }
-    int sms7 = 148;
+    int sms = 148;
     {
         int dev = 0;
         if (cudaGetDevice(&dev) == cudaSuccess)
-            cudaDeviceGetAttribute(&sms7, cudaDevAttrMultiProcessorCount, dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const int v7_max = getenv("MOE_ROUTER_V7_MAX") ? atoi(getenv("MOE_ROUTER_V7_MAX")) : 64;
-    if ((!ver || atoi(ver) == 7) && ne <= v7_max) {   // default for N_e <= 64 (v6 above)
+    if (!ver || atoi(ver) == 7) {
         const char* ev = getenv("MOE_ROUTER_EPT");
         const int ept = ev ? atoi(ev) : 0;
         int tpt = 4;
-        while (tpt > 1 && (T + kRouteTile * tpt - 1) / (kRouteTile * tpt) < sms7) tpt >>= 1;
+        while (tpt > 1 && (T + kRouteTile * tpt - 1) / (kRouteTile * tpt) < sms) tpt >>= 1;
         if (const char* e = getenv("MOE_ROUTER_TPT")) {
             const int v = atoi(e);
             if (v == 1 || v == 2 || v == 4) tpt = v;
@@ -1106,7 +903,10 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
     do {                                                                                     \
         if (tpt == 1) MOE_ROUTER7(E, 1, N, CW_);                                             \
         else if (tpt == 2) MOE_ROUTER7(E, 2, N, CW_);                                        \
-        else if constexpr (E < 8) MOE_ROUTER7(E, 4, N, CW_);                                 \
+        else {                                                                               \
+            if constexpr (E < 8) MOE_ROUTER7(E, 4, N, CW_);                                  \
+            else return cudaErrorInvalidValue;   /* 4 x 8 chains per lane: capped above */   \
+        }                                                                                    \
     } while (0)
         if (!wr64) return cudaErrorInvalidValue;
         const int ne_pad = router_ne_pad(ne);
@@ -1124,60 +924,6 @@ cudaError_t launch_router_topk(const __nv_bfloat16* x, int T, int h, const __nv_
         else MOE_ROUTER7_TPT(8, 16, 32);
 #undef MOE_ROUTER7_TPT
 #undef MOE_ROUTER7
-        return cudaGetLastError();
-    }
-    if (!ver || atoi(ver) == 6 || atoi(ver) == 7) {   // v7 covers N_e <= 64
-        *launches += 1;
-        // v6 buckets: N_e padded to NW * EPT; tokens per lane TPT (MOE_ROUTER_TPT = 1/2/4): the
-        // most tokens per lane (each router broadcast feeds 2 TPT DFMAs) that still leaves every
-        // SM a block -- below that the chains are latency-bound and want more warps instead
-        // (measured, profiles/r02/router: C1 4096 tokens TPT 1 80 us vs 2 133; C4 TPT 4 551 us
-        // vs 1 783; DBRX TPT 2 344 vs 1 449; 131k x 8 experts TPT 4 1005 vs 1 1375)
-        int sms = 148;
-        {
-            int dev = 0;
-            if (cudaGetDevice(&dev) == cudaSuccess)
-                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        }
-        int tpt = 4;
-        while (tpt > 1 && (T + kRouteTile * tpt - 1) / (kRouteTile * tpt) < sms) tpt >>= 1;
-        if (const char* e = getenv("MOE_ROUTER_TPT")) {
-            const int v = atoi(e);
-            if (v == 1 || v == 2 || v == 4) tpt = v;
-        }
-        const int ktok = kRouteTile * tpt;
-        const int blocks = (T + ktok - 1) / ktok;
-        cudaError_t err = cudaSuccess;
-#define MOE_ROUTER6(E, P, N)                                                                 \
-    do {                                                                                     \
-        constexpr int cw_ = router_v6_cw(kRouteTile * P + N * E);                            \
-        const size_t dyn_ = std::max<size_t>(                                                \
-            (size_t)(16 + 2 * kRouterStages) * cw_ * (kRouteTile * P + N * E),               \
-            sizeof(double) * (size_t)(kRouteTile * P) * (N * E));                            \
-        if (h % cw_) return cudaErrorInvalidValue;                                           \
-        constexpr int pf_ = router_v6_prefetch(E, P);                                        \
-        err = cudaFuncSetAttribute(router_v6_kernel<E, P, N, cw_, pf_>,                      \
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_);  \
-        if (err != cudaSuccess) return err;                                                  \
-        router_v6_kernel<E, P, N, cw_, pf_><<<blocks, N * 32, dyn_, st>>>(x, T, h, wr, ne,   \
-                                                                         k, renorm, idx,     \
-                                                                         gates, tile_counts);\
-    } while (0)
-#define MOE_ROUTER6_TPT(E, N)                                                                \
-    do {                                                                                     \
-        if (tpt == 1) MOE_ROUTER6(E, 1, N);                                                  \
-        else if (tpt == 2) MOE_ROUTER6(E, 2, N);                                             \
-        else MOE_ROUTER6(E, 4, N);                                                           \
-    } while (0)
-        const char* ev = getenv("MOE_ROUTER_EPT");
-        if (ne <= 8 && ev && atoi(ev) == 1) MOE_ROUTER6_TPT(1, 8);   // one chain per lane
-        else if (ne <= 8) MOE_ROUTER6_TPT(2, 4);
-        else if (ne <= 16) MOE_ROUTER6_TPT(4, 4);
-        else if (ne <= 32) MOE_ROUTER6_TPT(8, 4);
-        else if (ne <= 64) MOE_ROUTER6_TPT(8, 8);
-        else MOE_ROUTER6_TPT(8, 16);
-#undef MOE_ROUTER6_TPT
-#undef MOE_ROUTER6
         return cudaGetLastError();
     }
     return cudaErrorInvalidValue;   // MOE_ROUTER=<unknown>

@@ -392,19 +392,17 @@ def test_experts_per_gemm_launch(rows, copy_group, launches, monkeypatch):
 
 
 @pytest.mark.parametrize("variant", ["v3-1", "v3-2", "v3-4", "v3-8",
-                                     "v6-0-tpt1", "v6-0-tpt2", "v6-0-tpt4", "v6-1-tpt1", "v6-1-tpt2",
-                                     "v7-0-tpt1", "v7-0-tpt2", "v7-0-tpt4", "v7-1-tpt1", "v7-4-tpt2",
-                                     "v7-8-tpt4"])
+                                     "v7-0-tpt1", "v7-0-tpt2", "v7-0-tpt4", "v7-1-tpt1", "v7-1-tpt2",
+                                     "v7-4-tpt2", "v7-8-tpt1", "v7-8-tpt4"])
 @pytest.mark.parametrize("ne,k", [(5, 2), (8, 2), (16, 4), (40, 6), (128, 8)])
 def test_router_experts_per_warp_variants(ne, k, variant, monkeypatch):
     """Every router kernel instantiation -- round 1's router_topk_kernel<EPT> (MOE_ROUTER=3) and
-    router_v6_kernel<EPT, TPT, NW, CW, PF> (every N_e bucket x MOE_ROUTER_TPT = 1 / 2 / 4, one
-    chain per lane with MOE_ROUTER_EPT=1) and router_v7_kernel<EPT, TPT, NW, CW> (MOE_ROUTER=7:
-    producer-warp bulk-copy ring, per-thread top-k; the EPT overrides 1 / 4 / 8) -- gives the same bit-exact selection and gates as
+    the default router_v7_kernel<EPT, TPT, NW, CW> (every N_e bucket x MOE_ROUTER_TPT = 1 / 2 / 4,
+    the EPT overrides 1 / 4 / 8; TMA producer ring, integer-key top-k) -- gives the same bit-exact selection and gates as
     the oracle (one fp64 FMA chain per logit, ascending channels, in every kernel)."""
     ver, ept, *rest = variant.split("-")
     if ne == 128 and ver == "v3":
-        pytest.skip("128 experts: v6 / v7 buckets only")
+        pytest.skip("128 experts: v7 only")
     monkeypatch.setenv("MOE_ROUTER", ver[1])
     if ept != "0":
         monkeypatch.setenv("MOE_ROUTER_EPT", ept)
@@ -725,12 +723,12 @@ def test_ipc_connect_rejects_mismatched_blob():
         r0.close()
 
 
-@pytest.mark.parametrize("ver", ["6", "7"])
+@pytest.mark.parametrize("ver", ["3", "7"])
 def test_router_special_values(ver, monkeypatch):
     """Routing on inputs with special bf16 values (R5, R13): all-zero rows (every logit ties ->
     experts 0..k-1), -0.0, subnormals, +-inf (logits +-inf or NaN -> NaN ranks last), and a NaN
     channel.  idx must equal the oracle's bit for bit on every token, gates wherever the oracle's
-    are finite (router v7's integer keys and v6's fp64 compares implement the same order)."""
+    are finite (router v7's integer keys and round 1's fp64 compares implement the same order)."""
     monkeypatch.setenv("MOE_ROUTER", ver)
     cfg = synth.MoEConfig("custom", 23, 128, 256, 8, 2, 64)
     inp = synth.gen_inputs(cfg)
