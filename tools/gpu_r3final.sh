@@ -8,8 +8,8 @@ mkdir -p $O
 python __graft_entry__.py > $O/build.log 2>&1
 mkdir -p build
 nvcc -gencode arch=compute_100a,code=sm_100a -O2 -I include -I paper_2504_09345_b200/csrc tools/router_bench.cu -L paper_2504_09345_b200 -lmoe_b200 -o build/router_bench
-for shape in "64 128 8 2" "4096 4096 8 2" "8192 6144 8 2" "16384 6144 16 4" "32768 2048 64 6" "131072 4096 8 2" "4000 2048 128 1"; do
-  LD_LIBRARY_PATH=paper_2504_09345_b200 MOE_ROUTER=6 ./build/router_bench $shape; LD_LIBRARY_PATH=paper_2504_09345_b200 ./build/router_bench $shape
+for shape in "64 128 8 2" "4096 4096 8 2" "8192 6144 8 2" "16384 6144 16 4" "32768 2048 64 6" "131072 4096 8 2" "4000 2048 128 1" "8192 2048 128 8" "1000 512 40 3"; do
+  LD_LIBRARY_PATH=paper_2504_09345_b200 ./build/router_bench $shape
 done > $O/router_sweep.txt 2>&1
 timeout 2400 python -m pytest tests -m gpu -q --durations=15 > $O/tests.log 2>&1; echo "rc=$?" >> $O/tests.log
 tail -3 $O/tests.log
@@ -26,7 +26,5 @@ MOE_BENCH_SHARE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --n
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c1.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:expert_gemm -s 4 -c 2 -o $O/prof_gemm_c1 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"router_v7|permute|combine" -c 3 -o $O/prof_route_c1 python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu > /dev/null 2>&1
-for S in memcheck racecheck synccheck; do
-  timeout 1500 compute-sanitizer --tool $S --target-processes all python tools/sanitize_paths.py > $O/sanitizer_$S.log 2>&1; echo "$S rc=$?"; tail -1 $O/sanitizer_$S.log
-done
+# (compute-sanitizer is closed on this GPU pool: no sanitizer runs)
 ls $O
