@@ -758,3 +758,23 @@ def test_router_special_values(ver, monkeypatch):
         assert np.max(np.abs(g[fin] - g_ref[fin])) <= 1e-6
     finally:
         run.close()
+
+
+@pytest.mark.parametrize("T,h,ne,k", [
+    (1, 128, 8, 2),        # one token: 31 zero-filled TMA rows
+    (31, 128, 8, 1),       # a single partial routing tile
+    (33, 256, 16, 4),      # one full tile + one token
+    (97, 128, 40, 3),      # 64-B swizzle chunks (N_e > 32), 4 threads per token in the top-k
+    (130, 384, 64, 6),     # C4's bucket, ragged
+    (257, 256, 128, 8),    # the 128-expert envelope, top-8
+    (4113, 128, 8, 2),     # > 128 blocks: TPT 2 / 4 chosen by grid fill, ragged
+])
+def test_router_edge_shapes(T, h, ne, k):
+    """Router v7 on ragged and tiny shapes across its buckets (one-token calls, partial tiles,
+    zero-filled TMA rows, 32- and 64-channel chunks, top-k split over 4 threads per token):
+    expert selection bit-exact and gates within 1e-6 of the oracle on every token; the layer
+    output within the per-token tolerance."""
+    cfg = synth.MoEConfig("custom", 29, h, 256, ne, k, T)
+    inp = synth.gen_inputs(cfg)
+    run, *_ = _check_full(inp)
+    run.close()
