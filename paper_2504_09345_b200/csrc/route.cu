@@ -664,7 +664,10 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int h, int k, int ne,
         }
         // MOE_FLAG_SHARD_SHARED: the row also goes to every shared-slice owner (the gather)
         const uint32_t smask = (pr && pr->shard_row >= 0) ? pr->shard_mask : 0u;
-        constexpr int U = 4;
+        // 8 vectors (4 KB per warp) in flight; the destination loop is unrolled over kMaxTopK so
+        // dst_ptr stays in registers (a loop to the run-time k indexed it from a local-memory
+        // stack frame)
+        constexpr int U = 8;
         for (int v0 = lane; v0 < nvec; v0 += 32 * U) {
             int4 buf[U];
 #pragma unroll
@@ -672,13 +675,15 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, int T, int h, int k, int ne,
                 const int v = v0 + 32 * u;
                 if (v < nvec) buf[u] = ptx::ld_nc_v4(src + v);
             }
-            for (int j = 0; j < k; ++j) {
-                int4* dst = reinterpret_cast<int4*>(dst_ptr[j]);
-                if (!dst) continue;
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int v = v0 + 32 * u;
-                    if (v < nvec) dst[v] = buf[u];
+            for (int j = 0; j < kMaxTopK; ++j) {
+                int4* dst = reinterpret_cast<int4*>(dst_ptr[j]);
+                if (j < k && dst) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int v = v0 + 32 * u;
+                        if (v < nvec) dst[v] = buf[u];
+                    }
                 }
             }
             for (uint32_t m = smask; m; m &= m - 1) {
