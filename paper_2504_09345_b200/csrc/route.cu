@@ -743,7 +743,7 @@ combine_kernel(const __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ 
             }
         }
     }
-    constexpr int U = 2;
+    constexpr int U = K <= 2 ? 4 : 2;   // U x K row vectors in flight per lane
     for (int vb = v0 + lane; vb < v0 + per; vb += 32 * U) {
         int4 raw[U][K];
 #pragma unroll
