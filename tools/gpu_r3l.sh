@@ -1,4 +1,4 @@
-# router v7 over the 65..128-expert envelope (MOE_ROUTER_V7_MAX=128) vs v6: sweep + parity
+# router v7 over the 65..128-expert envelope vs v6 (MOE_ROUTER_V7_MAX was a knob of that build only; v6 and the knob were removed after this run): sweep + parity
 O=gpurun_out/router7o
 cd ${GRAFT_REPO_ROOT:-.}
 mkdir -p $O build
